@@ -1,0 +1,438 @@
+#!/usr/bin/env python
+"""Benchmark: H-CNN hash-conv layer forward+backward on synthetic voxelised shells.
+
+A step = one 3x3x3 stride-1 hash-conv layer fwd+bwd over this rank's batch of
+whole shapes (`--shapes-per-gpu` copies of the sphere shell of bench.cpp:33-77 at
+`--res`), i.e. forward (field probes + gather + contraction), dW, and the input
+gradient; with N GPUs each rank runs its own shapes (weak scaling) and dW is
+all-reduced over NCCL. The metric is occupied voxels per second (whole job);
+shapes/s is reported beside it.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Timing: W untimed warm-up steps, then K steps between barrier+synchronize,
+CUDA events on the launching stream, max over ranks. The working set (column
+matrices / feature maps of ~1.8M voxels) is far larger than L2, so no flush is
+needed. --impl reference runs the unmodified reference CPU library
+(oracle/_ref/libhcref.so, built from /root/reference) on rank 0 over a bounded
+sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+CACHE = os.path.join(ROOT, "paper_1803_11385_b200", "_cache")
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--res", type=int, default=256)
+    p.add_argument("--shapes-per-gpu", type=int, default=8)
+    p.add_argument("--cin", type=int, default=16)
+    p.add_argument("--cout", type=int, default=16)
+    p.add_argument("--path", default="materialized", choices=["materialized", "fused"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ inputs
+def shell_levels(res: int):
+    """Finest and next-coarser PSH level of the synthetic shell, cached as .psh."""
+    from paper_1803_11385_b200.psh import PshLevel, VoxelSet, mix_seed, read_psh_file, write_psh_file
+    os.makedirs(CACHE, exist_ok=True)
+    path = os.path.join(CACHE, f"shell{res}_l01.psh")
+    if os.path.exists(path):
+        lv = read_psh_file(path)
+        if len(lv) == 2 and lv[0].resolution == res:
+            return lv
+    s = VoxelSet.sphere(res, True)
+    lv = [PshLevel.build(s, mix_seed(1, 0)), PshLevel.build(s.coarsen(), mix_seed(1, 1))]
+    write_psh_file(path + ".tmp", lv)
+    os.replace(path + ".tmp", path)
+    return lv
+
+
+def peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return FALLBACK_PEAKS, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.proc, self.lines = index, None, []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU reference
+def _level_arrays(level):
+    h, o, t, d = level.arrays()
+
+    class A:
+        pass
+
+    a = A()
+    a.dim, a.resolution, a.batch = level.dim, level.resolution, 1
+    a.hash, a.offsets, a.tags = h, o, t
+    a.model_of_slot = np.ones(h.size, np.int32)
+    a.hash_acc = np.array([0, h.size], np.int64)
+    a.offset_acc = np.array([0, level.offset_cells()], np.int64)
+    a.data_acc = np.array([0, level.n], np.int64)
+    a.hash_dims = np.array([level.hash_dim], np.int32)
+    a.offset_dims = np.array([level.offset_dim], np.int32)
+    a.data = d
+    a.total_columns = lambda: level.n
+    a.total_slots = lambda: h.size
+    return a
+
+
+def cpu_conv_sample(res, cin, cout, reps=1):
+    """Time the reference CPU conv layer fwd+bwd (hash2col, matmul, conv_backward —
+    cnn_ops.cpp:123-232) on ONE shape of the workload."""
+    from oracle.oracle import Ref, Restated, have_ref
+    lv = shell_levels(res)
+    arr = _level_arrays(lv[0])
+    n = lv[0].n
+    rng = np.random.default_rng(3)
+    x = rng.uniform(-1, 1, (cin, n)).astype(np.float32)
+    w = rng.uniform(-1, 1, (cout, cin * 27)).astype(np.float32)
+    dy = rng.uniform(-1, 1, (cout, n)).astype(np.float32)
+    spec = (3, 1, 0, cin, cout)
+    if have_ref():
+        ref = Ref()
+        s = ref.super_from(arr)
+        kind, cores = "reference", ref.max_threads()
+
+        def run():
+            cols = ref.hash2col(s, x, s, spec)
+            ref.matmul(w, cols)
+            ref.conv_backward(dy, w, cols, s, s, spec)
+    else:
+        R = Restated()
+        kind, cores = "port", 1
+
+        def run():
+            cols = R.hash2col(arr, x, arr, spec)
+            R.matmul(w, cols)
+            R.conv_backward(dy, w, cols, arr, arr, spec)
+    best = float("inf")
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        run()
+        best = min(best, time.perf_counter() - t0)
+    sample = f"1 of the workload's shapes ({res}^3 shell, {n} voxels), conv {cin}->{cout} fwd+bwd, best of {reps}"
+    return best, n, kind, cores, sample
+
+
+# ------------------------------------------------------------------ GPU steps
+class MaterializedStep:
+    """Reference-layout path through the C ABI: hash2col -> W*cols -> dW = dY*cols^T ->
+    dcols = W^T*dY -> col2hash (HC_MATH_FAST contraction)."""
+
+    name = "materialized (reference layout, fp32)"
+    dtype = "f32"
+
+    def __init__(self, fine, cin, cout, dev):
+        import torch
+        from paper_1803_11385_b200 import ops
+        self.ops, self.torch = ops, torch
+        self.fine = fine
+        self.spec = ops.ConvSpec(3, 1, 0, cin, cout)
+        N = fine.total_columns()
+        g = torch.Generator(device=dev).manual_seed(0)
+        self.x = torch.rand((cin, N), device=dev, generator=g) * 2 - 1
+        self.w = torch.rand((cout, cin * 27), device=dev, generator=g) * 2 - 1
+        self.dy = torch.rand((cout, N), device=dev, generator=g) * 2 - 1
+        self.N, self.cin, self.cout = N, cin, cout
+        self.op_names = ["hash2col", "fwd_gemm", "dW_gemm", "dcols_gemm", "col2hash"]
+
+    def run(self, x, w, dy, marks=None):
+        ops, f, sp = self.ops, self.fine, self.spec
+        mark = (lambda i: marks[i].record()) if marks else (lambda i: None)
+        with ops.math_mode("fast"):
+            mark(0)
+            cols = ops.hash2col(f, x, f, sp)
+            mark(1)
+            y = ops.matmul(w, cols)
+            mark(2)
+            dw = ops.matmul_trans_b(dy, cols)
+            mark(3)
+            dcols = ops.matmul_trans_a(w, dy)
+            mark(4)
+            dx = ops.col2hash(dcols, f, f, sp)
+            mark(5)
+        return y, dw, dx
+
+    def op_model(self, M, R):
+        """Algorithmic bytes / flops per op."""
+        s, N, ci, co = 4, self.N, self.cin, self.cout
+        gather = 28 * ci * N * s + 10 * M + 3 * R + 16 * N
+        fl = 2.0 * co * 27 * ci * N
+        return {"hash2col": ("hbm", gather), "fwd_gemm": ("flop", fl), "dW_gemm": ("flop", fl),
+                "dcols_gemm": ("flop", fl), "col2hash": ("hbm", gather)}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_1803_11385_b200 import _lib
+    from paper_1803_11385_b200.psh import SuperPsh
+
+    lv = shell_levels(args.res)
+    fine = SuperPsh.from_levels([lv[0]] * args.shapes_per_gpu)
+    step = MaterializedStep(fine, args.cin, args.cout, dev)
+    N = fine.total_columns()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def one(marks=None):
+        y, dw, dx = step.run(step.x, step.w, step.dy, marks)
+        if world > 1:
+            dist.all_reduce(dw)
+        return dx
+
+    for _ in range(max(args.warmup, 3)):
+        one()
+    barrier()
+
+    nops = len(step.op_names)
+    per_op = [0.0] * nops
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    marks_all = [[torch.cuda.Event(enable_timing=True) for _ in range(nops + 1)] for _ in range(args.steps)]
+    launches0 = _lib.lib.hc_launch_count()
+    with ClockSampler(local) as clk:
+        barrier()
+        start.record()
+        for k in range(args.steps):
+            one(marks_all[k])
+        end.record()
+        barrier()
+    launches = _lib.lib.hc_launch_count() - launches0
+    elapsed_ms = start.elapsed_time(end)
+    for m in marks_all:
+        for i in range(nops):
+            per_op[i] += m[i].elapsed_time(m[i + 1])
+    t = torch.tensor([elapsed_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    total_vox = N * world
+    value = total_vox / (ms_step / 1e3)
+
+    # ---- e2e through the public API with host buffers (H2D inputs, D2H results)
+    e2e = None
+    if not args.no_e2e:
+        hx = step.x.cpu().pin_memory()
+        hw = step.w.cpu().pin_memory()
+        hdy = step.dy.cpu().pin_memory()
+        outs = [torch.empty((args.cout, N), pin_memory=True), torch.empty((args.cout, args.cin * 27),
+                pin_memory=True), torch.empty((args.cin, N), pin_memory=True)]
+
+        def e2e_step():
+            x = hx.to(dev, non_blocking=True)
+            w = hw.to(dev, non_blocking=True)
+            dy = hdy.to(dev, non_blocking=True)
+            y, dw, dx = step.run(x, w, dy)
+            if world > 1:
+                dist.all_reduce(dw)
+            for o, r in zip(outs, (y, dw, dx)):
+                o.copy_(r, non_blocking=True)
+
+        e2e_step()
+        barrier()
+        es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ke = max(3, args.steps // 2)
+        es.record()
+        for _ in range(ke):
+            e2e_step()
+        ee.record()
+        barrier()
+        et = torch.tensor([es.elapsed_time(ee) / ke], device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        h2d = (hx.numel() + hw.numel() + hdy.numel()) * 4
+        d2h = sum(o.numel() for o in outs) * 4
+        e2e = {"value": total_vox / (float(et.item()) / 1e3), "unit": "voxels/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": float(et.item())}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel
+    pk, pk_kind = peaks()
+    info = np.zeros(6, np.int64)
+    import ctypes
+    _lib.lib.hc_psh_info(fine._h, info.ctypes.data_as(ctypes.c_void_p))
+    model = step.op_model(int(info[3]), int(info[4]))
+    kernels = {}
+    for i, name in enumerate(step.op_names):
+        avg_ms = per_op[i] / args.steps
+        kind, amount = model[name]
+        if kind == "hbm":
+            ach = amount / (avg_ms / 1e3) / 1e9
+            kernels[name] = {"ms": avg_ms, "bound": "hbm", "achieved_GBps": ach,
+                             "frac": ach / pk["hbm_gbs"], "algorithmic_bytes": amount}
+        else:
+            ach = amount / (avg_ms / 1e3) / 1e12
+            kernels[name] = {"ms": avg_ms, "achieved_TFLOPs": ach, "flops": amount}
+    dom = max(step.op_names, key=lambda n: per_op[step.op_names.index(n)])
+    dk = kernels[dom]
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dom)
+        except Exception:
+            traffic = None
+    if dk.get("bound") == "hbm":
+        roof = {"bound": "hbm", "kernel": dom, "achieved": dk["achieved_GBps"], "peak": pk["hbm_gbs"],
+                "unit": "GB/s", "frac": dk["frac"], "traffic": traffic, "peak_source": pk_kind}
+    else:
+        ach = dk["achieved_TFLOPs"]
+        peak = pk["bf16_tflops_sustained"]
+        roof = {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                "frac": ach / peak, "traffic": traffic, "peak_source": pk_kind}
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        secs, n1, kind, cores, sample = cpu_conv_sample(args.res, args.cin, args.cout)
+        cpu = {"value": n1 / secs, "unit": "voxels/s", "cores": cores, "kind": kind, "sample": sample}
+
+    line = {
+        "metric": "hash-conv fwd+bwd occupied voxels/sec",
+        "value": value, "unit": "voxels/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": step.dtype, "data": "synthetic (sphere shells, bench.cpp:33-77; uniform[-1,1] features/weights)",
+        "config": {"workload": f"{args.res}^3 shell x {args.shapes_per_gpu}/GPU, 3x3x3 hash-conv "
+                               f"{args.cin}->{args.cout} fwd+bwd (BASELINE config 4 per-GPU shard)",
+                   "res": args.res, "shapes_per_gpu": args.shapes_per_gpu, "global_batch": args.shapes_per_gpu * world,
+                   "c_in": args.cin, "c_out": args.cout, "voxels_per_gpu": N, "path": step.name,
+                   "parallelism": f"dp{world} (shapes sharded, dW all-reduce)",
+                   "l2": "working set >> L2 (no flush needed)"},
+        "shapes_per_s": args.shapes_per_gpu * world / (ms_step / 1e3),
+        "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": int(launches), "clocks": clk.summary(),
+    }
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the unmodified reference CPU library on rank 0 only."""
+    if rank != 0:
+        return
+    import ctypes  # noqa: F401
+    from oracle.oracle import have_ref
+    if not have_ref():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libhcref.so not built"}))
+        return
+    for _ in range(args.warmup and 1):
+        cpu_conv_sample(args.res, args.cin, args.cout)
+    times = []
+    n1 = None
+    kind = cores = sample = None
+    for _ in range(args.steps):
+        secs, n1, kind, cores, sample = cpu_conv_sample(args.res, args.cin, args.cout)
+        times.append(secs)
+    ms = 1e3 * sum(times) / len(times)
+    value = n1 / (ms / 1e3)
+    print(json.dumps({
+        "impl": "reference", "metric": "hash-conv fwd+bwd occupied voxels/sec", "value": value, "unit": "voxels/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.res}^3 shell, 3x3x3 hash-conv {args.cin}->{args.cout} fwd+bwd",
+                   "res": args.res, "c_in": args.cin, "c_out": args.cout, "sample_voxels_per_step": n1},
+        "cpu_baseline": {"value": value, "unit": "voxels/s", "cores": cores, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": "voxels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+
+
+if __name__ == "__main__":
+    main()

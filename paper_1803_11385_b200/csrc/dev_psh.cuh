@@ -1,0 +1,169 @@
+// dev_psh.cuh — device-resident super-PSH and the inlined probe (locate).
+//
+// Layout in HBM (built once by hc_psh_upload*, see device_psh.cu):
+//   slots[M]   uint2 {idx (int32, -1 = redundant), key}: H* and T* fused into one
+//              8-byte word per hash slot; key = x | y<<kb | z<<2kb (kb = bits of
+//              resolution-1), 0xFFFFFFFF when a tag component cannot be a
+//              coordinate (never matches). One load per probe instead of 4+6 bytes.
+//   phi[R]     uint32 {x | y<<8 | z<<16}: Phi* with each component pre-reduced mod
+//              m_bar of its model (exact: (a + phi) mod m == (a + phi mod m) mod m).
+//   models[b]  per-model bases (M*, R*, N*), m_bar, r_bar and float reciprocals.
+//   cols[N]    int4 {x, y, z, model}: column_info (cnn_ops.cpp:50-66), built on device.
+// The raw H*/Phi*/T*/V* arrays are kept too (download, validation).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace hcb {
+
+struct ModelParam {
+    long long hash_base;    // M*[v-1]
+    long long offset_base;  // R*[v-1]
+    long long data_base;    // N*[v-1]
+    int m, r;               // m_bar, r_bar
+    float inv_m, inv_r;     // 1/m, 1/r (fast exact mod for 0 <= p < 2^17)
+};
+
+struct DevPsh {
+    int dim, resolution, batch, key_bits;
+    long long M, R, N;
+    const uint2* slots;
+    const unsigned* phi;
+    const ModelParam* models;
+    const int4* cols;
+};
+
+// exact p mod d for 0 <= p < 2^17, d >= 1, using a float reciprocal + one fixup
+__device__ __forceinline__ int fmod_small(int p, int d, float inv) {
+    int q = __float2int_rz(__int2float_rn(p) * inv);
+    int r = p - q * d;
+    if (r < 0) r += d;
+    if (r >= d) r -= d;
+    return r;
+}
+
+__device__ __forceinline__ unsigned pack_key(int x, int y, int z, int kb) {
+    return static_cast<unsigned>(x) | (static_cast<unsigned>(y) << kb) | (static_cast<unsigned>(z) << (2 * kb));
+}
+
+// psh_batch.cpp:56-78 locate for one in-domain coordinate, given its residues.
+//   rm*, rr*: p mod m_bar / p mod r_bar per axis (z terms 0 for dim 2)
+__device__ __forceinline__ int probe_res(const DevPsh& s, const ModelParam& mp, int dim, int x, int y,
+                                         int z, int rmx, int rmy, int rmz, int rrx, int rry, int rrz) {
+    const long long cell = dim == 3 ? ((long long)rrz * mp.r + rry) * mp.r + rrx : (long long)rry * mp.r + rrx;
+    const unsigned ph = __ldg(s.phi + mp.offset_base + cell);
+    int sx = rmx + (int)(ph & 0xFF);
+    int sy = rmy + (int)((ph >> 8) & 0xFF);
+    int sz = rmz + (int)((ph >> 16) & 0xFF);
+    if (sx >= mp.m) sx -= mp.m;
+    if (sy >= mp.m) sy -= mp.m;
+    if (sz >= mp.m) sz -= mp.m;
+    const long long slot = dim == 3 ? ((long long)sz * mp.m + sy) * mp.m + sx : (long long)sy * mp.m + sx;
+    const uint2 e = __ldg(s.slots + mp.hash_base + slot);
+    const int idx = (int)e.x;
+    if (idx < 0 || e.y != pack_key(x, y, z, s.key_bits)) return -1;
+    return (int)(mp.data_base + idx);
+}
+
+__device__ __forceinline__ int probe(const DevPsh& s, const ModelParam& mp, int x, int y, int z) {
+    const int dim = s.dim;
+    return probe_res(s, mp, dim, x, y, z, fmod_small(x, mp.m, mp.inv_m), fmod_small(y, mp.m, mp.inv_m),
+                     dim == 3 ? fmod_small(z, mp.m, mp.inv_m) : 0, fmod_small(x, mp.r, mp.inv_r),
+                     fmod_small(y, mp.r, mp.inv_r), dim == 3 ? fmod_small(z, mp.r, mp.inv_r) : 0);
+}
+
+// Field taps of one output voxel: base = field origin (cnn_ops.cpp:36-42), F per
+// axis, taps in (dz,dy,dx) row order (cnn_ops.cpp:100-119). Residues are
+// computed once per axis coordinate (3F fast mods instead of 6F^3).
+template <int F>
+__device__ __forceinline__ void probe_field(const DevPsh& s, const ModelParam& mp, int bx, int by, int bz,
+                                            int* out /* F^dim */) {
+    const int dim = s.dim, res = s.resolution;
+    int rmx[F], rmy[F], rmz[F], rrx[F], rry[F], rrz[F];
+    bool vx[F], vy[F], vz[F];
+#pragma unroll
+    for (int d = 0; d < F; ++d) {
+        const int x = bx + d, y = by + d, z = bz + d;
+        vx[d] = x >= 0 && x < res;
+        vy[d] = y >= 0 && y < res;
+        vz[d] = dim == 3 ? (z >= 0 && z < res) : (d == 0);
+        rmx[d] = vx[d] ? fmod_small(x, mp.m, mp.inv_m) : 0;
+        rmy[d] = vy[d] ? fmod_small(y, mp.m, mp.inv_m) : 0;
+        rmz[d] = (dim == 3 && vz[d]) ? fmod_small(z, mp.m, mp.inv_m) : 0;
+        rrx[d] = vx[d] ? fmod_small(x, mp.r, mp.inv_r) : 0;
+        rry[d] = vy[d] ? fmod_small(y, mp.r, mp.inv_r) : 0;
+        rrz[d] = (dim == 3 && vz[d]) ? fmod_small(z, mp.r, mp.inv_r) : 0;
+    }
+    const int fz = dim == 3 ? F : 1;
+#pragma unroll
+    for (int dz = 0; dz < F; ++dz) {
+        if (dz >= fz) break;
+#pragma unroll
+        for (int dy = 0; dy < F; ++dy)
+#pragma unroll
+            for (int dx = 0; dx < F; ++dx) {
+                const int t = (dz * F + dy) * F + dx;
+                out[t] = (vx[dx] && vy[dy] && vz[dz])
+                             ? probe_res(s, mp, dim, bx + dx, by + dy, dim == 3 ? bz + dz : 0, rmx[dx], rmy[dy],
+                                         rmz[dz], rrx[dx], rry[dy], rrz[dz])
+                             : -1;
+            }
+    }
+}
+
+// Generic-F single tap (any kernel size): used by the fallback kernels.
+__device__ __forceinline__ int probe_tap(const DevPsh& s, const ModelParam& mp, int bx, int by, int bz, int F,
+                                         int t) {
+    const int dim = s.dim;
+    const int dx = t % F, dy = (t / F) % F, dz = dim == 3 ? t / (F * F) : 0;
+    const int x = bx + dx, y = by + dy, z = dim == 3 ? bz + dz : 0;
+    const int res = s.resolution;
+    if (x < 0 || x >= res || y < 0 || y >= res || (dim == 3 && (z < 0 || z >= res))) return -1;
+    return probe(s, mp, x, y, z);
+}
+
+// cnn_ops.cpp:15-18
+__device__ __forceinline__ int floordiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+// cnn_ops.cpp:70-85 covering_range (per axis, clipped to the output domain)
+__device__ __forceinline__ void cover_axis(int p, int F, int S, int pad, int out_res, int& lo, int& hi) {
+    int l, h;
+    if (S == 1) {
+        l = p - (F - 1) / 2;
+        h = p + (F - 1) / 2;
+    } else {
+        l = floordiv(p + pad - F + 1 + S - 1, S);
+        h = floordiv(p + pad, S);
+    }
+    lo = l > 0 ? l : 0;
+    hi = h < out_res - 1 ? h : out_res - 1;
+}
+
+__device__ __forceinline__ int origin_axis(int po, int F, int S, int pad) {
+    return S == 1 ? po - (F - 1) / 2 : po * S - pad;
+}
+
+}  // namespace hcb
+
+// Opaque handle behind hc_psh*.
+struct hc_psh {
+    hcb::DevPsh d;
+    // raw device copies of the reference arrays
+    int32_t* hash = nullptr;
+    uint8_t* offsets = nullptr;
+    uint16_t* tags = nullptr;
+    int32_t* model_of_slot = nullptr;
+    // host copies of the small per-model arrays (batch entries)
+    int64_t* h_hash_acc = nullptr;
+    int64_t* h_offset_acc = nullptr;
+    int64_t* h_data_acc = nullptr;
+    int32_t* h_hash_dims = nullptr;
+    int32_t* h_offset_dims = nullptr;
+    // owned derived device tables
+    uint2* slots = nullptr;
+    unsigned* phi = nullptr;
+    hcb::ModelParam* models = nullptr;
+    int4* cols = nullptr;
+};

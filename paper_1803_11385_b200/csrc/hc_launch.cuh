@@ -1,0 +1,53 @@
+// hc_launch.cuh — small launch helpers shared by the .cu files (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "hashconv_b200.h"
+
+namespace hcb {
+
+void cuda_check(cudaError_t e, const char* what);
+void* dev_alloc(size_t bytes);
+hc_math current_math();
+
+// Kernel-launch accounting (hc_launch_count): every launch site reports how many
+// kernels it enqueued, then checks the launch.
+void count_launches(long long n);
+inline void launched(const char* what, long long n = 1) {
+    count_launches(n);
+    cuda_check(cudaGetLastError(), what);
+}
+
+inline cudaStream_t as_stream(hc_stream s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline unsigned grid_for(long long n, int threads) {
+    return static_cast<unsigned>((n + threads - 1) / threads);
+}
+
+// Stream-ordered scratch buffer (cudaMallocAsync / cudaFreeAsync).
+struct Scratch {
+    void* p = nullptr;
+    cudaStream_t s = nullptr;
+    Scratch(size_t bytes, cudaStream_t st) : s(st) {
+        cuda_check(cudaMallocAsync(&p, bytes ? bytes : 16, st), "cudaMallocAsync");
+    }
+    ~Scratch() {
+        if (p) cudaFreeAsync(p, s);
+    }
+    Scratch(const Scratch&) = delete;
+    Scratch& operator=(const Scratch&) = delete;
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+// Exact fp32 GEMMs (gemm_exact.cu) — reference accumulation order.
+void gemm_nn_exact(const float* a, const float* b, float* c, long long ra, long long k, long long cb, cudaStream_t s);
+void gemm_tn_exact(const float* a, const float* b, float* c, long long ra, long long k, long long cb, cudaStream_t s);
+void gemm_nt_exact(const float* a, const float* b, float* c, long long ra, long long k, long long rb, cudaStream_t s);
+
+}  // namespace hcb

@@ -1,0 +1,698 @@
+// ops_ref.cu — the hot-path operators in the reference's layouts (channel-major
+// feature matrices, (C*F^3) x N column matrices), bit-exact with
+// src/cnn_ops.cpp. Work is enumerated by DATA COLUMN (one thread per output
+// column for gathers, one per input column for the pull-based adjoints), so
+// consecutive threads are z,y,x-raster neighbours: their probes and gathers hit
+// the same L2 lines and their column-matrix stores coalesce.
+//
+// Arithmetic: order-defined reductions keep the reference order and use
+// __fadd_rn/__fmul_rn so nvcc cannot contract them into FMAs.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <string>
+
+#include "dev_psh.cuh"
+#include "hc_internal.h"
+#include "hc_launch.cuh"
+
+namespace hcb {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+// cnn_ops.cpp:20-33 check_pair (same messages, same order)
+void check_pair(const hc_psh* in, const hc_psh* out, const hc_conv_spec& sp) {
+    if (!in || !out) throw std::invalid_argument("null super-PSH handle");
+    if (in->d.dim != out->d.dim) throw std::invalid_argument("structure dim mismatch");
+    if (in->d.batch != out->d.batch) throw std::invalid_argument("batch size mismatch");
+    if (sp.kernel < 1 || sp.stride < 1 || sp.pad < 0) throw std::invalid_argument("bad conv spec");
+    if (sp.stride == 1) {
+        if (sp.kernel % 2 == 0) throw std::invalid_argument("stride-1 fields need an odd kernel size");
+        if (in->d.resolution != out->d.resolution) throw std::invalid_argument("stride-1 ops keep the level fixed");
+    } else if (in->d.resolution != out->d.resolution * sp.stride) {
+        throw std::invalid_argument("input resolution must be output resolution * stride");
+    }
+}
+
+long long field_volume(const hc_conv_spec& sp, int dim) {
+    long long v = 1;
+    for (int a = 0; a < dim; ++a) v *= sp.kernel;
+    return v;
+}
+
+// ============================================================== K0 field map
+template <int F>
+__global__ void k_field_map(DevPsh in, DevPsh out, int S, int pad, int* map) {
+    const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (col >= out.N) return;
+    const int4 c = out.cols[col];
+    const ModelParam mp = in.models[c.w - 1];
+    const int fd = in.dim == 3 ? F * F * F : F * F;
+    int nb[F * F * F];
+    probe_field<F>(in, mp, origin_axis(c.x, F, S, pad), origin_axis(c.y, F, S, pad),
+                   origin_axis(c.z, F, S, pad), nb);
+    int* dst = map + col * fd;
+#pragma unroll
+    for (int t = 0; t < F * F * F; ++t)
+        if (t < fd) dst[t] = nb[t];
+}
+
+__global__ void k_field_map_any(DevPsh in, DevPsh out, int F, int S, int pad, int fd, int* map) {
+    const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (col >= out.N) return;
+    const int4 c = out.cols[col];
+    const ModelParam mp = in.models[c.w - 1];
+    const int bx = origin_axis(c.x, F, S, pad), by = origin_axis(c.y, F, S, pad), bz = origin_axis(c.z, F, S, pad);
+    for (int t = 0; t < fd; ++t) map[col * fd + t] = probe_tap(in, mp, bx, by, bz, F, t);
+}
+
+// ============================================================== hash2col
+// cnn_ops.cpp:123-158: cols[(c*fd + row), col] = data[c, hit] or 0.
+template <int F>
+__global__ void k_hash2col(DevPsh in, DevPsh out, int S, int pad, const float* __restrict__ data, int C,
+                           float* __restrict__ cols) {
+    const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (col >= out.N) return;
+    const int4 c = out.cols[col];
+    const ModelParam mp = in.models[c.w - 1];
+    const int fd = in.dim == 3 ? F * F * F : F * F;
+    int nb[F * F * F];
+    probe_field<F>(in, mp, origin_axis(c.x, F, S, pad), origin_axis(c.y, F, S, pad),
+                   origin_axis(c.z, F, S, pad), nb);
+    const long long Nin = in.N, Nout = out.N;
+    for (int ch = 0; ch < C; ++ch) {
+        const float* src = data + ch * Nin;
+        float* dst = cols + (long long)ch * fd * Nout + col;
+#pragma unroll
+        for (int t = 0; t < F * F * F; ++t) {
+            if (t < fd) {
+                const float v = nb[t] >= 0 ? __ldg(src + nb[t]) : 0.0f;
+                __stcs(dst + (long long)t * Nout, v);
+            }
+        }
+    }
+}
+
+__global__ void k_hash2col_any(DevPsh in, DevPsh out, int F, int S, int pad, int fd, const float* __restrict__ data,
+                               int C, float* __restrict__ cols) {
+    const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (col >= out.N) return;
+    const int4 c = out.cols[col];
+    const ModelParam mp = in.models[c.w - 1];
+    const int bx = origin_axis(c.x, F, S, pad), by = origin_axis(c.y, F, S, pad), bz = origin_axis(c.z, F, S, pad);
+    const long long Nin = in.N, Nout = out.N;
+    for (int t = 0; t < fd; ++t) {
+        const int g = probe_tap(in, mp, bx, by, bz, F, t);
+        for (int ch = 0; ch < C; ++ch)
+            cols[((long long)ch * fd + t) * Nout + col] = g >= 0 ? __ldg(data + ch * Nin + g) : 0.0f;
+    }
+}
+
+// ============================================================== covering probes
+// Covering outputs of input voxel p_i in ascending (z,y,x) order with the field
+// row of p_i inside each (cnn_ops.cpp:70-92, 184-196). KA = max outputs per axis.
+template <int KA>
+__device__ __forceinline__ int cover_hits(const DevPsh& out, const ModelParam& mp, int px, int py, int pz, int F,
+                                          int S, int pad, int* hcol, int* hrow) {
+    const int dim = out.dim;
+    int lox, hix, loy, hiy, loz = 0, hiz = 0;
+    cover_axis(px, F, S, pad, out.resolution, lox, hix);
+    cover_axis(py, F, S, pad, out.resolution, loy, hiy);
+    if (dim == 3) cover_axis(pz, F, S, pad, out.resolution, loz, hiz);
+    int n = 0;
+    for (int z = loz; z <= hiz; ++z)
+        for (int y = loy; y <= hiy; ++y)
+            for (int x = lox; x <= hix; ++x) {
+                const int g = probe(out, mp, x, y, z);
+                if (g < 0) continue;
+                const int rx = px - origin_axis(x, F, S, pad), ry = py - origin_axis(y, F, S, pad);
+                const int rz = dim == 3 ? pz - origin_axis(z, F, S, pad) : 0;
+                hcol[n] = g;
+                hrow[n] = (rz * F + ry) * F + rx;
+                ++n;
+            }
+    return n;
+}
+
+// Stride-1 covering set via the residue-sharing field probe: outputs p_i + d,
+// row = fd - 1 - tap (the field of p_o = p_i + d holds p_i at offset -d).
+template <int F>
+__device__ __forceinline__ int cover_hits_s1(const DevPsh& out, const ModelParam& mp, int px, int py, int pz,
+                                             int* hcol, int* hrow) {
+    const int h = (F - 1) / 2;
+    const int fd = out.dim == 3 ? F * F * F : F * F;
+    int nb[F * F * F];
+    probe_field<F>(out, mp, px - h, py - h, pz - h, nb);
+    int n = 0;
+#pragma unroll
+    for (int t = 0; t < F * F * F; ++t) {
+        if (t < fd && nb[t] >= 0) {
+            hcol[n] = nb[t];
+            hrow[n] = fd - 1 - t;
+            ++n;
+        }
+    }
+    return n;
+}
+
+// ============================================================== col2hash
+// cnn_ops.cpp:160-204 (Alg. 2): pull per input column; per channel the sum runs
+// over covering outputs in ascending order (deterministic, bit-exact).
+template <int KMAX, bool STRIDE1, int F>
+__global__ void k_col2hash(DevPsh in, DevPsh out, int Fr, int S, int pad, int fd, const float* __restrict__ g,
+                           int C, float* __restrict__ res) {
+    const long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (gi >= in.N) return;
+    const int4 c = in.cols[gi];
+    const ModelParam mp = out.models[c.w - 1];
+    int hcol[KMAX], hrow[KMAX];
+    int n;
+    if constexpr (STRIDE1) n = cover_hits_s1<F>(out, mp, c.x, c.y, c.z, hcol, hrow);
+    else n = cover_hits<1>(out, mp, c.x, c.y, c.z, Fr, S, pad, hcol, hrow);
+    const long long Nout = out.N, Nin = in.N;
+    for (int ch = 0; ch < C; ++ch) {
+        float acc = 0.0f;
+        const float* base = g + (long long)ch * fd * Nout;
+#pragma unroll
+        for (int h = 0; h < KMAX; ++h)
+            if (h < n) acc = __fadd_rn(acc, __ldg(base + (long long)hrow[h] * Nout + hcol[h]));
+        res[ch * Nin + gi] = acc;
+    }
+}
+
+// any F / stride: recompute covering probes per channel (no register arrays)
+__global__ void k_col2hash_any(DevPsh in, DevPsh out, int F, int S, int pad, int fd, const float* __restrict__ g,
+                               int C, float* __restrict__ res) {
+    const long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (gi >= in.N) return;
+    const int4 c = in.cols[gi];
+    const ModelParam mp = out.models[c.w - 1];
+    const int dim = out.dim;
+    int lox, hix, loy, hiy, loz = 0, hiz = 0;
+    cover_axis(c.x, F, S, pad, out.resolution, lox, hix);
+    cover_axis(c.y, F, S, pad, out.resolution, loy, hiy);
+    if (dim == 3) cover_axis(c.z, F, S, pad, out.resolution, loz, hiz);
+    const long long Nout = out.N, Nin = in.N;
+    for (int ch = 0; ch < C; ++ch) {
+        float acc = 0.0f;
+        for (int z = loz; z <= hiz; ++z)
+            for (int y = loy; y <= hiy; ++y)
+                for (int x = lox; x <= hix; ++x) {
+                    const int col = probe(out, mp, x, y, z);
+                    if (col < 0) continue;
+                    const int rx = c.x - origin_axis(x, F, S, pad), ry = c.y - origin_axis(y, F, S, pad);
+                    const int rz = dim == 3 ? c.z - origin_axis(z, F, S, pad) : 0;
+                    const int row = (rz * F + ry) * F + rx;
+                    acc = __fadd_rn(acc, g[((long long)ch * fd + row) * Nout + col]);
+                }
+        res[ch * Nin + gi] = acc;
+    }
+}
+
+// ============================================================== pooling
+// cnn_ops.cpp:234-284 max_pool: first present tap seeds, strict '>' (ties keep
+// the smallest field row); empty field -> 0 / -1.
+template <int F>
+__global__ void k_max_pool(DevPsh in, DevPsh out, int S, int pad, const float* __restrict__ data, int C,
+                           float* __restrict__ res, int* __restrict__ sw) {
+    const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (col >= out.N) return;
+    const int4 c = out.cols[col];
+    const ModelParam mp = in.models[c.w - 1];
+    const int fd = in.dim == 3 ? F * F * F : F * F;
+    int nb[F * F * F];
+    probe_field<F>(in, mp, origin_axis(c.x, F, S, pad), origin_axis(c.y, F, S, pad),
+                   origin_axis(c.z, F, S, pad), nb);
+    const long long Nin = in.N, Nout = out.N;
+    for (int ch = 0; ch < C; ++ch) {
+        const float* src = data + ch * Nin;
+        float best = 0.0f;
+        int arg = -1;
+#pragma unroll
+        for (int t = 0; t < F * F * F; ++t) {
+            if (t < fd && nb[t] >= 0) {
+                const float v = __ldg(src + nb[t]);
+                if (arg < 0 || v > best) {
+                    best = v;
+                    arg = t;
+                }
+            }
+        }
+        res[ch * Nout + col] = arg < 0 ? 0.0f : best;
+        sw[ch * Nout + col] = arg;
+    }
+}
+
+__global__ void k_max_pool_any(DevPsh in, DevPsh out, int F, int S, int pad, int fd, const float* __restrict__ data,
+                               int C, float* __restrict__ res, int* __restrict__ sw) {
+    const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (col >= out.N) return;
+    const int4 c = out.cols[col];
+    const ModelParam mp = in.models[c.w - 1];
+    const int bx = origin_axis(c.x, F, S, pad), by = origin_axis(c.y, F, S, pad), bz = origin_axis(c.z, F, S, pad);
+    const long long Nin = in.N, Nout = out.N;
+    for (int ch = 0; ch < C; ++ch) {
+        float best = 0.0f;
+        int arg = -1;
+        for (int t = 0; t < fd; ++t) {
+            const int g = probe_tap(in, mp, bx, by, bz, F, t);
+            if (g < 0) continue;
+            const float v = data[ch * Nin + g];
+            if (arg < 0 || v > best) {
+                best = v;
+                arg = t;
+            }
+        }
+        res[ch * Nout + col] = arg < 0 ? 0.0f : best;
+        sw[ch * Nout + col] = arg;
+    }
+}
+
+// cnn_ops.cpp:286-322 avg_pool: (sum over present taps, row order) * inv_fd
+template <int F>
+__global__ void k_avg_pool(DevPsh in, DevPsh out, int S, int pad, const float* __restrict__ data, int C, float inv,
+                           float* __restrict__ res) {
+    const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (col >= out.N) return;
+    const int4 c = out.cols[col];
+    const ModelParam mp = in.models[c.w - 1];
+    const int fd = in.dim == 3 ? F * F * F : F * F;
+    int nb[F * F * F];
+    probe_field<F>(in, mp, origin_axis(c.x, F, S, pad), origin_axis(c.y, F, S, pad),
+                   origin_axis(c.z, F, S, pad), nb);
+    const long long Nin = in.N, Nout = out.N;
+    for (int ch = 0; ch < C; ++ch) {
+        const float* src = data + ch * Nin;
+        float acc = 0.0f;
+#pragma unroll
+        for (int t = 0; t < F * F * F; ++t)
+            if (t < fd && nb[t] >= 0) acc = __fadd_rn(acc, __ldg(src + nb[t]));
+        res[ch * Nout + col] = __fmul_rn(acc, inv);
+    }
+}
+
+__global__ void k_avg_pool_any(DevPsh in, DevPsh out, int F, int S, int pad, int fd, const float* __restrict__ data,
+                               int C, float inv, float* __restrict__ res) {
+    const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (col >= out.N) return;
+    const int4 c = out.cols[col];
+    const ModelParam mp = in.models[c.w - 1];
+    const int bx = origin_axis(c.x, F, S, pad), by = origin_axis(c.y, F, S, pad), bz = origin_axis(c.z, F, S, pad);
+    const long long Nin = in.N, Nout = out.N;
+    for (int ch = 0; ch < C; ++ch) {
+        float acc = 0.0f;
+        for (int t = 0; t < fd; ++t) {
+            const int g = probe_tap(in, mp, bx, by, bz, F, t);
+            if (g >= 0) acc = __fadd_rn(acc, data[ch * Nin + g]);
+        }
+        res[ch * Nout + col] = __fmul_rn(acc, inv);
+    }
+}
+
+// ============================================================== unpooling
+// cnn_ops.cpp:336-372 max_unpool: out[c,g] = 0 (+) coarse[c,col] for covering
+// outputs whose switch equals g's field row, ascending output order.
+template <int KMAX, bool AVG>
+__global__ void k_unpool(DevPsh fine, DevPsh coarse, int F, int S, int pad, const float* __restrict__ cd,
+                         const int* __restrict__ sw, int C, float inv, float* __restrict__ res) {
+    const long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (gi >= fine.N) return;
+    const int4 c = fine.cols[gi];
+    const ModelParam mp = coarse.models[c.w - 1];
+    int hcol[KMAX], hrow[KMAX];
+    const int n = cover_hits<1>(coarse, mp, c.x, c.y, c.z, F, S, pad, hcol, hrow);
+    const long long Nc = coarse.N, Nf = fine.N;
+    for (int ch = 0; ch < C; ++ch) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int h = 0; h < KMAX; ++h) {
+            if (h < n) {
+                const long long k = ch * Nc + hcol[h];
+                if constexpr (AVG) acc = __fadd_rn(acc, __fmul_rn(__ldg(cd + k), inv));
+                else if (__ldg(sw + k) == hrow[h]) acc = __fadd_rn(acc, __ldg(cd + k));
+            }
+        }
+        res[ch * Nf + gi] = acc;
+    }
+}
+
+template <bool AVG>
+__global__ void k_unpool_any(DevPsh fine, DevPsh coarse, int F, int S, int pad, const float* __restrict__ cd,
+                             const int* __restrict__ sw, int C, float inv, float* __restrict__ res) {
+    const long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (gi >= fine.N) return;
+    const int4 c = fine.cols[gi];
+    const ModelParam mp = coarse.models[c.w - 1];
+    const int dim = fine.dim;
+    int lox, hix, loy, hiy, loz = 0, hiz = 0;
+    cover_axis(c.x, F, S, pad, coarse.resolution, lox, hix);
+    cover_axis(c.y, F, S, pad, coarse.resolution, loy, hiy);
+    if (dim == 3) cover_axis(c.z, F, S, pad, coarse.resolution, loz, hiz);
+    const long long Nc = coarse.N, Nf = fine.N;
+    for (int ch = 0; ch < C; ++ch) {
+        float acc = 0.0f;
+        for (int z = loz; z <= hiz; ++z)
+            for (int y = loy; y <= hiy; ++y)
+                for (int x = lox; x <= hix; ++x) {
+                    const int col = probe(coarse, mp, x, y, z);
+                    if (col < 0) continue;
+                    const long long k = ch * Nc + col;
+                    if constexpr (AVG) {
+                        acc = __fadd_rn(acc, __fmul_rn(cd[k], inv));
+                    } else {
+                        const int rx = c.x - origin_axis(x, F, S, pad), ry = c.y - origin_axis(y, F, S, pad);
+                        const int rz = dim == 3 ? c.z - origin_axis(z, F, S, pad) : 0;
+                        if (sw[k] == (rz * F + ry) * F + rx) acc = __fadd_rn(acc, cd[k]);
+                    }
+                }
+        res[ch * Nf + gi] = acc;
+    }
+}
+
+__global__ void k_check_switches(const int* sw, long long n, int fd, int* bad) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int s = sw[i];
+    if (s >= fd || s < -1) atomicOr(bad, 1);
+}
+
+// ============================================================== dispatch helpers
+// cover count per axis: stride 1 -> F, else ceil(F/S)
+int cover_per_axis(const hc_conv_spec& sp) {
+    return sp.stride == 1 ? sp.kernel : (sp.kernel + sp.stride - 1) / sp.stride;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+void launch_field_map(const hc_psh* in, const hc_psh* out, const hc_conv_spec& sp, int* map, cudaStream_t s) {
+    const long long n = out->d.N;
+    if (n == 0) return;
+    const unsigned g = grid_for(n, kThreads);
+    if (sp.kernel == 3) k_field_map<3><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, map);
+    else if (sp.kernel == 2) k_field_map<2><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, map);
+    else k_field_map_any<<<g, kThreads, 0, s>>>(in->d, out->d, sp.kernel, sp.stride, sp.pad,
+                                              (int)field_volume(sp, in->d.dim), map);
+    launched("field_map");
+}
+
+void launch_hash2col(const hc_psh* in, const float* data, const hc_psh* out, const hc_conv_spec& sp, float* cols,
+                     cudaStream_t s) {
+    const long long n = out->d.N;
+    if (n == 0 || sp.in_channels == 0) return;
+    const unsigned g = grid_for(n, kThreads);
+    if (sp.kernel == 3)
+        k_hash2col<3><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, cols);
+    else if (sp.kernel == 2)
+        k_hash2col<2><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, cols);
+    else
+        k_hash2col_any<<<g, kThreads, 0, s>>>(in->d, out->d, sp.kernel, sp.stride, sp.pad,
+                                            (int)field_volume(sp, in->d.dim), data, sp.in_channels, cols);
+    launched("hash2col");
+}
+
+void launch_col2hash(const float* gcols, const hc_psh* in, const hc_psh* out, const hc_conv_spec& sp, float* res,
+                     cudaStream_t s) {
+    const long long n = in->d.N;
+    if (n == 0 || sp.in_channels == 0) return;
+    const unsigned g = grid_for(n, kThreads);
+    const int fd = (int)field_volume(sp, in->d.dim);
+    const int C = sp.in_channels;
+    if (sp.stride == 1 && sp.kernel == 3)
+        k_col2hash<27, true, 3><<<g, kThreads, 0, s>>>(in->d, out->d, 3, 1, 0, fd, gcols, C, res);
+    else if (sp.stride == 1 && sp.kernel == 1)
+        k_col2hash<1, true, 1><<<g, kThreads, 0, s>>>(in->d, out->d, 1, 1, 0, fd, gcols, C, res);
+    else if (sp.stride > 1 && cover_per_axis(sp) == 1)
+        k_col2hash<1, false, 1><<<g, kThreads, 0, s>>>(in->d, out->d, sp.kernel, sp.stride, sp.pad, fd, gcols, C, res);
+    else if (sp.stride > 1 && cover_per_axis(sp) == 2)
+        k_col2hash<8, false, 1><<<g, kThreads, 0, s>>>(in->d, out->d, sp.kernel, sp.stride, sp.pad, fd, gcols, C, res);
+    else
+        k_col2hash_any<<<g, kThreads, 0, s>>>(in->d, out->d, sp.kernel, sp.stride, sp.pad, fd, gcols, C, res);
+    launched("col2hash");
+}
+
+void launch_max_pool(const hc_psh* in, const float* data, const hc_psh* out, const hc_conv_spec& sp, float* res,
+                     int* sw, cudaStream_t s) {
+    const long long n = out->d.N;
+    if (n == 0 || sp.in_channels == 0) return;
+    const unsigned g = grid_for(n, kThreads);
+    if (sp.kernel == 2)
+        k_max_pool<2><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, res, sw);
+    else if (sp.kernel == 3)
+        k_max_pool<3><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, res, sw);
+    else
+        k_max_pool_any<<<g, kThreads, 0, s>>>(in->d, out->d, sp.kernel, sp.stride, sp.pad,
+                                            (int)field_volume(sp, in->d.dim), data, sp.in_channels, res, sw);
+    launched("max_pool");
+}
+
+void launch_avg_pool(const hc_psh* in, const float* data, const hc_psh* out, const hc_conv_spec& sp, float* res,
+                     cudaStream_t s) {
+    const long long n = out->d.N;
+    if (n == 0 || sp.in_channels == 0) return;
+    const unsigned g = grid_for(n, kThreads);
+    const long long fd = field_volume(sp, in->d.dim);
+    const float inv = 1.0f / static_cast<float>(fd);  // cnn_ops.cpp:295
+    if (sp.kernel == 2)
+        k_avg_pool<2><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, inv, res);
+    else if (sp.kernel == 3)
+        k_avg_pool<3><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, inv, res);
+    else
+        k_avg_pool_any<<<g, kThreads, 0, s>>>(in->d, out->d, sp.kernel, sp.stride, sp.pad, (int)fd, data,
+                                            sp.in_channels, inv, res);
+    launched("avg_pool");
+}
+
+void launch_unpool(bool avg, const float* cd, const int* sw, const hc_psh* fine, const hc_psh* coarse,
+                   const hc_conv_spec& sp, float* res, cudaStream_t s) {
+    const long long n = fine->d.N;
+    if (n == 0 || sp.in_channels == 0) return;
+    const unsigned g = grid_for(n, kThreads);
+    const float inv = 1.0f / static_cast<float>(field_volume(sp, fine->d.dim));  // cnn_ops.cpp:381
+    const int ka = cover_per_axis(sp);
+    const int kmax = fine->d.dim == 3 ? ka * ka * ka : ka * ka;
+    const int C = sp.in_channels;
+#define HC_UNPOOL(K)                                                                                             \
+    (avg ? k_unpool<K, true><<<g, kThreads, 0, s>>>(fine->d, coarse->d, sp.kernel, sp.stride, sp.pad, cd, sw, C, \
+                                                     inv, res)                                                   \
+         : k_unpool<K, false><<<g, kThreads, 0, s>>>(fine->d, coarse->d, sp.kernel, sp.stride, sp.pad, cd, sw, C, \
+                                                      inv, res))
+    if (kmax <= 1) HC_UNPOOL(1);
+    else if (kmax <= 8) HC_UNPOOL(8);
+    else if (kmax <= 27) HC_UNPOOL(27);
+    else if (avg)
+        k_unpool_any<true><<<g, kThreads, 0, s>>>(fine->d, coarse->d, sp.kernel, sp.stride, sp.pad, cd, sw, C, inv, res);
+    else
+        k_unpool_any<false><<<g, kThreads, 0, s>>>(fine->d, coarse->d, sp.kernel, sp.stride, sp.pad, cd, sw, C, inv, res);
+#undef HC_UNPOOL
+    launched("unpool");
+}
+
+// ------------------------------------------------------------------ contraction dispatch
+void fast_gemm_nn(const float* a, const float* b, float* c, long long ra, long long k, long long cb, cudaStream_t s);
+void fast_gemm_tn(const float* a, const float* b, float* c, long long ra, long long k, long long cb, cudaStream_t s);
+void fast_gemm_nt(const float* a, const float* b, float* c, long long ra, long long k, long long rb, cudaStream_t s);
+
+void gemm_nn(const float* a, const float* b, float* c, long long ra, long long k, long long cb, cudaStream_t s) {
+    if (current_math() == HC_MATH_FAST) fast_gemm_nn(a, b, c, ra, k, cb, s);
+    else gemm_nn_exact(a, b, c, ra, k, cb, s);
+}
+void gemm_tn(const float* a, const float* b, float* c, long long ra, long long k, long long cb, cudaStream_t s) {
+    if (current_math() == HC_MATH_FAST) fast_gemm_tn(a, b, c, ra, k, cb, s);
+    else gemm_tn_exact(a, b, c, ra, k, cb, s);
+}
+void gemm_nt(const float* a, const float* b, float* c, long long ra, long long k, long long rb, cudaStream_t s) {
+    if (current_math() == HC_MATH_FAST) fast_gemm_nt(a, b, c, ra, k, rb, s);
+    else gemm_nt_exact(a, b, c, ra, k, rb, s);
+}
+
+}  // namespace hcb
+
+using namespace hcb;
+
+// ====================================================================== C ABI
+extern "C" {
+
+hc_status hc_field_map(const hc_psh* in, const hc_psh* out, hc_conv_spec spec, int32_t* map, hc_stream stream) {
+    return guard([&] {
+        check_pair(in, out, spec);
+        launch_field_map(in, out, spec, map, as_stream(stream));
+    });
+}
+
+hc_status hc_hash2col_f32(const hc_psh* in, const float* data, int64_t data_rows, int64_t data_cols, const hc_psh* out,
+                          hc_conv_spec spec, float* cols, hc_stream stream) {
+    return guard([&] {
+        check_pair(in, out, spec);
+        if (data_rows != spec.in_channels || data_cols != in->d.N)
+            throw std::invalid_argument("hash2col: input data shape mismatch");
+        launch_hash2col(in, data, out, spec, cols, as_stream(stream));
+    });
+}
+
+hc_status hc_col2hash_f32(const float* col_grads, int64_t rows, int64_t cols, const hc_psh* in, const hc_psh* out,
+                          hc_conv_spec spec, float* result, hc_stream stream) {
+    return guard([&] {
+        check_pair(in, out, spec);
+        const long long fd = field_volume(spec, in->d.dim);
+        if (rows != spec.in_channels * fd || cols != out->d.N)
+            throw std::invalid_argument("col2hash: column gradient shape mismatch");
+        launch_col2hash(col_grads, in, out, spec, result, as_stream(stream));
+    });
+}
+
+hc_status hc_conv_forward_f32(const hc_psh* in, const float* data, int64_t data_rows, int64_t data_cols,
+                              const hc_psh* out, const float* w, int64_t w_rows, int64_t w_cols, hc_conv_spec spec,
+                              float* result, hc_stream stream) {
+    return guard([&] {
+        if (!in || !out) throw std::invalid_argument("null super-PSH handle");
+        const long long fd = field_volume(spec, in->d.dim);
+        if (w_rows != spec.out_channels || w_cols != spec.in_channels * fd)
+            throw std::invalid_argument("conv_forward: weight shape mismatch");
+        check_pair(in, out, spec);
+        if (data_rows != spec.in_channels || data_cols != in->d.N)
+            throw std::invalid_argument("hash2col: input data shape mismatch");
+        cudaStream_t s = as_stream(stream);
+        const long long K = spec.in_channels * fd, N = out->d.N;
+        Scratch cols(sizeof(float) * K * N, s);
+        launch_hash2col(in, data, out, spec, cols.as<float>(), s);
+        gemm_nn(w, cols.as<float>(), result, spec.out_channels, K, N, s);
+    });
+}
+
+hc_status hc_conv_backward_f32(const float* output_grad, int64_t g_rows, int64_t g_cols, const float* w,
+                               int64_t w_rows, int64_t w_cols, const float* cached_cols, int64_t c_rows,
+                               int64_t c_cols, const hc_psh* in, const hc_psh* out, hc_conv_spec spec, float* dw,
+                               float* dx, hc_stream stream) {
+    return guard([&] {
+        if (!in || !out) throw std::invalid_argument("null super-PSH handle");
+        const long long fd = field_volume(spec, in->d.dim);
+        if (g_rows != spec.out_channels || g_cols != out->d.N)
+            throw std::invalid_argument("conv_backward: output gradient shape mismatch");
+        if (c_rows != spec.in_channels * fd || c_cols != out->d.N)
+            throw std::invalid_argument("conv_backward: cached column shape mismatch");
+        // gemm.cpp:80-93 shape checks of the two products, then col2hash's
+        if (w_rows != g_rows) throw std::invalid_argument("matmul_trans_a: shape mismatch");
+        check_pair(in, out, spec);
+        if (w_cols != spec.in_channels * fd) throw std::invalid_argument("col2hash: column gradient shape mismatch");
+        cudaStream_t s = as_stream(stream);
+        gemm_nt(output_grad, cached_cols, dw, g_rows, g_cols, c_rows, s);  // dW = dDo * cols^T
+        Scratch dcols(sizeof(float) * w_cols * g_cols, s);
+        gemm_tn(w, output_grad, dcols.as<float>(), w_rows, w_cols, g_cols, s);  // W^T * dDo
+        launch_col2hash(dcols.as<float>(), in, out, spec, dx, s);
+    });
+}
+
+hc_status hc_max_pool_f32(const hc_psh* in, const float* data, int64_t data_rows, int64_t data_cols, const hc_psh* out,
+                          hc_conv_spec spec, float* result, int32_t* switches, hc_stream stream) {
+    return guard([&] {
+        check_pair(in, out, spec);
+        if (spec.stride < 2) throw std::invalid_argument("pooling requires stride >= 2");
+        if (data_rows != spec.in_channels || data_cols != in->d.N)
+            throw std::invalid_argument("max_pool: input data shape mismatch");
+        launch_max_pool(in, data, out, spec, result, switches, as_stream(stream));
+    });
+}
+
+hc_status hc_avg_pool_f32(const hc_psh* in, const float* data, int64_t data_rows, int64_t data_cols, const hc_psh* out,
+                          hc_conv_spec spec, float* result, hc_stream stream) {
+    return guard([&] {
+        check_pair(in, out, spec);
+        if (spec.stride < 2) throw std::invalid_argument("pooling requires stride >= 2");
+        if (data_rows != spec.in_channels || data_cols != in->d.N)
+            throw std::invalid_argument("avg_pool: input data shape mismatch");
+        launch_avg_pool(in, data, out, spec, result, as_stream(stream));
+    });
+}
+
+hc_status hc_max_unpool_f32(const float* coarse_data, int64_t c_rows, int64_t c_cols, const int32_t* switches,
+                            int64_t s_rows, int64_t s_cols, const hc_psh* fine, const hc_psh* coarse,
+                            hc_conv_spec spec, float* result, hc_stream stream) {
+    return guard([&] {
+        check_pair(fine, coarse, spec);
+        const long long fd = field_volume(spec, fine->d.dim);
+        if (c_rows != spec.in_channels || c_cols != coarse->d.N)
+            throw std::invalid_argument("max_unpool: coarse data shape mismatch");
+        // cnn_ops.cpp:326-332 check_switches (device scan; synchronises)
+        if (s_rows != spec.in_channels || s_cols != coarse->d.N)
+            throw std::invalid_argument("unpool: switch shape mismatch");
+        cudaStream_t s = as_stream(stream);
+        const long long n = s_rows * s_cols;
+        if (n > 0) {
+            Scratch flag(sizeof(int), s);
+            cuda_check(cudaMemsetAsync(flag.p, 0, sizeof(int), s), "memset");
+            k_check_switches<<<grid_for(n, kThreads), kThreads, 0, s>>>(switches, n, (int)fd, flag.as<int>());
+            launched("switch check");
+            int bad = 0;
+            cuda_check(cudaMemcpyAsync(&bad, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s), "switch check");
+            cuda_check(cudaStreamSynchronize(s), "switch check");
+            if (bad) throw std::invalid_argument("unpool: switch index out of range");
+        }
+        launch_unpool(false, coarse_data, switches, fine, coarse, spec, result, s);
+    });
+}
+
+hc_status hc_avg_unpool_f32(const float* coarse_data, int64_t c_rows, int64_t c_cols, const hc_psh* fine,
+                            const hc_psh* coarse, hc_conv_spec spec, float* result, hc_stream stream) {
+    return guard([&] {
+        check_pair(fine, coarse, spec);
+        if (c_rows != spec.in_channels || c_cols != coarse->d.N)
+            throw std::invalid_argument("avg_unpool: coarse data shape mismatch");
+        launch_unpool(true, coarse_data, nullptr, fine, coarse, spec, result, as_stream(stream));
+    });
+}
+
+hc_status hc_deconv_forward_f32(const hc_psh* coarse, const float* coarse_data, int64_t d_rows, int64_t d_cols,
+                                const hc_psh* fine, const float* w, int64_t w_rows, int64_t w_cols,
+                                hc_conv_spec spec, float* result, hc_stream stream) {
+    return guard([&] {
+        if (!coarse || !fine) throw std::invalid_argument("null super-PSH handle");
+        const long long fd = field_volume(spec, fine->d.dim);
+        if (w_rows != spec.out_channels || w_cols != spec.in_channels * fd)
+            throw std::invalid_argument("deconv_forward: weight shape mismatch");
+        if (d_rows != spec.out_channels || d_cols != coarse->d.N)
+            throw std::invalid_argument("deconv_forward: coarse data shape mismatch");
+        check_pair(fine, coarse, spec);
+        cudaStream_t s = as_stream(stream);
+        Scratch cols(sizeof(float) * w_cols * d_cols, s);
+        gemm_tn(w, coarse_data, cols.as<float>(), w_rows, w_cols, d_cols, s);  // W^T * D_i
+        launch_col2hash(cols.as<float>(), fine, coarse, spec, result, s);
+    });
+}
+
+hc_status hc_deconv_backward_f32(const float* fine_grad, int64_t g_rows, int64_t g_cols, const float* w,
+                                 int64_t w_rows, int64_t w_cols, const float* cached_coarse, int64_t c_rows,
+                                 int64_t c_cols, const hc_psh* coarse, const hc_psh* fine, hc_conv_spec spec,
+                                 float* dw, float* dx, hc_stream stream) {
+    return guard([&] {
+        if (!coarse || !fine) throw std::invalid_argument("null super-PSH handle");
+        if (g_rows != spec.in_channels || g_cols != fine->d.N)
+            throw std::invalid_argument("deconv_backward: fine gradient shape mismatch");
+        check_pair(fine, coarse, spec);
+        const long long fd = field_volume(spec, fine->d.dim);
+        const long long K = spec.in_channels * fd, N = coarse->d.N;
+        if (c_cols != N) throw std::invalid_argument("matmul_trans_b: shape mismatch");
+        if (w_cols != K) throw std::invalid_argument("matmul: shape mismatch");
+        cudaStream_t s = as_stream(stream);
+        Scratch dcols(sizeof(float) * K * N, s);
+        launch_hash2col(fine, fine_grad, coarse, spec, dcols.as<float>(), s);  // adjoint of col2hash
+        gemm_nt(cached_coarse, dcols.as<float>(), dw, c_rows, N, K, s);        // dW = D_i * dcols^T
+        gemm_nn(w, dcols.as<float>(), dx, w_rows, K, N, s);                    // dD_i = W * dcols
+    });
+}
+
+hc_status hc_matmul_f32(const float* a, const float* b, float* c, int64_t ra, int64_t k, int64_t cb, hc_stream stream) {
+    return guard([&] { gemm_nn(a, b, c, ra, k, cb, as_stream(stream)); });
+}
+hc_status hc_matmul_trans_a_f32(const float* a, const float* b, float* c, int64_t ra, int64_t k, int64_t cb,
+                                hc_stream stream) {
+    return guard([&] { gemm_tn(a, b, c, ra, k, cb, as_stream(stream)); });
+}
+hc_status hc_matmul_trans_b_f32(const float* a, const float* b, float* c, int64_t ra, int64_t k, int64_t rb,
+                                hc_stream stream) {
+    return guard([&] { gemm_nt(a, b, c, ra, k, rb, as_stream(stream)); });
+}
+
+}  // extern "C"

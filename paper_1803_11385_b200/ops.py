@@ -1,0 +1,285 @@
+"""Reference operator surface (cnn_ops.hpp / gemm.hpp) on the B200 path.
+
+Same names, argument meaning and error behaviour as `namespace hashconv`:
+structures are device super-PSHs (psh.SuperPsh), feature matrices are
+channels x columns fp32 tensors (feature_matrix.hpp:14-40), column matrices are
+(C*F^3) x N_out (cnn_ops.hpp:32-37). Spec/shape errors raise ValueError with the
+reference's std::invalid_argument message. Outputs are returned by value (new
+tensors), like the reference.
+
+Inputs may be CUDA tensors (device-resident path) or host numpy arrays / CPU
+tensors (end-to-end path: uploaded, computed on the GPU, downloaded). There is
+no CPU fallback: every call runs the sm_100a kernels of libhcb200.so.
+"""
+from __future__ import annotations
+
+import contextlib
+import ctypes as C
+from typing import NamedTuple
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, lib
+from .psh import SuperPsh
+
+
+class ConvSpec(NamedTuple):
+    """cnn_ops.hpp:11-17"""
+
+    kernel: int = 3
+    stride: int = 1
+    pad: int = 0
+    in_channels: int = 0
+    out_channels: int = 0
+
+    def c(self) -> _lib.ConvSpecC:
+        return _lib.ConvSpecC(int(self.kernel), int(self.stride), int(self.pad), int(self.in_channels),
+                              int(self.out_channels))
+
+
+def field_size(spec: ConvSpec, dim: int = 3) -> int:
+    """cnn_ops.hpp:19 field_size"""
+    return int(spec.kernel) ** dim
+
+
+class ConvGradients(NamedTuple):
+    """cnn_ops.hpp:48-52"""
+
+    weights: torch.Tensor
+    input: torch.Tensor
+
+
+class MaxPoolResult(NamedTuple):
+    """cnn_ops.hpp:75-79 (switches: int32 C x N_coarse)"""
+
+    output: torch.Tensor
+    switches: torch.Tensor
+
+
+# ------------------------------------------------------------------ plumbing
+def _dev() -> torch.device:
+    if not torch.cuda.is_available():
+        raise _lib.HashConvCudaError("no CUDA device: the hash-conv path runs on sm_100a only (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class _Args:
+    """Tracks whether the call came with host inputs (=> host outputs)."""
+
+    def __init__(self):
+        self.host = False
+
+    def f32(self, x) -> torch.Tensor:
+        if isinstance(x, np.ndarray):
+            self.host = True
+            x = torch.from_numpy(np.ascontiguousarray(x, np.float32))
+        if not x.is_cuda:
+            self.host = True
+            x = x.to(_dev(), non_blocking=True)
+        if x.dtype != torch.float32:
+            x = x.float()
+        return x.contiguous()
+
+    def i32(self, x) -> torch.Tensor:
+        if isinstance(x, np.ndarray):
+            self.host = True
+            x = torch.from_numpy(np.ascontiguousarray(x, np.int32))
+        if not x.is_cuda:
+            self.host = True
+            x = x.to(_dev(), non_blocking=True)
+        return x.to(torch.int32).contiguous()
+
+    def out(self, t: torch.Tensor):
+        return t.cpu().numpy() if self.host else t
+
+
+def _shape(t: torch.Tensor):
+    if t.dim() != 2:
+        raise ValueError("feature matrices are 2-D (rows x cols)")
+    return int(t.shape[0]), int(t.shape[1])
+
+
+def _p(t: torch.Tensor):
+    return C.c_void_p(t.data_ptr())
+
+
+def _empty(rows, cols, dtype=torch.float32):
+    return torch.empty((int(rows), int(cols)), dtype=dtype, device=_dev())
+
+
+@contextlib.contextmanager
+def math_mode(mode: str):
+    """'exact' (bit-identical to src/gemm.cpp order) or 'fast' (FFMA tiles / tensor cores)."""
+    prev = lib.hc_get_math()
+    check(lib.hc_set_math(_lib.HC_MATH_FAST if mode == "fast" else _lib.HC_MATH_EXACT))
+    try:
+        yield
+    finally:
+        lib.hc_set_math(prev)
+
+
+# ------------------------------------------------------------------ operators
+def field_map(input: SuperPsh, output: SuperPsh, spec: ConvSpec) -> torch.Tensor:
+    """K0: int32 N_out x F^dim, input column or -1 (cnn_ops.cpp:100-119 for every output)."""
+    spec = ConvSpec(*spec)
+    m = _empty(output.total_columns(), field_size(spec, input.dim), torch.int32)
+    check(lib.hc_field_map(input._h, output._h, spec.c(), _p(m), _stream()))
+    return m
+
+
+def locate(structure: SuperPsh, queries) -> torch.Tensor:
+    """psh_batch.cpp:56-78 batched: queries n x 4 int32 {model, x, y, z} -> int64 column or -1."""
+    a = _Args()
+    q = a.i32(queries)
+    r = torch.empty(q.shape[0], dtype=torch.int64, device=_dev())
+    check(lib.hc_locate(structure._h, _p(q), q.shape[0], _p(r), _stream()))
+    return a.out(r)
+
+
+def hash2col(input: SuperPsh, input_data, output: SuperPsh, spec: ConvSpec):
+    """cnn_ops.cpp:123-158"""
+    spec = ConvSpec(*spec)
+    a = _Args()
+    d = a.f32(input_data)
+    cols = _empty(spec.in_channels * field_size(spec, input.dim), output.total_columns())
+    check(lib.hc_hash2col_f32(input._h, _p(d), *_shape(d), output._h, spec.c(), _p(cols), _stream()))
+    return a.out(cols)
+
+
+def col2hash(col_grads, input: SuperPsh, output: SuperPsh, spec: ConvSpec):
+    """cnn_ops.cpp:160-204"""
+    spec = ConvSpec(*spec)
+    a = _Args()
+    g = a.f32(col_grads)
+    res = _empty(spec.in_channels, input.total_columns())
+    check(lib.hc_col2hash_f32(_p(g), *_shape(g), input._h, output._h, spec.c(), _p(res), _stream()))
+    return a.out(res)
+
+
+def conv_forward(input: SuperPsh, input_data, output: SuperPsh, weights, spec: ConvSpec):
+    """cnn_ops.cpp:206-215 (weights: C_out x C_in*F^dim)"""
+    spec = ConvSpec(*spec)
+    a = _Args()
+    d, w = a.f32(input_data), a.f32(weights)
+    res = _empty(spec.out_channels, output.total_columns())
+    check(lib.hc_conv_forward_f32(input._h, _p(d), *_shape(d), output._h, _p(w), *_shape(w), spec.c(), _p(res),
+                                  _stream()))
+    return a.out(res)
+
+
+def conv_backward(output_grad, weights, cached_cols, input: SuperPsh, output: SuperPsh, spec: ConvSpec):
+    """cnn_ops.cpp:217-232 -> ConvGradients(weights=dW, input=dX)"""
+    spec = ConvSpec(*spec)
+    a = _Args()
+    g, w, cc = a.f32(output_grad), a.f32(weights), a.f32(cached_cols)
+    gr, gc = _shape(g)
+    wr, wc = _shape(w)
+    dw = _empty(gr, _shape(cc)[0])
+    dx = _empty(spec.in_channels, input.total_columns())
+    check(lib.hc_conv_backward_f32(_p(g), gr, gc, _p(w), wr, wc, _p(cc), *_shape(cc), input._h, output._h,
+                                   spec.c(), _p(dw), _p(dx), _stream()))
+    return ConvGradients(a.out(dw), a.out(dx))
+
+
+def max_pool(input: SuperPsh, input_data, output: SuperPsh, spec: ConvSpec) -> MaxPoolResult:
+    """cnn_ops.cpp:234-284"""
+    spec = ConvSpec(*spec)
+    a = _Args()
+    d = a.f32(input_data)
+    res = _empty(spec.in_channels, output.total_columns())
+    sw = _empty(spec.in_channels, output.total_columns(), torch.int32)
+    check(lib.hc_max_pool_f32(input._h, _p(d), *_shape(d), output._h, spec.c(), _p(res), _p(sw), _stream()))
+    return MaxPoolResult(a.out(res), a.out(sw))
+
+
+def avg_pool(input: SuperPsh, input_data, output: SuperPsh, spec: ConvSpec):
+    """cnn_ops.cpp:286-322"""
+    spec = ConvSpec(*spec)
+    a = _Args()
+    d = a.f32(input_data)
+    res = _empty(spec.in_channels, output.total_columns())
+    check(lib.hc_avg_pool_f32(input._h, _p(d), *_shape(d), output._h, spec.c(), _p(res), _stream()))
+    return a.out(res)
+
+
+def max_unpool(coarse_data, switches, fine: SuperPsh, coarse: SuperPsh, spec: ConvSpec):
+    """cnn_ops.cpp:336-372 (switch range validated; synchronises)"""
+    spec = ConvSpec(*spec)
+    a = _Args()
+    cd, sw = a.f32(coarse_data), a.i32(switches)
+    res = _empty(spec.in_channels, fine.total_columns())
+    check(lib.hc_max_unpool_f32(_p(cd), *_shape(cd), _p(sw), *_shape(sw), fine._h, coarse._h, spec.c(), _p(res),
+                                _stream()))
+    return a.out(res)
+
+
+def avg_unpool(coarse_data, fine: SuperPsh, coarse: SuperPsh, spec: ConvSpec):
+    """cnn_ops.cpp:374-406"""
+    spec = ConvSpec(*spec)
+    a = _Args()
+    cd = a.f32(coarse_data)
+    res = _empty(spec.in_channels, fine.total_columns())
+    check(lib.hc_avg_unpool_f32(_p(cd), *_shape(cd), fine._h, coarse._h, spec.c(), _p(res), _stream()))
+    return a.out(res)
+
+
+def deconv_forward(coarse: SuperPsh, coarse_data, fine: SuperPsh, weights, spec: ConvSpec):
+    """cnn_ops.cpp:408-419"""
+    spec = ConvSpec(*spec)
+    a = _Args()
+    d, w = a.f32(coarse_data), a.f32(weights)
+    res = _empty(spec.in_channels, fine.total_columns())
+    check(lib.hc_deconv_forward_f32(coarse._h, _p(d), *_shape(d), fine._h, _p(w), *_shape(w), spec.c(), _p(res),
+                                    _stream()))
+    return a.out(res)
+
+
+def deconv_backward(fine_grad, weights, cached_coarse_data, coarse: SuperPsh, fine: SuperPsh, spec: ConvSpec):
+    """cnn_ops.cpp:421-435 -> ConvGradients(weights=dW, input=dX(coarse))"""
+    spec = ConvSpec(*spec)
+    a = _Args()
+    g, w, cd = a.f32(fine_grad), a.f32(weights), a.f32(cached_coarse_data)
+    dw = _empty(_shape(cd)[0], spec.in_channels * field_size(spec, fine.dim))
+    dx = _empty(_shape(w)[0], coarse.total_columns())
+    check(lib.hc_deconv_backward_f32(_p(g), *_shape(g), _p(w), *_shape(w), _p(cd), *_shape(cd), coarse._h, fine._h,
+                                     spec.c(), _p(dw), _p(dx), _stream()))
+    return ConvGradients(a.out(dw), a.out(dx))
+
+
+def matmul(a_, b_):
+    """gemm.cpp:71-77: c = a * b"""
+    a = _Args()
+    x, y = a.f32(a_), a.f32(b_)
+    if x.shape[1] != y.shape[0]:
+        raise ValueError("matmul: shape mismatch")
+    c = _empty(x.shape[0], y.shape[1])
+    check(lib.hc_matmul_f32(_p(x), _p(y), _p(c), x.shape[0], x.shape[1], y.shape[1], _stream()))
+    return a.out(c)
+
+
+def matmul_trans_a(a_, b_):
+    """gemm.cpp:79-85: c = a^T * b"""
+    a = _Args()
+    x, y = a.f32(a_), a.f32(b_)
+    if x.shape[0] != y.shape[0]:
+        raise ValueError("matmul_trans_a: shape mismatch")
+    c = _empty(x.shape[1], y.shape[1])
+    check(lib.hc_matmul_trans_a_f32(_p(x), _p(y), _p(c), x.shape[0], x.shape[1], y.shape[1], _stream()))
+    return a.out(c)
+
+
+def matmul_trans_b(a_, b_):
+    """gemm.cpp:87-93: c = a * b^T"""
+    a = _Args()
+    x, y = a.f32(a_), a.f32(b_)
+    if x.shape[1] != y.shape[1]:
+        raise ValueError("matmul_trans_b: shape mismatch")
+    c = _empty(x.shape[0], y.shape[0])
+    check(lib.hc_matmul_trans_b_f32(_p(x), _p(y), _p(c), x.shape[0], x.shape[1], y.shape[0], _stream()))
+    return a.out(c)

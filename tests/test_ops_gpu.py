@@ -1,0 +1,347 @@
+"""GPU parity of the reference-layout operators (C ABI through ops.py) against the
+reference's golden fixtures, the CPU oracle (oracle/hc_oracle.c) and the reference's
+own known-answer tests (tests/test_cnn_ops.cpp). EXACT math is bit-identical; FAST
+math is checked against the double instantiation with a normwise bound."""
+import numpy as np
+import pytest
+import torch
+
+from helpers import GOLDEN, golden_instances, levels_to_arrays, load_instance, random_pair, rel_fro, sha, shell_pair
+
+pytestmark = pytest.mark.gpu
+
+from paper_1803_11385_b200 import ops  # noqa: E402
+from paper_1803_11385_b200.ops import ConvSpec  # noqa: E402
+from paper_1803_11385_b200.psh import PshLevel, SuperPsh, VoxelSet  # noqa: E402
+
+FAST_TOL = 1e-5  # ||gpu - ref64||_F / ||ref64||_F for fp32
+
+
+def _np(t):
+    return t.detach().cpu().numpy() if isinstance(t, torch.Tensor) else t
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+# ---------------------------------------------------------------- golden instances
+@pytest.mark.parametrize("path", golden_instances(), ids=lambda p: p.split("/")[-1])
+def test_golden_instance_bit_exact(cuda, path):
+    z, fa, ca = load_instance(path)
+    fine, coarse = SuperPsh.from_host(fa), SuperPsh.from_host(ca)
+    spec = ConvSpec(*(int(x) for x in z["spec"]))
+    dc_spec = ConvSpec(*(int(x) for x in z["dc_spec"]))
+    pool = ConvSpec(*(int(x) for x in z["pool_spec"]))
+    out_s = fine if spec.stride == 1 else coarse
+    data, w, dout = _dev(z["data"]), _dev(z["w"]), _dev(z["dout"])
+    cols = ops.hash2col(fine, data, out_s, spec)
+    assert sha(_np(cols)) == str(z["cols_sha"])
+    assert np.array_equal(_np(ops.conv_forward(fine, data, out_s, w, spec)), z["conv_out"])
+    g = ops.conv_backward(dout, w, cols, fine, out_s, spec)
+    assert np.array_equal(_np(g.weights), z["dw"])
+    assert np.array_equal(_np(g.input), z["dx"])
+    mp = ops.max_pool(fine, data, coarse, pool)
+    assert np.array_equal(_np(mp.output), z["mp"]) and np.array_equal(_np(mp.switches), z["sw"])
+    assert np.array_equal(_np(ops.avg_pool(fine, data, coarse, pool)), z["ap"])
+    assert np.array_equal(_np(ops.max_unpool(mp.output, mp.switches, fine, coarse, pool)), z["max_restored"])
+    assert np.array_equal(_np(ops.avg_unpool(_dev(z["coarse_vals"]), fine, coarse, pool)), z["avg_restored"])
+    assert np.array_equal(_np(ops.deconv_forward(coarse, _dev(z["dc_in"]), fine, _dev(z["dc_w"]), dc_spec)),
+                          z["dc_out"])
+    b = ops.deconv_backward(data, _dev(z["dc_w"]), _dev(z["dc_in"]), coarse, fine, dc_spec)
+    assert np.array_equal(_np(b.weights), z["dcb_dw"]) and np.array_equal(_np(b.input), z["dcb_dx"])
+    assert np.array_equal(_np(ops.col2hash(_dev(z["y"]), fine, out_s, spec)), z["c2h"])
+
+
+@pytest.mark.parametrize("path", golden_instances()[:6], ids=lambda p: p.split("/")[-1])
+def test_golden_instance_fast_math_tolerance(cuda, path):
+    z, fa, ca = load_instance(path)
+    fine, coarse = SuperPsh.from_host(fa), SuperPsh.from_host(ca)
+    spec = ConvSpec(*(int(x) for x in z["spec"]))
+    out_s = fine if spec.stride == 1 else coarse
+    with ops.math_mode("fast"):
+        data, w, dout = _dev(z["data"]), _dev(z["w"]), _dev(z["dout"])
+        out = ops.conv_forward(fine, data, out_s, w, spec)
+        cols = ops.hash2col(fine, data, out_s, spec)
+        g = ops.conv_backward(dout, w, cols, fine, out_s, spec)
+    assert rel_fro(_np(out), z["conv64"]) <= FAST_TOL
+    assert rel_fro(_np(g.weights), z["dw64"]) <= FAST_TOL
+    assert rel_fro(_np(g.input), z["dx64"]) <= FAST_TOL
+
+
+def test_shell32_config1_digests(cuda):
+    """BASELINE config 1: 32^3 shell, 3x3x3 conv C 8->16 fwd/bwd + max-pool (+unpool)."""
+    from oracle.oracle import Ref, have_ref
+    z = np.load(f"{GOLDEN}/shell32.npz")
+    f, c = shell_pair(32, 1)
+    fine, coarse = SuperPsh.from_levels(f), SuperPsh.from_levels(c)
+    assert fine.total_columns() == 3680 and coarse.total_columns() == 896
+    if not have_ref():
+        pytest.skip("seeded inputs come from the reference RNG (oracle/_ref)")
+    ref = Ref()
+    data = _dev(ref.random_matrix(8, 3680, 5))
+    w = _dev(ref.random_matrix(16, 8 * 27, 6))
+    dout = _dev(ref.random_matrix(16, 3680, 7))
+    spec, pool = ConvSpec(3, 1, 0, 8, 16), ConvSpec(2, 2, 0, 8, 8)
+    cols = ops.hash2col(fine, data, fine, spec)
+    assert sha(_np(cols)) == str(z["cols"])
+    assert sha(_np(ops.conv_forward(fine, data, fine, w, spec))) == str(z["conv_out"])
+    g = ops.conv_backward(dout, w, cols, fine, fine, spec)
+    assert sha(_np(g.weights)) == str(z["dw"]) and sha(_np(g.input)) == str(z["dx"])
+    mp = ops.max_pool(fine, data, coarse, pool)
+    assert sha(_np(mp.output)) == str(z["mp"]) and sha(_np(mp.switches)) == str(z["sw"])
+    assert sha(_np(ops.max_unpool(mp.output, mp.switches, fine, coarse, pool))) == str(z["unpool"])
+
+
+# ---------------------------------------------------------------- oracle parity, larger
+@pytest.mark.parametrize("spec", [(3, 1, 0), (2, 2, 0), (3, 2, 0), (2, 2, 1), (1, 1, 0), (5, 1, 0), (4, 2, 1)])
+def test_random_batches_vs_oracle(cuda, restated, spec):
+    f, c = random_pair(16, 3, seed=hash(spec) & 0xFFFF, n_lo=150, n_hi=600)
+    fa, ca = levels_to_arrays(f), levels_to_arrays(c)
+    fine, coarse = SuperPsh.from_levels(f), SuperPsh.from_levels(c)
+    sp = ConvSpec(*spec, 5, 7)
+    out_s, out_a = (fine, fa) if sp.stride == 1 else (coarse, ca)
+    rng = np.random.default_rng(1)
+    fd = sp.kernel ** 3
+    data = rng.uniform(-1, 1, (5, fa.total_columns())).astype(np.float32)
+    w = rng.uniform(-1, 1, (7, 5 * fd)).astype(np.float32)
+    dout = rng.uniform(-1, 1, (7, out_a.total_columns())).astype(np.float32)
+    fm = _np(ops.field_map(fine, out_s, sp))
+    assert np.array_equal(fm.astype(np.int64), restated.field_map(fa, out_a, sp))
+    cols = ops.hash2col(fine, _dev(data), out_s, sp)
+    ocols = restated.hash2col(fa, data, out_a, sp)
+    assert np.array_equal(_np(cols), ocols)
+    assert np.array_equal(_np(ops.conv_forward(fine, _dev(data), out_s, _dev(w), sp)), restated.matmul(w, ocols))
+    g = ops.conv_backward(_dev(dout), _dev(w), cols, fine, out_s, sp)
+    odw, odx = restated.conv_backward(dout, w, ocols, fa, out_a, sp)
+    assert np.array_equal(_np(g.weights), odw) and np.array_equal(_np(g.input), odx)
+    if sp.stride > 1:
+        psp = ConvSpec(sp.kernel, sp.stride, sp.pad, 5, 5)
+        mp = ops.max_pool(fine, _dev(data), coarse, psp)
+        om, osw = restated.max_pool(fa, data, ca, psp)
+        assert np.array_equal(_np(mp.output), om) and np.array_equal(_np(mp.switches), osw)
+        assert np.array_equal(_np(ops.max_unpool(mp.output, mp.switches, fine, coarse, psp)),
+                              restated.max_unpool(om, osw, fa, ca, psp))
+        assert np.array_equal(_np(ops.avg_pool(fine, _dev(data), coarse, psp)), restated.avg_pool(fa, data, ca, psp))
+        cv = rng.uniform(-1, 1, (5, ca.total_columns())).astype(np.float32)
+        assert np.array_equal(_np(ops.avg_unpool(_dev(cv), fine, coarse, psp)), restated.avg_unpool(cv, fa, ca, psp))
+
+
+def test_shell64_batch4_vs_oracle(cuda, restated):
+    f, c = shell_pair(64, 4)
+    fa, ca = levels_to_arrays(f), levels_to_arrays(c)
+    fine, coarse = SuperPsh.from_levels(f), SuperPsh.from_levels(c)
+    sp = ConvSpec(3, 1, 0, 16, 16)
+    rng = np.random.default_rng(2)
+    N = fa.total_columns()
+    data = rng.uniform(-1, 1, (16, N)).astype(np.float32)
+    cols = ops.hash2col(fine, _dev(data), fine, sp)
+    ocols = restated.hash2col(fa, data, fa, sp)
+    assert np.array_equal(_np(cols), ocols)
+    y = rng.uniform(-1, 1, ocols.shape).astype(np.float32)
+    assert np.array_equal(_np(ops.col2hash(_dev(y), fine, fine, sp)), restated.col2hash(y, fa, fa, sp))
+    psp = ConvSpec(2, 2, 0, 16, 16)
+    mp = ops.max_pool(fine, _dev(data), coarse, psp)
+    om, osw = restated.max_pool(fa, data, ca, psp)
+    assert np.array_equal(_np(mp.output), om) and np.array_equal(_np(mp.switches), osw)
+    assert np.array_equal(_np(ops.max_unpool(mp.output, mp.switches, fine, coarse, psp)),
+                          restated.max_unpool(om, osw, fa, ca, psp))
+
+
+def test_locate_matches_oracle(cuda, restated):
+    f, _ = random_pair(16, 2, seed=5)
+    fa = levels_to_arrays(f)
+    s = SuperPsh.from_levels(f)
+    rng = np.random.default_rng(0)
+    q = np.concatenate([rng.integers(1, 3, (4000, 1)), rng.integers(0, 16, (4000, 3))], axis=1).astype(np.int32)
+    got = _np(ops.locate(s, _dev(q)))
+    want = np.array([restated.locate(fa, int(r[0]), r[1:]) for r in q])
+    assert np.array_equal(got, want)
+    back = s.download()
+    for k in ("hash", "offsets", "tags", "model_of_slot", "hash_acc", "offset_acc", "data_acc"):
+        assert np.array_equal(getattr(back, k), getattr(fa, k).astype(getattr(back, k).dtype))
+
+
+# ---------------------------------------------------------------- known-answer tests (test_cnn_ops.cpp)
+def _single(p, res, value=2.5):
+    lvl = PshLevel.build(VoxelSet.make(3, res, [p], [[value]]))
+    return SuperPsh.from_levels([lvl]), torch.tensor([[value]], device="cuda")
+
+
+def test_kat_isolated_voxel_center_row(cuda):  # test_cnn_ops.cpp:53-62
+    s, d = _single((4, 4, 4), 8)
+    cols = _np(ops.hash2col(s, d, s, ConvSpec(3, 1, 0, 1, 1)))
+    assert cols.shape == (27, 1)
+    assert all(cols[r, 0] == (2.5 if r == 13 else 0.0) for r in range(27))
+
+
+def test_kat_stride2_field_gathers_cube(cuda):  # test_cnn_ops.cpp:64-97
+    coords = [(x, y, z) for z in (2, 3) for y in (2, 3) for x in (2, 3)] + [(0, 0, 0), (5, 5, 5)]
+    vals = [100 + i for i in range(8)] + [7, 9]
+    fs = VoxelSet.make(3, 8, coords, [vals])
+    fine = SuperPsh.from_levels([PshLevel.build(fs)])
+    coarse = SuperPsh.from_levels([PshLevel.build(VoxelSet.make(3, 4, [(1, 1, 1)], [[0.0]]))])
+    fc, ff = fs.arrays()
+    cols = _np(ops.hash2col(fine, _dev(ff), coarse, ConvSpec(2, 2, 0, 1, 1)))
+    assert cols.shape == (8, 1)
+    for row in range(8):
+        p = (2 + (row & 1), 2 + ((row >> 1) & 1), 2 + (row >> 2))
+        idx = [tuple(c) for c in fc].index(p)
+        assert cols[row, 0] == ff[0, idx]
+
+
+def test_kat_col2hash_two_voxels(cuda):  # test_cnn_ops.cpp:140-156
+    s = SuperPsh.from_levels([PshLevel.build(VoxelSet.make(3, 8, [(3, 3, 3), (4, 3, 3)], [[1.0, 1.0]]))])
+    dcols = np.zeros((27, 2), np.float32)
+    dcols[13, 0], dcols[14, 0], dcols[12, 1], dcols[13, 1] = 10, 20, 40, 80
+    g = _np(ops.col2hash(_dev(dcols), s, s, ConvSpec(3, 1, 0, 1, 1)))
+    assert g[0, 0] == 50.0 and g[0, 1] == 100.0
+
+
+def test_kat_delta_kernel_and_all_ones(cuda):  # test_cnn_ops.cpp:196-216
+    f, _ = random_pair(16, 2, seed=43)
+    s = SuperPsh.from_levels(f)
+    data = levels_to_arrays(f).data
+    w = np.zeros((3, 81), np.float32)
+    for ch in range(3):
+        w[ch, ch * 27 + 13] = 1.0
+    assert np.array_equal(_np(ops.conv_forward(s, _dev(data), s, _dev(w), ConvSpec(3, 1, 0, 3, 3))), data)
+    s1, d1 = _single((4, 4, 4), 8, 1.75)
+    out = _np(ops.conv_forward(s1, d1, s1, torch.ones((1, 27), device="cuda"), ConvSpec(3, 1, 0, 1, 1)))
+    assert out[0, 0] == np.float32(1.75)
+
+
+def test_kat_dw_center_tap_only(cuda):  # test_cnn_ops.cpp:248-262
+    s, d = _single((4, 4, 4), 8, 3.0)
+    sp = ConvSpec(3, 1, 0, 1, 2)
+    w = torch.rand((2, 27), device="cuda")
+    cols = ops.hash2col(s, d, s, sp)
+    dout = torch.tensor([[5.0], [-2.0]], device="cuda")
+    dw = _np(ops.conv_backward(dout, w, cols, s, s, sp).weights)
+    for r, v in enumerate((5.0, -2.0)):
+        for k in range(27):
+            assert dw[r, k] == (v * 3.0 if k == 13 else 0.0)
+
+
+def test_kat_zero_output_grad(cuda):  # test_cnn_ops.cpp:236-246
+    f, _ = random_pair(16, 1, seed=51)
+    s = SuperPsh.from_levels(f)
+    sp = ConvSpec(3, 1, 0, 3, 4)
+    d = _dev(levels_to_arrays(f).data)
+    cols = ops.hash2col(s, d, s, sp)
+    g = ops.conv_backward(torch.zeros((4, s.total_columns()), device="cuda"), torch.rand((4, 81), device="cuda"),
+                          cols, s, s, sp)
+    assert not _np(g.weights).any() and not _np(g.input).any()
+
+
+def test_kat_pools_over_block_1_to_8(cuda):  # test_cnn_ops.cpp:308-344
+    coords = [(x, y, z) for z in (4, 5) for y in (4, 5) for x in (4, 5)]
+    fs = VoxelSet.make(3, 8, coords, [list(range(1, 9))])
+    fine = SuperPsh.from_levels([PshLevel.build(fs)])
+    coarse = SuperPsh.from_levels([PshLevel.build(fs.coarsen())])
+    sp = ConvSpec(2, 2, 0, 1, 1)
+    d = _dev(fs.arrays()[1])
+    mp = ops.max_pool(fine, d, coarse, sp)
+    assert _np(mp.output)[0, 0] == 8.0 and _np(mp.switches)[0, 0] == 7
+    assert _np(ops.avg_pool(fine, d, coarse, sp))[0, 0] == np.float32(36.0 / 8.0)
+    one = VoxelSet.make(3, 8, [(4, 4, 4)], [[-3.5]])
+    f1, c1 = SuperPsh.from_levels([PshLevel.build(one)]), SuperPsh.from_levels([PshLevel.build(one.coarsen())])
+    m1 = ops.max_pool(f1, torch.tensor([[-3.5]], device="cuda"), c1, sp)
+    assert _np(m1.output)[0, 0] == -3.5 and _np(m1.switches)[0, 0] == 0
+
+
+def test_kat_unpools(cuda):  # test_cnn_ops.cpp:373-400, 446-468
+    one = VoxelSet.make(3, 8, [(5, 2, 7)], [[4.25]])
+    f1, c1 = SuperPsh.from_levels([PshLevel.build(one)]), SuperPsh.from_levels([PshLevel.build(one.coarsen())])
+    sp = ConvSpec(2, 2, 0, 1, 1)
+    d = torch.tensor([[4.25]], device="cuda")
+    mp = ops.max_pool(f1, d, c1, sp)
+    assert np.array_equal(_np(ops.max_unpool(mp.output, mp.switches, f1, c1, sp)), np.array([[4.25]], np.float32))
+    cube = VoxelSet.make(3, 8, [(x, y, z) for z in (0, 1) for y in (0, 1) for x in (0, 1)], [[0.0] * 8])
+    fc, cc = SuperPsh.from_levels([PshLevel.build(cube)]), SuperPsh.from_levels([PshLevel.build(cube.coarsen())])
+    out = _np(ops.avg_unpool(torch.tensor([[8.0]], device="cuda"), fc, cc, sp))
+    assert np.allclose(out, 1.0)
+    cube2 = VoxelSet.make(3, 8, [(x, y, z) for z in (2, 3) for y in (2, 3) for x in (2, 3)], [[0.0] * 8])
+    f2, c2 = SuperPsh.from_levels([PshLevel.build(cube2)]), SuperPsh.from_levels([PshLevel.build(cube2.coarsen())])
+    dc = _np(ops.deconv_forward(c2, torch.tensor([[6.5]], device="cuda"), f2, torch.ones((1, 8), device="cuda"), sp))
+    assert np.array_equal(dc, np.full((1, 8), 6.5, np.float32))
+
+
+def test_errors_mirror_reference_messages(cuda):
+    f, c = random_pair(16, 1, seed=97)
+    f2, _ = random_pair(16, 2, seed=98)
+    fine, coarse, two = SuperPsh.from_levels(f), SuperPsh.from_levels(c), SuperPsh.from_levels(f2)
+    d = _dev(levels_to_arrays(f).data)
+    sp = ConvSpec(2, 2, 0, 3, 3)
+    mp = ops.max_pool(fine, d, coarse, sp)
+    sw = mp.switches.clone()
+    sw[0, 0] = 8  # F^3 == 8 is out of range (test_cnn_ops.cpp:436-444)
+    with pytest.raises(ValueError, match="unpool: switch index out of range"):
+        ops.max_unpool(mp.output, sw, fine, coarse, sp)
+    with pytest.raises(ValueError, match="batch size mismatch"):
+        ops.hash2col(fine, d, two, ConvSpec(3, 1, 0, 3, 3))
+    with pytest.raises(ValueError, match="stride-1 fields need an odd kernel size"):
+        ops.hash2col(fine, d, fine, ConvSpec(2, 1, 0, 3, 3))
+    with pytest.raises(ValueError, match="stride-1 ops keep the level fixed"):
+        ops.hash2col(fine, d, coarse, ConvSpec(3, 1, 0, 3, 3))
+    with pytest.raises(ValueError, match="input resolution must be output resolution \\* stride"):
+        ops.hash2col(fine, d, fine, ConvSpec(2, 2, 0, 3, 3))
+    with pytest.raises(ValueError, match="bad conv spec"):
+        ops.hash2col(fine, d, fine, ConvSpec(0, 1, 0, 3, 3))
+    with pytest.raises(ValueError, match="hash2col: input data shape mismatch"):
+        ops.hash2col(fine, d[:2], fine, ConvSpec(3, 1, 0, 3, 3))
+    with pytest.raises(ValueError, match="pooling requires stride >= 2"):
+        ops.max_pool(fine, d, fine, ConvSpec(3, 1, 0, 3, 3))
+    with pytest.raises(ValueError, match="conv_forward: weight shape mismatch"):
+        ops.conv_forward(fine, d, fine, torch.ones((4, 80), device="cuda"), ConvSpec(3, 1, 0, 3, 4))
+    with pytest.raises(ValueError, match="col2hash: column gradient shape mismatch"):
+        ops.col2hash(torch.ones((80, fine.total_columns()), device="cuda"), fine, fine, ConvSpec(3, 1, 0, 3, 3))
+
+
+# ---------------------------------------------------------------- full-size properties (256^3, b=8)
+@pytest.fixture(scope="module")
+def shell256(cuda):
+    f, c = shell_pair(256, 8)
+    return SuperPsh.from_levels(f), SuperPsh.from_levels(c)
+
+
+def test_full_size_pool_unpool_idempotence(shell256):
+    """pool(unpool(pool(x))) == pool(x) at BASELINE config 4 size (test_cnn_ops.cpp:402-410)."""
+    fine, coarse = shell256
+    assert fine.total_columns() == 8 * 228296
+    sp = ConvSpec(2, 2, 0, 16, 16)
+    x = torch.rand((16, fine.total_columns()), device="cuda") * 2 - 1
+    once = ops.max_pool(fine, x, coarse, sp)
+    back = ops.max_unpool(once.output, once.switches, fine, coarse, sp)
+    twice = ops.max_pool(fine, back, coarse, sp)
+    assert torch.equal(twice.output, once.output)
+    assert torch.equal(twice.switches, once.switches)
+
+
+def test_full_size_delta_kernel_and_adjoint(shell256):
+    fine, _ = shell256
+    C = 4
+    sp = ConvSpec(3, 1, 0, C, C)
+    x = torch.rand((C, fine.total_columns()), device="cuda") * 2 - 1
+    w = torch.zeros((C, C * 27), device="cuda")
+    for ch in range(C):
+        w[ch, ch * 27 + 13] = 1.0
+    assert torch.equal(ops.conv_forward(fine, x, fine, w, sp), x)
+    cols = ops.hash2col(fine, x, fine, sp)
+    y = torch.rand_like(cols) * 2 - 1
+    lhs = torch.dot(cols.double().flatten(), y.double().flatten())
+    rhs = torch.dot(x.double().flatten(), ops.col2hash(y, fine, fine, sp).double().flatten())
+    assert abs(float(lhs - rhs)) / max(abs(float(lhs)), 1e-6) <= 1e-6
+
+
+def test_full_size_field_map_symmetry(shell256):
+    """Stride-1 neighbourhoods are symmetric: map[o, t] = g  <=>  map[g, 26 - t] = o."""
+    fine, _ = shell256
+    m = ops.field_map(fine, fine, ConvSpec(3, 1, 0, 1, 1)).long()
+    n = m.shape[0]
+    o = torch.arange(n, device="cuda").unsqueeze(1).expand(n, 27)
+    t = torch.arange(27, device="cuda").unsqueeze(0).expand(n, 27)
+    hit = m >= 0
+    back = m.clamp(min=0)[hit], (26 - t)[hit]
+    assert torch.equal(m[back[0], back[1]], o[hit])
+    assert torch.equal(m[:, 13], torch.arange(n, device="cuda"))  # centre tap is the voxel itself
