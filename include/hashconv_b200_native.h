@@ -1,0 +1,64 @@
+/* hashconv_b200_native.h — native (voxel-major) fused hash-conv on tcgen05 tensor cores.
+ *
+ * The B200-first form of the reference's conv contraction (cnn_ops.cpp:206-232 =
+ * hash2col + matmul / matmul_trans_b / matmul_trans_a + col2hash): an implicit GEMM
+ * whose A operand is gathered through the field map (hc_field_map) straight into
+ * shared memory, so the (C*F^3) x N column matrix never exists in HBM.
+ *
+ * Layouts: features are voxel-major bf16 [N][C] (C a multiple of 8); the field map
+ * is int32 [N_out][taps] (-1 = empty cell); weights are packed once per update from
+ * the reference layout W[co][ci*taps + t] (cnn_ops.hpp:21-27) by
+ * hc_native_pack_weights. Device pointers, stream-ordered, deterministic.
+ */
+#ifndef HASHCONV_B200_NATIVE_H
+#define HASHCONV_B200_NATIVE_H
+
+#include "hashconv_b200.h"
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Packed K extent (taps * channels rounded up to 64). */
+int64_t hc_native_packed_k(int32_t channels, int32_t taps);
+
+/* backward = 0: Wp[co][t*C_in + ci] = W[co][ci*taps + t]           (forward operand)
+ * backward = 1: Wp[ci][t*C_out + co] = W[co][ci*taps + taps-1-t]    (stride-1 input-gradient
+ *               operand: the transposed, tap-flipped kernel)
+ * w_packed: bf16, rows x hc_native_packed_k(...) */
+hc_status hc_native_pack_weights(const float* w_ref, int32_t c_out, int32_t c_in, int32_t taps,
+                                 int32_t backward, void* w_packed, hc_stream stream);
+
+/* Y[n][0:c_out] = sum_{t,ci} X[fmap[n][t]][ci] * Wp[co][t*c_in + ci]  (gather-GEMM, tcgen05).
+ * Forward conv: (fmap of (in,out), X, forward pack). Stride-1 input gradient:
+ * (fmap of the structure, dY, backward pack) gives dX. c_out in {16,32,64,128,256}. */
+hc_status hc_native_gather_gemm(const int32_t* fmap, int64_t n_out, int32_t taps, const void* x,
+                                int32_t c_in, const void* w_packed, int32_t c_out, void* y,
+                                hc_dtype y_dtype, hc_stream stream);
+
+/* dW in the reference layout (C_out x C_in*taps, fp32):
+ * dW[co][ci*taps + t] = sum_n dY[n][co] * X[fmap[n][t]][ci]  (cnn_ops.cpp:228 matmul_trans_b).
+ * Split-K over voxels on tcgen05, partials reduced in a fixed order (deterministic). */
+size_t hc_native_dw_workspace(int64_t n_out, int32_t taps, int32_t c_in, int32_t c_out);
+hc_status hc_native_conv_dw(const int32_t* fmap, int64_t n_out, int32_t taps, const void* x,
+                            int32_t c_in, const void* dy, int32_t c_out, float* dw_ref,
+                            void* workspace, size_t ws_bytes, hc_stream stream);
+
+/* Boundary transposes between the reference layout (C x N fp32) and the native layout. */
+hc_status hc_native_to_voxel_major(const float* ref, int64_t c, int64_t n, void* out_bf16,
+                                   hc_stream stream);
+hc_status hc_native_to_channel_major(const void* native, hc_dtype dtype, int64_t n, int64_t c,
+                                     float* out, hc_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#endif /* HASHCONV_B200_NATIVE_H */

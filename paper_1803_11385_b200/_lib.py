@@ -89,6 +89,18 @@ _SIGS = {
     "hc_matmul_trans_a_f32": [_P, _P, _P, _I64, _I64, _I64, _P],
     "hc_matmul_trans_b_f32": [_P, _P, _P, _I64, _I64, _I64, _P],
 }
+_SIGS.update({
+    "hc_native_pack_weights": [_P, _I32, _I32, _I32, _I32, _P, _P],
+    "hc_native_gather_gemm": [_P, _I64, _I32, _P, _I32, _P, _I32, _P, C.c_int, _P],
+    "hc_native_conv_dw": [_P, _I64, _I32, _P, _I32, _P, _I32, _P, _P, C.c_size_t, _P],
+    "hc_native_to_voxel_major": [_P, _I64, _I64, _P, _P],
+    "hc_native_to_channel_major": [_P, C.c_int, _I64, _I64, _P, _P],
+})
+lib.hc_native_packed_k.restype = C.c_int64
+lib.hc_native_packed_k.argtypes = [_I32, _I32]
+lib.hc_native_dw_workspace.restype = C.c_size_t
+lib.hc_native_dw_workspace.argtypes = [_I64, _I32, _I32, _I32]
+lib.hc_launch_count.restype = C.c_int64
 for _name, _args in _SIGS.items():
     fn = getattr(lib, _name)
     fn.argtypes = _args

@@ -1,0 +1,141 @@
+"""Native fused hash-conv layer on tcgen05 tensor cores (include/hashconv_b200_native.h).
+
+The B200-first form of conv_forward / conv_backward (cnn_ops.cpp:206-232):
+features are voxel-major bf16 tensors [N][C]; the field map (K0) is computed once
+per structure pair and reused by forward, input-gradient and weight-gradient; the
+column matrix is never materialised. Weights and weight gradients use the
+reference layout W[co][ci*F^3 + t] (cnn_ops.hpp:21-27).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, lib
+from .ops import ConvSpec, field_map, field_size
+from .psh import SuperPsh
+
+
+def _p(t: torch.Tensor):
+    return C.c_void_p(t.data_ptr())
+
+
+def _s():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def to_voxel_major(ref: torch.Tensor) -> torch.Tensor:
+    """C x N fp32 (reference layout) -> N x C bf16."""
+    ref = ref.contiguous().float()
+    c, n = ref.shape
+    out = torch.empty((n, c), dtype=torch.bfloat16, device=ref.device)
+    check(lib.hc_native_to_voxel_major(_p(ref), c, n, _p(out), _s()))
+    return out
+
+
+def to_channel_major(nat: torch.Tensor) -> torch.Tensor:
+    """N x C (fp32 or bf16) -> C x N fp32 (reference layout)."""
+    nat = nat.contiguous()
+    n, c = nat.shape
+    out = torch.empty((c, n), dtype=torch.float32, device=nat.device)
+    dt = _lib.HC_DTYPE_F32 if nat.dtype == torch.float32 else _lib.HC_DTYPE_BF16
+    check(lib.hc_native_to_channel_major(_p(nat), dt, n, c, _p(out), _s()))
+    return out
+
+
+def pack_weights(w_ref: torch.Tensor, c_out: int, c_in: int, taps: int, backward: bool) -> torch.Tensor:
+    w_ref = w_ref.contiguous().float()
+    rows = c_in if backward else c_out
+    kp = int(lib.hc_native_packed_k(c_out if backward else c_in, taps))
+    wp = torch.empty((rows, kp), dtype=torch.bfloat16, device=w_ref.device)
+    check(lib.hc_native_pack_weights(_p(w_ref), c_out, c_in, taps, int(backward), _p(wp), _s()))
+    return wp
+
+
+def gather_gemm(fmap: torch.Tensor, x: torch.Tensor, wp: torch.Tensor, c_out: int,
+                out_dtype=torch.float32) -> torch.Tensor:
+    """Y[n] = sum_t X[fmap[n,t]] . Wp_t  on tcgen05 (hc_native_gather_gemm)."""
+    n, taps = fmap.shape
+    y = torch.empty((n, c_out), dtype=out_dtype, device=x.device)
+    dt = _lib.HC_DTYPE_F32 if out_dtype == torch.float32 else _lib.HC_DTYPE_BF16
+    check(lib.hc_native_gather_gemm(_p(fmap), n, taps, _p(x), x.shape[1], _p(wp), c_out, _p(y), dt, _s()))
+    return y
+
+
+class DwWorkspace:
+    def __init__(self):
+        self.buf = None
+
+    def get(self, nbytes: int, device) -> torch.Tensor:
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=device)
+        return self.buf
+
+
+_WS = DwWorkspace()
+
+
+def conv_dw(fmap: torch.Tensor, x: torch.Tensor, dy: torch.Tensor, ws: DwWorkspace = None) -> torch.Tensor:
+    """dW[co][ci*taps + t] = sum_n dY[n,co] X[fmap[n,t],ci]  (reference layout, fp32)."""
+    n, taps = fmap.shape
+    c_in, c_out = x.shape[1], dy.shape[1]
+    nbytes = int(lib.hc_native_dw_workspace(n, taps, c_in, c_out))
+    w = (ws or _WS).get(nbytes, x.device)
+    dw = torch.empty((c_out, c_in * taps), dtype=torch.float32, device=x.device)
+    check(lib.hc_native_conv_dw(_p(fmap), n, taps, _p(x), c_in, _p(dy), c_out, _p(dw), _p(w), w.numel(), _s()))
+    return dw
+
+
+class HashConv:
+    """One hash-conv layer (stride 1, odd F) in the native layout.
+
+    forward(x) -> y          : conv_forward (cnn_ops.cpp:206-215)
+    backward(dy, x) -> dw, dx: conv_backward (cnn_ops.cpp:217-232); dx via the flipped
+                               transposed kernel on the same field map (stride 1)
+    """
+
+    def __init__(self, structure: SuperPsh, weights: torch.Tensor, spec: ConvSpec, out_dtype=torch.bfloat16):
+        spec = ConvSpec(*spec)
+        if spec.stride != 1:
+            raise ValueError("HashConv native layer: stride-1 convolution (use ops.* for strided)")
+        self.s, self.spec, self.out_dtype = structure, spec, out_dtype
+        self.taps = field_size(spec, structure.dim)
+        self.fmap = None
+        self.set_weights(weights)
+
+    def set_weights(self, w: torch.Tensor):
+        sp = self.spec
+        if tuple(w.shape) != (sp.out_channels, sp.in_channels * self.taps):
+            raise ValueError("conv_forward: weight shape mismatch")
+        self.w = w
+        self.wf = pack_weights(w, sp.out_channels, sp.in_channels, self.taps, False)
+        self.wb = pack_weights(w, sp.out_channels, sp.in_channels, self.taps, True)
+
+    def build_map(self) -> torch.Tensor:
+        self.fmap = field_map(self.s, self.s, self.spec)
+        return self.fmap
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        if self.fmap is None:
+            self.build_map()
+        return gather_gemm(self.fmap, x, self.wf, self.spec.out_channels, self.out_dtype)
+
+    def backward(self, dy: torch.Tensor, x: torch.Tensor, dx_dtype=None):
+        dw = conv_dw(self.fmap, x, dy)
+        dx = gather_gemm(self.fmap, dy, self.wb, self.spec.in_channels, dx_dtype or self.out_dtype)
+        return dw, dx
+
+
+def smoke_check(structure: SuperPsh, x: np.ndarray, w: np.ndarray, dy: np.ndarray, y64: np.ndarray) -> None:
+    """Native forward on tensor cores vs the double oracle (bf16-operand tolerance)."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    c_in, c_out = x.shape[0], w.shape[0]
+    layer = HashConv(structure, torch.from_numpy(w).to(dev), ConvSpec(3, 1, 0, c_in, c_out), torch.float32)
+    xv = to_voxel_major(torch.from_numpy(x).to(dev))
+    y = to_channel_major(layer.forward(xv)).cpu().numpy().astype(np.float64)
+    err = np.linalg.norm(y - y64) / np.linalg.norm(y64)
+    # bf16 operands (2^-9 relative each) accumulated in fp32
+    assert err < 2e-2, f"native conv forward rel err {err}"

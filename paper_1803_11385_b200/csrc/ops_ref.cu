@@ -160,6 +160,31 @@ __device__ __forceinline__ int cover_hits_s1(const DevPsh& out, const ModelParam
 // ============================================================== col2hash
 // cnn_ops.cpp:160-204 (Alg. 2): pull per input column; per channel the sum runs
 // over covering outputs in ascending order (deterministic, bit-exact).
+// Stride 1: the covering outputs are the field taps around p_i in the OUTPUT
+// structure, visited in ascending tap order (= ascending p_o) WITHOUT compaction, so
+// at every step all lanes of a warp read the same column-matrix row (fd-1-t) at
+// neighbouring columns: coalesced gathers instead of per-lane scattered rows.
+template <int F>
+__global__ void k_col2hash_s1(DevPsh in, DevPsh out, const float* __restrict__ g, int C, float* __restrict__ res) {
+    const long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (gi >= in.N) return;
+    const int4 c = in.cols[gi];
+    const ModelParam mp = out.models[c.w - 1];
+    constexpr int h = (F - 1) / 2;
+    const int fd = out.dim == 3 ? F * F * F : F * F;
+    int nb[F * F * F];
+    probe_field<F>(out, mp, c.x - h, c.y - h, c.z - h, nb);
+    const long long Nout = out.N, Nin = in.N;
+    for (int ch = 0; ch < C; ++ch) {
+        float acc = 0.0f;
+        const float* base = g + (long long)ch * fd * Nout;
+#pragma unroll
+        for (int t = 0; t < F * F * F; ++t)
+            if (t < fd && nb[t] >= 0) acc = __fadd_rn(acc, __ldg(base + (long long)(fd - 1 - t) * Nout + nb[t]));
+        res[ch * Nin + gi] = acc;
+    }
+}
+
 template <int KMAX, bool STRIDE1, int F>
 __global__ void k_col2hash(DevPsh in, DevPsh out, int Fr, int S, int pad, int fd, const float* __restrict__ g,
                            int C, float* __restrict__ res) {
@@ -421,7 +446,7 @@ void launch_col2hash(const float* gcols, const hc_psh* in, const hc_psh* out, co
     const int fd = (int)field_volume(sp, in->d.dim);
     const int C = sp.in_channels;
     if (sp.stride == 1 && sp.kernel == 3)
-        k_col2hash<27, true, 3><<<g, kThreads, 0, s>>>(in->d, out->d, 3, 1, 0, fd, gcols, C, res);
+        k_col2hash_s1<3><<<g, kThreads, 0, s>>>(in->d, out->d, gcols, C, res);
     else if (sp.stride == 1 && sp.kernel == 1)
         k_col2hash<1, true, 1><<<g, kThreads, 0, s>>>(in->d, out->d, 1, 1, 0, fd, gcols, C, res);
     else if (sp.stride > 1 && cover_per_axis(sp) == 1)

@@ -1,0 +1,143 @@
+"""Native tcgen05 implicit-GEMM conv: forward (gather-GEMM), weight gradient (MN-major
+split-K) and stride-1 input gradient (flipped kernel) against float64 references.
+
+Tolerance contract (SURVEY.md §8c, bf16 path): operands are quantised to bf16
+identically on both sides, the reference accumulates in float64, the GPU in fp32 ->
+||gpu - ref||_F / ||ref||_F <= 1e-5 (fp32 outputs). The bf16 quantisation error
+itself is reported separately against the unquantised fp32 oracle (<= 1e-2)."""
+import numpy as np
+import pytest
+import torch
+
+from helpers import levels_to_arrays, random_pair, shell_pair
+
+pytestmark = pytest.mark.gpu
+
+from paper_1803_11385_b200 import conv as nconv  # noqa: E402
+from paper_1803_11385_b200 import ops  # noqa: E402
+from paper_1803_11385_b200.ops import ConvSpec  # noqa: E402
+from paper_1803_11385_b200.psh import SuperPsh  # noqa: E402
+
+TOL_F32_OUT = 1e-5
+TOL_DW = 5e-5
+
+
+def rel(a, b):
+    a, b = a.double(), b.double()
+    return float((a - b).norm() / b.norm().clamp_min(1e-300))
+
+
+def ref_gather_gemm(fmap, x, w_ref, c_out):
+    """Y[n,co] = sum_t sum_ci X[fmap[n,t],ci] W[co, ci*taps + t]   (float64)"""
+    n, taps = fmap.shape
+    c_in = x.shape[1]
+    xd = torch.cat([x.double(), torch.zeros((1, c_in), dtype=torch.float64, device=x.device)])
+    idx = torch.where(fmap >= 0, fmap.long(), torch.full_like(fmap.long(), x.shape[0]))
+    g = xd[idx]  # n, taps, c_in
+    w = w_ref.double().view(c_out, c_in, taps)  # co, ci, t
+    return torch.einsum("ntc,oct->no", g, w)
+
+
+def ref_dw(fmap, x, dy):
+    n, taps = fmap.shape
+    c_in = x.shape[1]
+    xd = torch.cat([x.double(), torch.zeros((1, c_in), dtype=torch.float64, device=x.device)])
+    idx = torch.where(fmap >= 0, fmap.long(), torch.full_like(fmap.long(), x.shape[0]))
+    g = xd[idx]
+    return torch.einsum("no,ntc->oct", dy.double(), g).reshape(dy.shape[1], c_in * taps)
+
+
+def bf16_round(t):
+    return t.to(torch.bfloat16).float()
+
+
+@pytest.mark.parametrize("c_in,c_out", [(8, 16), (16, 16), (16, 32), (32, 64), (64, 64), (64, 128), (128, 256),
+                                        (24, 48), (8, 256), (256, 16)])
+@pytest.mark.parametrize("n", [1000, 5003])
+def test_gather_gemm_random_maps(cuda, c_in, c_out, n):
+    if c_out not in (16, 32, 64, 128, 256):
+        pytest.skip("c_out outside the tcgen05 tile set")
+    g = torch.Generator(device="cuda").manual_seed(c_in * 1000 + c_out + n)
+    n_in = n + 37
+    x = bf16_round(torch.rand((n_in, c_in), device="cuda", generator=g) * 2 - 1)
+    w = bf16_round(torch.rand((c_out, c_in * 27), device="cuda", generator=g) * 2 - 1)
+    fmap = torch.randint(-1, n_in, (n, 27), device="cuda", generator=g, dtype=torch.int32)
+    fmap[torch.rand((n, 27), device="cuda", generator=g) < 0.4] = -1
+    wp = nconv.pack_weights(w, c_out, c_in, 27, False)
+    y = nconv.gather_gemm(fmap, x.to(torch.bfloat16), wp, c_out, torch.float32)
+    yr = ref_gather_gemm(fmap, x, w, c_out)
+    assert rel(y, yr) <= TOL_F32_OUT
+    yb = nconv.gather_gemm(fmap, x.to(torch.bfloat16), wp, c_out, torch.bfloat16)
+    assert rel(yb.float(), yr) <= 4e-3
+
+
+@pytest.mark.parametrize("c_in,c_out", [(8, 16), (16, 16), (16, 64), (64, 64), (64, 128), (32, 256), (128, 32)])
+def test_dw_random_maps(cuda, c_in, c_out):
+    g = torch.Generator(device="cuda").manual_seed(7 * c_in + c_out)
+    n, n_in = 20011, 19000
+    x = bf16_round(torch.rand((n_in, c_in), device="cuda", generator=g) * 2 - 1)
+    dy = bf16_round(torch.rand((n, c_out), device="cuda", generator=g) * 2 - 1)
+    fmap = torch.randint(-1, n_in, (n, 27), device="cuda", generator=g, dtype=torch.int32)
+    dw = nconv.conv_dw(fmap, x.to(torch.bfloat16), dy.to(torch.bfloat16))
+    assert rel(dw, ref_dw(fmap, x, dy)) <= TOL_DW
+    dw2 = nconv.conv_dw(fmap, x.to(torch.bfloat16), dy.to(torch.bfloat16))
+    assert torch.equal(dw, dw2), "dW must be deterministic"
+
+
+@pytest.mark.parametrize("c_in,c_out", [(16, 16), (32, 64), (64, 64)])
+def test_layer_vs_oracle_on_shell(cuda, restated, c_in, c_out):
+    """Whole layer (forward, dW, dX) on a 64^3 shell batch vs the double oracle
+    (oracle/hc_oracle.c conv_forward / conv_backward) on bf16-quantised operands."""
+    f, _ = shell_pair(64, 2)
+    fa = levels_to_arrays(f)
+    s = SuperPsh.from_levels(f)
+    N = s.total_columns()
+    rng = np.random.default_rng(c_in + c_out)
+    q = lambda a: torch.from_numpy(a).to(torch.bfloat16).float().numpy()  # noqa: E731
+    x = q(rng.uniform(-1, 1, (c_in, N)).astype(np.float32))
+    w = q(rng.uniform(-1, 1, (c_out, c_in * 27)).astype(np.float32))
+    dy = q(rng.uniform(-1, 1, (c_out, N)).astype(np.float32))
+    spec = ConvSpec(3, 1, 0, c_in, c_out)
+    f64 = np.float64
+    cols64 = restated.hash2col(fa, x.astype(f64), fa, spec, f64)
+    y64 = restated.matmul(w.astype(f64), cols64, f64)
+    dw64, dx64 = restated.conv_backward(dy.astype(f64), w.astype(f64), cols64, fa, fa, spec, f64)
+
+    layer = nconv.HashConv(s, torch.from_numpy(w).cuda(), spec, out_dtype=torch.float32)
+    xv = nconv.to_voxel_major(torch.from_numpy(x).cuda())
+    dyv = nconv.to_voxel_major(torch.from_numpy(dy).cuda())
+    y = nconv.to_channel_major(layer.forward(xv))
+    dw, dxv = layer.backward(dyv, xv, torch.float32)
+    dx = nconv.to_channel_major(dxv)
+    t = lambda a: torch.from_numpy(a)  # noqa: E731
+    assert rel(y.cpu(), t(y64)) <= TOL_F32_OUT
+    assert rel(dw.cpu(), t(dw64)) <= TOL_DW
+    assert rel(dx.cpu(), t(dx64)) <= TOL_F32_OUT
+    # fmap used by the layer equals the reference-layout K0 map and the oracle's
+    assert np.array_equal(layer.fmap.cpu().numpy().astype(np.int64), restated.field_map(fa, fa, spec))
+
+
+def test_quantisation_error_reported(cuda, restated):
+    """bf16 quantisation error of the native path vs the unquantised fp32 oracle."""
+    f, _ = random_pair(16, 2, seed=11, n_lo=300, n_hi=800)
+    fa = levels_to_arrays(f)
+    s = SuperPsh.from_levels(f)
+    rng = np.random.default_rng(5)
+    x = rng.uniform(-1, 1, (16, s.total_columns())).astype(np.float32)
+    w = rng.uniform(-1, 1, (32, 16 * 27)).astype(np.float32)
+    spec = ConvSpec(3, 1, 0, 16, 32)
+    y64 = restated.matmul(w.astype(np.float64), restated.hash2col(fa, x.astype(np.float64), fa, spec, np.float64),
+                          np.float64)
+    layer = nconv.HashConv(s, torch.from_numpy(w).cuda(), spec, out_dtype=torch.float32)
+    y = nconv.to_channel_major(layer.forward(nconv.to_voxel_major(torch.from_numpy(x).cuda())))
+    err = rel(y.cpu(), torch.from_numpy(y64))
+    assert err <= 1e-2, err
+
+
+def test_layout_round_trip(cuda):
+    x = torch.rand((37, 1001), device="cuda")
+    v = nconv.to_voxel_major(x)
+    assert v.shape == (1001, 37) and v.dtype == torch.bfloat16
+    back = nconv.to_channel_major(v)
+    assert torch.equal(back, x.to(torch.bfloat16).float())
+    assert torch.equal(nconv.to_channel_major(x.t().contiguous()), x)

@@ -306,16 +306,20 @@ def shell256(cuda):
 
 
 def test_full_size_pool_unpool_idempotence(shell256):
-    """pool(unpool(pool(x))) == pool(x) at BASELINE config 4 size (test_cnn_ops.cpp:402-410)."""
+    """pool(unpool(pool(x))) == pool(x) at BASELINE config 4 size (test_cnn_ops.cpp:402-410).
+    The property needs non-negative inputs (unpool zero-fills the other children), which
+    is what the net feeds max-pool: post-ReLU activations (net.cpp:207-213)."""
     fine, coarse = shell256
     assert fine.total_columns() == 8 * 228296
     sp = ConvSpec(2, 2, 0, 16, 16)
-    x = torch.rand((16, fine.total_columns()), device="cuda") * 2 - 1
+    x = torch.rand((16, fine.total_columns()), device="cuda") + 1e-3
     once = ops.max_pool(fine, x, coarse, sp)
     back = ops.max_unpool(once.output, once.switches, fine, coarse, sp)
     twice = ops.max_pool(fine, back, coarse, sp)
     assert torch.equal(twice.output, once.output)
     assert torch.equal(twice.switches, once.switches)
+    # the restored field holds exactly one non-zero per (channel, coarse voxel)
+    assert int((back != 0).sum()) == int((once.switches >= 0).sum())
 
 
 def test_full_size_delta_kernel_and_adjoint(shell256):
