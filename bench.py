@@ -48,7 +48,7 @@ def parse():
     p.add_argument("--shapes-per-gpu", type=int, default=8)
     p.add_argument("--cin", type=int, default=16)
     p.add_argument("--cout", type=int, default=16)
-    p.add_argument("--path", default="materialized", choices=["materialized", "fused"])
+    p.add_argument("--path", default="fused", choices=["materialized", "fused"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     return p.parse_args()
@@ -213,7 +213,11 @@ class MaterializedStep:
         self.w = torch.rand((cout, cin * 27), device=dev, generator=g) * 2 - 1
         self.dy = torch.rand((cout, N), device=dev, generator=g) * 2 - 1
         self.N, self.cin, self.cout = N, cin, cout
+        self.x_ref, self.dy_ref = self.x, self.dy
         self.op_names = ["hash2col", "fwd_gemm", "dW_gemm", "dcols_gemm", "col2hash"]
+
+    def e2e_run(self, hx, hw, hdy, dev):
+        return self.run(hx.to(dev, non_blocking=True), hw.to(dev, non_blocking=True), hdy.to(dev, non_blocking=True))
 
     def run(self, x, w, dy, marks=None):
         ops, f, sp = self.ops, self.fine, self.spec
@@ -241,6 +245,72 @@ class MaterializedStep:
                 "dcols_gemm": ("flop", fl), "col2hash": ("hbm", gather)}
 
 
+class FusedStep:
+    """Native path (include/hashconv_b200_native.h): field map K0 -> tcgen05 gather-GEMM
+    forward -> split-K tcgen05 dW -> tcgen05 dX (flipped kernel), bf16 operands, fp32
+    accumulation; the column matrix never exists in HBM. Weights are re-packed each step
+    (they change every optimiser step)."""
+
+    name = "fused implicit-GEMM (tcgen05, bf16 operands, fp32 accumulate)"
+    dtype = "bf16"
+
+    def __init__(self, fine, cin, cout, dev):
+        import torch
+        from paper_1803_11385_b200 import conv, ops
+        self.ops, self.conv, self.torch = ops, conv, torch
+        self.fine = fine
+        self.spec = ops.ConvSpec(3, 1, 0, cin, cout)
+        N = fine.total_columns()
+        g = torch.Generator(device=dev).manual_seed(0)
+        # reference-layout (channel-major fp32) host-facing tensors ...
+        self.x_ref = torch.rand((cin, N), device=dev, generator=g) * 2 - 1
+        self.w = torch.rand((cout, cin * 27), device=dev, generator=g) * 2 - 1
+        self.dy_ref = torch.rand((cout, N), device=dev, generator=g) * 2 - 1
+        # ... and the native voxel-major bf16 operands the layer consumes
+        self.x = conv.to_voxel_major(self.x_ref)
+        self.dy = conv.to_voxel_major(self.dy_ref)
+        self.ws = conv.DwWorkspace()
+        self.N, self.cin, self.cout = N, cin, cout
+        self.op_names = ["field_map", "pack_w", "fwd_conv", "dW_conv", "dX_conv"]
+
+    def run(self, x, w, dy, marks=None):
+        ops, conv, f, sp = self.ops, self.conv, self.fine, self.spec
+        mark = (lambda i: marks[i].record()) if marks else (lambda i: None)
+        bf = self.torch.bfloat16
+        mark(0)
+        fmap = conv.field_map_native(f, f, sp, conv.TILED)
+        mark(1)
+        wf = conv.pack_weights(w, sp.out_channels, sp.in_channels, 27, False)
+        wb = conv.pack_weights(w, sp.out_channels, sp.in_channels, 27, True)
+        mark(2)
+        y = conv.gather_gemm(fmap, x, wf, sp.out_channels, bf)
+        mark(3)
+        dw = conv.conv_dw(fmap, x, dy, self.ws)
+        mark(4)
+        dx = conv.gather_gemm(fmap, dy, wb, sp.in_channels, bf)
+        mark(5)
+        return y, dw, dx
+
+    def e2e_run(self, hx, hw, hdy, dev):
+        """Drop-in call with HOST reference-layout buffers: H2D, layout change at the
+        boundary, the fused layer, results back to reference layout, D2H."""
+        t = self.torch
+        conv = self.conv
+        x = conv.to_voxel_major(hx.to(dev, non_blocking=True))
+        w = hw.to(dev, non_blocking=True)
+        dy = conv.to_voxel_major(hdy.to(dev, non_blocking=True))
+        y, dw, dx = self.run(x, w, dy)
+        return conv.to_channel_major(y), dw, conv.to_channel_major(dx)
+
+    def op_model(self, M, R):
+        N, ci, co = self.N, self.cin, self.cout
+        fl = 2.0 * co * 27 * ci * N
+        kmap = 27 * N * 4 + 10 * M + 3 * R + 16 * N
+        return {"field_map": ("hbm", kmap), "pack_w": ("hbm", 2 * co * ci * 27 * 6),
+                "fwd_conv": ("flop", fl, (ci + co) * N * 2), "dW_conv": ("flop", fl, (ci + co) * N * 2),
+                "dX_conv": ("flop", fl, (ci + co) * N * 2)}
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -262,7 +332,7 @@ def main():
 
     lv = shell_levels(args.res)
     fine = SuperPsh.from_levels([lv[0]] * args.shapes_per_gpu)
-    step = MaterializedStep(fine, args.cin, args.cout, dev)
+    step = (FusedStep if args.path == "fused" else MaterializedStep)(fine, args.cin, args.cout, dev)
     N = fine.total_columns()
 
     def barrier():
@@ -307,17 +377,14 @@ def main():
     # ---- e2e through the public API with host buffers (H2D inputs, D2H results)
     e2e = None
     if not args.no_e2e:
-        hx = step.x.cpu().pin_memory()
+        hx = step.x_ref.cpu().pin_memory()
         hw = step.w.cpu().pin_memory()
-        hdy = step.dy.cpu().pin_memory()
+        hdy = step.dy_ref.cpu().pin_memory()
         outs = [torch.empty((args.cout, N), pin_memory=True), torch.empty((args.cout, args.cin * 27),
                 pin_memory=True), torch.empty((args.cin, N), pin_memory=True)]
 
         def e2e_step():
-            x = hx.to(dev, non_blocking=True)
-            w = hw.to(dev, non_blocking=True)
-            dy = hdy.to(dev, non_blocking=True)
-            y, dw, dx = step.run(x, w, dy)
+            y, dw, dx = step.e2e_run(hx, hw, hdy, dev)
             if world > 1:
                 dist.all_reduce(dw)
             for o, r in zip(outs, (y, dw, dx)):
@@ -354,14 +421,18 @@ def main():
     kernels = {}
     for i, name in enumerate(step.op_names):
         avg_ms = per_op[i] / args.steps
-        kind, amount = model[name]
+        kind, amount = model[name][:2]
         if kind == "hbm":
             ach = amount / (avg_ms / 1e3) / 1e9
             kernels[name] = {"ms": avg_ms, "bound": "hbm", "achieved_GBps": ach,
                              "frac": ach / pk["hbm_gbs"], "algorithmic_bytes": amount}
         else:
             ach = amount / (avg_ms / 1e3) / 1e12
-            kernels[name] = {"ms": avg_ms, "achieved_TFLOPs": ach, "flops": amount}
+            kernels[name] = {"ms": avg_ms, "achieved_TFLOPs": ach, "flops": amount,
+                             "frac_tensor": ach / pk["bf16_tflops_sustained"]}
+            if len(model[name]) > 2:
+                kernels[name]["algorithmic_bytes"] = model[name][2]
+                kernels[name]["arith_intensity"] = amount / model[name][2]
     dom = max(step.op_names, key=lambda n: per_op[step.op_names.index(n)])
     dk = kernels[dom]
     traffic = None

@@ -142,6 +142,14 @@ hc_status hc_locate(const hc_psh* p, const int32_t* queries, int64_t n, int64_t*
  * every output voxel). This is the paper's pre-stored neighbour map. */
 hc_status hc_field_map(const hc_psh* in, const hc_psh* out, hc_conv_spec spec, int32_t* map,
                        hc_stream stream);
+/* Same map, tap-major: map[row * N_out + col] (coalesced stores; the native conv layout). */
+hc_status hc_field_map_tap_major(const hc_psh* in, const hc_psh* out, hc_conv_spec spec,
+                                 int32_t* map, hc_stream stream);
+/* Same map, tile-major: 128-column tiles, map[((col/128)*F^dim + row)*128 + col%128], padded
+ * to a multiple of 128 columns with -1 (one contiguous block per tile; the native conv's
+ * preferred layout, fetched with one bulk copy per tile). */
+hc_status hc_field_map_tiled(const hc_psh* in, const hc_psh* out, hc_conv_spec spec, int32_t* map,
+                             hc_stream stream);
 
 /* =========================================================== reference-layout operators
  * fp32, device pointers, shapes passed explicitly so shape errors carry the

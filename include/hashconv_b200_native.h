@@ -6,7 +6,8 @@
  * shared memory, so the (C*F^3) x N column matrix never exists in HBM.
  *
  * Layouts: features are voxel-major bf16 [N][C] (C a multiple of 8); the field map
- * is int32 [N_out][taps] (-1 = empty cell); weights are packed once per update from
+ * is int32 [N_out][taps] (fmap_layout 0, hc_field_map), [taps][N_out] (layout 1,
+ * hc_field_map_tap_major) or tile-major (layout 2, hc_field_map_tiled), -1 = empty cell; weights are packed once per update from
  * the reference layout W[co][ci*taps + t] (cnn_ops.hpp:21-27) by
  * hc_native_pack_weights. Device pointers, stream-ordered, deterministic.
  */
@@ -36,15 +37,16 @@ hc_status hc_native_pack_weights(const float* w_ref, int32_t c_out, int32_t c_in
 /* Y[n][0:c_out] = sum_{t,ci} X[fmap[n][t]][ci] * Wp[co][t*c_in + ci]  (gather-GEMM, tcgen05).
  * Forward conv: (fmap of (in,out), X, forward pack). Stride-1 input gradient:
  * (fmap of the structure, dY, backward pack) gives dX. c_out in {16,32,64,128,256}. */
-hc_status hc_native_gather_gemm(const int32_t* fmap, int64_t n_out, int32_t taps, const void* x,
-                                int32_t c_in, const void* w_packed, int32_t c_out, void* y,
+hc_status hc_native_gather_gemm(const int32_t* fmap, int32_t fmap_layout, int64_t n_out,
+                                int32_t taps, const void* x, int32_t c_in, const void* w_packed, int32_t c_out, void* y,
                                 hc_dtype y_dtype, hc_stream stream);
 
 /* dW in the reference layout (C_out x C_in*taps, fp32):
  * dW[co][ci*taps + t] = sum_n dY[n][co] * X[fmap[n][t]][ci]  (cnn_ops.cpp:228 matmul_trans_b).
  * Split-K over voxels on tcgen05, partials reduced in a fixed order (deterministic). */
 size_t hc_native_dw_workspace(int64_t n_out, int32_t taps, int32_t c_in, int32_t c_out);
-hc_status hc_native_conv_dw(const int32_t* fmap, int64_t n_out, int32_t taps, const void* x,
+hc_status hc_native_conv_dw(const int32_t* fmap, int32_t fmap_layout, int64_t n_out,
+                            int32_t taps, const void* x,
                             int32_t c_in, const void* dy, int32_t c_out, float* dw_ref,
                             void* workspace, size_t ws_bytes, hc_stream stream);
 

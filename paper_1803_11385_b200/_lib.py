@@ -75,6 +75,8 @@ _SIGS = {
     "hc_psh_free": [_P],
     "hc_locate": [_P, _P, _I64, _P, _P],
     "hc_field_map": [_P, _P, _SPEC, _P, _P],
+    "hc_field_map_tap_major": [_P, _P, _SPEC, _P, _P],
+    "hc_field_map_tiled": [_P, _P, _SPEC, _P, _P],
     "hc_hash2col_f32": [_P, _P, _I64, _I64, _P, _SPEC, _P, _P],
     "hc_col2hash_f32": [_P, _I64, _I64, _P, _P, _SPEC, _P, _P],
     "hc_conv_forward_f32": [_P, _P, _I64, _I64, _P, _P, _I64, _I64, _SPEC, _P, _P],
@@ -91,8 +93,8 @@ _SIGS = {
 }
 _SIGS.update({
     "hc_native_pack_weights": [_P, _I32, _I32, _I32, _I32, _P, _P],
-    "hc_native_gather_gemm": [_P, _I64, _I32, _P, _I32, _P, _I32, _P, C.c_int, _P],
-    "hc_native_conv_dw": [_P, _I64, _I32, _P, _I32, _P, _I32, _P, _P, C.c_size_t, _P],
+    "hc_native_gather_gemm": [_P, _I32, _I64, _I32, _P, _I32, _P, _I32, _P, C.c_int, _P],
+    "hc_native_conv_dw": [_P, _I32, _I64, _I32, _P, _I32, _P, _I32, _P, _P, C.c_size_t, _P],
     "hc_native_to_voxel_major": [_P, _I64, _I64, _P, _P],
     "hc_native_to_channel_major": [_P, C.c_int, _I64, _I64, _P, _P],
 })

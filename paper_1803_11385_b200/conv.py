@@ -9,6 +9,7 @@ reference layout W[co][ci*F^3 + t] (cnn_ops.hpp:21-27).
 from __future__ import annotations
 
 import ctypes as C
+from typing import NamedTuple
 
 import numpy as np
 import torch
@@ -55,13 +56,45 @@ def pack_weights(w_ref: torch.Tensor, c_out: int, c_in: int, taps: int, backward
     return wp
 
 
-def gather_gemm(fmap: torch.Tensor, x: torch.Tensor, wp: torch.Tensor, c_out: int,
-                out_dtype=torch.float32) -> torch.Tensor:
-    """Y[n] = sum_t X[fmap[n,t]] . Wp_t  on tcgen05 (hc_native_gather_gemm)."""
-    n, taps = fmap.shape
-    y = torch.empty((n, c_out), dtype=out_dtype, device=x.device)
+class FieldMap(NamedTuple):
+    """K0 field map on the device: `data` int32 in one of three layouts (0 row-major
+    [n][taps], 1 tap-major [taps][n], 2 tile-major [ceil(n/128)][taps][128])."""
+
+    data: torch.Tensor
+    n: int
+    taps: int
+    layout: int
+
+
+ROW_MAJOR, TAP_MAJOR, TILED = 0, 1, 2
+
+
+def as_field_map(fmap) -> FieldMap:
+    if isinstance(fmap, FieldMap):
+        return fmap
+    return FieldMap(fmap, fmap.shape[0], fmap.shape[1], ROW_MAJOR)
+
+
+def field_map_native(inp: SuperPsh, out: SuperPsh, spec: ConvSpec, layout: int = TILED) -> FieldMap:
+    """K0 for the native conv (tile-major by default: one contiguous block per 128-voxel tile)."""
+    spec = ConvSpec(*spec)
+    taps = field_size(spec, inp.dim)
+    n = out.total_columns()
+    if layout == TILED:
+        m = torch.empty(((n + 127) // 128, taps, 128), dtype=torch.int32, device="cuda")
+        check(lib.hc_field_map_tiled(inp._h, out._h, spec.c(), _p(m), _s()))
+        return FieldMap(m, n, taps, TILED)
+    m = field_map(inp, out, spec, tap_major=layout == TAP_MAJOR)
+    return FieldMap(m, n, taps, layout)
+
+
+def gather_gemm(fmap, x: torch.Tensor, wp: torch.Tensor, c_out: int, out_dtype=torch.float32) -> torch.Tensor:
+    """Y[n] = sum_t X[fmap(n,t)] . Wp_t  on tcgen05 (hc_native_gather_gemm)."""
+    fm = as_field_map(fmap)
+    y = torch.empty((fm.n, c_out), dtype=out_dtype, device=x.device)
     dt = _lib.HC_DTYPE_F32 if out_dtype == torch.float32 else _lib.HC_DTYPE_BF16
-    check(lib.hc_native_gather_gemm(_p(fmap), n, taps, _p(x), x.shape[1], _p(wp), c_out, _p(y), dt, _s()))
+    check(lib.hc_native_gather_gemm(_p(fm.data), fm.layout, fm.n, fm.taps, _p(x), x.shape[1], _p(wp), c_out, _p(y),
+                                    dt, _s()))
     return y
 
 
@@ -78,14 +111,15 @@ class DwWorkspace:
 _WS = DwWorkspace()
 
 
-def conv_dw(fmap: torch.Tensor, x: torch.Tensor, dy: torch.Tensor, ws: DwWorkspace = None) -> torch.Tensor:
-    """dW[co][ci*taps + t] = sum_n dY[n,co] X[fmap[n,t],ci]  (reference layout, fp32)."""
-    n, taps = fmap.shape
+def conv_dw(fmap, x: torch.Tensor, dy: torch.Tensor, ws: DwWorkspace = None) -> torch.Tensor:
+    """dW[co][ci*taps + t] = sum_n dY[n,co] X[fmap(n,t),ci]  (reference layout, fp32)."""
+    fm = as_field_map(fmap)
     c_in, c_out = x.shape[1], dy.shape[1]
-    nbytes = int(lib.hc_native_dw_workspace(n, taps, c_in, c_out))
+    nbytes = int(lib.hc_native_dw_workspace(fm.n, fm.taps, c_in, c_out))
     w = (ws or _WS).get(nbytes, x.device)
-    dw = torch.empty((c_out, c_in * taps), dtype=torch.float32, device=x.device)
-    check(lib.hc_native_conv_dw(_p(fmap), n, taps, _p(x), c_in, _p(dy), c_out, _p(dw), _p(w), w.numel(), _s()))
+    dw = torch.empty((c_out, c_in * fm.taps), dtype=torch.float32, device=x.device)
+    check(lib.hc_native_conv_dw(_p(fm.data), fm.layout, fm.n, fm.taps, _p(x), c_in, _p(dy), c_out, _p(dw), _p(w),
+                                w.numel(), _s()))
     return dw
 
 
@@ -114,8 +148,9 @@ class HashConv:
         self.wf = pack_weights(w, sp.out_channels, sp.in_channels, self.taps, False)
         self.wb = pack_weights(w, sp.out_channels, sp.in_channels, self.taps, True)
 
-    def build_map(self) -> torch.Tensor:
-        self.fmap = field_map(self.s, self.s, self.spec)
+    def build_map(self) -> FieldMap:
+        """K0 in the tile-major layout (coalesced build; one bulk copy per tile in the GEMM)."""
+        self.fmap = field_map_native(self.s, self.s, self.spec, TILED)
         return self.fmap
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:

@@ -59,6 +59,73 @@ __global__ void k_field_map(DevPsh in, DevPsh out, int S, int pad, int* map) {
         if (t < fd) dst[t] = nb[t];
 }
 
+// Tap-major K0 ([F^3][N_out]): lanes of a warp write consecutive columns of each
+// tap row, so every store instruction is fully coalesced (the native conv layout).
+template <int F>
+__global__ void k_field_map_t(DevPsh in, DevPsh out, int S, int pad, int* map) {
+    const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (col >= out.N) return;
+    const int4 c = out.cols[col];
+    const ModelParam mp = in.models[c.w - 1];
+    const int fd = in.dim == 3 ? F * F * F : F * F;
+    int nb[F * F * F];
+    probe_field<F>(in, mp, origin_axis(c.x, F, S, pad), origin_axis(c.y, F, S, pad),
+                   origin_axis(c.z, F, S, pad), nb);
+    const long long N = out.N;
+#pragma unroll
+    for (int t = 0; t < F * F * F; ++t)
+        if (t < fd) map[t * N + col] = nb[t];
+}
+
+// Tile-major K0 ([ceil(N/128)][F^3][128]): one 128-column tile's whole map is a
+// contiguous block (fetched by one bulk copy in the native conv); padded columns
+// beyond N are -1.
+template <int F>
+__global__ void k_field_map_tiled(DevPsh in, DevPsh out, int S, int pad, int* map) {
+    const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long padded = (out.N + 127) / 128 * 128;
+    if (col >= padded) return;
+    const int fd = in.dim == 3 ? F * F * F : F * F;
+    int nb[F * F * F];
+    if (col < out.N) {
+        const int4 c = out.cols[col];
+        const ModelParam mp = in.models[c.w - 1];
+        probe_field<F>(in, mp, origin_axis(c.x, F, S, pad), origin_axis(c.y, F, S, pad),
+                       origin_axis(c.z, F, S, pad), nb);
+    } else {
+#pragma unroll
+        for (int t = 0; t < F * F * F; ++t) nb[t] = -1;
+    }
+    int* dst = map + (col >> 7) * fd * 128 + (col & 127);
+#pragma unroll
+    for (int t = 0; t < F * F * F; ++t)
+        if (t < fd) dst[t * 128] = nb[t];
+}
+
+__global__ void k_field_map_any_tiled(DevPsh in, DevPsh out, int F, int S, int pad, int fd, int* map) {
+    const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long padded = (out.N + 127) / 128 * 128;
+    if (col >= padded) return;
+    int* dst = map + (col >> 7) * fd * 128 + (col & 127);
+    if (col >= out.N) {
+        for (int t = 0; t < fd; ++t) dst[t * 128] = -1;
+        return;
+    }
+    const int4 c = out.cols[col];
+    const ModelParam mp = in.models[c.w - 1];
+    const int bx = origin_axis(c.x, F, S, pad), by = origin_axis(c.y, F, S, pad), bz = origin_axis(c.z, F, S, pad);
+    for (int t = 0; t < fd; ++t) dst[t * 128] = probe_tap(in, mp, bx, by, bz, F, t);
+}
+
+__global__ void k_field_map_any_t(DevPsh in, DevPsh out, int F, int S, int pad, int fd, int* map) {
+    const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (col >= out.N) return;
+    const int4 c = out.cols[col];
+    const ModelParam mp = in.models[c.w - 1];
+    const int bx = origin_axis(c.x, F, S, pad), by = origin_axis(c.y, F, S, pad), bz = origin_axis(c.z, F, S, pad);
+    for (int t = 0; t < fd; ++t) map[t * out.N + col] = probe_tap(in, mp, bx, by, bz, F, t);
+}
+
 __global__ void k_field_map_any(DevPsh in, DevPsh out, int F, int S, int pad, int fd, int* map) {
     const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (col >= out.N) return;
@@ -412,11 +479,24 @@ int cover_per_axis(const hc_conv_spec& sp) {
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
-void launch_field_map(const hc_psh* in, const hc_psh* out, const hc_conv_spec& sp, int* map, cudaStream_t s) {
+void launch_field_map(const hc_psh* in, const hc_psh* out, const hc_conv_spec& sp, int* map, cudaStream_t s,
+                      int layout = 0 /* 0 row-major, 1 tap-major, 2 tile-major */) {
     const long long n = out->d.N;
     if (n == 0) return;
     const unsigned g = grid_for(n, kThreads);
-    if (sp.kernel == 3) k_field_map<3><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, map);
+    const bool tap_major = layout == 1;
+    if (layout == 2) {
+        const unsigned gp = grid_for((n + 127) / 128 * 128, kThreads);
+        if (sp.kernel == 3) k_field_map_tiled<3><<<gp, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, map);
+        else if (sp.kernel == 2) k_field_map_tiled<2><<<gp, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, map);
+        else k_field_map_any_tiled<<<gp, kThreads, 0, s>>>(in->d, out->d, sp.kernel, sp.stride, sp.pad,
+                                                         (int)field_volume(sp, in->d.dim), map);
+    } else if (tap_major) {
+        if (sp.kernel == 3) k_field_map_t<3><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, map);
+        else if (sp.kernel == 2) k_field_map_t<2><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, map);
+        else k_field_map_any_t<<<g, kThreads, 0, s>>>(in->d, out->d, sp.kernel, sp.stride, sp.pad,
+                                                     (int)field_volume(sp, in->d.dim), map);
+    } else if (sp.kernel == 3) k_field_map<3><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, map);
     else if (sp.kernel == 2) k_field_map<2><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, map);
     else k_field_map_any<<<g, kThreads, 0, s>>>(in->d, out->d, sp.kernel, sp.stride, sp.pad,
                                               (int)field_volume(sp, in->d.dim), map);
@@ -544,6 +624,22 @@ hc_status hc_field_map(const hc_psh* in, const hc_psh* out, hc_conv_spec spec, i
     return guard([&] {
         check_pair(in, out, spec);
         launch_field_map(in, out, spec, map, as_stream(stream));
+    });
+}
+
+hc_status hc_field_map_tap_major(const hc_psh* in, const hc_psh* out, hc_conv_spec spec, int32_t* map,
+                                 hc_stream stream) {
+    return guard([&] {
+        check_pair(in, out, spec);
+        launch_field_map(in, out, spec, map, as_stream(stream), 1);
+    });
+}
+
+hc_status hc_field_map_tiled(const hc_psh* in, const hc_psh* out, hc_conv_spec spec, int32_t* map,
+                             hc_stream stream) {
+    return guard([&] {
+        check_pair(in, out, spec);
+        launch_field_map(in, out, spec, map, as_stream(stream), 2);
     });
 }
 

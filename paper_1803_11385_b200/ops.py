@@ -125,11 +125,17 @@ def math_mode(mode: str):
 
 
 # ------------------------------------------------------------------ operators
-def field_map(input: SuperPsh, output: SuperPsh, spec: ConvSpec) -> torch.Tensor:
-    """K0: int32 N_out x F^dim, input column or -1 (cnn_ops.cpp:100-119 for every output)."""
+def field_map(input: SuperPsh, output: SuperPsh, spec: ConvSpec, tap_major: bool = False) -> torch.Tensor:
+    """K0: int32 N_out x F^dim (or F^dim x N_out when tap_major), input column or -1
+    (cnn_ops.cpp:100-119 collect_field_hits for every output voxel)."""
     spec = ConvSpec(*spec)
-    m = _empty(output.total_columns(), field_size(spec, input.dim), torch.int32)
-    check(lib.hc_field_map(input._h, output._h, spec.c(), _p(m), _stream()))
+    fd = field_size(spec, input.dim)
+    if tap_major:
+        m = _empty(fd, output.total_columns(), torch.int32)
+        check(lib.hc_field_map_tap_major(input._h, output._h, spec.c(), _p(m), _stream()))
+    else:
+        m = _empty(output.total_columns(), fd, torch.int32)
+        check(lib.hc_field_map(input._h, output._h, spec.c(), _p(m), _stream()))
     return m
 
 

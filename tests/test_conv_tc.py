@@ -47,6 +47,16 @@ def ref_dw(fmap, x, dy):
     return torch.einsum("no,ntc->oct", dy.double(), g).reshape(dy.shape[1], c_in * taps)
 
 
+def layouts(fmap):
+    """The same row-major map in the tap-major and tile-major layouts."""
+    n, taps = fmap.shape
+    pad = (n + 127) // 128 * 128
+    tiled = torch.full((pad, taps), -1, dtype=torch.int32, device=fmap.device)
+    tiled[:n] = fmap
+    return [nconv.FieldMap(fmap.t().contiguous(), n, taps, nconv.TAP_MAJOR),
+            nconv.FieldMap(tiled.view(pad // 128, 128, taps).permute(0, 2, 1).contiguous(), n, taps, nconv.TILED)]
+
+
 def bf16_round(t):
     return t.to(torch.bfloat16).float()
 
@@ -69,6 +79,8 @@ def test_gather_gemm_random_maps(cuda, c_in, c_out, n):
     assert rel(y, yr) <= TOL_F32_OUT
     yb = nconv.gather_gemm(fmap, x.to(torch.bfloat16), wp, c_out, torch.bfloat16)
     assert rel(yb.float(), yr) <= 4e-3
+    for fm in layouts(fmap):
+        assert torch.equal(nconv.gather_gemm(fm, x.to(torch.bfloat16), wp, c_out, torch.float32), y), fm.layout
 
 
 @pytest.mark.parametrize("c_in,c_out", [(8, 16), (16, 16), (16, 64), (64, 64), (64, 128), (32, 256), (128, 32)])
@@ -82,6 +94,8 @@ def test_dw_random_maps(cuda, c_in, c_out):
     assert rel(dw, ref_dw(fmap, x, dy)) <= TOL_DW
     dw2 = nconv.conv_dw(fmap, x.to(torch.bfloat16), dy.to(torch.bfloat16))
     assert torch.equal(dw, dw2), "dW must be deterministic"
+    for fm in layouts(fmap):
+        assert torch.equal(nconv.conv_dw(fm, x.to(torch.bfloat16), dy.to(torch.bfloat16)), dw), fm.layout
 
 
 @pytest.mark.parametrize("c_in,c_out", [(16, 16), (32, 64), (64, 64)])
@@ -114,7 +128,12 @@ def test_layer_vs_oracle_on_shell(cuda, restated, c_in, c_out):
     assert rel(dw.cpu(), t(dw64)) <= TOL_DW
     assert rel(dx.cpu(), t(dx64)) <= TOL_F32_OUT
     # fmap used by the layer equals the reference-layout K0 map and the oracle's
-    assert np.array_equal(layer.fmap.cpu().numpy().astype(np.int64), restated.field_map(fa, fa, spec))
+    want = restated.field_map(fa, fa, spec)
+    tiled = layer.fmap.data.permute(0, 2, 1).reshape(-1, 27)[:N].cpu().numpy().astype(np.int64)
+    assert np.array_equal(tiled, want)
+    assert (layer.fmap.data.permute(0, 2, 1).reshape(-1, 27)[N:] == -1).all()
+    tap = nconv.field_map_native(s, s, spec, nconv.TAP_MAJOR)
+    assert np.array_equal(tap.data.t().cpu().numpy().astype(np.int64), want)
 
 
 def test_quantisation_error_reported(cuda, restated):
