@@ -46,8 +46,8 @@ def parse():
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--res", type=int, default=256)
     p.add_argument("--shapes-per-gpu", type=int, default=8)
-    p.add_argument("--cin", type=int, default=16)
-    p.add_argument("--cout", type=int, default=16)
+    p.add_argument("--cin", type=int, default=64)
+    p.add_argument("--cout", type=int, default=64)
     p.add_argument("--path", default="fused", choices=["materialized", "fused"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
@@ -93,7 +93,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
