@@ -330,8 +330,10 @@ def main():
     from paper_1803_11385_b200 import _lib
     from paper_1803_11385_b200.psh import SuperPsh
 
+    from paper_1803_11385_b200.dist import allreduce_gradients, local_levels
     lv = shell_levels(args.res)
-    fine = SuperPsh.from_levels([lv[0]] * args.shapes_per_gpu)
+    # global batch of shapes_per_gpu * world shells; this rank owns a contiguous block
+    fine = SuperPsh.from_levels(local_levels([lv[0]] * (args.shapes_per_gpu * world), world, rank))
     step = (FusedStep if args.path == "fused" else MaterializedStep)(fine, args.cin, args.cout, dev)
     N = fine.total_columns()
 
@@ -342,27 +344,26 @@ def main():
 
     def one(marks=None):
         y, dw, dx = step.run(step.x, step.w, step.dy, marks)
-        if world > 1:
-            dist.all_reduce(dw)
+        allreduce_gradients([dw])
         return dx
 
-    for _ in range(max(args.warmup, 3)):
-        one()
-    barrier()
-
+    args.warmup = max(args.warmup, 3)
     nops = len(step.op_names)
     per_op = [0.0] * nops
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     marks_all = [[torch.cuda.Event(enable_timing=True) for _ in range(nops + 1)] for _ in range(args.steps)]
-    launches0 = _lib.lib.hc_launch_count()
-    with ClockSampler(local) as clk:
+    with ClockSampler(local) as clk:  # sampling spans warm-up and the timed region
+        for _ in range(args.warmup):
+            one()
+        barrier()
+        launches0 = _lib.lib.hc_launch_count()
         barrier()
         start.record()
         for k in range(args.steps):
             one(marks_all[k])
         end.record()
         barrier()
-    launches = _lib.lib.hc_launch_count() - launches0
+        launches = _lib.lib.hc_launch_count() - launches0
     elapsed_ms = start.elapsed_time(end)
     for m in marks_all:
         for i in range(nops):
@@ -385,8 +386,7 @@ def main():
 
         def e2e_step():
             y, dw, dx = step.e2e_run(hx, hw, hdy, dev)
-            if world > 1:
-                dist.all_reduce(dw)
+            allreduce_gradients([dw])
             for o, r in zip(outs, (y, dw, dx)):
                 o.copy_(r, non_blocking=True)
 
