@@ -57,6 +57,14 @@ int64_t hc_launch_count(void);
 hc_status hc_set_math(hc_math mode);
 hc_math hc_get_math(void);
 
+/* Device-memory plumbing for hosts that do not link CUDA themselves (the header-only
+ * C++ drop-in shim include/hashconv_b200.hpp uses only these). */
+hc_status hc_malloc(void** ptr, size_t bytes);
+hc_status hc_free(void* ptr);
+hc_status hc_memcpy_h2d(void* dst, const void* src, size_t bytes, hc_stream stream);
+hc_status hc_memcpy_d2h(void* dst, const void* src, size_t bytes, hc_stream stream);
+hc_status hc_stream_synchronize(hc_stream stream);
+
 /* cnn_ops.hpp:11-17 ConvSpec */
 typedef struct {
     int32_t kernel, stride, pad, in_channels, out_channels;

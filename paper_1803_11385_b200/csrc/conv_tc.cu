@@ -59,6 +59,17 @@ __device__ __forceinline__ int fm_ld(const FMap& f, long long n, int t) {
     return __ldg(f.p + n * f.sn + (long long)t * f.st);
 }
 
+// Producers signal stage completion with cp.async.mbarrier.arrive.noinc (non-blocking)
+// instead of wait_group + arrive. HCB_ASYNC_ARRIVE=0 selects the blocking form (A/B).
+int async_arrive() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("HCB_ASYNC_ARRIVE");
+        v = e ? (std::atoi(e) != 0) : 1;
+    }
+    return v;
+}
+
 int num_sms() {
     static int n = 0;
     if (!n) {
@@ -109,7 +120,7 @@ struct FwdCfg {
 template <int BN, int CPS, bool TILED, typename OutT>
 __global__ void __launch_bounds__(FwdCfg<BN, CPS, TILED>::THREADS, CPS)
     k_gather_gemm(FMap fm, long long rows, const bf16* __restrict__ X, int C, int K, const bf16* __restrict__ Wp,
-                  int Kp, OutT* __restrict__ Y, int tiles) {
+                  int Kp, OutT* __restrict__ Y, int tiles, int async_arrive) {
     using Cfg = FwdCfg<BN, CPS, TILED>;
     constexpr int S = Cfg::STAGES;
     constexpr int LAG = Cfg::LAG;
@@ -187,20 +198,26 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, TILED>::THREADS, CPS)
                     const int r = r0 + 16 * j;
                     cp_async16(smem_u32(B + sw128_offset(r, c)), Wp + (long long)r * Kp + kb * BK + c * 8, 16u);
                 }
-                cp_async_commit();
-                if (it >= LAG) {
-                    cp_async_wait<LAG>();
-                    fence_proxy_async();
-                    mbar_arrive(full0 + 8 * (int)((it - LAG) % S));
+                if (async_arrive) {
+                    cp_async_arrive_noinc(full0 + 8 * s);  // non-blocking: barrier completes on landing
+                } else {
+                    cp_async_commit();
+                    if (it >= LAG) {
+                        cp_async_wait<LAG>();
+                        fence_proxy_async();
+                        mbar_arrive(full0 + 8 * (int)((it - LAG) % S));
+                    }
                 }
             }
             // every producer is past this tile's map: refill the slot with tile i+2
             named_sync(1, kProducers);
             if (tid == 0 && tile + 2 * (int)gridDim.x < tiles) request(tile + 2 * gridDim.x, buf);
         }
-        cp_async_wait<0>();
-        fence_proxy_async();
-        for (long long q = std::max<long long>(0, it - LAG); q < it; ++q) mbar_arrive(full0 + 8 * (int)(q % S));
+        if (!async_arrive) {
+            cp_async_wait<0>();
+            fence_proxy_async();
+            for (long long q = std::max<long long>(0, it - LAG); q < it; ++q) mbar_arrive(full0 + 8 * (int)(q % S));
+        }
     } else if (!TILED && warp < 4) {
         // ---------------- producers
         const int c = tid & 7;    // 16-byte chunk within a 128-byte row
@@ -312,6 +329,7 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, TILED>::THREADS, CPS)
             for (int kb = 0; kb < nkb; ++kb, ++it) {
                 const int s = (int)(it % S);
                 mbar_wait(full0 + 8 * s, (uint32_t)((it / S) & 1));
+                if (async_arrive) fence_proxy_async();
                 tc_fence_after();
                 const uint32_t a = smem_u32(smem + s * Cfg::STAGE_BYTES);
                 const uint32_t b = a + Cfg::A_BYTES;
@@ -352,7 +370,7 @@ struct DwCfg {
 template <int NB>
 __global__ void __launch_bounds__(DwCfg<NB>::THREADS)
     k_gather_dw(FMap fm, long long rows, const bf16* __restrict__ X, int C, int K, const bf16* __restrict__ dY,
-                int Cout, int kb_per_split, float* __restrict__ partial, int Mtot) {
+                int Cout, int kb_per_split, float* __restrict__ partial, int Mtot, int async_arrive) {
     using Cfg = DwCfg<NB>;
     constexpr int S = Cfg::STAGES;
     constexpr int LAG = Cfg::LAG;
@@ -428,11 +446,15 @@ __global__ void __launch_bounds__(DwCfg<NB>::THREADS)
                 const bf16* src = ok ? dY + n * Cout + co : dY;
                 cp_async16(smem_u32(B + blk * (KB * 128) + sw128_offset(r, c)), src, ok ? 16u : 0u);
             }
-            cp_async_commit();
-            if (kb >= LAG) {
-                cp_async_wait<LAG>();
-                fence_proxy_async();
-                mbar_arrive(full0 + 8 * ((kb - LAG) % S));
+            if (async_arrive) {
+                cp_async_arrive_noinc(full0 + 8 * s);
+            } else {
+                cp_async_commit();
+                if (kb >= LAG) {
+                    cp_async_wait<LAG>();
+                    fence_proxy_async();
+                    mbar_arrive(full0 + 8 * ((kb - LAG) % S));
+                }
             }
         };
         // field-map entries two stages ahead; buffers rotate by unrolling (no copies)
@@ -452,9 +474,11 @@ __global__ void __launch_bounds__(DwCfg<NB>::THREADS)
             issue(kb++, cur);
         }
         if (kb < nkb) issue(kb++, nx1);
-        cp_async_wait<0>();
-        fence_proxy_async();
-        for (int kb = std::max(0, nkb - LAG); kb < nkb; ++kb) mbar_arrive(full0 + 8 * (kb % S));
+        if (!async_arrive) {
+            cp_async_wait<0>();
+            fence_proxy_async();
+            for (int q = std::max(0, nkb - LAG); q < nkb; ++q) mbar_arrive(full0 + 8 * (q % S));
+        }
 
         // epilogue: row m = (t,ci) index, columns co
         const int row = warp * 32 + (int)lane_id();
@@ -482,6 +506,7 @@ __global__ void __launch_bounds__(DwCfg<NB>::THREADS)
         for (int kb = 0; kb < nkb; ++kb) {
             const int s = kb % S;
             mbar_wait(full0 + 8 * s, (kb / S) & 1);
+            if (async_arrive) fence_proxy_async();
             tc_fence_after();
             const uint32_t a = smem_u32(smem + s * Cfg::STAGE_BYTES);
             const uint32_t b = a + Cfg::A_BYTES;
@@ -593,7 +618,7 @@ void launch_gg_cps(const FMap& fm, long long rows, const bf16* X, int C, int K, 
     }
     const int tiles = (int)((rows + BM - 1) / BM);
     const int grid = std::min(tiles, CPS * num_sms());
-    kern<<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(fm, rows, X, C, K, Wp, Kp, Y, tiles);
+    kern<<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(fm, rows, X, C, K, Wp, Kp, Y, tiles, TILED ? async_arrive() : 0);
     launched("conv gather-GEMM (tcgen05)");
 }
 
@@ -682,7 +707,7 @@ void launch_dw(const DwPlan& p, const FMap& fm, long long rows, const bf16* X, i
         attr = true;
     }
     dim3 g((unsigned)p.mt, (unsigned)p.splits);
-    kern<<<g, Cfg::THREADS, Cfg::SMEM, s>>>(fm, rows, X, C, K, dY, Cout, p.kbps, partial, p.mt * BM);
+    kern<<<g, Cfg::THREADS, Cfg::SMEM, s>>>(fm, rows, X, C, K, dY, Cout, p.kbps, partial, p.mt * BM, async_arrive());
     launched("conv dW gather-GEMM (tcgen05)");
 }
 

@@ -218,6 +218,28 @@ extern "C" {
 const char* hc_last_error(void) { return g_last_error.c_str(); }
 const char* hc_version(void) { return "hashconv_b200 0.1 (sm_100a)"; }
 int64_t hc_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+hc_status hc_malloc(void** ptr, size_t bytes) {
+    return guard([&] { *ptr = dev_alloc(bytes); });
+}
+hc_status hc_free(void* ptr) {
+    return guard([&] { cuda_check(cudaFree(ptr), "cudaFree"); });
+}
+hc_status hc_memcpy_h2d(void* dst, const void* src, size_t bytes, hc_stream stream) {
+    return guard([&] {
+        cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, reinterpret_cast<cudaStream_t>(stream)),
+                   "H2D copy");
+    });
+}
+hc_status hc_memcpy_d2h(void* dst, const void* src, size_t bytes, hc_stream stream) {
+    return guard([&] {
+        cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, reinterpret_cast<cudaStream_t>(stream)),
+                   "D2H copy");
+    });
+}
+hc_status hc_stream_synchronize(hc_stream stream) {
+    return guard([&] { cuda_check(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)), "sync"); });
+}
 hc_status hc_set_math(hc_math mode) {
     if (mode != HC_MATH_EXACT && mode != HC_MATH_FAST) {
         set_last_error("unknown math mode");
