@@ -363,8 +363,11 @@ struct DwCfg {
     static constexpr int A_BYTES = 2 * KB * 128;  // two 64-wide MN blocks (M = 128)
     static constexpr int B_BYTES = (NB / 64) * KB * 128;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int THREADS = 160;
+    static constexpr int PRODUCERS = 256;          // warps 0-7 (epilogue: warps 0-3)
+    static constexpr int THREADS = PRODUCERS + 32;  // + warp 8: TMEM allocator and MMA issuer
     static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256;
+    static constexpr int AJ = 1024 / PRODUCERS;            // A chunks per producer per stage
+    static constexpr int BJ = (NB / 64) * 512 / PRODUCERS;  // B chunks per producer per stage
 };
 
 template <int NB>
@@ -375,6 +378,8 @@ __global__ void __launch_bounds__(DwCfg<NB>::THREADS)
     constexpr int S = Cfg::STAGES;
     constexpr int LAG = Cfg::LAG;
     constexpr int KB = Cfg::KB;
+    constexpr int AJ = Cfg::AJ, BJ = Cfg::BJ;
+    constexpr int P = Cfg::PRODUCERS;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * Cfg::STAGE_BYTES);
@@ -389,62 +394,72 @@ __global__ void __launch_bounds__(DwCfg<NB>::THREADS)
 
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
-            mbar_init(full0 + 8 * s, kProducers);
+            mbar_init(full0 + 8 * s, P);
             mbar_init(empty0 + 8 * s, 1);
         }
         mbar_init(done, 1);
         mbar_init_fence();
     }
-    if (warp == 4) tmem_alloc(smem_u32(tmem_slot), tmem_cols(NB));
+    if (warp == 8) tmem_alloc(smem_u32(tmem_slot), tmem_cols(NB));
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp < 4) {
+    if (warp < 8) {
+        // ---------------- producers. Per-thread constants (hoisted out of the stage loop):
+        // A chunk j: MN block / voxel row / 16-byte chunk -> its swizzled smem offset, the
+        // field-map tap it reads, and its channel offset inside the gathered X row.
         const int c = tid & 7;
-        const int q0 = tid >> 3;  // 0..15
-        // per-thread A chunk plan: (block, voxel row) pairs q0 + 16j; the field-map
-        // entries are prefetched two stages ahead into registers
-        int cur[8], nx1[8], nx2[8], tap[8], cio[8];
+        const int q0 = tid >> 3;  // 0..31
+        uint32_t a_off[AJ], b_off[BJ];
+        int tap[AJ], cio[AJ], rj[AJ], b_r[BJ], b_co[BJ];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int q = q0 + 16 * j;
-            const int mm = mt * BM + (q >> 6) * 64 + c * 8;
+        for (int j = 0; j < AJ; ++j) {
+            const int q = q0 + 32 * j;  // 0..127 = (block, voxel row)
+            const int blk = q >> 6, r = q & 63;
+            const int mm = mt * BM + blk * 64 + c * 8;
             tap[j] = mm < K ? mm / C : -1;
             cio[j] = mm < K ? mm - (mm / C) * C : 0;
+            rj[j] = r;
+            a_off[j] = blk * (KB * 128) + sw128_offset(r, c);
         }
-        auto fetch = [&](int kb, int (&dst)[8]) {
+#pragma unroll
+        for (int j = 0; j < BJ; ++j) {
+            const int q = q0 + 32 * j;
+            const int blk = q >> 6, r = q & 63;
+            b_r[j] = r;
+            b_co[j] = blk * 64 + c * 8;
+            b_off[j] = blk * (KB * 128) + sw128_offset(r, c);
+        }
+        int cur[AJ], nx1[AJ], nx2[AJ];
+        auto fetch = [&](int kb, int (&dst)[AJ]) {
             const long long n0 = (kb_begin + kb) * KB;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const long long n = n0 + ((q0 + 16 * j) & 63);
+            for (int j = 0; j < AJ; ++j) {
+                const long long n = n0 + rj[j];
                 dst[j] = (kb < nkb && tap[j] >= 0 && n < rows) ? fm_ld(fm, n, tap[j]) : -1;
             }
         };
-        auto issue = [&](int kb, const int (&use)[8]) {
+        auto issue = [&](int kb, const int (&use)[AJ]) {
             const int s = kb % S;
             if (kb >= S) mbar_wait(empty0 + 8 * s, ((kb / S) + 1) & 1);
-            uint8_t* A = smem + s * Cfg::STAGE_BYTES;
-            uint8_t* B = A + Cfg::A_BYTES;
+            const uint32_t A = smem_u32(smem + s * Cfg::STAGE_BYTES);
+            const uint32_t B = A + Cfg::A_BYTES;
             const long long n0 = (kb_begin + kb) * KB;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int q = q0 + 16 * j;
-                const int blk = q >> 6, r = q & 63;
+            for (int j = 0; j < AJ; ++j) {
                 const int g = use[j];
                 const bf16* src = g >= 0 ? X + (long long)g * C + cio[j] : X;
-                cp_async16(smem_u32(A + blk * (KB * 128) + sw128_offset(r, c)), src, g >= 0 ? 16u : 0u);
+                cp_async16(A + a_off[j], src, g >= 0 ? 16u : 0u);
             }
+            const bf16* dyb = dY + n0 * Cout;
+            const bool full_stage = n0 + KB <= rows;
 #pragma unroll
-            for (int j = 0; j < (NB / 64) * 4; ++j) {
-                const int q = q0 + 16 * j;
-                const int blk = q >> 6, r = q & 63;
-                const int co = blk * 64 + c * 8;
-                const long long n = n0 + r;
-                const bool ok = co < Cout && n < rows;
-                const bf16* src = ok ? dY + n * Cout + co : dY;
-                cp_async16(smem_u32(B + blk * (KB * 128) + sw128_offset(r, c)), src, ok ? 16u : 0u);
+            for (int j = 0; j < BJ; ++j) {
+                const bool ok = b_co[j] < Cout && (full_stage || n0 + b_r[j] < rows);
+                const bf16* src = ok ? dyb + (long long)b_r[j] * Cout + b_co[j] : dY;
+                cp_async16(B + b_off[j], src, ok ? 16u : 0u);
             }
             if (async_arrive) {
                 cp_async_arrive_noinc(full0 + 8 * s);
@@ -480,27 +495,29 @@ __global__ void __launch_bounds__(DwCfg<NB>::THREADS)
             for (int q = std::max(0, nkb - LAG); q < nkb; ++q) mbar_arrive(full0 + 8 * (q % S));
         }
 
-        // epilogue: row m = (t,ci) index, columns co
-        const int row = warp * 32 + (int)lane_id();
-        float* dst = partial + ((long long)split * Mtot + (long long)mt * BM + row) * NB;
-        if (nkb == 0) {
+        // epilogue (warps 0-3 = TMEM lane quadrants): row m = (t,ci) index, columns co
+        if (warp < 4) {
+            const int row = warp * 32 + (int)lane_id();
+            float* dst = partial + ((long long)split * Mtot + (long long)mt * BM + row) * NB;
+            if (nkb == 0) {
 #pragma unroll
-            for (int c0 = 0; c0 < NB; c0 += 4) *reinterpret_cast<float4*>(dst + c0) = make_float4(0, 0, 0, 0);
-        } else {
-            mbar_wait(done, 0);
-            tc_fence_after();
+                for (int c0 = 0; c0 < NB; c0 += 4) *reinterpret_cast<float4*>(dst + c0) = make_float4(0, 0, 0, 0);
+            } else {
+                mbar_wait(done, 0);
+                tc_fence_after();
 #pragma unroll
-            for (int c0 = 0; c0 < NB; c0 += 16) {
-                uint32_t v[16];
-                tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
-                tmem_ld_wait();
-                float f[16];
+                for (int c0 = 0; c0 < NB; c0 += 16) {
+                    uint32_t v[16];
+                    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
+                    tmem_ld_wait();
+                    float f[16];
 #pragma unroll
-                for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(v[e]);
-                store_row(dst + c0, f);
+                    for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(v[e]);
+                    store_row(dst + c0, f);
+                }
             }
         }
-    } else if (tid == 4 * 32 && nkb > 0) {
+    } else if (tid == 8 * 32 && nkb > 0) {
         constexpr uint32_t idesc = idesc_bf16_f32(BM, NB, true, true);
         constexpr uint32_t LBO = KB * 128;  // next 64-wide MN block
         for (int kb = 0; kb < nkb; ++kb) {
@@ -520,7 +537,7 @@ __global__ void __launch_bounds__(DwCfg<NB>::THREADS)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 4) {
+    if (warp == 8) {
         __syncwarp();
         tc_fence_after();
         tmem_dealloc(tmem, tmem_cols(NB));
