@@ -70,6 +70,16 @@ int async_arrive() {
     return v;
 }
 
+// Producer warps of the bulk-staged forward kernel (8, or 4 with HCB_FWD_PW=4).
+int fwd_pw() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("HCB_FWD_PW");
+        v = (e && std::atoi(e) == 4) ? 4 : 8;
+    }
+    return v;
+}
+
 int num_sms() {
     static int n = 0;
     if (!n) {
@@ -103,7 +113,7 @@ __device__ __forceinline__ void store_row(bf16* dst, const float (&v)[16]) {
 constexpr int kMaxTaps = 27;
 constexpr int kNbrBytes = kMaxTaps * BM * 4;  // 13.5 KB per buffer
 
-template <int BN, int CPS, bool TILED>
+template <int BN, int CPS, bool TILED, int PW = 4>
 struct FwdCfg {
     static constexpr int A_BYTES = BM * 128;      // 16 KB
     static constexpr int B_BYTES = BN * 128;
@@ -112,16 +122,21 @@ struct FwdCfg {
     static constexpr int NBR = TILED ? 2 * kNbrBytes : 0;
     static constexpr int STAGES = (BUDGET - NBR) / STAGE_BYTES;
     static constexpr int LAG = STAGES - 1;        // cp.async groups kept in flight per producer
-    static constexpr int THREADS = 288;           // producers 0-3, epilogue 4-7, MMA 8
+    static constexpr int PRODUCERS = PW * 32;     // producer warps 0..PW-1
+    static constexpr int THREADS = PW * 32 + 160;  // + epilogue warps PW..PW+3, MMA warp PW+4
     static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + NBR + 256;
 };
 
 // Y[m][0:BN] = sum_k A[m][k] * Wp[0:BN][k],  A[m][k] = X[nbr(m, k / C)][k % C] (0 if -1)
-template <int BN, int CPS, bool TILED, typename OutT>
-__global__ void __launch_bounds__(FwdCfg<BN, CPS, TILED>::THREADS, CPS)
+template <int BN, int CPS, bool TILED, typename OutT, int PW = 4>
+__global__ void __launch_bounds__(FwdCfg<BN, CPS, TILED, PW>::THREADS, CPS)
     k_gather_gemm(FMap fm, long long rows, const bf16* __restrict__ X, int C, int K, const bf16* __restrict__ Wp,
                   int Kp, OutT* __restrict__ Y, int tiles, int async_arrive) {
-    using Cfg = FwdCfg<BN, CPS, TILED>;
+    using Cfg = FwdCfg<BN, CPS, TILED, PW>;
+    constexpr int NP = Cfg::PRODUCERS;
+    static_assert(TILED || PW == 4, "the register-prefetch producer is written for 4 warps");
+    static_assert(PW % 4 == 0, "epilogue warps must start on a TMEM lane-quadrant boundary");
+    constexpr int RS = NP / 8;  // row stride between a producer thread's rows
     constexpr int S = Cfg::STAGES;
     constexpr int LAG = Cfg::LAG;
     static_assert(S >= 2, "ring too shallow");
@@ -141,7 +156,7 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, TILED>::THREADS, CPS)
 
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
-            mbar_init(full0 + 8 * s, kProducers);
+            mbar_init(full0 + 8 * s, NP);
             mbar_init(empty0 + 8 * s, 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -151,16 +166,16 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, TILED>::THREADS, CPS)
         }
         mbar_init_fence();
     }
-    if (warp == 8) tmem_alloc(smem_u32(tmem_slot), tmem_cols(2 * BN));
+    if (warp == PW + 4) tmem_alloc(smem_u32(tmem_slot), tmem_cols(2 * BN));
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (TILED && warp < 4) {
+    if (TILED && warp < PW) {
         // ---------------- producers (tile-major map, staged by bulk copies)
         const int c = tid & 7;    // 16-byte chunk within a 128-byte row
-        const int r0 = tid >> 3;  // rows r0 + 16j
+        const int r0 = tid >> 3;  // rows r0 + RS*j
         auto request = [&](int tile, int buf) {
             mbar_arrive_expect_tx(nfull0 + 8 * buf, nbr_bytes);
             bulk_g2s(smem_u32(nbr_s + buf * kMaxTaps * BM), fm.p + (long long)tile * taps * BM, nbr_bytes,
@@ -187,16 +202,17 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, TILED>::THREADS, CPS)
                 const int ci = kin ? k - t * C : 0;
                 const int* nbt = nb + t * BM;
 #pragma unroll
-                for (int j = 0; j < BM / 16; ++j) {
-                    const int r = r0 + 16 * j;
+                for (int j = 0; j < BM / RS; ++j) {
+                    const int r = r0 + RS * j;
                     const int g = kin ? nbt[r] : -1;
                     const bf16* src = g >= 0 ? X + (long long)g * C + ci : X;
                     cp_async16(smem_u32(A + sw128_offset(r, c)), src, g >= 0 ? 16u : 0u);
                 }
 #pragma unroll
-                for (int j = 0; j < BN / 16; ++j) {
-                    const int r = r0 + 16 * j;
-                    cp_async16(smem_u32(B + sw128_offset(r, c)), Wp + (long long)r * Kp + kb * BK + c * 8, 16u);
+                for (int j = 0; j < (BN + RS - 1) / RS; ++j) {
+                    const int r = r0 + RS * j;
+                    if (r < BN)
+                        cp_async16(smem_u32(B + sw128_offset(r, c)), Wp + (long long)r * Kp + kb * BK + c * 8, 16u);
                 }
                 if (async_arrive) {
                     cp_async_arrive_noinc(full0 + 8 * s);  // non-blocking: barrier completes on landing
@@ -210,7 +226,7 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, TILED>::THREADS, CPS)
                 }
             }
             // every producer is past this tile's map: refill the slot with tile i+2
-            named_sync(1, kProducers);
+            named_sync(1, NP);
             if (tid == 0 && tile + 2 * (int)gridDim.x < tiles) request(tile + 2 * gridDim.x, buf);
         }
         if (!async_arrive) {
@@ -218,7 +234,7 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, TILED>::THREADS, CPS)
             fence_proxy_async();
             for (long long q = std::max<long long>(0, it - LAG); q < it; ++q) mbar_arrive(full0 + 8 * (int)(q % S));
         }
-    } else if (!TILED && warp < 4) {
+    } else if (!TILED && warp < 4) {  // register-prefetch producers (PW == 4)
         // ---------------- producers
         const int c = tid & 7;    // 16-byte chunk within a 128-byte row
         const int r0 = tid >> 3;  // rows r0 + 16j
@@ -293,7 +309,7 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, TILED>::THREADS, CPS)
         cp_async_wait<0>();
         fence_proxy_async();
         for (long long i = std::max<long long>(0, it - LAG); i < it; ++i) mbar_arrive(full0 + 8 * (int)(i % S));
-    } else if (warp < 8) {
+    } else if (warp < PW + 4) {
         // ---------------- epilogue warpgroup: TMEM -> registers -> Y rows
         const int q = warp & 3;  // TMEM lane quadrant of this warp
         const int row = q * 32 + (int)lane_id();
@@ -316,7 +332,7 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, TILED>::THREADS, CPS)
             tc_fence_before();
             mbar_arrive(tempty0 + 8 * acc);
         }
-    } else if (tid == 8 * 32) {
+    } else if (tid == (PW + 4) * 32) {
         // ---------------- MMA issuer (single thread)
         constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, false, false);
         long long it = 0;
@@ -344,7 +360,7 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, TILED>::THREADS, CPS)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 8) {
+    if (warp == PW + 4) {
         __syncwarp();
         tc_fence_after();
         tmem_dealloc(tmem, tmem_cols(2 * BN));
@@ -623,11 +639,11 @@ __global__ void k_to_channel_major(const T* __restrict__ in, long long N, long l
 }
 
 // ====================================================================== launchers
-template <int BN, int CPS, bool TILED, typename OutT>
+template <int BN, int CPS, bool TILED, typename OutT, int PW = 4>
 void launch_gg_cps(const FMap& fm, long long rows, const bf16* X, int C, int K, const bf16* Wp, int Kp, OutT* Y,
                    cudaStream_t s) {
-    using Cfg = FwdCfg<BN, CPS, TILED>;
-    auto kern = k_gather_gemm<BN, CPS, TILED, OutT>;
+    using Cfg = FwdCfg<BN, CPS, TILED, PW>;
+    auto kern = k_gather_gemm<BN, CPS, TILED, OutT, PW>;
     static bool attr = false;  // per instantiation
     if (!attr) {
         cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM), "smem attr");
@@ -667,7 +683,10 @@ void launch_gg(const FMap& fm, long long rows, const bf16* X, int C, int K, cons
     }
     const bool one = fwd_env_cps() == 1;
     if constexpr (tiled_two) {
-        if (fm.tiled && variant != 1 && !one) return launch_gg_cps<BN, 2, true>(fm, rows, X, C, K, Wp, Kp, Y, s);
+        if (fm.tiled && variant != 1 && !one) {
+            if (fwd_pw() == 8) return launch_gg_cps<BN, 2, true, OutT, 8>(fm, rows, X, C, K, Wp, Kp, Y, s);
+            return launch_gg_cps<BN, 2, true, OutT, 4>(fm, rows, X, C, K, Wp, Kp, Y, s);
+        }
     }
     if constexpr (reg_two) {
         if (!one) return launch_gg_cps<BN, 2, false>(fm, rows, X, C, K, Wp, Kp, Y, s);

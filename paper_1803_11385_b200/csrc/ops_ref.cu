@@ -81,7 +81,7 @@ __global__ void k_field_map_t(DevPsh in, DevPsh out, int S, int pad, int* map) {
 // contiguous block (fetched by one bulk copy in the native conv); padded columns
 // beyond N are -1.
 template <int F>
-__global__ void k_field_map_tiled(DevPsh in, DevPsh out, int S, int pad, int* map) {
+__global__ void __launch_bounds__(256, 4) k_field_map_tiled(DevPsh in, DevPsh out, int S, int pad, int* map) {
     const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     const long long padded = (out.N + 127) / 128 * 128;
     if (col >= padded) return;
