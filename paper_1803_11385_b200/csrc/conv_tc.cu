@@ -36,6 +36,12 @@
 
 namespace hcb {
 
+// conv_tma.cu: the TMA tile::gather4 variant of the forward gather-GEMM
+bool gather_gemm_tma_supported(int C, int N);
+template <typename OutT>
+void gather_gemm_tma(const int* fmap, int taps, long long rows, const __nv_bfloat16* X, int C,
+                     const __nv_bfloat16* Wp, int Kp, int N, OutT* Y, cudaStream_t s);
+
 namespace {
 
 using bf16 = __nv_bfloat16;
@@ -698,6 +704,10 @@ void launch_gg(const FMap& fm, long long rows, const bf16* X, int C, int K, cons
 template <typename OutT>
 void gather_gemm(const FMap& fm, long long rows, const bf16* X, int C, int K, const bf16* Wp, int Kp, int N, OutT* Y,
                  cudaStream_t s) {
+    if (fm.tiled && gather_gemm_tma_supported(C, N)) {  // TMA gather4 producers (conv_tma.cu)
+        gather_gemm_tma<OutT>(fm.p, fm.taps, rows, X, C, Wp, Kp, N, Y, s);
+        return;
+    }
     switch (N) {
         case 16: launch_gg<16>(fm, rows, X, C, K, Wp, Kp, Y, s); break;
         case 32: launch_gg<32>(fm, rows, X, C, K, Wp, Kp, Y, s); break;
