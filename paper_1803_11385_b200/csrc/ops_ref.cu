@@ -22,6 +22,12 @@ namespace {
 
 constexpr int kThreads = 256;
 
+// tuning knobs read once from the environment (A/B experiments; defaults are the tuned values)
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+
 // cnn_ops.cpp:20-33 check_pair (same messages, same order)
 void check_pair(const hc_psh* in, const hc_psh* out, const hc_conv_spec& sp) {
     if (!in || !out) throw std::invalid_argument("null super-PSH handle");
@@ -137,9 +143,12 @@ __global__ void k_field_map_any(DevPsh in, DevPsh out, int F, int S, int pad, in
 
 // ============================================================== hash2col
 // cnn_ops.cpp:123-158: cols[(c*fd + row), col] = data[c, hit] or 0.
-template <int F>
-__global__ void k_hash2col(DevPsh in, DevPsh out, int S, int pad, const float* __restrict__ data, int C,
-                           float* __restrict__ cols) {
+// Memory-bound: occupancy matters more than per-thread ILP, so registers are capped
+// (MINB resident 256-thread blocks per SM).
+template <int F, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+    k_hash2col(DevPsh in, DevPsh out, int S, int pad, const float* __restrict__ data, int C,
+               float* __restrict__ cols) {
     const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (col >= out.N) return;
     const int4 c = out.cols[col];
@@ -231,8 +240,54 @@ __device__ __forceinline__ int cover_hits_s1(const DevPsh& out, const ModelParam
 // structure, visited in ascending tap order (= ascending p_o) WITHOUT compaction, so
 // at every step all lanes of a warp read the same column-matrix row (fd-1-t) at
 // neighbouring columns: coalesced gathers instead of per-lane scattered rows.
-template <int F>
-__global__ void k_col2hash_s1(DevPsh in, DevPsh out, const float* __restrict__ g, int C, float* __restrict__ res) {
+// Taps-outer variant: the 27 probed columns are parked in shared memory ([tap][thread],
+// conflict-free), then for each tap every thread issues CB independent channel loads
+// into CB accumulators. Per channel the taps are still added in ascending order, so the
+// result is bit-identical to cnn_ops.cpp:184-196.
+template <int F, int CB>
+__global__ void __launch_bounds__(256, 4)
+    k_col2hash_s1_tb(DevPsh in, DevPsh out, const float* __restrict__ g, int C, float* __restrict__ res) {
+    constexpr int T3 = F * F * F;
+    __shared__ int nbs[T3][256];
+    const long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const bool live = gi < in.N;
+    const int fd = out.dim == 3 ? T3 : F * F;
+    if (live) {
+        const int4 c = in.cols[gi];
+        const ModelParam mp = out.models[c.w - 1];
+        constexpr int h = (F - 1) / 2;
+        int nb[T3];
+        probe_field<F>(out, mp, c.x - h, c.y - h, c.z - h, nb);
+#pragma unroll
+        for (int t = 0; t < T3; ++t) nbs[t][threadIdx.x] = t < fd ? nb[t] : -1;
+    }
+    if (!live) return;  // no block-wide barrier below: each thread reads only its own column
+    const long long Nout = out.N, Nin = in.N;
+    const long long plane = (long long)fd * Nout;
+    for (int cb = 0; cb < C; cb += CB) {
+        float acc[CB];
+#pragma unroll
+        for (int u = 0; u < CB; ++u) acc[u] = 0.0f;
+        const float* base = g + (long long)cb * plane;
+        for (int t = 0; t < fd; ++t) {
+            const int col = nbs[t][threadIdx.x];
+            if (col < 0) continue;
+            const float* p = base + (long long)(fd - 1 - t) * Nout + col;
+#pragma unroll
+            for (int u = 0; u < CB; ++u)
+                if (cb + u < C) acc[u] = __fadd_rn(acc[u], __ldg(p + u * plane));
+        }
+#pragma unroll
+        for (int u = 0; u < CB; ++u)
+            if (cb + u < C) res[(cb + u) * Nin + gi] = acc[u];
+    }
+}
+
+// CU channels per pass: CU independent accumulator chains (each still adds its taps in
+// ascending order -> bit-exact); registers capped for MINB resident blocks per SM.
+template <int F, int CU, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+    k_col2hash_s1(DevPsh in, DevPsh out, const float* __restrict__ g, int C, float* __restrict__ res) {
     const long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (gi >= in.N) return;
     const int4 c = in.cols[gi];
@@ -242,9 +297,27 @@ __global__ void k_col2hash_s1(DevPsh in, DevPsh out, const float* __restrict__ g
     int nb[F * F * F];
     probe_field<F>(out, mp, c.x - h, c.y - h, c.z - h, nb);
     const long long Nout = out.N, Nin = in.N;
-    for (int ch = 0; ch < C; ++ch) {
+    const long long plane = (long long)fd * Nout;  // one channel's block of the column matrix
+    int ch = 0;
+    for (; ch + CU <= C; ch += CU) {
+        float a[CU];
+#pragma unroll
+        for (int u = 0; u < CU; ++u) a[u] = 0.0f;
+        const float* b0 = g + (long long)ch * plane;
+#pragma unroll
+        for (int t = 0; t < F * F * F; ++t) {
+            if (t < fd && nb[t] >= 0) {
+                const float* p = b0 + (long long)(fd - 1 - t) * Nout + nb[t];
+#pragma unroll
+                for (int u = 0; u < CU; ++u) a[u] = __fadd_rn(a[u], __ldg(p + u * plane));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < CU; ++u) res[(ch + u) * Nin + gi] = a[u];
+    }
+    for (; ch < C; ++ch) {
         float acc = 0.0f;
-        const float* base = g + (long long)ch * fd * Nout;
+        const float* base = g + (long long)ch * plane;
 #pragma unroll
         for (int t = 0; t < F * F * F; ++t)
             if (t < fd && nb[t] >= 0) acc = __fadd_rn(acc, __ldg(base + (long long)(fd - 1 - t) * Nout + nb[t]));
@@ -509,9 +582,14 @@ void launch_hash2col(const hc_psh* in, const float* data, const hc_psh* out, con
     if (n == 0 || sp.in_channels == 0) return;
     const unsigned g = grid_for(n, kThreads);
     if (sp.kernel == 3)
-        k_hash2col<3><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, cols);
+    {
+        static const int minb = env_int("HCB_H2C_MINB", 4);
+        if (minb >= 4) k_hash2col<3, 4><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, cols);
+        else if (minb >= 2) k_hash2col<3, 2><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, cols);
+        else k_hash2col<3, 1><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, cols);
+    }
     else if (sp.kernel == 2)
-        k_hash2col<2><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, cols);
+        k_hash2col<2, 4><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, cols);
     else
         k_hash2col_any<<<g, kThreads, 0, s>>>(in->d, out->d, sp.kernel, sp.stride, sp.pad,
                                             (int)field_volume(sp, in->d.dim), data, sp.in_channels, cols);
@@ -526,7 +604,14 @@ void launch_col2hash(const float* gcols, const hc_psh* in, const hc_psh* out, co
     const int fd = (int)field_volume(sp, in->d.dim);
     const int C = sp.in_channels;
     if (sp.stride == 1 && sp.kernel == 3)
-        k_col2hash_s1<3><<<g, kThreads, 0, s>>>(in->d, out->d, gcols, C, res);
+    {
+        static const int cu = env_int("HCB_C2H_CU", 16);
+        if (cu == 16) k_col2hash_s1_tb<3, 16><<<g, kThreads, 0, s>>>(in->d, out->d, gcols, C, res);
+        else if (cu == 8) k_col2hash_s1_tb<3, 8><<<g, kThreads, 0, s>>>(in->d, out->d, gcols, C, res);
+        else if (cu >= 4) k_col2hash_s1<3, 4, 4><<<g, kThreads, 0, s>>>(in->d, out->d, gcols, C, res);
+        else if (cu >= 2) k_col2hash_s1<3, 2, 4><<<g, kThreads, 0, s>>>(in->d, out->d, gcols, C, res);
+        else k_col2hash_s1<3, 1, 4><<<g, kThreads, 0, s>>>(in->d, out->d, gcols, C, res);
+    }
     else if (sp.stride == 1 && sp.kernel == 1)
         k_col2hash<1, true, 1><<<g, kThreads, 0, s>>>(in->d, out->d, 1, 1, 0, fd, gcols, C, res);
     else if (sp.stride > 1 && cover_per_axis(sp) == 1)
