@@ -11,7 +11,7 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libhcb200.so")
+LIB_PATH = os.environ.get("HCB_LIB_PATH") or os.path.join(HERE, "_lib", "libhcb200.so")  # override: A/B builds
 HEADERS = [os.path.join(os.path.dirname(HERE), "include", h)
            for h in ("hashconv_b200.h", "hashconv_b200_native.h")]
 

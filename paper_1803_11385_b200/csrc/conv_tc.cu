@@ -2,32 +2,44 @@
 //
 // Implicit GEMM: the hash2col column matrix is never materialised. For output
 // voxel n and field row t the field map (K0, ops_ref.cu) gives the input column
-// nbr(n,t) (or -1); the A operand is gathered straight from the voxel-major
+// nbr(n,t) (or -1); the gathered operand is copied straight from the voxel-major
 // feature rows X[nbr][:] into shared memory with 16-byte cp.async (zero-fill for
-// empty cells), laid out in the UMMA SWIZZLE_128B canonical form, and
-// tcgen05.mma accumulates in TMEM.
+// empty cells) in the UMMA SWIZZLE_128B canonical form, the dense operand (packed
+// weights, or dY for the weight gradient) arrives by 2-D TMA, and tcgen05.mma
+// accumulates in TMEM.
 //
 //   forward        Y [n][co]  = sum_{t,ci} X[nbr(n,t)][ci] * W[co][t][ci]
 //   backward-data  dX[g][ci]  = sum_{t,co} dY[nbr(g,t)][co] * W[co][26-t][ci]
 //                  (stride 1: the same kernel with flipped/transposed weights;
 //                   cnn_ops.cpp:217-232 computes col2hash(W^T dY), the same sum)
 //   weight grad    dW[co][t][ci] = sum_n dY[n][co] * X[nbr(n,t)][ci]
-//                  (reduction over voxels: split-K over CTAs, partials reduced in a
-//                   fixed order -> deterministic; both operands MN-major)
+//                  (cnn_ops.cpp:228 matmul_trans_b; reduction over voxels: split-K over
+//                   CTAs, partials reduced in a fixed order -> deterministic)
 //
-// Forward kernel: persistent, warp-specialised — 4 producer warps stream the
-// gathered operand ring continuously across tiles (field-map entries are
-// prefetched into registers two stages ahead, so no dependent load sits on the
-// issue path), one elected thread issues tcgen05.mma, and a separate epilogue
-// warpgroup drains double-buffered TMEM accumulators while the next tile's MMAs
-// run.
+// Both kernels are persistent and warp-specialised:
+//   producers  — warps that issue the gathers; per stage each thread does one shared
+//                load of the tile's field-map entry (the map block of a 128-voxel tile is
+//                staged by one bulk copy a tile ahead) and one cp.async per 16-byte chunk;
+//                the stage completes on the mbarrier when the copies land
+//                (cp.async.mbarrier.arrive.noinc), so no producer ever blocks on its own
+//                copies. Stage/phase cursors and the (tap, channel) cursor advance
+//                incrementally — no divisions on the issue path.
+//   TMA        — one thread loads the dense operand of each stage (forward: its own warp).
+//   MMA        — one thread issues tcgen05.mma (M128 x N x K16) and commits the stage.
+//   epilogue   — one warpgroup drains double-buffered TMEM accumulators (forward).
+// Long waits use mbarrier.try_wait with a suspend-time hint, so idle warps sleep
+// instead of stealing issue slots from the producers (the round-1 profile showed
+// ~30% of all issued instructions were try_wait spins).
 //
 // Numerics: bf16 operands, fp32 accumulation (TMEM), fp32 or bf16 outputs.
 // Tolerance-level parity against the double oracle (tests/test_conv_tc.py).
+#include <cuda.h>  // CUtensorMap / enums only; the encoder comes from cudaGetDriverEntryPoint
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "hashconv_b200_native.h"
 #include "hc_internal.h"
@@ -35,55 +47,27 @@
 #include "tc_common.cuh"
 
 namespace hcb {
-
-// conv_tma.cu: the TMA tile::gather4 variant of the forward gather-GEMM
-bool gather_gemm_tma_supported(int C, int N);
-template <typename OutT>
-void gather_gemm_tma(const int* fmap, int taps, long long rows, const __nv_bfloat16* X, int C,
-                     const __nv_bfloat16* Wp, int Kp, int N, OutT* Y, cudaStream_t s);
-
 namespace {
 
 using bf16 = __nv_bfloat16;
 using namespace tc;
 
-constexpr int BM = 128;          // voxels (GEMM M) per tile
-constexpr int BK = 64;           // K elements (bf16) per pipeline stage = one 128 B row
-constexpr int kProducers = 128;  // warps 0-3
+#ifdef HCB_WAIT_SPIN  // A/B: plain try_wait spins for the long waits too
+#define mbar_wait_sleep mbar_wait
+#endif
 
-__host__ __device__ constexpr int tmem_cols(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512; }
+constexpr int BM = 128;  // voxels per forward tile (GEMM M) / (t,ci) rows per dW m-tile
+constexpr int BK = 64;   // K elements (bf16) per stage = one 128-byte row
+constexpr int kMaxTaps = 27;
+constexpr int kNbrBytes = kMaxTaps * BM * 4;  // 13.5 KB field-map block per tile
 
-// Field map access: element (n, t) at p[n*sn + t*st] (row-major [N][taps] or tap-major [taps][N]).
-// Layouts: 0 row-major [N][taps], 1 tap-major [taps][N], 2 tile-major [N/128][taps][128].
-struct FMap {
-    const int* p;
-    long long sn, st;
-    int tiled, taps;
-};
-__device__ __forceinline__ int fm_ld(const FMap& f, long long n, int t) {
-    if (f.tiled) return __ldg(f.p + ((n >> 7) * f.taps + t) * 128 + (n & 127));
-    return __ldg(f.p + n * f.sn + (long long)t * f.st);
+__host__ __device__ constexpr int tmem_cols(int n) {
+    return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512;
 }
 
-// Producers signal stage completion with cp.async.mbarrier.arrive.noinc (non-blocking)
-// instead of wait_group + arrive. HCB_ASYNC_ARRIVE=0 selects the blocking form (A/B).
-int async_arrive() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = std::getenv("HCB_ASYNC_ARRIVE");
-        v = e ? (std::atoi(e) != 0) : 1;
-    }
-    return v;
-}
-
-// Producer warps of the bulk-staged forward kernel (8, or 4 with HCB_FWD_PW=4).
-int fwd_pw() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = std::getenv("HCB_FWD_PW");
-        v = (e && std::atoi(e) == 4) ? 4 : 8;
-    }
-    return v;
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
 }
 
 int num_sms() {
@@ -94,6 +78,39 @@ int num_sms() {
         cuda_check(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev), "sm count");
     }
     return n;
+}
+
+// ---------------------------------------------------------------------- TMA descriptors
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encoder() {
+    static EncodeTiled fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        cuda_check(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q),
+                   "cudaGetDriverEntryPoint(cuTensorMapEncodeTiled)");
+        if (!p || q != cudaDriverEntryPointSuccess) throw cuda_error("cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeTiled>(p);
+    }
+    return fn;
+}
+
+// 2-D bf16 tensor [rows][inner] (row pitch `pitch` bytes), box = box_rows x 64 elements
+// (one 128-byte swizzle span), SWIZZLE_128B, out-of-bounds elements read as zero.
+CUtensorMap map2d(const void* base, uint64_t inner, uint64_t rows, uint64_t pitch, uint32_t box_rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {inner, rows};
+    const cuuint64_t strides[1] = {pitch};
+    const cuuint32_t box[2] = {64, box_rows};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                                 es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw cuda_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return m;
 }
 
 __device__ __forceinline__ void store_row(float* dst, const float (&v)[16]) {
@@ -111,64 +128,56 @@ __device__ __forceinline__ void store_row(bf16* dst, const float (&v)[16]) {
     *reinterpret_cast<uint4*>(dst + 8) = make_uint4(p[4], p[5], p[6], p[7]);
 }
 
-// ====================================================================== gather-GEMM (persistent)
-// CPS = resident CTAs per SM: 2 (4-stage rings, twice the producer warps per SM)
-// or 1 (one deep ring). Both fit ~200 KB of shared memory per SM.
-// TILED: the field map is tile-major and each tile's 27x128 map block is brought into
-// a double-buffered shared-memory slot by one bulk copy a tile ahead.
-constexpr int kMaxTaps = 27;
-constexpr int kNbrBytes = kMaxTaps * BM * 4;  // 13.5 KB per buffer
-
-template <int BN, int CPS, bool TILED, int PW = 4>
+// ====================================================================== forward gather-GEMM
+// Y[m][0:BN] = sum_k A[m][k] * Wp[0:BN][k],  A[m][k] = X[nbr(m, k / C)][k % C] (0 if -1)
+// CPS resident CTAs per SM (1: one deep ring; 2: two shallower rings), PW producer warps.
+template <int BN, int CPS, int PW>
 struct FwdCfg {
-    static constexpr int A_BYTES = BM * 128;      // 16 KB
+    static constexpr int A_BYTES = BM * 128;  // 16 KB
     static constexpr int B_BYTES = BN * 128;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int BUDGET = (CPS == 2 ? 113 : 226) * 1024 - 1280;
-    static constexpr int NBR = TILED ? 2 * kNbrBytes : 0;
-    static constexpr int STAGES = (BUDGET - NBR) / STAGE_BYTES;
-    static constexpr int LAG = STAGES - 1;        // cp.async groups kept in flight per producer
-    static constexpr int PRODUCERS = PW * 32;     // producer warps 0..PW-1
-    static constexpr int THREADS = PW * 32 + 160;  // + epilogue warps PW..PW+3, MMA warp PW+4
-    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + NBR + 256;
+    static constexpr int NBR = 2 * kNbrBytes;
+    static constexpr int BUDGET = (CPS == 2 ? 113 : 226) * 1024 - 1024 - 320 - NBR;
+    static constexpr int STAGES = BUDGET / STAGE_BYTES > 10 ? 10 : BUDGET / STAGE_BYTES;
+    static constexpr int PRODUCERS = PW * 32;      // warps 0..PW-1
+    static constexpr int THREADS = PW * 32 + 192;  // + epilogue warps PW..PW+3, MMA warp PW+4, TMA warp PW+5
+    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + NBR + 320;
 };
 
-// Y[m][0:BN] = sum_k A[m][k] * Wp[0:BN][k],  A[m][k] = X[nbr(m, k / C)][k % C] (0 if -1)
-template <int BN, int CPS, bool TILED, typename OutT, int PW = 4>
-__global__ void __launch_bounds__(FwdCfg<BN, CPS, TILED, PW>::THREADS, CPS)
-    k_gather_gemm(FMap fm, long long rows, const bf16* __restrict__ X, int C, int K, const bf16* __restrict__ Wp,
-                  int Kp, OutT* __restrict__ Y, int tiles, int async_arrive) {
-    using Cfg = FwdCfg<BN, CPS, TILED, PW>;
+template <int BN, int CPS, int PW, typename OutT>
+__global__ void __launch_bounds__(FwdCfg<BN, CPS, PW>::THREADS, CPS)
+    k_conv_fwd(const __grid_constant__ CUtensorMap wmap, const int* __restrict__ fmap, int taps, long long rows,
+               const bf16* __restrict__ X, int C, int nkb, OutT* __restrict__ Y, int tiles) {
+    using Cfg = FwdCfg<BN, CPS, PW>;
     constexpr int NP = Cfg::PRODUCERS;
-    static_assert(TILED || PW == 4, "the register-prefetch producer is written for 4 warps");
-    static_assert(PW % 4 == 0, "epilogue warps must start on a TMEM lane-quadrant boundary");
-    constexpr int RS = NP / 8;  // row stride between a producer thread's rows
     constexpr int S = Cfg::STAGES;
-    constexpr int LAG = Cfg::LAG;
-    static_assert(S >= 2, "ring too shallow");
+    constexpr int RS = NP / 8;  // row stride between one producer thread's rows
+    constexpr int J = BM / RS;  // rows per producer thread per stage
+    static_assert(BM % RS == 0 && S >= 2, "producer / ring shape");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    int* nbr_s = reinterpret_cast<int*>(smem + S * Cfg::STAGE_BYTES);  // [2][taps][128] when TILED
+    int* nbr_s = reinterpret_cast<int*>(smem + S * Cfg::STAGE_BYTES);  // [2][taps][128]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * Cfg::STAGE_BYTES + Cfg::NBR);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 6);
+    int* nbr_cnt = reinterpret_cast<int*>(tmem_slot + 2);  // warps done with each map buffer
 
     const int tid = threadIdx.x, warp = tid >> 5;
-    const int nkb = Kp / BK;
+    const uint32_t sbase = smem_u32(smem);
     const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S);
     const uint32_t tfull0 = smem_u32(bars + 2 * S), tempty0 = smem_u32(bars + 2 * S + 2);
     const uint32_t nfull0 = smem_u32(bars + 2 * S + 4);
-    const int taps = fm.taps;
     const uint32_t nbr_bytes = (uint32_t)(taps * BM * 4);
 
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
-            mbar_init(full0 + 8 * s, NP);
+            mbar_init(full0 + 8 * s, NP + 1);  // NP cp.async arrivals + the TMA expect_tx arrival
             mbar_init(empty0 + 8 * s, 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull0 + 8 * a, 1);
             mbar_init(tempty0 + 8 * a, 128);
             mbar_init(nfull0 + 8 * a, 1);
+            nbr_cnt[a] = 0;
         }
         mbar_init_fence();
     }
@@ -178,143 +187,66 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, TILED, PW>::THREADS, CPS)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (TILED && warp < PW) {
-        // ---------------- producers (tile-major map, staged by bulk copies)
+    if (warp < PW) {
+        // ---------------- producers
         const int c = tid & 7;    // 16-byte chunk within a 128-byte row
         const int r0 = tid >> 3;  // rows r0 + RS*j
+        uint32_t doff[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) doff[j] = sw128_offset(r0 + RS * j, c);
+        const int t0 = (c * 8) / C, ci0 = c * 8 - t0 * C;
+        const uint32_t row_bytes = (uint32_t)C * 2;
         auto request = [&](int tile, int buf) {
             mbar_arrive_expect_tx(nfull0 + 8 * buf, nbr_bytes);
-            bulk_g2s(smem_u32(nbr_s + buf * kMaxTaps * BM), fm.p + (long long)tile * taps * BM, nbr_bytes,
+            bulk_g2s(smem_u32(nbr_s + buf * kMaxTaps * BM), fmap + (long long)tile * taps * BM, nbr_bytes,
                      nfull0 + 8 * buf);
         };
         if (tid == 0) {
             if (blockIdx.x < tiles) request(blockIdx.x, 0);
             if (blockIdx.x + gridDim.x < tiles) request(blockIdx.x + gridDim.x, 1);
         }
-        long long it = 0;
+        int s = 0;
+        uint32_t ph = 0;
         int i = 0;
         for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++i) {
             const int buf = i & 1;
-            mbar_wait(nfull0 + 8 * buf, (uint32_t)((i >> 1) & 1));
-            const int* nb = nbr_s + buf * kMaxTaps * BM;
-            for (int kb = 0; kb < nkb; ++kb, ++it) {
-                const int s = (int)(it % S);
-                if (it >= S) mbar_wait(empty0 + 8 * s, (uint32_t)(((it / S) + 1) & 1));
-                uint8_t* A = smem + s * Cfg::STAGE_BYTES;
-                uint8_t* B = A + Cfg::A_BYTES;
-                const int k = kb * BK + c * 8;
-                const bool kin = k < K;
-                const int t = kin ? k / C : 0;
-                const int ci = kin ? k - t * C : 0;
-                const int* nbt = nb + t * BM;
+            mbar_wait_sleep(nfull0 + 8 * buf, (uint32_t)((i >> 1) & 1));
+            const uint32_t nb = smem_u32(nbr_s + buf * kMaxTaps * BM + r0);
+            int t = t0, ci = ci0;
+            for (int kb = 0; kb < nkb; ++kb) {
+                // field-map entries first (independent shared loads, batched), then the copies
+                int g[J];
+                if (t < taps) {  // k = t*C + ci < K
 #pragma unroll
-                for (int j = 0; j < BM / RS; ++j) {
-                    const int r = r0 + RS * j;
-                    const int g = kin ? nbt[r] : -1;
-                    const bf16* src = g >= 0 ? X + (long long)g * C + ci : X;
-                    cp_async16(smem_u32(A + sw128_offset(r, c)), src, g >= 0 ? 16u : 0u);
-                }
-#pragma unroll
-                for (int j = 0; j < (BN + RS - 1) / RS; ++j) {
-                    const int r = r0 + RS * j;
-                    if (r < BN)
-                        cp_async16(smem_u32(B + sw128_offset(r, c)), Wp + (long long)r * Kp + kb * BK + c * 8, 16u);
-                }
-                if (async_arrive) {
-                    cp_async_arrive_noinc(full0 + 8 * s);  // non-blocking: barrier completes on landing
+                    for (int j = 0; j < J; ++j) g[j] = ld_shared_s32(nb + (t * BM + RS * j) * 4);
                 } else {
-                    cp_async_commit();
-                    if (it >= LAG) {
-                        cp_async_wait<LAG>();
-                        fence_proxy_async();
-                        mbar_arrive(full0 + 8 * (int)((it - LAG) % S));
-                    }
+#pragma unroll
+                    for (int j = 0; j < J; ++j) g[j] = -1;
+                }
+                mbar_wait_sleep(empty0 + 8 * s, ph ^ 1);
+                const uint32_t A = sbase + s * Cfg::STAGE_BYTES;
+                const char* xs = reinterpret_cast<const char*>(X + ci);
+#pragma unroll
+                for (int j = 0; j < J; ++j) cp_async16_row(A + doff[j], xs, g[j], row_bytes);
+                cp_async_arrive_noinc(full0 + 8 * s);
+                ci += BK;
+                while (ci >= C) {
+                    ci -= C;
+                    ++t;
+                }
+                if (++s == S) {
+                    s = 0;
+                    ph ^= 1;
                 }
             }
-            // every producer is past this tile's map: refill the slot with tile i+2
-            named_sync(1, NP);
-            if (tid == 0 && tile + 2 * (int)gridDim.x < tiles) request(tile + 2 * gridDim.x, buf);
+            // this warp is past the tile's map block; the last warp to get here refills it
+            // with tile i+2 (no CTA-wide barrier: producers never wait for each other)
+            __syncwarp();
+            if ((tid & 31) == 0 && atomicAdd(&nbr_cnt[buf], 1) == PW - 1) {
+                nbr_cnt[buf] = 0;
+                if (tile + 2 * (int)gridDim.x < tiles) request(tile + 2 * gridDim.x, buf);
+            }
         }
-        if (!async_arrive) {
-            cp_async_wait<0>();
-            fence_proxy_async();
-            for (long long q = std::max<long long>(0, it - LAG); q < it; ++q) mbar_arrive(full0 + 8 * (int)(q % S));
-        }
-    } else if (!TILED && warp < 4) {  // register-prefetch producers (PW == 4)
-        // ---------------- producers
-        const int c = tid & 7;    // 16-byte chunk within a 128-byte row
-        const int r0 = tid >> 3;  // rows r0 + 16j
-        // Field-map entries for stage it+2 are loaded while stage it is issued; the three
-        // register buffers rotate by unrolling (no register copies, which would force
-        // the in-flight loads to complete early).
-        int fa[BM / 16], fb[BM / 16], fc[BM / 16];
-        int lt = blockIdx.x, lk = 0;  // load cursor (two stages ahead)
-        int ut = blockIdx.x, uk = 0;  // issue cursor
-        auto fetch = [&](int (&dst)[BM / 16]) {
-            const int k = lk * BK + c * 8;
-            const bool ok = lt < tiles && k < K;
-            const int t = ok ? k / C : 0;
-#pragma unroll
-            for (int j = 0; j < BM / 16; ++j) {
-                const long long n = (long long)lt * BM + r0 + 16 * j;
-                dst[j] = (ok && n < rows) ? fm_ld(fm, n, t) : -1;
-            }
-            if (++lk == nkb) {
-                lk = 0;
-                lt += gridDim.x;
-            }
-        };
-        auto issue = [&](long long it, const int (&use)[BM / 16]) {
-            const int s = (int)(it % S);
-            if (it >= S) mbar_wait(empty0 + 8 * s, (uint32_t)(((it / S) + 1) & 1));
-            uint8_t* A = smem + s * Cfg::STAGE_BYTES;
-            uint8_t* B = A + Cfg::A_BYTES;
-            const int k = uk * BK + c * 8;
-            const int ci = k < K ? k - (k / C) * C : 0;
-#pragma unroll
-            for (int j = 0; j < BM / 16; ++j) {
-                const int r = r0 + 16 * j;
-                const int g = use[j];
-                const bf16* src = g >= 0 ? X + (long long)g * C + ci : X;
-                cp_async16(smem_u32(A + sw128_offset(r, c)), src, g >= 0 ? 16u : 0u);
-            }
-#pragma unroll
-            for (int j = 0; j < BN / 16; ++j) {
-                const int r = r0 + 16 * j;
-                cp_async16(smem_u32(B + sw128_offset(r, c)), Wp + (long long)r * Kp + uk * BK + c * 8, 16u);
-            }
-            cp_async_commit();
-            if (it >= LAG) {
-                cp_async_wait<LAG>();
-                fence_proxy_async();
-                mbar_arrive(full0 + 8 * (int)((it - LAG) % S));
-            }
-            if (++uk == nkb) {
-                uk = 0;
-                ut += gridDim.x;
-            }
-        };
-        const long long my_tiles = blockIdx.x < tiles ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-        const long long total = my_tiles * nkb;
-        fetch(fa);
-        fetch(fb);
-        long long it = 0;
-        for (; it + 3 <= total; it += 3) {
-            fetch(fc);
-            issue(it, fa);
-            fetch(fa);
-            issue(it + 1, fb);
-            fetch(fb);
-            issue(it + 2, fc);
-        }
-        if (it < total) {
-            fetch(fc);
-            issue(it++, fa);
-        }
-        if (it < total) issue(it++, fb);
-        cp_async_wait<0>();
-        fence_proxy_async();
-        for (long long i = std::max<long long>(0, it - LAG); i < it; ++i) mbar_arrive(full0 + 8 * (int)(i % S));
     } else if (warp < PW + 4) {
         // ---------------- epilogue warpgroup: TMEM -> registers -> Y rows
         const int q = warp & 3;  // TMEM lane quadrant of this warp
@@ -322,7 +254,7 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, TILED, PW>::THREADS, CPS)
         int i = 0;
         for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++i) {
             const int acc = i & 1;
-            mbar_wait(tfull0 + 8 * acc, (uint32_t)((i >> 1) & 1));
+            mbar_wait_sleep(tfull0 + 8 * acc, (uint32_t)((i >> 1) & 1));
             tc_fence_after();
             const long long m = (long long)tile * BM + row;
 #pragma unroll
@@ -338,28 +270,47 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, TILED, PW>::THREADS, CPS)
             tc_fence_before();
             mbar_arrive(tempty0 + 8 * acc);
         }
+    } else if (tid == (PW + 5) * 32) {
+        // ---------------- weight-tile loader (single thread): one 2-D TMA per stage
+        int s = 0;
+        uint32_t ph = 0;
+        for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+            for (int kb = 0; kb < nkb; ++kb) {
+                mbar_wait_sleep(empty0 + 8 * s, ph ^ 1);
+                mbar_arrive_expect_tx(full0 + 8 * s, Cfg::B_BYTES);
+                tma_load2d(sbase + s * Cfg::STAGE_BYTES + Cfg::A_BYTES, &wmap, kb * BK, 0, full0 + 8 * s);
+                if (++s == S) {
+                    s = 0;
+                    ph ^= 1;
+                }
+            }
+        }
     } else if (tid == (PW + 4) * 32) {
         // ---------------- MMA issuer (single thread)
         constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, false, false);
-        long long it = 0;
+        int s = 0;
+        uint32_t ph = 0;
         int i = 0;
         for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++i) {
             const int acc = i & 1;
-            if (i >= 2) mbar_wait(tempty0 + 8 * acc, (uint32_t)(((i >> 1) - 1) & 1));
+            mbar_wait(tempty0 + 8 * acc, (uint32_t)(((i >> 1) & 1) ^ 1));
             tc_fence_after();
             const uint32_t d = tmem + acc * BN;
-            for (int kb = 0; kb < nkb; ++kb, ++it) {
-                const int s = (int)(it % S);
-                mbar_wait(full0 + 8 * s, (uint32_t)((it / S) & 1));
-                if (async_arrive) fence_proxy_async();
+            for (int kb = 0; kb < nkb; ++kb) {
+                mbar_wait(full0 + 8 * s, ph);
+                fence_proxy_async();  // cp.async (generic proxy) writes -> tcgen05 operand reads
                 tc_fence_after();
-                const uint32_t a = smem_u32(smem + s * Cfg::STAGE_BYTES);
+                const uint32_t a = sbase + s * Cfg::STAGE_BYTES;
                 const uint32_t b = a + Cfg::A_BYTES;
 #pragma unroll
                 for (int kk = 0; kk < BK / 16; ++kk)
                     mma_bf16(d, sw128_desc(a + kk * 32, 16, 1024), sw128_desc(b + kk * 32, 16, 1024), idesc,
                              (kb | kk) != 0);
                 mma_commit(empty0 + 8 * s);
+                if (++s == S) {
+                    s = 0;
+                    ph ^= 1;
+                }
             }
             mma_commit(tfull0 + 8 * acc);
         }
@@ -375,210 +326,258 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, TILED, PW>::THREADS, CPS)
 
 // ====================================================================== weight gradient
 // Partial[split][m][co] = sum over this split's voxels n of A[m][n] * B[co][n]
-//   A[m][n] = X[nbr(n, m / C)][m % C]  (m = t*C + ci; MN-major: 128 B rows per voxel)
-//   B[co][n] = dY[n][co]               (MN-major; C_out < 64 zero-padded to 64)
-template <int NB>  // N tile = padded C_out (64, 128 or 256)
+//   A[m][n] = X[nbr(n, m / C)][m % C]   (m = t*C + ci; MN-major: one 128-byte gathered row
+//                                        per voxel and 64-wide MN block)
+//   B[co][n] = dY[n][co]                 (MN-major; 2-D TMA of 64 voxel rows per block,
+//                                        C_out < 64 zero-filled out of bounds)
+// One CTA per SM: grid = splits x groups. A group owns `mpg` m-tiles whose fp32
+// accumulators (mpg * NB TMEM columns) stay resident for the CTA's whole voxel range,
+// so each dY stage is loaded once and feeds all of them (the previous one-m-tile-per-
+// CTA plan re-read dY mt = 14 times at C=64).
+template <int NB, int PW>
 struct DwCfg {
-    static constexpr int KB = 64;  // voxels per stage
-    static constexpr int STAGES = NB <= 64 ? 4 : 3;
-    static constexpr int LAG = STAGES - 1;
-    static constexpr int A_BYTES = 2 * KB * 128;  // two 64-wide MN blocks (M = 128)
+    static constexpr int KB = 64;                      // voxels per stage
+    static constexpr int A_BYTES = 2 * KB * 128;       // two 64-wide MN blocks (M = 128)
     static constexpr int B_BYTES = (NB / 64) * KB * 128;
-    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int PRODUCERS = 256;          // warps 0-7 (epilogue: warps 0-3)
-    static constexpr int THREADS = PRODUCERS + 32;  // + warp 8: TMEM allocator and MMA issuer
-    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256;
-    static constexpr int AJ = 1024 / PRODUCERS;            // A chunks per producer per stage
-    static constexpr int BJ = (NB / 64) * 512 / PRODUCERS;  // B chunks per producer per stage
+    static constexpr int BSTAGES = 2;
+    static constexpr int NBR = 2 * kNbrBytes;
+    static constexpr int BUDGET = 226 * 1024 - 1024 - 512 - 1024 - NBR - BSTAGES * B_BYTES;
+    static constexpr int STAGES = BUDGET / A_BYTES > 10 ? 10 : BUDGET / A_BYTES;
+    static constexpr int PRODUCERS = PW * 32;
+    static constexpr int THREADS = PRODUCERS + 32;  // + MMA / TMEM warp
+    static constexpr int MPG = 512 / NB;            // m-tiles whose accumulators fit TMEM
+    static constexpr int SMEM = 1024 + STAGES * A_BYTES + BSTAGES * B_BYTES + NBR + 1024 + 512;
 };
 
-template <int NB>
-__global__ void __launch_bounds__(DwCfg<NB>::THREADS)
-    k_gather_dw(FMap fm, long long rows, const bf16* __restrict__ X, int C, int K, const bf16* __restrict__ dY,
-                int Cout, int kb_per_split, float* __restrict__ partial, int Mtot, int async_arrive) {
-    using Cfg = DwCfg<NB>;
-    constexpr int S = Cfg::STAGES;
-    constexpr int LAG = Cfg::LAG;
-    constexpr int KB = Cfg::KB;
-    constexpr int AJ = Cfg::AJ, BJ = Cfg::BJ;
-    constexpr int P = Cfg::PRODUCERS;
+template <int NB, int PW>
+__global__ void __launch_bounds__(DwCfg<NB, PW>::THREADS, 1)
+    k_conv_dw(const __grid_constant__ CUtensorMap dymap, const int* __restrict__ fmap, int taps, long long rows,
+              const bf16* __restrict__ X, int C, int mt, int mpg, int tiles_per_split, int tiles,
+              float* __restrict__ partial) {
+    using Cfg = DwCfg<NB, PW>;
+    constexpr int S = Cfg::STAGES, BS = Cfg::BSTAGES;
+    constexpr int NP = Cfg::PRODUCERS;
+    constexpr int RS = NP / 8;
+    constexpr int J = 128 / RS;  // rows (of 128 = 2 blocks x 64 voxels) per thread per stage
+    static_assert(128 % RS == 0 && RS <= 64, "producer shape");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * Cfg::STAGE_BYTES);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 1);
+    uint8_t* bsm = smem + S * Cfg::A_BYTES;
+    int* nbr_s = reinterpret_cast<int*>(bsm + BS * Cfg::B_BYTES);
+    int* tab = nbr_s + 2 * kMaxTaps * BM;  // [mpg][2 blocks][8 chunks]: (t << 16 | ci) or -1
+    uint64_t* bars = reinterpret_cast<uint64_t*>(tab + 256);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 2 * BS + 3);
+    int* nbr_cnt = reinterpret_cast<int*>(tmem_slot + 2);
 
     const int tid = threadIdx.x, warp = tid >> 5;
-    const int mt = blockIdx.x, split = blockIdx.y;
-    const long long total_kb = (rows + KB - 1) / KB;
-    const long long kb_begin = (long long)split * kb_per_split;
-    const int nkb = (int)std::max<long long>(0, std::min<long long>(kb_per_split, total_kb - kb_begin));
-    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S), done = smem_u32(bars + 2 * S);
+    const int split = blockIdx.x, grp = blockIdx.y;
+    const int m0 = grp * mpg;
+    const int nm = min(mpg, mt - m0);
+    const int tile0 = split * tiles_per_split;
+    const int ntl = max(0, min(tiles_per_split, tiles - tile0));
+    const int K = taps * C;
+    const uint32_t sbase = smem_u32(smem), bbase = smem_u32(bsm);
+    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S);
+    const uint32_t bfull0 = smem_u32(bars + 2 * S), bempty0 = smem_u32(bars + 2 * S + BS);
+    const uint32_t nfull0 = smem_u32(bars + 2 * S + 2 * BS), done = nfull0 + 16;
+    const uint32_t nbr_bytes = (uint32_t)(taps * BM * 4);
 
+    for (int e = tid; e < nm * 16; e += blockDim.x) {
+        const int m = (m0 + e / 16) * 128 + ((e / 8) & 1) * 64 + (e & 7) * 8;
+        tab[e] = m < K ? ((m / C) << 16) | (m % C) : -1;
+    }
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
-            mbar_init(full0 + 8 * s, P);
+            mbar_init(full0 + 8 * s, NP);
             mbar_init(empty0 + 8 * s, 1);
         }
+        for (int s = 0; s < BS; ++s) {
+            mbar_init(bfull0 + 8 * s, 1);
+            mbar_init(bempty0 + 8 * s, 1);
+        }
+        mbar_init(nfull0, 1);
+        mbar_init(nfull0 + 8, 1);
+        nbr_cnt[0] = nbr_cnt[1] = 0;
         mbar_init(done, 1);
         mbar_init_fence();
     }
-    if (warp == 8) tmem_alloc(smem_u32(tmem_slot), tmem_cols(NB));
+    if (warp == PW) tmem_alloc(smem_u32(tmem_slot), 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp < 8) {
-        // ---------------- producers. Per-thread constants (hoisted out of the stage loop):
-        // A chunk j: MN block / voxel row / 16-byte chunk -> its swizzled smem offset, the
-        // field-map tap it reads, and its channel offset inside the gathered X row.
+    if (warp < PW) {
+        // ---------------- producers
         const int c = tid & 7;
-        const int q0 = tid >> 3;  // 0..31
-        uint32_t a_off[AJ], b_off[BJ];
-        int tap[AJ], cio[AJ], rj[AJ], b_r[BJ], b_co[BJ];
+        const int q = tid >> 3;  // rows q + RS*j of the stage's 128 (block, voxel) rows
+        const uint32_t row_bytes = (uint32_t)C * 2;
+        const uint32_t tab_s = smem_u32(tab);
+        uint32_t doff[J];
+        int vj[J];
 #pragma unroll
-        for (int j = 0; j < AJ; ++j) {
-            const int q = q0 + 32 * j;  // 0..127 = (block, voxel row)
-            const int blk = q >> 6, r = q & 63;
-            const int mm = mt * BM + blk * 64 + c * 8;
-            tap[j] = mm < K ? mm / C : -1;
-            cio[j] = mm < K ? mm - (mm / C) * C : 0;
-            rj[j] = r;
-            a_off[j] = blk * (KB * 128) + sw128_offset(r, c);
+        for (int j = 0; j < J; ++j) {
+            const int row = q + RS * j, blk = row >> 6, v = row & 63;
+            doff[j] = blk * (Cfg::KB * 128) + sw128_offset(v, c);
+            vj[j] = v;
         }
-#pragma unroll
-        for (int j = 0; j < BJ; ++j) {
-            const int q = q0 + 32 * j;
-            const int blk = q >> 6, r = q & 63;
-            b_r[j] = r;
-            b_co[j] = blk * 64 + c * 8;
-            b_off[j] = blk * (KB * 128) + sw128_offset(r, c);
-        }
-        int cur[AJ], nx1[AJ], nx2[AJ];
-        auto fetch = [&](int kb, int (&dst)[AJ]) {
-            const long long n0 = (kb_begin + kb) * KB;
-#pragma unroll
-            for (int j = 0; j < AJ; ++j) {
-                const long long n = n0 + rj[j];
-                dst[j] = (kb < nkb && tap[j] >= 0 && n < rows) ? fm_ld(fm, n, tap[j]) : -1;
-            }
+        auto request = [&](int lt, int buf) {
+            mbar_arrive_expect_tx(nfull0 + 8 * buf, nbr_bytes);
+            bulk_g2s(smem_u32(nbr_s + buf * kMaxTaps * BM), fmap + (long long)(tile0 + lt) * taps * BM, nbr_bytes,
+                     nfull0 + 8 * buf);
         };
-        auto issue = [&](int kb, const int (&use)[AJ]) {
-            const int s = kb % S;
-            if (kb >= S) mbar_wait(empty0 + 8 * s, ((kb / S) + 1) & 1);
-            const uint32_t A = smem_u32(smem + s * Cfg::STAGE_BYTES);
-            const uint32_t B = A + Cfg::A_BYTES;
-            const long long n0 = (kb_begin + kb) * KB;
+        if (tid == 0) {
+            if (ntl > 0) request(0, 0);
+            if (ntl > 1) request(1, 1);
+        }
+        int s = 0, bs = 0;
+        uint32_t ph = 0, bph = 0;
+        for (int lt = 0; lt < ntl; ++lt) {
+            const int buf = lt & 1;
+            mbar_wait_sleep(nfull0 + 8 * buf, (uint32_t)((lt >> 1) & 1));
+            const uint32_t nb = smem_u32(nbr_s + buf * kMaxTaps * BM);
+            for (int h = 0; h < 2; ++h) {
+                if (tid == 0) {  // dY rows of this half tile -> B stage (all NB/64 co blocks)
+                    mbar_wait_sleep(bempty0 + 8 * bs, bph ^ 1);
+                    mbar_arrive_expect_tx(bfull0 + 8 * bs, Cfg::B_BYTES);
+                    const int n0 = (tile0 + lt) * BM + h * 64;
 #pragma unroll
-            for (int j = 0; j < AJ; ++j) {
-                const int g = use[j];
-                const bf16* src = g >= 0 ? X + (long long)g * C + cio[j] : X;
-                cp_async16(A + a_off[j], src, g >= 0 ? 16u : 0u);
-            }
-            const bf16* dyb = dY + n0 * Cout;
-            const bool full_stage = n0 + KB <= rows;
+                    for (int cb = 0; cb < NB / 64; ++cb)
+                        tma_load2d(bbase + bs * Cfg::B_BYTES + cb * (Cfg::KB * 128), &dymap, cb * 64, n0,
+                                   bfull0 + 8 * bs);
+                }
+                if (++bs == BS) {
+                    bs = 0;
+                    bph ^= 1;
+                }
+                const uint32_t nbh = nb + h * 64 * 4;
+                for (int mi = 0; mi < nm; ++mi) {
+                    const int e0 = ld_shared_s32(tab_s + (mi * 16 + c) * 4);
+                    const int e1 = ld_shared_s32(tab_s + (mi * 16 + 8 + c) * 4);
+                    int g[J];
 #pragma unroll
-            for (int j = 0; j < BJ; ++j) {
-                const bool ok = b_co[j] < Cout && (full_stage || n0 + b_r[j] < rows);
-                const bf16* src = ok ? dyb + (long long)b_r[j] * Cout + b_co[j] : dY;
-                cp_async16(B + b_off[j], src, ok ? 16u : 0u);
-            }
-            if (async_arrive) {
-                cp_async_arrive_noinc(full0 + 8 * s);
-            } else {
-                cp_async_commit();
-                if (kb >= LAG) {
-                    cp_async_wait<LAG>();
-                    fence_proxy_async();
-                    mbar_arrive(full0 + 8 * ((kb - LAG) % S));
+                    for (int j = 0; j < J; ++j) {
+                        const int e = ((q + RS * j) >> 6) ? e1 : e0;
+                        g[j] = e >= 0 ? ld_shared_s32(nbh + ((e >> 16) * BM + vj[j]) * 4) : -1;
+                    }
+                    mbar_wait_sleep(empty0 + 8 * s, ph ^ 1);
+                    const uint32_t A = sbase + s * Cfg::A_BYTES;
+                    const char* x0 = reinterpret_cast<const char*>(X + (e0 & 0xffff));
+                    const char* x1 = reinterpret_cast<const char*>(X + (e1 & 0xffff));
+#pragma unroll
+                    for (int j = 0; j < J; ++j)
+                        cp_async16_row(A + doff[j], ((q + RS * j) >> 6) ? x1 : x0, g[j], row_bytes);
+                    cp_async_arrive_noinc(full0 + 8 * s);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1;
+                    }
                 }
             }
-        };
-        // field-map entries two stages ahead; buffers rotate by unrolling (no copies)
-        fetch(0, cur);
-        fetch(1, nx1);
-        int kb = 0;
-        for (; kb + 3 <= nkb; kb += 3) {
-            fetch(kb + 2, nx2);
-            issue(kb, cur);
-            fetch(kb + 3, cur);
-            issue(kb + 1, nx1);
-            fetch(kb + 4, nx1);
-            issue(kb + 2, nx2);
-        }
-        if (kb < nkb) {
-            fetch(kb + 2, nx2);
-            issue(kb++, cur);
-        }
-        if (kb < nkb) issue(kb++, nx1);
-        if (!async_arrive) {
-            cp_async_wait<0>();
-            fence_proxy_async();
-            for (int q = std::max(0, nkb - LAG); q < nkb; ++q) mbar_arrive(full0 + 8 * (q % S));
+            __syncwarp();
+            if ((tid & 31) == 0 && atomicAdd(&nbr_cnt[buf], 1) == PW - 1) {
+                nbr_cnt[buf] = 0;
+                if (lt + 2 < ntl) request(lt + 2, buf);
+            }
         }
 
-        // epilogue (warps 0-3 = TMEM lane quadrants): row m = (t,ci) index, columns co
+        // ---------------- epilogue (warps 0-3 = TMEM lane quadrants): row m, columns co
         if (warp < 4) {
             const int row = warp * 32 + (int)lane_id();
-            float* dst = partial + ((long long)split * Mtot + (long long)mt * BM + row) * NB;
-            if (nkb == 0) {
-#pragma unroll
-                for (int c0 = 0; c0 < NB; c0 += 4) *reinterpret_cast<float4*>(dst + c0) = make_float4(0, 0, 0, 0);
-            } else {
-                mbar_wait(done, 0);
+            if (ntl > 0) {
+                mbar_wait_sleep(done, 0);
                 tc_fence_after();
+            }
+            for (int mi = 0; mi < nm; ++mi) {
+                float* dst = partial + ((long long)split * mt * BM + (long long)(m0 + mi) * BM + row) * NB;
 #pragma unroll
                 for (int c0 = 0; c0 < NB; c0 += 16) {
-                    uint32_t v[16];
-                    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c0, v);
-                    tmem_ld_wait();
                     float f[16];
+                    if (ntl > 0) {
+                        uint32_t v[16];
+                        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + mi * NB + c0, v);
+                        tmem_ld_wait();
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(v[e]);
+                        for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(v[e]);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) f[e] = 0.0f;
+                    }
                     store_row(dst + c0, f);
                 }
             }
         }
-    } else if (tid == 8 * 32 && nkb > 0) {
+    } else if (tid == PW * 32 && ntl > 0) {
+        // ---------------- MMA issuer
         constexpr uint32_t idesc = idesc_bf16_f32(BM, NB, true, true);
-        constexpr uint32_t LBO = KB * 128;  // next 64-wide MN block
-        for (int kb = 0; kb < nkb; ++kb) {
-            const int s = kb % S;
-            mbar_wait(full0 + 8 * s, (kb / S) & 1);
-            if (async_arrive) fence_proxy_async();
-            tc_fence_after();
-            const uint32_t a = smem_u32(smem + s * Cfg::STAGE_BYTES);
-            const uint32_t b = a + Cfg::A_BYTES;
+        constexpr uint32_t LBO = Cfg::KB * 128;  // next 64-wide MN block
+        int s = 0, bs = 0;
+        uint32_t ph = 0, bph = 0;
+        for (int lt = 0; lt < ntl; ++lt) {
+            for (int h = 0; h < 2; ++h) {
+                mbar_wait(bfull0 + 8 * bs, bph);
+                const uint32_t b = bbase + bs * Cfg::B_BYTES;
+                for (int mi = 0; mi < nm; ++mi) {
+                    mbar_wait(full0 + 8 * s, ph);
+                    fence_proxy_async();
+                    tc_fence_after();
+                    const uint32_t a = sbase + s * Cfg::A_BYTES;
 #pragma unroll
-            for (int kk = 0; kk < KB / 16; ++kk)  // 16 voxels = two 8-row atoms per MMA
-                mma_bf16(tmem, sw128_desc(a + kk * 2048, LBO, 1024), sw128_desc(b + kk * 2048, LBO, 1024), idesc,
-                         (kb | kk) != 0);
-            mma_commit(empty0 + 8 * s);
+                    for (int kk = 0; kk < Cfg::KB / 16; ++kk)  // 16 voxels = two 8-row atoms per MMA
+                        mma_bf16(tmem + mi * NB, sw128_desc(a + kk * 2048, LBO, 1024),
+                                 sw128_desc(b + kk * 2048, LBO, 1024), idesc, (lt | h | kk) != 0);
+                    mma_commit(empty0 + 8 * s);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+                mma_commit(bempty0 + 8 * bs);
+                if (++bs == BS) {
+                    bs = 0;
+                    bph ^= 1;
+                }
+            }
         }
         mma_commit(done);
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 8) {
+    if (warp == PW) {
         __syncwarp();
         tc_fence_after();
-        tmem_dealloc(tmem, tmem_cols(NB));
+        tmem_dealloc(tmem, 512);
     }
 }
 
-// dW_ref[co][ci*taps + t] = sum_split partial[split][t*C + ci][co]  (fixed split order)
-__global__ void k_reduce_dw(const float* __restrict__ partial, int splits, int Mtot, int NB, int taps, int C,
+// dW_ref[co][ci*taps + t] = sum_split partial[split][t*C + ci][co]  (fixed split order).
+// Thread i -> (m, co) with co fastest: the partial reads are coalesced.
+__global__ void k_reduce_dw(const float* __restrict__ partial, int splits, long long Mtot, int NB, int taps, int C,
                             int Cout, float* __restrict__ dw) {
-    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // over Cout * C * taps (ref order)
-    const long long total = (long long)Cout * C * taps;
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // over (taps*C) x Cout
+    const long long total = (long long)taps * C * Cout;
     if (i >= total) return;
-    const int co = (int)(i / (C * taps));
-    const int rem = (int)(i % (C * taps));
-    const int ci = rem / taps, t = rem % taps;
-    const long long m = (long long)t * C + ci;
+    const long long m = i / Cout;
+    const int co = (int)(i - m * Cout);
+    const int t = (int)(m / C), ci = (int)(m - (long long)t * C);
     float acc = 0.0f;
     for (int s = 0; s < splits; ++s) acc += partial[((long long)s * Mtot + m) * NB + co];
-    dw[i] = acc;
+    dw[(long long)co * C * taps + (long long)ci * taps + t] = acc;
+}
+
+// Row-major [n][taps] (layout 0) or tap-major [taps][n] (layout 1) -> tile-major
+// [ceil(n/128)][taps][128] with -1 padding (the layout both kernels consume).
+__global__ void k_retile(const int* __restrict__ src, int layout, long long n, int taps, int* __restrict__ dst) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // over padded n x taps (tile-major)
+    const long long padded = (n + 127) / 128 * 128;
+    if (i >= padded * taps) return;
+    const long long tile = i / (taps * 128);
+    const int rem = (int)(i - tile * taps * 128);
+    const int t = rem / 128;
+    const long long col = tile * 128 + (rem & 127);
+    int v = -1;
+    if (col < n) v = layout == 0 ? src[col * taps + t] : src[(long long)t * n + col];
+    dst[i] = v;
 }
 
 // ====================================================================== layout helpers
@@ -644,84 +643,67 @@ __global__ void k_to_channel_major(const T* __restrict__ in, long long N, long l
     }
 }
 
+
 // ====================================================================== launchers
-template <int BN, int CPS, bool TILED, typename OutT, int PW = 4>
-void launch_gg_cps(const FMap& fm, long long rows, const bf16* X, int C, int K, const bf16* Wp, int Kp, OutT* Y,
-                   cudaStream_t s) {
-    using Cfg = FwdCfg<BN, CPS, TILED, PW>;
-    auto kern = k_gather_gemm<BN, CPS, TILED, OutT, PW>;
+// Forward variant: HCB_FWD_CPS = CTAs per SM (2: BN <= 64 only, so both CTAs'
+// double-buffered accumulators fit TMEM; 1: one deep ring), HCB_FWD_PW = producer warps
+// (4, 8 or 16).
+template <int BN, int CPS, int PW, typename OutT>
+void launch_fwd(const int* fmap, int taps, long long rows, const bf16* X, int C, const bf16* Wp, int Kp, OutT* Y,
+                cudaStream_t s) {
+    using Cfg = FwdCfg<BN, CPS, PW>;
+    auto kern = k_conv_fwd<BN, CPS, PW, OutT>;
     static bool attr = false;  // per instantiation
     if (!attr) {
         cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM), "smem attr");
         attr = true;
     }
+    const CUtensorMap wm = map2d(Wp, (uint64_t)Kp, (uint64_t)BN, (uint64_t)Kp * 2, BN);
     const int tiles = (int)((rows + BM - 1) / BM);
     const int grid = std::min(tiles, CPS * num_sms());
-    kern<<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(fm, rows, X, C, K, Wp, Kp, Y, tiles, TILED ? async_arrive() : 0);
+    kern<<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(wm, fmap, taps, rows, X, C, Kp / BK, Y, tiles);
     launched("conv gather-GEMM (tcgen05)");
 }
 
-// Two resident CTAs per SM (twice the producer warps) whenever the ring still gets >= 3
-// stages and the two CTAs' double-buffered TMEM accumulators fit (2 * 2 * BN <= 512);
-// HCB_FWD_CPS=1 forces one.
-int fwd_env_cps() {
-    static int env = -1;
-    if (env < 0) {
-        const char* e = std::getenv("HCB_FWD_CPS");
-        env = e ? std::atoi(e) : 0;
-    }
-    return env;
-}
-
-// Variant choice: the bulk-staged (TILED) producer when the map is tile-major and two
-// CTAs per SM still get a >= 3-stage ring; otherwise the register-prefetch producer with
-// two CTAs per SM; one CTA per SM only when nothing else fits (BN = 256).
-// HCB_FWD_VARIANT=1 forces the register-prefetch producer (A/B experiments).
 template <int BN, typename OutT>
-void launch_gg(const FMap& fm, long long rows, const bf16* X, int C, int K, const bf16* Wp, int Kp, OutT* Y,
-               cudaStream_t s) {
-    constexpr bool tiled_two = BN <= 128 && FwdCfg<BN, 2, true>::STAGES >= 3;
-    constexpr bool reg_two = BN <= 128 && FwdCfg<BN, 2, false>::STAGES >= 3;
-    static int variant = -1;
-    if (variant < 0) {
-        const char* e = std::getenv("HCB_FWD_VARIANT");
-        variant = e ? std::atoi(e) : 0;
-    }
-    const bool one = fwd_env_cps() == 1;
-    if constexpr (tiled_two) {
-        if (fm.tiled && variant != 1 && !one) {
-            if (fwd_pw() == 8) return launch_gg_cps<BN, 2, true, OutT, 8>(fm, rows, X, C, K, Wp, Kp, Y, s);
-            return launch_gg_cps<BN, 2, true, OutT, 4>(fm, rows, X, C, K, Wp, Kp, Y, s);
+void launch_fwd_bn(const int* fmap, int taps, long long rows, const bf16* X, int C, const bf16* Wp, int Kp, OutT* Y,
+                   cudaStream_t s) {
+    // Defaults measured on B200 at 256^3 x 8 shells (scripts/gpu_ab.sh): two CTAs per SM
+    // with 4 producer warps each wherever both CTAs' accumulators fit (BN <= 64), else one
+    // CTA with 4 producer warps.
+    static const int cps = env_int("HCB_FWD_CPS", 2);
+    static const int pw = env_int("HCB_FWD_PW", 4);
+    if constexpr (BN <= 64) {
+        if (cps == 2) {
+            if (pw == 4) return launch_fwd<BN, 2, 4>(fmap, taps, rows, X, C, Wp, Kp, Y, s);
+            return launch_fwd<BN, 2, 8>(fmap, taps, rows, X, C, Wp, Kp, Y, s);
         }
     }
-    if constexpr (reg_two) {
-        if (!one) return launch_gg_cps<BN, 2, false>(fm, rows, X, C, K, Wp, Kp, Y, s);
-    }
-    if (fm.tiled && variant != 1) return launch_gg_cps<BN, 1, true>(fm, rows, X, C, K, Wp, Kp, Y, s);
-    launch_gg_cps<BN, 1, false>(fm, rows, X, C, K, Wp, Kp, Y, s);
+    if (pw == 4) return launch_fwd<BN, 1, 4>(fmap, taps, rows, X, C, Wp, Kp, Y, s);
+    if (pw == 16) return launch_fwd<BN, 1, 16>(fmap, taps, rows, X, C, Wp, Kp, Y, s);
+    launch_fwd<BN, 1, 8>(fmap, taps, rows, X, C, Wp, Kp, Y, s);
 }
 
 template <typename OutT>
-void gather_gemm(const FMap& fm, long long rows, const bf16* X, int C, int K, const bf16* Wp, int Kp, int N, OutT* Y,
-                 cudaStream_t s) {
-    if (fm.tiled && gather_gemm_tma_supported(C, N)) {  // TMA gather4 producers (conv_tma.cu)
-        gather_gemm_tma<OutT>(fm.p, fm.taps, rows, X, C, Wp, Kp, N, Y, s);
-        return;
-    }
+void conv_fwd(const int* fmap, int taps, long long rows, const bf16* X, int C, const bf16* Wp, int Kp, int N, OutT* Y,
+              cudaStream_t s) {
     switch (N) {
-        case 16: launch_gg<16>(fm, rows, X, C, K, Wp, Kp, Y, s); break;
-        case 32: launch_gg<32>(fm, rows, X, C, K, Wp, Kp, Y, s); break;
-        case 64: launch_gg<64>(fm, rows, X, C, K, Wp, Kp, Y, s); break;
-        case 128: launch_gg<128>(fm, rows, X, C, K, Wp, Kp, Y, s); break;
-        case 256: launch_gg<256>(fm, rows, X, C, K, Wp, Kp, Y, s); break;
+        case 16: launch_fwd_bn<16>(fmap, taps, rows, X, C, Wp, Kp, Y, s); break;
+        case 32: launch_fwd_bn<32>(fmap, taps, rows, X, C, Wp, Kp, Y, s); break;
+        case 64: launch_fwd_bn<64>(fmap, taps, rows, X, C, Wp, Kp, Y, s); break;
+        case 128: launch_fwd_bn<128>(fmap, taps, rows, X, C, Wp, Kp, Y, s); break;
+        case 256: launch_fwd_bn<256>(fmap, taps, rows, X, C, Wp, Kp, Y, s); break;
         default: throw std::invalid_argument("native conv: output channels must be 16, 32, 64, 128 or 256");
     }
 }
 
 int dw_nb(int cout) { return cout <= 64 ? 64 : cout <= 128 ? 128 : 256; }
 
+// Split plan: m-tiles are grouped so each group's accumulators fit TMEM (mpg * NB <= 512
+// columns), groups balanced; the voxel tiles are split so groups x splits fills every SM
+// once (one CTA per SM). Deterministic for a given SM count.
 struct DwPlan {
-    int nb, mt, splits, kbps;
+    int nb, mt, groups, mpg, splits, tps, tiles;
     long long partial_floats;
 };
 
@@ -729,32 +711,43 @@ DwPlan dw_plan(long long rows, int taps, int cin, int cout) {
     DwPlan p{};
     p.nb = dw_nb(cout);
     p.mt = (taps * cin + BM - 1) / BM;
-    const long long total_kb = (rows + 63) / 64;
-    const int smem = p.nb <= 64 ? DwCfg<64>::SMEM : p.nb <= 128 ? DwCfg<128>::SMEM : DwCfg<256>::SMEM;
-    const int per_sm = smem <= 113 * 1024 ? 2 : 1;  // resident CTAs per SM (shared-memory bound)
-    const int slots = num_sms() * per_sm;
-    // one wave: mt * splits <= resident slots
-    int want = std::max(1, slots / p.mt);
-    want = (int)std::min<long long>(want, std::max<long long>(1, total_kb));
-    p.kbps = (int)((total_kb + want - 1) / want);
-    p.splits = (int)((total_kb + p.kbps - 1) / p.kbps);
+    const int cap = 512 / p.nb;
+    p.groups = (p.mt + cap - 1) / cap;
+    p.mpg = (p.mt + p.groups - 1) / p.groups;
+    p.tiles = (int)((rows + BM - 1) / BM);
+    const int want = std::max(1, std::min(p.tiles, num_sms() / p.groups));
+    p.tps = (p.tiles + want - 1) / want;
+    p.splits = std::max(1, (p.tiles + p.tps - 1) / p.tps);
     p.partial_floats = (long long)p.splits * p.mt * BM * p.nb;
     return p;
 }
 
-template <int NB>
-void launch_dw(const DwPlan& p, const FMap& fm, long long rows, const bf16* X, int C, int K, const bf16* dY, int Cout,
-               float* partial, cudaStream_t s) {
-    using Cfg = DwCfg<NB>;
-    auto kern = k_gather_dw<NB>;
+template <int NB, int PW>
+void launch_dw_pw(const DwPlan& p, const int* fmap, int taps, long long rows, const bf16* X, int C, const bf16* dY,
+                  int Cout, float* partial, cudaStream_t s) {
+    using Cfg = DwCfg<NB, PW>;
+    auto kern = k_conv_dw<NB, PW>;
     static bool attr = false;
     if (!attr) {
         cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM), "smem attr");
         attr = true;
     }
-    dim3 g((unsigned)p.mt, (unsigned)p.splits);
-    kern<<<g, Cfg::THREADS, Cfg::SMEM, s>>>(fm, rows, X, C, K, dY, Cout, p.kbps, partial, p.mt * BM, async_arrive());
+    // dY [rows][Cout] bf16: boxes of 64 voxels x 64 channels; channels >= Cout and voxels
+    // >= rows are out of bounds -> zero.
+    const CUtensorMap dm = map2d(dY, (uint64_t)Cout, (uint64_t)rows, (uint64_t)Cout * 2, 64);
+    dim3 g((unsigned)p.splits, (unsigned)p.groups);
+    kern<<<g, Cfg::THREADS, Cfg::SMEM, s>>>(dm, fmap, taps, rows, X, C, p.mt, p.mpg, p.tps, p.tiles, partial);
     launched("conv dW gather-GEMM (tcgen05)");
+}
+
+// HCB_DW_PW = producer warps of the dW kernel (4, 8 or 16; default 8).
+template <int NB>
+void launch_dw(const DwPlan& p, const int* fmap, int taps, long long rows, const bf16* X, int C, const bf16* dY,
+               int Cout, float* partial, cudaStream_t s) {
+    static const int pw = env_int("HCB_DW_PW", 8);
+    if (pw == 4) return launch_dw_pw<NB, 4>(p, fmap, taps, rows, X, C, dY, Cout, partial, s);
+    if (pw == 16) return launch_dw_pw<NB, 16>(p, fmap, taps, rows, X, C, dY, Cout, partial, s);
+    launch_dw_pw<NB, 8>(p, fmap, taps, rows, X, C, dY, Cout, partial, s);
 }
 
 void check_native(int cin, int cout, int taps) {
@@ -763,12 +756,24 @@ void check_native(int cin, int cout, int taps) {
     if (taps < 1 || taps > 27) throw std::invalid_argument("native conv: 1..27 field taps supported");
 }
 
-FMap make_fmap(const int32_t* fmap, int32_t layout, long long n, int taps) {
-    if (layout == 2) return FMap{fmap, 0, 0, 1, taps};
-    if (layout == 1) return FMap{fmap, 1, n, 0, taps};
-    if (layout != 0) throw std::invalid_argument("native conv: unknown field-map layout");
-    return FMap{fmap, taps, 1, 0, taps};
-}
+// The kernels consume the tile-major map; the row-major / tap-major layouts are
+// re-tiled into stream-ordered scratch first.
+struct TiledMap {
+    const int* p;
+    Scratch* tmp;
+    TiledMap(const int32_t* fmap, int32_t layout, long long n, int taps, cudaStream_t s) : p(fmap), tmp(nullptr) {
+        if (layout == 2) return;
+        if (layout != 0 && layout != 1) throw std::invalid_argument("native conv: unknown field-map layout");
+        const long long total = (n + 127) / 128 * 128 * taps;
+        tmp = new Scratch((size_t)total * 4, s);
+        k_retile<<<grid_for(total, 256), 256, 0, s>>>(fmap, layout, n, taps, tmp->as<int>());
+        launched("field map re-tile");
+        p = tmp->as<int>();
+    }
+    ~TiledMap() { delete tmp; }
+    TiledMap(const TiledMap&) = delete;
+    TiledMap& operator=(const TiledMap&) = delete;
+};
 
 }  // namespace
 }  // namespace hcb
@@ -798,15 +803,15 @@ hc_status hc_native_gather_gemm(const int32_t* fmap, int32_t fmap_layout, int64_
     return guard([&] {
         check_native(c_in, c_out, taps);
         if (n_out <= 0) return;
-        const int Kp = (int)hc_native_packed_k(c_in, taps);
-        const FMap fm = make_fmap(fmap, fmap_layout, n_out, taps);
         cudaStream_t s = as_stream(stream);
+        const int Kp = (int)hc_native_packed_k(c_in, taps);
+        const TiledMap fm(fmap, fmap_layout, n_out, taps, s);
         const bf16* X = static_cast<const bf16*>(x);
         const bf16* W = static_cast<const bf16*>(w_packed);
         if (y_dtype == HC_DTYPE_F32)
-            gather_gemm<float>(fm, n_out, X, c_in, taps * c_in, W, Kp, c_out, static_cast<float*>(y), s);
+            conv_fwd<float>(fm.p, taps, n_out, X, c_in, W, Kp, c_out, static_cast<float*>(y), s);
         else
-            gather_gemm<bf16>(fm, n_out, X, c_in, taps * c_in, W, Kp, c_out, static_cast<bf16*>(y), s);
+            conv_fwd<bf16>(fm.p, taps, n_out, X, c_in, W, Kp, c_out, static_cast<bf16*>(y), s);
     });
 }
 
@@ -830,16 +835,17 @@ hc_status hc_native_conv_dw(const int32_t* fmap, int32_t fmap_layout, int64_t n_
             return;
         }
         float* part = static_cast<float*>(workspace);
-        const FMap fm = make_fmap(fmap, fmap_layout, n_out, taps);
+        const TiledMap fm(fmap, fmap_layout, n_out, taps, s);
         const bf16* X = static_cast<const bf16*>(x);
         const bf16* DY = static_cast<const bf16*>(dy);
         switch (p.nb) {
-            case 64: launch_dw<64>(p, fm, n_out, X, c_in, taps * c_in, DY, c_out, part, s); break;
-            case 128: launch_dw<128>(p, fm, n_out, X, c_in, taps * c_in, DY, c_out, part, s); break;
-            default: launch_dw<256>(p, fm, n_out, X, c_in, taps * c_in, DY, c_out, part, s); break;
+            case 64: launch_dw<64>(p, fm.p, taps, n_out, X, c_in, DY, c_out, part, s); break;
+            case 128: launch_dw<128>(p, fm.p, taps, n_out, X, c_in, DY, c_out, part, s); break;
+            default: launch_dw<256>(p, fm.p, taps, n_out, X, c_in, DY, c_out, part, s); break;
         }
         const long long total = (long long)c_out * c_in * taps;
-        k_reduce_dw<<<grid_for(total, 256), 256, 0, s>>>(part, p.splits, p.mt * BM, p.nb, taps, c_in, c_out, dw_ref);
+        k_reduce_dw<<<grid_for(total, 256), 256, 0, s>>>(part, p.splits, (long long)p.mt * BM, p.nb, taps, c_in,
+                                                          c_out, dw_ref);
         launched("dW split reduction");
     });
 }

@@ -59,10 +59,52 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         : "memory");
 }
 
+// Same wait with a suspend-time hint: the thread sleeps in hardware until the phase
+// completes (or the hint expires) instead of re-issuing try_wait every few cycles.
+// Used by warps that wait long (producers on a full ring, epilogue on a whole tile) so
+// they do not steal issue slots from the warps doing work.
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "HC_WAITS:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+        "@P1 bra HC_DONES;\n"
+        "bra HC_WAITS;\n"
+        "HC_DONES:\n"
+        "}\n" ::"r"(bar),
+        "r"(parity), "r"(1000000u)
+        : "memory");
+}
+
+// 2-D tiled TMA load (box and swizzle from the tensor map), completion counted on an mbarrier.
+__device__ __forceinline__ void tma_load2d(uint32_t dst, const void* map, int c0, int c1, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(map), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
+
 // ------------------------------------------------------------------ cp.async
 // 16-byte global->shared copy; src_bytes = 0 zero-fills the destination.
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+// Gather form: row `g` (>= 0) of a row-major array with `row_bytes` per row, plus a byte
+// offset; g < 0 zero-fills. One IMAD.WIDE for the address, no branches.
+__device__ __forceinline__ void cp_async16_row(uint32_t dst, const char* base, int g, uint32_t row_bytes) {
+    const char* src = base + (unsigned long long)(unsigned)max(g, 0) * row_bytes;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(g >= 0 ? 16u : 0u)
+                 : "memory");
+}
+// 32-bit shared load by address (volatile: stays ordered after the mbarrier wait that
+// published the data, but — unlike a "memory"-clobbering asm — lets the compiler batch
+// several of these ahead of the cp.async that consume them).
+__device__ __forceinline__ int ld_shared_s32(uint32_t addr) {
+    int v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 // Arrive on an mbarrier once ALL of this thread's prior cp.async copies have landed

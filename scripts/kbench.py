@@ -32,6 +32,7 @@ def main():
     cs = [int(a) for a in sys.argv[1:]] or [16, 64, 128]
     lv = bench.shell_levels(256)
     s = SuperPsh.from_levels([lv[0]] * 8)
+    tag = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("HCB_"))
     n = s.total_columns()
     for c in cs:
         spec = ConvSpec(3, 1, 0, c, c)
@@ -39,12 +40,12 @@ def main():
         x = (torch.rand((n, c), device="cuda") * 2 - 1).to(torch.bfloat16)
         w = torch.rand((c, c * 27), device="cuda") * 2 - 1
         wp = conv.pack_weights(w, c, c, 27, False)
-        for name, lay in (("tap", conv.TAP_MAJOR), ("tiled", conv.TILED)):
+        for name, lay in (("tiled", conv.TILED),):
             fm = conv.field_map_native(s, s, spec, lay)
             t_map = timeit(lambda: conv.field_map_native(s, s, spec, lay))
             t_fwd = timeit(lambda: conv.gather_gemm(fm, x, wp, c, torch.bfloat16))
             t_dw = timeit(lambda: conv.conv_dw(fm, x, x))
-            print(f"C={c:4d} {name:6s} map {t_map:.3f} ms | fwd {t_fwd:.3f} ms {fl / t_fwd / 1e9:7.1f} TF/s"
+            print(f"[{tag}] C={c:4d} {name:6s} map {t_map:.3f} ms | fwd {t_fwd:.3f} ms {fl / t_fwd / 1e9:7.1f} TF/s"
                   f" | dW {t_dw:.3f} ms {fl / t_dw / 1e9:7.1f} TF/s", flush=True)
 
 
