@@ -285,9 +285,10 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, PW>::THREADS, CPS)
                 }
             }
         }
-    } else if (tid == (PW + 4) * 32) {
-        // ---------------- MMA issuer (single thread)
+    } else if (warp == PW + 4) {
+        // ---------------- MMA issuer: warp-uniform loop, one elected lane issues
         constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, false, false);
+        const uint64_t a0 = sw128_desc(sbase, 16, 1024), b0 = sw128_desc(sbase + Cfg::A_BYTES, 16, 1024);
         int s = 0;
         uint32_t ph = 0;
         int i = 0;
@@ -300,19 +301,21 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, PW>::THREADS, CPS)
                 mbar_wait(full0 + 8 * s, ph);
                 fence_proxy_async();  // cp.async (generic proxy) writes -> tcgen05 operand reads
                 tc_fence_after();
-                const uint32_t a = sbase + s * Cfg::STAGE_BYTES;
-                const uint32_t b = a + Cfg::A_BYTES;
+                if (elect_one()) {
+                    const uint64_t so = (uint64_t)((s * Cfg::STAGE_BYTES) >> 4);  // descriptor start-address units
 #pragma unroll
-                for (int kk = 0; kk < BK / 16; ++kk)
-                    mma_bf16(d, sw128_desc(a + kk * 32, 16, 1024), sw128_desc(b + kk * 32, 16, 1024), idesc,
-                             (kb | kk) != 0);
-                mma_commit(empty0 + 8 * s);
+                    for (int kk = 0; kk < BK / 16; ++kk)
+                        mma_bf16(d, a0 + so + 2 * kk, b0 + so + 2 * kk, idesc, (kb | kk) != 0);
+                    mma_commit(empty0 + 8 * s);
+                }
+                __syncwarp();
                 if (++s == S) {
                     s = 0;
                     ph ^= 1;
                 }
             }
-            mma_commit(tfull0 + 8 * acc);
+            if (elect_one()) mma_commit(tfull0 + 8 * acc);
+            __syncwarp();
         }
     }
     tc_fence_before();
@@ -507,39 +510,45 @@ __global__ void __launch_bounds__(DwCfg<NB, PW>::THREADS, 1)
                 }
             }
         }
-    } else if (tid == PW * 32 && ntl > 0) {
-        // ---------------- MMA issuer
+    } else if (warp == PW && ntl > 0) {
+        // ---------------- MMA issuer: warp-uniform loop, one elected lane issues
         constexpr uint32_t idesc = idesc_bf16_f32(BM, NB, true, true);
         constexpr uint32_t LBO = Cfg::KB * 128;  // next 64-wide MN block
+        const uint64_t a0 = sw128_desc(sbase, LBO, 1024), b0 = sw128_desc(bbase, LBO, 1024);
         int s = 0, bs = 0;
         uint32_t ph = 0, bph = 0;
         for (int lt = 0; lt < ntl; ++lt) {
             for (int h = 0; h < 2; ++h) {
                 mbar_wait(bfull0 + 8 * bs, bph);
-                const uint32_t b = bbase + bs * Cfg::B_BYTES;
+                const uint64_t bo = (uint64_t)((bs * Cfg::B_BYTES) >> 4);
                 for (int mi = 0; mi < nm; ++mi) {
                     mbar_wait(full0 + 8 * s, ph);
                     fence_proxy_async();
                     tc_fence_after();
-                    const uint32_t a = sbase + s * Cfg::A_BYTES;
+                    if (elect_one()) {
+                        const uint64_t ao = (uint64_t)((s * Cfg::A_BYTES) >> 4);
 #pragma unroll
-                    for (int kk = 0; kk < Cfg::KB / 16; ++kk)  // 16 voxels = two 8-row atoms per MMA
-                        mma_bf16(tmem + mi * NB, sw128_desc(a + kk * 2048, LBO, 1024),
-                                 sw128_desc(b + kk * 2048, LBO, 1024), idesc, (lt | h | kk) != 0);
-                    mma_commit(empty0 + 8 * s);
+                        for (int kk = 0; kk < Cfg::KB / 16; ++kk)  // 16 voxels = two 8-row atoms per MMA
+                            mma_bf16(tmem + mi * NB, a0 + ao + 128 * kk, b0 + bo + 128 * kk, idesc,
+                                     (lt | h | kk) != 0);
+                        mma_commit(empty0 + 8 * s);
+                    }
+                    __syncwarp();
                     if (++s == S) {
                         s = 0;
                         ph ^= 1;
                     }
                 }
-                mma_commit(bempty0 + 8 * bs);
+                if (elect_one()) mma_commit(bempty0 + 8 * bs);
+                __syncwarp();
                 if (++bs == BS) {
                     bs = 0;
                     bph ^= 1;
                 }
             }
         }
-        mma_commit(done);
+        if (elect_one()) mma_commit(done);
+        __syncwarp();
     }
     tc_fence_before();
     __syncthreads();
