@@ -1,10 +1,12 @@
-# full evidence pass: gpu tests, smoke, bench line, launch list, ncu full capture
+# full evidence pass: gpu tests, smoke, bench line, reference arm, kernel tables, launch list, ncu full capture
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -2 gpurun_out/smoke.log
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; cat gpurun_out/bench.json; tail -2 gpurun_out/bench.err
-timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2>&1; echo "ref rc=$?"; cat gpurun_out/bench_ref.json | tail -c 600
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2>&1; echo "ref rc=$?"; tail -c 300 gpurun_out/bench_ref.json
+for c in 16 64 128; do timeout 300 python scripts/kbench.py $c >> gpurun_out/kbench.txt 2>&1; done; cat gpurun_out/kbench.txt
+for c in 16 64 256; do timeout 300 python scripts/kbench_ref.py $c > gpurun_out/kbench_ref_c$c.txt 2>&1; grep "C=" gpurun_out/kbench_ref_c$c.txt; done
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
-  python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > /dev/null 2>&1; echo "ncu list rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_gather|k_field_map_tiled" -s 6 -c 4 \
-  -o gpurun_out/prof_round python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_round.log 2>&1; echo "ncu full rc=$?"
+  python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1; echo "ncu list rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_conv|k_field_map_tiled" -s 8 -c 4 \
+  -o gpurun_out/prof_round python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_round.log 2>&1; echo "ncu full rc=$?"

@@ -12,7 +12,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-OP_OF = {"k_field_map": "field_map", "k_gather_dw": "dW_conv", "k_gather_gemm": "fwd_conv",
+OP_OF = {"k_field_map": "field_map", "k_conv_dw": "dW_conv", "k_conv_fwd": "fwd_conv",
          "k_hash2col": "hash2col", "k_col2hash": "col2hash"}
 METRICS = [
     ("gpu__time_duration.sum", "time"),
@@ -32,7 +32,7 @@ METRICS = [
 def scale(v, unit):
     u = unit.strip().lower()
     mult = {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0,
-            "second": 1e3}
+            "second": 1e3, "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}
     return v * mult.get(u, 1.0)
 
 
