@@ -379,34 +379,50 @@ __global__ void k_col2hash_any(DevPsh in, DevPsh out, int F, int S, int pad, int
 // ============================================================== pooling
 // cnn_ops.cpp:234-284 max_pool: first present tap seeds, strict '>' (ties keep
 // the smallest field row); empty field -> 0 / -1.
-template <int F>
-__global__ void k_max_pool(DevPsh in, DevPsh out, int S, int pad, const float* __restrict__ data, int C,
-                           float* __restrict__ res, int* __restrict__ sw) {
+// Channels are processed CB at a time with all (tap, channel) loads issued before any
+// compare, so each thread keeps CB*F^3 independent gathers in flight (a per-channel loop
+// is one dependent latency chain per channel). Per channel the taps are still visited in
+// row order with the same seed/tie rule -> bit-identical results.
+template <int F, int CB>
+__global__ void __launch_bounds__(256) k_max_pool(DevPsh in, DevPsh out, int S, int pad,
+                                                  const float* __restrict__ data, int C, float* __restrict__ res,
+                                                  int* __restrict__ sw) {
+    constexpr int T = F * F * F;
     const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (col >= out.N) return;
     const int4 c = out.cols[col];
     const ModelParam mp = in.models[c.w - 1];
-    const int fd = in.dim == 3 ? F * F * F : F * F;
-    int nb[F * F * F];
+    const int fd = in.dim == 3 ? T : F * F;
+    int nb[T];
     probe_field<F>(in, mp, origin_axis(c.x, F, S, pad), origin_axis(c.y, F, S, pad),
                    origin_axis(c.z, F, S, pad), nb);
-    const long long Nin = in.N, Nout = out.N;
-    for (int ch = 0; ch < C; ++ch) {
-        const float* src = data + ch * Nin;
-        float best = 0.0f;
-        int arg = -1;
 #pragma unroll
-        for (int t = 0; t < F * F * F; ++t) {
-            if (t < fd && nb[t] >= 0) {
-                const float v = __ldg(src + nb[t]);
-                if (arg < 0 || v > best) {
-                    best = v;
+    for (int t = 0; t < T; ++t)
+        if (t >= fd) nb[t] = -1;
+    const long long Nin = in.N, Nout = out.N;
+    for (int ch0 = 0; ch0 < C; ch0 += CB) {
+        float v[CB][T];
+#pragma unroll
+        for (int u = 0; u < CB; ++u) {
+            const float* src = data + (long long)min(ch0 + u, C - 1) * Nin;
+#pragma unroll
+            for (int t = 0; t < T; ++t) v[u][t] = nb[t] >= 0 ? __ldg(src + nb[t]) : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < CB; ++u) {
+            if (ch0 + u >= C) break;
+            float best = 0.0f;
+            int arg = -1;
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+                if (nb[t] >= 0 && (arg < 0 || v[u][t] > best)) {
+                    best = v[u][t];
                     arg = t;
                 }
             }
+            res[(long long)(ch0 + u) * Nout + col] = arg < 0 ? 0.0f : best;
+            sw[(long long)(ch0 + u) * Nout + col] = arg;
         }
-        res[ch * Nout + col] = arg < 0 ? 0.0f : best;
-        sw[ch * Nout + col] = arg;
     }
 }
 
@@ -435,26 +451,42 @@ __global__ void k_max_pool_any(DevPsh in, DevPsh out, int F, int S, int pad, int
     }
 }
 
-// cnn_ops.cpp:286-322 avg_pool: (sum over present taps, row order) * inv_fd
-template <int F>
-__global__ void k_avg_pool(DevPsh in, DevPsh out, int S, int pad, const float* __restrict__ data, int C, float inv,
-                           float* __restrict__ res) {
+// cnn_ops.cpp:286-322 avg_pool: (sum over present taps, row order) * inv_fd; CB channels
+// per pass with independent loads (see k_max_pool).
+template <int F, int CB>
+__global__ void __launch_bounds__(256) k_avg_pool(DevPsh in, DevPsh out, int S, int pad,
+                                                  const float* __restrict__ data, int C, float inv,
+                                                  float* __restrict__ res) {
+    constexpr int T = F * F * F;
     const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (col >= out.N) return;
     const int4 c = out.cols[col];
     const ModelParam mp = in.models[c.w - 1];
-    const int fd = in.dim == 3 ? F * F * F : F * F;
-    int nb[F * F * F];
+    const int fd = in.dim == 3 ? T : F * F;
+    int nb[T];
     probe_field<F>(in, mp, origin_axis(c.x, F, S, pad), origin_axis(c.y, F, S, pad),
                    origin_axis(c.z, F, S, pad), nb);
-    const long long Nin = in.N, Nout = out.N;
-    for (int ch = 0; ch < C; ++ch) {
-        const float* src = data + ch * Nin;
-        float acc = 0.0f;
 #pragma unroll
-        for (int t = 0; t < F * F * F; ++t)
-            if (t < fd && nb[t] >= 0) acc = __fadd_rn(acc, __ldg(src + nb[t]));
-        res[ch * Nout + col] = __fmul_rn(acc, inv);
+    for (int t = 0; t < T; ++t)
+        if (t >= fd) nb[t] = -1;
+    const long long Nin = in.N, Nout = out.N;
+    for (int ch0 = 0; ch0 < C; ch0 += CB) {
+        float v[CB][T];
+#pragma unroll
+        for (int u = 0; u < CB; ++u) {
+            const float* src = data + (long long)min(ch0 + u, C - 1) * Nin;
+#pragma unroll
+            for (int t = 0; t < T; ++t) v[u][t] = nb[t] >= 0 ? __ldg(src + nb[t]) : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < CB; ++u) {
+            if (ch0 + u >= C) break;
+            float acc = 0.0f;
+#pragma unroll
+            for (int t = 0; t < T; ++t)
+                if (nb[t] >= 0) acc = __fadd_rn(acc, v[u][t]);
+            res[(long long)(ch0 + u) * Nout + col] = __fmul_rn(acc, inv);
+        }
     }
 }
 
@@ -479,9 +511,12 @@ __global__ void k_avg_pool_any(DevPsh in, DevPsh out, int F, int S, int pad, int
 // ============================================================== unpooling
 // cnn_ops.cpp:336-372 max_unpool: out[c,g] = 0 (+) coarse[c,col] for covering
 // outputs whose switch equals g's field row, ascending output order.
-template <int KMAX, bool AVG>
-__global__ void k_unpool(DevPsh fine, DevPsh coarse, int F, int S, int pad, const float* __restrict__ cd,
-                         const int* __restrict__ sw, int C, float inv, float* __restrict__ res) {
+// CB channels per pass: the switch and value loads of all CB channels are issued before
+// any compare (the per-channel form serialised a switch load -> value load chain per channel).
+template <int KMAX, bool AVG, int CB>
+__global__ void __launch_bounds__(256) k_unpool(DevPsh fine, DevPsh coarse, int F, int S, int pad,
+                                                const float* __restrict__ cd, const int* __restrict__ sw, int C,
+                                                float inv, float* __restrict__ res) {
     const long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (gi >= fine.N) return;
     const int4 c = fine.cols[gi];
@@ -489,17 +524,31 @@ __global__ void k_unpool(DevPsh fine, DevPsh coarse, int F, int S, int pad, cons
     int hcol[KMAX], hrow[KMAX];
     const int n = cover_hits<1>(coarse, mp, c.x, c.y, c.z, F, S, pad, hcol, hrow);
     const long long Nc = coarse.N, Nf = fine.N;
-    for (int ch = 0; ch < C; ++ch) {
-        float acc = 0.0f;
+    for (int ch0 = 0; ch0 < C; ch0 += CB) {
+        float acc[CB];
+#pragma unroll
+        for (int u = 0; u < CB; ++u) acc[u] = 0.0f;
 #pragma unroll
         for (int h = 0; h < KMAX; ++h) {
             if (h < n) {
-                const long long k = ch * Nc + hcol[h];
-                if constexpr (AVG) acc = __fadd_rn(acc, __fmul_rn(__ldg(cd + k), inv));
-                else if (__ldg(sw + k) == hrow[h]) acc = __fadd_rn(acc, __ldg(cd + k));
+                float v[CB];
+                int w[CB];
+#pragma unroll
+                for (int u = 0; u < CB; ++u) {
+                    const long long k = (long long)min(ch0 + u, C - 1) * Nc + hcol[h];
+                    v[u] = __ldg(cd + k);
+                    if constexpr (!AVG) w[u] = __ldg(sw + k);
+                }
+#pragma unroll
+                for (int u = 0; u < CB; ++u) {
+                    if constexpr (AVG) acc[u] = __fadd_rn(acc[u], __fmul_rn(v[u], inv));
+                    else if (w[u] == hrow[h]) acc[u] = __fadd_rn(acc[u], v[u]);
+                }
             }
         }
-        res[ch * Nf + gi] = acc;
+#pragma unroll
+        for (int u = 0; u < CB; ++u)
+            if (ch0 + u < C) res[(long long)(ch0 + u) * Nf + gi] = acc[u];
     }
 }
 
@@ -629,9 +678,9 @@ void launch_max_pool(const hc_psh* in, const float* data, const hc_psh* out, con
     if (n == 0 || sp.in_channels == 0) return;
     const unsigned g = grid_for(n, kThreads);
     if (sp.kernel == 2)
-        k_max_pool<2><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, res, sw);
+        k_max_pool<2, 4><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, res, sw);
     else if (sp.kernel == 3)
-        k_max_pool<3><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, res, sw);
+        k_max_pool<3, 1><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, res, sw);
     else
         k_max_pool_any<<<g, kThreads, 0, s>>>(in->d, out->d, sp.kernel, sp.stride, sp.pad,
                                             (int)field_volume(sp, in->d.dim), data, sp.in_channels, res, sw);
@@ -646,9 +695,9 @@ void launch_avg_pool(const hc_psh* in, const float* data, const hc_psh* out, con
     const long long fd = field_volume(sp, in->d.dim);
     const float inv = 1.0f / static_cast<float>(fd);  // cnn_ops.cpp:295
     if (sp.kernel == 2)
-        k_avg_pool<2><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, inv, res);
+        k_avg_pool<2, 4><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, inv, res);
     else if (sp.kernel == 3)
-        k_avg_pool<3><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, inv, res);
+        k_avg_pool<3, 1><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, inv, res);
     else
         k_avg_pool_any<<<g, kThreads, 0, s>>>(in->d, out->d, sp.kernel, sp.stride, sp.pad, (int)fd, data,
                                             sp.in_channels, inv, res);
@@ -665,10 +714,10 @@ void launch_unpool(bool avg, const float* cd, const int* sw, const hc_psh* fine,
     const int kmax = fine->d.dim == 3 ? ka * ka * ka : ka * ka;
     const int C = sp.in_channels;
 #define HC_UNPOOL(K)                                                                                             \
-    (avg ? k_unpool<K, true><<<g, kThreads, 0, s>>>(fine->d, coarse->d, sp.kernel, sp.stride, sp.pad, cd, sw, C, \
-                                                     inv, res)                                                   \
-         : k_unpool<K, false><<<g, kThreads, 0, s>>>(fine->d, coarse->d, sp.kernel, sp.stride, sp.pad, cd, sw, C, \
-                                                      inv, res))
+    (avg ? k_unpool<K, true, (K <= 1 ? 8 : 4)><<<g, kThreads, 0, s>>>(fine->d, coarse->d, sp.kernel, sp.stride, \
+                                                                        sp.pad, cd, sw, C, inv, res)             \
+         : k_unpool<K, false, (K <= 1 ? 8 : 4)><<<g, kThreads, 0, s>>>(fine->d, coarse->d, sp.kernel, sp.stride, \
+                                                                         sp.pad, cd, sw, C, inv, res))
     if (kmax <= 1) HC_UNPOOL(1);
     else if (kmax <= 8) HC_UNPOOL(8);
     else if (kmax <= 27) HC_UNPOOL(27);
