@@ -55,6 +55,9 @@ using namespace tc;
 #ifdef HCB_WAIT_SPIN  // A/B: plain try_wait spins for the long waits too
 #define mbar_wait_sleep mbar_wait
 #endif
+#ifdef HCB_NO_PROXY_FENCE  // A/B only (not a valid memory-model protocol): measures the fence's cost
+#define fence_proxy_async() ((void)0)
+#endif
 
 constexpr int BM = 128;  // voxels per forward tile (GEMM M) / (t,ci) rows per dW m-tile
 constexpr int BK = 64;   // K elements (bf16) per stage = one 128-byte row
@@ -337,27 +340,27 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, PW>::THREADS, CPS)
 // accumulators (mpg * NB TMEM columns) stay resident for the CTA's whole voxel range,
 // so each dY stage is loaded once and feeds all of them (the previous one-m-tile-per-
 // CTA plan re-read dY mt = 14 times at C=64).
-template <int NB, int PW>
+template <int NB, int PW, int CPS = 1>
 struct DwCfg {
     static constexpr int KB = 64;                      // voxels per stage
     static constexpr int A_BYTES = 2 * KB * 128;       // two 64-wide MN blocks (M = 128)
     static constexpr int B_BYTES = (NB / 64) * KB * 128;
     static constexpr int BSTAGES = 2;
     static constexpr int NBR = 2 * kNbrBytes;
-    static constexpr int BUDGET = 226 * 1024 - 1024 - 512 - 1024 - NBR - BSTAGES * B_BYTES;
+    static constexpr int BUDGET = (CPS == 2 ? 113 : 226) * 1024 - 1024 - 512 - 1024 - NBR - BSTAGES * B_BYTES;
     static constexpr int STAGES = BUDGET / A_BYTES > 10 ? 10 : BUDGET / A_BYTES;
     static constexpr int PRODUCERS = PW * 32;
     static constexpr int THREADS = PRODUCERS + 32;  // + MMA / TMEM warp
-    static constexpr int MPG = 512 / NB;            // m-tiles whose accumulators fit TMEM
+    static constexpr int TMEM_COLS = 512 / CPS;     // per CTA (CPS resident CTAs per SM)
     static constexpr int SMEM = 1024 + STAGES * A_BYTES + BSTAGES * B_BYTES + NBR + 1024 + 512;
 };
 
-template <int NB, int PW>
-__global__ void __launch_bounds__(DwCfg<NB, PW>::THREADS, 1)
+template <int NB, int PW, int CPS>
+__global__ void __launch_bounds__(DwCfg<NB, PW, CPS>::THREADS, CPS)
     k_conv_dw(const __grid_constant__ CUtensorMap dymap, const int* __restrict__ fmap, int taps, long long rows,
               const bf16* __restrict__ X, int C, int mt, int mpg, int tiles_per_split, int tiles,
               float* __restrict__ partial) {
-    using Cfg = DwCfg<NB, PW>;
+    using Cfg = DwCfg<NB, PW, CPS>;
     constexpr int S = Cfg::STAGES, BS = Cfg::BSTAGES;
     constexpr int NP = Cfg::PRODUCERS;
     constexpr int RS = NP / 8;
@@ -404,7 +407,7 @@ __global__ void __launch_bounds__(DwCfg<NB, PW>::THREADS, 1)
         mbar_init(done, 1);
         mbar_init_fence();
     }
-    if (warp == PW) tmem_alloc(smem_u32(tmem_slot), 512);
+    if (warp == PW) tmem_alloc(smem_u32(tmem_slot), Cfg::TMEM_COLS);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -555,7 +558,7 @@ __global__ void __launch_bounds__(DwCfg<NB, PW>::THREADS, 1)
     if (warp == PW) {
         __syncwarp();
         tc_fence_after();
-        tmem_dealloc(tmem, 512);
+        tmem_dealloc(tmem, Cfg::TMEM_COLS);
     }
 }
 
@@ -684,8 +687,9 @@ void launch_fwd_bn(const int* fmap, int taps, long long rows, const bf16* X, int
     static const int pw = env_int("HCB_FWD_PW", 4);
     if constexpr (BN <= 64) {
         if (cps == 2) {
-            if (pw == 4) return launch_fwd<BN, 2, 4>(fmap, taps, rows, X, C, Wp, Kp, Y, s);
-            return launch_fwd<BN, 2, 8>(fmap, taps, rows, X, C, Wp, Kp, Y, s);
+            if (pw == 2) return launch_fwd<BN, 2, 2>(fmap, taps, rows, X, C, Wp, Kp, Y, s);
+            if (pw == 8) return launch_fwd<BN, 2, 8>(fmap, taps, rows, X, C, Wp, Kp, Y, s);
+            return launch_fwd<BN, 2, 4>(fmap, taps, rows, X, C, Wp, Kp, Y, s);
         }
     }
     if (pw == 4) return launch_fwd<BN, 1, 4>(fmap, taps, rows, X, C, Wp, Kp, Y, s);
@@ -712,30 +716,38 @@ int dw_nb(int cout) { return cout <= 64 ? 64 : cout <= 128 ? 128 : 256; }
 // columns), groups balanced; the voxel tiles are split so groups x splits fills every SM
 // once (one CTA per SM). Deterministic for a given SM count.
 struct DwPlan {
-    int nb, mt, groups, mpg, splits, tps, tiles;
+    int nb, mt, cps, groups, mpg, splits, tps, tiles;
     long long partial_floats;
 };
+
+// HCB_DW_CPS = resident dW CTAs per SM (2, default: 256 TMEM columns each, NB <= 128 —
+// two independent pipelines per SM measured 11% faster at C=64; 1: 512 columns).
+int dw_cps(int nb) {
+    static const int env = env_int("HCB_DW_CPS", 2);
+    return (env == 2 && nb <= 128) ? 2 : 1;
+}
 
 DwPlan dw_plan(long long rows, int taps, int cin, int cout) {
     DwPlan p{};
     p.nb = dw_nb(cout);
     p.mt = (taps * cin + BM - 1) / BM;
-    const int cap = 512 / p.nb;
+    p.cps = dw_cps(p.nb);
+    const int cap = 512 / (p.nb * p.cps);
     p.groups = (p.mt + cap - 1) / cap;
     p.mpg = (p.mt + p.groups - 1) / p.groups;
     p.tiles = (int)((rows + BM - 1) / BM);
-    const int want = std::max(1, std::min(p.tiles, num_sms() / p.groups));
+    const int want = std::max(1, std::min(p.tiles, num_sms() * p.cps / p.groups));
     p.tps = (p.tiles + want - 1) / want;
     p.splits = std::max(1, (p.tiles + p.tps - 1) / p.tps);
     p.partial_floats = (long long)p.splits * p.mt * BM * p.nb;
     return p;
 }
 
-template <int NB, int PW>
+template <int NB, int PW, int CPS>
 void launch_dw_pw(const DwPlan& p, const int* fmap, int taps, long long rows, const bf16* X, int C, const bf16* dY,
                   int Cout, float* partial, cudaStream_t s) {
-    using Cfg = DwCfg<NB, PW>;
-    auto kern = k_conv_dw<NB, PW>;
+    using Cfg = DwCfg<NB, PW, CPS>;
+    auto kern = k_conv_dw<NB, PW, CPS>;
     static bool attr = false;
     if (!attr) {
         cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM), "smem attr");
@@ -749,14 +761,22 @@ void launch_dw_pw(const DwPlan& p, const int* fmap, int taps, long long rows, co
     launched("conv dW gather-GEMM (tcgen05)");
 }
 
-// HCB_DW_PW = producer warps of the dW kernel (4, 8 or 16; default 8).
+// HCB_DW_PW = producer warps of the dW kernel (2/4/8 with 2 CTAs per SM, default 4;
+// 4/8/16 with one, default 8). Measured on B200 (scripts/gpu_ab.sh).
 template <int NB>
 void launch_dw(const DwPlan& p, const int* fmap, int taps, long long rows, const bf16* X, int C, const bf16* dY,
                int Cout, float* partial, cudaStream_t s) {
-    static const int pw = env_int("HCB_DW_PW", 8);
-    if (pw == 4) return launch_dw_pw<NB, 4>(p, fmap, taps, rows, X, C, dY, Cout, partial, s);
-    if (pw == 16) return launch_dw_pw<NB, 16>(p, fmap, taps, rows, X, C, dY, Cout, partial, s);
-    launch_dw_pw<NB, 8>(p, fmap, taps, rows, X, C, dY, Cout, partial, s);
+    static const int pw = env_int("HCB_DW_PW", p.cps == 2 ? 4 : 8);
+    if constexpr (NB <= 128) {
+        if (p.cps == 2) {
+            if (pw == 2) return launch_dw_pw<NB, 2, 2>(p, fmap, taps, rows, X, C, dY, Cout, partial, s);
+            if (pw == 8) return launch_dw_pw<NB, 8, 2>(p, fmap, taps, rows, X, C, dY, Cout, partial, s);
+            return launch_dw_pw<NB, 4, 2>(p, fmap, taps, rows, X, C, dY, Cout, partial, s);
+        }
+    }
+    if (pw == 4) return launch_dw_pw<NB, 4, 1>(p, fmap, taps, rows, X, C, dY, Cout, partial, s);
+    if (pw == 16) return launch_dw_pw<NB, 16, 1>(p, fmap, taps, rows, X, C, dY, Cout, partial, s);
+    launch_dw_pw<NB, 8, 1>(p, fmap, taps, rows, X, C, dY, Cout, partial, s);
 }
 
 void check_native(int cin, int cout, int taps) {
