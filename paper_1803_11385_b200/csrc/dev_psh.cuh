@@ -76,11 +76,18 @@ __device__ __forceinline__ int probe(const DevPsh& s, const ModelParam& mp, int 
 
 // Field taps of one output voxel: base = field origin (cnn_ops.cpp:36-42), F per
 // axis, taps in (dz,dy,dx) row order (cnn_ops.cpp:100-119). Residues are
-// computed once per axis coordinate (3F fast mods instead of 6F^3).
+// computed once per axis coordinate (3F fast mods instead of 6F^3); the cell row,
+// the packed-key prefix and the per-model table bases are hoisted out of the tap
+// loop, and all per-tap index math is 32-bit (tables < 2^31 entries, columns < 2^31),
+// so a probe is ~25 instructions around its two dependent loads.
 template <int F>
 __device__ __forceinline__ void probe_field(const DevPsh& s, const ModelParam& mp, int bx, int by, int bz,
                                             int* out /* F^dim */) {
-    const int dim = s.dim, res = s.resolution;
+    const int dim = s.dim, res = s.resolution, kb = s.key_bits;
+    const int m = mp.m, r = mp.r;
+    const unsigned* phib = s.phi + mp.offset_base;
+    const uint2* slotb = s.slots + mp.hash_base;
+    const int dbase = (int)mp.data_base;
     int rmx[F], rmy[F], rmz[F], rrx[F], rry[F], rrz[F];
     bool vx[F], vy[F], vz[F];
 #pragma unroll
@@ -89,27 +96,41 @@ __device__ __forceinline__ void probe_field(const DevPsh& s, const ModelParam& m
         vx[d] = x >= 0 && x < res;
         vy[d] = y >= 0 && y < res;
         vz[d] = dim == 3 ? (z >= 0 && z < res) : (d == 0);
-        rmx[d] = vx[d] ? fmod_small(x, mp.m, mp.inv_m) : 0;
-        rmy[d] = vy[d] ? fmod_small(y, mp.m, mp.inv_m) : 0;
-        rmz[d] = (dim == 3 && vz[d]) ? fmod_small(z, mp.m, mp.inv_m) : 0;
-        rrx[d] = vx[d] ? fmod_small(x, mp.r, mp.inv_r) : 0;
-        rry[d] = vy[d] ? fmod_small(y, mp.r, mp.inv_r) : 0;
-        rrz[d] = (dim == 3 && vz[d]) ? fmod_small(z, mp.r, mp.inv_r) : 0;
+        rmx[d] = vx[d] ? fmod_small(x, m, mp.inv_m) : 0;
+        rmy[d] = vy[d] ? fmod_small(y, m, mp.inv_m) : 0;
+        rmz[d] = (dim == 3 && vz[d]) ? fmod_small(z, m, mp.inv_m) : 0;
+        rrx[d] = vx[d] ? fmod_small(x, r, mp.inv_r) : 0;
+        rry[d] = vy[d] ? fmod_small(y, r, mp.inv_r) : 0;
+        rrz[d] = (dim == 3 && vz[d]) ? fmod_small(z, r, mp.inv_r) : 0;
     }
     const int fz = dim == 3 ? F : 1;
 #pragma unroll
     for (int dz = 0; dz < F; ++dz) {
         if (dz >= fz) break;
+        const unsigned kz = dim == 3 ? (unsigned)(bz + dz) << (2 * kb) : 0u;
 #pragma unroll
-        for (int dy = 0; dy < F; ++dy)
+        for (int dy = 0; dy < F; ++dy) {
+            const bool vzy = vz[dz] && vy[dy];
+            const int cell_zy = (rrz[dz] * r + rry[dy]) * r;  // dim 2: rrz = 0 -> rry * r
+            const unsigned key_zy = kz | ((unsigned)(by + dy) << kb);
 #pragma unroll
             for (int dx = 0; dx < F; ++dx) {
                 const int t = (dz * F + dy) * F + dx;
-                out[t] = (vx[dx] && vy[dy] && vz[dz])
-                             ? probe_res(s, mp, dim, bx + dx, by + dy, dim == 3 ? bz + dz : 0, rmx[dx], rmy[dy],
-                                         rmz[dz], rrx[dx], rry[dy], rrz[dz])
-                             : -1;
+                int v = -1;
+                if (vzy && vx[dx]) {
+                    const unsigned ph = __ldg(phib + cell_zy + rrx[dx]);
+                    int sx = rmx[dx] + (int)(ph & 0xFF);
+                    int sy = rmy[dy] + (int)((ph >> 8) & 0xFF);
+                    int sz = rmz[dz] + (int)((ph >> 16) & 0xFF);  // dim 2: both terms 0
+                    if (sx >= m) sx -= m;
+                    if (sy >= m) sy -= m;
+                    if (sz >= m) sz -= m;
+                    const uint2 e = __ldg(slotb + (sz * m + sy) * m + sx);
+                    if ((int)e.x >= 0 && e.y == (key_zy | (unsigned)(bx + dx))) v = dbase + (int)e.x;
+                }
+                out[t] = v;
             }
+        }
     }
 }
 

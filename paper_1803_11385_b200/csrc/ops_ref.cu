@@ -87,7 +87,7 @@ __global__ void k_field_map_t(DevPsh in, DevPsh out, int S, int pad, int* map) {
 // contiguous block (fetched by one bulk copy in the native conv); padded columns
 // beyond N are -1.
 template <int F>
-__global__ void __launch_bounds__(256, 4) k_field_map_tiled(DevPsh in, DevPsh out, int S, int pad, int* map) {
+__global__ void __launch_bounds__(256, 3) k_field_map_tiled(DevPsh in, DevPsh out, int S, int pad, int* map) {
     const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     const long long padded = (out.N + 127) / 128 * 128;
     if (col >= padded) return;
@@ -657,8 +657,8 @@ void launch_col2hash(const float* gcols, const hc_psh* in, const hc_psh* out, co
         static const int cu = env_int("HCB_C2H_CU", 16);
         if (cu == 16) k_col2hash_s1_tb<3, 16><<<g, kThreads, 0, s>>>(in->d, out->d, gcols, C, res);
         else if (cu == 8) k_col2hash_s1_tb<3, 8><<<g, kThreads, 0, s>>>(in->d, out->d, gcols, C, res);
-        else if (cu >= 4) k_col2hash_s1<3, 4, 4><<<g, kThreads, 0, s>>>(in->d, out->d, gcols, C, res);
-        else if (cu >= 2) k_col2hash_s1<3, 2, 4><<<g, kThreads, 0, s>>>(in->d, out->d, gcols, C, res);
+        else if (cu >= 4) k_col2hash_s1<3, 4, 3><<<g, kThreads, 0, s>>>(in->d, out->d, gcols, C, res);
+        else if (cu >= 2) k_col2hash_s1<3, 2, 3><<<g, kThreads, 0, s>>>(in->d, out->d, gcols, C, res);
         else k_col2hash_s1<3, 1, 4><<<g, kThreads, 0, s>>>(in->d, out->d, gcols, C, res);
     }
     else if (sp.stride == 1 && sp.kernel == 1)
