@@ -134,6 +134,66 @@ __device__ __forceinline__ void probe_field(const DevPsh& s, const ModelParam& m
     }
 }
 
+// probe_field in three explicit phases — all F^dim offset-table loads, then all hash-slot
+// loads, then the tag compares — so a thread keeps F^dim independent probe chains in
+// flight (the fused form leaves ~1 chain in flight per thread; the K0 map kernels are
+// bound by that latency, not by bytes). Same results as probe_field.
+template <int F>
+__device__ __forceinline__ void probe_field_batched(const DevPsh& s, const ModelParam& mp, int bx, int by, int bz,
+                                                    int* out /* F^dim */) {
+    constexpr int T = F * F * F;
+    const int dim = s.dim, res = s.resolution, kb = s.key_bits;
+    const int m = mp.m, r = mp.r;
+    const unsigned* phib = s.phi + mp.offset_base;
+    const uint2* slotb = s.slots + mp.hash_base;
+    const int dbase = (int)mp.data_base;
+    int rmx[F], rmy[F], rmz[F], rrx[F], rry[F], rrz[F];
+    bool vx[F], vy[F], vz[F];
+#pragma unroll
+    for (int d = 0; d < F; ++d) {
+        const int x = bx + d, y = by + d, z = bz + d;
+        vx[d] = x >= 0 && x < res;
+        vy[d] = y >= 0 && y < res;
+        vz[d] = dim == 3 ? (z >= 0 && z < res) : (d == 0);
+        rmx[d] = vx[d] ? fmod_small(x, m, mp.inv_m) : 0;
+        rmy[d] = vy[d] ? fmod_small(y, m, mp.inv_m) : 0;
+        rmz[d] = (dim == 3 && vz[d]) ? fmod_small(z, m, mp.inv_m) : 0;
+        rrx[d] = vx[d] ? fmod_small(x, r, mp.inv_r) : 0;
+        rry[d] = vy[d] ? fmod_small(y, r, mp.inv_r) : 0;
+        rrz[d] = (dim == 3 && vz[d]) ? fmod_small(z, r, mp.inv_r) : 0;
+    }
+    unsigned ph[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+        const int dz = t / (F * F), dy = (t / F) % F, dx = t % F;
+        const bool ok = vz[dz] && vy[dy] && vx[dx];
+        ph[t] = ok ? __ldg(phib + (rrz[dz] * r + rry[dy]) * r + rrx[dx]) : 0xFFFFFFFFu;
+    }
+    uint2 e[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+        const int dz = t / (F * F), dy = (t / F) % F, dx = t % F;
+        if (ph[t] != 0xFFFFFFFFu) {
+            int sx = rmx[dx] + (int)(ph[t] & 0xFF);
+            int sy = rmy[dy] + (int)((ph[t] >> 8) & 0xFF);
+            int sz = rmz[dz] + (int)((ph[t] >> 16) & 0xFF);
+            if (sx >= m) sx -= m;
+            if (sy >= m) sy -= m;
+            if (sz >= m) sz -= m;
+            e[t] = __ldg(slotb + (sz * m + sy) * m + sx);
+        } else {
+            e[t] = make_uint2(0xFFFFFFFFu, 0u);
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+        const int dz = t / (F * F), dy = (t / F) % F, dx = t % F;
+        const unsigned key = (dim == 3 ? (unsigned)(bz + dz) << (2 * kb) : 0u) | ((unsigned)(by + dy) << kb) |
+                             (unsigned)(bx + dx);
+        out[t] = ((int)e[t].x >= 0 && e[t].y == key) ? dbase + (int)e[t].x : -1;
+    }
+}
+
 // Generic-F single tap (any kernel size): used by the fallback kernels.
 __device__ __forceinline__ int probe_tap(const DevPsh& s, const ModelParam& mp, int bx, int by, int bz, int F,
                                          int t) {

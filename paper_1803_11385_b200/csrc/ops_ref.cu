@@ -87,7 +87,7 @@ __global__ void k_field_map_t(DevPsh in, DevPsh out, int S, int pad, int* map) {
 // contiguous block (fetched by one bulk copy in the native conv); padded columns
 // beyond N are -1.
 template <int F>
-__global__ void __launch_bounds__(256, 3) k_field_map_tiled(DevPsh in, DevPsh out, int S, int pad, int* map) {
+__global__ void __launch_bounds__(256, 2) k_field_map_tiled(DevPsh in, DevPsh out, int S, int pad, int* map) {
     const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     const long long padded = (out.N + 127) / 128 * 128;
     if (col >= padded) return;
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(256, 3) k_field_map_tiled(DevPsh in, DevPsh ou
     if (col < out.N) {
         const int4 c = out.cols[col];
         const ModelParam mp = in.models[c.w - 1];
-        probe_field<F>(in, mp, origin_axis(c.x, F, S, pad), origin_axis(c.y, F, S, pad),
+        probe_field_batched<F>(in, mp, origin_axis(c.x, F, S, pad), origin_axis(c.y, F, S, pad),
                        origin_axis(c.z, F, S, pad), nb);
     } else {
 #pragma unroll
@@ -262,24 +262,28 @@ __global__ void __launch_bounds__(256, 4)
         for (int t = 0; t < T3; ++t) nbs[t][threadIdx.x] = t < fd ? nb[t] : -1;
     }
     if (!live) return;  // no block-wide barrier below: each thread reads only its own column
-    const long long Nout = out.N, Nin = in.N;
+    const int Nout = (int)out.N;  // fd * N_out < 2^31 (checked at launch): 32-bit row offsets
+    const long long Nin = in.N;
     const long long plane = (long long)fd * Nout;
     for (int cb = 0; cb < C; cb += CB) {
+        // one 64-bit base per channel (clamped past C: loads stay in bounds, results unused);
+        // per tap a 32-bit offset shared by all CB loads -> ~3 instructions per gathered float
+        const float* bp[CB];
+#pragma unroll
+        for (int u = 0; u < CB; ++u) bp[u] = g + (long long)min(cb + u, C - 1) * plane;
         float acc[CB];
 #pragma unroll
         for (int u = 0; u < CB; ++u) acc[u] = 0.0f;
-        const float* base = g + (long long)cb * plane;
         for (int t = 0; t < fd; ++t) {
             const int col = nbs[t][threadIdx.x];
             if (col < 0) continue;
-            const float* p = base + (long long)(fd - 1 - t) * Nout + col;
+            const unsigned off = (unsigned)(fd - 1 - t) * (unsigned)Nout + (unsigned)col;
 #pragma unroll
-            for (int u = 0; u < CB; ++u)
-                if (cb + u < C) acc[u] = __fadd_rn(acc[u], __ldg(p + u * plane));
+            for (int u = 0; u < CB; ++u) acc[u] = __fadd_rn(acc[u], __ldg(bp[u] + off));
         }
 #pragma unroll
         for (int u = 0; u < CB; ++u)
-            if (cb + u < C) res[(cb + u) * Nin + gi] = acc[u];
+            if (cb + u < C) res[(long long)(cb + u) * Nin + gi] = acc[u];
     }
 }
 
@@ -652,7 +656,7 @@ void launch_col2hash(const float* gcols, const hc_psh* in, const hc_psh* out, co
     const unsigned g = grid_for(n, kThreads);
     const int fd = (int)field_volume(sp, in->d.dim);
     const int C = sp.in_channels;
-    if (sp.stride == 1 && sp.kernel == 3)
+    if (sp.stride == 1 && sp.kernel == 3 && (long long)fd * out->d.N < (1LL << 31))
     {
         static const int cu = env_int("HCB_C2H_CU", 16);
         if (cu == 16) k_col2hash_s1_tb<3, 16><<<g, kThreads, 0, s>>>(in->d, out->d, gcols, C, res);
