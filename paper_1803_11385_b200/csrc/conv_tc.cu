@@ -141,7 +141,10 @@ struct FwdCfg {
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int NBR = 2 * kNbrBytes;
     static constexpr int BUDGET = (CPS == 2 ? 113 : 226) * 1024 - 1024 - 320 - NBR;
-    static constexpr int STAGES = BUDGET / STAGE_BYTES > 10 ? 10 : BUDGET / STAGE_BYTES;
+#ifndef HCB_FWD_MAXSTAGES
+#define HCB_FWD_MAXSTAGES 10
+#endif
+    static constexpr int STAGES = BUDGET / STAGE_BYTES > HCB_FWD_MAXSTAGES ? HCB_FWD_MAXSTAGES : BUDGET / STAGE_BYTES;
     static constexpr int PRODUCERS = PW * 32;      // warps 0..PW-1
     static constexpr int THREADS = PW * 32 + 192;  // + epilogue warps PW..PW+3, MMA warp PW+4, TMA warp PW+5
     static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + NBR + 320;
@@ -336,10 +339,22 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, PW>::THREADS, CPS)
 //                                        per voxel and 64-wide MN block)
 //   B[co][n] = dY[n][co]                 (MN-major; 2-D TMA of 64 voxel rows per block,
 //                                        C_out < 64 zero-filled out of bounds)
-// One CTA per SM: grid = splits x groups. A group owns `mpg` m-tiles whose fp32
-// accumulators (mpg * NB TMEM columns) stay resident for the CTA's whole voxel range,
+// Grid = CTA slots of the SM count (DwGroups): a group owns up to 512/(NB*CPS) m-tiles whose
+// fp32 accumulators (NB TMEM columns each) stay resident for the CTA's whole voxel range,
 // so each dY stage is loaded once and feeds all of them (the previous one-m-tile-per-
 // CTA plan re-read dY mt = 14 times at C=64).
+// Split plan, passed by value: group g owns m-tiles [m_begin[g], m_begin[g+1]) and CTAs
+// [cta_begin[g], cta_begin[g+1]), each CTA a run of tps[g] voxel tiles; its partials start
+// at part_begin[g] (floats), laid out [split][m-tile][128][NB].
+constexpr int kMaxGroups = 32;
+struct DwGroups {
+    int groups;
+    int m_begin[kMaxGroups + 1];
+    int cta_begin[kMaxGroups + 1];
+    int tps[kMaxGroups];
+    long long part_begin[kMaxGroups];
+};
+
 template <int NB, int PW, int CPS = 1>
 struct DwCfg {
     static constexpr int KB = 64;                      // voxels per stage
@@ -358,8 +373,7 @@ struct DwCfg {
 template <int NB, int PW, int CPS>
 __global__ void __launch_bounds__(DwCfg<NB, PW, CPS>::THREADS, CPS)
     k_conv_dw(const __grid_constant__ CUtensorMap dymap, const int* __restrict__ fmap, int taps, long long rows,
-              const bf16* __restrict__ X, int C, int mt, int mpg, int tiles_per_split, int tiles,
-              float* __restrict__ partial) {
+              const bf16* __restrict__ X, int C, const DwGroups grp_tab, int tiles, float* __restrict__ partial) {
     using Cfg = DwCfg<NB, PW, CPS>;
     constexpr int S = Cfg::STAGES, BS = Cfg::BSTAGES;
     constexpr int NP = Cfg::PRODUCERS;
@@ -370,17 +384,20 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS>::THREADS, CPS)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* bsm = smem + S * Cfg::A_BYTES;
     int* nbr_s = reinterpret_cast<int*>(bsm + BS * Cfg::B_BYTES);
-    int* tab = nbr_s + 2 * kMaxTaps * BM;  // [mpg][2 blocks][8 chunks]: (t << 16 | ci) or -1
+    int* tab = nbr_s + 2 * kMaxTaps * BM;  // [m-tile][2 blocks][8 chunks]: (t << 16 | ci) or -1
     uint64_t* bars = reinterpret_cast<uint64_t*>(tab + 256);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 2 * BS + 3);
     int* nbr_cnt = reinterpret_cast<int*>(tmem_slot + 2);
 
     const int tid = threadIdx.x, warp = tid >> 5;
-    const int split = blockIdx.x, grp = blockIdx.y;
-    const int m0 = grp * mpg;
-    const int nm = min(mpg, mt - m0);
-    const int tile0 = split * tiles_per_split;
-    const int ntl = max(0, min(tiles_per_split, tiles - tile0));
+    int grp = 0;  // this CTA's m-tile group and its voxel split inside the group
+    while (grp + 1 < grp_tab.groups && (int)blockIdx.x >= grp_tab.cta_begin[grp + 1]) ++grp;
+    const int split = (int)blockIdx.x - grp_tab.cta_begin[grp];
+    const int m0 = grp_tab.m_begin[grp];
+    const int nm = grp_tab.m_begin[grp + 1] - m0;
+    const int tps = grp_tab.tps[grp];
+    const int tile0 = split * tps;
+    const int ntl = max(0, min(tps, tiles - tile0));
     const int K = taps * C;
     const uint32_t sbase = smem_u32(smem), bbase = smem_u32(bsm);
     const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S);
@@ -495,7 +512,7 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS>::THREADS, CPS)
                 tc_fence_after();
             }
             for (int mi = 0; mi < nm; ++mi) {
-                float* dst = partial + ((long long)split * mt * BM + (long long)(m0 + mi) * BM + row) * NB;
+                float* dst = partial + grp_tab.part_begin[grp] + (((long long)split * nm + mi) * BM + row) * NB;
 #pragma unroll
                 for (int c0 = 0; c0 < NB; c0 += 16) {
                     float f[16];
@@ -564,7 +581,7 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS>::THREADS, CPS)
 
 // dW_ref[co][ci*taps + t] = sum_split partial[split][t*C + ci][co]  (fixed split order).
 // Thread i -> (m, co) with co fastest: the partial reads are coalesced.
-__global__ void k_reduce_dw(const float* __restrict__ partial, int splits, long long Mtot, int NB, int taps, int C,
+__global__ void k_reduce_dw(const float* __restrict__ partial, const DwGroups grp_tab, int NB, int taps, int C,
                             int Cout, float* __restrict__ dw) {
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // over (taps*C) x Cout
     const long long total = (long long)taps * C * Cout;
@@ -572,8 +589,15 @@ __global__ void k_reduce_dw(const float* __restrict__ partial, int splits, long 
     const long long m = i / Cout;
     const int co = (int)(i - m * Cout);
     const int t = (int)(m / C), ci = (int)(m - (long long)t * C);
+    const int mtile = (int)(m / BM), row = (int)(m % BM);
+    int g = 0;
+    while (g + 1 < grp_tab.groups && mtile >= grp_tab.m_begin[g + 1]) ++g;
+    const int nm = grp_tab.m_begin[g + 1] - grp_tab.m_begin[g];
+    const int splits = grp_tab.cta_begin[g + 1] - grp_tab.cta_begin[g];
+    const float* p = partial + grp_tab.part_begin[g] + ((long long)(mtile - grp_tab.m_begin[g]) * BM + row) * NB + co;
+    const long long stride = (long long)nm * BM * NB;
     float acc = 0.0f;
-    for (int s = 0; s < splits; ++s) acc += partial[((long long)s * Mtot + m) * NB + co];
+    for (int s = 0; s < splits; ++s) acc += p[s * stride];
     dw[(long long)co * C * taps + (long long)ci * taps + t] = acc;
 }
 
@@ -712,14 +736,9 @@ void conv_fwd(const int* fmap, int taps, long long rows, const bf16* X, int C, c
 
 int dw_nb(int cout) { return cout <= 64 ? 64 : cout <= 128 ? 128 : 256; }
 
-// Split plan: m-tiles are grouped so each group's accumulators fit TMEM (mpg * NB <= 512
-// columns), groups balanced; the voxel tiles are split so groups x splits fills every SM
-// once (one CTA per SM). Deterministic for a given SM count.
-struct DwPlan {
-    int nb, mt, cps, groups, mpg, splits, tps, tiles;
-    long long partial_floats;
-};
-
+// Split plan: m-tiles are grouped so each group's accumulators fit TMEM (m-tiles * NB <=
+// 512 / CPS columns) and the groups' CTAs fill the SMs x CPS slots. Deterministic for a
+// given SM count.
 // HCB_DW_CPS = resident dW CTAs per SM (2, default: 256 TMEM columns each, NB <= 128 —
 // two independent pipelines per SM measured 11% faster at C=64; 1: 512 columns).
 int dw_cps(int nb) {
@@ -727,19 +746,49 @@ int dw_cps(int nb) {
     return (env == 2 && nb <= 128) ? 2 : 1;
 }
 
+struct DwPlan {
+    int nb, mt, cps, ctas, tiles;
+    DwGroups g;
+    long long partial_floats;
+};
+
 DwPlan dw_plan(long long rows, int taps, int cin, int cout) {
     DwPlan p{};
     p.nb = dw_nb(cout);
     p.mt = (taps * cin + BM - 1) / BM;
     p.cps = dw_cps(p.nb);
-    const int cap = 512 / (p.nb * p.cps);
-    p.groups = (p.mt + cap - 1) / cap;
-    p.mpg = (p.mt + p.groups - 1) / p.groups;
     p.tiles = (int)((rows + BM - 1) / BM);
-    const int want = std::max(1, std::min(p.tiles, num_sms() * p.cps / p.groups));
-    p.tps = (p.tiles + want - 1) / want;
-    p.splits = std::max(1, (p.tiles + p.tps - 1) / p.tps);
-    p.partial_floats = (long long)p.splits * p.mt * BM * p.nb;
+    const int cap = 512 / (p.nb * p.cps);
+    const int G = std::min(kMaxGroups, (p.mt + cap - 1) / cap);
+    const int slots = num_sms() * p.cps;
+    DwGroups& g = p.g;
+    g.groups = G;
+    // Few groups (C_out <= 64): CTAs proportional to each group's m-tiles, so groups of
+    // 4 and 3 m-tiles finish together (C=64: 0.667 -> 0.607 ms). Many groups (C_out >= 128,
+    // 14+ groups re-reading dY): equal voxel splits in lockstep, so one range's dY tile and
+    // gathered rows are shared through L2 by all groups (proportional splits lose that
+    // alignment: C=128 1.51 -> 2.0 ms); the imbalance of 2-vs-1 m-tile groups is small there.
+    const bool proportional = G <= 4;
+    const int eq_want = std::max(1, std::min(p.tiles, slots / G));
+    long long part = 0;
+    g.m_begin[0] = 0;
+    g.cta_begin[0] = 0;
+    for (int i = 0; i < G; ++i) {
+        g.m_begin[i + 1] = (int)((long long)p.mt * (i + 1) / G);
+        const int mg = g.m_begin[i + 1] - g.m_begin[i];
+        int want = eq_want;
+        if (proportional) {
+            const int end = (int)((long long)slots * g.m_begin[i + 1] / p.mt);
+            want = std::max(1, std::min(p.tiles, end - g.cta_begin[i]));
+        }
+        g.tps[i] = std::max(1, (p.tiles + want - 1) / want);
+        const int splits = std::max(1, (p.tiles + g.tps[i] - 1) / g.tps[i]);
+        g.cta_begin[i + 1] = g.cta_begin[i] + splits;
+        g.part_begin[i] = part;
+        part += (long long)splits * mg * BM * p.nb;
+    }
+    p.ctas = g.cta_begin[G];
+    p.partial_floats = part;
     return p;
 }
 
@@ -756,8 +805,7 @@ void launch_dw_pw(const DwPlan& p, const int* fmap, int taps, long long rows, co
     // dY [rows][Cout] bf16: boxes of 64 voxels x 64 channels; channels >= Cout and voxels
     // >= rows are out of bounds -> zero.
     const CUtensorMap dm = map2d(dY, (uint64_t)Cout, (uint64_t)rows, (uint64_t)Cout * 2, 64);
-    dim3 g((unsigned)p.splits, (unsigned)p.groups);
-    kern<<<g, Cfg::THREADS, Cfg::SMEM, s>>>(dm, fmap, taps, rows, X, C, p.mt, p.mpg, p.tps, p.tiles, partial);
+    kern<<<p.ctas, Cfg::THREADS, Cfg::SMEM, s>>>(dm, fmap, taps, rows, X, C, p.g, p.tiles, partial);
     launched("conv dW gather-GEMM (tcgen05)");
 }
 
@@ -873,8 +921,7 @@ hc_status hc_native_conv_dw(const int32_t* fmap, int32_t fmap_layout, int64_t n_
             default: launch_dw<256>(p, fm.p, taps, n_out, X, c_in, DY, c_out, part, s); break;
         }
         const long long total = (long long)c_out * c_in * taps;
-        k_reduce_dw<<<grid_for(total, 256), 256, 0, s>>>(part, p.splits, (long long)p.mt * BM, p.nb, taps, c_in,
-                                                          c_out, dw_ref);
+        k_reduce_dw<<<grid_for(total, 256), 256, 0, s>>>(part, p.g, p.nb, taps, c_in, c_out, dw_ref);
         launched("dW split reduction");
     });
 }

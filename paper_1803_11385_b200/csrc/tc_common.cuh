@@ -95,8 +95,13 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32
 // offset; g < 0 zero-fills. One IMAD.WIDE for the address, no branches.
 __device__ __forceinline__ void cp_async16_row(uint32_t dst, const char* base, int g, uint32_t row_bytes) {
     const char* src = base + (unsigned long long)(unsigned)max(g, 0) * row_bytes;
+#ifdef HCB_GATHER_CA  // A/B: L1-allocating gathers (rows reused across a tile's taps can hit L1)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(g >= 0 ? 16u : 0u)
+                 : "memory");
+#else
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(g >= 0 ? 16u : 0u)
                  : "memory");
+#endif
 }
 // 32-bit shared load by address (volatile: stays ordered after the mbarrier wait that
 // published the data, but — unlike a "memory"-clobbering asm — lets the compiler batch
