@@ -404,13 +404,19 @@ __global__ void __launch_bounds__(256) k_max_pool(DevPsh in, DevPsh out, int S, 
     for (int t = 0; t < T; ++t)
         if (t >= fd) nb[t] = -1;
     const long long Nin = in.N, Nout = out.N;
+    int kt[T];  // gather offsets (0 for absent taps: the load is harmless, the value unused)
+#pragma unroll
+    for (int t = 0; t < T; ++t) kt[t] = max(nb[t], 0);
+    const float* src = data;
+    float* rp = res + col;
+    int* sp = sw + col;
     for (int ch0 = 0; ch0 < C; ch0 += CB) {
         float v[CB][T];
 #pragma unroll
         for (int u = 0; u < CB; ++u) {
-            const float* src = data + (long long)min(ch0 + u, C - 1) * Nin;
+            const float* su = src + (ch0 + u < C ? u * Nin : 0);
 #pragma unroll
-            for (int t = 0; t < T; ++t) v[u][t] = nb[t] >= 0 ? __ldg(src + nb[t]) : 0.0f;
+            for (int t = 0; t < T; ++t) v[u][t] = __ldg(su + kt[t]);
         }
 #pragma unroll
         for (int u = 0; u < CB; ++u) {
@@ -424,9 +430,12 @@ __global__ void __launch_bounds__(256) k_max_pool(DevPsh in, DevPsh out, int S, 
                     arg = t;
                 }
             }
-            res[(long long)(ch0 + u) * Nout + col] = arg < 0 ? 0.0f : best;
-            sw[(long long)(ch0 + u) * Nout + col] = arg;
+            rp[u * Nout] = arg < 0 ? 0.0f : best;
+            sp[u * Nout] = arg;
         }
+        src += CB * Nin;
+        rp += CB * Nout;
+        sp += CB * Nout;
     }
 }
 
@@ -474,13 +483,18 @@ __global__ void __launch_bounds__(256) k_avg_pool(DevPsh in, DevPsh out, int S, 
     for (int t = 0; t < T; ++t)
         if (t >= fd) nb[t] = -1;
     const long long Nin = in.N, Nout = out.N;
+    int kt[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) kt[t] = max(nb[t], 0);
+    const float* src = data;
+    float* rp = res + col;
     for (int ch0 = 0; ch0 < C; ch0 += CB) {
         float v[CB][T];
 #pragma unroll
         for (int u = 0; u < CB; ++u) {
-            const float* src = data + (long long)min(ch0 + u, C - 1) * Nin;
+            const float* su = src + (ch0 + u < C ? u * Nin : 0);
 #pragma unroll
-            for (int t = 0; t < T; ++t) v[u][t] = nb[t] >= 0 ? __ldg(src + nb[t]) : 0.0f;
+            for (int t = 0; t < T; ++t) v[u][t] = __ldg(su + kt[t]);
         }
 #pragma unroll
         for (int u = 0; u < CB; ++u) {
@@ -489,8 +503,10 @@ __global__ void __launch_bounds__(256) k_avg_pool(DevPsh in, DevPsh out, int S, 
 #pragma unroll
             for (int t = 0; t < T; ++t)
                 if (nb[t] >= 0) acc = __fadd_rn(acc, v[u][t]);
-            res[(long long)(ch0 + u) * Nout + col] = __fmul_rn(acc, inv);
+            rp[u * Nout] = __fmul_rn(acc, inv);
         }
+        src += CB * Nin;
+        rp += CB * Nout;
     }
 }
 
@@ -528,6 +544,9 @@ __global__ void __launch_bounds__(256) k_unpool(DevPsh fine, DevPsh coarse, int 
     int hcol[KMAX], hrow[KMAX];
     const int n = cover_hits<1>(coarse, mp, c.x, c.y, c.z, F, S, pad, hcol, hrow);
     const long long Nc = coarse.N, Nf = fine.N;
+    const float* cp = cd;
+    const int* wp = sw;
+    float* rp = res + gi;
     for (int ch0 = 0; ch0 < C; ch0 += CB) {
         float acc[CB];
 #pragma unroll
@@ -539,9 +558,9 @@ __global__ void __launch_bounds__(256) k_unpool(DevPsh fine, DevPsh coarse, int 
                 int w[CB];
 #pragma unroll
                 for (int u = 0; u < CB; ++u) {
-                    const long long k = (long long)min(ch0 + u, C - 1) * Nc + hcol[h];
-                    v[u] = __ldg(cd + k);
-                    if constexpr (!AVG) w[u] = __ldg(sw + k);
+                    const long long k = (ch0 + u < C ? u * Nc : 0) + hcol[h];
+                    v[u] = __ldg(cp + k);
+                    if constexpr (!AVG) w[u] = __ldg(wp + k);
                 }
 #pragma unroll
                 for (int u = 0; u < CB; ++u) {
@@ -552,7 +571,10 @@ __global__ void __launch_bounds__(256) k_unpool(DevPsh fine, DevPsh coarse, int 
         }
 #pragma unroll
         for (int u = 0; u < CB; ++u)
-            if (ch0 + u < C) res[(long long)(ch0 + u) * Nf + gi] = acc[u];
+            if (ch0 + u < C) rp[u * Nf] = acc[u];
+        cp += CB * Nc;
+        wp += CB * Nc;
+        rp += CB * Nf;
     }
 }
 
