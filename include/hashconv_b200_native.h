@@ -50,6 +50,46 @@ hc_status hc_native_conv_dw(const int32_t* fmap, int32_t fmap_layout, int64_t n_
                             int32_t c_in, const void* dy, int32_t c_out, float* dw_ref,
                             void* workspace, size_t ws_bytes, hc_stream stream);
 
+/* ---- Native net layers (voxel-major [N][C], C a multiple of 8) ----------------------
+ * The block operators of net.cpp:181-323 around the conv: max pool / unpool
+ * (cnn_ops.cpp:234-284, 336-372), batch norm + ReLU (cnn_ops.cpp:437-489, 542-561) and
+ * the final 2^3 dense pool (net.cpp:69-122). Switches are int8 field rows (-1 = empty).
+ *
+ * Pool map: hc_field_map(fine, coarse, {2,2,0,C,C}) -> [n_coarse][8] fine columns.
+ * hc_native_pool_parents inverts it (F == S fields tile the fine level): parent[g] =
+ * coarse column covering g or -1, prow[g] = g's field row in it. */
+hc_status hc_native_pool_parents(const int32_t* pmap, int64_t n_coarse, int32_t fd, int64_t n_fine,
+                                 int32_t* parent, int8_t* prow, hc_stream stream);
+/* y[p][c] = max over present field rows (first seeds, strict '>'), 0 if empty; switches[p][c]
+ * = winning row or -1 (cnn_ops.cpp:234-284). x, y: dtype (bf16 or f32), fd must be 8. */
+hc_status hc_native_max_pool(const int32_t* pmap, int64_t n_coarse, int32_t fd, const void* x,
+                             hc_dtype dtype, int32_t c, void* y, int8_t* switches, hc_stream stream);
+/* dx[g][c] = dy[parent[g]][c] if switches[parent[g]][c] == prow[g], else 0 (cnn_ops.cpp:336-372). */
+hc_status hc_native_max_unpool(const int32_t* parent, const int8_t* prow, int64_t n_fine, const void* dy,
+                               hc_dtype dtype, int32_t c, const int8_t* switches, void* dx,
+                               hc_stream stream);
+/* Training-mode batch norm over the N rows + ReLU: batch mean / biased variance (double,
+ * two-pass), running stats updated with `momentum`, inv_std = 1/sqrt(var + eps);
+ * xhat (fp32, optional) = (x - mean) * inv_std, out_bf16 = max(0, xhat). */
+size_t hc_native_bn_workspace(int64_t n, int32_t c);
+hc_status hc_native_bn_relu_forward(const float* x, int64_t n, int32_t c, int32_t training,
+                                    float momentum, float eps, float* running_mean, float* running_var,
+                                    float* inv_std, float* xhat, void* out_bf16, void* workspace,
+                                    size_t ws_bytes, hc_stream stream);
+/* d_conv = inv_std * (g - sum(g)/n - xhat * sum(g*xhat)/n), g = d_relu * (xhat > 0), bf16 out. */
+hc_status hc_native_bn_relu_backward(const void* d_relu, hc_dtype dtype, const float* xhat,
+                                     const float* inv_std, int64_t n, int32_t c, void* d_conv_bf16,
+                                     void* workspace, size_t ws_bytes, hc_stream stream);
+/* Final dense pool: cmap [b][8 cells][8 children] resolution-4 columns (or -1); head
+ * [(c*8 + cell)][b] fp32 = max over present children, src = winning column or -1. */
+hc_status hc_native_dense_pool(const int32_t* cmap, int32_t b, const void* x_bf16, int32_t c,
+                               float* head, int32_t* src, hc_stream stream);
+hc_status hc_native_dense_pool_backward(const float* d_head, const int32_t* src, int32_t b, int32_t c,
+                                        int64_t n_fine, float* dx, hc_stream stream);
+/* SGD with momentum and weight decay (net.cpp:339-346): v = momentum*v + lr*(g + wd*w); w -= v. */
+hc_status hc_native_sgd_update(float* w, float* v, const float* g, int64_t n, float lr, float momentum,
+                               float weight_decay, hc_stream stream);
+
 /* Boundary transposes between the reference layout (C x N fp32) and the native layout. */
 hc_status hc_native_to_voxel_major(const float* ref, int64_t c, int64_t n, void* out_bf16,
                                    hc_stream stream);

@@ -420,6 +420,14 @@ class Ref:
             self.lib.hcref_random_matrix_f64(rows, cols, seed, lo, hi, _ptr(out))
         return out
 
+    # ---------------------------------------------------------------- net (net.cpp)
+    def net_make(self, level_max: int, classes: int, seed: int, input_channels: int = 3) -> "RefNet":
+        """net.cpp:135-180 make_graph<float>."""
+        L = self.lib
+        L.hcref_net_make.restype = C.c_void_p
+        L.hcref_net_make.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_int]
+        return RefNet(self, self._handle(L.hcref_net_make(level_max, classes, seed, input_channels)))
+
     # ---------------------------------------------------------------- ops
     @staticmethod
     def _suf(dtype):
@@ -604,6 +612,71 @@ class RefPsh:
             self.ref.lib.hcref_psh_free(self.h)
         except Exception:
             pass
+
+
+class RefNet:
+    """Reference LayerGraph<float> (net.hpp:40-60) behind the shim: weights out, one
+    net_loss_and_gradients call (net.cpp:260-323, training mode) at a time."""
+
+    def __init__(self, ref: "Ref", h):
+        self.ref, self.h = ref, h
+        L = ref.lib
+        L.hcref_net_blocks.argtypes = [C.c_void_p]
+        L.hcref_net_conv_shape.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        L.hcref_net_get_conv.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        L.hcref_net_get_bn.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+        L.hcref_net_get_fc.argtypes = [C.c_void_p] * 5
+        L.hcref_net_set_dropout.argtypes = [C.c_void_p, C.c_float]
+        L.hcref_net_loss_grads.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p,
+                                           C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.hcref_net_free.argtypes = [C.c_void_p]
+        self.nblocks = int(L.hcref_net_blocks(h))
+        self.shapes = []
+        for i in range(self.nblocks):
+            rc = np.zeros(2, np.int64)
+            L.hcref_net_conv_shape(h, i, _ptr(rc))
+            self.shapes.append((int(rc[0]), int(rc[1])))
+
+    def conv(self, i: int) -> np.ndarray:
+        w = np.empty(self.shapes[i], np.float32)
+        self.ref.lib.hcref_net_get_conv(self.h, i, _ptr(w))
+        return w
+
+    def bn(self, i: int):
+        c = self.shapes[i][0]
+        m, v = np.empty(c, np.float32), np.empty(c, np.float32)
+        self.ref.lib.hcref_net_get_bn(self.h, i, _ptr(m), _ptr(v))
+        return m, v
+
+    def fc(self, classes: int, head_in: int):
+        w1, b1 = np.empty((128, head_in), np.float32), np.empty(128, np.float32)
+        w2, b2 = np.empty((classes, 128), np.float32), np.empty(classes, np.float32)
+        self.ref.lib.hcref_net_get_fc(self.h, _ptr(w1), _ptr(b1), _ptr(w2), _ptr(b2))
+        return w1, b1, w2, b2
+
+    def set_dropout(self, ratio: float):
+        self.ref.lib.hcref_net_set_dropout(self.h, ratio)
+
+    def loss_and_gradients(self, levels, labels, classes: int, head_in: int):
+        arr = (C.c_void_p * len(levels))(*[lv.h for lv in levels])
+        labels = np.ascontiguousarray(labels, np.int32)
+        loss = np.zeros(1, np.float32)
+        cg = np.empty(sum(r * c for r, c in self.shapes), np.float32)
+        w1, b1 = np.empty((128, head_in), np.float32), np.empty(128, np.float32)
+        w2, b2 = np.empty((classes, 128), np.float32), np.empty(classes, np.float32)
+        self.ref._check(self.ref.lib.hcref_net_loss_grads(self.h, arr, len(levels), _ptr(labels), labels.size,
+                                                          _ptr(loss), _ptr(cg), _ptr(w1), _ptr(b1), _ptr(w2),
+                                                          _ptr(b2)))
+        grads, o = [], 0
+        for r, c in self.shapes:
+            grads.append(cg[o:o + r * c].reshape(r, c))
+            o += r * c
+        return float(loss[0]), grads, (w1, b1, w2, b2)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.ref.lib.hcref_net_free(self.h)
+            self.h = None
 
 
 class RefSuper(SuperArrays):

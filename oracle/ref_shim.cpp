@@ -407,4 +407,59 @@ int hcref_serial_max_pool(const void* in, const float* data, std::int64_t dr, st
     });
 }
 
+// ---------------------------------------------------------------- net (net.cpp)
+// net.cpp:135-180 make_graph<float>
+void* hcref_net_make(int level_max, int classes, std::uint64_t seed, int input_channels) {
+    void* r = nullptr;
+    guarded([&] { r = new LayerGraph(make_graph<float>(level_max, classes, seed, input_channels)); });
+    return r;
+}
+void hcref_net_free(void* g) { delete static_cast<LayerGraph*>(g); }
+int hcref_net_blocks(const void* g) { return (int)static_cast<const LayerGraph*>(g)->blocks.size(); }
+// block i conv weights (rows x cols = C_out x C_in*27, KernelWeightsT layout cnn_ops.hpp:21-27)
+void hcref_net_conv_shape(const void* g, int i, std::int64_t* rc) {
+    const auto& w = static_cast<const LayerGraph*>(g)->blocks[i].conv.w;
+    rc[0] = w.rows;
+    rc[1] = w.cols;
+}
+void hcref_net_get_conv(const void* g, int i, float* w) { out(static_cast<const LayerGraph*>(g)->blocks[i].conv.w, w); }
+void hcref_net_get_bn(const void* g, int i, float* mean, float* var) {
+    const auto& bn = static_cast<const LayerGraph*>(g)->blocks[i].bn;
+    std::memcpy(mean, bn.running_mean.data(), bn.running_mean.size() * 4);
+    std::memcpy(var, bn.running_var.data(), bn.running_var.size() * 4);
+}
+void hcref_net_get_fc(const void* g, float* w1, float* b1, float* w2, float* b2) {
+    const auto* G = static_cast<const LayerGraph*>(g);
+    out(G->fc1.weights, w1);
+    std::memcpy(b1, G->fc1.bias.data(), G->fc1.bias.size() * 4);
+    out(G->fc2.weights, w2);
+    std::memcpy(b2, G->fc2.bias.data(), G->fc2.bias.size() * 4);
+}
+void hcref_net_set_dropout(void* g, float ratio) { static_cast<LayerGraph*>(g)->dropout_ratio = ratio; }
+// net.cpp:260-323 net_loss_and_gradients, training mode (running stats updated); the batch
+// is the given super-PSH levels (finest first, finest carrying the input data array).
+// conv_grads: the blocks' C_out x C_in*27 gradients concatenated.
+int hcref_net_loss_grads(void* g, const void* const* levels, int nlevels, const int* labels, int b, float* loss,
+                         float* conv_grads, float* fc1w, float* fc1b, float* fc2w, float* fc2b) {
+    return guarded([&] {
+        auto* G = static_cast<LayerGraph*>(g);
+        MultiLevelBatch batch;
+        for (int i = 0; i < nlevels; ++i) batch.levels.push_back(S(levels[i]));
+        NetRunOptions opt;
+        opt.training = true;
+        opt.update_running_stats = true;
+        NetGradientsT<float> grads;
+        *loss = net_loss_and_gradients(*G, batch, std::vector<int>(labels, labels + b), opt, &grads);
+        float* dst = conv_grads;
+        for (const auto& m : grads.conv) {
+            out(m, dst);
+            dst += m.values.size();
+        }
+        out(grads.fc1_w, fc1w);
+        std::memcpy(fc1b, grads.fc1_b.data(), grads.fc1_b.size() * 4);
+        out(grads.fc2_w, fc2w);
+        std::memcpy(fc2b, grads.fc2_b.data(), grads.fc2_b.size() * 4);
+    });
+}
+
 }  // extern "C"

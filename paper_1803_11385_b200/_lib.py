@@ -97,7 +97,18 @@ _SIGS.update({
     "hc_native_conv_dw": [_P, _I32, _I64, _I32, _P, _I32, _P, _I32, _P, _P, C.c_size_t, _P],
     "hc_native_to_voxel_major": [_P, _I64, _I64, _P, _P],
     "hc_native_to_channel_major": [_P, C.c_int, _I64, _I64, _P, _P],
+    "hc_native_pool_parents": [_P, _I64, _I32, _I64, _P, _P, _P],
+    "hc_native_max_pool": [_P, _I64, _I32, _P, C.c_int, _I32, _P, _P, _P],
+    "hc_native_max_unpool": [_P, _P, _I64, _P, C.c_int, _I32, _P, _P, _P],
+    "hc_native_bn_relu_forward": [_P, _I64, _I32, _I32, C.c_float, C.c_float, _P, _P, _P, _P, _P, _P, C.c_size_t,
+                                  _P],
+    "hc_native_bn_relu_backward": [_P, C.c_int, _P, _P, _I64, _I32, _P, _P, C.c_size_t, _P],
+    "hc_native_dense_pool": [_P, _I32, _P, _I32, _P, _P, _P],
+    "hc_native_dense_pool_backward": [_P, _P, _I32, _I32, _I64, _P, _P],
+    "hc_native_sgd_update": [_P, _P, _P, _I64, C.c_float, C.c_float, C.c_float, _P],
 })
+lib.hc_native_bn_workspace.restype = C.c_size_t
+lib.hc_native_bn_workspace.argtypes = [_I64, _I32]
 lib.hc_native_packed_k.restype = C.c_int64
 lib.hc_native_packed_k.argtypes = [_I32, _I32]
 lib.hc_native_dw_workspace.restype = C.c_size_t

@@ -1,0 +1,483 @@
+// net_ops.cu — the native (voxel-major) layers around the hash conv: max pooling with
+// switches and its unpooling, batch norm + ReLU (forward and backward), and the final
+// 2^3 dense pool of the classification head. These are the net.cpp:181-323 block
+// operators (conv -> batch_norm -> relu -> max_pool, cnn_ops.cpp:234-284, 336-372,
+// 437-489, 542-561; final_dense_pool net.cpp:69-122) on [N][C] feature rows, so every
+// thread moves whole 16-byte channel chunks (8 bf16 or 4 fp32 channels) instead of
+// the reference layout's strided single channels.
+//
+// Pool maps come from hc_field_map (row-major [N_coarse][F^3], F = S = 2): field row t of
+// coarse voxel p is the fine column pmap[p][t] or -1. Pooling fields with F == S tile the
+// fine level, so every fine voxel has at most one parent; hc_native_pool_parents inverts
+// the map once per level pair (parent column + field row), which makes unpooling a
+// coalesced pull instead of a scatter.
+//
+// Batch statistics are reduced in a fixed order (per-block double partials, then one
+// ordered pass) -> deterministic; mean/var/inv_std follow cnn_ops.cpp:455-474 (two-pass,
+// biased variance, double accumulation, inv_std = 1/sqrt(var + eps)).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "hashconv_b200_native.h"
+#include "hc_internal.h"
+#include "hc_launch.cuh"
+
+namespace hcb {
+namespace {
+
+using bf16 = __nv_bfloat16;
+constexpr int kT = 256;
+
+// 8 channels of one row as floats (bf16: one 16-byte load; fp32: two)
+__device__ __forceinline__ void load8(const bf16* p, float (&v)[8]) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(h[i]);
+        v[2 * i] = f.x;
+        v[2 * i + 1] = f.y;
+    }
+}
+__device__ __forceinline__ void load8(const float* p, float (&v)[8]) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(p + 4));
+    v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
+}
+__device__ __forceinline__ void store8(bf16* p, const float (&v)[8]) {
+    uint4 u;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+    *reinterpret_cast<uint4*>(p) = u;
+}
+__device__ __forceinline__ void store8(float* p, const float (&v)[8]) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+}
+
+// ---------------------------------------------------------------------- pooling
+__global__ void k_pool_parents(const int* __restrict__ pmap, long long nc, int fd, int* __restrict__ parent,
+                               signed char* __restrict__ prow) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // over nc * fd
+    if (i >= nc * fd) return;
+    const int g = pmap[i];
+    if (g < 0) return;
+    parent[g] = (int)(i / fd);
+    prow[g] = (signed char)(i % fd);
+}
+
+// cnn_ops.cpp:234-284: per channel, the first present field row seeds the max and a
+// later row replaces it only if strictly greater; an empty field gives 0 and switch -1.
+template <typename T, int FD>
+__global__ void __launch_bounds__(kT) k_nmax_pool(const int* __restrict__ pmap, long long nc, const T* __restrict__ x,
+                                                 int C, T* __restrict__ y, signed char* __restrict__ sw) {
+    const int chunks = C >> 3;
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // over nc * chunks
+    if (i >= nc * chunks) return;
+    const long long p = i / chunks;
+    const int c0 = (int)(i - p * chunks) * 8;
+    float best[8];
+    int arg[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        best[e] = 0.0f;
+        arg[e] = -1;
+    }
+#pragma unroll
+    for (int t = 0; t < FD; ++t) {
+        const int g = __ldg(pmap + p * FD + t);
+        if (g < 0) continue;
+        float v[8];
+        load8(x + (long long)g * C + c0, v);
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+            if (arg[e] < 0 || v[e] > best[e]) {
+                best[e] = v[e];
+                arg[e] = t;
+            }
+    }
+    store8(y + p * C + c0, best);
+    char4 s0 = make_char4(arg[0], arg[1], arg[2], arg[3]), s1 = make_char4(arg[4], arg[5], arg[6], arg[7]);
+    *reinterpret_cast<int2*>(sw + p * C + c0) = make_int2(*reinterpret_cast<int*>(&s0), *reinterpret_cast<int*>(&s1));
+}
+
+// cnn_ops.cpp:336-372 with one covering output per fine voxel (F == S): the fine
+// voxel takes the coarse gradient where the coarse switch names its field row.
+template <typename T>
+__global__ void __launch_bounds__(kT) k_nmax_unpool(const int* __restrict__ parent, const signed char* __restrict__ prow,
+                                                   long long nf, const T* __restrict__ dy,
+                                                   const signed char* __restrict__ sw, int C, T* __restrict__ dx) {
+    const int chunks = C >> 3;
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // over nf * chunks
+    if (i >= nf * chunks) return;
+    const long long g = i / chunks;
+    const int c0 = (int)(i - g * chunks) * 8;
+    float o[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[e] = 0.0f;
+    const int p = __ldg(parent + g);
+    if (p >= 0) {
+        const int r = __ldg(prow + g);
+        float v[8];
+        load8(dy + (long long)p * C + c0, v);
+        const int2 s = __ldg(reinterpret_cast<const int2*>(sw + (long long)p * C + c0));
+        const signed char* sc = reinterpret_cast<const signed char*>(&s);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = sc[e] == r ? 0.0f + v[e] : 0.0f;
+    }
+    store8(dx + g * C + c0, o);
+}
+
+// ---------------------------------------------------------------------- batch norm + ReLU
+// Column partial sums over row blocks: thread (r, q) owns channel quad q of rows
+// r, r + R, ... inside the block's row range; partials [block][C] in double.
+// MODE 0: sum x; 1: sum (x - mean)^2; 2: (sum dyb, sum dyb*xhat) with dyb = dy*(xhat > 0).
+constexpr int kRowsPerBlock = 2048;
+
+template <int MODE, typename DT>
+__global__ void __launch_bounds__(kT) k_col_partials(const float* __restrict__ a, const DT* __restrict__ b, long long n,
+                                                    int C, const double* __restrict__ mean, double* __restrict__ part) {
+    const int quads = C >> 2;
+    const int R = kT / quads;  // rows in flight per block step
+    const int q = threadIdx.x % quads, r = threadIdx.x / quads;
+    __shared__ double red[2][kT * 4];
+    double s[4] = {0, 0, 0, 0}, t[4] = {0, 0, 0, 0};
+    if (r < R) {
+        const long long r0 = (long long)blockIdx.x * kRowsPerBlock;
+        const long long r1 = min(n, r0 + kRowsPerBlock);
+        double mu[4] = {0, 0, 0, 0};
+        if (MODE == 1)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) mu[e] = mean[q * 4 + e];
+        for (long long row = r0 + r; row < r1; row += R) {
+            const float4 x = __ldg(reinterpret_cast<const float4*>(a + row * C + q * 4));
+            const float xv[4] = {x.x, x.y, x.z, x.w};
+            if (MODE == 2) {
+                float dv[4];
+                if constexpr (sizeof(DT) == 2) {
+                    const uint2 u = __ldg(reinterpret_cast<const uint2*>(b + row * C + q * 4));
+                    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+                    const float2 f0 = __bfloat1622float2(h[0]), f1 = __bfloat1622float2(h[1]);
+                    dv[0] = f0.x, dv[1] = f0.y, dv[2] = f1.x, dv[3] = f1.y;
+                } else {
+                    const float4 d = __ldg(reinterpret_cast<const float4*>(b + row * C + q * 4));
+                    dv[0] = d.x, dv[1] = d.y, dv[2] = d.z, dv[3] = d.w;
+                }
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const double g = xv[e] > 0.0f ? (double)dv[e] : 0.0;
+                    s[e] += g;
+                    t[e] += g * xv[e];
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const double d = MODE == 1 ? (double)xv[e] - mu[e] : (double)xv[e];
+                    s[e] += MODE == 1 ? d * d : d;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        red[0][threadIdx.x * 4 + e] = s[e];
+        red[1][threadIdx.x * 4 + e] = t[e];
+    }
+    __syncthreads();
+    if (threadIdx.x < C) {  // fixed-order fold over the R row lanes of channel c
+        const int c = threadIdx.x, cq = c >> 2, ce = c & 3;
+        double u = 0, v = 0;
+        for (int rr = 0; rr < R; ++rr) {
+            u += red[0][(rr * quads + cq) * 4 + ce];
+            v += red[1][(rr * quads + cq) * 4 + ce];
+        }
+        part[((long long)blockIdx.x * 2 + 0) * C + c] = u;
+        part[((long long)blockIdx.x * 2 + 1) * C + c] = v;
+    }
+}
+
+// Fold the per-block partials in block order; MODE 0 -> mean, MODE 1 -> var and the
+// running-stat update (cnn_ops.cpp:463-470), MODE 2 -> backward sums.
+template <int MODE>
+__global__ void k_col_fold(const double* __restrict__ part, int blocks, long long n, int C, double* __restrict__ out0,
+                           double* __restrict__ out1, float* __restrict__ run_mean, float* __restrict__ run_var,
+                           float momentum, float eps, const double* __restrict__ mean, float* __restrict__ inv_std) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C) return;
+    double u = 0, v = 0;
+    for (int b = 0; b < blocks; ++b) {
+        u += part[((long long)b * 2 + 0) * C + c];
+        v += part[((long long)b * 2 + 1) * C + c];
+    }
+    if (MODE == 0) {
+        out0[c] = u / (double)n;
+    } else if (MODE == 1) {
+        const double var = u / (double)n;
+        out1[c] = var;
+        if (run_mean) {
+            run_mean[c] = (1.0f - momentum) * run_mean[c] + momentum * (float)mean[c];
+            run_var[c] = (1.0f - momentum) * run_var[c] + momentum * (float)var;
+        }
+        inv_std[c] = (float)(1.0 / sqrt(var + (double)eps));
+    } else {
+        out0[c] = u;
+        out1[c] = v;
+    }
+}
+
+// xhat = (x - mean) * inv_std (float, cnn_ops.cpp:472); out = relu(xhat) (bf16 for the
+// next layer); xhat kept (fp32) for the backward pass.
+__global__ void __launch_bounds__(kT) k_bn_relu_apply(const float* __restrict__ x, long long n, int C,
+                                                     const double* __restrict__ mean,
+                                                     const float* __restrict__ inv_std, float* __restrict__ xhat,
+                                                     bf16* __restrict__ out) {
+    const int chunks = C >> 3;
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n * chunks) return;
+    const long long row = i / chunks;
+    const int c0 = (int)(i - row * chunks) * 8;
+    float v[8], h[8], o[8];
+    load8(x + row * C + c0, v);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        h[e] = (v[e] - (float)mean[c0 + e]) * inv_std[c0 + e];
+        o[e] = fmaxf(0.0f, h[e]);
+    }
+    if (xhat) store8(xhat + row * C + c0, h);
+    store8(out + row * C + c0, o);
+}
+
+// dx = inv_std * (dyb - s1/n - xhat * s2/n), dyb = dy * (xhat > 0)  (cnn_ops.cpp:476-489
+// after relu_backward cnn_ops.cpp:553-561); bf16 out = the conv layer's output gradient.
+template <typename DT>
+__global__ void __launch_bounds__(kT) k_bn_relu_bwd_apply(const DT* __restrict__ dy, const float* __restrict__ xhat,
+                                                         long long n, int C, const double* __restrict__ s1,
+                                                         const double* __restrict__ s2,
+                                                         const float* __restrict__ inv_std, bf16* __restrict__ dx) {
+    const int chunks = C >> 3;
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n * chunks) return;
+    const long long row = i / chunks;
+    const int c0 = (int)(i - row * chunks) * 8;
+    float d[8], h[8], o[8];
+    load8(dy + row * C + c0, d);
+    load8(xhat + row * C + c0, h);
+    const double inv_n = 1.0 / (double)n;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const double g = h[e] > 0.0f ? (double)d[e] : 0.0;
+        o[e] = (float)((double)inv_std[c0 + e] * (g - s1[c0 + e] * inv_n - (double)h[e] * s2[c0 + e] * inv_n));
+    }
+    store8(dx + row * C + c0, o);
+}
+
+// ---------------------------------------------------------------------- final dense pool
+// net.cpp:69-106: per model v and dense parent cell q of the 2^3 grid, max over the present
+// resolution-4 children (first hit seeds, strict '>'); head_in[(c*8 + cell)][v], src = the
+// winning fine column (-1 when the cell's field is empty). cmap: [b][8][8] child columns.
+__global__ void k_dense_pool(const int* __restrict__ cmap, int b, const bf16* __restrict__ x, int C,
+                             float* __restrict__ head, int* __restrict__ src) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;  // over b * 8 * C
+    if (i >= b * 8 * C) return;
+    const int c = i % C, cell = (i / C) % 8, v = i / (8 * C);
+    const int* kids = cmap + (v * 8 + cell) * 8;
+    float best = 0.0f;
+    int col = -1;
+    for (int k = 0; k < 8; ++k) {
+        const int g = kids[k];
+        if (g < 0) continue;
+        const float val = __bfloat162float(x[(long long)g * C + c]);
+        if (col < 0 || val > best) {
+            best = val;
+            col = g;
+        }
+    }
+    head[(long long)(c * 8 + cell) * b + v] = col < 0 ? 0.0f : best;
+    src[(c * 8 + cell) * b + v] = col;
+}
+
+// net.cpp:108-122: dx[c][src] += d_head (each fine column is the source of at most one
+// (c, cell, v) entry per channel, so this is a plain scatter; dx pre-zeroed).
+__global__ void k_dense_pool_bwd(const float* __restrict__ dhead, const int* __restrict__ src, int b, int C,
+                                 float* __restrict__ dx) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;  // over C * 8 * b
+    if (i >= C * 8 * b) return;
+    const int col = src[i];
+    if (col < 0) return;
+    const int c = i / (8 * b);
+    dx[(long long)col * C + c] += dhead[i];
+}
+
+// net.cpp:339-346 sgd_update: v = momentum*v + lr*(g + wd*w); w -= v (separate fp32
+// roundings, as the reference's non-FMA build).
+__global__ void k_sgd(float* __restrict__ w, float* __restrict__ v, const float* __restrict__ g, long long n, float lr,
+                      float momentum, float wd) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float vi = __fadd_rn(__fmul_rn(momentum, v[i]), __fmul_rn(lr, __fadd_rn(g[i], __fmul_rn(wd, w[i]))));
+    v[i] = vi;
+    w[i] = __fsub_rn(w[i], vi);
+}
+
+void check_c8(int c) {
+    if (c <= 0 || c % 8 != 0) throw std::invalid_argument("native net ops: channels must be a multiple of 8");
+}
+
+}  // namespace
+}  // namespace hcb
+
+using namespace hcb;
+
+extern "C" {
+
+hc_status hc_native_pool_parents(const int32_t* pmap, int64_t n_coarse, int32_t fd, int64_t n_fine, int32_t* parent,
+                                 int8_t* prow, hc_stream stream) {
+    return guard([&] {
+        cudaStream_t s = as_stream(stream);
+        if (n_fine > 0) cuda_check(cudaMemsetAsync(parent, 0xFF, sizeof(int32_t) * n_fine, s), "memset");
+        if (n_coarse <= 0) return;
+        k_pool_parents<<<grid_for(n_coarse * fd, kT), kT, 0, s>>>(pmap, n_coarse, fd, parent,
+                                                                  reinterpret_cast<signed char*>(prow));
+        launched("pool parents");
+    });
+}
+
+hc_status hc_native_max_pool(const int32_t* pmap, int64_t n_coarse, int32_t fd, const void* x, hc_dtype dtype,
+                             int32_t c, void* y, int8_t* switches, hc_stream stream) {
+    return guard([&] {
+        check_c8(c);
+        if (fd != 8) throw std::invalid_argument("native max_pool: 2x2x2 fields (F = S = 2) only");
+        if (n_coarse <= 0) return;
+        cudaStream_t s = as_stream(stream);
+        const long long n = n_coarse * (c / 8);
+        signed char* sw = reinterpret_cast<signed char*>(switches);
+        if (dtype == HC_DTYPE_BF16)
+            k_nmax_pool<bf16, 8><<<grid_for(n, kT), kT, 0, s>>>(pmap, n_coarse, static_cast<const bf16*>(x), c,
+                                                                static_cast<bf16*>(y), sw);
+        else
+            k_nmax_pool<float, 8><<<grid_for(n, kT), kT, 0, s>>>(pmap, n_coarse, static_cast<const float*>(x), c,
+                                                                 static_cast<float*>(y), sw);
+        launched("native max_pool");
+    });
+}
+
+hc_status hc_native_max_unpool(const int32_t* parent, const int8_t* prow, int64_t n_fine, const void* dy,
+                               hc_dtype dtype, int32_t c, const int8_t* switches, void* dx, hc_stream stream) {
+    return guard([&] {
+        check_c8(c);
+        if (n_fine <= 0) return;
+        cudaStream_t s = as_stream(stream);
+        const long long n = n_fine * (c / 8);
+        const signed char* pr = reinterpret_cast<const signed char*>(prow);
+        const signed char* sw = reinterpret_cast<const signed char*>(switches);
+        if (dtype == HC_DTYPE_BF16)
+            k_nmax_unpool<bf16><<<grid_for(n, kT), kT, 0, s>>>(parent, pr, n_fine, static_cast<const bf16*>(dy), sw,
+                                                               c, static_cast<bf16*>(dx));
+        else
+            k_nmax_unpool<float><<<grid_for(n, kT), kT, 0, s>>>(parent, pr, n_fine, static_cast<const float*>(dy), sw,
+                                                                c, static_cast<float*>(dx));
+        launched("native max_unpool");
+    });
+}
+
+size_t hc_native_bn_workspace(int64_t n, int32_t c) {
+    const long long blocks = (n + kRowsPerBlock - 1) / kRowsPerBlock;
+    return (size_t)(blocks * 2 * c + 4 * c) * sizeof(double);
+}
+
+hc_status hc_native_bn_relu_forward(const float* x, int64_t n, int32_t c, int32_t training, float momentum, float eps,
+                                    float* running_mean, float* running_var, float* inv_std, float* xhat,
+                                    void* out_bf16, void* workspace, size_t ws_bytes, hc_stream stream) {
+    return guard([&] {
+        check_c8(c);
+        if (c > kT) throw std::invalid_argument("native batch norm: at most 256 channels");
+        if (n <= 0) throw std::invalid_argument("batch_norm: empty input");
+        if (ws_bytes < hc_native_bn_workspace(n, c)) throw std::invalid_argument("native batch norm: workspace too small");
+        cudaStream_t s = as_stream(stream);
+        const int blocks = (int)((n + kRowsPerBlock - 1) / kRowsPerBlock);
+        double* part = static_cast<double*>(workspace);
+        double* mean = part + (long long)blocks * 2 * c;
+        double* var = mean + c;
+        if (training) {
+            k_col_partials<0, float><<<blocks, kT, 0, s>>>(x, nullptr, n, c, nullptr, part);
+            k_col_fold<0><<<1, kT, 0, s>>>(part, blocks, n, c, mean, nullptr, nullptr, nullptr, 0, 0, nullptr, nullptr);
+            k_col_partials<1, float><<<blocks, kT, 0, s>>>(x, nullptr, n, c, mean, part);
+            k_col_fold<1><<<1, kT, 0, s>>>(part, blocks, n, c, nullptr, var, running_mean, running_var, momentum, eps,
+                                          mean, inv_std);
+            launched("batch-norm statistics", 4);
+        } else {
+            throw std::invalid_argument("native batch norm: inference mode uses the reference-layout path");
+        }
+        const long long m = n * (c / 8);
+        k_bn_relu_apply<<<grid_for(m, kT), kT, 0, s>>>(x, n, c, mean, inv_std, xhat, static_cast<bf16*>(out_bf16));
+        launched("batch-norm + relu");
+    });
+}
+
+hc_status hc_native_bn_relu_backward(const void* d_relu, hc_dtype dtype, const float* xhat, const float* inv_std,
+                                     int64_t n, int32_t c, void* d_conv_bf16, void* workspace, size_t ws_bytes,
+                                     hc_stream stream) {
+    return guard([&] {
+        check_c8(c);
+        if (c > kT) throw std::invalid_argument("native batch norm: at most 256 channels");
+        if (n <= 0) return;
+        if (ws_bytes < hc_native_bn_workspace(n, c)) throw std::invalid_argument("native batch norm: workspace too small");
+        cudaStream_t s = as_stream(stream);
+        const int blocks = (int)((n + kRowsPerBlock - 1) / kRowsPerBlock);
+        double* part = static_cast<double*>(workspace);
+        double* s1 = part + (long long)blocks * 2 * c;
+        double* s2 = s1 + c;
+        const long long m = n * (c / 8);
+        if (dtype == HC_DTYPE_BF16) {
+            const bf16* d = static_cast<const bf16*>(d_relu);
+            k_col_partials<2, bf16><<<blocks, kT, 0, s>>>(xhat, d, n, c, nullptr, part);
+            k_col_fold<2><<<1, kT, 0, s>>>(part, blocks, n, c, s1, s2, nullptr, nullptr, 0, 0, nullptr, nullptr);
+            k_bn_relu_bwd_apply<bf16><<<grid_for(m, kT), kT, 0, s>>>(d, xhat, n, c, s1, s2, inv_std,
+                                                                     static_cast<bf16*>(d_conv_bf16));
+        } else {
+            const float* d = static_cast<const float*>(d_relu);
+            k_col_partials<2, float><<<blocks, kT, 0, s>>>(xhat, d, n, c, nullptr, part);
+            k_col_fold<2><<<1, kT, 0, s>>>(part, blocks, n, c, s1, s2, nullptr, nullptr, 0, 0, nullptr, nullptr);
+            k_bn_relu_bwd_apply<float><<<grid_for(m, kT), kT, 0, s>>>(d, xhat, n, c, s1, s2, inv_std,
+                                                                      static_cast<bf16*>(d_conv_bf16));
+        }
+        launched("batch-norm + relu backward", 3);
+    });
+}
+
+hc_status hc_native_dense_pool(const int32_t* cmap, int32_t b, const void* x_bf16, int32_t c, float* head,
+                               int32_t* src, hc_stream stream) {
+    return guard([&] {
+        if (b <= 0 || c <= 0) return;
+        const int n = b * 8 * c;
+        k_dense_pool<<<grid_for(n, kT), kT, 0, as_stream(stream)>>>(cmap, b, static_cast<const bf16*>(x_bf16), c, head,
+                                                                    src);
+        launched("dense pool");
+    });
+}
+
+hc_status hc_native_dense_pool_backward(const float* d_head, const int32_t* src, int32_t b, int32_t c,
+                                        int64_t n_fine, float* dx, hc_stream stream) {
+    return guard([&] {
+        cudaStream_t s = as_stream(stream);
+        if (n_fine > 0) cuda_check(cudaMemsetAsync(dx, 0, sizeof(float) * n_fine * c, s), "memset");
+        if (b <= 0 || c <= 0) return;
+        const int n = c * 8 * b;
+        k_dense_pool_bwd<<<grid_for(n, kT), kT, 0, s>>>(d_head, src, b, c, dx);
+        launched("dense pool backward");
+    });
+}
+
+hc_status hc_native_sgd_update(float* w, float* v, const float* g, int64_t n, float lr, float momentum,
+                               float weight_decay, hc_stream stream) {
+    return guard([&] {
+        if (n <= 0) return;
+        k_sgd<<<grid_for(n, kT), kT, 0, as_stream(stream)>>>(w, v, g, n, lr, momentum, weight_decay);
+        launched("sgd update");
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,284 @@
+"""Native H-CNN classification net on the B200 path.
+
+The LeNet-style hierarchy of net.hpp:40-60 / net.cpp:181-375 — per level, finest to
+resolution 4: hash conv 3^3 -> batch norm -> ReLU -> 2^3 max pool; the last level's
+output goes through the final 2^3 dense pool, dropout -> FC(128) -> dropout ->
+FC(classes) -> softmax cross-entropy; SGD with momentum and weight decay — built from the
+native kernels: tcgen05 implicit-GEMM conv (conv.py), and voxel-major pooling, batch
+norm + ReLU, dense pool and SGD (csrc/net_ops.cu). The two FC layers (b x 1024 -> 128 ->
+classes) are plain cuBLAS GEMMs through torch.
+
+Layout: features are voxel-major [N][C]; channel counts are padded to the tensor-core
+tile set (input 3 -> 8 channels, 8 output channels -> 16) with zero weights, so padded
+channels stay exactly zero through conv, batch norm (xhat = 0), pooling and SGD.
+Field maps (conv K0 tile-major, pool maps and their inverses, the dense-pool child map)
+depend only on the batch's PSH tables and are built once per batch (`NetBatch`).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import conv as nconv
+from ._lib import check, lib
+from .ops import ConvSpec, field_map, locate
+from .psh import SuperPsh
+
+BF16 = torch.bfloat16
+
+
+def _p(t: torch.Tensor):
+    return C.c_void_p(t.data_ptr())
+
+
+def _s():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def channels_at_level(level: int) -> int:
+    """net.cpp:15-17: max{2, 2^(9-l)}."""
+    return max(2, 1 << max(0, 9 - level))
+
+
+def _pad_in(c: int) -> int:
+    return (c + 7) // 8 * 8
+
+
+def _pad_out(c: int) -> int:
+    for t in (16, 32, 64, 128, 256):
+        if c <= t:
+            return t
+    raise ValueError("native net: at most 256 channels per level")
+
+
+@dataclass
+class NetBatch:
+    """Device-side per-batch structure: one SuperPsh per level (finest first) plus the maps
+    every layer needs. Mirrors net.hpp:22-31 MultiLevelBatch."""
+
+    levels: List[SuperPsh]
+    conv_maps: list
+    pool_maps: list
+    parents: list
+    dense_children: torch.Tensor
+
+    @classmethod
+    def build(cls, levels: Sequence[SuperPsh]) -> "NetBatch":
+        levels = list(levels)
+        if levels[-1].resolution != 4:
+            raise RuntimeError("final pool expects the resolution-4 level")
+        conv_maps, pool_maps, parents = [], [], []
+        for i, s in enumerate(levels):
+            conv_maps.append(nconv.field_map_native(s, s, ConvSpec(3, 1, 0, 8, 8), nconv.TILED))
+            if i + 1 < len(levels):
+                c = levels[i + 1]
+                pm = field_map(s, c, ConvSpec(2, 2, 0, 8, 8))  # [N_coarse][8] fine columns
+                par = torch.empty(s.total_columns(), dtype=torch.int32, device="cuda")
+                prow = torch.empty(s.total_columns(), dtype=torch.int8, device="cuda")
+                check(lib.hc_native_pool_parents(_p(pm), pm.shape[0], 8, s.total_columns(), _p(par), _p(prow), _s()))
+                pool_maps.append(pm)
+                parents.append((par, prow))
+        # dense-pool children: [b][8 cells][8 kids] (net.cpp:76-88: cell q unflattened x-fastest,
+        # kids in (dz, dy, dx) order)
+        last = levels[-1]
+        b = last.batch
+        q = []
+        for v in range(1, b + 1):
+            for cell in range(8):
+                qx, qy, qz = cell & 1, (cell >> 1) & 1, (cell >> 2) & 1
+                for dz in range(2):
+                    for dy in range(2):
+                        for dx in range(2):
+                            q.append((v, qx * 2 + dx, qy * 2 + dy, qz * 2 + dz))
+        kids = locate(last, torch.tensor(q, dtype=torch.int32, device="cuda")).to(torch.int32)
+        return cls(levels, conv_maps, pool_maps, parents, kids.view(b, 8, 8).contiguous())
+
+    @property
+    def batch(self) -> int:
+        return self.levels[0].batch
+
+
+class NativeHashNet:
+    """net.hpp:40-60 LayerGraph + net.cpp training step on the native path."""
+
+    def __init__(self, level_max: int, num_classes: int, seed: int = 0, input_channels: int = 3,
+                 dropout: float = 0.5, lr: float = 0.1, momentum: float = 0.9, weight_decay: float = 5e-4,
+                 bn_momentum: float = 0.1, bn_eps: float = 1e-5):
+        if level_max < 2 or level_max > 16:
+            raise ValueError("level_max out of range")
+        if num_classes < 2:
+            raise ValueError("need at least two classes")
+        self.level_max, self.num_classes, self.input_channels = level_max, num_classes, input_channels
+        self.dropout, self.lr, self.momentum, self.wd = dropout, lr, momentum, weight_decay
+        self.bn_momentum, self.bn_eps = bn_momentum, bn_eps
+        g = torch.Generator(device="cuda").manual_seed(seed)
+        self.blocks = []
+        for lvl in range(level_max, 1, -1):
+            cin = input_channels if lvl == level_max else channels_at_level(lvl + 1)
+            cout = channels_at_level(lvl)
+            cin_p = _pad_in(cin) if lvl == level_max else _pad_out(cin)
+            cout_p = _pad_out(cout)
+            bound = math.sqrt(6.0 / (cin * 27 + cout * 27))  # net.cpp:60-65 xavier (fan = C*27)
+            w = torch.zeros((cout_p, cin_p * 27), device="cuda")
+            wr = (torch.rand((cout, cin * 27), device="cuda", generator=g) * 2 - 1) * bound
+            w.view(cout_p, cin_p, 27)[:cout, :cin] = wr.view(cout, cin, 27)
+            self.blocks.append(dict(level=lvl, cin=cin, cout=cout, cin_p=cin_p, cout_p=cout_p, w=w,
+                                    v=torch.zeros_like(w),
+                                    run_mean=torch.zeros(cout_p, device="cuda"),
+                                    run_var=torch.ones(cout_p, device="cuda"),  # cnn_ops.hpp:125-127
+                                    inv_std=torch.empty(cout_p, device="cuda")))
+        head_in = channels_at_level(2) * 8
+        b1 = math.sqrt(6.0 / (head_in + 128))
+        b2 = math.sqrt(6.0 / (128 + num_classes))
+        self.fc1_w = (torch.rand((128, head_in), device="cuda", generator=g) * 2 - 1) * b1
+        self.fc1_b = torch.zeros(128, device="cuda")
+        self.fc2_w = (torch.rand((num_classes, 128), device="cuda", generator=g) * 2 - 1) * b2
+        self.fc2_b = torch.zeros(num_classes, device="cuda")
+        self.head_v = [torch.zeros_like(t) for t in (self.fc1_w, self.fc1_b, self.fc2_w, self.fc2_b)]
+        self._ws = {}
+        self._dw_ws = nconv.DwWorkspace()
+        self._gen = torch.Generator(device="cuda").manual_seed(seed + 1)
+
+    # ------------------------------------------------------------------ helpers
+    def reference_weights(self, i: int) -> torch.Tensor:
+        """Block i's conv weights in the reference layout W[co][ci*27 + t] (unpadded)."""
+        b = self.blocks[i]
+        return b["w"].view(b["cout_p"], b["cin_p"], 27)[:b["cout"], :b["cin"]].reshape(b["cout"], b["cin"] * 27)
+
+    def set_reference_weights(self, i: int, w_ref: torch.Tensor) -> None:
+        b = self.blocks[i]
+        b["w"].zero_()
+        b["w"].view(b["cout_p"], b["cin_p"], 27)[:b["cout"], :b["cin"]] = w_ref.view(b["cout"], b["cin"], 27)
+
+    def _bn_ws(self, n: int, c: int) -> torch.Tensor:
+        nbytes = int(lib.hc_native_bn_workspace(n, c))
+        t = self._ws.get("bn")
+        if t is None or t.numel() < nbytes:
+            t = torch.empty(max(nbytes, 16), dtype=torch.uint8, device="cuda")
+            self._ws["bn"] = t
+        return t
+
+    def input_features(self, ref: torch.Tensor) -> torch.Tensor:
+        """Finest-level data (C x N fp32, psh data array) -> padded voxel-major bf16."""
+        c, n = ref.shape
+        x = torch.zeros((n, self.blocks[0]["cin_p"]), dtype=BF16, device="cuda")
+        x[:, :c] = nconv.to_voxel_major(ref)
+        return x
+
+    # ------------------------------------------------------------------ forward / backward
+    def forward(self, nb: NetBatch, x: torch.Tensor, training: bool = True, cache: Optional[dict] = None):
+        """net.cpp:181-258 net_forward (training mode): class scores (classes x b)."""
+        if not training:
+            raise ValueError("native net: training-mode forward (inference uses running stats: reference path)")
+        acts = []
+        for i, blk in enumerate(self.blocks):
+            s = nb.levels[i]
+            n = s.total_columns()
+            wf = nconv.pack_weights(blk["w"], blk["cout_p"], blk["cin_p"], 27, False)
+            y = nconv.gather_gemm(nb.conv_maps[i], x, wf, blk["cout_p"], torch.float32)
+            xhat = torch.empty_like(y)
+            r = torch.empty((n, blk["cout_p"]), dtype=BF16, device="cuda")
+            ws = self._bn_ws(n, blk["cout_p"])
+            check(lib.hc_native_bn_relu_forward(_p(y), n, blk["cout_p"], 1, self.bn_momentum, self.bn_eps,
+                                                _p(blk["run_mean"]), _p(blk["run_var"]), _p(blk["inv_std"]),
+                                                _p(xhat), _p(r), _p(ws), ws.numel(), _s()))
+            acts.append(dict(x=x, xhat=xhat))
+            if i + 1 < len(self.blocks):
+                pm = nb.pool_maps[i]
+                nc = pm.shape[0]
+                pooled = torch.empty((nc, blk["cout_p"]), dtype=BF16, device="cuda")
+                sw = torch.empty((nc, blk["cout_p"]), dtype=torch.int8, device="cuda")
+                check(lib.hc_native_max_pool(_p(pm), nc, 8, _p(r), _lib.HC_DTYPE_BF16, blk["cout_p"], _p(pooled),
+                                             _p(sw), _s()))
+                acts[-1]["sw"] = sw
+                x = pooled
+            else:
+                b = nb.batch
+                c = blk["cout_p"]
+                head = torch.empty((c * 8, b), device="cuda")
+                src = torch.empty((c * 8, b), dtype=torch.int32, device="cuda")
+                check(lib.hc_native_dense_pool(_p(nb.dense_children), b, _p(r), c, _p(head), _p(src), _s()))
+                acts[-1]["src"] = src
+                x = head
+        # head: dropout -> FC(128) -> dropout -> FC(classes)   (net.cpp:236-251)
+        keep = 1.0 - self.dropout
+        m1 = (torch.rand(x.shape, device="cuda", generator=self._gen) < keep).float() / keep
+        fc1_in = x * m1
+        fc1_out = self.fc1_w @ fc1_in + self.fc1_b[:, None]
+        m2 = (torch.rand(fc1_out.shape, device="cuda", generator=self._gen) < keep).float() / keep
+        fc2_in = fc1_out * m2
+        scores = self.fc2_w @ fc2_in + self.fc2_b[:, None]
+        if cache is not None:
+            cache.update(acts=acts, m1=m1, m2=m2, fc1_in=fc1_in, fc2_in=fc2_in)
+        return scores
+
+    def loss_and_gradients(self, nb: NetBatch, x: torch.Tensor, labels: torch.Tensor):
+        """net.cpp:260-323: softmax cross-entropy (mean over the batch), gradients of every
+        conv and FC weight; returns (loss tensor, conv weight gradients (padded ref layout))."""
+        cache = {}
+        scores = self.forward(nb, x, True, cache)
+        b = scores.shape[1]
+        logp = torch.log_softmax(scores.double(), dim=0)
+        loss = -logp[labels, torch.arange(b, device="cuda")].mean()
+        dscores = torch.softmax(scores.double(), dim=0)
+        dscores[labels, torch.arange(b, device="cuda")] -= 1.0
+        dscores = (dscores / b).float()
+        g_fc2_w = dscores @ cache["fc2_in"].t()
+        g_fc2_b = dscores.sum(1)
+        d_fc1_out = (self.fc2_w.t() @ dscores) * cache["m2"]
+        g_fc1_w = d_fc1_out @ cache["fc1_in"].t()
+        g_fc1_b = d_fc1_out.sum(1)
+        d_head = ((self.fc1_w.t() @ d_fc1_out) * cache["m1"]).contiguous()
+        acts = cache["acts"]
+        conv_grads = [None] * len(self.blocks)
+        d_relu, d_dtype = None, None
+        for i in range(len(self.blocks) - 1, -1, -1):
+            blk, a = self.blocks[i], acts[i]
+            s = nb.levels[i]
+            n, c = s.total_columns(), blk["cout_p"]
+            if i == len(self.blocks) - 1:  # net.cpp:301-304 final_dense_pool_backward
+                d_relu = torch.empty((n, c), device="cuda")
+                check(lib.hc_native_dense_pool_backward(_p(d_head), _p(a["src"]), nb.batch, c, n, _p(d_relu), _s()))
+                d_dtype = _lib.HC_DTYPE_F32
+            d_conv = torch.empty((n, c), dtype=BF16, device="cuda")
+            ws = self._bn_ws(n, c)
+            check(lib.hc_native_bn_relu_backward(_p(d_relu), d_dtype, _p(a["xhat"]), _p(blk["inv_std"]), n, c,
+                                                 _p(d_conv), _p(ws), ws.numel(), _s()))
+            conv_grads[i] = nconv.conv_dw(nb.conv_maps[i], a["x"], d_conv, self._dw_ws)
+            # input gradient (net.cpp:316-317; the finest one is the net's input gradient, g.input).
+            # The tensor-core tile set starts at 16 output channels: an 8-channel input level
+            # takes its gradient through a zero-padded 16-channel kernel.
+            cin_g = max(16, blk["cin_p"])
+            w = blk["w"]
+            if cin_g != blk["cin_p"]:
+                w = torch.zeros((blk["cout_p"], cin_g * 27), device="cuda")
+                w.view(blk["cout_p"], cin_g, 27)[:, :blk["cin_p"]] = blk["w"].view(blk["cout_p"], blk["cin_p"], 27)
+            wb = nconv.pack_weights(w, blk["cout_p"], cin_g, 27, True)
+            dx = nconv.gather_gemm(nb.conv_maps[i], d_conv, wb, cin_g, BF16)[:, :blk["cin_p"]]
+            if i > 0:  # net.cpp:296-300: unpool through the finer level's switches
+                prev = self.blocks[i - 1]
+                par, prow = nb.parents[i - 1]
+                nf = nb.levels[i - 1].total_columns()
+                d_relu = torch.empty((nf, prev["cout_p"]), dtype=BF16, device="cuda")
+                check(lib.hc_native_max_unpool(_p(par), _p(prow), nf, _p(dx), _lib.HC_DTYPE_BF16, prev["cout_p"],
+                                               _p(acts[i - 1]["sw"]), _p(d_relu), _s()))
+                d_dtype = _lib.HC_DTYPE_BF16
+        head_grads = (g_fc1_w, g_fc1_b, g_fc2_w, g_fc2_b)
+        return loss, conv_grads, head_grads
+
+    def train_step(self, nb: NetBatch, x: torch.Tensor, labels: torch.Tensor):
+        """net.cpp:349-375 train_step: loss + SGD with momentum and weight decay."""
+        loss, conv_grads, head_grads = self.loss_and_gradients(nb, x, labels)
+        for blk, g in zip(self.blocks, conv_grads):
+            check(lib.hc_native_sgd_update(_p(blk["w"]), _p(blk["v"]), _p(g), g.numel(), self.lr, self.momentum,
+                                           self.wd, _s()))
+        for w, v, g in zip((self.fc1_w, self.fc1_b, self.fc2_w, self.fc2_b), self.head_v, head_grads):
+            g = g.contiguous()
+            check(lib.hc_native_sgd_update(_p(w), _p(v), _p(g), g.numel(), self.lr, self.momentum, self.wd, _s()))
+        return loss
