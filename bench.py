@@ -51,6 +51,10 @@ def parse():
     p.add_argument("--path", default="fused", choices=["materialized", "fused"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--workload", default="conv", choices=["conv", "net"],
+                   help="conv: one hash-conv layer fwd+bwd (the BASELINE metric); net: a full H-CNN "
+                        "classification train step (BASELINE configs 2/3)")
+    p.add_argument("--classes", type=int, default=40)
     return p.parse_args()
 
 
@@ -314,6 +318,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
+    if args.workload == "net":
+        return net_main(args, rank, world, local)
     if args.impl == "reference":
         return reference_arm(args, rank, world)
 
@@ -526,6 +532,124 @@ def reference_arm(args, rank, world):
                    "res": args.res, "c_in": args.cin, "c_out": args.cout, "sample_voxels_per_step": n1},
         "cpu_baseline": {"value": value, "unit": "voxels/s", "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "voxels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+
+
+# ------------------------------------------------------------------ net workload
+def shell_pyramid(res: int):
+    """build_pyramid (net.cpp:19-32) of the synthetic shell, cached as .psh."""
+    from paper_1803_11385_b200.psh import VoxelSet, build_pyramid, read_psh_file, write_psh_file
+    os.makedirs(CACHE, exist_ok=True)
+    path = os.path.join(CACHE, f"shell{res}_pyramid.psh")
+    if os.path.exists(path):
+        lv = read_psh_file(path)
+        if lv and lv[0].resolution == res and lv[-1].resolution == 4:
+            return lv
+    lv = build_pyramid(VoxelSet.sphere(res, True), 1)
+    write_psh_file(path + ".tmp", lv)
+    os.replace(path + ".tmp", path)
+    return lv
+
+
+def cpu_net_sample(res: int, b: int, classes: int):
+    """The reference net's net_loss_and_gradients (net.cpp:260-323) on b shell copies."""
+    from oracle.oracle import Ref
+    ref = Ref()
+    s = ref.sphere_set(res, True)
+    levels, cur, i = [], s, 0
+    while True:
+        levels.append(ref.build_psh(cur, 0))
+        if cur.resolution == 4:
+            break
+        cur = ref.coarsen(cur)
+        i += 1
+    supers = [ref.build_super([lv] * b) for lv in levels]
+    lmax = int(round(np.log2(res)))
+    rn = ref.net_make(lmax, classes, 7)
+    labels = np.arange(b, dtype=np.int32) % classes
+    t0 = time.perf_counter()
+    rn.loss_and_gradients(supers, labels, classes, 1024)
+    return time.perf_counter() - t0, ref.max_threads()
+
+
+def net_main(args, rank, world, local):
+    """H-CNN classification train step (net.cpp:349-375) on the native path: per-batch maps +
+    forward + loss + backward + SGD; b shells per GPU, weight gradients all-reduced."""
+    import torch
+    import torch.distributed as dist
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        b = 2
+        secs, cores = cpu_net_sample(args.res, b, args.classes)
+        v = b / secs
+        print(json.dumps({"impl": "reference", "metric": "hcnn train step shapes/sec", "value": v,
+                          "unit": "shapes/s", "n_gpus": world, "steps": 1, "warmup": 0, "ms_per_step": secs * 1e3,
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                          "data": "synthetic", "config": {"workload": f"hcnn net {args.res}^3 x {b} shells"},
+                          "cpu_baseline": {"value": v, "unit": "shapes/s", "cores": cores, "kind": "reference",
+                                           "sample": f"{b} shells, loss+gradients"},
+                          "e2e": {"value": v, "unit": "shapes/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}))
+        return
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_1803_11385_b200 import _lib
+    from paper_1803_11385_b200 import net as nnet
+    from paper_1803_11385_b200.dist import allreduce_gradients
+    from paper_1803_11385_b200.psh import SuperPsh
+    pyr = shell_pyramid(args.res)
+    b = args.shapes_per_gpu
+    lmax = int(round(np.log2(args.res)))
+    levels = [SuperPsh.from_levels([lv] * b) for lv in pyr]
+    feats = np.concatenate([pyr[0].arrays()[3]] * b, axis=1)
+    net = nnet.NativeHashNet(lmax, args.classes, seed=rank)
+    x = net.input_features(torch.from_numpy(np.ascontiguousarray(feats)).to(dev))
+    labels = torch.randint(0, args.classes, (b,), device=dev)
+    voxels = sum(s.total_columns() for s in levels)
+
+    def one():
+        nb = nnet.NetBatch.build(levels)  # the batch's K0 / pool / dense-pool maps: per step
+        return net.train_step(nb, x, labels, allreduce_gradients, b * world)
+
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:  # sampling spans warm-up and the timed region
+        for _ in range(max(3, args.warmup)):
+            one()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        launches0 = _lib.lib.hc_launch_count()
+        st.record()
+        for _ in range(args.steps):
+            one()
+        en.record()
+        torch.cuda.synchronize()
+        launches = _lib.lib.hc_launch_count() - launches0
+    t = torch.tensor([st.elapsed_time(en) / args.steps], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            secs, cores = cpu_net_sample(args.res, 2, args.classes)
+            cpu = {"value": 2 / secs, "unit": "shapes/s", "cores": cores, "kind": "reference",
+                   "sample": "2 shells, net_loss_and_gradients"}
+        print(json.dumps({
+            "metric": "hcnn train step shapes/sec", "value": b * world / (ms / 1e3), "unit": "shapes/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (sphere shell pyramid, bench.cpp:33-77; random labels)",
+            "config": {"workload": f"hcnn classification net {args.res}^3, {lmax - 1} conv/pool levels, "
+                                   f"{b} shells/GPU", "res": args.res, "global_batch": b * world,
+                       "classes": args.classes, "voxels_per_gpu_all_levels": voxels,
+                       "parallelism": f"dp{world}"},
+            "voxels_per_s": voxels * world / (ms / 1e3), "cpu_baseline": cpu, "gpu_launches": int(launches),
+            "clocks": clk.summary()}))
+    if world > 1:
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

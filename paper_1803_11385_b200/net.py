@@ -57,6 +57,24 @@ def _pad_out(c: int) -> int:
     raise ValueError("native net: at most 256 channels per level")
 
 
+_QUERIES = {}
+
+
+def _dense_queries(b: int) -> torch.Tensor:
+    """{model, x, y, z} of every (model, cell, child) of the final dense pool (device, cached)."""
+    if b not in _QUERIES:
+        q = []
+        for v in range(1, b + 1):
+            for cell in range(8):
+                qx, qy, qz = cell & 1, (cell >> 1) & 1, (cell >> 2) & 1
+                for dz in range(2):
+                    for dy in range(2):
+                        for dx in range(2):
+                            q.append((v, qx * 2 + dx, qy * 2 + dy, qz * 2 + dz))
+        _QUERIES[b] = torch.tensor(q, dtype=torch.int32, device="cuda")
+    return _QUERIES[b]
+
+
 @dataclass
 class NetBatch:
     """Device-side per-batch structure: one SuperPsh per level (finest first) plus the maps
@@ -88,15 +106,7 @@ class NetBatch:
         # kids in (dz, dy, dx) order)
         last = levels[-1]
         b = last.batch
-        q = []
-        for v in range(1, b + 1):
-            for cell in range(8):
-                qx, qy, qz = cell & 1, (cell >> 1) & 1, (cell >> 2) & 1
-                for dz in range(2):
-                    for dy in range(2):
-                        for dx in range(2):
-                            q.append((v, qx * 2 + dx, qy * 2 + dy, qz * 2 + dz))
-        kids = locate(last, torch.tensor(q, dtype=torch.int32, device="cuda")).to(torch.int32)
+        kids = locate(last, _dense_queries(b)).to(torch.int32)
         return cls(levels, conv_maps, pool_maps, parents, kids.view(b, 8, 8).contiguous())
 
     @property
@@ -218,9 +228,12 @@ class NativeHashNet:
             cache.update(acts=acts, m1=m1, m2=m2, fc1_in=fc1_in, fc2_in=fc2_in)
         return scores
 
-    def loss_and_gradients(self, nb: NetBatch, x: torch.Tensor, labels: torch.Tensor):
+    def loss_and_gradients(self, nb: NetBatch, x: torch.Tensor, labels: torch.Tensor,
+                           global_batch: Optional[int] = None):
         """net.cpp:260-323: softmax cross-entropy (mean over the batch), gradients of every
-        conv and FC weight; returns (loss tensor, conv weight gradients (padded ref layout))."""
+        conv and FC weight; returns (loss tensor, conv weight gradients (padded ref layout),
+        FC gradients). With data parallelism the scores' gradient is divided by the GLOBAL
+        batch (net.cpp:281 divides by b; shards must not divide by their local b)."""
         cache = {}
         scores = self.forward(nb, x, True, cache)
         b = scores.shape[1]
@@ -228,7 +241,7 @@ class NativeHashNet:
         loss = -logp[labels, torch.arange(b, device="cuda")].mean()
         dscores = torch.softmax(scores.double(), dim=0)
         dscores[labels, torch.arange(b, device="cuda")] -= 1.0
-        dscores = (dscores / b).float()
+        dscores = (dscores / (global_batch or b)).float()
         g_fc2_w = dscores @ cache["fc2_in"].t()
         g_fc2_b = dscores.sum(1)
         d_fc1_out = (self.fc2_w.t() @ dscores) * cache["m2"]
@@ -272,9 +285,13 @@ class NativeHashNet:
         head_grads = (g_fc1_w, g_fc1_b, g_fc2_w, g_fc2_b)
         return loss, conv_grads, head_grads
 
-    def train_step(self, nb: NetBatch, x: torch.Tensor, labels: torch.Tensor):
-        """net.cpp:349-375 train_step: loss + SGD with momentum and weight decay."""
-        loss, conv_grads, head_grads = self.loss_and_gradients(nb, x, labels)
+    def train_step(self, nb: NetBatch, x: torch.Tensor, labels: torch.Tensor, allreduce=None,
+                   global_batch: Optional[int] = None):
+        """net.cpp:349-375 train_step: loss + SGD with momentum and weight decay. `allreduce`
+        (e.g. dist.allreduce_gradients) sums the gradients over data-parallel ranks first."""
+        loss, conv_grads, head_grads = self.loss_and_gradients(nb, x, labels, global_batch)
+        if allreduce is not None:
+            allreduce(list(conv_grads) + [g.contiguous() for g in head_grads])
         for blk, g in zip(self.blocks, conv_grads):
             check(lib.hc_native_sgd_update(_p(blk["w"]), _p(blk["v"]), _p(g), g.numel(), self.lr, self.momentum,
                                            self.wd, _s()))
