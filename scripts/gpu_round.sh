@@ -4,7 +4,9 @@ timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/py
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -2 gpurun_out/smoke.log
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; cat gpurun_out/bench.json; tail -2 gpurun_out/bench.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2>&1; echo "ref rc=$?"; tail -c 300 gpurun_out/bench_ref.json
-for c in 16 64 128; do timeout 300 python scripts/kbench.py $c >> gpurun_out/kbench.txt 2>&1; done; cat gpurun_out/kbench.txt
+rm -f gpurun_out/kbench.txt; for c in 16 32 64 128 256; do timeout 300 python scripts/kbench.py $c >> gpurun_out/kbench.txt 2>&1; done; cat gpurun_out/kbench.txt
+timeout 600 python bench.py --workload net --res 64 --shapes-per-gpu 32 --steps 20 > gpurun_out/bench_net64.json 2>gpurun_out/bench_net64.err; echo "net64 rc=$?"; tail -c 400 gpurun_out/bench_net64.json
+timeout 600 python bench.py --workload net --res 128 --shapes-per-gpu 64 --steps 10 --no-cpu-baseline > gpurun_out/bench_net128.json 2>gpurun_out/bench_net128.err; echo "net128 rc=$?"
 for c in 16 64 256; do timeout 300 python scripts/kbench_ref.py $c > gpurun_out/kbench_ref_c$c.txt 2>&1; grep "C=" gpurun_out/kbench_ref_c$c.txt; done
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1; echo "ncu list rc=$?"
