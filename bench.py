@@ -55,6 +55,7 @@ def parse():
                    help="conv: one hash-conv layer fwd+bwd (the BASELINE metric); net: a full H-CNN "
                         "classification train step (BASELINE configs 2/3)")
     p.add_argument("--classes", type=int, default=40)
+    p.add_argument("--no-graph", action="store_true", help="net workload: time the eager step")
     return p.parse_args()
 
 
@@ -609,9 +610,19 @@ def net_main(args, rank, world, local):
     labels = torch.randint(0, args.classes, (b,), device=dev)
     voxels = sum(s.total_columns() for s in levels)
 
-    def one():
+    def eager():
         nb = nnet.NetBatch.build(levels)  # the batch's K0 / pool / dense-pool maps: per step
         return net.train_step(nb, x, labels, allreduce_gradients, b * world)
+
+    one = eager
+    mode = "eager"
+    if not args.no_graph and world == 1:
+        try:  # the whole step as one CUDA graph (per-batch maps included in the graph)
+            one = nnet.GraphedStep(net, levels, x, labels, allreduce_gradients, b * world)
+            mode = "cuda-graph"
+        except Exception as e:  # noqa: BLE001 — report and time the eager step instead
+            print(f"cuda graph capture failed ({e}); timing the eager step", file=sys.stderr)
+            one = eager
 
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:  # sampling spans warm-up and the timed region
@@ -645,7 +656,7 @@ def net_main(args, rank, world, local):
             "config": {"workload": f"hcnn classification net {args.res}^3, {lmax - 1} conv/pool levels, "
                                    f"{b} shells/GPU", "res": args.res, "global_batch": b * world,
                        "classes": args.classes, "voxels_per_gpu_all_levels": voxels,
-                       "parallelism": f"dp{world}"},
+                       "parallelism": f"dp{world}", "launch": mode},
             "voxels_per_s": voxels * world / (ms / 1e3), "cpu_baseline": cpu, "gpu_launches": int(launches),
             "clocks": clk.summary()}))
     if world > 1:

@@ -153,7 +153,8 @@ class NativeHashNet:
         self.head_v = [torch.zeros_like(t) for t in (self.fc1_w, self.fc1_b, self.fc2_w, self.fc2_b)]
         self._ws = {}
         self._dw_ws = nconv.DwWorkspace()
-        self._gen = torch.Generator(device="cuda").manual_seed(seed + 1)
+        self._seed = seed + 1
+        self._gen = None  # dropout masks: a private generator in eager mode, the default one in graphs
 
     # ------------------------------------------------------------------ helpers
     def reference_weights(self, i: int) -> torch.Tensor:
@@ -218,10 +219,13 @@ class NativeHashNet:
                 x = head
         # head: dropout -> FC(128) -> dropout -> FC(classes)   (net.cpp:236-251)
         keep = 1.0 - self.dropout
-        m1 = (torch.rand(x.shape, device="cuda", generator=self._gen) < keep).float() / keep
+        if self._gen is None and not torch.cuda.is_current_stream_capturing():
+            self._gen = torch.Generator(device="cuda").manual_seed(self._seed)
+        gen = None if torch.cuda.is_current_stream_capturing() else self._gen
+        m1 = (torch.rand(x.shape, device="cuda", generator=gen) < keep).float() / keep
         fc1_in = x * m1
         fc1_out = self.fc1_w @ fc1_in + self.fc1_b[:, None]
-        m2 = (torch.rand(fc1_out.shape, device="cuda", generator=self._gen) < keep).float() / keep
+        m2 = (torch.rand(fc1_out.shape, device="cuda", generator=gen) < keep).float() / keep
         fc2_in = fc1_out * m2
         scores = self.fc2_w @ fc2_in + self.fc2_b[:, None]
         if cache is not None:
@@ -299,3 +303,33 @@ class NativeHashNet:
             g = g.contiguous()
             check(lib.hc_native_sgd_update(_p(w), _p(v), _p(g), g.numel(), self.lr, self.momentum, self.wd, _s()))
         return loss
+
+
+class GraphedStep:
+    """A whole training step (per-batch maps + forward + backward + [all-reduce] + SGD)
+    captured once as a CUDA graph and replayed: ~100 launches per step become one graph
+    launch, so small batches are not host-bound. Valid while the batch's structure
+    tensors, the input features and the labels stay at the captured addresses (the
+    tables of a new batch of the same shapes are copied in place)."""
+
+    def __init__(self, net: NativeHashNet, levels: Sequence[SuperPsh], x: torch.Tensor, labels: torch.Tensor,
+                 allreduce=None, global_batch: Optional[int] = None, warmup: int = 2):
+        self.net, self.levels, self.x, self.labels = net, list(levels), x, labels
+        self.allreduce, self.global_batch = allreduce, global_batch
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(warmup):  # allocator / attribute setup outside the capture
+                self._step()
+        torch.cuda.current_stream().wait_stream(s)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.loss = self._step()
+
+    def _step(self):
+        nb = NetBatch.build(self.levels)
+        return self.net.train_step(nb, self.x, self.labels, self.allreduce, self.global_batch)
+
+    def __call__(self):
+        self.graph.replay()
+        return self.loss

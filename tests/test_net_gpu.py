@@ -147,3 +147,23 @@ def test_native_net_train_step_descends(cuda, ref):
     labels = torch.tensor([0, 1, 2, 3], device="cuda")
     losses = [float(net.train_step(nb, x, labels)) for _ in range(12)]
     assert all(np.isfinite(losses)) and max(losses[-3:]) < 0.5 * losses[0], losses
+
+
+def test_graphed_step_matches_eager(cuda, ref):
+    """The CUDA-graph step replays exactly the eager step's kernels (deterministic): same
+    losses step for step (the graph's 2 warm-up steps are real training steps)."""
+    supers = _ref_pyramid_batch(ref, 3, 16, seed=9)
+    labels = torch.tensor([2, 0, 1], device="cuda")
+
+    def fresh():
+        net = nnet.NativeHashNet(4, 3, seed=4, dropout=0.0, lr=0.01)
+        levels = [SuperPsh.from_host(s) for s in supers]
+        x = net.input_features(torch.from_numpy(supers[0].data).cuda())
+        return net, levels, x
+
+    net_e, lev_e, x_e = fresh()
+    eager = [float(net_e.train_step(nnet.NetBatch.build(lev_e), x_e, labels)) for _ in range(5)]
+    net_g, lev_g, x_g = fresh()
+    step = nnet.GraphedStep(net_g, lev_g, x_g, labels, warmup=2)
+    graphed = [float(step()) for _ in range(3)]
+    assert graphed == eager[2:], (graphed, eager)
