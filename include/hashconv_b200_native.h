@@ -30,6 +30,8 @@ int64_t hc_native_packed_k(int32_t channels, int32_t taps);
 /* backward = 0: Wp[co][t*C_in + ci] = W[co][ci*taps + t]           (forward operand)
  * backward = 1: Wp[ci][t*C_out + co] = W[co][ci*taps + taps-1-t]    (stride-1 input-gradient
  *               operand: the transposed, tap-flipped kernel)
+ * backward = 2: Wp[ci][t*C_out + co] = W[co][ci*taps + t]           (deconvolution operand W^T,
+ *               cnn_ops.cpp:408-419, with the transposed field map below)
  * w_packed: bf16, rows x hc_native_packed_k(...) */
 hc_status hc_native_pack_weights(const float* w_ref, int32_t c_out, int32_t c_in, int32_t taps,
                                  int32_t backward, void* w_packed, hc_stream stream);
@@ -89,6 +91,15 @@ hc_status hc_native_dense_pool_backward(const float* d_head, const int32_t* src,
 /* SGD with momentum and weight decay (net.cpp:339-346): v = momentum*v + lr*(g + wd*w); w -= v. */
 hc_status hc_native_sgd_update(float* w, float* v, const float* g, int64_t n, float lr, float momentum,
                                float weight_decay, hc_stream stream);
+
+/* Transposed field map of a strided (coarsening) conv field: from pmap [n_coarse][taps]
+ * (hc_field_map(fine, coarse, spec)) build the tile-major map tmap[g][t] = coarse voxel whose
+ * field holds fine voxel g at row t (or -1). deconv_forward (cnn_ops.cpp:408-419) is then
+ * hc_native_gather_gemm(tmap, D_coarse, pack mode 2, C_in); deconv_backward (:421-435) is
+ * hc_native_conv_dw(pmap, fine_grad, D_coarse) for dW and hc_native_gather_gemm(pmap,
+ * fine_grad, pack mode 0, C_out) for the coarse-data gradient. */
+hc_status hc_native_transpose_map(const int32_t* pmap, int64_t n_coarse, int32_t taps, int64_t n_fine,
+                                  int32_t* tmap_tiled, hc_stream stream);
 
 /* Boundary transposes between the reference layout (C x N fp32) and the native layout. */
 hc_status hc_native_to_voxel_major(const float* ref, int64_t c, int64_t n, void* out_bf16,

@@ -47,12 +47,20 @@ def to_channel_major(nat: torch.Tensor) -> torch.Tensor:
     return out
 
 
-def pack_weights(w_ref: torch.Tensor, c_out: int, c_in: int, taps: int, backward: bool) -> torch.Tensor:
+PACK_FORWARD, PACK_BACKWARD, PACK_TRANSPOSE = 0, 1, 2
+
+
+def pack_weights(w_ref: torch.Tensor, c_out: int, c_in: int, taps: int, backward: bool = False,
+                 mode: int = None) -> torch.Tensor:
+    """W[co][ci*taps + t] -> the bf16 GEMM operand (hc_native_pack_weights): forward
+    (mode 0), flipped transpose for the stride-1 input gradient (1, `backward=True`), or the
+    plain transpose W^T for the deconvolution (2)."""
+    mode = (PACK_BACKWARD if backward else PACK_FORWARD) if mode is None else mode
     w_ref = w_ref.contiguous().float()
-    rows = c_in if backward else c_out
-    kp = int(lib.hc_native_packed_k(c_out if backward else c_in, taps))
+    rows = c_in if mode else c_out
+    kp = int(lib.hc_native_packed_k(c_out if mode else c_in, taps))
     wp = torch.empty((rows, kp), dtype=torch.bfloat16, device=w_ref.device)
-    check(lib.hc_native_pack_weights(_p(w_ref), c_out, c_in, taps, int(backward), _p(wp), _s()))
+    check(lib.hc_native_pack_weights(_p(w_ref), c_out, c_in, taps, mode, _p(wp), _s()))
     return wp
 
 
@@ -162,6 +170,44 @@ class HashConv:
         dw = conv_dw(self.fmap, x, dy)
         dx = gather_gemm(self.fmap, dy, self.wb, self.spec.in_channels, dx_dtype or self.out_dtype)
         return dw, dx
+
+
+class HashDeconv:
+    """Native deconvolution onto the finer structure (cnn_ops.cpp:408-435): the transpose
+    of the strided conv `spec` (fine -> coarse field). Forward Y_fine = col2hash(W^T D_coarse)
+    is a gather-GEMM over the TRANSPOSED field map (fine voxel g, row t -> the coarse voxel
+    whose field holds g at t) with the W^T operand; backward is the strided conv's own
+    structure: dW by the split-K dW kernel on the field map, dD_coarse by the gather-GEMM
+    with the forward operand. Nothing is materialised (no column matrix, no col2hash)."""
+
+    def __init__(self, coarse: SuperPsh, fine: SuperPsh, weights: torch.Tensor, spec: ConvSpec,
+                 out_dtype=torch.bfloat16):
+        spec = ConvSpec(*spec)
+        self.coarse, self.fine, self.spec, self.out_dtype = coarse, fine, spec, out_dtype
+        self.taps = field_size(spec, fine.dim)
+        if tuple(weights.shape) != (spec.out_channels, spec.in_channels * self.taps):
+            raise ValueError("deconv_forward: weight shape mismatch")
+        self.w = weights
+        self.pmap = field_map_native(fine, coarse, spec, TILED)  # coarse voxel p, row t -> fine column
+        rows = field_map(fine, coarse, spec)                     # same map, row-major
+        nf = fine.total_columns()
+        tm = torch.empty(((nf + 127) // 128, self.taps, 128), dtype=torch.int32, device=weights.device)
+        check(lib.hc_native_transpose_map(_p(rows), rows.shape[0], self.taps, nf, _p(tm), _s()))
+        self.tmap = FieldMap(tm, nf, self.taps, TILED)
+
+    def forward(self, coarse_data: torch.Tensor) -> torch.Tensor:
+        """[N_coarse][C_out] bf16 -> [N_fine][C_in]   (cnn_ops.cpp:408-419)"""
+        sp = self.spec
+        wt = pack_weights(self.w, sp.out_channels, sp.in_channels, self.taps, mode=PACK_TRANSPOSE)
+        return gather_gemm(self.tmap, coarse_data, wt, sp.in_channels, self.out_dtype)
+
+    def backward(self, fine_grad: torch.Tensor, coarse_data: torch.Tensor, d_dtype=None):
+        """-> (dW [C_out][C_in*taps] fp32, dD_coarse [N_coarse][C_out])   (cnn_ops.cpp:421-435)"""
+        sp = self.spec
+        dw = conv_dw(self.pmap, fine_grad, coarse_data)
+        wf = pack_weights(self.w, sp.out_channels, sp.in_channels, self.taps, mode=PACK_FORWARD)
+        dd = gather_gemm(self.pmap, fine_grad, wf, sp.out_channels, d_dtype or self.out_dtype)
+        return dw, dd
 
 
 def smoke_check(structure: SuperPsh, x: np.ndarray, w: np.ndarray, dy: np.ndarray, y64: np.ndarray) -> None:

@@ -618,16 +618,17 @@ __global__ void k_retile(const int* __restrict__ src, int layout, long long n, i
 
 // ====================================================================== layout helpers
 // W_ref[co][ci*taps + t] (fp32, kernel weights layout cnn_ops.hpp:21-27) ->
-//   forward:  Wp[co][t*C_in + ci]           (bf16, K padded to Kp with zeros)
-//   backward: Wp[ci][t*C_out + co] = W_ref[co][ci*taps + (taps-1-t)]
-__global__ void k_pack_w(const float* __restrict__ w, int cout, int cin, int taps, int flip, int Kp,
+//   mode 0 (forward):    Wp[co][t*C_in + ci]  = W_ref[co][ci*taps + t]   (bf16, K padded to Kp)
+//   mode 1 (backward):   Wp[ci][t*C_out + co] = W_ref[co][ci*taps + (taps-1-t)]
+//   mode 2 (transpose):  Wp[ci][t*C_out + co] = W_ref[co][ci*taps + t]   (deconvolution, W^T)
+__global__ void k_pack_w(const float* __restrict__ w, int cout, int cin, int taps, int mode, int Kp,
                          bf16* __restrict__ wp) {
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    const int rows = flip ? cin : cout;
+    const int rows = mode ? cin : cout;
     if (i >= (long long)rows * Kp) return;
     const int r = (int)(i / Kp), k = (int)(i % Kp);
     float v = 0.0f;
-    if (!flip) {
+    if (mode == 0) {
         if (k < taps * cin) {
             const int t = k / cin, ci = k % cin;
             v = w[(long long)r * cin * taps + ci * taps + t];
@@ -635,10 +636,24 @@ __global__ void k_pack_w(const float* __restrict__ w, int cout, int cin, int tap
     } else {
         if (k < taps * cout) {
             const int t = k / cout, co = k % cout;
-            v = w[(long long)co * cin * taps + r * taps + (taps - 1 - t)];
+            v = w[(long long)co * cin * taps + r * taps + (mode == 1 ? taps - 1 - t : t)];
         }
     }
     wp[i] = __float2bfloat16_rn(v);
+}
+
+// Transposed field map for the deconvolution (cnn_ops.cpp:408-419, col2hash of W^T D):
+// from the conv map pmap [n_coarse][taps] (fine column of coarse voxel p's field row t)
+// build tmap [ceil(n_fine/128)][taps][128] (tile-major): tmap[g][t] = the coarse voxel
+// whose field holds fine voxel g at row t, or -1. (g, t) determines p uniquely
+// (p*S - pad = g - offset(t)), so the scatter has no conflicts; tmap pre-filled with -1.
+__global__ void k_transpose_map(const int* __restrict__ pmap, long long nc, int taps, int* __restrict__ tmap) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= nc * taps) return;
+    const int g = pmap[i];
+    if (g < 0) return;
+    const int t = (int)(i % taps);
+    tmap[((long long)(g >> 7) * taps + t) * 128 + (g & 127)] = (int)(i / taps);
 }
 
 // channel-major fp32 (C x N) -> voxel-major bf16 (N x C), tiled transpose
@@ -865,12 +880,26 @@ hc_status hc_native_pack_weights(const float* w_ref, int32_t c_out, int32_t c_in
                                  void* w_packed, hc_stream stream) {
     return guard([&] {
         check_native(c_in, c_out, taps);
+        if (backward < 0 || backward > 2) throw std::invalid_argument("native conv: pack mode must be 0, 1 or 2");
         const int rows = backward ? c_in : c_out;
         const long long Kp = hc_native_packed_k(backward ? c_out : c_in, taps);
         const long long n = rows * Kp;
         k_pack_w<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(w_ref, c_out, c_in, taps, backward, (int)Kp,
                                                                    static_cast<bf16*>(w_packed));
         launched("pack weights");
+    });
+}
+
+hc_status hc_native_transpose_map(const int32_t* pmap, int64_t n_coarse, int32_t taps, int64_t n_fine,
+                                  int32_t* tmap_tiled, hc_stream stream) {
+    return guard([&] {
+        if (taps < 1 || taps > 27) throw std::invalid_argument("native conv: 1..27 field taps supported");
+        cudaStream_t s = as_stream(stream);
+        const long long total = (n_fine + 127) / 128 * 128 * taps;
+        if (total > 0) cuda_check(cudaMemsetAsync(tmap_tiled, 0xFF, sizeof(int32_t) * total, s), "memset");
+        if (n_coarse <= 0) return;
+        k_transpose_map<<<grid_for(n_coarse * taps, 256), 256, 0, s>>>(pmap, n_coarse, taps, tmap_tiled);
+        launched("transposed field map");
     });
 }
 

@@ -160,3 +160,31 @@ def test_layout_round_trip(cuda):
     back = nconv.to_channel_major(v)
     assert torch.equal(back, x.to(torch.bfloat16).float())
     assert torch.equal(nconv.to_channel_major(x.t().contiguous()), x)
+
+
+@pytest.mark.parametrize("c_in,c_out", [(16, 16), (32, 64), (64, 32)])
+def test_native_deconv_vs_oracle(cuda, restated, c_in, c_out):
+    """Native deconvolution (transposed field map + W^T gather-GEMM; backward on the conv's
+    own map) vs the double oracle deconv_forward / deconv_backward (cnn_ops.cpp:408-435) on
+    bf16-quantised operands, coarsening spec {2,2,0}."""
+    f, cl = shell_pair(32, 2)
+    fa, ca = levels_to_arrays(f), levels_to_arrays(cl)
+    fine, coarse = SuperPsh.from_levels(f), SuperPsh.from_levels(cl)
+    nf, nc = fine.total_columns(), coarse.total_columns()
+    rng = np.random.default_rng(c_in * 7 + c_out)
+    q = lambda a: torch.from_numpy(a).to(torch.bfloat16).float().numpy()  # noqa: E731
+    spec = ConvSpec(2, 2, 0, c_in, c_out)
+    w = q(rng.uniform(-1, 1, (c_out, c_in * 8)).astype(np.float32))
+    dc = q(rng.uniform(-1, 1, (c_out, nc)).astype(np.float32))
+    fg = q(rng.uniform(-1, 1, (c_in, nf)).astype(np.float32))
+    f64 = np.float64
+    y64 = restated.deconv_forward(ca, dc.astype(f64), fa, w.astype(f64), spec, f64)
+    dw64, dd64 = restated.deconv_backward(fg.astype(f64), w.astype(f64), dc.astype(f64), ca, fa, spec, f64)
+    layer = nconv.HashDeconv(coarse, fine, torch.from_numpy(w).cuda(), spec, out_dtype=torch.float32)
+    dcv = nconv.to_voxel_major(torch.from_numpy(dc).cuda())
+    y = nconv.to_channel_major(layer.forward(dcv))
+    dw, ddv = layer.backward(nconv.to_voxel_major(torch.from_numpy(fg).cuda()), dcv, torch.float32)
+    t = lambda a: torch.from_numpy(a)  # noqa: E731
+    assert rel(y.cpu(), t(y64)) <= TOL_F32_OUT
+    assert rel(dw.cpu(), t(dw64)) <= TOL_DW
+    assert rel(nconv.to_channel_major(ddv).cpu(), t(dd64)) <= TOL_F32_OUT
