@@ -51,7 +51,7 @@ def parse():
     p.add_argument("--path", default="fused", choices=["materialized", "fused"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--workload", default="conv", choices=["conv", "net"],
+    p.add_argument("--workload", default="conv", choices=["conv", "net", "seg"],
                    help="conv: one hash-conv layer fwd+bwd (the BASELINE metric); net: a full H-CNN "
                         "classification train step (BASELINE configs 2/3)")
     p.add_argument("--classes", type=int, default=40)
@@ -321,6 +321,8 @@ def main():
 
     if args.workload == "net":
         return net_main(args, rank, world, local)
+    if args.workload == "seg":
+        return seg_main(args, rank, world, local)
     if args.impl == "reference":
         return reference_arm(args, rank, world)
 
@@ -659,6 +661,65 @@ def net_main(args, rank, world, local):
                        "parallelism": f"dp{world}", "launch": mode},
             "voxels_per_s": voxels * world / (ms / 1e3), "cpu_baseline": cpu, "gpu_launches": int(launches),
             "clocks": clk.summary()}))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ segmentation workload
+def seg_main(args, rank, world, local):
+    """BASELINE config 4's composition: a SegNet/DeconvNet-style encoder-decoder training step
+    on the 256^3 shell level pair (conv, BN+ReLU, max pool, conv, unpool + stride-2 deconv,
+    conv, per-voxel softmax, SGD), --shapes-per-gpu shells per GPU, C = --cin channels."""
+    import torch
+    import torch.distributed as dist
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps({"impl": "reference", "unavailable": "the reference has no segmentation net "
+                                                                  "(only its operators: see --workload conv)"}))
+        return
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_1803_11385_b200 import _lib
+    from paper_1803_11385_b200.psh import SuperPsh
+    from paper_1803_11385_b200.dist import allreduce_gradients
+    from paper_1803_11385_b200.seg import NativeSegNet
+    lv = shell_levels(args.res)
+    b = args.shapes_per_gpu
+    fine, coarse = SuperPsh.from_levels([lv[0]] * b), SuperPsh.from_levels([lv[1]] * b)
+    seg = NativeSegNet(fine, coarse, c_in=8, c=args.cin, classes=16, seed=rank)
+    g = torch.Generator(device=dev).manual_seed(rank)
+    nf = fine.total_columns()
+    x = (torch.rand((nf, 8), device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
+    labels = torch.randint(0, 16, (nf,), device=dev, generator=g)
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        for _ in range(max(3, args.warmup)):
+            seg.step(x, labels, allreduce_gradients, world)
+        torch.cuda.synchronize()
+        launches0 = _lib.lib.hc_launch_count()
+        st.record()
+        for _ in range(args.steps):
+            seg.step(x, labels, allreduce_gradients, world)
+        en.record()
+        torch.cuda.synchronize()
+        launches = _lib.lib.hc_launch_count() - launches0
+    t = torch.tensor([st.elapsed_time(en) / args.steps], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    if rank == 0:
+        print(json.dumps({
+            "metric": "segmentation train step occupied voxels/sec", "value": nf * world / (ms / 1e3),
+            "unit": "voxels/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (sphere shells; random features and per-voxel labels)",
+            "config": {"workload": f"seg encoder-decoder {args.res}^3 -> {args.res // 2}^3 -> {args.res}^3, "
+                                   f"{b} shells/GPU, C={args.cin}", "res": args.res, "global_batch": b * world,
+                       "fine_voxels_per_gpu": nf, "coarse_voxels_per_gpu": coarse.total_columns(),
+                       "parallelism": f"dp{world} (shapes sharded, weight gradients all-reduced)"},
+            "shapes_per_s": b * world / (ms / 1e3), "gpu_launches": int(launches), "clocks": clk.summary()}))
     if world > 1:
         dist.destroy_process_group()
 

@@ -70,6 +70,10 @@ hc_status hc_native_max_pool(const int32_t* pmap, int64_t n_coarse, int32_t fd, 
 hc_status hc_native_max_unpool(const int32_t* parent, const int8_t* prow, int64_t n_fine, const void* dy,
                                hc_dtype dtype, int32_t c, const int8_t* switches, void* dx,
                                hc_stream stream);
+/* Adjoint of hc_native_max_unpool: out[p][c] = fine[pmap[p][switches[p][c]]][c] (0 for -1). */
+hc_status hc_native_switch_gather(const int32_t* pmap, int64_t n_coarse, int32_t fd, const void* fine,
+                                  hc_dtype dtype, int32_t c, const int8_t* switches, void* out,
+                                  hc_stream stream);
 /* Training-mode batch norm over the N rows + ReLU: batch mean / biased variance (double,
  * two-pass), running stats updated with `momentum`, inv_std = 1/sqrt(var + eps);
  * xhat (fp32, optional) = (x - mean) * inv_std, out_bf16 = max(0, xhat). */

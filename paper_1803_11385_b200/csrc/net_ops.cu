@@ -131,6 +131,34 @@ __global__ void __launch_bounds__(kT) k_nmax_unpool(const int* __restrict__ pare
     store8(dx + g * C + c0, o);
 }
 
+// Adjoint of max_unpool (= the max pool's forward selection applied to a gradient):
+// out[p][c] = fine[pmap[p][sw[p][c]]][c], 0 where the switch is -1.
+template <typename T>
+__global__ void __launch_bounds__(kT) k_switch_gather(const int* __restrict__ pmap, long long nc, int fd,
+                                                     const T* __restrict__ fine, const signed char* __restrict__ sw,
+                                                     int C, T* __restrict__ out) {
+    const int chunks = C >> 3;
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= nc * chunks) return;
+    const long long p = i / chunks;
+    const int c0 = (int)(i - p * chunks) * 8;
+    const int2 s = __ldg(reinterpret_cast<const int2*>(sw + p * C + c0));
+    const signed char* sc = reinterpret_cast<const signed char*>(&s);
+    float o[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        o[e] = 0.0f;
+        if (sc[e] >= 0) {
+            const int g = __ldg(pmap + p * fd + sc[e]);
+            if (g >= 0) {
+                if constexpr (sizeof(T) == 2) o[e] = __bfloat162float(fine[(long long)g * C + c0 + e]);
+                else o[e] = fine[(long long)g * C + c0 + e];
+            }
+        }
+    }
+    store8(out + p * C + c0, o);
+}
+
 // ---------------------------------------------------------------------- batch norm + ReLU
 // Column partial sums over row blocks: thread (r, q) owns channel quad q of rows
 // r, r + R, ... inside the block's row range; partials [block][C] in double.
@@ -380,6 +408,24 @@ hc_status hc_native_max_unpool(const int32_t* parent, const int8_t* prow, int64_
             k_nmax_unpool<float><<<grid_for(n, kT), kT, 0, s>>>(parent, pr, n_fine, static_cast<const float*>(dy), sw,
                                                                 c, static_cast<float*>(dx));
         launched("native max_unpool");
+    });
+}
+
+hc_status hc_native_switch_gather(const int32_t* pmap, int64_t n_coarse, int32_t fd, const void* fine, hc_dtype dtype,
+                                  int32_t c, const int8_t* switches, void* out, hc_stream stream) {
+    return guard([&] {
+        check_c8(c);
+        if (n_coarse <= 0) return;
+        cudaStream_t s = as_stream(stream);
+        const long long n = n_coarse * (c / 8);
+        const signed char* sw = reinterpret_cast<const signed char*>(switches);
+        if (dtype == HC_DTYPE_BF16)
+            k_switch_gather<bf16><<<grid_for(n, kT), kT, 0, s>>>(pmap, n_coarse, fd, static_cast<const bf16*>(fine), sw,
+                                                                 c, static_cast<bf16*>(out));
+        else
+            k_switch_gather<float><<<grid_for(n, kT), kT, 0, s>>>(pmap, n_coarse, fd, static_cast<const float*>(fine),
+                                                                  sw, c, static_cast<float*>(out));
+        launched("switch gather");
     });
 }
 

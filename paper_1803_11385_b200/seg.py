@@ -1,0 +1,150 @@
+"""Segmentation-style composition on the native path (BASELINE config 4).
+
+A SegNet / DeconvNet-style encoder-decoder on two PSH levels (PAPER.md:381 DeconvNet:
+unpooling with the encoder's switches followed by convolution, plus a learned stride-2
+deconvolution), built only from the reference's operators in their native form:
+
+    encoder   x -> conv1 (fine, Cin->C) -> BN -> ReLU -> max_pool (switches) ->
+              conv2 (coarse, C->2C) -> BN -> ReLU = e2
+    decoder   max_unpool(conv3(e2): coarse 2C->C, the encoder's switches)   (cnn_ops.cpp:336-372)
+              + deconv(e2): coarse 2C -> fine C, spec {2,2,0}                (cnn_ops.cpp:408-419)
+              -> BN -> ReLU -> conv4 (fine, C->K) = per-voxel scores
+    loss      per-voxel softmax cross-entropy against labels, mean over voxels
+
+forward + backward of every layer (the unpool's backward is the pool's gather through the
+same switches, the deconvolution's backward is the strided conv) — the col2hash-heavy
+backward of config 4 without ever materialising a column matrix. Maps are built once per
+batch. Weights are plain SGD-updated fp32 in the reference layout W[co][ci*taps + t].
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _lib
+from . import conv as nconv
+from ._lib import check, lib
+from .net import BF16, _p, _s
+from .ops import ConvSpec, field_map
+from .psh import SuperPsh
+
+
+class NativeSegNet:
+    def __init__(self, fine: SuperPsh, coarse: SuperPsh, c_in: int = 8, c: int = 32, classes: int = 16,
+                 seed: int = 0, lr: float = 0.01):
+        if c_in % 8 or c % 16 or classes % 16:
+            raise ValueError("native seg net: c_in % 8, c % 16, classes % 16 (tensor-core tile set)")
+        self.fine, self.coarse, self.c_in, self.c, self.k, self.lr = fine, coarse, c_in, c, classes, lr
+        g = torch.Generator(device="cuda").manual_seed(seed)
+
+        def xavier(co, ci, taps):
+            b = math.sqrt(6.0 / ((ci + co) * taps))
+            return (torch.rand((co, ci * taps), device="cuda", generator=g) * 2 - 1) * b
+
+        self.w = {"conv1": xavier(c, c_in, 27), "conv2": xavier(2 * c, c, 27), "conv3": xavier(c, 2 * c, 27),
+                  "deconv": xavier(2 * c, c, 8), "conv4": xavier(classes, c, 27)}
+        nf, nc = fine.total_columns(), coarse.total_columns()
+        self.nf, self.nc = nf, nc
+        # per-batch maps
+        self.fmap_f = nconv.field_map_native(fine, fine, ConvSpec(3, 1, 0, 8, 8), nconv.TILED)
+        self.fmap_c = nconv.field_map_native(coarse, coarse, ConvSpec(3, 1, 0, 8, 8), nconv.TILED)
+        self.pmap = field_map(fine, coarse, ConvSpec(2, 2, 0, 8, 8))
+        self.parent = torch.empty(nf, dtype=torch.int32, device="cuda")
+        self.prow = torch.empty(nf, dtype=torch.int8, device="cuda")
+        check(lib.hc_native_pool_parents(_p(self.pmap), nc, 8, nf, _p(self.parent), _p(self.prow), _s()))
+        self.deconv = nconv.HashDeconv(coarse, fine, self.w["deconv"], ConvSpec(2, 2, 0, c, 2 * c), torch.float32)
+        self.bn = {k: dict(mean=torch.zeros(n, device="cuda"), var=torch.ones(n, device="cuda"),
+                           inv=torch.empty(n, device="cuda"))
+                   for k, n in (("bn1", c), ("bn2", 2 * c), ("bn3", c))}
+        self._dw = nconv.DwWorkspace()
+        self._bnws = None
+
+    # ------------------------------------------------------------------ pieces
+    def _bnws_for(self, n, c):
+        need = int(lib.hc_native_bn_workspace(n, c))
+        if self._bnws is None or self._bnws.numel() < need:
+            self._bnws = torch.empty(need, dtype=torch.uint8, device="cuda")
+        return self._bnws
+
+    def _conv(self, fmap, x, name, c_out, dtype=torch.float32):
+        w = self.w[name]
+        wf = nconv.pack_weights(w, c_out, x.shape[1], 27, False)
+        return nconv.gather_gemm(fmap, x, wf, c_out, dtype)
+
+    def _conv_bwd(self, fmap, x, dy, name, need_dx=True):
+        w = self.w[name]
+        c_out, c_in = w.shape[0], x.shape[1]
+        dw = nconv.conv_dw(fmap, x, dy, self._dw)
+        dx = None
+        if need_dx:
+            wb = nconv.pack_weights(w, c_out, c_in, 27, True)
+            dx = nconv.gather_gemm(fmap, dy, wb, c_in, BF16)
+        return dw, dx
+
+    def _bn_relu(self, y, name):
+        n, c = y.shape
+        b = self.bn[name]
+        xhat = torch.empty_like(y)
+        out = torch.empty((n, c), dtype=BF16, device="cuda")
+        ws = self._bnws_for(n, c)
+        check(lib.hc_native_bn_relu_forward(_p(y), n, c, 1, 0.1, 1e-5, _p(b["mean"]), _p(b["var"]), _p(b["inv"]),
+                                            _p(xhat), _p(out), _p(ws), ws.numel(), _s()))
+        return out, xhat
+
+    def _bn_relu_bwd(self, d, dtype, xhat, name):
+        n, c = xhat.shape
+        out = torch.empty((n, c), dtype=BF16, device="cuda")
+        ws = self._bnws_for(n, c)
+        check(lib.hc_native_bn_relu_backward(_p(d), dtype, _p(xhat), _p(self.bn[name]["inv"]), n, c, _p(out), _p(ws),
+                                             ws.numel(), _s()))
+        return out
+
+    # ------------------------------------------------------------------ step
+    def step(self, x: torch.Tensor, labels: torch.Tensor, allreduce=None, world: int = 1):
+        """One training step; x [N_fine][c_in] bf16, labels [N_fine] int64. Returns the loss.
+        Data parallel: `allreduce` sums the weight gradients over `world` equal shards, which
+        are then averaged (the loss is the mean over all voxels of the global batch)."""
+        c, nc, nf = self.c, self.nc, self.nf
+        # ---- encoder
+        r1, h1 = self._bn_relu(self._conv(self.fmap_f, x, "conv1", c), "bn1")
+        p1 = torch.empty((nc, c), dtype=BF16, device="cuda")
+        sw = torch.empty((nc, c), dtype=torch.int8, device="cuda")
+        check(lib.hc_native_max_pool(_p(self.pmap), nc, 8, _p(r1), _lib.HC_DTYPE_BF16, c, _p(p1), _p(sw), _s()))
+        e2, h2 = self._bn_relu(self._conv(self.fmap_c, p1, "conv2", 2 * c), "bn2")
+        # ---- decoder: unpool(conv3(e2)) + deconv(e2)
+        d3 = self._conv(self.fmap_c, e2, "conv3", c, BF16)
+        up = torch.empty((nf, c), dtype=BF16, device="cuda")
+        check(lib.hc_native_max_unpool(_p(self.parent), _p(self.prow), nf, _p(d3), _lib.HC_DTYPE_BF16, c, _p(sw),
+                                       _p(up), _s()))
+        s3 = self.deconv.forward(e2).float() + up.float()
+        r3, h3 = self._bn_relu(s3, "bn3")
+        scores = self._conv(self.fmap_f, r3, "conv4", self.k)  # [N_fine][K] fp32
+        # ---- per-voxel softmax cross-entropy (mean over voxels)
+        logp = torch.log_softmax(scores, dim=1)
+        loss = -logp.gather(1, labels[:, None]).mean()
+        dscores = torch.softmax(scores, dim=1)
+        dscores.scatter_add_(1, labels[:, None], torch.full((nf, 1), -1.0, device="cuda"))
+        dscores = (dscores / nf).to(BF16)
+        # ---- backward
+        g = {}
+        g["conv4"], d_r3 = self._conv_bwd(self.fmap_f, r3, dscores, "conv4")
+        d_s3 = self._bn_relu_bwd(d_r3, _lib.HC_DTYPE_BF16, h3, "bn3")          # [N_fine][C] bf16
+        g["deconv"], d_e2a = self.deconv.backward(d_s3, e2)                    # deconv branch
+        d_d3 = torch.empty((nc, c), dtype=BF16, device="cuda")                  # unpool branch: adjoint =
+        check(lib.hc_native_switch_gather(_p(self.pmap), nc, 8, _p(d_s3), _lib.HC_DTYPE_BF16, c, _p(sw), _p(d_d3),
+                                          _s()))
+        g["conv3"], d_e2b = self._conv_bwd(self.fmap_c, e2, d_d3, "conv3")
+        d_e2 = (d_e2a.float() + d_e2b.float())
+        d_y2 = self._bn_relu_bwd(d_e2, _lib.HC_DTYPE_F32, h2, "bn2")
+        g["conv2"], d_p1 = self._conv_bwd(self.fmap_c, p1, d_y2, "conv2")
+        d_r1 = torch.empty((nf, c), dtype=BF16, device="cuda")                 # pool backward = unpool
+        check(lib.hc_native_max_unpool(_p(self.parent), _p(self.prow), nf, _p(d_p1), _lib.HC_DTYPE_BF16, c, _p(sw),
+                                       _p(d_r1), _s()))
+        d_y1 = self._bn_relu_bwd(d_r1, _lib.HC_DTYPE_BF16, h1, "bn1")
+        g["conv1"], _ = self._conv_bwd(self.fmap_f, x, d_y1, "conv1", need_dx=False)
+        if allreduce is not None:
+            allreduce(list(g.values()))
+        for k, gr in g.items():  # plain SGD
+            self.w[k].sub_((self.lr / world) * gr)
+        return loss

@@ -167,3 +167,18 @@ def test_graphed_step_matches_eager(cuda, ref):
     step = nnet.GraphedStep(net_g, lev_g, x_g, labels, warmup=2)
     graphed = [float(step()) for _ in range(3)]
     assert graphed == eager[2:], (graphed, eager)
+
+
+def test_native_seg_step_descends(cuda):
+    """Segmentation-style composition (conv/BN/ReLU/pool -> conv -> unpool + deconv -> conv,
+    per-voxel softmax) trains on a 32^3 shell pair: the loss falls under SGD."""
+    from helpers import shell_pair
+    from paper_1803_11385_b200.seg import NativeSegNet
+    f, cl = shell_pair(32, 2)
+    fine, coarse = SuperPsh.from_levels(f), SuperPsh.from_levels(cl)
+    seg = NativeSegNet(fine, coarse, c_in=8, c=32, classes=16, seed=3, lr=0.5)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    x = (torch.rand((fine.total_columns(), 8), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    labels = (x[:, 0].float() > 0).long() + 2 * (x[:, 1].float() > 0).long()  # learnable from the input
+    losses = [float(seg.step(x, labels)) for _ in range(15)]
+    assert all(np.isfinite(losses)) and losses[-1] < 0.8 * losses[0], losses
