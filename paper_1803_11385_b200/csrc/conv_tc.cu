@@ -355,13 +355,15 @@ struct DwGroups {
     long long part_begin[kMaxGroups];
 };
 
-template <int NB, int PW, int CPS = 1>
+// NT = field-map taps one buffer holds: a CTA stages only the taps its m-tiles touch
+// (C=64, 4 m-tiles: 9 of 27), which leaves shared memory for a deeper A ring.
+template <int NB, int PW, int CPS = 1, int NT = kMaxTaps>
 struct DwCfg {
     static constexpr int KB = 64;                      // voxels per stage
     static constexpr int A_BYTES = 2 * KB * 128;       // two 64-wide MN blocks (M = 128)
     static constexpr int B_BYTES = (NB / 64) * KB * 128;
     static constexpr int BSTAGES = 2;
-    static constexpr int NBR = 2 * kNbrBytes;
+    static constexpr int NBR = 2 * NT * BM * 4;
     static constexpr int BUDGET = (CPS == 2 ? 113 : 226) * 1024 - 1024 - 512 - 1024 - NBR - BSTAGES * B_BYTES;
     static constexpr int STAGES = BUDGET / A_BYTES > 10 ? 10 : BUDGET / A_BYTES;
     static constexpr int PRODUCERS = PW * 32;
@@ -370,11 +372,11 @@ struct DwCfg {
     static constexpr int SMEM = 1024 + STAGES * A_BYTES + BSTAGES * B_BYTES + NBR + 1024 + 512;
 };
 
-template <int NB, int PW, int CPS>
-__global__ void __launch_bounds__(DwCfg<NB, PW, CPS>::THREADS, CPS)
+template <int NB, int PW, int CPS, int NT>
+__global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
     k_conv_dw(const __grid_constant__ CUtensorMap dymap, const int* __restrict__ fmap, int taps, long long rows,
               const bf16* __restrict__ X, int C, const DwGroups grp_tab, int tiles, float* __restrict__ partial) {
-    using Cfg = DwCfg<NB, PW, CPS>;
+    using Cfg = DwCfg<NB, PW, CPS, NT>;
     constexpr int S = Cfg::STAGES, BS = Cfg::BSTAGES;
     constexpr int NP = Cfg::PRODUCERS;
     constexpr int RS = NP / 8;
@@ -384,7 +386,7 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS>::THREADS, CPS)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* bsm = smem + S * Cfg::A_BYTES;
     int* nbr_s = reinterpret_cast<int*>(bsm + BS * Cfg::B_BYTES);
-    int* tab = nbr_s + 2 * kMaxTaps * BM;  // [m-tile][2 blocks][8 chunks]: (t << 16 | ci) or -1
+    int* tab = nbr_s + 2 * NT * BM;  // [m-tile][2 blocks][8 chunks]: ((t - t_lo) << 16 | ci) or -1
     uint64_t* bars = reinterpret_cast<uint64_t*>(tab + 256);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 2 * BS + 3);
     int* nbr_cnt = reinterpret_cast<int*>(tmem_slot + 2);
@@ -403,11 +405,14 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS>::THREADS, CPS)
     const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S);
     const uint32_t bfull0 = smem_u32(bars + 2 * S), bempty0 = smem_u32(bars + 2 * S + BS);
     const uint32_t nfull0 = smem_u32(bars + 2 * S + 2 * BS), done = nfull0 + 16;
-    const uint32_t nbr_bytes = (uint32_t)(taps * BM * 4);
+    // taps [t_lo, t_lo + ntb) cover this CTA's (t, ci) rows; only they are staged
+    const int t_lo = (m0 * 128) / C;
+    const int ntb = min(NT, (min(K, (m0 + nm) * 128) - 1) / C - t_lo + 1);
+    const uint32_t nbr_bytes = (uint32_t)(ntb * BM * 4);
 
     for (int e = tid; e < nm * 16; e += blockDim.x) {
         const int m = (m0 + e / 16) * 128 + ((e / 8) & 1) * 64 + (e & 7) * 8;
-        tab[e] = m < K ? ((m / C) << 16) | (m % C) : -1;
+        tab[e] = m < K ? ((m / C - t_lo) << 16) | (m % C) : -1;
     }
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
@@ -446,7 +451,7 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS>::THREADS, CPS)
         }
         auto request = [&](int lt, int buf) {
             mbar_arrive_expect_tx(nfull0 + 8 * buf, nbr_bytes);
-            bulk_g2s(smem_u32(nbr_s + buf * kMaxTaps * BM), fmap + (long long)(tile0 + lt) * taps * BM, nbr_bytes,
+            bulk_g2s(smem_u32(nbr_s + buf * NT * BM), fmap + ((long long)(tile0 + lt) * taps + t_lo) * BM, nbr_bytes,
                      nfull0 + 8 * buf);
         };
         if (tid == 0) {
@@ -458,7 +463,7 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS>::THREADS, CPS)
         for (int lt = 0; lt < ntl; ++lt) {
             const int buf = lt & 1;
             mbar_wait_sleep(nfull0 + 8 * buf, (uint32_t)((lt >> 1) & 1));
-            const uint32_t nb = smem_u32(nbr_s + buf * kMaxTaps * BM);
+            const uint32_t nb = smem_u32(nbr_s + buf * NT * BM);
             for (int h = 0; h < 2; ++h) {
                 if (tid == 0) {  // dY rows of this half tile -> B stage (all NB/64 co blocks)
                     mbar_wait_sleep(bempty0 + 8 * bs, bph ^ 1);
@@ -762,7 +767,7 @@ int dw_cps(int nb) {
 }
 
 struct DwPlan {
-    int nb, mt, cps, ctas, tiles;
+    int nb, mt, cps, ctas, tiles, max_taps;
     DwGroups g;
     long long partial_floats;
 };
@@ -804,14 +809,20 @@ DwPlan dw_plan(long long rows, int taps, int cin, int cout) {
     }
     p.ctas = g.cta_begin[G];
     p.partial_floats = part;
+    p.max_taps = 0;  // widest tap range any group's m-tiles touch
+    for (int i = 0; i < G; ++i) {
+        const int lo = g.m_begin[i] * 128 / cin;
+        const int hi = (std::min(taps * cin, g.m_begin[i + 1] * 128) - 1) / cin;
+        p.max_taps = std::max(p.max_taps, hi - lo + 1);
+    }
     return p;
 }
 
-template <int NB, int PW, int CPS>
+template <int NB, int PW, int CPS, int NT = kMaxTaps>
 void launch_dw_pw(const DwPlan& p, const int* fmap, int taps, long long rows, const bf16* X, int C, const bf16* dY,
                   int Cout, float* partial, cudaStream_t s) {
-    using Cfg = DwCfg<NB, PW, CPS>;
-    auto kern = k_conv_dw<NB, PW, CPS>;
+    using Cfg = DwCfg<NB, PW, CPS, NT>;
+    auto kern = k_conv_dw<NB, PW, CPS, NT>;
     static bool attr = false;
     if (!attr) {
         cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM), "smem attr");
@@ -834,6 +845,8 @@ void launch_dw(const DwPlan& p, const int* fmap, int taps, long long rows, const
         if (p.cps == 2) {
             if (pw == 2) return launch_dw_pw<NB, 2, 2>(p, fmap, taps, rows, X, C, dY, Cout, partial, s);
             if (pw == 8) return launch_dw_pw<NB, 8, 2>(p, fmap, taps, rows, X, C, dY, Cout, partial, s);
+            static const int small_map = env_int("HCB_DW_SMALLMAP", 1);
+            if (small_map && p.max_taps <= 9) return launch_dw_pw<NB, 4, 2, 9>(p, fmap, taps, rows, X, C, dY, Cout, partial, s);
             return launch_dw_pw<NB, 4, 2>(p, fmap, taps, rows, X, C, dY, Cout, partial, s);
         }
     }

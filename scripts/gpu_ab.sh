@@ -1,7 +1,5 @@
 mkdir -p gpurun_out
-HCB_FWD_NACC=2 timeout 300 python -m pytest tests/test_conv_tc.py -q -x -p no:cacheprovider -k "gather or layer" > gpurun_out/pytest_tc.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_tc.log
+timeout 300 python -m pytest tests/test_conv_tc.py -q -x -p no:cacheprovider > gpurun_out/pytest_tc.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_tc.log
 run() { env "$@" timeout 200 python scripts/kbench.py ${CS:-64} 2>&1 | grep -E "C=|Error|error" | tail -5; }
-run HCB_FWD_NACC=1
-run HCB_FWD_NACC=2
-run HCB_FWD_NACC=2 HCB_FWD_CPS=1 HCB_FWD_PW=8
-run HCB_FWD_NACC=2 HCB_FWD_CPS=1 HCB_FWD_PW=4
+run HCB_DW_SMALLMAP=1
+run HCB_DW_SMALLMAP=0
