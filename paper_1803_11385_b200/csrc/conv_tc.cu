@@ -584,26 +584,41 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
     }
 }
 
-// dW_ref[co][ci*taps + t] = sum_split partial[split][t*C + ci][co]  (fixed split order).
-// Thread i -> (m, co) with co fastest: the partial reads are coalesced.
-__global__ void k_reduce_dw(const float* __restrict__ partial, const DwGroups grp_tab, int NB, int taps, int C,
-                            int Cout, float* __restrict__ dw) {
-    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // over (taps*C) x Cout
+// dW_ref[co][ci*taps + t] = sum_split partial[split][t*C + ci][co]  (fixed order).
+// Block = 32 consecutive (m, co) outputs x 8 split lanes: lane j sums splits j, j+8, ...,
+// then the 8 lane sums are added in lane order -> deterministic, 8x the loads in flight of
+// a thread-per-output loop (hundreds of splits at small C).
+__global__ void __launch_bounds__(256) k_reduce_dw(const float* __restrict__ partial, const DwGroups grp_tab, int NB,
+                                                  int taps, int C, int Cout, float* __restrict__ dw) {
+    __shared__ float red[8][33];
+    const int lane = threadIdx.x & 31, j = threadIdx.x >> 5;
+    const long long i = blockIdx.x * 32LL + lane;  // over (taps*C) x Cout
     const long long total = (long long)taps * C * Cout;
-    if (i >= total) return;
-    const long long m = i / Cout;
-    const int co = (int)(i - m * Cout);
-    const int t = (int)(m / C), ci = (int)(m - (long long)t * C);
-    const int mtile = (int)(m / BM), row = (int)(m % BM);
-    int g = 0;
-    while (g + 1 < grp_tab.groups && mtile >= grp_tab.m_begin[g + 1]) ++g;
-    const int nm = grp_tab.m_begin[g + 1] - grp_tab.m_begin[g];
-    const int splits = grp_tab.cta_begin[g + 1] - grp_tab.cta_begin[g];
-    const float* p = partial + grp_tab.part_begin[g] + ((long long)(mtile - grp_tab.m_begin[g]) * BM + row) * NB + co;
-    const long long stride = (long long)nm * BM * NB;
     float acc = 0.0f;
-    for (int s = 0; s < splits; ++s) acc += p[s * stride];
-    dw[(long long)co * C * taps + (long long)ci * taps + t] = acc;
+    long long m = 0;
+    int co = 0;
+    if (i < total) {
+        m = i / Cout;
+        co = (int)(i - m * Cout);
+        const int mtile = (int)(m / BM), row = (int)(m % BM);
+        int g = 0;
+        while (g + 1 < grp_tab.groups && mtile >= grp_tab.m_begin[g + 1]) ++g;
+        const int nm = grp_tab.m_begin[g + 1] - grp_tab.m_begin[g];
+        const int splits = grp_tab.cta_begin[g + 1] - grp_tab.cta_begin[g];
+        const float* p = partial + grp_tab.part_begin[g] + ((long long)(mtile - grp_tab.m_begin[g]) * BM + row) * NB + co;
+        const long long stride = (long long)nm * BM * NB;
+#pragma unroll 4
+        for (int s = j; s < splits; s += 8) acc += p[s * stride];
+    }
+    red[j][lane] = acc;
+    __syncthreads();
+    if (j == 0 && i < total) {
+        float v = red[0][lane];
+#pragma unroll
+        for (int k = 1; k < 8; ++k) v += red[k][lane];
+        const int t = (int)(m / C), ci = (int)(m - (long long)t * C);
+        dw[(long long)co * C * taps + (long long)ci * taps + t] = v;
+    }
 }
 
 // Row-major [n][taps] (layout 0) or tap-major [taps][n] (layout 1) -> tile-major
@@ -963,7 +978,7 @@ hc_status hc_native_conv_dw(const int32_t* fmap, int32_t fmap_layout, int64_t n_
             default: launch_dw<256>(p, fm.p, taps, n_out, X, c_in, DY, c_out, part, s); break;
         }
         const long long total = (long long)c_out * c_in * taps;
-        k_reduce_dw<<<grid_for(total, 256), 256, 0, s>>>(part, p.g, p.nb, taps, c_in, c_out, dw_ref);
+        k_reduce_dw<<<grid_for(total, 32), 256, 0, s>>>(part, p.g, p.nb, taps, c_in, c_out, dw_ref);
         launched("dW split reduction");
     });
 }

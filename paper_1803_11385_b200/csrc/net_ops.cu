@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(kT) k_switch_gather(const int* __restrict__ pm
 // Column partial sums over row blocks: thread (r, q) owns channel quad q of rows
 // r, r + R, ... inside the block's row range; partials [block][C] in double.
 // MODE 0: sum x; 1: sum (x - mean)^2; 2: (sum dyb, sum dyb*xhat) with dyb = dy*(xhat > 0).
-constexpr int kRowsPerBlock = 2048;
+constexpr int kRowsPerBlock = 1024;
 
 template <int MODE, typename DT>
 __global__ void __launch_bounds__(kT) k_col_partials(const float* __restrict__ a, const DT* __restrict__ b, long long n,
@@ -180,7 +180,8 @@ __global__ void __launch_bounds__(kT) k_col_partials(const float* __restrict__ a
         if (MODE == 1)
 #pragma unroll
             for (int e = 0; e < 4; ++e) mu[e] = mean[q * 4 + e];
-        for (long long row = r0 + r; row < r1; row += R) {
+#pragma unroll 4
+        for (long long row = r0 + r; row < r1; row += R) {  // unrolled: 4 row loads in flight per thread
             const float4 x = __ldg(reinterpret_cast<const float4*>(a + row * C + q * 4));
             const float xv[4] = {x.x, x.y, x.z, x.w};
             if (MODE == 2) {
@@ -233,13 +234,28 @@ template <int MODE>
 __global__ void k_col_fold(const double* __restrict__ part, int blocks, long long n, int C, double* __restrict__ out0,
                            double* __restrict__ out1, float* __restrict__ run_mean, float* __restrict__ run_var,
                            float momentum, float eps, const double* __restrict__ mean, float* __restrict__ inv_std) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= C) return;
+    // one block per channel: thread j folds partial blocks j, j + kT, ..., then a fixed-shape
+    // tree over the kT lanes (deterministic for a given partial count)
+    const int c = blockIdx.x;
+    __shared__ double su[kT], sv[kT];
     double u = 0, v = 0;
-    for (int b = 0; b < blocks; ++b) {
+    for (int b = threadIdx.x; b < blocks; b += kT) {
         u += part[((long long)b * 2 + 0) * C + c];
         v += part[((long long)b * 2 + 1) * C + c];
     }
+    su[threadIdx.x] = u;
+    sv[threadIdx.x] = v;
+    __syncthreads();
+    for (int w = kT / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            su[threadIdx.x] += su[threadIdx.x + w];
+            sv[threadIdx.x] += sv[threadIdx.x + w];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
+    u = su[0];
+    v = sv[0];
     if (MODE == 0) {
         out0[c] = u / (double)n;
     } else if (MODE == 1) {
@@ -449,9 +465,9 @@ hc_status hc_native_bn_relu_forward(const float* x, int64_t n, int32_t c, int32_
         double* var = mean + c;
         if (training) {
             k_col_partials<0, float><<<blocks, kT, 0, s>>>(x, nullptr, n, c, nullptr, part);
-            k_col_fold<0><<<1, kT, 0, s>>>(part, blocks, n, c, mean, nullptr, nullptr, nullptr, 0, 0, nullptr, nullptr);
+            k_col_fold<0><<<c, kT, 0, s>>>(part, blocks, n, c, mean, nullptr, nullptr, nullptr, 0, 0, nullptr, nullptr);
             k_col_partials<1, float><<<blocks, kT, 0, s>>>(x, nullptr, n, c, mean, part);
-            k_col_fold<1><<<1, kT, 0, s>>>(part, blocks, n, c, nullptr, var, running_mean, running_var, momentum, eps,
+            k_col_fold<1><<<c, kT, 0, s>>>(part, blocks, n, c, nullptr, var, running_mean, running_var, momentum, eps,
                                           mean, inv_std);
             launched("batch-norm statistics", 4);
         } else {
@@ -480,13 +496,13 @@ hc_status hc_native_bn_relu_backward(const void* d_relu, hc_dtype dtype, const f
         if (dtype == HC_DTYPE_BF16) {
             const bf16* d = static_cast<const bf16*>(d_relu);
             k_col_partials<2, bf16><<<blocks, kT, 0, s>>>(xhat, d, n, c, nullptr, part);
-            k_col_fold<2><<<1, kT, 0, s>>>(part, blocks, n, c, s1, s2, nullptr, nullptr, 0, 0, nullptr, nullptr);
+            k_col_fold<2><<<c, kT, 0, s>>>(part, blocks, n, c, s1, s2, nullptr, nullptr, 0, 0, nullptr, nullptr);
             k_bn_relu_bwd_apply<bf16><<<grid_for(m, kT), kT, 0, s>>>(d, xhat, n, c, s1, s2, inv_std,
                                                                      static_cast<bf16*>(d_conv_bf16));
         } else {
             const float* d = static_cast<const float*>(d_relu);
             k_col_partials<2, float><<<blocks, kT, 0, s>>>(xhat, d, n, c, nullptr, part);
-            k_col_fold<2><<<1, kT, 0, s>>>(part, blocks, n, c, s1, s2, nullptr, nullptr, 0, 0, nullptr, nullptr);
+            k_col_fold<2><<<c, kT, 0, s>>>(part, blocks, n, c, s1, s2, nullptr, nullptr, 0, 0, nullptr, nullptr);
             k_bn_relu_bwd_apply<float><<<grid_for(m, kT), kT, 0, s>>>(d, xhat, n, c, s1, s2, inv_std,
                                                                       static_cast<bf16*>(d_conv_bf16));
         }
