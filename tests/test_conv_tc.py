@@ -188,3 +188,38 @@ def test_native_deconv_vs_oracle(cuda, restated, c_in, c_out):
     assert rel(y.cpu(), t(y64)) <= TOL_F32_OUT
     assert rel(dw.cpu(), t(dw64)) <= TOL_DW
     assert rel(nconv.to_channel_major(ddv).cpu(), t(dd64)) <= TOL_F32_OUT
+
+
+@pytest.mark.parametrize("n", [1, 127, 128, 129])
+def test_native_tiny_and_ragged_batches(cuda, n):
+    """Single voxel, one partial tile, exactly one tile, one voxel past a tile: forward, dW and
+    dX match float64 (the tile-major map pads with -1; dW partials of idle splits are zero)."""
+    g = torch.Generator(device="cuda").manual_seed(n)
+    c_in, c_out, n_in = 16, 32, n + 5
+    x = bf16_round(torch.rand((n_in, c_in), device="cuda", generator=g) * 2 - 1)
+    dy = bf16_round(torch.rand((n, c_out), device="cuda", generator=g) * 2 - 1)
+    w = bf16_round(torch.rand((c_out, c_in * 27), device="cuda", generator=g) * 2 - 1)
+    fmap = torch.randint(-1, n_in, (n, 27), device="cuda", generator=g, dtype=torch.int32)
+    wp = nconv.pack_weights(w, c_out, c_in, 27, False)
+    assert rel(nconv.gather_gemm(fmap, x.to(torch.bfloat16), wp, c_out, torch.float32),
+               ref_gather_gemm(fmap, x, w, c_out)) <= TOL_F32_OUT
+    assert rel(nconv.conv_dw(fmap, x.to(torch.bfloat16), dy.to(torch.bfloat16)), ref_dw(fmap, x, dy)) <= TOL_DW
+
+
+def test_native_empty_batch(cuda):
+    x = torch.zeros((4, 16), dtype=torch.bfloat16, device="cuda")
+    fmap = torch.zeros((0, 27), dtype=torch.int32, device="cuda")
+    wp = nconv.pack_weights(torch.zeros((32, 16 * 27), device="cuda"), 32, 16, 27, False)
+    assert nconv.gather_gemm(fmap, x, wp, 32).shape == (0, 32)
+    dw = nconv.conv_dw(fmap, x, torch.zeros((0, 32), dtype=torch.bfloat16, device="cuda"))
+    assert dw.shape == (32, 16 * 27) and float(dw.abs().sum()) == 0.0
+
+
+def test_native_argument_errors(cuda):
+    x = torch.zeros((4, 12), dtype=torch.bfloat16, device="cuda")  # C_in not a multiple of 8
+    fmap = torch.zeros((4, 27), dtype=torch.int32, device="cuda")
+    with pytest.raises(ValueError, match="multiple of 8"):
+        nconv.gather_gemm(fmap, x, torch.zeros((16, 384), dtype=torch.bfloat16, device="cuda"), 16)
+    x = torch.zeros((4, 16), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ValueError, match="16, 32, 64, 128 or 256"):
+        nconv.gather_gemm(fmap, x, torch.zeros((24, 448), dtype=torch.bfloat16, device="cuda"), 24)
