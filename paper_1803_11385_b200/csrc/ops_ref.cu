@@ -49,20 +49,30 @@ long long field_volume(const hc_conv_spec& sp, int dim) {
 }
 
 // ============================================================== K0 field map
+// Row-major K0 ([N_out][F^dim]): batched probes (see k_field_map_tiled), results staged in
+// shared memory so the block's 128 * F^dim entries (one contiguous span of the map) leave
+// in coalesced stores instead of 27 strided 4-byte stores per thread.
 template <int F>
-__global__ void k_field_map(DevPsh in, DevPsh out, int S, int pad, int* map) {
-    const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (col >= out.N) return;
-    const int4 c = out.cols[col];
-    const ModelParam mp = in.models[c.w - 1];
-    const int fd = in.dim == 3 ? F * F * F : F * F;
-    int nb[F * F * F];
-    probe_field<F>(in, mp, origin_axis(c.x, F, S, pad), origin_axis(c.y, F, S, pad),
-                   origin_axis(c.z, F, S, pad), nb);
-    int* dst = map + col * fd;
+__global__ void __launch_bounds__(128, 4) k_field_map(DevPsh in, DevPsh out, int S, int pad, int* map) {
+    constexpr int T = F * F * F;
+    __shared__ int st[128 * T];
+    const long long col0 = (long long)blockIdx.x * 128;
+    const long long col = col0 + threadIdx.x;
+    const int fd = in.dim == 3 ? T : F * F;
+    if (col < out.N) {
+        const int4 c = out.cols[col];
+        const ModelParam mp = in.models[c.w - 1];
+        int nb[T];
+        probe_field_batched<F>(in, mp, origin_axis(c.x, F, S, pad), origin_axis(c.y, F, S, pad),
+                               origin_axis(c.z, F, S, pad), nb);
 #pragma unroll
-    for (int t = 0; t < F * F * F; ++t)
-        if (t < fd) dst[t] = nb[t];
+        for (int t = 0; t < T; ++t)
+            if (t < fd) st[threadIdx.x * fd + t] = nb[t];
+    }
+    __syncthreads();
+    const long long cols = min(128LL, out.N - col0);
+    int* dst = map + col0 * fd;
+    for (int i = threadIdx.x; i < cols * fd; i += 128) dst[i] = st[i];
 }
 
 // Tap-major K0 ([F^3][N_out]): lanes of a warp write consecutive columns of each
@@ -75,8 +85,8 @@ __global__ void k_field_map_t(DevPsh in, DevPsh out, int S, int pad, int* map) {
     const ModelParam mp = in.models[c.w - 1];
     const int fd = in.dim == 3 ? F * F * F : F * F;
     int nb[F * F * F];
-    probe_field<F>(in, mp, origin_axis(c.x, F, S, pad), origin_axis(c.y, F, S, pad),
-                   origin_axis(c.z, F, S, pad), nb);
+    probe_field_batched<F>(in, mp, origin_axis(c.x, F, S, pad), origin_axis(c.y, F, S, pad),
+                           origin_axis(c.z, F, S, pad), nb);
     const long long N = out.N;
 #pragma unroll
     for (int t = 0; t < F * F * F; ++t)
@@ -644,8 +654,11 @@ void launch_field_map(const hc_psh* in, const hc_psh* out, const hc_conv_spec& s
         else if (sp.kernel == 2) k_field_map_t<2><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, map);
         else k_field_map_any_t<<<g, kThreads, 0, s>>>(in->d, out->d, sp.kernel, sp.stride, sp.pad,
                                                      (int)field_volume(sp, in->d.dim), map);
-    } else if (sp.kernel == 3) k_field_map<3><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, map);
-    else if (sp.kernel == 2) k_field_map<2><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, map);
+    } else if (sp.kernel == 3) {
+        k_field_map<3><<<grid_for(n, 128), 128, 0, s>>>(in->d, out->d, sp.stride, sp.pad, map);
+    } else if (sp.kernel == 2) {
+        k_field_map<2><<<grid_for(n, 128), 128, 0, s>>>(in->d, out->d, sp.stride, sp.pad, map);
+    }
     else k_field_map_any<<<g, kThreads, 0, s>>>(in->d, out->d, sp.kernel, sp.stride, sp.pad,
                                               (int)field_volume(sp, in->d.dim), map);
     launched("field_map");
