@@ -30,8 +30,10 @@ def timeit(fn, reps=10):
 
 def main():
     cs = [int(a) for a in sys.argv[1:]] or [16, 64, 128]
-    lv = bench.shell_levels(256)
-    s = SuperPsh.from_levels([lv[0]] * 8)
+    res = int(os.environ.get("HCB_RES", "256"))
+    batch = int(os.environ.get("HCB_BATCH", "8"))
+    lv = bench.shell_levels(res)
+    s = SuperPsh.from_levels([lv[0]] * batch)
     tag = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("HCB_"))
     n = s.total_columns()
     for c in cs:

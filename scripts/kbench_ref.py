@@ -33,9 +33,11 @@ def timeit(fn, reps=10):
 def main():
     C = int(sys.argv[1]) if len(sys.argv) > 1 else 16
     peak = json.load(open(bench.PEAKS_PATH))["hbm_gbs"] if os.path.exists(bench.PEAKS_PATH) else 6650.0
-    lv = bench.shell_levels(256)
-    fine = SuperPsh.from_levels([lv[0]] * 8)
-    coarse = SuperPsh.from_levels([lv[1]] * 8)
+    res = int(os.environ.get("HCB_RES", "256"))
+    batch = int(os.environ.get("HCB_BATCH", "8"))
+    lv = bench.shell_levels(res)
+    fine = SuperPsh.from_levels([lv[0]] * batch)
+    coarse = SuperPsh.from_levels([lv[1]] * batch)
     N, Nc, M, R = fine.total_columns(), coarse.total_columns(), fine.M, fine.R
     sp, pool = ConvSpec(3, 1, 0, C, C), ConvSpec(2, 2, 0, C, C)
     x = torch.rand((C, N), device="cuda") * 2 - 1
