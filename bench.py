@@ -424,7 +424,7 @@ def main():
         comp.wait_stream(d2h_s)
         barrier()
         es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ke = max(3, args.steps // 2)
+        ke = max(5, args.steps)  # long enough that pipeline fill / drain amortise
         es.record(comp)
         for k in range(ke):
             e2e_step(k)
