@@ -93,6 +93,11 @@ void hc_voxel_set_free(hc_voxel_set* s);
  * `injected_dim` mirror PshBuildOptions::injected_offsets (psh.hpp:55-58); pass NULL/0. */
 hc_status hc_build_psh(const hc_voxel_set* s, uint64_t seed, const uint8_t* injected,
                        int64_t injected_len, int32_t injected_dim, hc_psh_level** out);
+/* The same construction on the GPU: identical sizing, growth schedule
+ * and lookup semantics (psh.cpp:170-227), offsets found by a parallel CAS-claimed search
+ * instead of the sequential greedy scan -> a different but equally perfect table (every
+ * lookup returns the reference's column). Returns a host PshLevel like hc_build_psh. */
+hc_status hc_build_psh_device(const hc_voxel_set* s, uint64_t seed, hc_psh_level** out);
 /* info: dim, resolution, n, hash_dim (m_bar), offset_dim (r_bar), channels */
 hc_status hc_psh_level_info(const hc_psh_level* l, int64_t info[6]);
 hc_status hc_psh_level_copy(const hc_psh_level* l, int32_t* hash, uint8_t* offsets, uint16_t* tags,

@@ -63,6 +63,7 @@ _SIGS = {
     "hc_voxel_set_info": [_P, _P],
     "hc_voxel_set_copy": [_P, _P, _P],
     "hc_build_psh": [_P, C.c_uint64, _P, _I64, _I32, _P],
+    "hc_build_psh_device": [_P, C.c_uint64, _P],
     "hc_psh_level_info": [_P, _P],
     "hc_psh_level_copy": [_P, _P, _P, _P, _P],
     "hc_write_psh_file": [C.c_char_p, _P, _I32],

@@ -67,6 +67,8 @@ struct PshLevel {
 };
 
 std::int64_t ipow(std::int64_t b, int e);
+std::int32_t psh_hash_dim(std::int64_t n, int dim);          // psh.cpp:170-175 minimal_hash_dim
+std::int32_t psh_first_offset_dim(std::int64_t n, int dim);  // psh.cpp:177-183 initial_offset_dim
 
 }  // namespace hcb
 

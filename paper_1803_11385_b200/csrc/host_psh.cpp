@@ -427,6 +427,10 @@ void get_array(std::istream& in, std::vector<T>& v, std::size_t count) {
 }
 
 }  // namespace
+
+// psh.cpp:170-185 sizing, shared with the device builder (psh_build.cu)
+std::int32_t psh_hash_dim(std::int64_t n, int dim) { return min_hash_dim(n, dim); }
+std::int32_t psh_first_offset_dim(std::int64_t n, int dim) { return first_offset_dim(n, dim); }
 }  // namespace hcb
 
 using namespace hcb;

@@ -90,6 +90,14 @@ class PshLevel:
         check(lib.hc_build_psh(s._h, seed, _ptr(inj), 0 if inj is None else inj.size, injected_dim, C.byref(h)))
         return cls(h)
 
+    @classmethod
+    def build_device(cls, s: VoxelSet, seed: int = 0) -> "PshLevel":
+        """build_psh on the GPU (hc_build_psh_device): same sizing and lookups, tables found
+        by a parallel search (a different valid PSH of the same set)."""
+        h = C.c_void_p()
+        check(lib.hc_build_psh_device(s._h, seed, C.byref(h)))
+        return cls(h)
+
     def hash_slots(self) -> int:
         return self.hash_dim ** self.dim
 
