@@ -640,6 +640,8 @@ def net_main(args, rank, world, local):
         en.record()
         torch.cuda.synchronize()
         launches = _lib.lib.hc_launch_count() - launches0
+        if mode == "cuda-graph":  # graph replays bypass the host launch counter
+            launches = one.launches_per_step * args.steps
     t = torch.tensor([st.elapsed_time(en) / args.steps], device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -323,8 +323,12 @@ class GraphedStep:
                 self._step()
         torch.cuda.current_stream().wait_stream(s)
         self.graph = torch.cuda.CUDAGraph()
+        before = int(lib.hc_launch_count())
         with torch.cuda.graph(self.graph):
             self.loss = self._step()
+        # this library's kernels captured per step (replays do not pass through the host
+        # launch counter; callers multiply by the replays they time)
+        self.launches_per_step = int(lib.hc_launch_count()) - before
 
     def _step(self):
         nb = NetBatch.build(self.levels)

@@ -332,10 +332,15 @@ def test_full_size_delta_kernel_and_adjoint(shell256):
         w[ch, ch * 27 + 13] = 1.0
     assert torch.equal(ops.conv_forward(fine, x, fine, w, sp), x)
     cols = ops.hash2col(fine, x, fine, sp)
-    y = torch.rand_like(cols) * 2 - 1
+    g = torch.Generator(device="cuda").manual_seed(13)
+    y = torch.rand(cols.shape, device="cuda", generator=g) * 2 - 1
     lhs = torch.dot(cols.double().flatten(), y.double().flatten())
     rhs = torch.dot(x.double().flatten(), ops.col2hash(y, fine, fine, sp).double().flatten())
-    assert abs(float(lhs - rhs)) / max(abs(float(lhs)), 1e-6) <= 1e-6
+    # col2hash rounds its fp32 sums (<= 27 terms each): bound the difference by the dot
+    # product's condition, sum |cols * y| (7.4M random-sign terms cancel to |lhs| ~ 40, so a
+    # bound relative to |lhs| would only measure the cancellation, not the operator).
+    scale = float(torch.dot(cols.double().abs().flatten(), y.double().abs().flatten()))
+    assert abs(float(lhs - rhs)) <= 1e-6 * scale
 
 
 def test_full_size_field_map_symmetry(shell256):
