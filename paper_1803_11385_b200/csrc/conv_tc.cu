@@ -195,11 +195,15 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, PW>::THREADS, CPS)
 
     if (warp < PW) {
         // ---------------- producers
-        const int c = tid & 7;    // 16-byte chunk within a 128-byte row
-        const int r0 = tid >> 3;  // rows r0 + RS*j
+        // thread (q, c): 16-byte chunk c of the J CONSECUTIVE rows q*J .. q*J+J-1, so its map
+        // entries are one or two 16-byte shared loads instead of J scalar ones (a warp's
+        // cp.async still covers 4 whole rows: the 4 q of the warp at the same j)
+        const int c = tid & 7;
+        const int r0 = (tid >> 3) * J;
+        static_assert(J % 4 == 0, "map entries are loaded 4 at a time");
         uint32_t doff[J];
 #pragma unroll
-        for (int j = 0; j < J; ++j) doff[j] = sw128_offset(r0 + RS * j, c);
+        for (int j = 0; j < J; ++j) doff[j] = sw128_offset(r0 + j, c);
         const int t0 = (c * 8) / C, ci0 = c * 8 - t0 * C;
         const uint32_t row_bytes = (uint32_t)C * 2;
         auto request = [&](int tile, int buf) {
@@ -224,7 +228,10 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, PW>::THREADS, CPS)
                 int g[J];
                 if (t < taps) {  // k = t*C + ci < K
 #pragma unroll
-                    for (int j = 0; j < J; ++j) g[j] = ld_shared_s32(nb + (t * BM + RS * j) * 4);
+                    for (int j = 0; j < J; j += 4) {
+                        const int4 v = ld_shared_v4(nb + (t * BM + j) * 4);
+                        g[j] = v.x, g[j + 1] = v.y, g[j + 2] = v.z, g[j + 3] = v.w;
+                    }
                 } else {
 #pragma unroll
                     for (int j = 0; j < J; ++j) g[j] = -1;
@@ -438,17 +445,17 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
     if (warp < PW) {
         // ---------------- producers
         const int c = tid & 7;
-        const int q = tid >> 3;  // rows q + RS*j of the stage's 128 (block, voxel) rows
+        // thread (q, c): chunk c of the J consecutive rows q*J .. q*J+J-1 of the stage's 128
+        // (block, voxel) rows — all in one 64-wide MN block, so one (tap, channel) entry per
+        // stage and the J map entries as 16-byte shared loads
+        const int q = tid >> 3;
+        static_assert(J % 4 == 0 && 64 % J == 0, "rows of a thread stay in one MN block");
+        const int blk = (q * J) >> 6, v0 = (q * J) & 63;
         const uint32_t row_bytes = (uint32_t)C * 2;
-        const uint32_t tab_s = smem_u32(tab);
+        const uint32_t tab_s = smem_u32(tab) + (blk * 8 + c) * 4;
         uint32_t doff[J];
-        int vj[J];
 #pragma unroll
-        for (int j = 0; j < J; ++j) {
-            const int row = q + RS * j, blk = row >> 6, v = row & 63;
-            doff[j] = blk * (Cfg::KB * 128) + sw128_offset(v, c);
-            vj[j] = v;
-        }
+        for (int j = 0; j < J; ++j) doff[j] = blk * (Cfg::KB * 128) + sw128_offset(v0 + j, c);
         auto request = [&](int lt, int buf) {
             mbar_arrive_expect_tx(nfull0 + 8 * buf, nbr_bytes);
             bulk_g2s(smem_u32(nbr_s + buf * NT * BM), fmap + ((long long)(tile0 + lt) * taps + t_lo) * BM, nbr_bytes,
@@ -480,21 +487,23 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
                 }
                 const uint32_t nbh = nb + h * 64 * 4;
                 for (int mi = 0; mi < nm; ++mi) {
-                    const int e0 = ld_shared_s32(tab_s + (mi * 16 + c) * 4);
-                    const int e1 = ld_shared_s32(tab_s + (mi * 16 + 8 + c) * 4);
+                    const int e = ld_shared_s32(tab_s + mi * 64);
                     int g[J];
+                    if (e >= 0) {
 #pragma unroll
-                    for (int j = 0; j < J; ++j) {
-                        const int e = ((q + RS * j) >> 6) ? e1 : e0;
-                        g[j] = e >= 0 ? ld_shared_s32(nbh + ((e >> 16) * BM + vj[j]) * 4) : -1;
+                        for (int j = 0; j < J; j += 4) {
+                            const int4 w = ld_shared_v4(nbh + ((e >> 16) * BM + v0 + j) * 4);
+                            g[j] = w.x, g[j + 1] = w.y, g[j + 2] = w.z, g[j + 3] = w.w;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < J; ++j) g[j] = -1;
                     }
                     mbar_wait_sleep(empty0 + 8 * s, ph ^ 1);
                     const uint32_t A = sbase + s * Cfg::A_BYTES;
-                    const char* x0 = reinterpret_cast<const char*>(X + (e0 & 0xffff));
-                    const char* x1 = reinterpret_cast<const char*>(X + (e1 & 0xffff));
+                    const char* xs = reinterpret_cast<const char*>(X + (e & 0xffff));
 #pragma unroll
-                    for (int j = 0; j < J; ++j)
-                        cp_async16_row(A + doff[j], ((q + RS * j) >> 6) ? x1 : x0, g[j], row_bytes);
+                    for (int j = 0; j < J; ++j) cp_async16_row(A + doff[j], xs, g[j], row_bytes);
                     cp_async_arrive_noinc(full0 + 8 * s);
                     if (++s == S) {
                         s = 0;
@@ -718,7 +727,7 @@ __global__ void k_to_channel_major(const T* __restrict__ in, long long N, long l
 // ====================================================================== launchers
 // Forward variant: HCB_FWD_CPS = CTAs per SM (2: BN <= 64 only, so both CTAs'
 // double-buffered accumulators fit TMEM; 1: one deep ring), HCB_FWD_PW = producer warps
-// (4, 8 or 16).
+// (2, 4 or 8).
 template <int BN, int CPS, int PW, typename OutT>
 void launch_fwd(const int* fmap, int taps, long long rows, const bf16* X, int C, const bf16* Wp, int Kp, OutT* Y,
                 cudaStream_t s) {
@@ -752,7 +761,6 @@ void launch_fwd_bn(const int* fmap, int taps, long long rows, const bf16* X, int
         }
     }
     if (pw == 4) return launch_fwd<BN, 1, 4>(fmap, taps, rows, X, C, Wp, Kp, Y, s);
-    if (pw == 16) return launch_fwd<BN, 1, 16>(fmap, taps, rows, X, C, Wp, Kp, Y, s);
     launch_fwd<BN, 1, 8>(fmap, taps, rows, X, C, Wp, Kp, Y, s);
 }
 
@@ -851,7 +859,7 @@ void launch_dw_pw(const DwPlan& p, const int* fmap, int taps, long long rows, co
 }
 
 // HCB_DW_PW = producer warps of the dW kernel (2/4/8 with 2 CTAs per SM, default 4;
-// 4/8/16 with one, default 8). Measured on B200 (scripts/gpu_ab.sh).
+// 4/8 with one, default 8). Measured on B200 (scripts/gpu_ab.sh).
 template <int NB>
 void launch_dw(const DwPlan& p, const int* fmap, int taps, long long rows, const bf16* X, int C, const bf16* dY,
                int Cout, float* partial, cudaStream_t s) {
@@ -866,7 +874,6 @@ void launch_dw(const DwPlan& p, const int* fmap, int taps, long long rows, const
         }
     }
     if (pw == 4) return launch_dw_pw<NB, 4, 1>(p, fmap, taps, rows, X, C, dY, Cout, partial, s);
-    if (pw == 16) return launch_dw_pw<NB, 16, 1>(p, fmap, taps, rows, X, C, dY, Cout, partial, s);
     launch_dw_pw<NB, 8, 1>(p, fmap, taps, rows, X, C, dY, Cout, partial, s);
 }
 

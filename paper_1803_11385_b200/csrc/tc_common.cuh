@@ -111,6 +111,12 @@ __device__ __forceinline__ int ld_shared_s32(uint32_t addr) {
     asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
 }
+// 16-byte shared load (4 consecutive int32) by address.
+__device__ __forceinline__ int4 ld_shared_v4(uint32_t addr) {
+    int4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 // Arrive on an mbarrier once ALL of this thread's prior cp.async copies have landed
 // (non-blocking; .noinc: the arrival counts against the barrier's expected count).
