@@ -116,6 +116,40 @@ CUtensorMap map2d(const void* base, uint64_t inner, uint64_t rows, uint64_t pitc
     return m;
 }
 
+// Row-major [rows][cols] output for the epilogue's TMA stores: box = box_rows x box_cols,
+// no swizzle, rows past `rows` are clipped by the TMA unit.
+CUtensorMap map_out(const void* base, bool fp32, uint64_t cols, uint64_t rows, uint32_t box_cols, uint32_t box_rows) {
+    CUtensorMap m;
+    const uint64_t es = fp32 ? 4 : 2;
+    const cuuint64_t dims[2] = {cols, rows};
+    const cuuint64_t strides[1] = {cols * es};
+    const cuuint32_t box[2] = {box_cols, box_rows};
+    const cuuint32_t ess[2] = {1, 1};
+    const CUresult r = encoder()(&m, fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                                 const_cast<void*>(base), dims, strides, box, ess, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw cuda_error("cuTensorMapEncodeTiled (output) failed (" + std::to_string((int)r) + ")");
+    return m;
+}
+
+// 16 channels of one row -> 32 (bf16) or 64 (fp32) bytes of shared memory
+__device__ __forceinline__ void stage_row16(uint8_t* dst, const float (&v)[16], bf16*) {
+    uint32_t p[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+        p[i] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    reinterpret_cast<uint4*>(dst)[0] = make_uint4(p[0], p[1], p[2], p[3]);
+    reinterpret_cast<uint4*>(dst)[1] = make_uint4(p[4], p[5], p[6], p[7]);
+}
+__device__ __forceinline__ void stage_row16(uint8_t* dst, const float (&v)[16], float*) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        reinterpret_cast<float4*>(dst)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+}
+
 __device__ __forceinline__ void store_row(float* dst, const float (&v)[16]) {
 #pragma unroll
     for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
@@ -134,27 +168,32 @@ __device__ __forceinline__ void store_row(bf16* dst, const float (&v)[16]) {
 // ====================================================================== forward gather-GEMM
 // Y[m][0:BN] = sum_k A[m][k] * Wp[0:BN][k],  A[m][k] = X[nbr(m, k / C)][k % C] (0 if -1)
 // CPS resident CTAs per SM (1: one deep ring; 2: two shallower rings), PW producer warps.
-template <int BN, int CPS, int PW>
+template <int BN, int CPS, int PW, int OUT_BYTES = 2>
 struct FwdCfg {
     static constexpr int A_BYTES = BM * 128;  // 16 KB
     static constexpr int B_BYTES = BN * 128;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int NBR = 2 * kNbrBytes;
-    static constexpr int BUDGET = (CPS == 2 ? 113 : 226) * 1024 - 1024 - 320 - NBR;
+    // epilogue staging: per epilogue warp EPI_BUFS buffers of 32 rows x 16 channels
+    static constexpr int EPI_BUFS = (OUT_BYTES == 2 && BN < 256) ? 2 : 1;  // BN=256 keeps a 4-stage ring
+    static constexpr int EPI_BUF = 32 * 16 * OUT_BYTES;
+    static constexpr int EPI = 4 * EPI_BUFS * EPI_BUF;
+    static constexpr int BUDGET = (CPS == 2 ? 113 : 226) * 1024 - 1024 - 320 - NBR - EPI;
 #ifndef HCB_FWD_MAXSTAGES
 #define HCB_FWD_MAXSTAGES 10
 #endif
     static constexpr int STAGES = BUDGET / STAGE_BYTES > HCB_FWD_MAXSTAGES ? HCB_FWD_MAXSTAGES : BUDGET / STAGE_BYTES;
     static constexpr int PRODUCERS = PW * 32;      // warps 0..PW-1
     static constexpr int THREADS = PW * 32 + 192;  // + epilogue warps PW..PW+3, MMA warp PW+4, TMA warp PW+5
-    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + NBR + 320;
+    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + NBR + EPI + 320;
 };
 
 template <int BN, int CPS, int PW, typename OutT>
-__global__ void __launch_bounds__(FwdCfg<BN, CPS, PW>::THREADS, CPS)
-    k_conv_fwd(const __grid_constant__ CUtensorMap wmap, const int* __restrict__ fmap, int taps, long long rows,
-               const bf16* __restrict__ X, int C, int nkb, OutT* __restrict__ Y, int tiles) {
-    using Cfg = FwdCfg<BN, CPS, PW>;
+__global__ void __launch_bounds__(FwdCfg<BN, CPS, PW, sizeof(OutT)>::THREADS, CPS)
+    k_conv_fwd(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap ymap,
+               const int* __restrict__ fmap, int taps, long long rows, const bf16* __restrict__ X, int C, int nkb,
+               int tiles) {
+    using Cfg = FwdCfg<BN, CPS, PW, sizeof(OutT)>;
     constexpr int NP = Cfg::PRODUCERS;
     constexpr int S = Cfg::STAGES;
     constexpr int RS = NP / 8;  // row stride between one producer thread's rows
@@ -163,7 +202,8 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, PW>::THREADS, CPS)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     int* nbr_s = reinterpret_cast<int*>(smem + S * Cfg::STAGE_BYTES);  // [2][taps][128]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * Cfg::STAGE_BYTES + Cfg::NBR);
+    uint8_t* epi_s = smem + S * Cfg::STAGE_BYTES + Cfg::NBR;           // [4 warps][EPI_BUFS][32][16]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * Cfg::STAGE_BYTES + Cfg::NBR + Cfg::EPI);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 6);
     int* nbr_cnt = reinterpret_cast<int*>(tmem_slot + 2);  // warps done with each map buffer
 
@@ -261,15 +301,19 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, PW>::THREADS, CPS)
             }
         }
     } else if (warp < PW + 4) {
-        // ---------------- epilogue warpgroup: TMEM -> registers -> Y rows
+        // ---------------- epilogue warpgroup: TMEM -> registers -> shared staging -> TMA store.
+        // Row-per-thread global stores would cost 32 L1 wavefronts per instruction (one line
+        // per lane) on the same LSU pipe the gathers need; staged 32 x 16 boxes leave by TMA.
         const int q = warp & 3;  // TMEM lane quadrant of this warp
-        const int row = q * 32 + (int)lane_id();
+        const int lane = (int)lane_id();
+        uint8_t* stage = epi_s + q * (Cfg::EPI_BUFS * Cfg::EPI_BUF);
+        int nb_issued = 0;
         int i = 0;
         for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++i) {
             const int acc = i & 1;
             mbar_wait_sleep(tfull0 + 8 * acc, (uint32_t)((i >> 1) & 1));
             tc_fence_after();
-            const long long m = (long long)tile * BM + row;
+            const int r0 = tile * BM + q * 32;
 #pragma unroll
             for (int c0 = 0; c0 < BN; c0 += 16) {
                 uint32_t v[16];
@@ -278,11 +322,25 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, PW>::THREADS, CPS)
                 float f[16];
 #pragma unroll
                 for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(v[e]);
-                if (m < rows) store_row(Y + m * BN + c0, f);
+                uint8_t* buf = stage + (nb_issued % Cfg::EPI_BUFS) * Cfg::EPI_BUF;
+                if (nb_issued >= Cfg::EPI_BUFS) {  // that buffer's previous store has been read
+                    if (lane == 0) bulk_wait_read<Cfg::EPI_BUFS - 1>();
+                    __syncwarp();
+                }
+                stage_row16(buf + lane * 16 * (int)sizeof(OutT), f, (OutT*)nullptr);
+                fence_proxy_async();  // generic smem writes -> TMA (async proxy) reads
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store2d(&ymap, smem_u32(buf), c0, r0);
+                    bulk_commit();
+                }
+                ++nb_issued;
             }
             tc_fence_before();
             mbar_arrive(tempty0 + 8 * acc);
         }
+        if (lane == 0) bulk_wait<0>();  // the last stores complete before the CTA retires
+        __syncwarp();
     } else if (tid == (PW + 5) * 32) {
         // ---------------- weight-tile loader (single thread): one 2-D TMA per stage
         int s = 0;
@@ -731,7 +789,7 @@ __global__ void k_to_channel_major(const T* __restrict__ in, long long N, long l
 template <int BN, int CPS, int PW, typename OutT>
 void launch_fwd(const int* fmap, int taps, long long rows, const bf16* X, int C, const bf16* Wp, int Kp, OutT* Y,
                 cudaStream_t s) {
-    using Cfg = FwdCfg<BN, CPS, PW>;
+    using Cfg = FwdCfg<BN, CPS, PW, sizeof(OutT)>;
     auto kern = k_conv_fwd<BN, CPS, PW, OutT>;
     static bool attr = false;  // per instantiation
     if (!attr) {
@@ -741,7 +799,8 @@ void launch_fwd(const int* fmap, int taps, long long rows, const bf16* X, int C,
     const CUtensorMap wm = map2d(Wp, (uint64_t)Kp, (uint64_t)BN, (uint64_t)Kp * 2, BN);
     const int tiles = (int)((rows + BM - 1) / BM);
     const int grid = std::min(tiles, CPS * num_sms());
-    kern<<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(wm, fmap, taps, rows, X, C, Kp / BK, Y, tiles);
+    const CUtensorMap ym = map_out(Y, sizeof(OutT) == 4, (uint64_t)BN, (uint64_t)rows, 16, 32);
+    kern<<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(wm, ym, fmap, taps, rows, X, C, Kp / BK, tiles);
     launched("conv gather-GEMM (tcgen05)");
 }
 
