@@ -432,7 +432,7 @@ struct DwCfg {
     static constexpr int BUDGET = (CPS == 2 ? 113 : 226) * 1024 - 1024 - 512 - 1024 - NBR - BSTAGES * B_BYTES;
     static constexpr int STAGES = BUDGET / A_BYTES > 10 ? 10 : BUDGET / A_BYTES;
     static constexpr int PRODUCERS = PW * 32;
-    static constexpr int THREADS = PRODUCERS + 32;  // + MMA / TMEM warp
+    static constexpr int THREADS = PRODUCERS + 64;  // + MMA / TMEM warp PW, dY TMA warp PW+1
     static constexpr int TMEM_COLS = 512 / CPS;     // per CTA (CPS resident CTAs per SM)
     static constexpr int SMEM = 1024 + STAGES * A_BYTES + BSTAGES * B_BYTES + NBR + 1024 + 512;
 };
@@ -523,26 +523,13 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
             if (ntl > 0) request(0, 0);
             if (ntl > 1) request(1, 1);
         }
-        int s = 0, bs = 0;
-        uint32_t ph = 0, bph = 0;
+        int s = 0;
+        uint32_t ph = 0;
         for (int lt = 0; lt < ntl; ++lt) {
             const int buf = lt & 1;
             mbar_wait_sleep(nfull0 + 8 * buf, (uint32_t)((lt >> 1) & 1));
             const uint32_t nb = smem_u32(nbr_s + buf * NT * BM);
             for (int h = 0; h < 2; ++h) {
-                if (tid == 0) {  // dY rows of this half tile -> B stage (all NB/64 co blocks)
-                    mbar_wait_sleep(bempty0 + 8 * bs, bph ^ 1);
-                    mbar_arrive_expect_tx(bfull0 + 8 * bs, Cfg::B_BYTES);
-                    const int n0 = (tile0 + lt) * BM + h * 64;
-#pragma unroll
-                    for (int cb = 0; cb < NB / 64; ++cb)
-                        tma_load2d(bbase + bs * Cfg::B_BYTES + cb * (Cfg::KB * 128), &dymap, cb * 64, n0,
-                                   bfull0 + 8 * bs);
-                }
-                if (++bs == BS) {
-                    bs = 0;
-                    bph ^= 1;
-                }
                 const uint32_t nbh = nb + h * 64 * 4;
                 for (int mi = 0; mi < nm; ++mi) {
                     const int e = ld_shared_s32(tab_s + mi * 64);
@@ -602,6 +589,25 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
                 }
             }
         }
+    } else if (tid == (PW + 1) * 32) {
+        // ---------------- dY loader (own warp: a producer thread blocking on the B ring
+        // would stall its A rows and with them every stage)
+        int bs = 0;
+        uint32_t bph = 0;
+        for (int lt = 0; lt < ntl; ++lt)
+            for (int h = 0; h < 2; ++h) {
+                mbar_wait_sleep(bempty0 + 8 * bs, bph ^ 1);
+                mbar_arrive_expect_tx(bfull0 + 8 * bs, Cfg::B_BYTES);
+                const int n0 = (tile0 + lt) * BM + h * 64;
+#pragma unroll
+                for (int cb = 0; cb < NB / 64; ++cb)
+                    tma_load2d(bbase + bs * Cfg::B_BYTES + cb * (Cfg::KB * 128), &dymap, cb * 64, n0,
+                               bfull0 + 8 * bs);
+                if (++bs == BS) {
+                    bs = 0;
+                    bph ^= 1;
+                }
+            }
     } else if (warp == PW && ntl > 0) {
         // ---------------- MMA issuer: warp-uniform loop, one elected lane issues
         constexpr uint32_t idesc = idesc_bf16_f32(BM, NB, true, true);
