@@ -71,9 +71,29 @@ def shell_levels(res: int):
             return lv
     s = VoxelSet.sphere(res, True)
     lv = [PshLevel.build(s, mix_seed(1, 0)), PshLevel.build(s.coarsen(), mix_seed(1, 1))]
-    write_psh_file(path + ".tmp", lv)
-    os.replace(path + ".tmp", path)
+    tmp = f"{path}.tmp{os.getpid()}"  # ranks of a multi-GPU launch may race to build the cache
+    write_psh_file(tmp, lv)
+    os.replace(tmp, path)
     return lv
+
+
+def _device(local: int):
+    """One process per GPU (LOCAL_RANK). HCB_TEST_SHARE_GPU=1 folds ranks onto the visible GPUs
+    (N>1 code-path checks on a 1-GPU box, with HCB_TEST_DIST_BACKEND=gloo; timings meaningless)."""
+    import torch
+    if os.environ.get("HCB_TEST_SHARE_GPU") == "1":
+        local = local % torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    return torch.device("cuda", local)
+
+
+def _init_dist(dev):
+    import torch.distributed as dist
+    backend = os.environ.get("HCB_TEST_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(backend)
 
 
 def peaks():
@@ -328,10 +348,9 @@ def main():
 
     import torch
     import torch.distributed as dist
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    dev = _device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        _init_dist(dev)
 
     from paper_1803_11385_b200 import _lib
     from paper_1803_11385_b200.psh import SuperPsh
@@ -548,8 +567,9 @@ def shell_pyramid(res: int):
         if lv and lv[0].resolution == res and lv[-1].resolution == 4:
             return lv
     lv = build_pyramid(VoxelSet.sphere(res, True), 1)
-    write_psh_file(path + ".tmp", lv)
-    os.replace(path + ".tmp", path)
+    tmp = f"{path}.tmp{os.getpid()}"  # ranks of a multi-GPU launch may race to build the cache
+    write_psh_file(tmp, lv)
+    os.replace(tmp, path)
     return lv
 
 
@@ -594,10 +614,9 @@ def net_main(args, rank, world, local):
                           "e2e": {"value": v, "unit": "shapes/s", "h2d_bytes_per_step": 0,
                                   "d2h_bytes_per_step": 0}}))
         return
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    dev = _device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        _init_dist(dev)
     from paper_1803_11385_b200 import _lib
     from paper_1803_11385_b200 import net as nnet
     from paper_1803_11385_b200.dist import allreduce_gradients
@@ -679,10 +698,9 @@ def seg_main(args, rank, world, local):
             print(json.dumps({"impl": "reference", "unavailable": "the reference has no segmentation net "
                                                                   "(only its operators: see --workload conv)"}))
         return
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    dev = _device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        _init_dist(dev)
     from paper_1803_11385_b200 import _lib
     from paper_1803_11385_b200.psh import SuperPsh
     from paper_1803_11385_b200.dist import allreduce_gradients
