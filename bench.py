@@ -410,18 +410,19 @@ def main():
                 pin_memory=True), torch.empty((args.cin, N), pin_memory=True)]
 
         # Pipelined across steps: H2D of step k+1 and D2H of step k-1 run on their own
-        # copy streams (independent copy engines) while step k computes; two slots of
+        # copy streams (independent copy engines) while step k computes; NSLOT slots of
         # device staging buffers; every byte of every step still crosses PCIe.
         comp = torch.cuda.current_stream()
         h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
+        NSLOT = int(os.environ.get("HCB_E2E_SLOTS", "3"))  # 3 decouples H2D(k+1) from compute(k-1)
         slots = [dict(x=torch.empty_like(step.x_ref), w=torch.empty_like(step.w), dy=torch.empty_like(step.dy_ref),
                       out=[torch.empty_like(o).pin_memory() for o in outs], free=torch.cuda.Event(),
-                      ready=torch.cuda.Event(), done=torch.cuda.Event()) for _ in range(2)]
+                      ready=torch.cuda.Event(), done=torch.cuda.Event()) for _ in range(NSLOT)]
         for sl in slots:
             sl["free"].record(comp)
 
         def e2e_step(k):
-            sl = slots[k % 2]
+            sl = slots[k % NSLOT]
             h2d_s.wait_event(sl["free"])
             with torch.cuda.stream(h2d_s):
                 sl["x"].copy_(hx, non_blocking=True)
