@@ -147,6 +147,47 @@ __device__ __forceinline__ void probe_field_batched(const DevPsh& s, const Model
     const unsigned* phib = s.phi + mp.offset_base;
     const uint2* slotb = s.slots + mp.hash_base;
     const int dbase = (int)mp.data_base;
+    if (dim == 3 && bx >= 0 && by >= 0 && bz >= 0 && bx + F <= res && by + F <= res && bz + F <= res) {
+        // interior field (every shell voxel away from the domain faces): no per-tap validity,
+        // cell / slot-row / key prefixes per (dz, dy), 32-bit offsets from the model's bases
+        int rmx[F], rmy[F], rmz[F], rrx[F], cyz[F * F];
+        unsigned kyz[F * F];
+#pragma unroll
+        for (int d = 0; d < F; ++d) {
+            rmx[d] = fmod_small(bx + d, m, mp.inv_m);
+            rmy[d] = fmod_small(by + d, m, mp.inv_m);
+            rmz[d] = fmod_small(bz + d, m, mp.inv_m);
+            rrx[d] = fmod_small(bx + d, r, mp.inv_r);
+        }
+#pragma unroll
+        for (int dz = 0; dz < F; ++dz)
+#pragma unroll
+            for (int dy = 0; dy < F; ++dy) {
+                cyz[dz * F + dy] =
+                    (fmod_small(bz + dz, r, mp.inv_r) * r + fmod_small(by + dy, r, mp.inv_r)) * r;
+                kyz[dz * F + dy] = ((unsigned)(bz + dz) << (2 * kb)) | ((unsigned)(by + dy) << kb);
+            }
+        unsigned ph[T];
+#pragma unroll
+        for (int t = 0; t < T; ++t) ph[t] = __ldg(phib + cyz[t / F] + rrx[t % F]);
+        uint2 e[T];
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+            const int dz = t / (F * F), dy = (t / F) % F, dx = t % F;
+            int sx = rmx[dx] + (int)(ph[t] & 0xFF);
+            int sy = rmy[dy] + (int)((ph[t] >> 8) & 0xFF);
+            int sz = rmz[dz] + (int)((ph[t] >> 16) & 0xFF);
+            if (sx >= m) sx -= m;
+            if (sy >= m) sy -= m;
+            if (sz >= m) sz -= m;
+            e[t] = __ldg(slotb + (sz * m + sy) * m + sx);
+        }
+#pragma unroll
+        for (int t = 0; t < T; ++t)
+            out[t] = ((int)e[t].x >= 0 && e[t].y == (kyz[t / F] | (unsigned)(bx + t % F))) ? dbase + (int)e[t].x
+                                                                                           : -1;
+        return;
+    }
     int rmx[F], rmy[F], rmz[F], rrx[F], rry[F], rrz[F];
     bool vx[F], vy[F], vz[F];
 #pragma unroll
