@@ -116,8 +116,8 @@ CUtensorMap map2d(const void* base, uint64_t inner, uint64_t rows, uint64_t pitc
     return m;
 }
 
-// Row-major [rows][cols] output for the epilogue's TMA stores: box = box_rows x box_cols,
-// no swizzle, rows past `rows` are clipped by the TMA unit.
+// Row-major [rows][cols] output for the epilogue's TMA stores: box = box_rows x box_cols
+// (16 channels = 32 / 64 bytes: SWIZZLE_32B / 64B staging), rows past `rows` are clipped.
 CUtensorMap map_out(const void* base, bool fp32, uint64_t cols, uint64_t rows, uint32_t box_cols, uint32_t box_rows) {
     CUtensorMap m;
     const uint64_t es = fp32 ? 4 : 2;
@@ -127,27 +127,34 @@ CUtensorMap map_out(const void* base, bool fp32, uint64_t cols, uint64_t rows, u
     const cuuint32_t ess[2] = {1, 1};
     const CUresult r = encoder()(&m, fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                                  const_cast<void*>(base), dims, strides, box, ess, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                 CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                 fp32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_NONE,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw cuda_error("cuTensorMapEncodeTiled (output) failed (" + std::to_string((int)r) + ")");
     return m;
 }
 
-// 16 channels of one row -> 32 (bf16) or 64 (fp32) bytes of shared memory
-__device__ __forceinline__ void stage_row16(uint8_t* dst, const float (&v)[16], bf16*) {
+// 16 channels of row r (0..31) -> its 32 (bf16) or 64 (fp32) bytes of the staging box, in the
+// TMA SWIZZLE_32B / SWIZZLE_64B layout (16-byte chunk k stored at k ^ (r>>2 & 1) resp.
+// k ^ (r>>1 & 3)), so a warp's 16-byte stores spread over all banks (4 wavefronts per
+// instruction instead of 8 with plain 32-byte rows).
+__device__ __forceinline__ void stage_row16(uint8_t* box, int r, const float (&v)[16], bf16*) {
     uint32_t p[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
         p[i] = *reinterpret_cast<uint32_t*>(&h);
     }
-    reinterpret_cast<uint4*>(dst)[0] = make_uint4(p[0], p[1], p[2], p[3]);
-    reinterpret_cast<uint4*>(dst)[1] = make_uint4(p[4], p[5], p[6], p[7]);
+    uint4* row = reinterpret_cast<uint4*>(box + r * 32);
+    const int x = (r >> 2) & 1;
+    row[0 ^ x] = make_uint4(p[0], p[1], p[2], p[3]);
+    row[1 ^ x] = make_uint4(p[4], p[5], p[6], p[7]);
 }
-__device__ __forceinline__ void stage_row16(uint8_t* dst, const float (&v)[16], float*) {
+__device__ __forceinline__ void stage_row16(uint8_t* box, int r, const float (&v)[16], float*) {
+    float4* row = reinterpret_cast<float4*>(box + r * 64);
+    const int x = (r >> 1) & 3;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-        reinterpret_cast<float4*>(dst)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    for (int i = 0; i < 4; ++i) row[i ^ x] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
 }
 
 __device__ __forceinline__ void store_row(float* dst, const float (&v)[16]) {
@@ -327,7 +334,7 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, PW, sizeof(OutT)>::THREADS, CP
                     if (lane == 0) bulk_wait_read<Cfg::EPI_BUFS - 1>();
                     __syncwarp();
                 }
-                stage_row16(buf + lane * 16 * (int)sizeof(OutT), f, (OutT*)nullptr);
+                stage_row16(buf, lane, f, (OutT*)nullptr);
                 fence_proxy_async();  // generic smem writes -> TMA (async proxy) reads
                 __syncwarp();
                 if (lane == 0) {
