@@ -20,7 +20,10 @@
  *     atomics in the order-defined kernels.
  *   - HC_MATH_EXACT (default) reproduces the reference's fp32 results bit-for-bit
  *     (same accumulation order, separate mul/add rounding). HC_MATH_FAST routes the
- *     contraction to the tcgen05 tensor-core path (tolerance-level parity).
+ *     contraction to tcgen05 tensor cores as 3xTF32 (operands split hi + lo in shared
+ *     memory; <= 1e-5 normwise vs double) when the matrices are TMA-eligible (inner
+ *     dimensions % 4 == 0, 16-byte aligned), else to FFMA tiles (same bar).
+ *     HC_MATH_TF32 is the single-pass tf32 product (~1e-3 normwise).
  */
 #ifndef HASHCONV_B200_H
 #define HASHCONV_B200_H
@@ -45,7 +48,7 @@ typedef enum {
     HC_ERR_CUDA = 3,             /* CUDA error (no reference counterpart) */
 } hc_status;
 
-typedef enum { HC_MATH_EXACT = 0, HC_MATH_FAST = 1 } hc_math;
+typedef enum { HC_MATH_EXACT = 0, HC_MATH_FAST = 1, HC_MATH_TF32 = 2 } hc_math;
 typedef enum { HC_DTYPE_F32 = 0, HC_DTYPE_BF16 = 1 } hc_dtype;
 
 /* Thread-local text of the last error (exact reference message for 1/2). */

@@ -22,7 +22,7 @@ if not os.path.exists(LIB_PATH):
 lib = C.CDLL(LIB_PATH)
 
 HC_OK, HC_ERR_INVALID_ARGUMENT, HC_ERR_RUNTIME, HC_ERR_CUDA = 0, 1, 2, 3
-HC_MATH_EXACT, HC_MATH_FAST = 0, 1
+HC_MATH_EXACT, HC_MATH_FAST, HC_MATH_TF32 = 0, 1, 2
 HC_DTYPE_F32, HC_DTYPE_BF16 = 0, 1
 
 

@@ -45,6 +45,7 @@
 #include "hc_internal.h"
 #include "hc_launch.cuh"
 #include "tc_common.cuh"
+#include "tma_host.h"
 
 namespace hcb {
 namespace {
@@ -84,22 +85,7 @@ int num_sms() {
 }
 
 // ---------------------------------------------------------------------- TMA descriptors
-using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiled encoder() {
-    static EncodeTiled fn = nullptr;
-    if (!fn) {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q{};
-        cuda_check(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q),
-                   "cudaGetDriverEntryPoint(cuTensorMapEncodeTiled)");
-        if (!p || q != cudaDriverEntryPointSuccess) throw cuda_error("cuTensorMapEncodeTiled unavailable");
-        fn = reinterpret_cast<EncodeTiled>(p);
-    }
-    return fn;
-}
+EncodeTiled encoder() { return tma_encoder(); }
 
 // 2-D bf16 tensor [rows][inner] (row pitch `pitch` bytes), box = box_rows x 64 elements
 // (one 128-byte swizzle span), SWIZZLE_128B, out-of-bounds elements read as zero.

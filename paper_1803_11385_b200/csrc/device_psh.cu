@@ -241,7 +241,7 @@ hc_status hc_stream_synchronize(hc_stream stream) {
     return guard([&] { cuda_check(cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream)), "sync"); });
 }
 hc_status hc_set_math(hc_math mode) {
-    if (mode != HC_MATH_EXACT && mode != HC_MATH_FAST) {
+    if (mode != HC_MATH_EXACT && mode != HC_MATH_FAST && mode != HC_MATH_TF32) {
         set_last_error("unknown math mode");
         return HC_ERR_INVALID_ARGUMENT;
     }

@@ -772,18 +772,29 @@ void launch_unpool(bool avg, const float* cd, const int* sw, const hc_psh* fine,
 void fast_gemm_nn(const float* a, const float* b, float* c, long long ra, long long k, long long cb, cudaStream_t s);
 void fast_gemm_tn(const float* a, const float* b, float* c, long long ra, long long k, long long cb, cudaStream_t s);
 void fast_gemm_nt(const float* a, const float* b, float* c, long long ra, long long k, long long rb, cudaStream_t s);
+bool tc_gemm_nn(const float* a, const float* b, float* c, long long ra, long long k, long long cb, bool three,
+                cudaStream_t s);
+bool tc_gemm_tn(const float* a, const float* b, float* c, long long ra, long long k, long long cb, bool three,
+                cudaStream_t s);
+bool tc_gemm_nt(const float* a, const float* b, float* c, long long ra, long long k, long long rb, bool three,
+                cudaStream_t s);
 
+// HC_MATH_FAST: 3xTF32 tcgen05 (gemm_tc.cu) where the shapes are TMA-eligible, else FFMA
+// tiles (gemm_fast.cu); HC_MATH_TF32: single-pass tf32 (same eligibility, FFMA otherwise).
 void gemm_nn(const float* a, const float* b, float* c, long long ra, long long k, long long cb, cudaStream_t s) {
-    if (current_math() == HC_MATH_FAST) fast_gemm_nn(a, b, c, ra, k, cb, s);
-    else gemm_nn_exact(a, b, c, ra, k, cb, s);
+    const hc_math m = current_math();
+    if (m == HC_MATH_EXACT) return gemm_nn_exact(a, b, c, ra, k, cb, s);
+    if (!tc_gemm_nn(a, b, c, ra, k, cb, m == HC_MATH_FAST, s)) fast_gemm_nn(a, b, c, ra, k, cb, s);
 }
 void gemm_tn(const float* a, const float* b, float* c, long long ra, long long k, long long cb, cudaStream_t s) {
-    if (current_math() == HC_MATH_FAST) fast_gemm_tn(a, b, c, ra, k, cb, s);
-    else gemm_tn_exact(a, b, c, ra, k, cb, s);
+    const hc_math m = current_math();
+    if (m == HC_MATH_EXACT) return gemm_tn_exact(a, b, c, ra, k, cb, s);
+    if (!tc_gemm_tn(a, b, c, ra, k, cb, m == HC_MATH_FAST, s)) fast_gemm_tn(a, b, c, ra, k, cb, s);
 }
 void gemm_nt(const float* a, const float* b, float* c, long long ra, long long k, long long rb, cudaStream_t s) {
-    if (current_math() == HC_MATH_FAST) fast_gemm_nt(a, b, c, ra, k, rb, s);
-    else gemm_nt_exact(a, b, c, ra, k, rb, s);
+    const hc_math m = current_math();
+    if (m == HC_MATH_EXACT) return gemm_nt_exact(a, b, c, ra, k, rb, s);
+    if (!tc_gemm_nt(a, b, c, ra, k, rb, m == HC_MATH_FAST, s)) fast_gemm_nt(a, b, c, ra, k, rb, s);
 }
 
 }  // namespace hcb

@@ -115,9 +115,13 @@ def _empty(rows, cols, dtype=torch.float32):
 
 @contextlib.contextmanager
 def math_mode(mode: str):
-    """'exact' (bit-identical to src/gemm.cpp order) or 'fast' (FFMA tiles / tensor cores)."""
+    """'exact' (bit-identical to src/gemm.cpp order), 'fast' (3xTF32 tensor cores, FFMA tiles
+    for shapes TMA cannot stage; <= 1e-5 normwise) or 'tf32' (single-pass tf32, ~1e-3)."""
+    modes = {"exact": _lib.HC_MATH_EXACT, "fast": _lib.HC_MATH_FAST, "tf32": _lib.HC_MATH_TF32}
+    if mode not in modes:
+        raise ValueError(f"unknown math mode {mode!r}")
     prev = lib.hc_get_math()
-    check(lib.hc_set_math(_lib.HC_MATH_FAST if mode == "fast" else _lib.HC_MATH_EXACT))
+    check(lib.hc_set_math(modes[mode]))
     try:
         yield
     finally:
