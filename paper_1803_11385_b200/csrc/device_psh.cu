@@ -2,6 +2,8 @@
 // derived probe tables, column table, batched locate, plus ABI plumbing.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <atomic>
 #include <cstring>
@@ -34,6 +36,20 @@ void* dev_alloc(size_t bytes) {
 }
 
 hc_math current_math() { return g_math; }
+void scratch_pool_init() {
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    if (done_dev == dev) return;
+    const char* e = std::getenv("HCB_POOL_KEEP_GB");
+    const double gb = e ? std::atof(e) : 48.0;
+    cudaMemPool_t pool;
+    cuda_check(cudaDeviceGetDefaultMemPool(&pool, dev), "cudaDeviceGetDefaultMemPool");
+    uint64_t keep = static_cast<uint64_t>(gb * (1ull << 30));
+    cuda_check(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep), "pool release threshold");
+    done_dev = dev;
+}
+
 
 namespace {
 std::atomic<long long> g_launches{0};

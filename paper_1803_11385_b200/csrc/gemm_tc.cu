@@ -13,11 +13,15 @@
 //   nt  C[ra][cb] = A[ra][K] * B[cb][K]^T   MMA-A <- B (K-major)   MMA-B <- A (K-major)
 //   tn  C[ra][cb] = A[K][ra]^T * B[K][cb]   MMA-A <- B (MN-major)  MMA-B <- A (MN-major)
 //
-// Precision. HC_MATH_FAST runs 3xTF32: each staged fp32 tile is split in shared memory
-// into hi = x with the low 13 mantissa bits cleared (exact in tf32) and lo = x - hi (exact
-// in fp32, |lo| < 2^-10 |x|), and D += lo_a*hi_b + hi_a*lo_b + hi_a*hi_b, which keeps the
-// fp32 bar of the FFMA path (<= 1e-5 normwise vs double; the dropped lo*lo term is
-// ~2^-20 relative). HC_MATH_TF32 is the single-pass product (~1e-3).
+// Precision. HC_MATH_FAST runs 3xTF32: with hi = x with the low 13 mantissa bits cleared
+// (exact in tf32) and lo = x - hi (exact in fp32, |lo| < 2^-10 |x|), D += lo_a*hi_b +
+// hi_a*lo_b + hi_a*hi_b keeps the fp32 bar of the FFMA path (<= 1e-5 normwise vs double;
+// the dropped lo*lo term is ~2^-20 relative). The B200 tensor core reads an fp32 operand
+// as tf32 by TRUNCATION (measured: products of raw and of explicitly truncated operands are
+// bit-identical, pinned by tests/test_gemm_tc.py), so the raw TMA tile already is hi and
+// only lo is written (a second shared-memory tile); -DHCB_TF32_EXPLICIT_HI writes hi too.
+// HC_MATH_TF32 is the single-pass product (~1e-3). (Rejected: splitting small operands
+// once in HBM and loading their lo planes by TMA — slower for matmul_trans_a at C >= 64.)
 //
 // Warp roles (192 threads): warp 0 TMA, warp 1 MMA issue (elect.sync), warps 2-5 split
 // the tiles (3xTF32) and drain TMEM in the epilogue. The long-K product (dW, K = voxels)
@@ -290,7 +294,9 @@ __global__ void __launch_bounds__(kThreads, GCfg<BN, SPLIT>::CTAS) k_gemm_tf32(c
                         split_tf32((uint32_t)v.y, h.y, l.y);
                         split_tf32((uint32_t)v.z, h.z, l.z);
                         split_tf32((uint32_t)v.w, h.w, l.w);
+#ifdef HCB_TF32_EXPLICIT_HI
                         st_shared_v4(raw + 16 * e, h);
+#endif
                         st_shared_v4(raw + Cfg::RAW + 16 * e, l);
                     }
                     fence_proxy_async();

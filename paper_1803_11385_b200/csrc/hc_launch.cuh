@@ -27,11 +27,17 @@ inline unsigned grid_for(long long n, int threads) {
     return static_cast<unsigned>((n + threads - 1) / threads);
 }
 
+// The default stream-ordered pool releases freed memory to the OS at every synchronisation
+// (release threshold 0), so a multi-GB scratch (a materialised column matrix, lo planes)
+// would be re-mapped on every call. Keep up to HCB_POOL_KEEP_GB (default 48) GB cached.
+void scratch_pool_init();
+
 // Stream-ordered scratch buffer (cudaMallocAsync / cudaFreeAsync).
 struct Scratch {
     void* p = nullptr;
     cudaStream_t s = nullptr;
     Scratch(size_t bytes, cudaStream_t st) : s(st) {
+        scratch_pool_init();
         cuda_check(cudaMallocAsync(&p, bytes ? bytes : 16, st), "cudaMallocAsync");
     }
     ~Scratch() {

@@ -78,3 +78,15 @@ def test_tf32_mode_is_tensor_core(cuda):
     assert not np.array_equal(_run(ops.matmul, a, b, "tf32"), _run(ops.matmul, a, b, "fast"))
     a, b = _rand(rng, 64, 255), _rand(rng, 255, 1023)
     assert np.array_equal(_run(ops.matmul, a, b, "tf32"), _run(ops.matmul, a, b, "fast"))
+
+
+def test_tensor_core_truncates_tf32_operands(cuda):
+    """gemm_tc.cu's 3xTF32 split uses the raw fp32 tile as its hi part, which is valid only
+    because the tensor core truncates fp32 operands to tf32 (low 13 bits ignored): pin that."""
+    rng = np.random.default_rng(5)
+    a, b = _rand(rng, 64, 256), _rand(rng, 256, 1024)
+
+    def trunc(x):
+        return (x.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+
+    assert np.array_equal(_run(ops.matmul, a, b, "tf32"), _run(ops.matmul, trunc(a), trunc(b), "tf32"))
