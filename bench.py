@@ -106,15 +106,53 @@ def peaks():
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed region.
+
+    NVML (nvidia_ml_py) is polled every ~2 ms from a thread, so even a ~20 ms timed region
+    gets several samples; `region(True/False)` brackets the timed region and summary()
+    reports the samples taken inside it (all samples if none landed there). Falls back to
+    `nvidia-smi -lms 50` when NVML is unavailable."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
-        self.index, self.proc, self.lines = index, None, []
+        self.index, self.proc, self.samples, self.in_region = index, None, [], False
+        self.stop = threading.Event()
+        self.nvml = None
+
+    def region(self, on: bool):
+        self.in_region = on
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.nvml = pynvml
+
+            def poll():
+                while not self.stop.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((self.in_region, float(sm), float(mx),
+                                             {n for n, bit in bits.items() if r & bit}))
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -127,9 +165,20 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm, mx = float(parts[0]), float(parts[1])
+            except ValueError:
+                continue
+            self.samples.append((self.in_region, sm, mx,
+                                 {n for n, v in zip(self.NAMES, parts[2:6]) if v.lower() == "active"}))
 
     def __exit__(self, *a):
+        self.stop.set()
+        if self.nvml is not None:
+            self.t.join(timeout=1)
         if self.proc:
             self.proc.terminate()
             try:
@@ -138,24 +187,14 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[2:6]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        if not sm:
+        inside = [x for x in self.samples if x[0]]
+        use = inside or self.samples
+        if not use:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        reasons = set().union(*(x[3] for x in use))
+        return {"sm_mhz": statistics.median(x[1] for x in use), "sm_max_mhz": max(x[2] for x in use),
+                "reasons": sorted(reasons), "samples": len(use), "samples_in_timed_region": len(inside),
+                "source": "nvml" if self.nvml is not None else "nvidia-smi"}
 
 
 # ------------------------------------------------------------------ CPU reference
@@ -266,9 +305,13 @@ class MaterializedStep:
         """Algorithmic bytes / flops per op."""
         s, N, ci, co = 4, self.N, self.cin, self.cout
         gather = 28 * ci * N * s + 10 * M + 3 * R + 16 * N
-        fl = 2.0 * co * 27 * ci * N
-        return {"hash2col": ("hbm", gather), "fwd_gemm": ("flop", fl), "dW_gemm": ("flop", fl),
-                "dcols_gemm": ("flop", fl), "col2hash": ("hbm", gather)}
+        # the fp32 contractions over the materialised column matrix (27*ci x N) are bound by
+        # moving that matrix (AI = 2*co/(4*(1 + co/(27 ci))) ~ 30 flop/B at 64->64, far below
+        # the tensor ridge): algorithmic bytes = column matrix + the C x N operand
+        colm = 27 * ci * N * s
+        return {"hash2col": ("hbm", gather), "fwd_gemm": ("hbm", colm + co * N * s),
+                "dW_gemm": ("hbm", colm + co * N * s), "dcols_gemm": ("hbm", colm + co * N * s),
+                "col2hash": ("hbm", gather)}
 
 
 class FusedStep:
@@ -383,11 +426,13 @@ def main():
         barrier()
         launches0 = _lib.lib.hc_launch_count()
         barrier()
+        clk.region(True)
         start.record()
         for k in range(args.steps):
             one(marks_all[k])
         end.record()
         barrier()
+        clk.region(False)
         launches = _lib.lib.hc_launch_count() - launches0
     elapsed_ms = start.elapsed_time(end)
     for m in marks_all:
@@ -444,7 +489,7 @@ def main():
         comp.wait_stream(d2h_s)
         barrier()
         es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ke = max(5, args.steps)  # long enough that pipeline fill / drain amortise
+        ke = max(20, args.steps)  # long enough that pipeline fill / drain amortise
         es.record(comp)
         for k in range(ke):
             e2e_step(k)
@@ -654,11 +699,13 @@ def net_main(args, rank, world, local):
             dist.barrier()
         torch.cuda.synchronize()
         launches0 = _lib.lib.hc_launch_count()
+        clk.region(True)
         st.record()
         for _ in range(args.steps):
             one()
         en.record()
         torch.cuda.synchronize()
+        clk.region(False)
         launches = _lib.lib.hc_launch_count() - launches0
         if mode == "cuda-graph":  # graph replays bypass the host launch counter
             launches = one.launches_per_step * args.steps
@@ -720,11 +767,13 @@ def seg_main(args, rank, world, local):
             seg.step(x, labels, allreduce_gradients, world)
         torch.cuda.synchronize()
         launches0 = _lib.lib.hc_launch_count()
+        clk.region(True)
         st.record()
         for _ in range(args.steps):
             seg.step(x, labels, allreduce_gradients, world)
         en.record()
         torch.cuda.synchronize()
+        clk.region(False)
         launches = _lib.lib.hc_launch_count() - launches0
     t = torch.tensor([st.elapsed_time(en) / args.steps], device=dev)
     if world > 1:

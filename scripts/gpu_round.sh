@@ -17,6 +17,9 @@ for res in (64, 128, 256, 512):
     s=VoxelSet.sphere(res, True); t=time.time(); g=PshLevel.build_device(s,1); print(res, s.n, 'gpu psh build %.3f s'%(time.time()-t), g.hash_dim, g.offset_dim)
 " > gpurun_out/psh_build.txt 2>&1; cat gpurun_out/psh_build.txt
 for c in 16 64 128; do timeout 300 python scripts/kbench_net.py $c; done > gpurun_out/kbench_net.txt 2>&1
+for c in 16 64 128; do timeout 300 python scripts/kbench_gemm.py $c; done > gpurun_out/kbench_gemm.txt 2>&1
+HCB_TC_GEMM=0 HCB_GEMM_MODES=fast timeout 300 python scripts/kbench_gemm.py 64 >> gpurun_out/kbench_gemm.txt 2>&1; cat gpurun_out/kbench_gemm.txt
+timeout 600 python bench.py --path materialized --steps 5 > gpurun_out/bench_materialized.json 2>gpurun_out/bench_materialized.err; echo "materialized rc=$?"
 for c in 16 64 256; do timeout 300 python scripts/kbench_ref.py $c > gpurun_out/kbench_ref_c$c.txt 2>&1; grep "C=" gpurun_out/kbench_ref_c$c.txt; done
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > /dev/null 2>&1; echo "ncu list rc=$?"

@@ -9,3 +9,5 @@ cp gpurun_out/kbench.txt profiles/${R}_kbench_native.txt
 cp gpurun_out/kbench_net.txt profiles/${R}_kbench_net.txt
 cp gpurun_out/psh_build.txt profiles/${R}_psh_build.txt
 cat gpurun_out/kbench_ref_c*.txt | grep "C=" > profiles/${R}_kbench_ref.txt
+cp gpurun_out/kbench_gemm.txt profiles/${R}_kbench_gemm.txt
+cp gpurun_out/bench_materialized.json profiles/${R}_bench_materialized.json
