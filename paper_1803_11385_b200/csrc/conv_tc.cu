@@ -147,16 +147,6 @@ __device__ __forceinline__ void store_row(float* dst, const float (&v)[16]) {
 #pragma unroll
     for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
 }
-__device__ __forceinline__ void store_row(bf16* dst, const float (&v)[16]) {
-    uint32_t p[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
-        p[i] = *reinterpret_cast<uint32_t*>(&h);
-    }
-    *reinterpret_cast<uint4*>(dst) = make_uint4(p[0], p[1], p[2], p[3]);
-    *reinterpret_cast<uint4*>(dst + 8) = make_uint4(p[4], p[5], p[6], p[7]);
-}
 
 // ====================================================================== forward gather-GEMM
 // Y[m][0:BN] = sum_k A[m][k] * Wp[0:BN][k],  A[m][k] = X[nbr(m, k / C)][k % C] (0 if -1)

@@ -63,6 +63,9 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 // completes (or the hint expires) instead of re-issuing try_wait every few cycles.
 // Used by warps that wait long (producers on a full ring, epilogue on a whole tile) so
 // they do not steal issue slots from the warps doing work.
+#ifndef HCB_SLEEP_NS
+#define HCB_SLEEP_NS 20000  // suspend-time hint (ns): bounds a missed wake-up; A/B 1 ms vs 20 us vs 2 us: equal
+#endif
 __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n"
@@ -73,7 +76,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
         "bra HC_WAITS;\n"
         "HC_DONES:\n"
         "}\n" ::"r"(bar),
-        "r"(parity), "r"(1000000u)
+        "r"(parity), "r"((uint32_t)HCB_SLEEP_NS)
         : "memory");
 }
 
