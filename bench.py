@@ -56,6 +56,9 @@ def parse():
                         "classification train step (BASELINE configs 2/3)")
     p.add_argument("--classes", type=int, default=40)
     p.add_argument("--no-graph", action="store_true", help="net workload: time the eager step")
+    p.add_argument("--sync-bn", action="store_true",
+                   help="net workload, N>1: batch-norm statistics over the global batch (3 small all-reduces per "
+                        "BN layer); default: per-rank statistics")
     return p.parse_args()
 
 
@@ -665,14 +668,16 @@ def net_main(args, rank, world, local):
         _init_dist(dev)
     from paper_1803_11385_b200 import _lib
     from paper_1803_11385_b200 import net as nnet
-    from paper_1803_11385_b200.dist import allreduce_gradients
+    from paper_1803_11385_b200.dist import allreduce_gradients, sum_over_ranks
     from paper_1803_11385_b200.psh import SuperPsh
     pyr = shell_pyramid(args.res)
     b = args.shapes_per_gpu
     lmax = int(round(np.log2(args.res)))
     levels = [SuperPsh.from_levels([lv] * b) for lv in pyr]
     feats = np.concatenate([pyr[0].arrays()[3]] * b, axis=1)
-    net = nnet.NativeHashNet(lmax, args.classes, seed=rank)
+    # every rank starts from the same weights (data parallelism)
+    net = nnet.NativeHashNet(lmax, args.classes, seed=0,
+                             sync_bn=sum_over_ranks if (args.sync_bn and world > 1) else None)
     x = net.input_features(torch.from_numpy(np.ascontiguousarray(feats)).to(dev))
     labels = torch.randint(0, args.classes, (b,), device=dev)
     voxels = sum(s.total_columns() for s in levels)
@@ -727,7 +732,8 @@ def net_main(args, rank, world, local):
             "config": {"workload": f"hcnn classification net {args.res}^3, {lmax - 1} conv/pool levels, "
                                    f"{b} shells/GPU", "res": args.res, "global_batch": b * world,
                        "classes": args.classes, "voxels_per_gpu_all_levels": voxels,
-                       "parallelism": f"dp{world}", "launch": mode},
+                       "parallelism": f"dp{world}", "launch": mode,
+                       "batch_norm": "global-batch (sync)" if net.sync_bn is not None else "per-rank"},
             "voxels_per_s": voxels * world / (ms / 1e3), "cpu_baseline": cpu, "gpu_launches": int(launches),
             "clocks": clk.summary()}))
     if world > 1:

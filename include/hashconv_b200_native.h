@@ -86,6 +86,27 @@ hc_status hc_native_bn_relu_forward(const float* x, int64_t n, int32_t c, int32_
 hc_status hc_native_bn_relu_backward(const void* d_relu, hc_dtype dtype, const float* xhat,
                                      const float* inv_std, int64_t n, int32_t c, void* d_conv_bf16,
                                      void* workspace, size_t ws_bytes, hc_stream stream);
+/* Synchronised batch norm for data parallelism (the reference normalises over
+ * the whole batch, cnn_ops.cpp:456-470), in phases so the caller can sum the per-channel
+ * statistics over ranks (e.g. ncclAllReduce, double) between them:
+ *   forward:  bn_stat(0, x) -> sum -> bn_finalize(sum_x, NULL) [mean]
+ *             bn_stat(1, x, mean) -> sum -> bn_finalize(sum_x, sum_sq) [running stats, inv_std]
+ *             bn_relu_apply
+ *   backward: bn_stat(2, xhat, d_relu) -> sum both rows -> bn_relu_backward_apply(n_total)
+ * sums: double [2][c] (mode 0/1 use row 0). With one rank (n_total = n) the phases give the
+ * fused calls' results bit for bit. */
+hc_status hc_native_bn_stat(int32_t mode, const float* x, const void* d, hc_dtype dtype, int64_t n,
+                            int32_t c, const double* mean, double* sums, void* workspace,
+                            size_t ws_bytes, hc_stream stream);
+hc_status hc_native_bn_finalize(const double* sum_x, const double* sum_sq, int64_t n_total, int32_t c,
+                                float momentum, float eps, float* running_mean, float* running_var,
+                                double* mean, float* inv_std, hc_stream stream);
+hc_status hc_native_bn_relu_apply(const float* x, int64_t n, int32_t c, const double* mean,
+                                  const float* inv_std, float* xhat, void* out_bf16, hc_stream stream);
+hc_status hc_native_bn_relu_backward_apply(const void* d_relu, hc_dtype dtype, const float* xhat,
+                                           const float* inv_std, int64_t n, int32_t c, const double* s1,
+                                           const double* s2, int64_t n_total, void* d_conv_bf16,
+                                           hc_stream stream);
 /* Final dense pool: cmap [b][8 cells][8 children] resolution-4 columns (or -1); head
  * [(c*8 + cell)][b] fp32 = max over present children, src = winning column or -1. */
 hc_status hc_native_dense_pool(const int32_t* cmap, int32_t b, const void* x_bf16, int32_t c,

@@ -272,6 +272,27 @@ __global__ void k_col_fold(const double* __restrict__ part, int blocks, long lon
     }
 }
 
+// Synchronised (data-parallel) batch norm: statistics from sums taken over the GLOBAL batch
+// (all-reduced by the caller). sum_sq == nullptr: mean = sum_x / n_total; otherwise
+// var = sum_sq / n_total (biased, cnn_ops.cpp:463-466), running stats, inv_std — the same
+// arithmetic as k_col_fold MODE 0 / 1, so one rank reproduces the fused call bit for bit.
+__global__ void k_bn_finalize(const double* __restrict__ sum_x, const double* __restrict__ sum_sq, long long n_total,
+                              int C, float* __restrict__ run_mean, float* __restrict__ run_var, float momentum,
+                              float eps, double* __restrict__ mean, float* __restrict__ inv_std) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= C) return;
+    if (!sum_sq) {
+        mean[c] = sum_x[c] / (double)n_total;
+        return;
+    }
+    const double var = sum_sq[c] / (double)n_total;
+    if (run_mean) {
+        run_mean[c] = (1.0f - momentum) * run_mean[c] + momentum * (float)mean[c];
+        run_var[c] = (1.0f - momentum) * run_var[c] + momentum * (float)var;
+    }
+    inv_std[c] = (float)(1.0 / sqrt(var + (double)eps));
+}
+
 // xhat = (x - mean) * inv_std (float, cnn_ops.cpp:472); out = relu(xhat) (bf16 for the
 // next layer); xhat kept (fp32) for the backward pass.
 __global__ void __launch_bounds__(kT) k_bn_relu_apply(const float* __restrict__ x, long long n, int C,
@@ -300,7 +321,8 @@ template <typename DT>
 __global__ void __launch_bounds__(kT) k_bn_relu_bwd_apply(const DT* __restrict__ dy, const float* __restrict__ xhat,
                                                          long long n, int C, const double* __restrict__ s1,
                                                          const double* __restrict__ s2,
-                                                         const float* __restrict__ inv_std, bf16* __restrict__ dx) {
+                                                         const float* __restrict__ inv_std, bf16* __restrict__ dx,
+                                                         long long n_total) {
     const int chunks = C >> 3;
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= n * chunks) return;
@@ -309,7 +331,7 @@ __global__ void __launch_bounds__(kT) k_bn_relu_bwd_apply(const DT* __restrict__
     float d[8], h[8], o[8];
     load8(dy + row * C + c0, d);
     load8(xhat + row * C + c0, h);
-    const double inv_n = 1.0 / (double)n;
+    const double inv_n = 1.0 / (double)n_total;  // the (global) batch the sums were taken over
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
         const double g = h[e] > 0.0f ? (double)d[e] : 0.0;
@@ -498,15 +520,86 @@ hc_status hc_native_bn_relu_backward(const void* d_relu, hc_dtype dtype, const f
             k_col_partials<2, bf16><<<blocks, kT, 0, s>>>(xhat, d, n, c, nullptr, part);
             k_col_fold<2><<<c, kT, 0, s>>>(part, blocks, n, c, s1, s2, nullptr, nullptr, 0, 0, nullptr, nullptr);
             k_bn_relu_bwd_apply<bf16><<<grid_for(m, kT), kT, 0, s>>>(d, xhat, n, c, s1, s2, inv_std,
-                                                                     static_cast<bf16*>(d_conv_bf16));
+                                                                     static_cast<bf16*>(d_conv_bf16), n);
         } else {
             const float* d = static_cast<const float*>(d_relu);
             k_col_partials<2, float><<<blocks, kT, 0, s>>>(xhat, d, n, c, nullptr, part);
             k_col_fold<2><<<c, kT, 0, s>>>(part, blocks, n, c, s1, s2, nullptr, nullptr, 0, 0, nullptr, nullptr);
             k_bn_relu_bwd_apply<float><<<grid_for(m, kT), kT, 0, s>>>(d, xhat, n, c, s1, s2, inv_std,
-                                                                      static_cast<bf16*>(d_conv_bf16));
+                                                                      static_cast<bf16*>(d_conv_bf16), n);
         }
         launched("batch-norm + relu backward", 3);
+    });
+}
+
+hc_status hc_native_bn_stat(int32_t mode, const float* x, const void* d, hc_dtype dtype, int64_t n, int32_t c,
+                            const double* mean, double* sums, void* workspace, size_t ws_bytes, hc_stream stream) {
+    return guard([&] {
+        check_c8(c);
+        if (c > kT) throw std::invalid_argument("native batch norm: at most 256 channels");
+        if (mode < 0 || mode > 2) throw std::invalid_argument("native batch norm: bad statistics mode");
+        if (mode == 1 && !mean) throw std::invalid_argument("native batch norm: mode 1 needs the mean");
+        if (mode == 2 && !d) throw std::invalid_argument("native batch norm: mode 2 needs the gradient");
+        cudaStream_t s = as_stream(stream);
+        if (n <= 0) {  // an empty shard contributes zeros to the global sums
+            cuda_check(cudaMemsetAsync(sums, 0, sizeof(double) * 2 * c, s), "memset");
+            return;
+        }
+        if (ws_bytes < hc_native_bn_workspace(n, c)) throw std::invalid_argument("native batch norm: workspace too small");
+        const int blocks = (int)((n + kRowsPerBlock - 1) / kRowsPerBlock);
+        double* part = static_cast<double*>(workspace);
+        if (mode == 0) k_col_partials<0, float><<<blocks, kT, 0, s>>>(x, nullptr, n, c, nullptr, part);
+        else if (mode == 1) k_col_partials<1, float><<<blocks, kT, 0, s>>>(x, nullptr, n, c, mean, part);
+        else if (dtype == HC_DTYPE_BF16)
+            k_col_partials<2, bf16><<<blocks, kT, 0, s>>>(x, static_cast<const bf16*>(d), n, c, nullptr, part);
+        else k_col_partials<2, float><<<blocks, kT, 0, s>>>(x, static_cast<const float*>(d), n, c, nullptr, part);
+        k_col_fold<2><<<c, kT, 0, s>>>(part, blocks, n, c, sums, sums + c, nullptr, nullptr, 0, 0, nullptr, nullptr);
+        launched("batch-norm partial sums", 2);
+    });
+}
+
+hc_status hc_native_bn_finalize(const double* sum_x, const double* sum_sq, int64_t n_total, int32_t c, float momentum,
+                                float eps, float* running_mean, float* running_var, double* mean, float* inv_std,
+                                hc_stream stream) {
+    return guard([&] {
+        if (n_total <= 0) throw std::invalid_argument("batch_norm: empty input");
+        if (c <= 0 || c > kT) throw std::invalid_argument("native batch norm: 1..256 channels");
+        k_bn_finalize<<<1, kT, 0, as_stream(stream)>>>(sum_x, sum_sq, n_total, c, running_mean, running_var, momentum,
+                                                      eps, mean, inv_std);
+        launched("batch-norm finalize");
+    });
+}
+
+hc_status hc_native_bn_relu_apply(const float* x, int64_t n, int32_t c, const double* mean, const float* inv_std,
+                                  float* xhat, void* out_bf16, hc_stream stream) {
+    return guard([&] {
+        check_c8(c);
+        if (n <= 0) return;
+        const long long m = n * (c / 8);
+        k_bn_relu_apply<<<grid_for(m, kT), kT, 0, as_stream(stream)>>>(x, n, c, mean, inv_std, xhat,
+                                                                       static_cast<bf16*>(out_bf16));
+        launched("batch-norm + relu");
+    });
+}
+
+hc_status hc_native_bn_relu_backward_apply(const void* d_relu, hc_dtype dtype, const float* xhat, const float* inv_std,
+                                           int64_t n, int32_t c, const double* s1, const double* s2, int64_t n_total,
+                                           void* d_conv_bf16, hc_stream stream) {
+    return guard([&] {
+        check_c8(c);
+        if (n <= 0) return;
+        if (n_total <= 0) throw std::invalid_argument("batch_norm: empty input");
+        cudaStream_t s = as_stream(stream);
+        const long long m = n * (c / 8);
+        if (dtype == HC_DTYPE_BF16)
+            k_bn_relu_bwd_apply<bf16><<<grid_for(m, kT), kT, 0, s>>>(static_cast<const bf16*>(d_relu), xhat, n, c, s1,
+                                                                     s2, inv_std, static_cast<bf16*>(d_conv_bf16),
+                                                                     n_total);
+        else
+            k_bn_relu_bwd_apply<float><<<grid_for(m, kT), kT, 0, s>>>(static_cast<const float*>(d_relu), xhat, n, c,
+                                                                      s1, s2, inv_std, static_cast<bf16*>(d_conv_bf16),
+                                                                      n_total);
+        launched("batch-norm + relu backward");
     });
 }
 

@@ -56,3 +56,11 @@ def max_over_ranks(value: float, device=None, group=None) -> float:
     t = torch.tensor([value], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+def sum_over_ranks(t: torch.Tensor, group=None) -> None:
+    """In-place sum over the data-parallel ranks (the NativeHashNet sync_bn hook: batch-norm
+    statistics over the global batch). No-op without an initialised multi-rank group."""
+    if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)

@@ -119,7 +119,11 @@ class NativeHashNet:
 
     def __init__(self, level_max: int, num_classes: int, seed: int = 0, input_channels: int = 3,
                  dropout: float = 0.5, lr: float = 0.1, momentum: float = 0.9, weight_decay: float = 5e-4,
-                 bn_momentum: float = 0.1, bn_eps: float = 1e-5):
+                 bn_momentum: float = 0.1, bn_eps: float = 1e-5, sync_bn=None):
+        """sync_bn: data parallelism with whole-batch statistics — a callable
+        that sums a float64 CUDA tensor in place over the ranks (e.g. dist.sum_over_ranks);
+        batch norm then normalises over the global batch, as the reference does for one
+        process (cnn_ops.cpp:456-470). None: statistics over this process's batch."""
         if level_max < 2 or level_max > 16:
             raise ValueError("level_max out of range")
         if num_classes < 2:
@@ -127,6 +131,7 @@ class NativeHashNet:
         self.level_max, self.num_classes, self.input_channels = level_max, num_classes, input_channels
         self.dropout, self.lr, self.momentum, self.wd = dropout, lr, momentum, weight_decay
         self.bn_momentum, self.bn_eps = bn_momentum, bn_eps
+        self.sync_bn, self._ntot = sync_bn, {}
         g = torch.Generator(device="cuda").manual_seed(seed)
         self.blocks = []
         for lvl in range(level_max, 1, -1):
@@ -175,6 +180,55 @@ class NativeHashNet:
             self._ws["bn"] = t
         return t
 
+    def _n_total(self, i: int, n: int) -> int:
+        """Global row count of block i's batch norm (cached per local size, so CUDA-graph
+        capture after the warm-up steps does not synchronise)."""
+        if self.sync_bn is None:
+            return n
+        key = (i, n)
+        if key not in self._ntot:
+            t = torch.tensor([float(n)], dtype=torch.float64, device="cuda")
+            self.sync_bn(t)
+            self._ntot[key] = int(round(float(t.item())))
+        return self._ntot[key]
+
+    def _bn_relu_forward(self, i: int, y: torch.Tensor, xhat: torch.Tensor, r: torch.Tensor) -> None:
+        blk = self.blocks[i]
+        n, c = y.shape
+        ws = self._bn_ws(n, c)
+        if self.sync_bn is None:
+            check(lib.hc_native_bn_relu_forward(_p(y), n, c, 1, self.bn_momentum, self.bn_eps, _p(blk["run_mean"]),
+                                                _p(blk["run_var"]), _p(blk["inv_std"]), _p(xhat), _p(r), _p(ws),
+                                                ws.numel(), _s()))
+            return
+        nt = self._n_total(i, n)
+        sx = torch.empty((2, c), dtype=torch.float64, device="cuda")
+        sq = torch.empty((2, c), dtype=torch.float64, device="cuda")
+        mean = torch.empty(c, dtype=torch.float64, device="cuda")
+        check(lib.hc_native_bn_stat(0, _p(y), None, 0, n, c, None, _p(sx), _p(ws), ws.numel(), _s()))
+        self.sync_bn(sx)
+        check(lib.hc_native_bn_finalize(_p(sx), None, nt, c, 0.0, 0.0, None, None, _p(mean), None, _s()))
+        check(lib.hc_native_bn_stat(1, _p(y), None, 0, n, c, _p(mean), _p(sq), _p(ws), ws.numel(), _s()))
+        self.sync_bn(sq)
+        check(lib.hc_native_bn_finalize(_p(sx), _p(sq), nt, c, self.bn_momentum, self.bn_eps, _p(blk["run_mean"]),
+                                        _p(blk["run_var"]), _p(mean), _p(blk["inv_std"]), _s()))
+        check(lib.hc_native_bn_relu_apply(_p(y), n, c, _p(mean), _p(blk["inv_std"]), _p(xhat), _p(r), _s()))
+
+    def _bn_relu_backward(self, i: int, d_relu: torch.Tensor, d_dtype: int, xhat: torch.Tensor,
+                          d_conv: torch.Tensor) -> None:
+        blk = self.blocks[i]
+        n, c = xhat.shape
+        ws = self._bn_ws(n, c)
+        if self.sync_bn is None:
+            check(lib.hc_native_bn_relu_backward(_p(d_relu), d_dtype, _p(xhat), _p(blk["inv_std"]), n, c,
+                                                 _p(d_conv), _p(ws), ws.numel(), _s()))
+            return
+        st = torch.empty((2, c), dtype=torch.float64, device="cuda")
+        check(lib.hc_native_bn_stat(2, _p(xhat), _p(d_relu), d_dtype, n, c, None, _p(st), _p(ws), ws.numel(), _s()))
+        self.sync_bn(st)
+        check(lib.hc_native_bn_relu_backward_apply(_p(d_relu), d_dtype, _p(xhat), _p(blk["inv_std"]), n, c,
+                                                   _p(st[0]), _p(st[1]), self._n_total(i, n), _p(d_conv), _s()))
+
     def input_features(self, ref: torch.Tensor) -> torch.Tensor:
         """Finest-level data (C x N fp32, psh data array) -> padded voxel-major bf16."""
         c, n = ref.shape
@@ -195,10 +249,7 @@ class NativeHashNet:
             y = nconv.gather_gemm(nb.conv_maps[i], x, wf, blk["cout_p"], torch.float32)
             xhat = torch.empty_like(y)
             r = torch.empty((n, blk["cout_p"]), dtype=BF16, device="cuda")
-            ws = self._bn_ws(n, blk["cout_p"])
-            check(lib.hc_native_bn_relu_forward(_p(y), n, blk["cout_p"], 1, self.bn_momentum, self.bn_eps,
-                                                _p(blk["run_mean"]), _p(blk["run_var"]), _p(blk["inv_std"]),
-                                                _p(xhat), _p(r), _p(ws), ws.numel(), _s()))
+            self._bn_relu_forward(i, y, xhat, r)
             acts.append(dict(x=x, xhat=xhat))
             if i + 1 < len(self.blocks):
                 pm = nb.pool_maps[i]
@@ -264,9 +315,7 @@ class NativeHashNet:
                 check(lib.hc_native_dense_pool_backward(_p(d_head), _p(a["src"]), nb.batch, c, n, _p(d_relu), _s()))
                 d_dtype = _lib.HC_DTYPE_F32
             d_conv = torch.empty((n, c), dtype=BF16, device="cuda")
-            ws = self._bn_ws(n, c)
-            check(lib.hc_native_bn_relu_backward(_p(d_relu), d_dtype, _p(a["xhat"]), _p(blk["inv_std"]), n, c,
-                                                 _p(d_conv), _p(ws), ws.numel(), _s()))
+            self._bn_relu_backward(i, d_relu, d_dtype, a["xhat"], d_conv)
             conv_grads[i] = nconv.conv_dw(nb.conv_maps[i], a["x"], d_conv, self._dw_ws)
             # input gradient (net.cpp:316-317; the finest one is the net's input gradient, g.input).
             # The tensor-core tile set starts at 16 output channels: an 8-channel input level

@@ -10,7 +10,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1803_11385_b200.dist import allreduce_gradients, max_over_ranks, shard_range
+from paper_1803_11385_b200.dist import allreduce_gradients, max_over_ranks, shard_range, sum_over_ranks
 
 
 @pytest.mark.parametrize("n,world", [(8, 1), (8, 2), (64, 8), (7, 3), (3, 4), (0, 2)])
@@ -60,6 +60,10 @@ def _worker(rank, world, port, q):
         g = torch.from_numpy(dw_local.copy())
         allreduce_gradients([g])
         t = max_over_ranks(float(rank))
+        # the sync-BN hook: per-channel double sums of this rank's rows (channel-major x) ->
+        # global sums, equal to the sums over the whole batch
+        bn = torch.from_numpy(x_all[:, lo:hi].astype(np.float64).sum(1))
+        sum_over_ranks(bn)
         if rank == 0:
             cols_all = R.hash2col(full, x_all, full, spec)
             dw_full = R.matmul_trans_b(dy_all, cols_all)
@@ -67,7 +71,8 @@ def _worker(rank, world, port, q):
             # the forward is shard-local: rank 0's output columns equal the full batch's
             y_local = R.matmul(w, cols)
             y_full = R.matmul(w, cols_all)
-            q.put((err, bool(np.array_equal(y_local, y_full[:, lo:hi])), t, len(mine)))
+            bn_err = float(np.abs(bn.numpy() - x_all.astype(np.float64).sum(1)).max())
+            q.put((err, bool(np.array_equal(y_local, y_full[:, lo:hi])), t, len(mine), bn_err))
     finally:
         dist.destroy_process_group()
 
@@ -79,10 +84,11 @@ def test_two_rank_gradient_allreduce_matches_full_batch():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    err, y_equal, tmax, nmine = q.get(timeout=120)
+    err, y_equal, tmax, nmine, bn_err = q.get(timeout=120)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     assert err < 1e-6, err
     assert y_equal
     assert tmax == 1.0 and nmine == 3
+    assert bn_err < 1e-9, bn_err
