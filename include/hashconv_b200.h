@@ -229,6 +229,53 @@ hc_status hc_matmul_trans_a_f32(const float* a, const float* b, float* c, int64_
 hc_status hc_matmul_trans_b_f32(const float* a, const float* b, float* c, int64_t ra, int64_t k,
                                 int64_t rb, hc_stream stream);
 
+
+/* fp64: the reference's double instantiation (cnn_ops.cpp:652-653, gemm.cpp:117-118) —
+ * the same operators with double data; always order-exact (bit-identical to the
+ * reference's double results; the math mode applies to fp32 only). Generic kernels:
+ * a parity / gradient-check path, not tuned for throughput. */
+hc_status hc_hash2col_f64(const hc_psh* in, const double* data, int64_t data_rows,
+                          int64_t data_cols, const hc_psh* out, hc_conv_spec spec, double* cols,
+                          hc_stream stream);
+hc_status hc_col2hash_f64(const double* col_grads, int64_t rows, int64_t cols, const hc_psh* in,
+                          const hc_psh* out, hc_conv_spec spec, double* result, hc_stream stream);
+hc_status hc_conv_forward_f64(const hc_psh* in, const double* data, int64_t data_rows,
+                              int64_t data_cols, const hc_psh* out, const double* w, int64_t w_rows,
+                              int64_t w_cols, hc_conv_spec spec, double* result, hc_stream stream);
+hc_status hc_conv_backward_f64(const double* output_grad, int64_t g_rows, int64_t g_cols,
+                               const double* w, int64_t w_rows, int64_t w_cols,
+                               const double* cached_cols, int64_t c_rows, int64_t c_cols,
+                               const hc_psh* in, const hc_psh* out, hc_conv_spec spec, double* dw,
+                               double* dx, hc_stream stream);
+hc_status hc_max_pool_f64(const hc_psh* in, const double* data, int64_t data_rows,
+                          int64_t data_cols, const hc_psh* out, hc_conv_spec spec, double* result,
+                          int32_t* switches, hc_stream stream);
+hc_status hc_avg_pool_f64(const hc_psh* in, const double* data, int64_t data_rows,
+                          int64_t data_cols, const hc_psh* out, hc_conv_spec spec, double* result,
+                          hc_stream stream);
+hc_status hc_max_unpool_f64(const double* coarse_data, int64_t c_rows, int64_t c_cols,
+                            const int32_t* switches, int64_t s_rows, int64_t s_cols,
+                            const hc_psh* fine, const hc_psh* coarse, hc_conv_spec spec,
+                            double* result, hc_stream stream);
+hc_status hc_avg_unpool_f64(const double* coarse_data, int64_t c_rows, int64_t c_cols,
+                            const hc_psh* fine, const hc_psh* coarse, hc_conv_spec spec,
+                            double* result, hc_stream stream);
+hc_status hc_deconv_forward_f64(const hc_psh* coarse, const double* coarse_data, int64_t d_rows,
+                                int64_t d_cols, const hc_psh* fine, const double* w,
+                                int64_t w_rows, int64_t w_cols, hc_conv_spec spec, double* result,
+                                hc_stream stream);
+hc_status hc_deconv_backward_f64(const double* fine_grad, int64_t g_rows, int64_t g_cols,
+                                 const double* w, int64_t w_rows, int64_t w_cols,
+                                 const double* cached_coarse, int64_t c_rows, int64_t c_cols,
+                                 const hc_psh* coarse, const hc_psh* fine, hc_conv_spec spec,
+                                 double* dw, double* dx, hc_stream stream);
+hc_status hc_matmul_f64(const double* a, const double* b, double* c, int64_t ra, int64_t k,
+                        int64_t cb, hc_stream stream);
+hc_status hc_matmul_trans_a_f64(const double* a, const double* b, double* c, int64_t ra, int64_t k,
+                                int64_t cb, hc_stream stream);
+hc_status hc_matmul_trans_b_f64(const double* a, const double* b, double* c, int64_t ra, int64_t k,
+                                int64_t rb, hc_stream stream);
+
 #ifdef __cplusplus
 }
 #endif

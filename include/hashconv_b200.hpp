@@ -13,7 +13,7 @@
 // Requirements on the types (exactly the reference's members):
 //   Super: dim, resolution, batch, hash, offsets, tags, model_of_slot, hash_acc,
 //          offset_acc, data_acc, hash_dims, offset_dims (std::vector-like .data()/.size())
-//   Mat:   rows, cols, values (contiguous float), constructor Mat(rows, cols)
+//   Mat:   rows, cols, values (contiguous float or double), constructor Mat(rows, cols)
 //   Spec:  kernel, stride, pad, in_channels, out_channels
 //   W:     member `w` of type Mat
 // Every call uploads its inputs, runs the kernels and downloads the result (the
@@ -25,6 +25,8 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "hashconv_b200.h"
@@ -39,6 +41,10 @@ inline void check(hc_status s) {
     if (s == HC_ERR_INVALID_ARGUMENT) throw std::invalid_argument(msg);
     throw std::runtime_error(msg);
 }
+
+// element type of a Mat (its `values` container)
+template <class Mat>
+using value_t = typename std::decay<decltype(std::declval<Mat>().values[0])>::type;
 
 // RAII device buffer
 class Buf {
@@ -74,7 +80,8 @@ inline Buf upload(const Mat& m) {
 template <class Mat>
 inline Mat download(const Buf& b, std::int64_t rows, std::int64_t cols) {
     Mat m(rows, cols);
-    check(hc_memcpy_d2h(m.values.data(), b.as<void>(), sizeof(float) * static_cast<size_t>(rows * cols), nullptr));
+    check(hc_memcpy_d2h(m.values.data(), b.as<void>(), sizeof(value_t<Mat>) * static_cast<size_t>(rows * cols),
+                        nullptr));
     check(hc_stream_synchronize(nullptr));
     return m;
 }
@@ -120,6 +127,43 @@ class Structure {
     hc_psh* p_ = nullptr;
 };
 
+// The reference instantiates every operator for float and double (cnn_ops.cpp:652-653,
+// gemm.cpp:117-118); the C ABI has one entry point per precision.
+template <class T>
+struct abi;
+template <>
+struct abi<float> {
+    static constexpr auto hash2col = hc_hash2col_f32;
+    static constexpr auto col2hash = hc_col2hash_f32;
+    static constexpr auto conv_forward = hc_conv_forward_f32;
+    static constexpr auto conv_backward = hc_conv_backward_f32;
+    static constexpr auto max_pool = hc_max_pool_f32;
+    static constexpr auto avg_pool = hc_avg_pool_f32;
+    static constexpr auto max_unpool = hc_max_unpool_f32;
+    static constexpr auto avg_unpool = hc_avg_unpool_f32;
+    static constexpr auto deconv_forward = hc_deconv_forward_f32;
+    static constexpr auto deconv_backward = hc_deconv_backward_f32;
+    static constexpr auto matmul = hc_matmul_f32;
+    static constexpr auto matmul_trans_a = hc_matmul_trans_a_f32;
+    static constexpr auto matmul_trans_b = hc_matmul_trans_b_f32;
+};
+template <>
+struct abi<double> {
+    static constexpr auto hash2col = hc_hash2col_f64;
+    static constexpr auto col2hash = hc_col2hash_f64;
+    static constexpr auto conv_forward = hc_conv_forward_f64;
+    static constexpr auto conv_backward = hc_conv_backward_f64;
+    static constexpr auto max_pool = hc_max_pool_f64;
+    static constexpr auto avg_pool = hc_avg_pool_f64;
+    static constexpr auto max_unpool = hc_max_unpool_f64;
+    static constexpr auto avg_unpool = hc_avg_unpool_f64;
+    static constexpr auto deconv_forward = hc_deconv_forward_f64;
+    static constexpr auto deconv_backward = hc_deconv_backward_f64;
+    static constexpr auto matmul = hc_matmul_f64;
+    static constexpr auto matmul_trans_a = hc_matmul_trans_a_f64;
+    static constexpr auto matmul_trans_b = hc_matmul_trans_b_f64;
+};
+
 template <class Spec>
 inline hc_conv_spec spec_of(const Spec& s) {
     return hc_conv_spec{s.kernel, s.stride, s.pad, s.in_channels, s.out_channels};
@@ -160,38 +204,41 @@ inline void set_fast_math(bool fast) { detail::check(hc_set_math(fast ? HC_MATH_
 // cnn_ops.cpp:123-158
 template <class Super, class Mat, class Spec>
 Mat hash2col(const Super& input, const Mat& input_data, const Super& output, const Spec& spec) {
+    using T = detail::value_t<Mat>;
     detail::Structure in(input), out(output);
     const hc_conv_spec sp = detail::spec_of(spec);
     const std::int64_t rows = sp.in_channels * detail::field_size(sp, in.dim()), cols = out.columns();
     auto d = detail::upload(input_data);
-    detail::Buf r(sizeof(float) * static_cast<size_t>(rows * cols));
-    detail::check(hc_hash2col_f32(in.get(), d.template as<float>(), input_data.rows, input_data.cols, out.get(), sp,
-                                  r.as<float>(), nullptr));
+    detail::Buf r(sizeof(T) * static_cast<size_t>(rows * cols));
+    detail::check(detail::abi<T>::hash2col(in.get(), d.template as<T>(), input_data.rows, input_data.cols, out.get(), sp,
+                                  r.as<T>(), nullptr));
     return detail::download<Mat>(r, rows, cols);
 }
 
 // cnn_ops.cpp:160-204
 template <class Super, class Mat, class Spec>
 Mat col2hash(const Mat& col_grads, const Super& input, const Super& output, const Spec& spec) {
+    using T = detail::value_t<Mat>;
     detail::Structure in(input), out(output);
     const hc_conv_spec sp = detail::spec_of(spec);
     auto g = detail::upload(col_grads);
-    detail::Buf r(sizeof(float) * static_cast<size_t>(sp.in_channels * in.columns()));
-    detail::check(hc_col2hash_f32(g.template as<float>(), col_grads.rows, col_grads.cols, in.get(), out.get(), sp,
-                                  r.as<float>(), nullptr));
+    detail::Buf r(sizeof(T) * static_cast<size_t>(sp.in_channels * in.columns()));
+    detail::check(detail::abi<T>::col2hash(g.template as<T>(), col_grads.rows, col_grads.cols, in.get(), out.get(), sp,
+                                  r.as<T>(), nullptr));
     return detail::download<Mat>(r, sp.in_channels, in.columns());
 }
 
 // cnn_ops.cpp:206-215
 template <class Super, class Mat, class W, class Spec>
 Mat conv_forward(const Super& input, const Mat& input_data, const Super& output, const W& weights, const Spec& spec) {
+    using T = detail::value_t<Mat>;
     detail::Structure in(input), out(output);
     const hc_conv_spec sp = detail::spec_of(spec);
     auto d = detail::upload(input_data);
     auto w = detail::upload(weights.w);
-    detail::Buf r(sizeof(float) * static_cast<size_t>(sp.out_channels * out.columns()));
-    detail::check(hc_conv_forward_f32(in.get(), d.template as<float>(), input_data.rows, input_data.cols, out.get(),
-                                      w.template as<float>(), weights.w.rows, weights.w.cols, sp, r.as<float>(),
+    detail::Buf r(sizeof(T) * static_cast<size_t>(sp.out_channels * out.columns()));
+    detail::check(detail::abi<T>::conv_forward(in.get(), d.template as<T>(), input_data.rows, input_data.cols, out.get(),
+                                      w.template as<T>(), weights.w.rows, weights.w.cols, sp, r.as<T>(),
                                       nullptr));
     return detail::download<Mat>(r, sp.out_channels, out.columns());
 }
@@ -200,17 +247,18 @@ Mat conv_forward(const Super& input, const Mat& input_data, const Super& output,
 template <class Mat, class W, class Super, class Spec>
 ConvGradients<Mat> conv_backward(const Mat& output_grad, const W& weights, const Mat& cached_cols, const Super& input,
                                  const Super& output, const Spec& spec) {
+    using T = detail::value_t<Mat>;
     detail::Structure in(input), out(output);
     const hc_conv_spec sp = detail::spec_of(spec);
     auto g = detail::upload(output_grad);
     auto w = detail::upload(weights.w);
     auto c = detail::upload(cached_cols);
-    detail::Buf dw(sizeof(float) * static_cast<size_t>(output_grad.rows * cached_cols.rows));
-    detail::Buf dx(sizeof(float) * static_cast<size_t>(sp.in_channels * in.columns()));
-    detail::check(hc_conv_backward_f32(g.template as<float>(), output_grad.rows, output_grad.cols,
-                                       w.template as<float>(), weights.w.rows, weights.w.cols, c.template as<float>(),
-                                       cached_cols.rows, cached_cols.cols, in.get(), out.get(), sp, dw.as<float>(),
-                                       dx.as<float>(), nullptr));
+    detail::Buf dw(sizeof(T) * static_cast<size_t>(output_grad.rows * cached_cols.rows));
+    detail::Buf dx(sizeof(T) * static_cast<size_t>(sp.in_channels * in.columns()));
+    detail::check(detail::abi<T>::conv_backward(g.template as<T>(), output_grad.rows, output_grad.cols,
+                                       w.template as<T>(), weights.w.rows, weights.w.cols, c.template as<T>(),
+                                       cached_cols.rows, cached_cols.cols, in.get(), out.get(), sp, dw.as<T>(),
+                                       dx.as<T>(), nullptr));
     return ConvGradients<Mat>{detail::download<Mat>(dw, output_grad.rows, cached_cols.rows),
                               detail::download<Mat>(dx, sp.in_channels, in.columns())};
 }
@@ -218,14 +266,15 @@ ConvGradients<Mat> conv_backward(const Mat& output_grad, const W& weights, const
 // cnn_ops.cpp:234-284
 template <class Super, class Mat, class Spec>
 MaxPoolResult<Mat> max_pool(const Super& input, const Mat& input_data, const Super& output, const Spec& spec) {
+    using T = detail::value_t<Mat>;
     detail::Structure in(input), out(output);
     const hc_conv_spec sp = detail::spec_of(spec);
     const std::int64_t n = out.columns();
     auto d = detail::upload(input_data);
-    detail::Buf r(sizeof(float) * static_cast<size_t>(sp.in_channels * n));
+    detail::Buf r(sizeof(T) * static_cast<size_t>(sp.in_channels * n));
     detail::Buf s(sizeof(std::int32_t) * static_cast<size_t>(sp.in_channels * n));
-    detail::check(hc_max_pool_f32(in.get(), d.template as<float>(), input_data.rows, input_data.cols, out.get(), sp,
-                                  r.as<float>(), s.as<std::int32_t>(), nullptr));
+    detail::check(detail::abi<T>::max_pool(in.get(), d.template as<T>(), input_data.rows, input_data.cols, out.get(), sp,
+                                  r.as<T>(), s.as<std::int32_t>(), nullptr));
     MaxPoolResult<Mat> res;
     res.switches.rows = sp.in_channels;
     res.switches.cols = n;
@@ -238,12 +287,13 @@ MaxPoolResult<Mat> max_pool(const Super& input, const Mat& input_data, const Sup
 // cnn_ops.cpp:286-322
 template <class Super, class Mat, class Spec>
 Mat avg_pool(const Super& input, const Mat& input_data, const Super& output, const Spec& spec) {
+    using T = detail::value_t<Mat>;
     detail::Structure in(input), out(output);
     const hc_conv_spec sp = detail::spec_of(spec);
     auto d = detail::upload(input_data);
-    detail::Buf r(sizeof(float) * static_cast<size_t>(sp.in_channels * out.columns()));
-    detail::check(hc_avg_pool_f32(in.get(), d.template as<float>(), input_data.rows, input_data.cols, out.get(), sp,
-                                  r.as<float>(), nullptr));
+    detail::Buf r(sizeof(T) * static_cast<size_t>(sp.in_channels * out.columns()));
+    detail::check(detail::abi<T>::avg_pool(in.get(), d.template as<T>(), input_data.rows, input_data.cols, out.get(), sp,
+                                  r.as<T>(), nullptr));
     return detail::download<Mat>(r, sp.in_channels, out.columns());
 }
 
@@ -251,26 +301,28 @@ Mat avg_pool(const Super& input, const Mat& input_data, const Super& output, con
 template <class Mat, class Switches, class Super, class Spec>
 Mat max_unpool(const Mat& coarse_data, const Switches& switches, const Super& fine, const Super& coarse,
                const Spec& spec) {
+    using T = detail::value_t<Mat>;
     detail::Structure f(fine), c(coarse);
     const hc_conv_spec sp = detail::spec_of(spec);
     auto d = detail::upload(coarse_data);
     auto s = detail::upload(switches.values.data(), switches.values.size());
-    detail::Buf r(sizeof(float) * static_cast<size_t>(sp.in_channels * f.columns()));
-    detail::check(hc_max_unpool_f32(d.template as<float>(), coarse_data.rows, coarse_data.cols,
+    detail::Buf r(sizeof(T) * static_cast<size_t>(sp.in_channels * f.columns()));
+    detail::check(detail::abi<T>::max_unpool(d.template as<T>(), coarse_data.rows, coarse_data.cols,
                                     s.template as<std::int32_t>(), switches.rows, switches.cols, f.get(), c.get(), sp,
-                                    r.as<float>(), nullptr));
+                                    r.as<T>(), nullptr));
     return detail::download<Mat>(r, sp.in_channels, f.columns());
 }
 
 // cnn_ops.cpp:374-406
 template <class Mat, class Super, class Spec>
 Mat avg_unpool(const Mat& coarse_data, const Super& fine, const Super& coarse, const Spec& spec) {
+    using T = detail::value_t<Mat>;
     detail::Structure f(fine), c(coarse);
     const hc_conv_spec sp = detail::spec_of(spec);
     auto d = detail::upload(coarse_data);
-    detail::Buf r(sizeof(float) * static_cast<size_t>(sp.in_channels * f.columns()));
-    detail::check(hc_avg_unpool_f32(d.template as<float>(), coarse_data.rows, coarse_data.cols, f.get(), c.get(), sp,
-                                    r.as<float>(), nullptr));
+    detail::Buf r(sizeof(T) * static_cast<size_t>(sp.in_channels * f.columns()));
+    detail::check(detail::abi<T>::avg_unpool(d.template as<T>(), coarse_data.rows, coarse_data.cols, f.get(), c.get(), sp,
+                                    r.as<T>(), nullptr));
     return detail::download<Mat>(r, sp.in_channels, f.columns());
 }
 
@@ -278,13 +330,14 @@ Mat avg_unpool(const Mat& coarse_data, const Super& fine, const Super& coarse, c
 template <class Super, class Mat, class W, class Spec>
 Mat deconv_forward(const Super& coarse, const Mat& coarse_data, const Super& fine, const W& weights,
                    const Spec& spec) {
+    using T = detail::value_t<Mat>;
     detail::Structure c(coarse), f(fine);
     const hc_conv_spec sp = detail::spec_of(spec);
     auto d = detail::upload(coarse_data);
     auto w = detail::upload(weights.w);
-    detail::Buf r(sizeof(float) * static_cast<size_t>(sp.in_channels * f.columns()));
-    detail::check(hc_deconv_forward_f32(c.get(), d.template as<float>(), coarse_data.rows, coarse_data.cols, f.get(),
-                                        w.template as<float>(), weights.w.rows, weights.w.cols, sp, r.as<float>(),
+    detail::Buf r(sizeof(T) * static_cast<size_t>(sp.in_channels * f.columns()));
+    detail::check(detail::abi<T>::deconv_forward(c.get(), d.template as<T>(), coarse_data.rows, coarse_data.cols, f.get(),
+                                        w.template as<T>(), weights.w.rows, weights.w.cols, sp, r.as<T>(),
                                         nullptr));
     return detail::download<Mat>(r, sp.in_channels, f.columns());
 }
@@ -293,18 +346,19 @@ Mat deconv_forward(const Super& coarse, const Mat& coarse_data, const Super& fin
 template <class Mat, class W, class Super, class Spec>
 ConvGradients<Mat> deconv_backward(const Mat& fine_grad, const W& weights, const Mat& cached_coarse_data,
                                    const Super& coarse, const Super& fine, const Spec& spec) {
+    using T = detail::value_t<Mat>;
     detail::Structure c(coarse), f(fine);
     const hc_conv_spec sp = detail::spec_of(spec);
     auto g = detail::upload(fine_grad);
     auto w = detail::upload(weights.w);
     auto cd = detail::upload(cached_coarse_data);
     const std::int64_t k = sp.in_channels * detail::field_size(sp, f.dim());
-    detail::Buf dw(sizeof(float) * static_cast<size_t>(cached_coarse_data.rows * k));
-    detail::Buf dx(sizeof(float) * static_cast<size_t>(weights.w.rows * c.columns()));
-    detail::check(hc_deconv_backward_f32(g.template as<float>(), fine_grad.rows, fine_grad.cols,
-                                         w.template as<float>(), weights.w.rows, weights.w.cols,
-                                         cd.template as<float>(), cached_coarse_data.rows, cached_coarse_data.cols,
-                                         c.get(), f.get(), sp, dw.as<float>(), dx.as<float>(), nullptr));
+    detail::Buf dw(sizeof(T) * static_cast<size_t>(cached_coarse_data.rows * k));
+    detail::Buf dx(sizeof(T) * static_cast<size_t>(weights.w.rows * c.columns()));
+    detail::check(detail::abi<T>::deconv_backward(g.template as<T>(), fine_grad.rows, fine_grad.cols,
+                                         w.template as<T>(), weights.w.rows, weights.w.cols,
+                                         cd.template as<T>(), cached_coarse_data.rows, cached_coarse_data.cols,
+                                         c.get(), f.get(), sp, dw.as<T>(), dx.as<T>(), nullptr));
     return ConvGradients<Mat>{detail::download<Mat>(dw, cached_coarse_data.rows, k),
                               detail::download<Mat>(dx, weights.w.rows, c.columns())};
 }
@@ -312,30 +366,33 @@ ConvGradients<Mat> deconv_backward(const Mat& fine_grad, const W& weights, const
 // gemm.cpp:71-93
 template <class Mat>
 Mat matmul(const Mat& a, const Mat& b) {
+    using T = detail::value_t<Mat>;
     if (a.cols != b.rows) throw std::invalid_argument("matmul: shape mismatch");
     auto da = detail::upload(a), db = detail::upload(b);
-    detail::Buf c(sizeof(float) * static_cast<size_t>(a.rows * b.cols));
-    detail::check(hc_matmul_f32(da.template as<float>(), db.template as<float>(), c.as<float>(), a.rows, a.cols,
+    detail::Buf c(sizeof(T) * static_cast<size_t>(a.rows * b.cols));
+    detail::check(detail::abi<T>::matmul(da.template as<T>(), db.template as<T>(), c.as<T>(), a.rows, a.cols,
                                 b.cols, nullptr));
     return detail::download<Mat>(c, a.rows, b.cols);
 }
 
 template <class Mat>
 Mat matmul_trans_a(const Mat& a, const Mat& b) {
+    using T = detail::value_t<Mat>;
     if (a.rows != b.rows) throw std::invalid_argument("matmul_trans_a: shape mismatch");
     auto da = detail::upload(a), db = detail::upload(b);
-    detail::Buf c(sizeof(float) * static_cast<size_t>(a.cols * b.cols));
-    detail::check(hc_matmul_trans_a_f32(da.template as<float>(), db.template as<float>(), c.as<float>(), a.rows,
+    detail::Buf c(sizeof(T) * static_cast<size_t>(a.cols * b.cols));
+    detail::check(detail::abi<T>::matmul_trans_a(da.template as<T>(), db.template as<T>(), c.as<T>(), a.rows,
                                         a.cols, b.cols, nullptr));
     return detail::download<Mat>(c, a.cols, b.cols);
 }
 
 template <class Mat>
 Mat matmul_trans_b(const Mat& a, const Mat& b) {
+    using T = detail::value_t<Mat>;
     if (a.cols != b.cols) throw std::invalid_argument("matmul_trans_b: shape mismatch");
     auto da = detail::upload(a), db = detail::upload(b);
-    detail::Buf c(sizeof(float) * static_cast<size_t>(a.rows * b.rows));
-    detail::check(hc_matmul_trans_b_f32(da.template as<float>(), db.template as<float>(), c.as<float>(), a.rows,
+    detail::Buf c(sizeof(T) * static_cast<size_t>(a.rows * b.rows));
+    detail::check(detail::abi<T>::matmul_trans_b(da.template as<T>(), db.template as<T>(), c.as<T>(), a.rows,
                                         a.cols, b.rows, nullptr));
     return detail::download<Mat>(c, a.rows, b.rows);
 }

@@ -91,6 +91,19 @@ _SIGS = {
     "hc_matmul_f32": [_P, _P, _P, _I64, _I64, _I64, _P],
     "hc_matmul_trans_a_f32": [_P, _P, _P, _I64, _I64, _I64, _P],
     "hc_matmul_trans_b_f32": [_P, _P, _P, _I64, _I64, _I64, _P],
+    "hc_hash2col_f64": [_P, _P, _I64, _I64, _P, _SPEC, _P, _P],
+    "hc_col2hash_f64": [_P, _I64, _I64, _P, _P, _SPEC, _P, _P],
+    "hc_conv_forward_f64": [_P, _P, _I64, _I64, _P, _P, _I64, _I64, _SPEC, _P, _P],
+    "hc_conv_backward_f64": [_P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64, _P, _P, _SPEC, _P, _P, _P],
+    "hc_max_pool_f64": [_P, _P, _I64, _I64, _P, _SPEC, _P, _P, _P],
+    "hc_avg_pool_f64": [_P, _P, _I64, _I64, _P, _SPEC, _P, _P],
+    "hc_max_unpool_f64": [_P, _I64, _I64, _P, _I64, _I64, _P, _P, _SPEC, _P, _P],
+    "hc_avg_unpool_f64": [_P, _I64, _I64, _P, _P, _SPEC, _P, _P],
+    "hc_deconv_forward_f64": [_P, _P, _I64, _I64, _P, _P, _I64, _I64, _SPEC, _P, _P],
+    "hc_deconv_backward_f64": [_P, _I64, _I64, _P, _I64, _I64, _P, _I64, _I64, _P, _P, _SPEC, _P, _P, _P],
+    "hc_matmul_f64": [_P, _P, _P, _I64, _I64, _I64, _P],
+    "hc_matmul_trans_a_f64": [_P, _P, _P, _I64, _I64, _I64, _P],
+    "hc_matmul_trans_b_f64": [_P, _P, _P, _I64, _I64, _I64, _P],
 }
 _SIGS.update({
     "hc_native_pack_weights": [_P, _I32, _I32, _I32, _I32, _P, _P],

@@ -51,9 +51,22 @@ struct Scratch {
     }
 };
 
-// Exact fp32 GEMMs (gemm_exact.cu) — reference accumulation order.
+// Exact GEMMs (gemm_exact.cu) — reference accumulation order, fp32 and fp64.
 void gemm_nn_exact(const float* a, const float* b, float* c, long long ra, long long k, long long cb, cudaStream_t s);
 void gemm_tn_exact(const float* a, const float* b, float* c, long long ra, long long k, long long cb, cudaStream_t s);
 void gemm_nt_exact(const float* a, const float* b, float* c, long long ra, long long k, long long rb, cudaStream_t s);
+void gemm_nn_exact(const double* a, const double* b, double* c, long long ra, long long k, long long cb,
+                   cudaStream_t s);
+void gemm_tn_exact(const double* a, const double* b, double* c, long long ra, long long k, long long cb,
+                   cudaStream_t s);
+void gemm_nt_exact(const double* a, const double* b, double* c, long long ra, long long k, long long rb,
+                   cudaStream_t s);
+
+// Separately rounded arithmetic (the reference is built without FMA contraction,
+// SURVEY.md §0.3), for both instantiations.
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 
 }  // namespace hcb

@@ -181,8 +181,9 @@ __global__ void __launch_bounds__(256, MINB)
     }
 }
 
-__global__ void k_hash2col_any(DevPsh in, DevPsh out, int F, int S, int pad, int fd, const float* __restrict__ data,
-                               int C, float* __restrict__ cols) {
+template <typename T>
+__global__ void k_hash2col_any(DevPsh in, DevPsh out, int F, int S, int pad, int fd, const T* __restrict__ data,
+                               int C, T* __restrict__ cols) {
     const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (col >= out.N) return;
     const int4 c = out.cols[col];
@@ -192,7 +193,7 @@ __global__ void k_hash2col_any(DevPsh in, DevPsh out, int F, int S, int pad, int
     for (int t = 0; t < fd; ++t) {
         const int g = probe_tap(in, mp, bx, by, bz, F, t);
         for (int ch = 0; ch < C; ++ch)
-            cols[((long long)ch * fd + t) * Nout + col] = g >= 0 ? __ldg(data + ch * Nin + g) : 0.0f;
+            cols[((long long)ch * fd + t) * Nout + col] = g >= 0 ? __ldg(data + ch * Nin + g) : T(0);
     }
 }
 
@@ -362,8 +363,9 @@ __global__ void k_col2hash(DevPsh in, DevPsh out, int Fr, int S, int pad, int fd
 }
 
 // any F / stride: recompute covering probes per channel (no register arrays)
-__global__ void k_col2hash_any(DevPsh in, DevPsh out, int F, int S, int pad, int fd, const float* __restrict__ g,
-                               int C, float* __restrict__ res) {
+template <typename T>
+__global__ void k_col2hash_any(DevPsh in, DevPsh out, int F, int S, int pad, int fd, const T* __restrict__ g,
+                               int C, T* __restrict__ res) {
     const long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (gi >= in.N) return;
     const int4 c = in.cols[gi];
@@ -375,7 +377,7 @@ __global__ void k_col2hash_any(DevPsh in, DevPsh out, int F, int S, int pad, int
     if (dim == 3) cover_axis(c.z, F, S, pad, out.resolution, loz, hiz);
     const long long Nout = out.N, Nin = in.N;
     for (int ch = 0; ch < C; ++ch) {
-        float acc = 0.0f;
+        T acc = T(0);
         for (int z = loz; z <= hiz; ++z)
             for (int y = loy; y <= hiy; ++y)
                 for (int x = lox; x <= hix; ++x) {
@@ -384,7 +386,7 @@ __global__ void k_col2hash_any(DevPsh in, DevPsh out, int F, int S, int pad, int
                     const int rx = c.x - origin_axis(x, F, S, pad), ry = c.y - origin_axis(y, F, S, pad);
                     const int rz = dim == 3 ? c.z - origin_axis(z, F, S, pad) : 0;
                     const int row = (rz * F + ry) * F + rx;
-                    acc = __fadd_rn(acc, g[((long long)ch * fd + row) * Nout + col]);
+                    acc = add_rn(acc, g[((long long)ch * fd + row) * Nout + col]);
                 }
         res[ch * Nin + gi] = acc;
     }
@@ -449,8 +451,9 @@ __global__ void __launch_bounds__(256) k_max_pool(DevPsh in, DevPsh out, int S, 
     }
 }
 
-__global__ void k_max_pool_any(DevPsh in, DevPsh out, int F, int S, int pad, int fd, const float* __restrict__ data,
-                               int C, float* __restrict__ res, int* __restrict__ sw) {
+template <typename T>
+__global__ void k_max_pool_any(DevPsh in, DevPsh out, int F, int S, int pad, int fd, const T* __restrict__ data,
+                               int C, T* __restrict__ res, int* __restrict__ sw) {
     const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (col >= out.N) return;
     const int4 c = out.cols[col];
@@ -458,18 +461,18 @@ __global__ void k_max_pool_any(DevPsh in, DevPsh out, int F, int S, int pad, int
     const int bx = origin_axis(c.x, F, S, pad), by = origin_axis(c.y, F, S, pad), bz = origin_axis(c.z, F, S, pad);
     const long long Nin = in.N, Nout = out.N;
     for (int ch = 0; ch < C; ++ch) {
-        float best = 0.0f;
+        T best = T(0);
         int arg = -1;
         for (int t = 0; t < fd; ++t) {
             const int g = probe_tap(in, mp, bx, by, bz, F, t);
             if (g < 0) continue;
-            const float v = data[ch * Nin + g];
+            const T v = data[ch * Nin + g];
             if (arg < 0 || v > best) {
                 best = v;
                 arg = t;
             }
         }
-        res[ch * Nout + col] = arg < 0 ? 0.0f : best;
+        res[ch * Nout + col] = arg < 0 ? T(0) : best;
         sw[ch * Nout + col] = arg;
     }
 }
@@ -520,8 +523,9 @@ __global__ void __launch_bounds__(256) k_avg_pool(DevPsh in, DevPsh out, int S, 
     }
 }
 
-__global__ void k_avg_pool_any(DevPsh in, DevPsh out, int F, int S, int pad, int fd, const float* __restrict__ data,
-                               int C, float inv, float* __restrict__ res) {
+template <typename T>
+__global__ void k_avg_pool_any(DevPsh in, DevPsh out, int F, int S, int pad, int fd, const T* __restrict__ data,
+                               int C, T inv, T* __restrict__ res) {
     const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (col >= out.N) return;
     const int4 c = out.cols[col];
@@ -529,12 +533,12 @@ __global__ void k_avg_pool_any(DevPsh in, DevPsh out, int F, int S, int pad, int
     const int bx = origin_axis(c.x, F, S, pad), by = origin_axis(c.y, F, S, pad), bz = origin_axis(c.z, F, S, pad);
     const long long Nin = in.N, Nout = out.N;
     for (int ch = 0; ch < C; ++ch) {
-        float acc = 0.0f;
+        T acc = T(0);
         for (int t = 0; t < fd; ++t) {
             const int g = probe_tap(in, mp, bx, by, bz, F, t);
-            if (g >= 0) acc = __fadd_rn(acc, data[ch * Nin + g]);
+            if (g >= 0) acc = add_rn(acc, data[ch * Nin + g]);
         }
-        res[ch * Nout + col] = __fmul_rn(acc, inv);
+        res[ch * Nout + col] = mul_rn(acc, inv);
     }
 }
 
@@ -588,9 +592,9 @@ __global__ void __launch_bounds__(256) k_unpool(DevPsh fine, DevPsh coarse, int 
     }
 }
 
-template <bool AVG>
-__global__ void k_unpool_any(DevPsh fine, DevPsh coarse, int F, int S, int pad, const float* __restrict__ cd,
-                             const int* __restrict__ sw, int C, float inv, float* __restrict__ res) {
+template <bool AVG, typename T>
+__global__ void k_unpool_any(DevPsh fine, DevPsh coarse, int F, int S, int pad, const T* __restrict__ cd,
+                             const int* __restrict__ sw, int C, T inv, T* __restrict__ res) {
     const long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (gi >= fine.N) return;
     const int4 c = fine.cols[gi];
@@ -602,7 +606,7 @@ __global__ void k_unpool_any(DevPsh fine, DevPsh coarse, int F, int S, int pad, 
     if (dim == 3) cover_axis(c.z, F, S, pad, coarse.resolution, loz, hiz);
     const long long Nc = coarse.N, Nf = fine.N;
     for (int ch = 0; ch < C; ++ch) {
-        float acc = 0.0f;
+        T acc = T(0);
         for (int z = loz; z <= hiz; ++z)
             for (int y = loy; y <= hiy; ++y)
                 for (int x = lox; x <= hix; ++x) {
@@ -610,11 +614,11 @@ __global__ void k_unpool_any(DevPsh fine, DevPsh coarse, int F, int S, int pad, 
                     if (col < 0) continue;
                     const long long k = ch * Nc + col;
                     if constexpr (AVG) {
-                        acc = __fadd_rn(acc, __fmul_rn(cd[k], inv));
+                        acc = add_rn(acc, mul_rn(cd[k], inv));
                     } else {
                         const int rx = c.x - origin_axis(x, F, S, pad), ry = c.y - origin_axis(y, F, S, pad);
                         const int rz = dim == 3 ? c.z - origin_axis(z, F, S, pad) : 0;
-                        if (sw[k] == (rz * F + ry) * F + rx) acc = __fadd_rn(acc, cd[k]);
+                        if (sw[k] == (rz * F + ry) * F + rx) acc = add_rn(acc, cd[k]);
                     }
                 }
         res[ch * Nf + gi] = acc;
@@ -679,7 +683,7 @@ void launch_hash2col(const hc_psh* in, const float* data, const hc_psh* out, con
     else if (sp.kernel == 2)
         k_hash2col<2, 4><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, cols);
     else
-        k_hash2col_any<<<g, kThreads, 0, s>>>(in->d, out->d, sp.kernel, sp.stride, sp.pad,
+        k_hash2col_any<float><<<g, kThreads, 0, s>>>(in->d, out->d, sp.kernel, sp.stride, sp.pad,
                                             (int)field_volume(sp, in->d.dim), data, sp.in_channels, cols);
     launched("hash2col");
 }
@@ -707,7 +711,7 @@ void launch_col2hash(const float* gcols, const hc_psh* in, const hc_psh* out, co
     else if (sp.stride > 1 && cover_per_axis(sp) == 2)
         k_col2hash<8, false, 1><<<g, kThreads, 0, s>>>(in->d, out->d, sp.kernel, sp.stride, sp.pad, fd, gcols, C, res);
     else
-        k_col2hash_any<<<g, kThreads, 0, s>>>(in->d, out->d, sp.kernel, sp.stride, sp.pad, fd, gcols, C, res);
+        k_col2hash_any<float><<<g, kThreads, 0, s>>>(in->d, out->d, sp.kernel, sp.stride, sp.pad, fd, gcols, C, res);
     launched("col2hash");
 }
 
@@ -721,7 +725,7 @@ void launch_max_pool(const hc_psh* in, const float* data, const hc_psh* out, con
     else if (sp.kernel == 3)
         k_max_pool<3, 1><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, res, sw);
     else
-        k_max_pool_any<<<g, kThreads, 0, s>>>(in->d, out->d, sp.kernel, sp.stride, sp.pad,
+        k_max_pool_any<float><<<g, kThreads, 0, s>>>(in->d, out->d, sp.kernel, sp.stride, sp.pad,
                                             (int)field_volume(sp, in->d.dim), data, sp.in_channels, res, sw);
     launched("max_pool");
 }
@@ -738,7 +742,7 @@ void launch_avg_pool(const hc_psh* in, const float* data, const hc_psh* out, con
     else if (sp.kernel == 3)
         k_avg_pool<3, 1><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, inv, res);
     else
-        k_avg_pool_any<<<g, kThreads, 0, s>>>(in->d, out->d, sp.kernel, sp.stride, sp.pad, (int)fd, data,
+        k_avg_pool_any<float><<<g, kThreads, 0, s>>>(in->d, out->d, sp.kernel, sp.stride, sp.pad, (int)fd, data,
                                             sp.in_channels, inv, res);
     launched("avg_pool");
 }
@@ -761,9 +765,9 @@ void launch_unpool(bool avg, const float* cd, const int* sw, const hc_psh* fine,
     else if (kmax <= 8) HC_UNPOOL(8);
     else if (kmax <= 27) HC_UNPOOL(27);
     else if (avg)
-        k_unpool_any<true><<<g, kThreads, 0, s>>>(fine->d, coarse->d, sp.kernel, sp.stride, sp.pad, cd, sw, C, inv, res);
+        k_unpool_any<true, float><<<g, kThreads, 0, s>>>(fine->d, coarse->d, sp.kernel, sp.stride, sp.pad, cd, sw, C, inv, res);
     else
-        k_unpool_any<false><<<g, kThreads, 0, s>>>(fine->d, coarse->d, sp.kernel, sp.stride, sp.pad, cd, sw, C, inv, res);
+        k_unpool_any<false, float><<<g, kThreads, 0, s>>>(fine->d, coarse->d, sp.kernel, sp.stride, sp.pad, cd, sw, C, inv, res);
 #undef HC_UNPOOL
     launched("unpool");
 }
@@ -797,11 +801,264 @@ void gemm_nt(const float* a, const float* b, float* c, long long ra, long long k
     if (!tc_gemm_nt(a, b, c, ra, k, rb, m == HC_MATH_FAST, s)) fast_gemm_nt(a, b, c, ra, k, rb, s);
 }
 
+// ------------------------------------------------------------------ fp64 (the reference's double
+// instantiation, cnn_ops.cpp:652-653): the generic kernels, same order and rounding rules.
+void launch_hash2col(const hc_psh* in, const double* data, const hc_psh* out, const hc_conv_spec& sp, double* cols,
+                     cudaStream_t s) {
+    const long long n = out->d.N;
+    if (n == 0 || sp.in_channels == 0) return;
+    k_hash2col_any<double><<<grid_for(n, kThreads), kThreads, 0, s>>>(
+        in->d, out->d, sp.kernel, sp.stride, sp.pad, (int)field_volume(sp, in->d.dim), data, sp.in_channels, cols);
+    launched("hash2col (f64)");
+}
+void launch_col2hash(const double* gcols, const hc_psh* in, const hc_psh* out, const hc_conv_spec& sp, double* res,
+                     cudaStream_t s) {
+    const long long n = in->d.N;
+    if (n == 0 || sp.in_channels == 0) return;
+    k_col2hash_any<double><<<grid_for(n, kThreads), kThreads, 0, s>>>(
+        in->d, out->d, sp.kernel, sp.stride, sp.pad, (int)field_volume(sp, in->d.dim), gcols, sp.in_channels, res);
+    launched("col2hash (f64)");
+}
+void launch_max_pool(const hc_psh* in, const double* data, const hc_psh* out, const hc_conv_spec& sp, double* res,
+                     int* sw, cudaStream_t s) {
+    const long long n = out->d.N;
+    if (n == 0 || sp.in_channels == 0) return;
+    k_max_pool_any<double><<<grid_for(n, kThreads), kThreads, 0, s>>>(
+        in->d, out->d, sp.kernel, sp.stride, sp.pad, (int)field_volume(sp, in->d.dim), data, sp.in_channels, res, sw);
+    launched("max_pool (f64)");
+}
+void launch_avg_pool(const hc_psh* in, const double* data, const hc_psh* out, const hc_conv_spec& sp, double* res,
+                     cudaStream_t s) {
+    const long long n = out->d.N;
+    if (n == 0 || sp.in_channels == 0) return;
+    const long long fd = field_volume(sp, in->d.dim);
+    const double inv = 1.0 / static_cast<double>(fd);  // cnn_ops.cpp:295
+    k_avg_pool_any<double><<<grid_for(n, kThreads), kThreads, 0, s>>>(in->d, out->d, sp.kernel, sp.stride, sp.pad,
+                                                                      (int)fd, data, sp.in_channels, inv, res);
+    launched("avg_pool (f64)");
+}
+void launch_unpool(bool avg, const double* cd, const int* sw, const hc_psh* fine, const hc_psh* coarse,
+                   const hc_conv_spec& sp, double* res, cudaStream_t s) {
+    const long long n = fine->d.N;
+    if (n == 0 || sp.in_channels == 0) return;
+    const unsigned g = grid_for(n, kThreads);
+    const double inv = 1.0 / static_cast<double>(field_volume(sp, fine->d.dim));  // cnn_ops.cpp:381
+    if (avg)
+        k_unpool_any<true, double><<<g, kThreads, 0, s>>>(fine->d, coarse->d, sp.kernel, sp.stride, sp.pad, cd, sw,
+                                                          sp.in_channels, inv, res);
+    else
+        k_unpool_any<false, double><<<g, kThreads, 0, s>>>(fine->d, coarse->d, sp.kernel, sp.stride, sp.pad, cd, sw,
+                                                           sp.in_channels, inv, res);
+    launched("unpool (f64)");
+}
+// fp64 contraction: always the order-exact kernels (the math mode selects fp32 paths only)
+void gemm_nn(const double* a, const double* b, double* c, long long ra, long long k, long long cb, cudaStream_t s) {
+    gemm_nn_exact(a, b, c, ra, k, cb, s);
+}
+void gemm_tn(const double* a, const double* b, double* c, long long ra, long long k, long long cb, cudaStream_t s) {
+    gemm_tn_exact(a, b, c, ra, k, cb, s);
+}
+void gemm_nt(const double* a, const double* b, double* c, long long ra, long long k, long long rb, cudaStream_t s) {
+    gemm_nt_exact(a, b, c, ra, k, rb, s);
+}
+
 }  // namespace hcb
 
 using namespace hcb;
 
 // ====================================================================== C ABI
+namespace hcb {
+
+template <typename T>
+hc_status hash2col_impl(const hc_psh* in, const T* data, int64_t data_rows, int64_t data_cols, const hc_psh* out,
+                          hc_conv_spec spec, T* cols, hc_stream stream) {
+    return guard([&] {
+        check_pair(in, out, spec);
+        if (data_rows != spec.in_channels || data_cols != in->d.N)
+            throw std::invalid_argument("hash2col: input data shape mismatch");
+        launch_hash2col(in, data, out, spec, cols, as_stream(stream));
+    });
+}
+
+template <typename T>
+hc_status col2hash_impl(const T* col_grads, int64_t rows, int64_t cols, const hc_psh* in, const hc_psh* out,
+                          hc_conv_spec spec, T* result, hc_stream stream) {
+    return guard([&] {
+        check_pair(in, out, spec);
+        const long long fd = field_volume(spec, in->d.dim);
+        if (rows != spec.in_channels * fd || cols != out->d.N)
+            throw std::invalid_argument("col2hash: column gradient shape mismatch");
+        launch_col2hash(col_grads, in, out, spec, result, as_stream(stream));
+    });
+}
+
+template <typename T>
+hc_status conv_forward_impl(const hc_psh* in, const T* data, int64_t data_rows, int64_t data_cols,
+                              const hc_psh* out, const T* w, int64_t w_rows, int64_t w_cols, hc_conv_spec spec,
+                              T* result, hc_stream stream) {
+    return guard([&] {
+        if (!in || !out) throw std::invalid_argument("null super-PSH handle");
+        const long long fd = field_volume(spec, in->d.dim);
+        if (w_rows != spec.out_channels || w_cols != spec.in_channels * fd)
+            throw std::invalid_argument("conv_forward: weight shape mismatch");
+        check_pair(in, out, spec);
+        if (data_rows != spec.in_channels || data_cols != in->d.N)
+            throw std::invalid_argument("hash2col: input data shape mismatch");
+        cudaStream_t s = as_stream(stream);
+        const long long K = spec.in_channels * fd, N = out->d.N;
+        Scratch cols(sizeof(T) * K * N, s);
+        launch_hash2col(in, data, out, spec, cols.as<T>(), s);
+        gemm_nn(w, cols.as<T>(), result, spec.out_channels, K, N, s);
+    });
+}
+
+template <typename T>
+hc_status conv_backward_impl(const T* output_grad, int64_t g_rows, int64_t g_cols, const T* w,
+                               int64_t w_rows, int64_t w_cols, const T* cached_cols, int64_t c_rows,
+                               int64_t c_cols, const hc_psh* in, const hc_psh* out, hc_conv_spec spec, T* dw,
+                               T* dx, hc_stream stream) {
+    return guard([&] {
+        if (!in || !out) throw std::invalid_argument("null super-PSH handle");
+        const long long fd = field_volume(spec, in->d.dim);
+        if (g_rows != spec.out_channels || g_cols != out->d.N)
+            throw std::invalid_argument("conv_backward: output gradient shape mismatch");
+        if (c_rows != spec.in_channels * fd || c_cols != out->d.N)
+            throw std::invalid_argument("conv_backward: cached column shape mismatch");
+        // gemm.cpp:80-93 shape checks of the two products, then col2hash's
+        if (w_rows != g_rows) throw std::invalid_argument("matmul_trans_a: shape mismatch");
+        check_pair(in, out, spec);
+        if (w_cols != spec.in_channels * fd) throw std::invalid_argument("col2hash: column gradient shape mismatch");
+        cudaStream_t s = as_stream(stream);
+        gemm_nt(output_grad, cached_cols, dw, g_rows, g_cols, c_rows, s);  // dW = dDo * cols^T
+        Scratch dcols(sizeof(T) * w_cols * g_cols, s);
+        gemm_tn(w, output_grad, dcols.as<T>(), w_rows, w_cols, g_cols, s);  // W^T * dDo
+        launch_col2hash(dcols.as<T>(), in, out, spec, dx, s);
+    });
+}
+
+template <typename T>
+hc_status max_pool_impl(const hc_psh* in, const T* data, int64_t data_rows, int64_t data_cols, const hc_psh* out,
+                          hc_conv_spec spec, T* result, int32_t* switches, hc_stream stream) {
+    return guard([&] {
+        check_pair(in, out, spec);
+        if (spec.stride < 2) throw std::invalid_argument("pooling requires stride >= 2");
+        if (data_rows != spec.in_channels || data_cols != in->d.N)
+            throw std::invalid_argument("max_pool: input data shape mismatch");
+        launch_max_pool(in, data, out, spec, result, switches, as_stream(stream));
+    });
+}
+
+template <typename T>
+hc_status avg_pool_impl(const hc_psh* in, const T* data, int64_t data_rows, int64_t data_cols, const hc_psh* out,
+                          hc_conv_spec spec, T* result, hc_stream stream) {
+    return guard([&] {
+        check_pair(in, out, spec);
+        if (spec.stride < 2) throw std::invalid_argument("pooling requires stride >= 2");
+        if (data_rows != spec.in_channels || data_cols != in->d.N)
+            throw std::invalid_argument("avg_pool: input data shape mismatch");
+        launch_avg_pool(in, data, out, spec, result, as_stream(stream));
+    });
+}
+
+template <typename T>
+hc_status max_unpool_impl(const T* coarse_data, int64_t c_rows, int64_t c_cols, const int32_t* switches,
+                            int64_t s_rows, int64_t s_cols, const hc_psh* fine, const hc_psh* coarse,
+                            hc_conv_spec spec, T* result, hc_stream stream) {
+    return guard([&] {
+        check_pair(fine, coarse, spec);
+        const long long fd = field_volume(spec, fine->d.dim);
+        if (c_rows != spec.in_channels || c_cols != coarse->d.N)
+            throw std::invalid_argument("max_unpool: coarse data shape mismatch");
+        // cnn_ops.cpp:326-332 check_switches (device scan; synchronises)
+        if (s_rows != spec.in_channels || s_cols != coarse->d.N)
+            throw std::invalid_argument("unpool: switch shape mismatch");
+        cudaStream_t s = as_stream(stream);
+        const long long n = s_rows * s_cols;
+        if (n > 0) {
+            Scratch flag(sizeof(int), s);
+            cuda_check(cudaMemsetAsync(flag.p, 0, sizeof(int), s), "memset");
+            k_check_switches<<<grid_for(n, kThreads), kThreads, 0, s>>>(switches, n, (int)fd, flag.as<int>());
+            launched("switch check");
+            int bad = 0;
+            cuda_check(cudaMemcpyAsync(&bad, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s), "switch check");
+            cuda_check(cudaStreamSynchronize(s), "switch check");
+            if (bad) throw std::invalid_argument("unpool: switch index out of range");
+        }
+        launch_unpool(false, coarse_data, switches, fine, coarse, spec, result, s);
+    });
+}
+
+template <typename T>
+hc_status avg_unpool_impl(const T* coarse_data, int64_t c_rows, int64_t c_cols, const hc_psh* fine,
+                            const hc_psh* coarse, hc_conv_spec spec, T* result, hc_stream stream) {
+    return guard([&] {
+        check_pair(fine, coarse, spec);
+        if (c_rows != spec.in_channels || c_cols != coarse->d.N)
+            throw std::invalid_argument("avg_unpool: coarse data shape mismatch");
+        launch_unpool(true, coarse_data, nullptr, fine, coarse, spec, result, as_stream(stream));
+    });
+}
+
+template <typename T>
+hc_status deconv_forward_impl(const hc_psh* coarse, const T* coarse_data, int64_t d_rows, int64_t d_cols,
+                                const hc_psh* fine, const T* w, int64_t w_rows, int64_t w_cols,
+                                hc_conv_spec spec, T* result, hc_stream stream) {
+    return guard([&] {
+        if (!coarse || !fine) throw std::invalid_argument("null super-PSH handle");
+        const long long fd = field_volume(spec, fine->d.dim);
+        if (w_rows != spec.out_channels || w_cols != spec.in_channels * fd)
+            throw std::invalid_argument("deconv_forward: weight shape mismatch");
+        if (d_rows != spec.out_channels || d_cols != coarse->d.N)
+            throw std::invalid_argument("deconv_forward: coarse data shape mismatch");
+        check_pair(fine, coarse, spec);
+        cudaStream_t s = as_stream(stream);
+        Scratch cols(sizeof(T) * w_cols * d_cols, s);
+        gemm_tn(w, coarse_data, cols.as<T>(), w_rows, w_cols, d_cols, s);  // W^T * D_i
+        launch_col2hash(cols.as<T>(), fine, coarse, spec, result, s);
+    });
+}
+
+template <typename T>
+hc_status deconv_backward_impl(const T* fine_grad, int64_t g_rows, int64_t g_cols, const T* w,
+                                 int64_t w_rows, int64_t w_cols, const T* cached_coarse, int64_t c_rows,
+                                 int64_t c_cols, const hc_psh* coarse, const hc_psh* fine, hc_conv_spec spec,
+                                 T* dw, T* dx, hc_stream stream) {
+    return guard([&] {
+        if (!coarse || !fine) throw std::invalid_argument("null super-PSH handle");
+        if (g_rows != spec.in_channels || g_cols != fine->d.N)
+            throw std::invalid_argument("deconv_backward: fine gradient shape mismatch");
+        check_pair(fine, coarse, spec);
+        const long long fd = field_volume(spec, fine->d.dim);
+        const long long K = spec.in_channels * fd, N = coarse->d.N;
+        if (c_cols != N) throw std::invalid_argument("matmul_trans_b: shape mismatch");
+        if (w_cols != K) throw std::invalid_argument("matmul: shape mismatch");
+        cudaStream_t s = as_stream(stream);
+        Scratch dcols(sizeof(T) * K * N, s);
+        launch_hash2col(fine, fine_grad, coarse, spec, dcols.as<T>(), s);  // adjoint of col2hash
+        gemm_nt(cached_coarse, dcols.as<T>(), dw, c_rows, N, K, s);        // dW = D_i * dcols^T
+        gemm_nn(w, dcols.as<T>(), dx, w_rows, K, N, s);                    // dD_i = W * dcols
+    });
+}
+
+template <typename T>
+hc_status matmul_impl(const T* a, const T* b, T* c, int64_t ra, int64_t k, int64_t cb, hc_stream stream) {
+    return guard([&] { gemm_nn(a, b, c, ra, k, cb, as_stream(stream)); });
+}
+
+template <typename T>
+hc_status matmul_trans_a_impl(const T* a, const T* b, T* c, int64_t ra, int64_t k, int64_t cb,
+                                hc_stream stream) {
+    return guard([&] { gemm_tn(a, b, c, ra, k, cb, as_stream(stream)); });
+}
+
+template <typename T>
+hc_status matmul_trans_b_impl(const T* a, const T* b, T* c, int64_t ra, int64_t k, int64_t rb,
+                                hc_stream stream) {
+    return guard([&] { gemm_nt(a, b, c, ra, k, rb, as_stream(stream)); });
+}
+
+}  // namespace hcb
+
 extern "C" {
 
 hc_status hc_field_map(const hc_psh* in, const hc_psh* out, hc_conv_spec spec, int32_t* map, hc_stream stream) {
@@ -829,175 +1086,129 @@ hc_status hc_field_map_tiled(const hc_psh* in, const hc_psh* out, hc_conv_spec s
 
 hc_status hc_hash2col_f32(const hc_psh* in, const float* data, int64_t data_rows, int64_t data_cols, const hc_psh* out,
                           hc_conv_spec spec, float* cols, hc_stream stream) {
-    return guard([&] {
-        check_pair(in, out, spec);
-        if (data_rows != spec.in_channels || data_cols != in->d.N)
-            throw std::invalid_argument("hash2col: input data shape mismatch");
-        launch_hash2col(in, data, out, spec, cols, as_stream(stream));
-    });
+    return hash2col_impl<float>(in, data, data_rows, data_cols, out, spec, cols, stream);
+}
+hc_status hc_hash2col_f64(const hc_psh* in, const double* data, int64_t data_rows, int64_t data_cols, const hc_psh* out,
+                          hc_conv_spec spec, double* cols, hc_stream stream) {
+    return hash2col_impl<double>(in, data, data_rows, data_cols, out, spec, cols, stream);
 }
 
 hc_status hc_col2hash_f32(const float* col_grads, int64_t rows, int64_t cols, const hc_psh* in, const hc_psh* out,
                           hc_conv_spec spec, float* result, hc_stream stream) {
-    return guard([&] {
-        check_pair(in, out, spec);
-        const long long fd = field_volume(spec, in->d.dim);
-        if (rows != spec.in_channels * fd || cols != out->d.N)
-            throw std::invalid_argument("col2hash: column gradient shape mismatch");
-        launch_col2hash(col_grads, in, out, spec, result, as_stream(stream));
-    });
+    return col2hash_impl<float>(col_grads, rows, cols, in, out, spec, result, stream);
+}
+hc_status hc_col2hash_f64(const double* col_grads, int64_t rows, int64_t cols, const hc_psh* in, const hc_psh* out,
+                          hc_conv_spec spec, double* result, hc_stream stream) {
+    return col2hash_impl<double>(col_grads, rows, cols, in, out, spec, result, stream);
 }
 
 hc_status hc_conv_forward_f32(const hc_psh* in, const float* data, int64_t data_rows, int64_t data_cols,
                               const hc_psh* out, const float* w, int64_t w_rows, int64_t w_cols, hc_conv_spec spec,
                               float* result, hc_stream stream) {
-    return guard([&] {
-        if (!in || !out) throw std::invalid_argument("null super-PSH handle");
-        const long long fd = field_volume(spec, in->d.dim);
-        if (w_rows != spec.out_channels || w_cols != spec.in_channels * fd)
-            throw std::invalid_argument("conv_forward: weight shape mismatch");
-        check_pair(in, out, spec);
-        if (data_rows != spec.in_channels || data_cols != in->d.N)
-            throw std::invalid_argument("hash2col: input data shape mismatch");
-        cudaStream_t s = as_stream(stream);
-        const long long K = spec.in_channels * fd, N = out->d.N;
-        Scratch cols(sizeof(float) * K * N, s);
-        launch_hash2col(in, data, out, spec, cols.as<float>(), s);
-        gemm_nn(w, cols.as<float>(), result, spec.out_channels, K, N, s);
-    });
+    return conv_forward_impl<float>(in, data, data_rows, data_cols, out, w, w_rows, w_cols, spec, result, stream);
+}
+hc_status hc_conv_forward_f64(const hc_psh* in, const double* data, int64_t data_rows, int64_t data_cols,
+                              const hc_psh* out, const double* w, int64_t w_rows, int64_t w_cols, hc_conv_spec spec,
+                              double* result, hc_stream stream) {
+    return conv_forward_impl<double>(in, data, data_rows, data_cols, out, w, w_rows, w_cols, spec, result, stream);
 }
 
 hc_status hc_conv_backward_f32(const float* output_grad, int64_t g_rows, int64_t g_cols, const float* w,
                                int64_t w_rows, int64_t w_cols, const float* cached_cols, int64_t c_rows,
                                int64_t c_cols, const hc_psh* in, const hc_psh* out, hc_conv_spec spec, float* dw,
                                float* dx, hc_stream stream) {
-    return guard([&] {
-        if (!in || !out) throw std::invalid_argument("null super-PSH handle");
-        const long long fd = field_volume(spec, in->d.dim);
-        if (g_rows != spec.out_channels || g_cols != out->d.N)
-            throw std::invalid_argument("conv_backward: output gradient shape mismatch");
-        if (c_rows != spec.in_channels * fd || c_cols != out->d.N)
-            throw std::invalid_argument("conv_backward: cached column shape mismatch");
-        // gemm.cpp:80-93 shape checks of the two products, then col2hash's
-        if (w_rows != g_rows) throw std::invalid_argument("matmul_trans_a: shape mismatch");
-        check_pair(in, out, spec);
-        if (w_cols != spec.in_channels * fd) throw std::invalid_argument("col2hash: column gradient shape mismatch");
-        cudaStream_t s = as_stream(stream);
-        gemm_nt(output_grad, cached_cols, dw, g_rows, g_cols, c_rows, s);  // dW = dDo * cols^T
-        Scratch dcols(sizeof(float) * w_cols * g_cols, s);
-        gemm_tn(w, output_grad, dcols.as<float>(), w_rows, w_cols, g_cols, s);  // W^T * dDo
-        launch_col2hash(dcols.as<float>(), in, out, spec, dx, s);
-    });
+    return conv_backward_impl<float>(output_grad, g_rows, g_cols, w, w_rows, w_cols, cached_cols, c_rows, c_cols, in, out, spec, dw, dx, stream);
+}
+hc_status hc_conv_backward_f64(const double* output_grad, int64_t g_rows, int64_t g_cols, const double* w,
+                               int64_t w_rows, int64_t w_cols, const double* cached_cols, int64_t c_rows,
+                               int64_t c_cols, const hc_psh* in, const hc_psh* out, hc_conv_spec spec, double* dw,
+                               double* dx, hc_stream stream) {
+    return conv_backward_impl<double>(output_grad, g_rows, g_cols, w, w_rows, w_cols, cached_cols, c_rows, c_cols, in, out, spec, dw, dx, stream);
 }
 
 hc_status hc_max_pool_f32(const hc_psh* in, const float* data, int64_t data_rows, int64_t data_cols, const hc_psh* out,
                           hc_conv_spec spec, float* result, int32_t* switches, hc_stream stream) {
-    return guard([&] {
-        check_pair(in, out, spec);
-        if (spec.stride < 2) throw std::invalid_argument("pooling requires stride >= 2");
-        if (data_rows != spec.in_channels || data_cols != in->d.N)
-            throw std::invalid_argument("max_pool: input data shape mismatch");
-        launch_max_pool(in, data, out, spec, result, switches, as_stream(stream));
-    });
+    return max_pool_impl<float>(in, data, data_rows, data_cols, out, spec, result, switches, stream);
+}
+hc_status hc_max_pool_f64(const hc_psh* in, const double* data, int64_t data_rows, int64_t data_cols, const hc_psh* out,
+                          hc_conv_spec spec, double* result, int32_t* switches, hc_stream stream) {
+    return max_pool_impl<double>(in, data, data_rows, data_cols, out, spec, result, switches, stream);
 }
 
 hc_status hc_avg_pool_f32(const hc_psh* in, const float* data, int64_t data_rows, int64_t data_cols, const hc_psh* out,
                           hc_conv_spec spec, float* result, hc_stream stream) {
-    return guard([&] {
-        check_pair(in, out, spec);
-        if (spec.stride < 2) throw std::invalid_argument("pooling requires stride >= 2");
-        if (data_rows != spec.in_channels || data_cols != in->d.N)
-            throw std::invalid_argument("avg_pool: input data shape mismatch");
-        launch_avg_pool(in, data, out, spec, result, as_stream(stream));
-    });
+    return avg_pool_impl<float>(in, data, data_rows, data_cols, out, spec, result, stream);
+}
+hc_status hc_avg_pool_f64(const hc_psh* in, const double* data, int64_t data_rows, int64_t data_cols, const hc_psh* out,
+                          hc_conv_spec spec, double* result, hc_stream stream) {
+    return avg_pool_impl<double>(in, data, data_rows, data_cols, out, spec, result, stream);
 }
 
 hc_status hc_max_unpool_f32(const float* coarse_data, int64_t c_rows, int64_t c_cols, const int32_t* switches,
                             int64_t s_rows, int64_t s_cols, const hc_psh* fine, const hc_psh* coarse,
                             hc_conv_spec spec, float* result, hc_stream stream) {
-    return guard([&] {
-        check_pair(fine, coarse, spec);
-        const long long fd = field_volume(spec, fine->d.dim);
-        if (c_rows != spec.in_channels || c_cols != coarse->d.N)
-            throw std::invalid_argument("max_unpool: coarse data shape mismatch");
-        // cnn_ops.cpp:326-332 check_switches (device scan; synchronises)
-        if (s_rows != spec.in_channels || s_cols != coarse->d.N)
-            throw std::invalid_argument("unpool: switch shape mismatch");
-        cudaStream_t s = as_stream(stream);
-        const long long n = s_rows * s_cols;
-        if (n > 0) {
-            Scratch flag(sizeof(int), s);
-            cuda_check(cudaMemsetAsync(flag.p, 0, sizeof(int), s), "memset");
-            k_check_switches<<<grid_for(n, kThreads), kThreads, 0, s>>>(switches, n, (int)fd, flag.as<int>());
-            launched("switch check");
-            int bad = 0;
-            cuda_check(cudaMemcpyAsync(&bad, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s), "switch check");
-            cuda_check(cudaStreamSynchronize(s), "switch check");
-            if (bad) throw std::invalid_argument("unpool: switch index out of range");
-        }
-        launch_unpool(false, coarse_data, switches, fine, coarse, spec, result, s);
-    });
+    return max_unpool_impl<float>(coarse_data, c_rows, c_cols, switches, s_rows, s_cols, fine, coarse, spec, result, stream);
+}
+hc_status hc_max_unpool_f64(const double* coarse_data, int64_t c_rows, int64_t c_cols, const int32_t* switches,
+                            int64_t s_rows, int64_t s_cols, const hc_psh* fine, const hc_psh* coarse,
+                            hc_conv_spec spec, double* result, hc_stream stream) {
+    return max_unpool_impl<double>(coarse_data, c_rows, c_cols, switches, s_rows, s_cols, fine, coarse, spec, result, stream);
 }
 
 hc_status hc_avg_unpool_f32(const float* coarse_data, int64_t c_rows, int64_t c_cols, const hc_psh* fine,
                             const hc_psh* coarse, hc_conv_spec spec, float* result, hc_stream stream) {
-    return guard([&] {
-        check_pair(fine, coarse, spec);
-        if (c_rows != spec.in_channels || c_cols != coarse->d.N)
-            throw std::invalid_argument("avg_unpool: coarse data shape mismatch");
-        launch_unpool(true, coarse_data, nullptr, fine, coarse, spec, result, as_stream(stream));
-    });
+    return avg_unpool_impl<float>(coarse_data, c_rows, c_cols, fine, coarse, spec, result, stream);
+}
+hc_status hc_avg_unpool_f64(const double* coarse_data, int64_t c_rows, int64_t c_cols, const hc_psh* fine,
+                            const hc_psh* coarse, hc_conv_spec spec, double* result, hc_stream stream) {
+    return avg_unpool_impl<double>(coarse_data, c_rows, c_cols, fine, coarse, spec, result, stream);
 }
 
 hc_status hc_deconv_forward_f32(const hc_psh* coarse, const float* coarse_data, int64_t d_rows, int64_t d_cols,
                                 const hc_psh* fine, const float* w, int64_t w_rows, int64_t w_cols,
                                 hc_conv_spec spec, float* result, hc_stream stream) {
-    return guard([&] {
-        if (!coarse || !fine) throw std::invalid_argument("null super-PSH handle");
-        const long long fd = field_volume(spec, fine->d.dim);
-        if (w_rows != spec.out_channels || w_cols != spec.in_channels * fd)
-            throw std::invalid_argument("deconv_forward: weight shape mismatch");
-        if (d_rows != spec.out_channels || d_cols != coarse->d.N)
-            throw std::invalid_argument("deconv_forward: coarse data shape mismatch");
-        check_pair(fine, coarse, spec);
-        cudaStream_t s = as_stream(stream);
-        Scratch cols(sizeof(float) * w_cols * d_cols, s);
-        gemm_tn(w, coarse_data, cols.as<float>(), w_rows, w_cols, d_cols, s);  // W^T * D_i
-        launch_col2hash(cols.as<float>(), fine, coarse, spec, result, s);
-    });
+    return deconv_forward_impl<float>(coarse, coarse_data, d_rows, d_cols, fine, w, w_rows, w_cols, spec, result, stream);
+}
+hc_status hc_deconv_forward_f64(const hc_psh* coarse, const double* coarse_data, int64_t d_rows, int64_t d_cols,
+                                const hc_psh* fine, const double* w, int64_t w_rows, int64_t w_cols,
+                                hc_conv_spec spec, double* result, hc_stream stream) {
+    return deconv_forward_impl<double>(coarse, coarse_data, d_rows, d_cols, fine, w, w_rows, w_cols, spec, result, stream);
 }
 
 hc_status hc_deconv_backward_f32(const float* fine_grad, int64_t g_rows, int64_t g_cols, const float* w,
                                  int64_t w_rows, int64_t w_cols, const float* cached_coarse, int64_t c_rows,
                                  int64_t c_cols, const hc_psh* coarse, const hc_psh* fine, hc_conv_spec spec,
                                  float* dw, float* dx, hc_stream stream) {
-    return guard([&] {
-        if (!coarse || !fine) throw std::invalid_argument("null super-PSH handle");
-        if (g_rows != spec.in_channels || g_cols != fine->d.N)
-            throw std::invalid_argument("deconv_backward: fine gradient shape mismatch");
-        check_pair(fine, coarse, spec);
-        const long long fd = field_volume(spec, fine->d.dim);
-        const long long K = spec.in_channels * fd, N = coarse->d.N;
-        if (c_cols != N) throw std::invalid_argument("matmul_trans_b: shape mismatch");
-        if (w_cols != K) throw std::invalid_argument("matmul: shape mismatch");
-        cudaStream_t s = as_stream(stream);
-        Scratch dcols(sizeof(float) * K * N, s);
-        launch_hash2col(fine, fine_grad, coarse, spec, dcols.as<float>(), s);  // adjoint of col2hash
-        gemm_nt(cached_coarse, dcols.as<float>(), dw, c_rows, N, K, s);        // dW = D_i * dcols^T
-        gemm_nn(w, dcols.as<float>(), dx, w_rows, K, N, s);                    // dD_i = W * dcols
-    });
+    return deconv_backward_impl<float>(fine_grad, g_rows, g_cols, w, w_rows, w_cols, cached_coarse, c_rows, c_cols, coarse, fine, spec, dw, dx, stream);
+}
+hc_status hc_deconv_backward_f64(const double* fine_grad, int64_t g_rows, int64_t g_cols, const double* w,
+                                 int64_t w_rows, int64_t w_cols, const double* cached_coarse, int64_t c_rows,
+                                 int64_t c_cols, const hc_psh* coarse, const hc_psh* fine, hc_conv_spec spec,
+                                 double* dw, double* dx, hc_stream stream) {
+    return deconv_backward_impl<double>(fine_grad, g_rows, g_cols, w, w_rows, w_cols, cached_coarse, c_rows, c_cols, coarse, fine, spec, dw, dx, stream);
 }
 
 hc_status hc_matmul_f32(const float* a, const float* b, float* c, int64_t ra, int64_t k, int64_t cb, hc_stream stream) {
-    return guard([&] { gemm_nn(a, b, c, ra, k, cb, as_stream(stream)); });
+    return matmul_impl<float>(a, b, c, ra, k, cb, stream);
+}
+hc_status hc_matmul_f64(const double* a, const double* b, double* c, int64_t ra, int64_t k, int64_t cb, hc_stream stream) {
+    return matmul_impl<double>(a, b, c, ra, k, cb, stream);
 }
 hc_status hc_matmul_trans_a_f32(const float* a, const float* b, float* c, int64_t ra, int64_t k, int64_t cb,
                                 hc_stream stream) {
-    return guard([&] { gemm_tn(a, b, c, ra, k, cb, as_stream(stream)); });
+    return matmul_trans_a_impl<float>(a, b, c, ra, k, cb, stream);
+}
+hc_status hc_matmul_trans_a_f64(const double* a, const double* b, double* c, int64_t ra, int64_t k, int64_t cb,
+                                hc_stream stream) {
+    return matmul_trans_a_impl<double>(a, b, c, ra, k, cb, stream);
 }
 hc_status hc_matmul_trans_b_f32(const float* a, const float* b, float* c, int64_t ra, int64_t k, int64_t rb,
                                 hc_stream stream) {
-    return guard([&] { gemm_nt(a, b, c, ra, k, rb, as_stream(stream)); });
+    return matmul_trans_b_impl<float>(a, b, c, ra, k, rb, stream);
+}
+hc_status hc_matmul_trans_b_f64(const double* a, const double* b, double* c, int64_t ra, int64_t k, int64_t rb,
+                                hc_stream stream) {
+    return matmul_trans_b_impl<double>(a, b, c, ra, k, rb, stream);
 }
 
 }  // extern "C"

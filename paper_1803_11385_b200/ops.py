@@ -70,21 +70,31 @@ def _stream():
 
 
 class _Args:
-    """Tracks whether the call came with host inputs (=> host outputs)."""
+    """Tracks whether the call came with host inputs (=> host outputs) and the call's
+    precision: like the reference's templates (instantiated for float and double,
+    cnn_ops.cpp:652-653), the first floating input picks T — float64 inputs run the fp64
+    entry points, anything else fp32 — and the other floating inputs follow it."""
 
     def __init__(self):
         self.host = False
+        self.dtype = None
 
-    def f32(self, x) -> torch.Tensor:
+    def fp(self, x) -> torch.Tensor:
         if isinstance(x, np.ndarray):
             self.host = True
-            x = torch.from_numpy(np.ascontiguousarray(x, np.float32))
+            x = torch.from_numpy(np.ascontiguousarray(x, np.float64 if x.dtype == np.float64 else np.float32))
+        if self.dtype is None:
+            self.dtype = torch.float64 if x.dtype == torch.float64 else torch.float32
         if not x.is_cuda:
             self.host = True
             x = x.to(_dev(), non_blocking=True)
-        if x.dtype != torch.float32:
-            x = x.float()
+        if x.dtype != self.dtype:
+            x = x.to(self.dtype)
         return x.contiguous()
+
+    def fn(self, name: str):
+        """The entry point of this call's precision: name_f32 or name_f64."""
+        return getattr(lib, name + ("_f64" if self.dtype == torch.float64 else "_f32"))
 
     def i32(self, x) -> torch.Tensor:
         if isinstance(x, np.ndarray):
@@ -156,9 +166,9 @@ def hash2col(input: SuperPsh, input_data, output: SuperPsh, spec: ConvSpec):
     """cnn_ops.cpp:123-158"""
     spec = ConvSpec(*spec)
     a = _Args()
-    d = a.f32(input_data)
-    cols = _empty(spec.in_channels * field_size(spec, input.dim), output.total_columns())
-    check(lib.hc_hash2col_f32(input._h, _p(d), *_shape(d), output._h, spec.c(), _p(cols), _stream()))
+    d = a.fp(input_data)
+    cols = _empty(spec.in_channels * field_size(spec, input.dim), output.total_columns(), a.dtype)
+    check(a.fn("hc_hash2col")(input._h, _p(d), *_shape(d), output._h, spec.c(), _p(cols), _stream()))
     return a.out(cols)
 
 
@@ -166,9 +176,9 @@ def col2hash(col_grads, input: SuperPsh, output: SuperPsh, spec: ConvSpec):
     """cnn_ops.cpp:160-204"""
     spec = ConvSpec(*spec)
     a = _Args()
-    g = a.f32(col_grads)
-    res = _empty(spec.in_channels, input.total_columns())
-    check(lib.hc_col2hash_f32(_p(g), *_shape(g), input._h, output._h, spec.c(), _p(res), _stream()))
+    g = a.fp(col_grads)
+    res = _empty(spec.in_channels, input.total_columns(), a.dtype)
+    check(a.fn("hc_col2hash")(_p(g), *_shape(g), input._h, output._h, spec.c(), _p(res), _stream()))
     return a.out(res)
 
 
@@ -176,9 +186,9 @@ def conv_forward(input: SuperPsh, input_data, output: SuperPsh, weights, spec: C
     """cnn_ops.cpp:206-215 (weights: C_out x C_in*F^dim)"""
     spec = ConvSpec(*spec)
     a = _Args()
-    d, w = a.f32(input_data), a.f32(weights)
-    res = _empty(spec.out_channels, output.total_columns())
-    check(lib.hc_conv_forward_f32(input._h, _p(d), *_shape(d), output._h, _p(w), *_shape(w), spec.c(), _p(res),
+    d, w = a.fp(input_data), a.fp(weights)
+    res = _empty(spec.out_channels, output.total_columns(), a.dtype)
+    check(a.fn("hc_conv_forward")(input._h, _p(d), *_shape(d), output._h, _p(w), *_shape(w), spec.c(), _p(res),
                                   _stream()))
     return a.out(res)
 
@@ -187,12 +197,12 @@ def conv_backward(output_grad, weights, cached_cols, input: SuperPsh, output: Su
     """cnn_ops.cpp:217-232 -> ConvGradients(weights=dW, input=dX)"""
     spec = ConvSpec(*spec)
     a = _Args()
-    g, w, cc = a.f32(output_grad), a.f32(weights), a.f32(cached_cols)
+    g, w, cc = a.fp(output_grad), a.fp(weights), a.fp(cached_cols)
     gr, gc = _shape(g)
     wr, wc = _shape(w)
-    dw = _empty(gr, _shape(cc)[0])
-    dx = _empty(spec.in_channels, input.total_columns())
-    check(lib.hc_conv_backward_f32(_p(g), gr, gc, _p(w), wr, wc, _p(cc), *_shape(cc), input._h, output._h,
+    dw = _empty(gr, _shape(cc)[0], a.dtype)
+    dx = _empty(spec.in_channels, input.total_columns(), a.dtype)
+    check(a.fn("hc_conv_backward")(_p(g), gr, gc, _p(w), wr, wc, _p(cc), *_shape(cc), input._h, output._h,
                                    spec.c(), _p(dw), _p(dx), _stream()))
     return ConvGradients(a.out(dw), a.out(dx))
 
@@ -201,10 +211,10 @@ def max_pool(input: SuperPsh, input_data, output: SuperPsh, spec: ConvSpec) -> M
     """cnn_ops.cpp:234-284"""
     spec = ConvSpec(*spec)
     a = _Args()
-    d = a.f32(input_data)
-    res = _empty(spec.in_channels, output.total_columns())
+    d = a.fp(input_data)
+    res = _empty(spec.in_channels, output.total_columns(), a.dtype)
     sw = _empty(spec.in_channels, output.total_columns(), torch.int32)
-    check(lib.hc_max_pool_f32(input._h, _p(d), *_shape(d), output._h, spec.c(), _p(res), _p(sw), _stream()))
+    check(a.fn("hc_max_pool")(input._h, _p(d), *_shape(d), output._h, spec.c(), _p(res), _p(sw), _stream()))
     return MaxPoolResult(a.out(res), a.out(sw))
 
 
@@ -212,9 +222,9 @@ def avg_pool(input: SuperPsh, input_data, output: SuperPsh, spec: ConvSpec):
     """cnn_ops.cpp:286-322"""
     spec = ConvSpec(*spec)
     a = _Args()
-    d = a.f32(input_data)
-    res = _empty(spec.in_channels, output.total_columns())
-    check(lib.hc_avg_pool_f32(input._h, _p(d), *_shape(d), output._h, spec.c(), _p(res), _stream()))
+    d = a.fp(input_data)
+    res = _empty(spec.in_channels, output.total_columns(), a.dtype)
+    check(a.fn("hc_avg_pool")(input._h, _p(d), *_shape(d), output._h, spec.c(), _p(res), _stream()))
     return a.out(res)
 
 
@@ -222,9 +232,9 @@ def max_unpool(coarse_data, switches, fine: SuperPsh, coarse: SuperPsh, spec: Co
     """cnn_ops.cpp:336-372 (switch range validated; synchronises)"""
     spec = ConvSpec(*spec)
     a = _Args()
-    cd, sw = a.f32(coarse_data), a.i32(switches)
-    res = _empty(spec.in_channels, fine.total_columns())
-    check(lib.hc_max_unpool_f32(_p(cd), *_shape(cd), _p(sw), *_shape(sw), fine._h, coarse._h, spec.c(), _p(res),
+    cd, sw = a.fp(coarse_data), a.i32(switches)
+    res = _empty(spec.in_channels, fine.total_columns(), a.dtype)
+    check(a.fn("hc_max_unpool")(_p(cd), *_shape(cd), _p(sw), *_shape(sw), fine._h, coarse._h, spec.c(), _p(res),
                                 _stream()))
     return a.out(res)
 
@@ -233,9 +243,9 @@ def avg_unpool(coarse_data, fine: SuperPsh, coarse: SuperPsh, spec: ConvSpec):
     """cnn_ops.cpp:374-406"""
     spec = ConvSpec(*spec)
     a = _Args()
-    cd = a.f32(coarse_data)
-    res = _empty(spec.in_channels, fine.total_columns())
-    check(lib.hc_avg_unpool_f32(_p(cd), *_shape(cd), fine._h, coarse._h, spec.c(), _p(res), _stream()))
+    cd = a.fp(coarse_data)
+    res = _empty(spec.in_channels, fine.total_columns(), a.dtype)
+    check(a.fn("hc_avg_unpool")(_p(cd), *_shape(cd), fine._h, coarse._h, spec.c(), _p(res), _stream()))
     return a.out(res)
 
 
@@ -243,9 +253,9 @@ def deconv_forward(coarse: SuperPsh, coarse_data, fine: SuperPsh, weights, spec:
     """cnn_ops.cpp:408-419"""
     spec = ConvSpec(*spec)
     a = _Args()
-    d, w = a.f32(coarse_data), a.f32(weights)
-    res = _empty(spec.in_channels, fine.total_columns())
-    check(lib.hc_deconv_forward_f32(coarse._h, _p(d), *_shape(d), fine._h, _p(w), *_shape(w), spec.c(), _p(res),
+    d, w = a.fp(coarse_data), a.fp(weights)
+    res = _empty(spec.in_channels, fine.total_columns(), a.dtype)
+    check(a.fn("hc_deconv_forward")(coarse._h, _p(d), *_shape(d), fine._h, _p(w), *_shape(w), spec.c(), _p(res),
                                     _stream()))
     return a.out(res)
 
@@ -254,10 +264,10 @@ def deconv_backward(fine_grad, weights, cached_coarse_data, coarse: SuperPsh, fi
     """cnn_ops.cpp:421-435 -> ConvGradients(weights=dW, input=dX(coarse))"""
     spec = ConvSpec(*spec)
     a = _Args()
-    g, w, cd = a.f32(fine_grad), a.f32(weights), a.f32(cached_coarse_data)
-    dw = _empty(_shape(cd)[0], spec.in_channels * field_size(spec, fine.dim))
-    dx = _empty(_shape(w)[0], coarse.total_columns())
-    check(lib.hc_deconv_backward_f32(_p(g), *_shape(g), _p(w), *_shape(w), _p(cd), *_shape(cd), coarse._h, fine._h,
+    g, w, cd = a.fp(fine_grad), a.fp(weights), a.fp(cached_coarse_data)
+    dw = _empty(_shape(cd)[0], spec.in_channels * field_size(spec, fine.dim), a.dtype)
+    dx = _empty(_shape(w)[0], coarse.total_columns(), a.dtype)
+    check(a.fn("hc_deconv_backward")(_p(g), *_shape(g), _p(w), *_shape(w), _p(cd), *_shape(cd), coarse._h, fine._h,
                                      spec.c(), _p(dw), _p(dx), _stream()))
     return ConvGradients(a.out(dw), a.out(dx))
 
@@ -265,31 +275,31 @@ def deconv_backward(fine_grad, weights, cached_coarse_data, coarse: SuperPsh, fi
 def matmul(a_, b_):
     """gemm.cpp:71-77: c = a * b"""
     a = _Args()
-    x, y = a.f32(a_), a.f32(b_)
+    x, y = a.fp(a_), a.fp(b_)
     if x.shape[1] != y.shape[0]:
         raise ValueError("matmul: shape mismatch")
-    c = _empty(x.shape[0], y.shape[1])
-    check(lib.hc_matmul_f32(_p(x), _p(y), _p(c), x.shape[0], x.shape[1], y.shape[1], _stream()))
+    c = _empty(x.shape[0], y.shape[1], a.dtype)
+    check(a.fn("hc_matmul")(_p(x), _p(y), _p(c), x.shape[0], x.shape[1], y.shape[1], _stream()))
     return a.out(c)
 
 
 def matmul_trans_a(a_, b_):
     """gemm.cpp:79-85: c = a^T * b"""
     a = _Args()
-    x, y = a.f32(a_), a.f32(b_)
+    x, y = a.fp(a_), a.fp(b_)
     if x.shape[0] != y.shape[0]:
         raise ValueError("matmul_trans_a: shape mismatch")
-    c = _empty(x.shape[1], y.shape[1])
-    check(lib.hc_matmul_trans_a_f32(_p(x), _p(y), _p(c), x.shape[0], x.shape[1], y.shape[1], _stream()))
+    c = _empty(x.shape[1], y.shape[1], a.dtype)
+    check(a.fn("hc_matmul_trans_a")(_p(x), _p(y), _p(c), x.shape[0], x.shape[1], y.shape[1], _stream()))
     return a.out(c)
 
 
 def matmul_trans_b(a_, b_):
     """gemm.cpp:87-93: c = a * b^T"""
     a = _Args()
-    x, y = a.f32(a_), a.f32(b_)
+    x, y = a.fp(a_), a.fp(b_)
     if x.shape[1] != y.shape[1]:
         raise ValueError("matmul_trans_b: shape mismatch")
-    c = _empty(x.shape[0], y.shape[0])
-    check(lib.hc_matmul_trans_b_f32(_p(x), _p(y), _p(c), x.shape[0], x.shape[1], y.shape[0], _stream()))
+    c = _empty(x.shape[0], y.shape[0], a.dtype)
+    check(a.fn("hc_matmul_trans_b")(_p(x), _p(y), _p(c), x.shape[0], x.shape[1], y.shape[0], _stream()))
     return a.out(c)

@@ -2,7 +2,7 @@
 // changing the namespace only. Builds fixtures with the UNMODIFIED reference library
 // (oracle/_ref objects; reference headers at build time) and checks, on the
 // reference's own types, that hashconv_b200::<op> == hashconv::<op> bit-for-bit
-// (EXACT math), including the reference's known-answer tests
+// (EXACT math; float AND double instantiations), including the reference's known-answer tests
 // (tests/test_cnn_ops.cpp:53-97, 140-156, 308-344) and its exception types.
 #include <cmath>
 #include <cstdio>
@@ -49,12 +49,13 @@ static Fixture fixture(int models, int res, std::uint64_t seed) {
     return fx;
 }
 
+template <class T>
 static void ops_equal(const Fixture& fx, const ConvSpec& spec, std::uint64_t seed) {
     const SuperPsh& out = spec.stride == 1 ? fx.fine : fx.coarse;
     const std::int64_t fd = field_size(spec, 3);
-    const auto data = testing::random_matrix<float>(spec.in_channels, fx.fine.total_columns(), seed);
-    const KernelWeights w{testing::random_matrix<float>(spec.out_channels, spec.in_channels * fd, seed + 1)};
-    const auto dout = testing::random_matrix<float>(spec.out_channels, out.total_columns(), seed + 2);
+    const auto data = testing::random_matrix<T>(spec.in_channels, fx.fine.total_columns(), seed);
+    const KernelWeightsT<T> w{testing::random_matrix<T>(spec.out_channels, spec.in_channels * fd, seed + 1)};
+    const auto dout = testing::random_matrix<T>(spec.out_channels, out.total_columns(), seed + 2);
     const auto cols = hash2col(fx.fine, data, out, spec);
     CHECK(hb::hash2col(fx.fine, data, out, spec) == cols, "hash2col");
     CHECK(hb::conv_forward(fx.fine, data, out, w, spec) == conv_forward(fx.fine, data, out, w, spec), "conv_forward");
@@ -62,7 +63,7 @@ static void ops_equal(const Fixture& fx, const ConvSpec& spec, std::uint64_t see
     const auto h = hb::conv_backward(dout, w, cols, fx.fine, out, spec);
     CHECK(h.weights == g.weights, "conv_backward dW");
     CHECK(h.input == g.input, "conv_backward dX");
-    const auto y = testing::random_matrix<float>(spec.in_channels * fd, out.total_columns(), seed + 3);
+    const auto y = testing::random_matrix<T>(spec.in_channels * fd, out.total_columns(), seed + 3);
     CHECK(hb::col2hash(y, fx.fine, out, spec) == col2hash(y, fx.fine, out, spec), "col2hash");
     const ConvSpec pool{2, 2, 0, spec.in_channels, spec.in_channels};
     const auto mp = max_pool(fx.fine, data, fx.coarse, pool);
@@ -72,10 +73,10 @@ static void ops_equal(const Fixture& fx, const ConvSpec& spec, std::uint64_t see
     CHECK(hb::max_unpool(mp.output, mp.switches, fx.fine, fx.coarse, pool) ==
               max_unpool(mp.output, mp.switches, fx.fine, fx.coarse, pool),
           "max_unpool");
-    const auto cv = testing::random_matrix<float>(spec.in_channels, fx.coarse.total_columns(), seed + 4);
+    const auto cv = testing::random_matrix<T>(spec.in_channels, fx.coarse.total_columns(), seed + 4);
     CHECK(hb::avg_unpool(cv, fx.fine, fx.coarse, pool) == avg_unpool(cv, fx.fine, fx.coarse, pool), "avg_unpool");
     if (spec.stride > 1) {
-        const auto ci = testing::random_matrix<float>(spec.out_channels, fx.coarse.total_columns(), seed + 5);
+        const auto ci = testing::random_matrix<T>(spec.out_channels, fx.coarse.total_columns(), seed + 5);
         CHECK(hb::deconv_forward(fx.coarse, ci, fx.fine, w, spec) == deconv_forward(fx.coarse, ci, fx.fine, w, spec),
               "deconv_forward");
         const auto a = deconv_backward(data, w, ci, fx.coarse, fx.fine, spec);
@@ -150,7 +151,8 @@ int main() {
     const ConvSpec specs[] = {{3, 1, 0, 3, 5}, {2, 2, 0, 4, 2}, {3, 2, 0, 2, 6}, {2, 2, 1, 5, 3}};
     for (int t = 0; t < 8; ++t) {
         const Fixture fx = fixture(1 + t % 3, t % 2 ? 16 : 32, 5000 + t);
-        ops_equal(fx, specs[t % 4], 100 + t);
+        ops_equal<float>(fx, specs[t % 4], 100 + t);
+        ops_equal<double>(fx, specs[t % 4], 200 + t);  // the reference's double instantiation
     }
     std::printf("%s: %d checks, %d failures\n", g_fail ? "DROPIN FAIL" : "DROPIN OK", g_checks, g_fail);
     return g_fail ? 1 : 0;
