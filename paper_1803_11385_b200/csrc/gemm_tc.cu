@@ -46,7 +46,12 @@ using namespace tc;
 
 constexpr int BM = 128;         // C columns per tile (TMEM lanes)
 constexpr int BKF = 32;         // fp32 K elements per stage = one 128-byte swizzle row
-constexpr int kThreads = 192;
+#ifndef HCB_GEMM_EW
+#define HCB_GEMM_EW 4  // A/B: 8 warps measured slower (fwd 3.33 -> 3.53 ms at C=64)
+#endif
+constexpr int kEW = HCB_GEMM_EW;           // split / epilogue warps (4 or 8)
+constexpr int kEpi = kEW * 32;             // their threads
+constexpr int kThreads = 64 + kEpi;        // + TMA warp + MMA warp
 constexpr int kBlk = 8;         // stages (8 x 32 = 256 K) per TMEM accumulation block
 
 template <int BN, int SPLIT>
@@ -117,12 +122,12 @@ __global__ void __launch_bounds__(kThreads, GCfg<BN, SPLIT>::CTAS) k_gemm_tf32(c
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(full0 + 8 * s, 1);
-            mbar_init(cvt0 + 8 * s, 128);
+            mbar_init(cvt0 + 8 * s, kEpi);
             mbar_init(empty0 + 8 * s, 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(tfull0 + 8 * b, 1);
-            mbar_init(tempty0 + 8 * b, 128);
+            mbar_init(tempty0 + 8 * b, kEpi);
         }
         mbar_init_fence();
     }
@@ -223,18 +228,21 @@ __global__ void __launch_bounds__(kThreads, GCfg<BN, SPLIT>::CTAS) k_gemm_tf32(c
         // in TMEM alone miss the 1e-5 bar at K >= ~2000).
         const int t_id = threadIdx.x - 64;
         const int q = warp & 3;  // TMEM lane quadrant this warp may read
-        float acc[BN];
+        // with 8 warps two share a quadrant and split the accumulator's columns
+        constexpr int BNW = BN * 4 / kEW;
+        const int cw = ((warp - 2) / 4) * BNW;
+        float acc[BNW];
 #pragma unroll
-        for (int j = 0; j < BN; ++j) acc[j] = 0.0f;
+        for (int j = 0; j < BNW; ++j) acc[j] = 0.0f;
         // drain global block b; `last`: the final block of tile T -> store and reset
         auto drain = [&](int b, const Tile& T, bool last) {
             const int buf = b & 1;
             mbar_wait(tfull0 + 8 * buf, (b >> 1) & 1);  // spin: the MMA warp needs this buffer back soon
             tc_fence_after();
 #pragma unroll
-            for (int c0 = 0; c0 < BN; c0 += 16) {
+            for (int c0 = 0; c0 < BNW; c0 += 16) {
                 uint32_t v[16];
-                tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + c0, v);
+                tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + buf * BN + cw + c0, v);
                 tmem_ld_wait();
 #pragma unroll
                 for (int j = 0; j < 16; ++j) acc[c0 + j] = __fadd_rn(acc[c0 + j], __uint_as_float(v[j]));
@@ -244,17 +252,17 @@ __global__ void __launch_bounds__(kThreads, GCfg<BN, SPLIT>::CTAS) k_gemm_tf32(c
             if (last) {
                 const long long m = T.m0 + q * 32 + lane_id();
                 if (m < cb) {
-                    float* p = C + T.z * split_stride + T.n0 * cb + m;
-                    const int rows = (int)min((long long)BN, ra - T.n0);
+                    float* p = C + T.z * split_stride + (T.n0 + cw) * cb + m;
+                    const int rows = (int)min((long long)BNW, ra - T.n0 - cw);
 #pragma unroll
-                    for (int j = 0; j < BN; ++j) {
+                    for (int j = 0; j < BNW; ++j) {
                         if (j < rows) __stcs(p, acc[j]);  // streaming: the output is not re-read here
                         p += cb;
                         asm volatile("" : "+l"(p));  // keep the address chain sequential (no 64 live pointers)
                     }
                 }
 #pragma unroll
-                for (int j = 0; j < BN; ++j) acc[j] = 0.0f;
+                for (int j = 0; j < BNW; ++j) acc[j] = 0.0f;
             }
         };
         int blk = -1;
@@ -287,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, GCfg<BN, SPLIT>::CTAS) k_gemm_tf32(c
                     mbar_wait(full0 + 8 * s, ph);
                     const uint32_t raw = sbase + s * Cfg::STAGE;
 #pragma unroll 4
-                    for (int e = t_id; e < Cfg::RAW / 16; e += 128) {
+                    for (int e = t_id; e < Cfg::RAW / 16; e += kEpi) {
                         const int4 v = ld_shared_v4(raw + 16 * e);
                         uint4 h, l;
                         split_tf32((uint32_t)v.x, h.x, l.x);

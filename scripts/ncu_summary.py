@@ -13,7 +13,9 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OP_OF = {"k_field_map": "field_map", "k_conv_dw": "dW_conv", "k_conv_fwd": "fwd_conv",
-         "k_hash2col": "hash2col", "k_col2hash": "col2hash"}
+         "k_hash2col": "hash2col", "k_col2hash": "col2hash",
+         # reference-layout contraction (gemm_tc.cu: <MMA-A MN-major, MMA-B MN-major, ...>)
+         "k_gemm_tf32<1, 0": "fwd_gemm", "k_gemm_tf32<0, 0": "dW_gemm", "k_gemm_tf32<1, 1": "dcols_gemm"}
 METRICS = [
     ("gpu__time_duration.sum", "time"),
     ("dram__bytes_read.sum", "DRAM read"),
@@ -95,7 +97,9 @@ def main():
             print(f"| `{k[:70]}` | {t:.3f} | {100 * t / s:.1f}% |")
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     os.makedirs(os.path.dirname(path), exist_ok=True)
-    json.dump(traffic, open(path, "w"), indent=1)
+    merged = json.load(open(path)) if os.path.exists(path) else {}
+    merged.update(traffic)  # captures of other workloads keep their entries
+    json.dump(merged, open(path, "w"), indent=1)
 
 
 if __name__ == "__main__":
