@@ -70,6 +70,8 @@ _SIGS = {
     "hc_read_psh_file": [C.c_char_p, _P, _I32, _P],
     "hc_psh_upload": [_P, _P, _P],
     "hc_psh_upload_levels": [_P, _I32, _P, _P],
+    "hc_malloc": [_P, C.c_size_t],
+    "hc_free": [_P],
     "hc_psh_info": [_P, _P],
     "hc_psh_download": [_P] * 10,
     "hc_psh_columns": [_P, _P],
