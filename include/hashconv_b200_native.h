@@ -86,6 +86,11 @@ hc_status hc_native_bn_relu_forward(const float* x, int64_t n, int32_t c, int32_
 hc_status hc_native_bn_relu_backward(const void* d_relu, hc_dtype dtype, const float* xhat,
                                      const float* inv_std, int64_t n, int32_t c, void* d_conv_bf16,
                                      void* workspace, size_t ws_bytes, hc_stream stream);
+/* Inference-mode batch norm + ReLU (net_forward with training = false, cnn_ops.cpp:470-475):
+ * the running statistics normalise; out_bf16 = max(0, (x - mean) * T(1/sqrt(var + eps))). */
+hc_status hc_native_bn_relu_inference(const float* x, int64_t n, int32_t c, const float* running_mean,
+                                      const float* running_var, float eps, void* out_bf16,
+                                      hc_stream stream);
 /* Synchronised batch norm for data parallelism (the reference normalises over
  * the whole batch, cnn_ops.cpp:456-470), in phases so the caller can sum the per-channel
  * statistics over ranks (e.g. ncclAllReduce, double) between them:

@@ -673,6 +673,16 @@ class RefNet:
             o += r * c
         return float(loss[0]), grads, (w1, b1, w2, b2)
 
+    def forward(self, levels, classes: int, training: bool = False) -> np.ndarray:
+        """net.cpp:181-258 net_forward: scores (classes x b); inference by default."""
+        L = self.ref.lib
+        L.hcref_net_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p]
+        arr = (C.c_void_p * len(levels))(*[lv.h for lv in levels])
+        b = int(levels[-1].batch)
+        scores = np.empty((classes, b), np.float32)
+        self.ref._check(L.hcref_net_forward(self.h, arr, len(levels), int(training), _ptr(scores)))
+        return scores
+
     def __del__(self):
         if getattr(self, "h", None):
             self.ref.lib.hcref_net_free(self.h)

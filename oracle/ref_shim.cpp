@@ -462,4 +462,18 @@ int hcref_net_loss_grads(void* g, const void* const* levels, int nlevels, const 
     });
 }
 
+// net.cpp:181-258 net_forward<float>; training = 0: running statistics, dropout off.
+// scores: classes x b.
+int hcref_net_forward(void* g, const void* const* levels, int nlevels, int training, float* scores) {
+    return guarded([&] {
+        auto* G = static_cast<LayerGraph*>(g);
+        MultiLevelBatch batch;
+        for (int i = 0; i < nlevels; ++i) batch.levels.push_back(S(levels[i]));
+        NetRunOptions opt;
+        opt.training = training != 0;
+        opt.update_running_stats = training != 0;
+        out(net_forward(*G, batch, opt), scores);
+    });
+}
+
 }  // extern "C"

@@ -121,6 +121,7 @@ _SIGS.update({
     "hc_native_bn_relu_forward": [_P, _I64, _I32, _I32, C.c_float, C.c_float, _P, _P, _P, _P, _P, _P, C.c_size_t,
                                   _P],
     "hc_native_bn_relu_backward": [_P, C.c_int, _P, _P, _I64, _I32, _P, _P, C.c_size_t, _P],
+    "hc_native_bn_relu_inference": [_P, _I64, _I32, _P, _P, C.c_float, _P, _P],
     "hc_native_bn_stat": [_I32, _P, _P, C.c_int, _I64, _I32, _P, _P, _P, C.c_size_t, _P],
     "hc_native_bn_finalize": [_P, _P, _I64, _I32, C.c_float, C.c_float, _P, _P, _P, _P, _P],
     "hc_native_bn_relu_apply": [_P, _I64, _I32, _P, _P, _P, _P, _P],

@@ -315,6 +315,27 @@ __global__ void __launch_bounds__(kT) k_bn_relu_apply(const float* __restrict__ 
     store8(out + row * C + c0, o);
 }
 
+// Inference batch norm + ReLU (cnn_ops.cpp:470-475 with training = false): the running
+// statistics stand in for the batch's, inv_std = T(1 / sqrt(double(var) + eps)),
+// y = (x - T(mean)) * inv_std, out = max(0, y) (bf16 for the next layer).
+__global__ void __launch_bounds__(kT) k_bn_relu_infer(const float* __restrict__ x, long long n, int C,
+                                                     const float* __restrict__ rmean, const float* __restrict__ rvar,
+                                                     float eps, bf16* __restrict__ out) {
+    const int chunks = C >> 3;
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n * chunks) return;
+    const long long row = i / chunks;
+    const int c0 = (int)(i - row * chunks) * 8;
+    float v[8], o[8];
+    load8(x + row * C + c0, v);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const float inv = (float)(1.0 / sqrt((double)rvar[c0 + e] + (double)eps));
+        o[e] = fmaxf(0.0f, __fmul_rn(__fsub_rn(v[e], rmean[c0 + e]), inv));
+    }
+    store8(out + row * C + c0, o);
+}
+
 // dx = inv_std * (dyb - s1/n - xhat * s2/n), dyb = dy * (xhat > 0)  (cnn_ops.cpp:476-489
 // after relu_backward cnn_ops.cpp:553-561); bf16 out = the conv layer's output gradient.
 template <typename DT>
@@ -529,6 +550,18 @@ hc_status hc_native_bn_relu_backward(const void* d_relu, hc_dtype dtype, const f
                                                                       static_cast<bf16*>(d_conv_bf16), n);
         }
         launched("batch-norm + relu backward", 3);
+    });
+}
+
+hc_status hc_native_bn_relu_inference(const float* x, int64_t n, int32_t c, const float* running_mean,
+                                      const float* running_var, float eps, void* out_bf16, hc_stream stream) {
+    return guard([&] {
+        check_c8(c);
+        if (n <= 0) return;
+        const long long m = n * (c / 8);
+        k_bn_relu_infer<<<grid_for(m, kT), kT, 0, as_stream(stream)>>>(x, n, c, running_mean, running_var, eps,
+                                                                       static_cast<bf16*>(out_bf16));
+        launched("batch-norm (inference) + relu");
     });
 }
 

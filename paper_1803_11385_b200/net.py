@@ -238,18 +238,23 @@ class NativeHashNet:
 
     # ------------------------------------------------------------------ forward / backward
     def forward(self, nb: NetBatch, x: torch.Tensor, training: bool = True, cache: Optional[dict] = None):
-        """net.cpp:181-258 net_forward (training mode): class scores (classes x b)."""
-        if not training:
-            raise ValueError("native net: training-mode forward (inference uses running stats: reference path)")
+        """net.cpp:181-258 net_forward: class scores (classes x b). training=True: batch
+        statistics (running stats updated) and dropout; training=False: the running statistics
+        normalise and dropout is the identity (net.cpp:203-208, 232-241)."""
         acts = []
         for i, blk in enumerate(self.blocks):
             s = nb.levels[i]
             n = s.total_columns()
             wf = nconv.pack_weights(blk["w"], blk["cout_p"], blk["cin_p"], 27, False)
             y = nconv.gather_gemm(nb.conv_maps[i], x, wf, blk["cout_p"], torch.float32)
-            xhat = torch.empty_like(y)
             r = torch.empty((n, blk["cout_p"]), dtype=BF16, device="cuda")
-            self._bn_relu_forward(i, y, xhat, r)
+            if training:
+                xhat = torch.empty_like(y)
+                self._bn_relu_forward(i, y, xhat, r)
+            else:
+                xhat = None
+                check(lib.hc_native_bn_relu_inference(_p(y), n, blk["cout_p"], _p(blk["run_mean"]), _p(blk["run_var"]),
+                                                      self.bn_eps, _p(r), _s()))
             acts.append(dict(x=x, xhat=xhat))
             if i + 1 < len(self.blocks):
                 pm = nb.pool_maps[i]
@@ -269,6 +274,9 @@ class NativeHashNet:
                 acts[-1]["src"] = src
                 x = head
         # head: dropout -> FC(128) -> dropout -> FC(classes)   (net.cpp:236-251)
+        if not training:
+            fc1_out = self.fc1_w @ x + self.fc1_b[:, None]
+            return self.fc2_w @ fc1_out + self.fc2_b[:, None]
         keep = 1.0 - self.dropout
         if self._gen is None and not torch.cuda.is_current_stream_capturing():
             self._gen = torch.Generator(device="cuda").manual_seed(self._seed)
@@ -282,6 +290,10 @@ class NativeHashNet:
         if cache is not None:
             cache.update(acts=acts, m1=m1, m2=m2, fc1_in=fc1_in, fc2_in=fc2_in)
         return scores
+
+    def predict(self, nb: NetBatch, x: torch.Tensor) -> torch.Tensor:
+        """Inference (running statistics, no dropout): predicted class per shape."""
+        return self.forward(nb, x, training=False).argmax(0)
 
     def loss_and_gradients(self, nb: NetBatch, x: torch.Tensor, labels: torch.Tensor,
                            global_batch: Optional[int] = None):

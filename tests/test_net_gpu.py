@@ -139,6 +139,39 @@ def test_native_net_step_matches_reference_net(cuda, ref):
         assert _rel(a.cpu().numpy(), r) < 8e-2
 
 
+def test_native_net_inference_matches_reference_net(cuda, ref):
+    """net_forward with training = false (net.cpp:203-208, 232-241): running statistics
+    normalise, dropout is off. The reference's running stats (after one training pass) are
+    loaded into the native net, so the comparison isolates the inference path (bf16 conv
+    operands: scores within 2e-2 normwise)."""
+    level_max, classes, b = 4, 5, 3
+    supers = _ref_pyramid_batch(ref, b, 1 << level_max, seed=13)
+    labels = np.array([1, 4, 0], np.int32)
+    rn = ref.net_make(level_max, classes, 9)
+    rn.set_dropout(0.0)
+    head_in = nnet.channels_at_level(2) * 8
+    net = nnet.NativeHashNet(level_max, classes, seed=1, dropout=0.0)
+    for i in range(rn.nblocks):
+        net.set_reference_weights(i, torch.from_numpy(rn.conv(i)).cuda())
+    for dst, src in zip((net.fc1_w, net.fc1_b, net.fc2_w, net.fc2_b), rn.fc(classes, head_in)):
+        dst.copy_(torch.from_numpy(src))
+    rn.loss_and_gradients(supers, labels, classes, head_in)  # training pass: running stats move
+    for i in range(rn.nblocks):
+        m_r, v_r = rn.bn(i)
+        blk = net.blocks[i]
+        assert np.abs(v_r - 1.0).max() > 1e-3  # the stats are not at their initial values
+        blk["run_mean"][:blk["cout"]] = torch.from_numpy(m_r).cuda()
+        blk["run_var"][:blk["cout"]] = torch.from_numpy(v_r).cuda()
+    want = rn.forward(supers, classes)
+    nb = nnet.NetBatch.build([SuperPsh.from_host(s) for s in supers])
+    x = net.input_features(torch.from_numpy(supers[0].data).cuda())
+    before = [blk["run_mean"].clone() for blk in net.blocks]
+    got = net.forward(nb, x, training=False)
+    assert _rel(got.cpu().numpy(), want) < 2e-2, _rel(got.cpu().numpy(), want)
+    assert all(torch.equal(a, blk["run_mean"]) for a, blk in zip(before, net.blocks))  # inference: stats untouched
+    assert net.predict(nb, x).shape == (b,)
+
+
 def test_native_net_train_step_descends(cuda, ref):
     supers = _ref_pyramid_batch(ref, 4, 16, seed=5)
     net = nnet.NativeHashNet(4, 4, seed=2, dropout=0.0, lr=0.01)  # batch 4: lr 0.05 oscillates
