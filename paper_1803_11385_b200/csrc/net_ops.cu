@@ -163,19 +163,27 @@ __global__ void __launch_bounds__(kT) k_switch_gather(const int* __restrict__ pm
 // Column partial sums over row blocks: thread (r, q) owns channel quad q of rows
 // r, r + R, ... inside the block's row range; partials [block][C] in double.
 // MODE 0: sum x; 1: sum (x - mean)^2; 2: (sum dyb, sum dyb*xhat) with dyb = dy*(xhat > 0).
-constexpr int kRowsPerBlock = 1024;
+// Rows per partial block: enough blocks for ~4 per SM (the statistics of a small level are
+// otherwise a few long serial chains), at most 1024; fixed for a given n -> deterministic.
+inline int bn_rows_per_block(long long n) {
+    long long r = (n + 591) / 592;
+    r = (r + 63) / 64 * 64;
+    return (int)(r < 64 ? 64 : r > 1024 ? 1024 : r);
+}
+inline int bn_blocks(long long n) { return (int)((n + bn_rows_per_block(n) - 1) / bn_rows_per_block(n)); }
 
 template <int MODE, typename DT>
 __global__ void __launch_bounds__(kT) k_col_partials(const float* __restrict__ a, const DT* __restrict__ b, long long n,
-                                                    int C, const double* __restrict__ mean, double* __restrict__ part) {
+                                                    int C, const double* __restrict__ mean, double* __restrict__ part,
+                                                    int rpb) {
     const int quads = C >> 2;
     const int R = kT / quads;  // rows in flight per block step
     const int q = threadIdx.x % quads, r = threadIdx.x / quads;
     __shared__ double red[2][kT * 4];
     double s[4] = {0, 0, 0, 0}, t[4] = {0, 0, 0, 0};
     if (r < R) {
-        const long long r0 = (long long)blockIdx.x * kRowsPerBlock;
-        const long long r1 = min(n, r0 + kRowsPerBlock);
+        const long long r0 = (long long)blockIdx.x * rpb;
+        const long long r1 = min(n, r0 + rpb);
         double mu[4] = {0, 0, 0, 0};
         if (MODE == 1)
 #pragma unroll
@@ -489,7 +497,7 @@ hc_status hc_native_switch_gather(const int32_t* pmap, int64_t n_coarse, int32_t
 }
 
 size_t hc_native_bn_workspace(int64_t n, int32_t c) {
-    const long long blocks = (n + kRowsPerBlock - 1) / kRowsPerBlock;
+    const long long blocks = bn_blocks(n);
     return (size_t)(blocks * 2 * c + 4 * c) * sizeof(double);
 }
 
@@ -502,14 +510,15 @@ hc_status hc_native_bn_relu_forward(const float* x, int64_t n, int32_t c, int32_
         if (n <= 0) throw std::invalid_argument("batch_norm: empty input");
         if (ws_bytes < hc_native_bn_workspace(n, c)) throw std::invalid_argument("native batch norm: workspace too small");
         cudaStream_t s = as_stream(stream);
-        const int blocks = (int)((n + kRowsPerBlock - 1) / kRowsPerBlock);
+        const int blocks = bn_blocks(n);
+        const int rpb = bn_rows_per_block(n);
         double* part = static_cast<double*>(workspace);
         double* mean = part + (long long)blocks * 2 * c;
         double* var = mean + c;
         if (training) {
-            k_col_partials<0, float><<<blocks, kT, 0, s>>>(x, nullptr, n, c, nullptr, part);
+            k_col_partials<0, float><<<blocks, kT, 0, s>>>(x, nullptr, n, c, nullptr, part, rpb);
             k_col_fold<0><<<c, kT, 0, s>>>(part, blocks, n, c, mean, nullptr, nullptr, nullptr, 0, 0, nullptr, nullptr);
-            k_col_partials<1, float><<<blocks, kT, 0, s>>>(x, nullptr, n, c, mean, part);
+            k_col_partials<1, float><<<blocks, kT, 0, s>>>(x, nullptr, n, c, mean, part, rpb);
             k_col_fold<1><<<c, kT, 0, s>>>(part, blocks, n, c, nullptr, var, running_mean, running_var, momentum, eps,
                                           mean, inv_std);
             launched("batch-norm statistics", 4);
@@ -531,20 +540,21 @@ hc_status hc_native_bn_relu_backward(const void* d_relu, hc_dtype dtype, const f
         if (n <= 0) return;
         if (ws_bytes < hc_native_bn_workspace(n, c)) throw std::invalid_argument("native batch norm: workspace too small");
         cudaStream_t s = as_stream(stream);
-        const int blocks = (int)((n + kRowsPerBlock - 1) / kRowsPerBlock);
+        const int blocks = bn_blocks(n);
+        const int rpb = bn_rows_per_block(n);
         double* part = static_cast<double*>(workspace);
         double* s1 = part + (long long)blocks * 2 * c;
         double* s2 = s1 + c;
         const long long m = n * (c / 8);
         if (dtype == HC_DTYPE_BF16) {
             const bf16* d = static_cast<const bf16*>(d_relu);
-            k_col_partials<2, bf16><<<blocks, kT, 0, s>>>(xhat, d, n, c, nullptr, part);
+            k_col_partials<2, bf16><<<blocks, kT, 0, s>>>(xhat, d, n, c, nullptr, part, rpb);
             k_col_fold<2><<<c, kT, 0, s>>>(part, blocks, n, c, s1, s2, nullptr, nullptr, 0, 0, nullptr, nullptr);
             k_bn_relu_bwd_apply<bf16><<<grid_for(m, kT), kT, 0, s>>>(d, xhat, n, c, s1, s2, inv_std,
                                                                      static_cast<bf16*>(d_conv_bf16), n);
         } else {
             const float* d = static_cast<const float*>(d_relu);
-            k_col_partials<2, float><<<blocks, kT, 0, s>>>(xhat, d, n, c, nullptr, part);
+            k_col_partials<2, float><<<blocks, kT, 0, s>>>(xhat, d, n, c, nullptr, part, rpb);
             k_col_fold<2><<<c, kT, 0, s>>>(part, blocks, n, c, s1, s2, nullptr, nullptr, 0, 0, nullptr, nullptr);
             k_bn_relu_bwd_apply<float><<<grid_for(m, kT), kT, 0, s>>>(d, xhat, n, c, s1, s2, inv_std,
                                                                       static_cast<bf16*>(d_conv_bf16), n);
@@ -579,13 +589,14 @@ hc_status hc_native_bn_stat(int32_t mode, const float* x, const void* d, hc_dtyp
             return;
         }
         if (ws_bytes < hc_native_bn_workspace(n, c)) throw std::invalid_argument("native batch norm: workspace too small");
-        const int blocks = (int)((n + kRowsPerBlock - 1) / kRowsPerBlock);
+        const int blocks = bn_blocks(n);
+        const int rpb = bn_rows_per_block(n);
         double* part = static_cast<double*>(workspace);
-        if (mode == 0) k_col_partials<0, float><<<blocks, kT, 0, s>>>(x, nullptr, n, c, nullptr, part);
-        else if (mode == 1) k_col_partials<1, float><<<blocks, kT, 0, s>>>(x, nullptr, n, c, mean, part);
+        if (mode == 0) k_col_partials<0, float><<<blocks, kT, 0, s>>>(x, nullptr, n, c, nullptr, part, rpb);
+        else if (mode == 1) k_col_partials<1, float><<<blocks, kT, 0, s>>>(x, nullptr, n, c, mean, part, rpb);
         else if (dtype == HC_DTYPE_BF16)
-            k_col_partials<2, bf16><<<blocks, kT, 0, s>>>(x, static_cast<const bf16*>(d), n, c, nullptr, part);
-        else k_col_partials<2, float><<<blocks, kT, 0, s>>>(x, static_cast<const float*>(d), n, c, nullptr, part);
+            k_col_partials<2, bf16><<<blocks, kT, 0, s>>>(x, static_cast<const bf16*>(d), n, c, nullptr, part, rpb);
+        else k_col_partials<2, float><<<blocks, kT, 0, s>>>(x, static_cast<const float*>(d), n, c, nullptr, part, rpb);
         k_col_fold<2><<<c, kT, 0, s>>>(part, blocks, n, c, sums, sums + c, nullptr, nullptr, 0, 0, nullptr, nullptr);
         launched("batch-norm partial sums", 2);
     });
