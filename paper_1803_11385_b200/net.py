@@ -304,11 +304,15 @@ class NativeHashNet:
         cache = {}
         scores = self.forward(nb, x, True, cache)
         b = scores.shape[1]
-        logp = torch.log_softmax(scores.double(), dim=0)
-        loss = -logp[labels, torch.arange(b, device="cuda")].mean()
-        dscores = torch.softmax(scores.double(), dim=0)
-        dscores[labels, torch.arange(b, device="cuda")] -= 1.0
-        dscores = (dscores / (global_batch or b)).float()
+        # softmax over classes, computed on the contiguous [b][classes] transpose (torch's
+        # inner-dimension softmax kernel; over dim 0 it takes a slow strided path)
+        st = scores.t().contiguous().double()
+        logp = torch.log_softmax(st, dim=1)
+        rows = torch.arange(b, device="cuda")
+        loss = -logp[rows, labels].mean()
+        dscores_t = logp.exp()
+        dscores_t[rows, labels] -= 1.0
+        dscores = (dscores_t.t() / (global_batch or b)).float()
         g_fc2_w = dscores @ cache["fc2_in"].t()
         g_fc2_b = dscores.sum(1)
         d_fc1_out = (self.fc2_w.t() @ dscores) * cache["m2"]
