@@ -59,6 +59,7 @@ class NativeSegNet:
                    for k, n in (("bn1", c), ("bn2", 2 * c), ("bn3", c))}
         self._dw = nconv.DwWorkspace()
         self._bnws = None
+        self._neg = None
 
     # ------------------------------------------------------------------ pieces
     def _bnws_for(self, n, c):
@@ -117,15 +118,18 @@ class NativeSegNet:
         up = torch.empty((nf, c), dtype=BF16, device="cuda")
         check(lib.hc_native_max_unpool(_p(self.parent), _p(self.prow), nf, _p(d3), _lib.HC_DTYPE_BF16, c, _p(sw),
                                        _p(up), _s()))
-        s3 = self.deconv.forward(e2).float() + up.float()
+        s3 = self.deconv.forward(e2)  # fp32 (the deconvolution's output dtype)
+        s3.add_(up)                   # + unpooled branch, one mixed-precision add
         r3, h3 = self._bn_relu(s3, "bn3")
         scores = self._conv(self.fmap_f, r3, "conv4", self.k)  # [N_fine][K] fp32
         # ---- per-voxel softmax cross-entropy (mean over voxels)
         logp = torch.log_softmax(scores, dim=1)
         loss = -logp.gather(1, labels[:, None]).mean()
-        dscores = torch.softmax(scores, dim=1)
-        dscores.scatter_add_(1, labels[:, None], torch.full((nf, 1), -1.0, device="cuda"))
-        dscores = (dscores / nf).to(BF16)
+        dscores = logp.exp_()  # softmax, in place (the loss has been gathered)
+        if self._neg is None or self._neg.shape[0] != nf:
+            self._neg = torch.full((nf, 1), -1.0, device="cuda")
+        dscores.scatter_add_(1, labels[:, None], self._neg)
+        dscores = dscores.mul_(1.0 / nf).to(BF16)
         # ---- backward
         g = {}
         g["conv4"], d_r3 = self._conv_bwd(self.fmap_f, r3, dscores, "conv4")
@@ -135,7 +139,8 @@ class NativeSegNet:
         check(lib.hc_native_switch_gather(_p(self.pmap), nc, 8, _p(d_s3), _lib.HC_DTYPE_BF16, c, _p(sw), _p(d_d3),
                                           _s()))
         g["conv3"], d_e2b = self._conv_bwd(self.fmap_c, e2, d_d3, "conv3")
-        d_e2 = (d_e2a.float() + d_e2b.float())
+        d_e2 = d_e2a.float()  # fp32 already (no copy)
+        d_e2.add_(d_e2b)
         d_y2 = self._bn_relu_bwd(d_e2, _lib.HC_DTYPE_F32, h2, "bn2")
         g["conv2"], d_p1 = self._conv_bwd(self.fmap_c, p1, d_y2, "conv2")
         d_r1 = torch.empty((nf, c), dtype=BF16, device="cuda")                 # pool backward = unpool
