@@ -223,3 +223,46 @@ def test_native_argument_errors(cuda):
     x = torch.zeros((4, 16), dtype=torch.bfloat16, device="cuda")
     with pytest.raises(ValueError, match="16, 32, 64, 128 or 256"):
         nconv.gather_gemm(fmap, x, torch.zeros((24, 448), dtype=torch.bfloat16, device="cuda"), 24)
+
+
+# ---------------------------------------------------------------- full size: the bench workload
+@pytest.fixture(scope="module")
+def bench_shell(cuda):
+    """BASELINE config 4's per-GPU shard, the exact `bench.py` workload: 8 x 256^3 shells."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    return SuperPsh.from_levels([bench.shell_levels(256)[0]] * 8)
+
+
+def test_full_size_native_layer_properties(bench_shell):
+    """Size-independent properties of the fused kernels at N = 1,826,368, C 64 -> 64:
+    (1) identity at the centre tap reproduces the input exactly; (2) the input gradient
+    (flipped-kernel gather-GEMM) is the adjoint of the forward, <W*x, dy> = <x, W^T*dy>;
+    (3) the weight gradient is the same bilinear form, <dW(x, dy), W> = <dy, W*x>. The fp32
+    accumulation bound is scaled by the absolute-value forms (|W|*|x| etc.)."""
+    s = bench_shell
+    n, C = s.total_columns(), 64
+    assert n == 8 * 228296
+    fm = nconv.field_map_native(s, s, ConvSpec(3, 1, 0, C, C), nconv.TILED)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    x = (torch.rand((n, C), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    eye = torch.zeros((C, C * 27), device="cuda")
+    eye.view(C, C, 27)[torch.arange(C), torch.arange(C), 13] = 1.0
+    y = nconv.gather_gemm(fm, x, nconv.pack_weights(eye, C, C, 27, False), C, torch.float32)
+    assert torch.equal(y, x.float())
+
+    w = bf16_round(torch.rand((C, C * 27), device="cuda", generator=g) * 2 - 1)
+    dy = (torch.rand((n, C), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    y = nconv.gather_gemm(fm, x, nconv.pack_weights(w, C, C, 27, False), C, torch.float32)
+    dx = nconv.gather_gemm(fm, dy, nconv.pack_weights(w, C, C, 27, True), C, torch.float32)
+    fwd_form = (y.double() * dy.double()).sum()
+    adj_form = (x.double() * dx.double()).sum()
+    ya = nconv.gather_gemm(fm, x.abs(), nconv.pack_weights(w.abs(), C, C, 27, False), C, torch.float32)
+    scale = float((ya.double() * dy.double().abs()).sum())
+    assert abs(float(fwd_form - adj_form)) <= 1e-5 * scale, (float(fwd_form), float(adj_form), scale)
+
+    dw = nconv.conv_dw(fm, x, dy)
+    dw_form = (dw.double() * w.double()).sum()
+    assert abs(float(dw_form - fwd_form)) <= 1e-5 * scale, (float(dw_form), float(fwd_form), scale)
