@@ -724,10 +724,17 @@ def net_main(args, rank, world, local):
             secs, cores = cpu_net_sample(args.res, 2, args.classes)
             cpu = {"value": 2 / secs, "unit": "shapes/s", "cores": cores, "kind": "reference",
                    "sample": "2 shells, net_loss_and_gradients"}
+        # the paper's GPU (GTX 1080, Caffe) classification-net iteration at batch 32
+        # (Table 2) -> shapes/s; comparable only at that batch
+        paper = {32: 1270.0, 64: 438.0, 128: 147.0, 256: 40.3, 512: 12.3}
+        value = b * world / (ms / 1e3)
+        vs = value / paper[args.res] if (b * world == 32 and args.res in paper) else None
         print(json.dumps({
-            "metric": "hcnn train step shapes/sec", "value": b * world / (ms / 1e3), "unit": "shapes/s",
+            "metric": "hcnn train step shapes/sec", "value": value, "unit": "shapes/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "scaling": "weak", "vs_baseline": vs,
+            "vs_baseline_source": "paper GPU net iteration, batch 32 (BASELINE.md §1, PAPER.md:485)" if vs else None,
+            "dtype": "bf16",
             "data": "synthetic (sphere shell pyramid, bench.cpp:33-77; random labels)",
             "config": {"workload": f"hcnn classification net {args.res}^3, {lmax - 1} conv/pool levels, "
                                    f"{b} shells/GPU", "res": args.res, "global_batch": b * world,
