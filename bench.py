@@ -561,12 +561,8 @@ def main():
         "value": value, "unit": "voxels/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": step.dtype, "data": "synthetic (sphere shells, bench.cpp:33-77; uniform[-1,1] features/weights)",
-        "config": {"workload": f"{args.res}^3 shell x {args.shapes_per_gpu}/GPU, 3x3x3 hash-conv "
-                               f"{args.cin}->{args.cout} fwd+bwd (BASELINE config 4 per-GPU shard)",
-                   "res": args.res, "shapes_per_gpu": args.shapes_per_gpu, "global_batch": args.shapes_per_gpu * world,
-                   "c_in": args.cin, "c_out": args.cout, "voxels_per_gpu": N, "path": step.name,
-                   "parallelism": f"dp{world} (shapes sharded, dW all-reduce)",
-                   "l2": "working set >> L2 (no flush needed)"},
+        "config": dict(conv_config(args, world), voxels_per_gpu=N, path=step.name,
+                       l2="working set >> L2 (no flush needed)"),
         "shapes_per_s": args.shapes_per_gpu * world / (ms_step / 1e3),
         "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": int(launches), "clocks": clk.summary(),
@@ -574,6 +570,15 @@ def main():
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def conv_config(args, world):
+    """The conv workload descriptor, shared by both arms (the reference arm times a bounded
+    sample of this same workload)."""
+    return {"workload": f"{args.res}^3 shell x {args.shapes_per_gpu}/GPU, 3x3x3 hash-conv "
+                        f"{args.cin}->{args.cout} fwd+bwd (BASELINE config 4 per-GPU shard)",
+            "res": args.res, "shapes_per_gpu": args.shapes_per_gpu, "global_batch": args.shapes_per_gpu * world,
+            "c_in": args.cin, "c_out": args.cout, "parallelism": f"dp{world} (shapes sharded, dW all-reduce)"}
 
 
 def reference_arm(args, rank, world):
@@ -598,9 +603,10 @@ def reference_arm(args, rank, world):
     print(json.dumps({
         "impl": "reference", "metric": "hash-conv fwd+bwd occupied voxels/sec", "value": value, "unit": "voxels/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"{args.res}^3 shell, 3x3x3 hash-conv {args.cin}->{args.cout} fwd+bwd",
-                   "res": args.res, "c_in": args.cin, "c_out": args.cout, "sample_voxels_per_step": n1},
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (sphere shells, bench.cpp:33-77; uniform[-1,1] features/weights)",
+        "config": dict(conv_config(args, world), sample_voxels_per_step=n1,
+                       path="reference CPU (oracle/_ref: the unmodified reference library)"),
         "cpu_baseline": {"value": value, "unit": "voxels/s", "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "voxels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
 
