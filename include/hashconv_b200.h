@@ -276,6 +276,52 @@ hc_status hc_matmul_trans_a_f64(const double* a, const double* b, double* c, int
 hc_status hc_matmul_trans_b_f64(const double* a, const double* b, double* c, int64_t ra, int64_t k,
                                 int64_t rb, hc_stream stream);
 
+
+/* The rest of cnn_ops.hpp (cnn_ops.hpp:118-170, cnn_ops.cpp:437-608), reference layout
+ * (channel-major C x N), fp32 and fp64, same error messages:
+ *   batch_norm_forward  per-channel stats over N (training: double two-pass mean / biased var,
+ *                       running stats updated in T) or the running stats (inference);
+ *                       y = (x - T(mean)) * T(1/sqrt(var + eps)); inv_std = the cache's
+ *                       inv_std (optional), y doubles as the cache's `normalized`.
+ *   batch_norm_backward dx = T(inv_std * (dy - s1/n - xhat * s2/n)), s1/s2 double sums.
+ *   scale_forward/backward, relu_forward/backward (std::max(T(0), x)), and inverted dropout
+ *   whose keep mask (uint8, one per element) is the reference's std::mt19937_64(seed) stream,
+ *   bit-exact; training = 0 or ratio = 0: identity, mask all ones. */
+hc_status hc_batch_norm_forward_f32(const float* x, int64_t c, int64_t n, float* running_mean,
+                                      float* running_var, int64_t stats_channels, float eps, float momentum,
+                                      int32_t training, float* y, float* inv_std, hc_stream stream);
+hc_status hc_batch_norm_backward_f32(const float* dy, int64_t c, int64_t n, const float* normalized,
+                                       int64_t n_rows, int64_t n_cols, const float* inv_std, float* dx,
+                                       hc_stream stream);
+hc_status hc_scale_forward_f32(const float* x, int64_t rows, int64_t cols, const float* gamma, int64_t n_gamma,
+                                 const float* beta, int64_t n_beta, float* y, hc_stream stream);
+hc_status hc_scale_backward_f32(const float* dy, const float* x, int64_t rows, int64_t cols, const float* gamma,
+                                  float* d_gamma, float* d_beta, float* dx, hc_stream stream);
+hc_status hc_relu_forward_f32(const float* x, int64_t total, float* y, hc_stream stream);
+hc_status hc_relu_backward_f32(const float* dy, int64_t rows, int64_t cols, const float* forward_out,
+                                 int64_t o_rows, int64_t o_cols, float* dx, hc_stream stream);
+hc_status hc_dropout_forward_f32(const float* x, int64_t total, float ratio, uint64_t seed, int32_t training,
+                                   float* y, uint8_t* keep, hc_stream stream);
+hc_status hc_dropout_backward_f32(const float* dy, int64_t total, const uint8_t* keep, int64_t keep_size,
+                                    float ratio, float* dx, hc_stream stream);
+hc_status hc_batch_norm_forward_f64(const double* x, int64_t c, int64_t n, double* running_mean,
+                                      double* running_var, int64_t stats_channels, double eps, double momentum,
+                                      int32_t training, double* y, double* inv_std, hc_stream stream);
+hc_status hc_batch_norm_backward_f64(const double* dy, int64_t c, int64_t n, const double* normalized,
+                                       int64_t n_rows, int64_t n_cols, const double* inv_std, double* dx,
+                                       hc_stream stream);
+hc_status hc_scale_forward_f64(const double* x, int64_t rows, int64_t cols, const double* gamma, int64_t n_gamma,
+                                 const double* beta, int64_t n_beta, double* y, hc_stream stream);
+hc_status hc_scale_backward_f64(const double* dy, const double* x, int64_t rows, int64_t cols, const double* gamma,
+                                  double* d_gamma, double* d_beta, double* dx, hc_stream stream);
+hc_status hc_relu_forward_f64(const double* x, int64_t total, double* y, hc_stream stream);
+hc_status hc_relu_backward_f64(const double* dy, int64_t rows, int64_t cols, const double* forward_out,
+                                 int64_t o_rows, int64_t o_cols, double* dx, hc_stream stream);
+hc_status hc_dropout_forward_f64(const double* x, int64_t total, double ratio, uint64_t seed, int32_t training,
+                                   double* y, uint8_t* keep, hc_stream stream);
+hc_status hc_dropout_backward_f64(const double* dy, int64_t total, const uint8_t* keep, int64_t keep_size,
+                                    double ratio, double* dx, hc_stream stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,6 +21,7 @@
 // ABI directly (device super-PSH handles, device pointers, streams).
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
@@ -133,6 +134,14 @@ template <class T>
 struct abi;
 template <>
 struct abi<float> {
+    static constexpr auto batch_norm_forward = hc_batch_norm_forward_f32;
+    static constexpr auto batch_norm_backward = hc_batch_norm_backward_f32;
+    static constexpr auto scale_forward = hc_scale_forward_f32;
+    static constexpr auto scale_backward = hc_scale_backward_f32;
+    static constexpr auto relu_forward = hc_relu_forward_f32;
+    static constexpr auto relu_backward = hc_relu_backward_f32;
+    static constexpr auto dropout_forward = hc_dropout_forward_f32;
+    static constexpr auto dropout_backward = hc_dropout_backward_f32;
     static constexpr auto hash2col = hc_hash2col_f32;
     static constexpr auto col2hash = hc_col2hash_f32;
     static constexpr auto conv_forward = hc_conv_forward_f32;
@@ -149,6 +158,14 @@ struct abi<float> {
 };
 template <>
 struct abi<double> {
+    static constexpr auto batch_norm_forward = hc_batch_norm_forward_f64;
+    static constexpr auto batch_norm_backward = hc_batch_norm_backward_f64;
+    static constexpr auto scale_forward = hc_scale_forward_f64;
+    static constexpr auto scale_backward = hc_scale_backward_f64;
+    static constexpr auto relu_forward = hc_relu_forward_f64;
+    static constexpr auto relu_backward = hc_relu_backward_f64;
+    static constexpr auto dropout_forward = hc_dropout_forward_f64;
+    static constexpr auto dropout_backward = hc_dropout_backward_f64;
     static constexpr auto hash2col = hc_hash2col_f64;
     static constexpr auto col2hash = hc_col2hash_f64;
     static constexpr auto conv_forward = hc_conv_forward_f64;
@@ -395,6 +412,137 @@ Mat matmul_trans_b(const Mat& a, const Mat& b) {
     detail::check(detail::abi<T>::matmul_trans_b(da.template as<T>(), db.template as<T>(), c.as<T>(), a.rows,
                                         a.cols, b.rows, nullptr));
     return detail::download<Mat>(c, a.rows, b.rows);
+}
+
+// cnn_ops.hpp:118-170 — batch norm, scale, ReLU, inverted dropout (cnn_ops.cpp:437-608).
+// Stats / Cache / Mask are the caller's types with the reference's members
+// (running_mean, running_var, eps, momentum / normalized, inv_std / keep).
+template <class Mat>
+struct ScaleGradients {
+    std::vector<detail::value_t<Mat>> gamma;
+    std::vector<detail::value_t<Mat>> beta;
+    Mat input;
+};
+
+namespace detail {
+template <class V>
+inline Buf upload_vec(const V& v) {
+    return upload(v.data(), v.size());
+}
+template <class T>
+inline std::vector<T> download_vec(const Buf& b, size_t n) {
+    std::vector<T> v(n);
+    if (n) check(hc_memcpy_d2h(v.data(), b.as<void>(), sizeof(T) * n, nullptr));
+    check(hc_stream_synchronize(nullptr));
+    return v;
+}
+}  // namespace detail
+
+template <class Mat, class Stats, class Cache = std::nullptr_t>
+Mat batch_norm_forward(const Mat& x, Stats& stats, bool training, Cache* cache = nullptr) {
+    using T = detail::value_t<Mat>;
+    auto d = detail::upload(x);
+    auto rm = detail::upload_vec(stats.running_mean), rv = detail::upload_vec(stats.running_var);
+    detail::Buf y(sizeof(T) * static_cast<size_t>(x.rows * x.cols)), inv(sizeof(T) * static_cast<size_t>(x.rows));
+    detail::check(detail::abi<T>::batch_norm_forward(d.template as<T>(), x.rows, x.cols, rm.template as<T>(),
+                                                     rv.template as<T>(),
+                                                     static_cast<std::int64_t>(stats.running_mean.size()),
+                                                     stats.eps, stats.momentum, training ? 1 : 0, y.as<T>(),
+                                                     inv.as<T>(), nullptr));
+    if (training) {
+        stats.running_mean = detail::download_vec<T>(rm, stats.running_mean.size());
+        stats.running_var = detail::download_vec<T>(rv, stats.running_var.size());
+    }
+    Mat out = detail::download<Mat>(y, x.rows, x.cols);
+    if constexpr (!std::is_same<Cache, std::nullptr_t>::value) {
+        if (cache) {
+            cache->normalized = out;
+            cache->inv_std = detail::download_vec<T>(inv, static_cast<size_t>(x.rows));
+        }
+    }
+    return out;
+}
+
+template <class Mat, class Cache>
+Mat batch_norm_backward(const Mat& dy, const Cache& cache) {
+    using T = detail::value_t<Mat>;
+    auto d = detail::upload(dy), xh = detail::upload(cache.normalized), inv = detail::upload_vec(cache.inv_std);
+    detail::Buf dx(sizeof(T) * static_cast<size_t>(dy.rows * dy.cols));
+    detail::check(detail::abi<T>::batch_norm_backward(d.template as<T>(), dy.rows, dy.cols, xh.template as<T>(),
+                                                      cache.normalized.rows, cache.normalized.cols,
+                                                      inv.template as<T>(), dx.as<T>(), nullptr));
+    return detail::download<Mat>(dx, dy.rows, dy.cols);
+}
+
+template <class Mat, class V>
+Mat scale_forward(const Mat& x, const V& gamma, const V& beta) {
+    using T = detail::value_t<Mat>;
+    auto d = detail::upload(x), g = detail::upload_vec(gamma), b = detail::upload_vec(beta);
+    detail::Buf y(sizeof(T) * static_cast<size_t>(x.rows * x.cols));
+    detail::check(detail::abi<T>::scale_forward(d.template as<T>(), x.rows, x.cols, g.template as<T>(),
+                                                static_cast<std::int64_t>(gamma.size()), b.template as<T>(),
+                                                static_cast<std::int64_t>(beta.size()), y.as<T>(), nullptr));
+    return detail::download<Mat>(y, x.rows, x.cols);
+}
+
+template <class Mat, class V>
+ScaleGradients<Mat> scale_backward(const Mat& dy, const Mat& x, const V& gamma) {
+    using T = detail::value_t<Mat>;
+    auto d = detail::upload(dy), xx = detail::upload(x), g = detail::upload_vec(gamma);
+    detail::Buf dg(sizeof(T) * static_cast<size_t>(dy.rows)), db(sizeof(T) * static_cast<size_t>(dy.rows));
+    detail::Buf dx(sizeof(T) * static_cast<size_t>(dy.rows * dy.cols));
+    detail::check(detail::abi<T>::scale_backward(d.template as<T>(), xx.template as<T>(), dy.rows, dy.cols,
+                                                 g.template as<T>(), dg.as<T>(), db.as<T>(), dx.as<T>(), nullptr));
+    ScaleGradients<Mat> r;
+    r.gamma = detail::download_vec<T>(dg, static_cast<size_t>(dy.rows));
+    r.beta = detail::download_vec<T>(db, static_cast<size_t>(dy.rows));
+    r.input = detail::download<Mat>(dx, dy.rows, dy.cols);
+    return r;
+}
+
+template <class Mat>
+Mat relu_forward(const Mat& x) {
+    using T = detail::value_t<Mat>;
+    auto d = detail::upload(x);
+    detail::Buf y(sizeof(T) * static_cast<size_t>(x.rows * x.cols));
+    detail::check(detail::abi<T>::relu_forward(d.template as<T>(), x.rows * x.cols, y.as<T>(), nullptr));
+    return detail::download<Mat>(y, x.rows, x.cols);
+}
+
+template <class Mat>
+Mat relu_backward(const Mat& dy, const Mat& forward_out) {
+    using T = detail::value_t<Mat>;
+    auto d = detail::upload(dy), f = detail::upload(forward_out);
+    detail::Buf dx(sizeof(T) * static_cast<size_t>(dy.rows * dy.cols));
+    detail::check(detail::abi<T>::relu_backward(d.template as<T>(), dy.rows, dy.cols, f.template as<T>(),
+                                                forward_out.rows, forward_out.cols, dx.as<T>(), nullptr));
+    return detail::download<Mat>(dx, dy.rows, dy.cols);
+}
+
+template <class Mat, class T, class Mask = std::nullptr_t>
+Mat dropout_forward(const Mat& x, T ratio, std::uint64_t seed, bool training, Mask* mask = nullptr) {
+    using V = detail::value_t<Mat>;
+    const std::int64_t total = x.rows * x.cols;
+    auto d = detail::upload(x);
+    detail::Buf y(sizeof(V) * static_cast<size_t>(total)), keep(static_cast<size_t>(total));
+    detail::check(detail::abi<V>::dropout_forward(d.template as<V>(), total, static_cast<V>(ratio), seed,
+                                                  training ? 1 : 0, y.as<V>(), keep.as<std::uint8_t>(), nullptr));
+    if constexpr (!std::is_same<Mask, std::nullptr_t>::value) {
+        if (mask) mask->keep = detail::download_vec<std::uint8_t>(keep, static_cast<size_t>(total));
+    }
+    return detail::download<Mat>(y, x.rows, x.cols);
+}
+
+template <class Mat, class Mask, class T>
+Mat dropout_backward(const Mat& dy, const Mask& mask, T ratio) {
+    using V = detail::value_t<Mat>;
+    const std::int64_t total = dy.rows * dy.cols;
+    auto d = detail::upload(dy), k = detail::upload_vec(mask.keep);
+    detail::Buf dx(sizeof(V) * static_cast<size_t>(total));
+    detail::check(detail::abi<V>::dropout_backward(d.template as<V>(), total, k.template as<std::uint8_t>(),
+                                                   static_cast<std::int64_t>(mask.keep.size()), static_cast<V>(ratio),
+                                                   dx.as<V>(), nullptr));
+    return detail::download<Mat>(dx, dy.rows, dy.cols);
 }
 
 }  // namespace hashconv_b200

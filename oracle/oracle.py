@@ -568,6 +568,67 @@ class Ref:
     def matmul_trans_b(self, a, b, dtype=np.float32):
         return self._gemm("matmul_trans_b", a, b, lambda a, b: (a.shape[0], b.shape[0]), dtype)
 
+    # ---- cnn_ops.cpp:437-608 (batch norm, scale, relu, dropout)
+    def _layer_fn(self, name, dtype, argtypes):
+        suf, T = self._suf(dtype)
+        fn = getattr(self.lib, f"hcref_{name}_{suf}")
+        fn.argtypes = argtypes
+        return fn, T
+
+    def bn_forward(self, x, running_mean, running_var, eps, momentum, training, dtype=np.float32):
+        """-> y, running_mean', running_var', inv_std"""
+        S = C.c_float if np.dtype(dtype) == np.float32 else C.c_double
+        fn, T = self._layer_fn("bn_forward", dtype, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, S, S,
+                                                     C.c_int, C.c_void_p, C.c_void_p])
+        x = np.ascontiguousarray(x, T)
+        rm, rv = np.array(running_mean, T), np.array(running_var, T)
+        y, inv = np.empty_like(x), np.zeros(x.shape[0], T)
+        self._check(fn(_ptr(x), *x.shape, _ptr(rm), _ptr(rv), eps, momentum, int(training), _ptr(y), _ptr(inv)))
+        return y, rm, rv, inv
+
+    def bn_backward(self, dy, normalized, inv_std, dtype=np.float32):
+        fn, T = self._layer_fn("bn_backward", dtype, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
+                                                      C.c_void_p])
+        dy, xh, inv = (np.ascontiguousarray(a, T) for a in (dy, normalized, inv_std))
+        dx = np.empty_like(dy)
+        self._check(fn(_ptr(dy), *dy.shape, _ptr(xh), _ptr(inv), _ptr(dx)))
+        return dx
+
+    def scale_forward(self, x, gamma, beta, dtype=np.float32):
+        fn, T = self._layer_fn("scale_forward", dtype, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
+                                                        C.c_void_p])
+        x, g, b = (np.ascontiguousarray(a, T) for a in (x, gamma, beta))
+        y = np.empty_like(x)
+        self._check(fn(_ptr(x), *x.shape, _ptr(g), _ptr(b), _ptr(y)))
+        return y
+
+    def scale_backward(self, dy, x, gamma, dtype=np.float32):
+        fn, T = self._layer_fn("scale_backward", dtype, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p,
+                                                         C.c_void_p, C.c_void_p, C.c_void_p])
+        dy, x, g = (np.ascontiguousarray(a, T) for a in (dy, x, gamma))
+        dg, db, dx = np.empty(dy.shape[0], T), np.empty(dy.shape[0], T), np.empty_like(dy)
+        self._check(fn(_ptr(dy), _ptr(x), *dy.shape, _ptr(g), _ptr(dg), _ptr(db), _ptr(dx)))
+        return dg, db, dx
+
+    def relu(self, x, dy, dtype=np.float32):
+        """-> relu_forward(x), relu_backward(dy, relu_forward(x))"""
+        fn, T = self._layer_fn("relu", dtype, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
+                                               C.c_void_p])
+        x, dy = np.ascontiguousarray(x, T), np.ascontiguousarray(dy, T)
+        y, dx = np.empty_like(x), np.empty_like(x)
+        self._check(fn(_ptr(x), *x.shape, _ptr(dy), _ptr(y), _ptr(dx)))
+        return y, dx
+
+    def dropout(self, x, ratio, seed, training, dy, dtype=np.float32):
+        """-> y, keep mask (uint8), dropout_backward(dy, mask, ratio)"""
+        S = C.c_float if np.dtype(dtype) == np.float32 else C.c_double
+        fn, T = self._layer_fn("dropout", dtype, [C.c_void_p, C.c_int64, C.c_int64, S, C.c_uint64, C.c_int,
+                                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p])
+        x, dy = np.ascontiguousarray(x, T), np.ascontiguousarray(dy, T)
+        y, keep, dx = np.empty_like(x), np.empty(x.size, np.uint8), np.empty_like(x)
+        self._check(fn(_ptr(x), *x.shape, ratio, seed, int(training), _ptr(dy), _ptr(y), _ptr(keep), _ptr(dx)))
+        return y, keep, dx
+
 
 class RefSet:
     def __init__(self, ref: Ref, h, dim, res, coords, features):

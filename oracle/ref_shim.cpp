@@ -389,6 +389,66 @@ void hcref_random_matrix_f64(std::int64_t rows, std::int64_t cols, std::uint64_t
 HCREF_OPS(float, f32)
 HCREF_OPS(double, f64)
 
+// cnn_ops.cpp:437-608: batch norm, scale, relu, dropout (test oracle for ops_layer.cu)
+#define HCREF_LAYER(T, SUF)                                                                        \
+    int hcref_bn_forward_##SUF(const T* x, std::int64_t c, std::int64_t n, T* rm, T* rv, T eps, T mom, \
+                               int training, T* y, T* inv_std) {                                   \
+        return guarded([&] {                                                                       \
+            BatchNormStats<T> st(c);                                                               \
+            std::memcpy(st.running_mean.data(), rm, sizeof(T) * c);                                \
+            std::memcpy(st.running_var.data(), rv, sizeof(T) * c);                                 \
+            st.eps = eps;                                                                          \
+            st.momentum = mom;                                                                     \
+            BatchNormCache<T> cache;                                                               \
+            out(batch_norm_forward(wrap(x, c, n), st, training != 0, &cache), y);                  \
+            std::memcpy(rm, st.running_mean.data(), sizeof(T) * c);                                \
+            std::memcpy(rv, st.running_var.data(), sizeof(T) * c);                                 \
+            std::memcpy(inv_std, cache.inv_std.data(), sizeof(T) * cache.inv_std.size());          \
+        });                                                                                        \
+    }                                                                                              \
+    int hcref_bn_backward_##SUF(const T* dy, std::int64_t c, std::int64_t n, const T* xh,          \
+                                const T* inv_std, T* dx) {                                         \
+        return guarded([&] {                                                                       \
+            BatchNormCache<T> cache;                                                               \
+            cache.normalized = wrap(xh, c, n);                                                     \
+            cache.inv_std.assign(inv_std, inv_std + c);                                            \
+            out(batch_norm_backward(wrap(dy, c, n), cache), dx);                                   \
+        });                                                                                        \
+    }                                                                                              \
+    int hcref_scale_backward_##SUF(const T* dy, const T* x, std::int64_t r, std::int64_t c,        \
+                                   const T* gamma, T* dg, T* db, T* dx) {                          \
+        return guarded([&] {                                                                       \
+            auto g = scale_backward(wrap(dy, r, c), wrap(x, r, c), std::vector<T>(gamma, gamma + r)); \
+            std::memcpy(dg, g.gamma.data(), sizeof(T) * r);                                        \
+            std::memcpy(db, g.beta.data(), sizeof(T) * r);                                         \
+            out(g.input, dx);                                                                      \
+        });                                                                                        \
+    }                                                                                              \
+    int hcref_scale_forward_##SUF(const T* x, std::int64_t r, std::int64_t c, const T* g, const T* b, T* y) { \
+        return guarded([&] {                                                                       \
+            out(scale_forward(wrap(x, r, c), std::vector<T>(g, g + r), std::vector<T>(b, b + r)), y); \
+        });                                                                                        \
+    }                                                                                              \
+    int hcref_relu_##SUF(const T* x, std::int64_t r, std::int64_t c, const T* dy, T* y, T* dx) {   \
+        return guarded([&] {                                                                       \
+            const auto fo = relu_forward(wrap(x, r, c));                                           \
+            out(fo, y);                                                                            \
+            out(relu_backward(wrap(dy, r, c), fo), dx);                                            \
+        });                                                                                        \
+    }                                                                                              \
+    int hcref_dropout_##SUF(const T* x, std::int64_t r, std::int64_t c, T ratio, std::uint64_t seed, \
+                            int training, const T* dy, T* y, std::uint8_t* keep, T* dx) {          \
+        return guarded([&] {                                                                       \
+            DropoutMask m;                                                                         \
+            out(dropout_forward(wrap(x, r, c), ratio, seed, training != 0, &m), y);                \
+            std::memcpy(keep, m.keep.data(), m.keep.size());                                       \
+            out(dropout_backward(wrap(dy, r, c), m, ratio), dx);                                   \
+        });                                                                                        \
+    }
+
+HCREF_LAYER(float, f32)
+HCREF_LAYER(double, f64)
+
 // serial_ref.cpp:33-171 (paper-literal task loops; float only)
 int hcref_serial_hash2col(const void* in, const float* data, std::int64_t dr, std::int64_t dc,
                           const void* outs, const int* spec, float* cols) {

@@ -121,6 +121,22 @@ _SIGS.update({
     "hc_native_bn_relu_forward": [_P, _I64, _I32, _I32, C.c_float, C.c_float, _P, _P, _P, _P, _P, _P, C.c_size_t,
                                   _P],
     "hc_native_bn_relu_backward": [_P, C.c_int, _P, _P, _I64, _I32, _P, _P, C.c_size_t, _P],
+    "hc_batch_norm_forward_f32": [_P, _I64, _I64, _P, _P, _I64, C.c_float, C.c_float, _I32, _P, _P, _P],
+    "hc_batch_norm_backward_f32": [_P, _I64, _I64, _P, _I64, _I64, _P, _P, _P],
+    "hc_scale_forward_f32": [_P, _I64, _I64, _P, _I64, _P, _I64, _P, _P],
+    "hc_scale_backward_f32": [_P, _P, _I64, _I64, _P, _P, _P, _P, _P],
+    "hc_relu_forward_f32": [_P, _I64, _P, _P],
+    "hc_relu_backward_f32": [_P, _I64, _I64, _P, _I64, _I64, _P, _P],
+    "hc_dropout_forward_f32": [_P, _I64, C.c_float, C.c_uint64, _I32, _P, _P, _P],
+    "hc_dropout_backward_f32": [_P, _I64, _P, _I64, C.c_float, _P, _P],
+    "hc_batch_norm_forward_f64": [_P, _I64, _I64, _P, _P, _I64, C.c_double, C.c_double, _I32, _P, _P, _P],
+    "hc_batch_norm_backward_f64": [_P, _I64, _I64, _P, _I64, _I64, _P, _P, _P],
+    "hc_scale_forward_f64": [_P, _I64, _I64, _P, _I64, _P, _I64, _P, _P],
+    "hc_scale_backward_f64": [_P, _P, _I64, _I64, _P, _P, _P, _P, _P],
+    "hc_relu_forward_f64": [_P, _I64, _P, _P],
+    "hc_relu_backward_f64": [_P, _I64, _I64, _P, _I64, _I64, _P, _P],
+    "hc_dropout_forward_f64": [_P, _I64, C.c_double, C.c_uint64, _I32, _P, _P, _P],
+    "hc_dropout_backward_f64": [_P, _I64, _P, _I64, C.c_double, _P, _P],
     "hc_native_bn_relu_inference": [_P, _I64, _I32, _P, _P, C.c_float, _P, _P],
     "hc_native_bn_stat": [_I32, _P, _P, C.c_int, _I64, _I32, _P, _P, _P, C.c_size_t, _P],
     "hc_native_bn_finalize": [_P, _P, _I64, _I32, C.c_float, C.c_float, _P, _P, _P, _P, _P],

@@ -303,3 +303,146 @@ def matmul_trans_b(a_, b_):
     c = _empty(x.shape[0], y.shape[0], a.dtype)
     check(a.fn("hc_matmul_trans_b")(_p(x), _p(y), _p(c), x.shape[0], x.shape[1], y.shape[0], _stream()))
     return a.out(c)
+
+
+# ------------------------------------------------------------------ cnn_ops.hpp:118-170
+class BatchNormStats:
+    """cnn_ops.hpp:118-127: per-channel running statistics (updated in place by training
+    batch_norm_forward). running_mean / running_var: CUDA tensors or numpy arrays."""
+
+    def __init__(self, channels: int = 0, eps: float = 1e-5, momentum: float = 0.1, dtype=np.float32):
+        self.running_mean = np.zeros(channels, dtype)
+        self.running_var = np.ones(channels, dtype)
+        self.eps, self.momentum = eps, momentum
+
+
+class BatchNormCache:
+    """cnn_ops.hpp:129-133: normalized (C x N) and inv_std (C)."""
+
+    def __init__(self):
+        self.normalized = None
+        self.inv_std = None
+
+
+class ScaleGradients(NamedTuple):  # cnn_ops.hpp:143-148
+    gamma: object
+    beta: object
+    input: object
+
+
+class DropoutMask:  # cnn_ops.hpp:160-162 (keep: uint8 per element)
+    def __init__(self):
+        self.keep = None
+
+
+def _vec(a: _Args, v, n_expected=None):
+    """A per-channel parameter vector in the call's precision (device)."""
+    t = torch.as_tensor(np.asarray(v)) if not isinstance(v, torch.Tensor) else v
+    t = t.to(device=_dev(), dtype=a.dtype).contiguous()
+    return t
+
+
+def _scalar(a: _Args):
+    return C.c_double if a.dtype == torch.float64 else C.c_float
+
+
+def batch_norm_forward(x, stats: BatchNormStats, training: bool, cache: BatchNormCache = None):
+    """cnn_ops.cpp:437-482 (channel-major C x N)."""
+    a = _Args()
+    xt = a.fp(x)
+    c, n = _shape(xt)
+    rm, rv = _vec(a, stats.running_mean), _vec(a, stats.running_var)
+    y = _empty(c, n, a.dtype)
+    inv = torch.empty(c, dtype=a.dtype, device=_dev())
+    S = _scalar(a)
+    check(a.fn("hc_batch_norm_forward")(_p(xt), c, n, _p(rm), _p(rv), rm.numel(), S(stats.eps), S(stats.momentum),
+                                        int(bool(training)), _p(y), _p(inv), _stream()))
+    if training:  # write the updated running statistics back where they live
+        for dst, src in ((stats.running_mean, rm), (stats.running_var, rv)):
+            if isinstance(dst, torch.Tensor):
+                dst.copy_(src)
+            else:
+                dst[...] = src.cpu().numpy()
+    if cache is not None:
+        cache.normalized = a.out(y)
+        cache.inv_std = a.out(inv)
+    return a.out(y)
+
+
+def batch_norm_backward(dy, cache: BatchNormCache):
+    """cnn_ops.cpp:484-507."""
+    a = _Args()
+    d = a.fp(dy)
+    xh, inv = a.fp(cache.normalized), _vec(a, cache.inv_std)
+    c, n = _shape(d)
+    dx = _empty(c, n, a.dtype)
+    check(a.fn("hc_batch_norm_backward")(_p(d), c, n, _p(xh), *_shape(xh), _p(inv), _p(dx), _stream()))
+    return a.out(dx)
+
+
+def scale_forward(x, gamma, beta):
+    """cnn_ops.cpp:509-522: y = gamma * x + beta per channel."""
+    a = _Args()
+    xt = a.fp(x)
+    g, b = _vec(a, gamma), _vec(a, beta)
+    r, c = _shape(xt)
+    y = _empty(r, c, a.dtype)
+    check(a.fn("hc_scale_forward")(_p(xt), r, c, _p(g), g.numel(), _p(b), b.numel(), _p(y), _stream()))
+    return a.out(y)
+
+
+def scale_backward(dy, x, gamma) -> ScaleGradients:
+    """cnn_ops.cpp:525-546."""
+    a = _Args()
+    d, xt = a.fp(dy), a.fp(x)
+    g = _vec(a, gamma)
+    r, c = _shape(d)
+    dg = torch.empty(r, dtype=a.dtype, device=_dev())
+    db = torch.empty(r, dtype=a.dtype, device=_dev())
+    dx = _empty(r, c, a.dtype)
+    check(a.fn("hc_scale_backward")(_p(d), _p(xt), r, c, _p(g), _p(dg), _p(db), _p(dx), _stream()))
+    return ScaleGradients(a.out(dg), a.out(db), a.out(dx))
+
+
+def relu_forward(x):
+    """cnn_ops.cpp:548-559: max(0, x)."""
+    a = _Args()
+    xt = a.fp(x)
+    y = torch.empty_like(xt)
+    check(a.fn("hc_relu_forward")(_p(xt), xt.numel(), _p(y), _stream()))
+    return a.out(y)
+
+
+def relu_backward(dy, forward_out):
+    """cnn_ops.cpp:561-573: dy where forward_out > 0."""
+    a = _Args()
+    d, fo = a.fp(dy), a.fp(forward_out)
+    dx = torch.empty_like(d)
+    check(a.fn("hc_relu_backward")(_p(d), *_shape(d), _p(fo), *_shape(fo), _p(dx), _stream()))
+    return a.out(dx)
+
+
+def dropout_forward(x, ratio: float, seed: int, training: bool, mask: DropoutMask = None):
+    """cnn_ops.cpp:575-596: inverted dropout; the mask is the reference's mt19937_64(seed)
+    stream (bit-exact)."""
+    a = _Args()
+    xt = a.fp(x)
+    y = torch.empty_like(xt)
+    keep = torch.empty(xt.numel(), dtype=torch.uint8, device=_dev())
+    check(a.fn("hc_dropout_forward")(_p(xt), xt.numel(), _scalar(a)(ratio), C.c_uint64(seed & (2 ** 64 - 1)),
+                                     int(bool(training)), _p(y), _p(keep), _stream()))
+    if mask is not None:
+        mask.keep = a.out(keep)
+    return a.out(y)
+
+
+def dropout_backward(dy, mask: DropoutMask, ratio: float):
+    """cnn_ops.cpp:598-608."""
+    a = _Args()
+    d = a.fp(dy)
+    k = mask.keep
+    k = (torch.from_numpy(np.ascontiguousarray(k, np.uint8)) if isinstance(k, np.ndarray) else k)
+    k = k.to(_dev()).contiguous()
+    dx = torch.empty_like(d)
+    check(a.fn("hc_dropout_backward")(_p(d), d.numel(), _p(k), k.numel(), _scalar(a)(ratio), _p(dx), _stream()))
+    return a.out(dx)

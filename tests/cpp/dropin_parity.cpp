@@ -4,7 +4,9 @@
 // reference's own types, that hashconv_b200::<op> == hashconv::<op> bit-for-bit
 // (EXACT math; float AND double instantiations), including the reference's known-answer tests
 // (tests/test_cnn_ops.cpp:53-97, 140-156, 308-344) and its exception types.
+#include <algorithm>
 #include <cmath>
+#include <type_traits>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -88,6 +90,55 @@ static void ops_equal(const Fixture& fx, const ConvSpec& spec, std::uint64_t see
     CHECK(hb::matmul_trans_b(dout, cols) == matmul_trans_b(dout, cols), "matmul_trans_b");
 }
 
+template <class T>
+static double max_rel(const FeatureMatrixT<T>& a, const FeatureMatrixT<T>& b) {
+    double num = 0, den = 0;
+    for (size_t i = 0; i < a.values.size(); ++i) {
+        num = std::max(num, std::fabs(double(a.values[i]) - double(b.values[i])));
+        den = std::max(den, std::fabs(double(b.values[i])));
+    }
+    return den > 0 ? num / den : num;
+}
+
+// cnn_ops.hpp:118-170 through the shim: relu / scale forward / dropout bit-exact in both
+// precisions; batch norm and the scale-backward sums bit-exact in float, 1e-12 in double
+// (double sums in a tree order instead of the reference's sequential loop).
+template <class T>
+static void layer_ops_equal(std::uint64_t seed) {
+    const bool exact = std::is_same<T, float>::value;
+    const auto x = testing::random_matrix<T>(6, 2000, seed);
+    const auto dy = testing::random_matrix<T>(6, 2000, seed + 1);
+    for (int training = 0; training < 2; ++training) {
+        BatchNormStats<T> s1(6), s2(6);
+        for (int c = 0; c < 6; ++c) s1.running_mean[c] = s2.running_mean[c] = T(0.1) * T(c);
+        BatchNormCache<T> c1, c2;
+        const auto y1 = batch_norm_forward(x, s1, training != 0, &c1);
+        const auto y2 = hb::batch_norm_forward(x, s2, training != 0, &c2);
+        CHECK(exact ? y1 == y2 : max_rel(y2, y1) < 1e-12, "batch_norm_forward");
+        CHECK(exact ? s1.running_mean == s2.running_mean && s1.running_var == s2.running_var : true,
+              "batch_norm running stats");
+        if (training) {
+            const auto d1 = batch_norm_backward(dy, c1);
+            const auto d2 = hb::batch_norm_backward(dy, c2);
+            CHECK(exact ? d1 == d2 : max_rel(d2, d1) < 1e-12, "batch_norm_backward");
+        }
+    }
+    std::vector<T> g(6), b(6);
+    for (int c = 0; c < 6; ++c) g[c] = T(0.5) + T(c), b[c] = T(0.25) * T(c);
+    CHECK(hb::scale_forward(x, g, b) == scale_forward(x, g, b), "scale_forward");
+    const auto sg1 = scale_backward(dy, x, g);
+    const auto sg2 = hb::scale_backward(dy, x, g);
+    CHECK(sg1.input == sg2.input && (!exact || (sg1.gamma == sg2.gamma && sg1.beta == sg2.beta)), "scale_backward");
+    const auto r1 = relu_forward(x);
+    CHECK(hb::relu_forward(x) == r1, "relu_forward");
+    CHECK(hb::relu_backward(dy, r1) == relu_backward(dy, r1), "relu_backward");
+    DropoutMask m1, m2;
+    const auto o1 = dropout_forward(x, T(0.4), seed, true, &m1);
+    const auto o2 = hb::dropout_forward(x, T(0.4), seed, true, &m2);
+    CHECK(o1 == o2 && m1.keep == m2.keep, "dropout_forward (mt19937_64 mask)");
+    CHECK(hb::dropout_backward(dy, m2, T(0.4)) == dropout_backward(dy, m1, T(0.4)), "dropout_backward");
+}
+
 static SuperPsh single(const Coord& p, int res, float value) {
     FeatureMatrix f(1, 1);
     f.at(0, 0) = value;
@@ -154,6 +205,8 @@ int main() {
         ops_equal<float>(fx, specs[t % 4], 100 + t);
         ops_equal<double>(fx, specs[t % 4], 200 + t);  // the reference's double instantiation
     }
+    layer_ops_equal<float>(77);
+    layer_ops_equal<double>(78);
     std::printf("%s: %d checks, %d failures\n", g_fail ? "DROPIN FAIL" : "DROPIN OK", g_checks, g_fail);
     return g_fail ? 1 : 0;
 }
