@@ -59,7 +59,10 @@ struct GCfg {
     static constexpr int A_BYTES = BM * 128;
     static constexpr int B_BYTES = BN * 128;
     static constexpr int RAW = A_BYTES + B_BYTES;
-    static constexpr int STAGE = RAW * (SPLIT == 3 ? 2 : 1);  // raw (-> hi in place) + lo
+    static constexpr int STAGE = RAW * (SPLIT >= 3 ? 2 : 1);  // raw (= hi) + lo
+    // SPLIT 5: only the A tile is split in shared memory; B's lo plane arrives by TMA
+    static constexpr int CVT = SPLIT == 5 ? A_BYTES : RAW;        // bytes the split warps convert
+    static constexpr int TX = SPLIT == 5 ? RAW + B_BYTES : RAW;   // TMA bytes per stage
     // two CTAs per SM when two rings of >= 2 stages fit, else one CTA with a deeper ring
     static constexpr int BUDGET = 2 * STAGE <= 104 * 1024 ? 104 * 1024 : 200 * 1024;
     static constexpr int S = BUDGET / STAGE < 8 ? BUDGET / STAGE : 8;
@@ -106,6 +109,7 @@ __device__ __forceinline__ Tile tile_at(long long t, long long tiles_n, long lon
 template <bool AMN, bool BMN, int BN, int SPLIT>
 __global__ void __launch_bounds__(kThreads, GCfg<BN, SPLIT>::CTAS) k_gemm_tf32(const __grid_constant__ CUtensorMap amap,
                                                         const __grid_constant__ CUtensorMap bmap,
+                                                        const __grid_constant__ CUtensorMap blomap,
                                                         float* __restrict__ C, long long ra, long long cb, long long K,
                                                         long long k_chunk, long long split_stride, long long tiles_n,
                                                         long long tiles_m, long long ntiles) {
@@ -146,7 +150,7 @@ __global__ void __launch_bounds__(kThreads, GCfg<BN, SPLIT>::CTAS) k_gemm_tf32(c
                 const Tile T = tile_at(t, tiles_n, tiles_m, BN, K, k_chunk);
                 for (int i = 0; i < T.nk; ++i) {
                     mbar_wait(empty0 + 8 * s, ph ^ 1);
-                    mbar_arrive_expect_tx(full0 + 8 * s, Cfg::RAW);
+                    mbar_arrive_expect_tx(full0 + 8 * s, Cfg::TX);
                     const int k0 = (int)((T.kb + (long long)i * k_chunk) * BKF);
                     const uint32_t a = sbase + s * Cfg::STAGE, b = a + Cfg::A_BYTES;
                     if (AMN) {
@@ -162,6 +166,10 @@ __global__ void __launch_bounds__(kThreads, GCfg<BN, SPLIT>::CTAS) k_gemm_tf32(c
                             tma_load2d(b + j * 4096, &bmap, (int)T.n0 + 32 * j, k0, full0 + 8 * s);
                     } else {
                         tma_load2d(b, &bmap, k0, (int)T.n0, full0 + 8 * s);
+                    }
+                    if constexpr (SPLIT == 5) {  // B's pre-split lo plane into the lo region
+                        static_assert(!BMN, "SPLIT 5 is for a K-major B operand");
+                        tma_load2d(b + Cfg::RAW, &blomap, k0, (int)T.n0, full0 + 8 * s);
                     }
                     if (++s == S) {
                         s = 0;
@@ -193,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, GCfg<BN, SPLIT>::CTAS) k_gemm_tf32(c
                     if (blk >= 2) mbar_wait(tempty0 + 8 * (blk & 1), ((blk >> 1) - 1) & 1);  // drained
                 }
                 const int buf = blk & 1;
-                mbar_wait(SPLIT == 3 ? cvt0 + 8 * s : full0 + 8 * s, ph);
+                mbar_wait(SPLIT >= 3 ? cvt0 + 8 * s : full0 + 8 * s, ph);
                 tc_fence_after();
                 if (elect_one()) {
                     const uint32_t d = tmem + buf * BN;
@@ -201,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, GCfg<BN, SPLIT>::CTAS) k_gemm_tf32(c
 #pragma unroll
                     for (int kk = 0; kk < BKF / 8; ++kk) {
                         const uint64_t a = ad + so + A_STEP * kk, b = bd + so + B_STEP * kk;
-                        if (SPLIT == 3) {
+                        if (SPLIT >= 3) {
                             mma_tf32(d, a + LO, b, idesc, (in_blk | kk) != 0);  // lo_a * hi_b
                             mma_tf32(d, a, b + LO, idesc, 1);                   // hi_a * lo_b
                             mma_tf32(d, a, b, idesc, 1);                        // hi_a * hi_b
@@ -266,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, GCfg<BN, SPLIT>::CTAS) k_gemm_tf32(c
             }
         };
         int blk = -1;
-        if constexpr (SPLIT == 3) {
+        if constexpr (SPLIT >= 3) {
             // convert stage by stage; once the first stage of block b+1 is converted, drain
             // block b (the MMA warp can finish b without more conversions). One drain call
             // site, so the BN-float accumulator is inlined once.
@@ -295,7 +303,7 @@ __global__ void __launch_bounds__(kThreads, GCfg<BN, SPLIT>::CTAS) k_gemm_tf32(c
                     mbar_wait(full0 + 8 * s, ph);
                     const uint32_t raw = sbase + s * Cfg::STAGE;
 #pragma unroll 4
-                    for (int e = t_id; e < Cfg::RAW / 16; e += kEpi) {
+                    for (int e = t_id; e < Cfg::CVT / 16; e += kEpi) {
                         const int4 v = ld_shared_v4(raw + 16 * e);
                         uint4 h, l;
                         split_tf32((uint32_t)v.x, h.x, l.x);
@@ -391,7 +399,8 @@ int sm_count() {
 // opB: MMA-B source. MN-major: X[K][ra] (inner = ra), K-major: X[ra][K] (inner = K).
 // opA: MMA-A source. MN-major: X[K][cb] (inner = cb), K-major: X[cb][K] (inner = K).
 template <bool AMN, bool BMN, int BN, int SPLIT>
-void launch(const float* asrc, const float* bsrc, float* C, long long ra, long long cb, long long K, cudaStream_t s) {
+void launch(const float* asrc, const float* bsrc, float* C, long long ra, long long cb, long long K, cudaStream_t s,
+            const float* blo = nullptr) {
     using Cfg = GCfg<BN, SPLIT>;
     auto kern = k_gemm_tf32<AMN, BMN, BN, SPLIT>;
     static bool attr = false;
@@ -401,6 +410,7 @@ void launch(const float* asrc, const float* bsrc, float* C, long long ra, long l
     }
     const CUtensorMap am = AMN ? fmap2d(asrc, cb, K, 32, 32, true) : fmap2d(asrc, K, cb, 32, BM, false);
     const CUtensorMap bm = BMN ? fmap2d(bsrc, ra, K, 32, 32, true) : fmap2d(bsrc, K, ra, 32, BN, false);
+    const CUtensorMap blm = SPLIT == 5 ? fmap2d(blo, K, ra, 32, BN, false) : bm;
     const long long tiles_m = (cb + BM - 1) / BM, tiles_n = (ra + BN - 1) / BN, tiles = tiles_m * tiles_n;
     const long long slots = (long long)Cfg::CTAS * sm_count();
     // long-K products with few output tiles (dW: K = voxels): split K over CTAs to fill one
@@ -420,21 +430,50 @@ void launch(const float* asrc, const float* bsrc, float* C, long long ra, long l
     const bool use_persist = persist == 1 || (persist != 0 && !long_tiles);
     const unsigned grid = (unsigned)(use_persist ? std::min<long long>(ntiles, slots) : ntiles);
     if (splits == 1) {
-        kern<<<grid, kThreads, Cfg::SMEM, s>>>(am, bm, C, ra, cb, K, splits, 0, tiles_n, tiles_m, ntiles);
+        kern<<<grid, kThreads, Cfg::SMEM, s>>>(am, bm, blm, C, ra, cb, K, splits, 0, tiles_n, tiles_m, ntiles);
         launched("gemm (tcgen05 tf32)");
         return;
     }
     const long long mn = ra * cb;  // % 4 == 0: cb % 4 == 0 by eligibility
     Scratch part(sizeof(float) * mn * splits, s);
-    kern<<<grid, kThreads, Cfg::SMEM, s>>>(am, bm, part.as<float>(), ra, cb, K, splits, mn, tiles_n, tiles_m, ntiles);
+    kern<<<grid, kThreads, Cfg::SMEM, s>>>(am, bm, blm, part.as<float>(), ra, cb, K, splits, mn, tiles_n, tiles_m,
+                                           ntiles);
     k_reduce_splits4<<<grid_for(mn / 4, 256), 256, 0, s>>>(part.as<const float4>(), reinterpret_cast<float4*>(C),
                                                           mn / 4, (int)splits);
     launched("gemm (tcgen05 tf32, split-K)", 2);
 }
 
+// lo = x - tf32_trunc(x) elementwise (the small operand's pre-split plane for SPLIT 5)
+__global__ void k_tf32_lo(const uint4* __restrict__ x, uint4* __restrict__ lo, long long n4) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n4) return;
+    const uint4 v = x[i];
+    uint4 h, l;
+    split_tf32(v.x, h.x, l.x);
+    split_tf32(v.y, h.y, l.y);
+    split_tf32(v.z, h.z, l.z);
+    split_tf32(v.w, h.w, l.w);
+    lo[i] = l;
+}
+
 template <bool AMN, bool BMN>
 void dispatch(const float* asrc, const float* bsrc, float* C, long long ra, long long cb, long long K, bool three,
               cudaStream_t s) {
+    static const int presplit = [] {
+        const char* e = std::getenv("HCB_TC_PRESPLIT_B");  // A/B: 0 splits B in shared memory too
+        return e ? std::atoi(e) : 1;
+    }();
+    // matmul (conv forward): B = the weights, tiny next to the column matrix -> split it once
+    // in HBM and stream its lo plane by TMA; the split warps then only convert A
+    if constexpr (AMN && !BMN) {
+        if (three && presplit && ra > 32) {
+            const long long n = ra * K;  // K % 4 == 0 by eligibility
+            Scratch lo(sizeof(float) * n, s);
+            k_tf32_lo<<<grid_for(n / 4, 256), 256, 0, s>>>(reinterpret_cast<const uint4*>(bsrc), lo.as<uint4>(), n / 4);
+            launched("tf32 lo plane (weights)");
+            return launch<AMN, BMN, 64, 5>(asrc, bsrc, C, ra, cb, K, s, lo.as<float>());
+        }
+    }
     if (ra <= 32) {
         if (three) return launch<AMN, BMN, 32, 3>(asrc, bsrc, C, ra, cb, K, s);
         return launch<AMN, BMN, 32, 1>(asrc, bsrc, C, ra, cb, K, s);
