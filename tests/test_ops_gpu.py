@@ -354,3 +354,43 @@ def test_full_size_field_map_symmetry(shell256):
     back = m.clamp(min=0)[hit], (26 - t)[hit]
     assert torch.equal(m[back[0], back[1]], o[hit])
     assert torch.equal(m[:, 13], torch.arange(n, device="cuda"))  # centre tap is the voxel itself
+
+
+# ---------------------------------------------------------------- dense-oracle equivalence
+def test_hash_conv_equals_dense_conv3d(cuda):
+    """test_cnn_ops.cpp:99-117 in spirit, independent of every oracle in this repo: on random
+    sparse sets the hash convolution equals a dense 3-D cross-correlation (zero padding) of the
+    densified grid at the occupied voxels — fp64 through the reference-layout path (<= 1e-12)
+    and bf16-quantised operands through the native tcgen05 path (fp32 accumulation, <= 1e-5)."""
+    import torch.nn.functional as F
+    from paper_1803_11385_b200 import conv as nconv
+    res, cin, cout = 16, 8, 16
+    rng = np.random.default_rng(21)
+    levels, coords_all = [], []
+    for k in range(2):
+        flat = rng.choice(res ** 3, size=300 + 150 * k, replace=False)
+        c = np.stack([flat % res, (flat // res) % res, flat // (res * res)], 1).astype(np.int32)
+        levels.append(PshLevel.build(VoxelSet.make(3, res, c, np.zeros((1, len(c)), np.float32)), 5 + k))
+        coords_all.append(c)
+    s = SuperPsh.from_levels(levels)
+    n = s.total_columns()
+    x = rng.uniform(-1, 1, (cin, n))
+    w = rng.uniform(-1, 1, (cout, cin * 27))
+    spec = ConvSpec(3, 1, 0, cin, cout)
+    y_hash = _np(ops.conv_forward(s, _dev(x), s, _dev(w), spec))  # fp64 path
+    xb = torch.from_numpy(x).to(torch.bfloat16).double().numpy()
+    wb = torch.from_numpy(w).to(torch.bfloat16).double().numpy()
+    fm = nconv.field_map_native(s, s, spec)
+    y_nat = nconv.gather_gemm(fm, _dev(xb.T.copy()).to(torch.bfloat16), nconv.pack_weights(_dev(wb).float(), cout, cin, 27),
+                              cout, torch.float32).double().cpu().numpy().T
+    for k, c in enumerate(coords_all):
+        q = np.concatenate([np.full((len(c), 1), k + 1), c], 1).astype(np.int32)
+        cols = _np(ops.locate(s, _dev(q))).astype(np.int64)
+        assert (cols >= 0).all()
+        for xs, ws, got, tol in ((x, w, y_hash, 1e-12), (xb, wb, y_nat, 1e-5)):
+            grid = torch.zeros((1, cin, res, res, res), dtype=torch.float64)
+            grid[0, :, c[:, 2], c[:, 1], c[:, 0]] = torch.from_numpy(xs[:, cols])
+            dense = F.conv3d(grid, torch.from_numpy(ws).view(cout, cin, 3, 3, 3), padding=1)[0]
+            want = dense[:, c[:, 2], c[:, 1], c[:, 0]].numpy()
+            err = np.linalg.norm(got[:, cols] - want) / np.linalg.norm(want)
+            assert err <= tol, (k, tol, err)
