@@ -217,6 +217,8 @@ struct MaxPoolResult {
 
 // Math mode of the contraction: exact (reference order, bit-identical) or fast.
 inline void set_fast_math(bool fast) { detail::check(hc_set_math(fast ? HC_MATH_FAST : HC_MATH_EXACT)); }
+// Any hc_math mode (EXACT / FAST = 3xTF32 / TF32), thread-local like the C ABI.
+inline void set_math(hc_math mode) { detail::check(hc_set_math(mode)); }
 
 // cnn_ops.cpp:123-158
 template <class Super, class Mat, class Spec>
