@@ -394,3 +394,77 @@ def test_hash_conv_equals_dense_conv3d(cuda):
             want = dense[:, c[:, 2], c[:, 1], c[:, 0]].numpy()
             err = np.linalg.norm(got[:, cols] - want) / np.linalg.norm(want)
             assert err <= tol, (k, tol, err)
+
+
+# ---------------------------------------------------------------- 2-D structures (dim = 2)
+def _random_pair_2d(res, models, seed, n_lo=60, n_hi=200):
+    from paper_1803_11385_b200.psh import mix_seed
+    rng = np.random.default_rng(seed)
+    fine, coarse = [], []
+    for k in range(models):
+        n = int(rng.integers(n_lo, n_hi + 1))
+        flat = rng.choice(res * res, size=n, replace=False)
+        coords = np.zeros((n, 3), np.int32)
+        coords[:, 0], coords[:, 1] = flat % res, flat // res
+        s = VoxelSet.make(2, res, coords, rng.uniform(-1, 1, (3, n)).astype(np.float32))
+        fine.append(PshLevel.build(s, mix_seed(seed, 20 + k)))
+        coarse.append(PshLevel.build(s.coarsen(), mix_seed(seed, 20 + k)))
+    return fine, coarse
+
+
+@pytest.mark.parametrize("spec", [(3, 1, 0), (2, 2, 0), (3, 2, 0), (5, 1, 0)])
+def test_2d_structures_vs_oracle(cuda, restated, spec):
+    """The reference's operators take dim-2 structures too (F^2 fields, psh.hpp:21-35):
+    every reference-layout operator on random 2-D batches, bit-exact vs the oracle."""
+    f, c = _random_pair_2d(32, 3, seed=hash(spec) & 0xFFF)
+    fa, ca = levels_to_arrays(f), levels_to_arrays(c)
+    fine, coarse = SuperPsh.from_levels(f), SuperPsh.from_levels(c)
+    assert fine.dim == 2
+    sp = ConvSpec(*spec, 4, 6)
+    out_s, out_a = (fine, fa) if sp.stride == 1 else (coarse, ca)
+    rng = np.random.default_rng(5)
+    fd = sp.kernel ** 2
+    data = rng.uniform(-1, 1, (4, fa.total_columns())).astype(np.float32)
+    w = rng.uniform(-1, 1, (6, 4 * fd)).astype(np.float32)
+    dout = rng.uniform(-1, 1, (6, out_a.total_columns())).astype(np.float32)
+    assert np.array_equal(_np(ops.field_map(fine, out_s, sp)).astype(np.int64), restated.field_map(fa, out_a, sp))
+    ocols = restated.hash2col(fa, data, out_a, sp)
+    cols = ops.hash2col(fine, _dev(data), out_s, sp)
+    assert np.array_equal(_np(cols), ocols)
+    assert np.array_equal(_np(ops.conv_forward(fine, _dev(data), out_s, _dev(w), sp)), restated.matmul(w, ocols))
+    g = ops.conv_backward(_dev(dout), _dev(w), cols, fine, out_s, sp)
+    odw, odx = restated.conv_backward(dout, w, ocols, fa, out_a, sp)
+    assert np.array_equal(_np(g.weights), odw) and np.array_equal(_np(g.input), odx)
+    if sp.stride > 1:
+        psp = ConvSpec(sp.kernel, sp.stride, sp.pad, 4, 4)
+        mp = ops.max_pool(fine, _dev(data), coarse, psp)
+        om, osw = restated.max_pool(fa, data, ca, psp)
+        assert np.array_equal(_np(mp.output), om) and np.array_equal(_np(mp.switches), osw)
+        assert np.array_equal(_np(ops.max_unpool(mp.output, mp.switches, fine, coarse, psp)),
+                              restated.max_unpool(om, osw, fa, ca, psp))
+        assert np.array_equal(_np(ops.avg_pool(fine, _dev(data), coarse, psp)), restated.avg_pool(fa, data, ca, psp))
+
+
+def test_2d_native_conv_vs_double(cuda):
+    """The fused tcgen05 path on a 2-D batch (9 taps): forward, input gradient and weight
+    gradient against float64 on the same bf16-quantised operands."""
+    from paper_1803_11385_b200 import conv as nconv
+    f, _ = _random_pair_2d(64, 4, seed=9, n_lo=400, n_hi=900)
+    s = SuperPsh.from_levels(f)
+    n, cin, cout = s.total_columns(), 32, 64
+    spec = ConvSpec(3, 1, 0, cin, cout)
+    fm = nconv.field_map_native(s, s, spec)
+    rm = ops.field_map(s, s, spec)  # row-major int32 [n][9]
+    assert rm.shape == (n, 9)
+    g = torch.Generator(device="cuda").manual_seed(4)
+    x = (torch.rand((n, cin), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    w = (torch.rand((cout, cin * 9), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16).float()
+    dy = (torch.rand((n, cout), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    xd = torch.cat([x.double(), torch.zeros((1, cin), dtype=torch.float64, device="cuda")])
+    idx = torch.where(rm >= 0, rm.long(), torch.full_like(rm.long(), n))
+    want = torch.einsum("ntc,oct->no", xd[idx], w.double().view(cout, cin, 9))
+    y = nconv.gather_gemm(fm, x, nconv.pack_weights(w, cout, cin, 9), cout, torch.float32)
+    assert float((y.double() - want).norm() / want.norm()) <= 1e-5
+    dw = nconv.conv_dw(fm, x, dy)
+    dw_want = torch.einsum("no,ntc->oct", dy.double(), xd[idx]).reshape(cout, cin * 9)
+    assert float((dw.double() - dw_want).norm() / dw_want.norm()) <= 5e-5
