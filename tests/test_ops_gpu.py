@@ -468,3 +468,23 @@ def test_2d_native_conv_vs_double(cuda):
     dw = nconv.conv_dw(fm, x, dy)
     dw_want = torch.einsum("no,ntc->oct", dy.double(), xd[idx]).reshape(cout, cin * 9)
     assert float((dw.double() - dw_want).norm() / dw_want.norm()) <= 5e-5
+
+
+def test_full_size_int64_index_paths(shell256):
+    """C = 64 at BASELINE config 4 size: the column matrix has 27 * 64 * 1,826,368 = 3.2e9
+    elements (> 2^31), so hash2col's and the contraction's 64-bit index math is exercised.
+    The centre-tap identity kernel must reproduce the input exactly (EXACT math: the zero
+    weights are skipped like gemm.cpp:21) and to fp32 accuracy through 3xTF32 (FAST)."""
+    fine, _ = shell256
+    C = 64
+    n = fine.total_columns()
+    assert 27 * C * n > 2 ** 31
+    sp = ConvSpec(3, 1, 0, C, C)
+    g = torch.Generator(device="cuda").manual_seed(17)
+    x = torch.rand((C, n), device="cuda", generator=g) * 2 - 1
+    w = torch.zeros((C, C * 27), device="cuda")
+    w.view(C, C, 27)[torch.arange(C), torch.arange(C), 13] = 1.0
+    assert torch.equal(ops.conv_forward(fine, x, fine, w, sp), x)
+    with ops.math_mode("fast"):
+        y = ops.conv_forward(fine, x, fine, w, sp)
+    assert float((y - x).abs().max()) <= 1e-6
