@@ -378,6 +378,21 @@ class FusedStep:
                 "fwd_conv": ("flop", fl, (ci + co) * N * 2), "dW_conv": ("flop", fl, (ci + co) * N * 2),
                 "dX_conv": ("flop", fl, (ci + co) * N * 2)}
 
+    def smem_model(self):
+        """Shared-memory bytes per launch of the fused kernels (the binding unit at C <= 64,
+        DESIGN.md): every 128-row x 64-K stage writes its gathered A tile (cp.async) and B tile
+        (TMA) and the SS-form MMA reads both back. dW: per 64-voxel stage each m-tile writes and
+        reads a 16 KB gathered tile and reads the group's dY tile (written once per group)."""
+        N, ci, co = self.N, self.cin, self.cout
+        tiles = (N + 127) // 128
+        kst = 27 * ((ci + 63) // 64)  # K stages per forward tile (per dX tile with ci <-> co)
+        fwd = tiles * kst * 2 * (128 * 128 + co * 128)
+        dx = tiles * 27 * ((co + 63) // 64) * 2 * (128 * 128 + ci * 128)
+        mt = (27 * ci + 127) // 128  # dW m-tiles, grouped <= 4 per CTA
+        groups = (mt + 3) // 4
+        dw = ((N + 63) // 64) * (mt * (2 * 128 * 128 + co * 128) + groups * co * 128)
+        return {"fwd_conv": fwd, "dX_conv": dx, "dW_conv": dw}
+
 
 def main():
     args = parse()
@@ -533,6 +548,13 @@ def main():
             if len(model[name]) > 2:
                 kernels[name]["algorithmic_bytes"] = model[name][2]
                 kernels[name]["arith_intensity"] = amount / model[name][2]
+    if hasattr(step, "smem_model"):  # shared-memory traffic per SM-clock (clock sampled in the run)
+        clk_mhz = clk.summary().get("sm_mhz") or 1965.0
+        for name, nbytes in step.smem_model().items():
+            if name in kernels:
+                per_clk = nbytes / (kernels[name]["ms"] / 1e3) / (pk.get("sms", 148) * clk_mhz * 1e6)
+                kernels[name]["smem_bytes"] = nbytes
+                kernels[name]["smem_B_per_clk_per_sm"] = per_clk  # SM limit: 128 B/clk
     dom = max(step.op_names, key=lambda n: per_op[step.op_names.index(n)])
     dk = kernels[dom]
     traffic = None
