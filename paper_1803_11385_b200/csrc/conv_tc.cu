@@ -656,7 +656,10 @@ struct DwCfg {
     static constexpr int KB = 64;                      // voxels per stage
     static constexpr int A_BYTES = 2 * KB * 128;       // two 64-wide MN blocks (M = 128)
     static constexpr int B_BYTES = (NB / 64) * KB * 128;
-    static constexpr int BSTAGES = 2;
+#ifndef HCB_DW_BSTAGES
+#define HCB_DW_BSTAGES 2
+#endif
+    static constexpr int BSTAGES = HCB_DW_BSTAGES;
     static constexpr int NBR = 2 * NT * BM * 4;
     static constexpr int BUDGET = (CPS == 2 ? 113 : 226) * 1024 - 1024 - 512 - 1024 - NBR - BSTAGES * B_BYTES;
     static constexpr int STAGES = BUDGET / A_BYTES > 10 ? 10 : BUDGET / A_BYTES;
