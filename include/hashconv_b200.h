@@ -143,6 +143,10 @@ hc_status hc_psh_info(const hc_psh* p, int64_t info[6]);
 hc_status hc_psh_download(const hc_psh* p, int32_t* hash, uint8_t* offsets, uint16_t* tags,
                           int32_t* model_of_slot, int64_t* hash_acc, int64_t* offset_acc,
                           int64_t* data_acc, int32_t* hash_dims, int32_t* offset_dims);
+/* psh_batch.cpp:80-102 split_super: the batch's models as host PshLevels (free each with
+ * hc_psh_level_free); `data` (device, channels x N) optional, supplies the levels' data. */
+hc_status hc_split_super(const hc_psh* p, const float* data, int64_t channels, hc_psh_level** out,
+                         int32_t max_levels, int32_t* count);
 /* Device pointers of the column table (cnn_ops.cpp:50-66 column_info): per data
  * column, int4 {x, y, z, model} (model 1-based). Valid until hc_psh_free. */
 hc_status hc_psh_columns(const hc_psh* p, const void** xyzm);

@@ -73,6 +73,7 @@ _SIGS = {
     "hc_malloc": [_P, C.c_size_t],
     "hc_free": [_P],
     "hc_psh_info": [_P, _P],
+    "hc_split_super": [_P, _P, _I64, _P, _I32, _P],
     "hc_psh_download": [_P] * 10,
     "hc_psh_columns": [_P, _P],
     "hc_psh_free": [_P],

@@ -388,6 +388,52 @@ hc_status hc_psh_download(const hc_psh* p, int32_t* hash, uint8_t* offsets, uint
     });
 }
 
+// psh_batch.cpp:80-102 split_super: one host PshLevel per model, tables sliced by the
+// prefix arrays; `data` (device, channels x N, optional) supplies each level's data rows.
+hc_status hc_split_super(const hc_psh* p, const float* data, int64_t channels, hc_psh_level** out,
+                         int32_t max_levels, int32_t* count) {
+    return guard([&] {
+        if (!p || !out || !count) throw std::invalid_argument("null argument");
+        const DevPsh& d = p->d;
+        const int b = d.batch, dim = d.dim;
+        if (b > max_levels) throw std::invalid_argument("split_super: output array too small");
+        std::vector<std::int32_t> hash(d.M);
+        std::vector<std::uint8_t> offsets(d.R * dim);
+        std::vector<std::uint16_t> tags(d.M * dim);
+        if (d.M) cuda_check(cudaMemcpy(hash.data(), p->hash, 4 * d.M, cudaMemcpyDeviceToHost), "download");
+        if (d.R) cuda_check(cudaMemcpy(offsets.data(), p->offsets, d.R * dim, cudaMemcpyDeviceToHost), "download");
+        if (d.M) cuda_check(cudaMemcpy(tags.data(), p->tags, 2 * d.M * dim, cudaMemcpyDeviceToHost), "download");
+        std::vector<float> hdata;
+        if (data && channels > 0 && d.N > 0) {
+            hdata.resize((size_t)(channels * d.N));
+            cuda_check(cudaMemcpy(hdata.data(), data, 4 * channels * d.N, cudaMemcpyDeviceToHost), "download");
+        }
+        for (int k = 0; k < b; ++k) {
+            auto* l = new hc_psh_level();
+            l->dim = dim;
+            l->resolution = d.resolution;
+            const long long h0 = p->h_hash_acc[k], h1 = p->h_hash_acc[k + 1];
+            const long long o0 = p->h_offset_acc[k], o1 = p->h_offset_acc[k + 1];
+            const long long n0 = p->h_data_acc[k], n1 = p->h_data_acc[k + 1];
+            l->n = n1 - n0;
+            l->hash_dim = p->h_hash_dims[k];
+            l->offset_dim = p->h_offset_dims[k];
+            l->hash.assign(hash.begin() + h0, hash.begin() + h1);
+            l->tags.assign(tags.begin() + h0 * dim, tags.begin() + h1 * dim);
+            l->offsets.assign(offsets.begin() + o0 * dim, offsets.begin() + o1 * dim);
+            if (!hdata.empty()) {
+                l->channels = channels;
+                l->data.resize((size_t)(channels * l->n));
+                for (long long r = 0; r < channels; ++r)
+                    std::copy(hdata.begin() + r * d.N + n0, hdata.begin() + r * d.N + n1,
+                              l->data.begin() + r * l->n);
+            }
+            out[k] = l;
+        }
+        *count = b;
+    });
+}
+
 hc_status hc_psh_columns(const hc_psh* p, const void** xyzm) {
     if (!p || !xyzm) {
         set_last_error("null argument");

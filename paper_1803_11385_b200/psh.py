@@ -238,6 +238,18 @@ class SuperPsh:
             "offset_dims"))))
         return out
 
+    def split(self, data=None) -> List[PshLevel]:
+        """psh_batch.cpp:80-102 split_super: one host PshLevel per model. `data`: optional
+        device tensor (C x N fp32) whose columns become the levels' data arrays."""
+        out = (C.c_void_p * max(self.batch, 1))()
+        count = C.c_int32()
+        ch, ptr = 0, None
+        if data is not None:
+            data = data.float().contiguous()
+            ch, ptr = int(data.shape[0]), C.c_void_p(data.data_ptr())
+        check(lib.hc_split_super(self._h, ptr, ch, out, self.batch, C.byref(count)))
+        return [PshLevel(C.c_void_p(out[i])) for i in range(count.value)]
+
     def columns_ptr(self) -> int:
         """Device pointer of the int4 {x,y,z,model} column table."""
         p = C.c_void_p()

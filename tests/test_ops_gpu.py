@@ -488,3 +488,26 @@ def test_full_size_int64_index_paths(shell256):
     with ops.math_mode("fast"):
         y = ops.conv_forward(fine, x, fine, w, sp)
     assert float((y - x).abs().max()) <= 1e-6
+
+
+def test_split_super_round_trip(cuda):
+    """psh_batch.cpp:80-102 split_super: the device super-PSH splits back into the levels it
+    was built from (tables and data rows), and rebuilding from the split levels reproduces
+    the super-PSH's arrays."""
+    f, _ = random_pair(16, 3, seed=41)
+    s = SuperPsh.from_levels(f)
+    data = torch.rand((3, s.total_columns()), device="cuda")
+    parts = s.split(data)
+    assert len(parts) == 3
+    acc = s.download().data_acc
+    for k, (orig, got) in enumerate(zip(f, parts)):
+        assert (got.dim, got.resolution, got.n, got.hash_dim, got.offset_dim) == \
+            (orig.dim, orig.resolution, orig.n, orig.hash_dim, orig.offset_dim)
+        ho, oo, to, _ = orig.arrays()
+        hg, og, tg, dg = got.arrays()
+        assert np.array_equal(ho, hg) and np.array_equal(oo, og) and np.array_equal(to, tg)
+        assert np.array_equal(dg, _np(data[:, int(acc[k]):int(acc[k + 1])]))
+    a, b = s.download(), SuperPsh.from_levels(parts).download()
+    for name in ("hash", "offsets", "tags", "model_of_slot", "hash_acc", "offset_acc", "data_acc", "hash_dims",
+                 "offset_dims"):
+        assert np.array_equal(getattr(a, name), getattr(b, name)), name
