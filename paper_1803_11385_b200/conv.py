@@ -145,6 +145,10 @@ class HashConv:
             raise ValueError("HashConv native layer: stride-1 convolution (use ops.* for strided)")
         self.s, self.spec, self.out_dtype = structure, spec, out_dtype
         self.taps = field_size(spec, structure.dim)
+        # any channel counts (the reference takes e.g. 3 -> 2): the tensor-core tile set is
+        # {16, 32, 64, 128, 256} channels, so both sides are zero-padded to it; padded weight
+        # rows/columns are zero, so the padded outputs and gradients are exactly zero
+        self.cin_p, self.cout_p = _tile_channels(spec.in_channels), _tile_channels(spec.out_channels)
         self.fmap = None
         self.set_weights(weights)
 
@@ -153,23 +157,51 @@ class HashConv:
         if tuple(w.shape) != (sp.out_channels, sp.in_channels * self.taps):
             raise ValueError("conv_forward: weight shape mismatch")
         self.w = w
-        self.wf = pack_weights(w, sp.out_channels, sp.in_channels, self.taps, False)
-        self.wb = pack_weights(w, sp.out_channels, sp.in_channels, self.taps, True)
+        wp = w
+        if (self.cin_p, self.cout_p) != (sp.in_channels, sp.out_channels):
+            wp = torch.zeros((self.cout_p, self.cin_p * self.taps), dtype=w.dtype, device=w.device)
+            wp.view(self.cout_p, self.cin_p, self.taps)[:sp.out_channels, :sp.in_channels] = \
+                w.view(sp.out_channels, sp.in_channels, self.taps)
+        self.wf = pack_weights(wp, self.cout_p, self.cin_p, self.taps, False)
+        self.wb = pack_weights(wp, self.cout_p, self.cin_p, self.taps, True)
 
     def build_map(self) -> FieldMap:
         """K0 in the tile-major layout (coalesced build; one bulk copy per tile in the GEMM)."""
         self.fmap = field_map_native(self.s, self.s, self.spec, TILED)
         return self.fmap
 
+    @staticmethod
+    def _pad(t: torch.Tensor, c: int) -> torch.Tensor:
+        if t.shape[1] == c:
+            return t
+        out = torch.zeros((t.shape[0], c), dtype=t.dtype, device=t.device)
+        out[:, :t.shape[1]] = t
+        return out
+
     def forward(self, x: torch.Tensor) -> torch.Tensor:
         if self.fmap is None:
             self.build_map()
-        return gather_gemm(self.fmap, x, self.wf, self.spec.out_channels, self.out_dtype)
+        y = gather_gemm(self.fmap, self._pad(x, self.cin_p), self.wf, self.cout_p, self.out_dtype)
+        return y if self.cout_p == self.spec.out_channels else y[:, :self.spec.out_channels].contiguous()
 
     def backward(self, dy: torch.Tensor, x: torch.Tensor, dx_dtype=None):
-        dw = conv_dw(self.fmap, x, dy)
-        dx = gather_gemm(self.fmap, dy, self.wb, self.spec.in_channels, dx_dtype or self.out_dtype)
+        sp = self.spec
+        dyp, xp = self._pad(dy, self.cout_p), self._pad(x, self.cin_p)
+        dw = conv_dw(self.fmap, xp, dyp)
+        if (self.cin_p, self.cout_p) != (sp.in_channels, sp.out_channels):
+            dw = dw.view(self.cout_p, self.cin_p, self.taps)[:sp.out_channels, :sp.in_channels].reshape(
+                sp.out_channels, sp.in_channels * self.taps)
+        dx = gather_gemm(self.fmap, dyp, self.wb, self.cin_p, dx_dtype or self.out_dtype)
+        if self.cin_p != sp.in_channels:
+            dx = dx[:, :sp.in_channels].contiguous()
         return dw, dx
+
+
+def _tile_channels(c: int) -> int:
+    for t in (16, 32, 64, 128, 256):
+        if c <= t:
+            return t
+    raise ValueError("native conv: at most 256 channels")
 
 
 class HashDeconv:

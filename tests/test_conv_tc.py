@@ -98,10 +98,12 @@ def test_dw_random_maps(cuda, c_in, c_out):
         assert torch.equal(nconv.conv_dw(fm, x.to(torch.bfloat16), dy.to(torch.bfloat16)), dw), fm.layout
 
 
-@pytest.mark.parametrize("c_in,c_out", [(16, 16), (32, 64), (64, 64)])
+@pytest.mark.parametrize("c_in,c_out", [(16, 16), (32, 64), (64, 64), (3, 2), (24, 48), (100, 70)])
 def test_layer_vs_oracle_on_shell(cuda, restated, c_in, c_out):
     """Whole layer (forward, dW, dX) on a 64^3 shell batch vs the double oracle
-    (oracle/hc_oracle.c conv_forward / conv_backward) on bf16-quantised operands."""
+    (oracle/hc_oracle.c conv_forward / conv_backward) on bf16-quantised operands; channel
+    counts outside the tensor-core tile set (the paper's 3 -> 2, 24 -> 48, 100 -> 70) are
+    zero-padded inside the layer."""
     f, _ = shell_pair(64, 2)
     fa = levels_to_arrays(f)
     s = SuperPsh.from_levels(f)
