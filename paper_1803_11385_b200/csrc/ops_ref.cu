@@ -97,7 +97,10 @@ __global__ void k_field_map_t(DevPsh in, DevPsh out, int S, int pad, int* map) {
 // contiguous block (fetched by one bulk copy in the native conv); padded columns
 // beyond N are -1.
 template <int F>
-__global__ void __launch_bounds__(256, 2) k_field_map_tiled(DevPsh in, DevPsh out, int S, int pad, int* map) {
+#ifndef HCB_K0_MINB
+#define HCB_K0_MINB 2
+#endif
+__global__ void __launch_bounds__(256, HCB_K0_MINB) k_field_map_tiled(DevPsh in, DevPsh out, int S, int pad, int* map) {
     const long long col = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     const long long padded = (out.N + 127) / 128 * 128;
     if (col >= padded) return;

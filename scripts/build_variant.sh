@@ -7,9 +7,10 @@ C=$R/paper_1803_11385_b200/csrc
 O=$R/paper_1803_11385_b200/_var/$name
 mkdir -p $O
 make -C $C > /dev/null
-objs=$(ls $R/paper_1803_11385_b200/_lib/obj/*.o | grep -v conv_tc.o)
+F=${HCB_VARIANT_FILE:-conv_tc}  # which source file gets the extra flags
+objs=$(ls $R/paper_1803_11385_b200/_lib/obj/*.o | grep -v "/$F.o")
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
-  -Xcompiler -fvisibility=hidden -I$R/include -I$C --expt-relaxed-constexpr "$@" -c $C/conv_tc.cu -o $O/conv_tc.o
+  -Xcompiler -fvisibility=hidden -I$R/include -I$C --expt-relaxed-constexpr "$@" -c $C/$F.cu -o $O/$F.o
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o $O/libhcb200.so \
-  $O/conv_tc.o $objs -Xlinker --exclude-libs,ALL
+  $O/$F.o $objs -Xlinker --exclude-libs,ALL
 echo $O/libhcb200.so
