@@ -554,7 +554,7 @@ def main():
             if name in kernels:
                 per_clk = nbytes / (kernels[name]["ms"] / 1e3) / (pk.get("sms", 148) * clk_mhz * 1e6)
                 kernels[name]["smem_bytes"] = nbytes
-                kernels[name]["smem_B_per_clk_per_sm"] = per_clk  # SM limit: 128 B/clk
+                kernels[name]["smem_B_per_clk_per_sm"] = per_clk  # fills + MMA operand reads (traffic figure)
     dom = max(step.op_names, key=lambda n: per_op[step.op_names.index(n)])
     dk = kernels[dom]
     traffic = None
