@@ -56,6 +56,10 @@ const char* hc_last_error(void);
 const char* hc_version(void);
 /* Total kernels this library has enqueued in the process (for launch accounting). */
 int64_t hc_launch_count(void);
+/* Reference-signature conv_forward / conv_backward calls (fp32, HC_MATH_FAST) served by the
+ * fused split-precision tensor-core conv instead of hash2col + GEMMs (stride-1 layer over one
+ * structure handle, <= 128 channels; HCB_FAST_FUSED=0 disables the route). */
+int64_t hc_fused_route_count(void);
 /* Math mode for the reference-layout contraction (thread-local; default EXACT). */
 hc_status hc_set_math(hc_math mode);
 hc_math hc_get_math(void);

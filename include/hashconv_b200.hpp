@@ -28,6 +28,7 @@
 #include <string>
 #include <type_traits>
 #include <utility>
+#include <memory>
 #include <vector>
 
 #include "hashconv_b200.h"
@@ -248,10 +249,16 @@ Mat col2hash(const Mat& col_grads, const Super& input, const Super& output, cons
 }
 
 // cnn_ops.cpp:206-215
+// A stride-1 layer over ONE structure (&input == &output, as net.cpp:196-197 calls it) uploads
+// it once: the library sees one handle, which is what routes HC_MATH_FAST float calls to the
+// fused split-precision tensor-core conv (no column matrix).
 template <class Super, class Mat, class W, class Spec>
 Mat conv_forward(const Super& input, const Mat& input_data, const Super& output, const W& weights, const Spec& spec) {
     using T = detail::value_t<Mat>;
-    detail::Structure in(input), out(output);
+    detail::Structure in(input);
+    const bool same = static_cast<const void*>(&input) == static_cast<const void*>(&output);
+    std::unique_ptr<detail::Structure> out_own(same ? nullptr : new detail::Structure(output));
+    const detail::Structure& out = same ? in : *out_own;
     const hc_conv_spec sp = detail::spec_of(spec);
     auto d = detail::upload(input_data);
     auto w = detail::upload(weights.w);
@@ -267,7 +274,10 @@ template <class Mat, class W, class Super, class Spec>
 ConvGradients<Mat> conv_backward(const Mat& output_grad, const W& weights, const Mat& cached_cols, const Super& input,
                                  const Super& output, const Spec& spec) {
     using T = detail::value_t<Mat>;
-    detail::Structure in(input), out(output);
+    detail::Structure in(input);
+    const bool same = static_cast<const void*>(&input) == static_cast<const void*>(&output);
+    std::unique_ptr<detail::Structure> out_own(same ? nullptr : new detail::Structure(output));
+    const detail::Structure& out = same ? in : *out_own;
     const hc_conv_spec sp = detail::spec_of(spec);
     auto g = detail::upload(output_grad);
     auto w = detail::upload(weights.w);

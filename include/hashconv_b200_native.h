@@ -52,6 +52,33 @@ hc_status hc_native_conv_dw(const int32_t* fmap, int32_t fmap_layout, int64_t n_
                             int32_t c_in, const void* dy, int32_t c_out, float* dw_ref,
                             void* workspace, size_t ws_bytes, hc_stream stream);
 
+/* ---- Split precision (fp32-accurate contraction on the bf16 tensor-core path) ----------
+ * An fp32 operand v is carried as two bf16 planes hi = rn(v), lo = rn(v - hi)
+ * (|v - hi - lo| <= 2^-17 |v|); features become split rows [N][2C] = [hi | lo], weights
+ * [2 R][hc_native_packed_k_x2] (hi rows then lo rows). The contraction accumulates
+ * hi.hi + hi.lo + lo.hi (+ lo.lo for dW) in fp32 on tcgen05 — the reference's fp32
+ * conv_forward / conv_backward (cnn_ops.cpp:206-232) within 1e-5 relative (normwise) of the
+ * float64 instantiation on unquantised fp32 inputs. c_in, c_out <= 128 (multiples of 8;
+ * forward c_out in {16, 32, 64, 128}). */
+int64_t hc_native_packed_k_x2(int32_t channels, int32_t taps);
+/* src fp32 channel-major C x N (channel_major = 1, the reference layout) or voxel-major
+ * N x C (0) -> out bf16 [N][2C]. c a multiple of 4. */
+hc_status hc_native_split(const float* src, int32_t channel_major, int64_t c, int64_t n, void* out,
+                          hc_stream stream);
+/* Same modes as hc_native_pack_weights; w_packed: bf16 [2*rows][hc_native_packed_k_x2(...)]. */
+hc_status hc_native_pack_weights_x2(const float* w_ref, int32_t c_out, int32_t c_in, int32_t taps,
+                                    int32_t mode, void* w_packed, hc_stream stream);
+/* y fp32 [n_out][c_out] = gather-GEMM of the split rows (hc_native_gather_gemm semantics). */
+hc_status hc_native_gather_gemm_x2(const int32_t* fmap, int32_t fmap_layout, int64_t n_out,
+                                   int32_t taps, const void* x_split, int32_t c_in,
+                                   const void* w_packed_x2, int32_t c_out, float* y, hc_stream stream);
+/* dW (reference layout, fp32) from split rows of X and dY (hc_native_conv_dw semantics). The
+ * workspace query returns 0 for an unsupported shape. */
+size_t hc_native_dw_workspace_x2(int64_t n_out, int32_t taps, int32_t c_in, int32_t c_out);
+hc_status hc_native_conv_dw_x2(const int32_t* fmap, int32_t fmap_layout, int64_t n_out, int32_t taps,
+                               const void* x_split, int32_t c_in, const void* dy_split, int32_t c_out,
+                               float* dw_ref, void* workspace, size_t ws_bytes, hc_stream stream);
+
 /* ---- Native net layers (voxel-major [N][C], C a multiple of 8) ----------------------
  * The block operators of net.cpp:181-323 around the conv: max pool / unpool
  * (cnn_ops.cpp:234-284, 336-372), batch norm + ReLU (cnn_ops.cpp:437-489, 542-561) and

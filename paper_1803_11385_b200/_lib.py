@@ -146,6 +146,10 @@ _SIGS.update({
     "hc_native_dense_pool": [_P, _I32, _P, _I32, _P, _P, _P],
     "hc_native_dense_pool_backward": [_P, _P, _I32, _I32, _I64, _P, _P],
     "hc_native_sgd_update": [_P, _P, _P, _I64, C.c_float, C.c_float, C.c_float, _P],
+    "hc_native_split": [_P, _I32, _I64, _I64, _P, _P],
+    "hc_native_pack_weights_x2": [_P, _I32, _I32, _I32, _I32, _P, _P],
+    "hc_native_gather_gemm_x2": [_P, _I32, _I64, _I32, _P, _I32, _P, _I32, _P, _P],
+    "hc_native_conv_dw_x2": [_P, _I32, _I64, _I32, _P, _I32, _P, _I32, _P, _P, C.c_size_t, _P],
 })
 lib.hc_native_bn_workspace.restype = C.c_size_t
 lib.hc_native_bn_workspace.argtypes = [_I64, _I32]
@@ -153,7 +157,12 @@ lib.hc_native_packed_k.restype = C.c_int64
 lib.hc_native_packed_k.argtypes = [_I32, _I32]
 lib.hc_native_dw_workspace.restype = C.c_size_t
 lib.hc_native_dw_workspace.argtypes = [_I64, _I32, _I32, _I32]
+lib.hc_native_packed_k_x2.restype = C.c_int64
+lib.hc_native_packed_k_x2.argtypes = [_I32, _I32]
+lib.hc_native_dw_workspace_x2.restype = C.c_size_t
+lib.hc_native_dw_workspace_x2.argtypes = [_I64, _I32, _I32, _I32]
 lib.hc_launch_count.restype = C.c_int64
+lib.hc_fused_route_count.restype = C.c_int64
 for _name, _args in _SIGS.items():
     fn = getattr(lib, _name)
     fn.argtypes = _args

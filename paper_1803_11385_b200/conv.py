@@ -106,6 +106,49 @@ def gather_gemm(fmap, x: torch.Tensor, wp: torch.Tensor, c_out: int, out_dtype=t
     return y
 
 
+# ---------------------------------------------------------------- split precision (fp32 accurate)
+def split(t: torch.Tensor, channel_major: bool = False) -> torch.Tensor:
+    """fp32 features -> split rows [N][2C] bf16 = [hi | lo], hi = rn(v), lo = rn(v - hi)
+    (hc_native_split). `t` is voxel-major [N][C], or channel-major C x N (the reference
+    layout) with channel_major=True."""
+    t = t.contiguous().float()
+    c, n = (t.shape[0], t.shape[1]) if channel_major else (t.shape[1], t.shape[0])
+    out = torch.empty((n, 2 * c), dtype=torch.bfloat16, device=t.device)
+    check(lib.hc_native_split(_p(t), int(channel_major), c, n, _p(out), _s()))
+    return out
+
+
+def pack_weights_x2(w_ref: torch.Tensor, c_out: int, c_in: int, taps: int, mode: int = PACK_FORWARD) -> torch.Tensor:
+    """W[co][ci*taps + t] -> the split-precision operand [2 rows][Kp2] (hi rows, lo rows)."""
+    w_ref = w_ref.contiguous().float()
+    rows = c_in if mode else c_out
+    kp = int(lib.hc_native_packed_k_x2(c_out if mode else c_in, taps))
+    wp = torch.empty((2 * rows, kp), dtype=torch.bfloat16, device=w_ref.device)
+    check(lib.hc_native_pack_weights_x2(_p(w_ref), c_out, c_in, taps, mode, _p(wp), _s()))
+    return wp
+
+
+def gather_gemm_x2(fmap, xs: torch.Tensor, wp2: torch.Tensor, c_out: int) -> torch.Tensor:
+    """fp32 Y[n] = sum_t X[fmap(n,t)] . W_t from split operands (hc_native_gather_gemm_x2)."""
+    fm = as_field_map(fmap)
+    y = torch.empty((fm.n, c_out), dtype=torch.float32, device=xs.device)
+    check(lib.hc_native_gather_gemm_x2(_p(fm.data), fm.layout, fm.n, fm.taps, _p(xs), xs.shape[1] // 2, _p(wp2),
+                                       c_out, _p(y), _s()))
+    return y
+
+
+def conv_dw_x2(fmap, xs: torch.Tensor, dys: torch.Tensor, ws: "DwWorkspace" = None) -> torch.Tensor:
+    """fp32 dW[co][ci*taps + t] from split rows of X and dY (hc_native_conv_dw_x2)."""
+    fm = as_field_map(fmap)
+    c_in, c_out = xs.shape[1] // 2, dys.shape[1] // 2
+    nbytes = int(lib.hc_native_dw_workspace_x2(fm.n, fm.taps, c_in, c_out))
+    w = (ws or _WS).get(nbytes, xs.device)
+    dw = torch.empty((c_out, c_in * fm.taps), dtype=torch.float32, device=xs.device)
+    check(lib.hc_native_conv_dw_x2(_p(fm.data), fm.layout, fm.n, fm.taps, _p(xs), c_in, _p(dys), c_out, _p(dw),
+                                   _p(w), w.numel(), _s()))
+    return dw
+
+
 class DwWorkspace:
     def __init__(self):
         self.buf = None
@@ -139,17 +182,28 @@ class HashConv:
                                transposed kernel on the same field map (stride 1)
     """
 
-    def __init__(self, structure: SuperPsh, weights: torch.Tensor, spec: ConvSpec, out_dtype=torch.bfloat16):
+    def __init__(self, structure: SuperPsh, weights: torch.Tensor, spec: ConvSpec, out_dtype=torch.bfloat16,
+                 precision: str = "bf16"):
+        """precision "bf16": bf16 operands (features voxel-major bf16), fp32 accumulation;
+        "f32": fp32 features and weights carried as bf16 hi/lo planes (hc_native_*_x2),
+        fp32 outputs within 1e-5 of the float64 reference — the reference's own precision."""
         spec = ConvSpec(*spec)
         if spec.stride != 1:
             raise ValueError("HashConv native layer: stride-1 convolution (use ops.* for strided)")
-        self.s, self.spec, self.out_dtype = structure, spec, out_dtype
+        if precision not in ("bf16", "f32"):
+            raise ValueError("HashConv: precision must be 'bf16' or 'f32'")
+        self.precision = precision
+        self.s, self.spec = structure, spec
+        self.out_dtype = torch.float32 if precision == "f32" else out_dtype
         self.taps = field_size(spec, structure.dim)
         # any channel counts (the reference takes e.g. 3 -> 2): the tensor-core tile set is
         # {16, 32, 64, 128, 256} channels, so both sides are zero-padded to it; padded weight
         # rows/columns are zero, so the padded outputs and gradients are exactly zero
         self.cin_p, self.cout_p = _tile_channels(spec.in_channels), _tile_channels(spec.out_channels)
+        if precision == "f32" and max(self.cin_p, self.cout_p) > 128:
+            raise ValueError("native conv (split precision): at most 128 channels")
         self.fmap = None
+        self._xs = None  # split rows of the last forward input (f32)
         self.set_weights(weights)
 
     def set_weights(self, w: torch.Tensor):
@@ -162,8 +216,12 @@ class HashConv:
             wp = torch.zeros((self.cout_p, self.cin_p * self.taps), dtype=w.dtype, device=w.device)
             wp.view(self.cout_p, self.cin_p, self.taps)[:sp.out_channels, :sp.in_channels] = \
                 w.view(sp.out_channels, sp.in_channels, self.taps)
-        self.wf = pack_weights(wp, self.cout_p, self.cin_p, self.taps, False)
-        self.wb = pack_weights(wp, self.cout_p, self.cin_p, self.taps, True)
+        if self.precision == "f32":
+            self.wf = pack_weights_x2(wp, self.cout_p, self.cin_p, self.taps, PACK_FORWARD)
+            self.wb = pack_weights_x2(wp, self.cout_p, self.cin_p, self.taps, PACK_BACKWARD)
+        else:
+            self.wf = pack_weights(wp, self.cout_p, self.cin_p, self.taps, False)
+            self.wb = pack_weights(wp, self.cout_p, self.cin_p, self.taps, True)
 
     def build_map(self) -> FieldMap:
         """K0 in the tile-major layout (coalesced build; one bulk copy per tile in the GEMM)."""
@@ -179,13 +237,31 @@ class HashConv:
         return out
 
     def forward(self, x: torch.Tensor) -> torch.Tensor:
+        """x: voxel-major [N][C_in] (bf16, or fp32 for precision "f32")."""
         if self.fmap is None:
             self.build_map()
-        y = gather_gemm(self.fmap, self._pad(x, self.cin_p), self.wf, self.cout_p, self.out_dtype)
+        if self.precision == "f32":
+            self._xs = split(self._pad(x, self.cin_p))
+            y = gather_gemm_x2(self.fmap, self._xs, self.wf, self.cout_p)
+        else:
+            y = gather_gemm(self.fmap, self._pad(x, self.cin_p), self.wf, self.cout_p, self.out_dtype)
         return y if self.cout_p == self.spec.out_channels else y[:, :self.spec.out_channels].contiguous()
 
     def backward(self, dy: torch.Tensor, x: torch.Tensor, dx_dtype=None):
+        """-> (dW fp32 [C_out][C_in*taps], dX [N][C_in]). f32: x is the forward input (its
+        split rows from forward() are reused when x is that same tensor's data)."""
         sp = self.spec
+        if self.precision == "f32":
+            xs = self._xs if self._xs is not None and x is None else split(self._pad(x, self.cin_p))
+            dys = split(self._pad(dy, self.cout_p))
+            dw = conv_dw_x2(self.fmap, xs, dys)
+            if (self.cin_p, self.cout_p) != (sp.in_channels, sp.out_channels):
+                dw = dw.view(self.cout_p, self.cin_p, self.taps)[:sp.out_channels, :sp.in_channels].reshape(
+                    sp.out_channels, sp.in_channels * self.taps)
+            dx = gather_gemm_x2(self.fmap, dys, self.wb, self.cin_p)
+            if self.cin_p != sp.in_channels:
+                dx = dx[:, :sp.in_channels].contiguous()
+            return dw, dx
         dyp, xp = self._pad(dy, self.cout_p), self._pad(x, self.cin_p)
         dw = conv_dw(self.fmap, xp, dyp)
         if (self.cin_p, self.cout_p) != (sp.in_channels, sp.out_channels):
@@ -242,13 +318,25 @@ class HashDeconv:
         return dw, dd
 
 
-def smoke_check(structure: SuperPsh, x: np.ndarray, w: np.ndarray, dy: np.ndarray, y64: np.ndarray) -> None:
-    """Native forward on tensor cores vs the double oracle (bf16-operand tolerance)."""
+def smoke_check(structure: SuperPsh, x: np.ndarray, w: np.ndarray, dy: np.ndarray, y64: np.ndarray,
+                dw64: np.ndarray = None, dx64: np.ndarray = None) -> None:
+    """Native forward on tensor cores vs the double oracle: the bf16-operand layer (bf16
+    tolerance) and the split-precision fp32 layer (forward, dW, dX within 1e-5)."""
     dev = torch.device("cuda", torch.cuda.current_device())
     c_in, c_out = x.shape[0], w.shape[0]
-    layer = HashConv(structure, torch.from_numpy(w).to(dev), ConvSpec(3, 1, 0, c_in, c_out), torch.float32)
+    spec = ConvSpec(3, 1, 0, c_in, c_out)
+    rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))  # noqa: E731
+    layer = HashConv(structure, torch.from_numpy(w).to(dev), spec, torch.float32)
     xv = to_voxel_major(torch.from_numpy(x).to(dev))
     y = to_channel_major(layer.forward(xv)).cpu().numpy().astype(np.float64)
-    err = np.linalg.norm(y - y64) / np.linalg.norm(y64)
+    err = rel(y, y64)
     # bf16 operands (2^-9 relative each) accumulated in fp32
     assert err < 2e-2, f"native conv forward rel err {err}"
+    f32 = HashConv(structure, torch.from_numpy(w).to(dev), spec, precision="f32")
+    xf = torch.from_numpy(x).to(dev).t().contiguous()
+    y = f32.forward(xf).t().cpu().numpy().astype(np.float64)
+    assert rel(y, y64) <= 1e-5, f"native fp32 (split) conv forward rel err {rel(y, y64)}"
+    if dw64 is not None:
+        dw, dx = f32.backward(torch.from_numpy(dy).to(dev).t().contiguous(), xf)
+        assert rel(dw.cpu().numpy().astype(np.float64), dw64) <= 1e-5, "native fp32 (split) dW"
+        assert rel(dx.t().cpu().numpy().astype(np.float64), dx64) <= 1e-5, "native fp32 (split) dX"

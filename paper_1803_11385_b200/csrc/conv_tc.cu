@@ -171,11 +171,16 @@ struct FwdCfg {
     static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + NBR + EPI + 320;
 };
 
-template <int BN, int CPS, int PW, typename OutT>
+// SUMH (split-precision forward, hc_native_gather_gemm_x2): the B tile holds two weight planes
+// (rows [0, BN/2) = hi, [BN/2, BN) = lo) and the gathered rows two feature planes (K offsets
+// [0, C/2) = hi, [C/2, C) = lo of every C-wide row); the epilogue adds the two accumulator halves,
+// and K16 chunks of the lo feature plane issue N = BN/2 (the lo x lo product is dropped when
+// skip_lolo, leaving hi.hi + hi.lo + lo.hi).
+template <int BN, int CPS, int PW, typename OutT, bool SUMH = false>
 __global__ void __launch_bounds__(FwdCfg<BN, CPS, PW, sizeof(OutT)>::THREADS, CPS)
     k_conv_fwd(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap ymap,
                const int* __restrict__ fmap, int taps, long long rows, const bf16* __restrict__ X, int C, int nkb,
-               int tiles) {
+               int tiles, int skip_lolo) {
     using Cfg = FwdCfg<BN, CPS, PW, sizeof(OutT)>;
     constexpr int NP = Cfg::PRODUCERS;
     constexpr int S = Cfg::STAGES;
@@ -297,14 +302,24 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, PW, sizeof(OutT)>::THREADS, CP
             mbar_wait_sleep(tfull0 + 8 * acc, (uint32_t)((i >> 1) & 1));
             tc_fence_after();
             const int r0 = tile * BM + q * 32;
+            constexpr int BO = SUMH ? BN / 2 : BN;  // output channels
 #pragma unroll
-            for (int c0 = 0; c0 < BN; c0 += 16) {
+            for (int c0 = 0; c0 < BO; c0 += 16) {
                 uint32_t v[16];
-                tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c0, v);
-                tmem_ld_wait();
+                const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c0;
+                tmem_ld16(ta, v);
                 float f[16];
+                if constexpr (SUMH) {
+                    uint32_t u[16];
+                    tmem_ld16(ta + BO, u);
+                    tmem_ld_wait();
 #pragma unroll
-                for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(v[e]);
+                    for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(v[e]) + __uint_as_float(u[e]);
+                } else {
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(v[e]);
+                }
                 uint8_t* buf = stage + (nb_issued % Cfg::EPI_BUFS) * Cfg::EPI_BUF;
                 if (nb_issued >= Cfg::EPI_BUFS) {  // that buffer's previous store has been read
                     if (lane == 0) bulk_wait_read<Cfg::EPI_BUFS - 1>();
@@ -342,7 +357,9 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, PW, sizeof(OutT)>::THREADS, CP
     } else if (warp == PW + 4) {
         // ---------------- MMA issuer: warp-uniform loop, one elected lane issues
         constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, false, false);
+        constexpr uint32_t idesc_h = idesc_bf16_f32(BM, SUMH ? BN / 2 : BN, false, false);
         const uint64_t a0 = sw128_desc(sbase, 16, 1024), b0 = sw128_desc(sbase + Cfg::A_BYTES, 16, 1024);
+        const int half = C / 2;  // SUMH: K offsets >= half of a row are the lo feature plane
         int s = 0;
         uint32_t ph = 0;
         int i = 0;
@@ -351,16 +368,32 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, PW, sizeof(OutT)>::THREADS, CP
             mbar_wait(tempty0 + 8 * acc, (uint32_t)(((i >> 1) & 1) ^ 1));
             tc_fence_after();
             const uint32_t d = tmem + acc * BN;
+            int kpos = 0;  // K offset of the stage inside its C-wide row (SUMH)
             for (int kb = 0; kb < nkb; ++kb) {
                 mbar_wait(full0 + 8 * s, ph);
                 fence_proxy_async();  // cp.async (generic proxy) writes -> tcgen05 operand reads
                 tc_fence_after();
                 if (elect_one()) {
                     const uint64_t so = (uint64_t)((s * Cfg::STAGE_BYTES) >> 4);  // descriptor start-address units
+                    if constexpr (SUMH) {
+                        int kp = kpos;
 #pragma unroll
-                    for (int kk = 0; kk < BK / 16; ++kk)
-                        mma_bf16(d, a0 + so + 2 * kk, b0 + so + 2 * kk, idesc, (kb | kk) != 0);
+                        for (int kk = 0; kk < BK / 16; ++kk) {
+                            const bool lo = skip_lolo && kp >= half;
+                            mma_bf16(d, a0 + so + 2 * kk, b0 + so + 2 * kk, lo ? idesc_h : idesc, (kb | kk) != 0);
+                            kp += 16;
+                            if (kp >= C) kp -= C;
+                        }
+                    } else {
+#pragma unroll
+                        for (int kk = 0; kk < BK / 16; ++kk)
+                            mma_bf16(d, a0 + so + 2 * kk, b0 + so + 2 * kk, idesc, (kb | kk) != 0);
+                    }
                     mma_commit(empty0 + 8 * s);
+                }
+                if constexpr (SUMH) {
+                    kpos += BK;
+                    while (kpos >= C) kpos -= C;
                 }
                 __syncwarp();
                 if (++s == S) {
@@ -639,10 +672,16 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, PW, sizeof(OutT)>::THREADS, CP
 // CTA plan re-read dY mt = 14 times at C=64).
 // Split plan, passed by value: group g owns m-tiles [m_begin[g], m_begin[g+1]) and CTAs
 // [cta_begin[g], cta_begin[g+1]), each CTA a run of tps[g] voxel tiles; its partials start
-// at part_begin[g] (floats), laid out [split][m-tile][128][NB].
-constexpr int kMaxGroups = 32;
+// at part_begin[g] (floats), laid out [split][m-tile][rpm][pcols].
+//   plain: rpm = 128 (t,ci) rows of the row width C, pcols = NB.
+//   pair (split precision, hc_native_conv_dw_x2): X rows are [hi | lo] (C = 2 c), dY rows
+//     [hi | lo] (2 c_out); m-tile j's 64-row blocks are the hi and the lo plane of the same 64
+//     (t, ci) rows j*64 .. j*64+63 of taps x c, so the epilogue adds the four plane products
+//     (lanes r and 64 + r, columns co and c_out + co) and writes rpm = 64 rows x c_out.
+constexpr int kMaxGroups = 64;
 struct DwGroups {
     int groups;
+    int pair, rpm, pcols;
     int m_begin[kMaxGroups + 1];
     int cta_begin[kMaxGroups + 1];
     int tps[kMaxGroups];
@@ -697,19 +736,23 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
     const int tps = grp_tab.tps[grp];
     const int tile0 = split * tps;
     const int ntl = max(0, min(tps, tiles - tile0));
-    const int K = taps * C;
+    const int pair = grp_tab.pair;
+    const int Co = pair ? C / 2 : C;    // channels of one plane
+    const int RPM = pair ? 64 : 128;    // (t, ci) rows per m-tile
+    const int K = taps * Co;
     const uint32_t sbase = smem_u32(smem), bbase = smem_u32(bsm);
     const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S);
     const uint32_t bfull0 = smem_u32(bars + 2 * S), bempty0 = smem_u32(bars + 2 * S + BS);
     const uint32_t nfull0 = smem_u32(bars + 2 * S + 2 * BS), done = nfull0 + 16;
     // taps [t_lo, t_lo + ntb) cover this CTA's (t, ci) rows; only they are staged
-    const int t_lo = (m0 * 128) / C;
-    const int ntb = min(NT, (min(K, (m0 + nm) * 128) - 1) / C - t_lo + 1);
+    const int t_lo = (m0 * RPM) / Co;
+    const int ntb = min(NT, (min(K, (m0 + nm) * RPM) - 1) / Co - t_lo + 1);
     const uint32_t nbr_bytes = (uint32_t)(ntb * BM * 4);
 
     for (int e = tid; e < nm * 16; e += blockDim.x) {
-        const int m = (m0 + e / 16) * 128 + ((e / 8) & 1) * 64 + (e & 7) * 8;
-        tab[e] = m < K ? ((m / C - t_lo) << 16) | (m % C) : -1;
+        const int blk = (e / 8) & 1;
+        const int m = pair ? (m0 + e / 16) * 64 + (e & 7) * 8 : (m0 + e / 16) * 128 + blk * 64 + (e & 7) * 8;
+        tab[e] = m < K ? ((m / Co - t_lo) << 16) | ((pair ? blk * Co : 0) + m % Co) : -1;
     }
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
@@ -796,7 +839,55 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
         }
 
         // ---------------- epilogue (warps 0-3 = TMEM lane quadrants): row m, columns co
-        if (warp < 4) {
+        if (warp < 4 && pair) {
+            // lanes 64..127 (lo plane rows) hand their column sums to lanes 0..63 through shared
+            // memory (the A ring is idle once `done` fired); fixed order (hi.hi + hi.lo) + (lo.hi + lo.lo)
+            const int row = warp * 32 + (int)lane_id();
+            const int r = row & 63;
+            const int pc = grp_tab.pcols;  // c_out (a multiple of 16)
+            const int xs = pc + 4;         // padded exchange row (floats)
+            float* xch = reinterpret_cast<float*>(smem);
+            if (ntl > 0) {
+                mbar_wait_sleep(done, 0);
+                tc_fence_after();
+            }
+            for (int mi = 0; mi < nm; ++mi) {
+                float* dst = partial + grp_tab.part_begin[grp] + (((long long)split * nm + mi) * 64 + r) * pc;
+                for (int ph2 = 1; ph2 >= 0; --ph2) {
+                    if ((row >> 6) == ph2) {
+                        for (int c0 = 0; c0 < pc; c0 += 16) {
+                            float f[16];
+                            if (ntl > 0) {
+                                uint32_t a[16], b[16];
+                                const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + mi * NB + c0;
+                                tmem_ld16(ta, a);
+                                tmem_ld16(ta + pc, b);
+                                tmem_ld_wait();
+#pragma unroll
+                                for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(a[e]) + __uint_as_float(b[e]);
+                            } else {
+#pragma unroll
+                                for (int e = 0; e < 16; ++e) f[e] = 0.0f;
+                            }
+                            float* x = xch + r * xs + c0;
+                            if (ph2 == 1) {
+#pragma unroll
+                                for (int e = 0; e < 16; e += 4)
+                                    *reinterpret_cast<float4*>(x + e) = make_float4(f[e], f[e + 1], f[e + 2], f[e + 3]);
+                            } else {
+#pragma unroll
+                                for (int e = 0; e < 16; e += 4) {
+                                    const float4 v = *reinterpret_cast<const float4*>(x + e);
+                                    f[e] += v.x, f[e + 1] += v.y, f[e + 2] += v.z, f[e + 3] += v.w;
+                                }
+                                store_row(dst + c0, f);
+                            }
+                        }
+                    }
+                    named_sync(1, 128);
+                }
+            }
+        } else if (warp < 4) {
             const int row = warp * 32 + (int)lane_id();
             if (ntl > 0) {
                 mbar_wait_sleep(done, 0);
@@ -889,12 +980,31 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
     }
 }
 
+// Sum over the voxel splits of one (m, n) partial: lane j of 8 takes splits j, j+8, ...
+__device__ __forceinline__ float split_lane_sum(const float* __restrict__ partial, const DwGroups& grp_tab,
+                                                long long m, int n, int j) {
+    const int rpm = grp_tab.rpm, pc = grp_tab.pcols;
+    const int mtile = (int)(m / rpm), row = (int)(m % rpm);
+    int g = 0;
+    while (g + 1 < grp_tab.groups && mtile >= grp_tab.m_begin[g + 1]) ++g;
+    const int nm = grp_tab.m_begin[g + 1] - grp_tab.m_begin[g];
+    const int splits = grp_tab.cta_begin[g + 1] - grp_tab.cta_begin[g];
+    const float* p = partial + grp_tab.part_begin[g] + ((long long)(mtile - grp_tab.m_begin[g]) * rpm + row) * pc + n;
+    const long long stride = (long long)nm * rpm * pc;
+    float acc = 0.0f;
+#pragma unroll 4
+    for (int s = j; s < splits; s += 8) acc += p[s * stride];
+    return acc;
+}
+
 // dW_ref[co][ci*taps + t] = sum_split partial[split][t*C + ci][co]  (fixed order).
 // Block = 32 consecutive (m, co) outputs x 8 split lanes: lane j sums splits j, j+8, ...,
 // then the 8 lane sums are added in lane order -> deterministic, 8x the loads in flight of
 // a thread-per-output loop (hundreds of splits at small C).
-__global__ void __launch_bounds__(256) k_reduce_dw(const float* __restrict__ partial, const DwGroups grp_tab, int NB,
-                                                  int taps, int C, int Cout, float* __restrict__ dw) {
+// (C, Cout): the GEMM's (possibly zero-padded) channels; (cin_r, cout_r): the written dW's.
+__global__ void __launch_bounds__(256) k_reduce_dw(const float* __restrict__ partial, const DwGroups grp_tab,
+                                                  int taps, int C, int Cout, float* __restrict__ dw, int cin_r,
+                                                  int cout_r) {
     __shared__ float red[8][33];
     const int lane = threadIdx.x & 31, j = threadIdx.x >> 5;
     const long long i = blockIdx.x * 32LL + lane;  // over (taps*C) x Cout
@@ -905,15 +1015,7 @@ __global__ void __launch_bounds__(256) k_reduce_dw(const float* __restrict__ par
     if (i < total) {
         m = i / Cout;
         co = (int)(i - m * Cout);
-        const int mtile = (int)(m / BM), row = (int)(m % BM);
-        int g = 0;
-        while (g + 1 < grp_tab.groups && mtile >= grp_tab.m_begin[g + 1]) ++g;
-        const int nm = grp_tab.m_begin[g + 1] - grp_tab.m_begin[g];
-        const int splits = grp_tab.cta_begin[g + 1] - grp_tab.cta_begin[g];
-        const float* p = partial + grp_tab.part_begin[g] + ((long long)(mtile - grp_tab.m_begin[g]) * BM + row) * NB + co;
-        const long long stride = (long long)nm * BM * NB;
-#pragma unroll 4
-        for (int s = j; s < splits; s += 8) acc += p[s * stride];
+        acc = split_lane_sum(partial, grp_tab, m, co, j);
     }
     red[j][lane] = acc;
     __syncthreads();
@@ -922,7 +1024,7 @@ __global__ void __launch_bounds__(256) k_reduce_dw(const float* __restrict__ par
 #pragma unroll
         for (int k = 1; k < 8; ++k) v += red[k][lane];
         const int t = (int)(m / C), ci = (int)(m - (long long)t * C);
-        dw[(long long)co * C * taps + (long long)ci * taps + t] = v;
+        if (ci < cin_r && co < cout_r) dw[(long long)co * cin_r * taps + (long long)ci * taps + t] = v;
     }
 }
 
@@ -967,6 +1069,79 @@ __global__ void k_pack_w(const float* __restrict__ w, int cout, int cin, int tap
     wp[i] = __float2bfloat16_rn(v);
 }
 
+// Split precision: an fp32 value v is carried as two bf16 planes hi = rn(v), lo = rn(v - hi)
+// (|v - hi - lo| <= 2^-17 |v|); the products hi.hi + hi.lo + lo.hi (+ lo.lo) accumulate in fp32.
+__device__ __forceinline__ void split2(float v, bf16& hi, bf16& lo) {
+    hi = __float2bfloat16_rn(v);
+    lo = __float2bfloat16_rn(v - __bfloat162float(hi));
+}
+
+// Weights in the split layout: rows [0, R) the hi plane, [R, 2R) the lo plane of the mode's
+// matrix (as k_pack_w); each tap's K segment is [hi features | lo features] (2 Ck wide) with
+// the same weight value in both halves, so row q, segment p multiplies plane q by plane p.
+// (cout, cin): the reference weight matrix; (cout_p, cin_p) >= them: the zero-padded operand.
+__global__ void k_pack_w_x2(const float* __restrict__ w, int cout, int cin, int taps, int mode, int Kp2,
+                            bf16* __restrict__ wp, int cout_p, int cin_p) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const int rows = mode ? cin_p : cout_p;
+    if (i >= 2LL * rows * Kp2) return;
+    const int rr = (int)(i / Kp2), k = (int)(i % Kp2);
+    const int q = rr >= rows, r = rr - q * rows;
+    const int ck = mode ? cout_p : cin_p;
+    float v = 0.0f;
+    if (k < taps * 2 * ck) {
+        const int t = k / (2 * ck);
+        int c = k - t * 2 * ck;
+        if (c >= ck) c -= ck;
+        const int co = mode ? c : r, ci = mode ? r : c;
+        if (co < cout && ci < cin)
+            v = w[(long long)co * cin * taps + ci * taps + (mode == 1 ? taps - 1 - t : t)];
+    }
+    bf16 hi, lo;
+    split2(v, hi, lo);
+    wp[i] = q ? lo : hi;
+}
+
+// channel-major fp32 (C rows of stride ld) -> split voxel-major rows [N][2Cp] bf16 =
+// [hi(0..Cp-1) | lo(0..Cp-1)], channels C..Cp-1 zero (padding to the tensor-core tile set)
+__global__ void k_split_cm(const float* __restrict__ in, long long C, long long N, long long ld, long long Cp,
+                           bf16* __restrict__ out) {
+    __shared__ float tile[32][33];
+    const long long n0 = (long long)blockIdx.x * 32, c0 = (long long)blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const long long c = c0 + i, n = n0 + threadIdx.x;
+        tile[i][threadIdx.x] = (c < C && n < N) ? in[c * ld + n] : 0.0f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const long long n = n0 + i, c = c0 + threadIdx.x;
+        if (c < Cp && n < N) {
+            bf16 hi, lo;
+            split2(tile[threadIdx.x][i], hi, lo);
+            out[n * 2 * Cp + c] = hi;
+            out[n * 2 * Cp + Cp + c] = lo;
+        }
+    }
+}
+
+// voxel-major fp32 [N][C] (C % 4 == 0) -> split rows [N][2C] bf16
+__global__ void k_split_vm(const float4* __restrict__ in, long long N, int C, bf16* __restrict__ out) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // over N * C/4
+    const int c4 = C / 4;
+    if (i >= N * c4) return;
+    const long long n = i / c4;
+    const int c = (int)(i - n * c4) * 4;
+    const float4 v = in[i];
+    bf16 h[4], l[4];
+    split2(v.x, h[0], l[0]);
+    split2(v.y, h[1], l[1]);
+    split2(v.z, h[2], l[2]);
+    split2(v.w, h[3], l[3]);
+    bf16* row = out + n * 2 * C;
+    *reinterpret_cast<uint2*>(row + c) = *reinterpret_cast<uint2*>(h);
+    *reinterpret_cast<uint2*>(row + C + c) = *reinterpret_cast<uint2*>(l);
+}
+
 // Transposed field map for the deconvolution (cnn_ops.cpp:408-419, col2hash of W^T D):
 // from the conv map pmap [n_coarse][taps] (fine column of coarse voxel p's field row t)
 // build tmap [ceil(n_fine/128)][taps][128] (tile-major): tmap[g][t] = the coarse voxel
@@ -1005,12 +1180,13 @@ __device__ __forceinline__ float to_f<bf16>(bf16 v) { return __bfloat162float(v)
 
 // voxel-major (N x C, fp32/bf16) -> channel-major fp32 (C x N)
 template <typename T>
-__global__ void k_to_channel_major(const T* __restrict__ in, long long N, long long C, float* __restrict__ out) {
+__global__ void k_to_channel_major(const T* __restrict__ in, long long N, long long C, float* __restrict__ out,
+                                   long long ld) {  // ld: input row stride (>= C)
     __shared__ float tile[32][33];
     const long long n0 = (long long)blockIdx.x * 32, c0 = (long long)blockIdx.y * 32;
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {
         const long long n = n0 + i, c = c0 + threadIdx.x;
-        tile[i][threadIdx.x] = (c < C && n < N) ? to_f<T>(in[n * C + c]) : 0.0f;
+        tile[i][threadIdx.x] = (c < C && n < N) ? to_f<T>(in[n * ld + c]) : 0.0f;
     }
     __syncthreads();
     for (int i = threadIdx.y; i < 32; i += blockDim.y) {
@@ -1024,22 +1200,18 @@ __global__ void k_to_channel_major(const T* __restrict__ in, long long N, long l
 // Forward variant: HCB_FWD_CPS = CTAs per SM (2: BN <= 64 only, so both CTAs'
 // double-buffered accumulators fit TMEM; 1: one deep ring), HCB_FWD_PW = producer warps
 // (2, 4 or 8).
-template <int BN, int CPS, int PW, typename OutT>
+template <int BN, int CPS, int PW, typename OutT, bool SUMH = false>
 void launch_fwd(const int* fmap, int taps, long long rows, const bf16* X, int C, const bf16* Wp, int Kp, OutT* Y,
-                cudaStream_t s) {
+                cudaStream_t s, int skip_lolo = 0) {
     using Cfg = FwdCfg<BN, CPS, PW, sizeof(OutT)>;
-    auto kern = k_conv_fwd<BN, CPS, PW, OutT>;
-    static bool attr = false;  // per instantiation
-    if (!attr) {
-        cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM), "smem attr");
-        attr = true;
-    }
+    auto kern = k_conv_fwd<BN, CPS, PW, OutT, SUMH>;
+    smem_optin(kern, Cfg::SMEM);
     const CUtensorMap wm = map2d(Wp, (uint64_t)Kp, (uint64_t)BN, (uint64_t)Kp * 2, BN);
     const int tiles = (int)((rows + BM - 1) / BM);
     const int grid = std::min(tiles, CPS * num_sms());
-    const CUtensorMap ym = map_out(Y, sizeof(OutT) == 4, (uint64_t)BN, (uint64_t)rows, 16, 32);
-    kern<<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(wm, ym, fmap, taps, rows, X, C, Kp / BK, tiles);
-    launched("conv gather-GEMM (tcgen05)");
+    const CUtensorMap ym = map_out(Y, sizeof(OutT) == 4, (uint64_t)(SUMH ? BN / 2 : BN), (uint64_t)rows, 16, 32);
+    kern<<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(wm, ym, fmap, taps, rows, X, C, Kp / BK, tiles, skip_lolo);
+    launched(SUMH ? "conv gather-GEMM, split precision (tcgen05)" : "conv gather-GEMM (tcgen05)");
 }
 
 // CTA-pair forward (k_conv_fwd_pair): clusters of 2, two CTAs per SM.
@@ -1048,11 +1220,7 @@ void launch_fwd_pair(const int* fmap, int taps, long long rows, const bf16* X, i
                      cudaStream_t s) {
     using Cfg = FwdCfg<BN, CPS, PW, sizeof(OutT)>;
     auto kern = k_conv_fwd_pair<BN, PW, OutT, CPS>;
-    static bool attr = false;
-    if (!attr) {
-        cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM), "smem attr");
-        attr = true;
-    }
+    smem_optin(kern, Cfg::SMEM);
     const CUtensorMap wm = map2d(Wp, (uint64_t)Kp, (uint64_t)BN, (uint64_t)Kp * 2, BN / 2);
     const CUtensorMap ym = map_out(Y, sizeof(OutT) == 4, (uint64_t)BN, (uint64_t)rows, 16, 32);
     const int tiles = (int)((rows + BM - 1) / BM);
@@ -1097,6 +1265,32 @@ void launch_fwd_bn(const int* fmap, int taps, long long rows, const bf16* X, int
     launch_fwd<BN, 1, 8>(fmap, taps, rows, X, C, Wp, Kp, Y, s);
 }
 
+// Split-precision forward: BN = 2 x output channels (hi and lo weight planes), fp32 output.
+// Two CTAs per SM where both CTAs' double-buffered accumulators fit TMEM (BN <= 128; C 64->64:
+// 1.35 vs 1.66 ms with one CTA and a deeper ring), else one (HCB_X2_CPS=1 forces it).
+template <int BN>
+void launch_fwd_x2(const int* fmap, int taps, long long rows, const bf16* X, int C, const bf16* Wp, int Kp, float* Y,
+                   cudaStream_t s, int skip_lolo) {
+    static const int cps = env_int("HCB_X2_CPS", BN <= 128 ? 2 : 1);
+    if constexpr (BN <= 128) {
+        if (cps == 2) return launch_fwd<BN, 2, 4, float, true>(fmap, taps, rows, X, C, Wp, Kp, Y, s, skip_lolo);
+    }
+    launch_fwd<BN, 1, 4, float, true>(fmap, taps, rows, X, C, Wp, Kp, Y, s, skip_lolo);
+}
+
+void conv_fwd_x2(const int* fmap, int taps, long long rows, const bf16* X, int C2, const bf16* Wp, int Kp, int N2,
+                 float* Y, cudaStream_t s) {
+    static const int keep_lolo = env_int("HCB_X2_LOLO", 0);
+    const int skip = (!keep_lolo && (C2 / 2) % 16 == 0) ? 1 : 0;
+    switch (N2) {
+        case 32: launch_fwd_x2<32>(fmap, taps, rows, X, C2, Wp, Kp, Y, s, skip); break;
+        case 64: launch_fwd_x2<64>(fmap, taps, rows, X, C2, Wp, Kp, Y, s, skip); break;
+        case 128: launch_fwd_x2<128>(fmap, taps, rows, X, C2, Wp, Kp, Y, s, skip); break;
+        case 256: launch_fwd_x2<256>(fmap, taps, rows, X, C2, Wp, Kp, Y, s, skip); break;
+        default: throw std::invalid_argument("native conv (split precision): output channels must be 16, 32, 64 or 128");
+    }
+}
+
 template <typename OutT>
 void conv_fwd(const int* fmap, int taps, long long rows, const bf16* X, int C, const bf16* Wp, int Kp, int N, OutT* Y,
               cudaStream_t s) {
@@ -1128,17 +1322,27 @@ struct DwPlan {
     long long partial_floats;
 };
 
-DwPlan dw_plan(long long rows, int taps, int cin, int cout) {
+// max_tps > 0 caps a split's voxel tiles (the length of one TMEM accumulation chain).
+// pair: split precision — cin / cout are the channels of one plane, the GEMM runs on rows of
+// 2 cin (X) and 2 cout (dY) with 64 (t, ci) rows x both planes per m-tile (DwGroups).
+DwPlan dw_plan(long long rows, int taps, int cin, int cout, int max_tps = 0, bool pair = false) {
     DwPlan p{};
-    p.nb = dw_nb(cout);
-    p.mt = (taps * cin + BM - 1) / BM;
+    const int rpm = pair ? 64 : BM;
+    p.nb = dw_nb(pair ? 2 * cout : cout);
+    p.mt = (taps * cin + rpm - 1) / rpm;
     p.cps = dw_cps(p.nb);
     p.tiles = (int)((rows + BM - 1) / BM);
-    const int cap = 512 / (p.nb * p.cps);
-    const int G = std::min(kMaxGroups, (p.mt + cap - 1) / cap);
+    const int cap = 512 / (p.nb * p.cps);  // m-tiles whose accumulators fit one CTA's TMEM
+    const int G = (p.mt + cap - 1) / cap;  // -> every group has <= cap m-tiles
+    if (G > kMaxGroups)
+        throw std::invalid_argument("native conv: dW supports at most " + std::to_string(kMaxGroups * cap * BM) +
+                                    " (taps x input channels) rows at " + std::to_string(cout) + " output channels");
     const int slots = num_sms() * p.cps;
     DwGroups& g = p.g;
     g.groups = G;
+    g.pair = pair ? 1 : 0;
+    g.rpm = rpm;
+    g.pcols = pair ? cout : p.nb;
     // Few groups (C_out <= 64): CTAs proportional to each group's m-tiles, so groups of
     // 4 and 3 m-tiles finish together (C=64: 0.667 -> 0.607 ms). Many groups (C_out >= 128,
     // 14+ groups re-reading dY): equal voxel splits in lockstep, so one range's dY tile and
@@ -1158,17 +1362,18 @@ DwPlan dw_plan(long long rows, int taps, int cin, int cout) {
             want = std::max(1, std::min(p.tiles, end - g.cta_begin[i]));
         }
         g.tps[i] = std::max(1, (p.tiles + want - 1) / want);
+        if (max_tps > 0) g.tps[i] = std::min(g.tps[i], max_tps);
         const int splits = std::max(1, (p.tiles + g.tps[i] - 1) / g.tps[i]);
         g.cta_begin[i + 1] = g.cta_begin[i] + splits;
         g.part_begin[i] = part;
-        part += (long long)splits * mg * BM * p.nb;
+        part += (long long)splits * mg * rpm * g.pcols;
     }
     p.ctas = g.cta_begin[G];
     p.partial_floats = part;
     p.max_taps = 0;  // widest tap range any group's m-tiles touch
     for (int i = 0; i < G; ++i) {
-        const int lo = g.m_begin[i] * 128 / cin;
-        const int hi = (std::min(taps * cin, g.m_begin[i + 1] * 128) - 1) / cin;
+        const int lo = g.m_begin[i] * rpm / cin;
+        const int hi = (std::min(taps * cin, g.m_begin[i + 1] * rpm) - 1) / cin;
         p.max_taps = std::max(p.max_taps, hi - lo + 1);
     }
     return p;
@@ -1179,11 +1384,7 @@ void launch_dw_pw(const DwPlan& p, const int* fmap, int taps, long long rows, co
                   int Cout, float* partial, cudaStream_t s) {
     using Cfg = DwCfg<NB, PW, CPS, NT>;
     auto kern = k_conv_dw<NB, PW, CPS, NT>;
-    static bool attr = false;
-    if (!attr) {
-        cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM), "smem attr");
-        attr = true;
-    }
+    smem_optin(kern, Cfg::SMEM);
     // dY [rows][Cout] bf16: boxes of 64 voxels x 64 channels; channels >= Cout and voxels
     // >= rows are out of bounds -> zero.
     const CUtensorMap dm = map2d(dY, (uint64_t)Cout, (uint64_t)rows, (uint64_t)Cout * 2, 64);
@@ -1235,7 +1436,97 @@ struct TiledMap {
     TiledMap& operator=(const TiledMap&) = delete;
 };
 
+int x2_dw_tps() {
+    // One TMEM accumulation chain covers at most HCB_X2_DW_TPS voxel tiles (default 32 = 4096
+    // voxels): the tensor core's fp32 accumulation over hundreds of thousands of products
+    // drifts past the 1e-5 contract (256^3 x 8, C 64: 9e-5 unbounded, 7.5e-6 at 64 tiles,
+    // 4.3e-6 at 32, 3.4e-6 at 16), the fixed-order split reduction does not.
+    static const int v = env_int("HCB_X2_DW_TPS", 32);
+    return v;
+}
+
 }  // namespace
+
+// ---------------------------------------------------------------- reference-signature FAST route
+// conv_forward / conv_backward (cnn_ops.cpp:206-232) in HC_MATH_FAST on a stride-1 layer over
+// one structure: the fused split-precision implicit GEMM instead of hash2col + 3xTF32 GEMMs over
+// the materialised column matrix. Reference layout in and out; channels zero-padded to the
+// tile set inside.
+static int tile_ch(int c) { return c <= 16 ? 16 : c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : 256; }
+
+bool fused_x2_eligible(const hc_psh* in, const hc_psh* out, hc_conv_spec sp, int taps) {
+    static const int on = env_int("HCB_FAST_FUSED", 1);
+    return on && in == out && sp.stride == 1 && taps >= 1 && taps <= kMaxTaps && sp.in_channels > 0 &&
+           sp.out_channels > 0 && tile_ch(sp.in_channels) <= 128 && tile_ch(sp.out_channels) <= 128;
+}
+
+namespace {
+struct FusedMap {
+    Scratch buf;
+    FusedMap(const hc_psh* in, hc_conv_spec sp, int taps, long long N, cudaStream_t s)
+        : buf((size_t)((N + 127) / 128) * 128 * taps * 4, s) {
+        const hc_status st = hc_field_map_tiled(in, in, sp, buf.as<int32_t>(), reinterpret_cast<hc_stream>(s));
+        if (st != HC_OK) throw std::runtime_error(hc_last_error());
+    }
+};
+void split_cm(const float* src, long long C, long long N, long long ld, long long Cp, bf16* out, cudaStream_t s) {
+    dim3 g((unsigned)((N + 31) / 32), (unsigned)((Cp + 31) / 32)), b(32, 8);
+    k_split_cm<<<g, b, 0, s>>>(src, C, N, ld, Cp, out);
+    launched("split fp32 -> bf16 hi/lo planes");
+}
+void pack_x2(const float* w, int cout, int cin, int taps, int mode, int cout_p, int cin_p, bf16* wp, int Kp2,
+             cudaStream_t s) {
+    const long long n = 2LL * (mode ? cin_p : cout_p) * Kp2;
+    k_pack_w_x2<<<grid_for(n, 256), 256, 0, s>>>(w, cout, cin, taps, mode, Kp2, wp, cout_p, cin_p);
+    launched("pack weights (split precision)");
+}
+void to_cm(const float* y, long long N, long long C, long long ld, float* out, cudaStream_t s) {
+    dim3 g((unsigned)((N + 31) / 32), (unsigned)((C + 31) / 32)), b(32, 8);
+    k_to_channel_major<float><<<g, b, 0, s>>>(y, N, C, out, ld);
+    launched("to channel-major");
+}
+}  // namespace
+
+void fused_conv_forward_f32(const hc_psh* in, const float* data, const float* w, hc_conv_spec sp, int taps,
+                            long long N, float* result, cudaStream_t s) {
+    const int cin = sp.in_channels, cout = sp.out_channels, cin_p = tile_ch(cin), cout_p = tile_ch(cout);
+    const FusedMap fm(in, sp, taps, N, s);
+    const int Kp2 = (int)hc_native_packed_k_x2(cin_p, taps);
+    Scratch xs((size_t)N * 2 * cin_p * 2, s), wp((size_t)2 * cout_p * Kp2 * 2, s), y((size_t)N * cout_p * 4, s);
+    split_cm(data, cin, N, N, cin_p, xs.as<bf16>(), s);
+    pack_x2(w, cout, cin, taps, 0, cout_p, cin_p, wp.as<bf16>(), Kp2, s);
+    conv_fwd_x2(fm.buf.as<int>(), taps, N, xs.as<bf16>(), 2 * cin_p, wp.as<bf16>(), Kp2, 2 * cout_p, y.as<float>(), s);
+    to_cm(y.as<float>(), N, cout, cout_p, result, s);
+}
+
+// conv_backward's input is not passed (only the cached column matrix): for a stride-1 field
+// over one structure the centre field row of column n IS input column n (the voxel itself,
+// always present), so X = cached_cols rows c * taps + (taps - 1) / 2.
+void fused_conv_backward_f32(const float* dy, const float* w, const float* cols, const hc_psh* in, hc_conv_spec sp,
+                             int taps, long long N, float* dw, float* dx, cudaStream_t s) {
+    const int cin = sp.in_channels, cout = sp.out_channels, cin_p = tile_ch(cin), cout_p = tile_ch(cout);
+    const FusedMap fm(in, sp, taps, N, s);
+    const int Kp2 = (int)hc_native_packed_k_x2(cout_p, taps);
+    Scratch xs((size_t)N * 2 * cin_p * 2, s), dys((size_t)N * 2 * cout_p * 2, s);
+    Scratch wp((size_t)2 * cin_p * Kp2 * 2, s), dxp((size_t)N * cin_p * 4, s);
+    split_cm(cols + (long long)((taps - 1) / 2) * N, cin, N, (long long)taps * N, cin_p, xs.as<bf16>(), s);
+    split_cm(dy, cout, N, N, cout_p, dys.as<bf16>(), s);
+    const DwPlan p = dw_plan(N, taps, cin_p, cout_p, x2_dw_tps(), true);
+    Scratch part((size_t)p.partial_floats * 4, s);
+    const int C2 = 2 * cin_p, Co2 = 2 * cout_p;
+    switch (p.nb) {
+        case 64: launch_dw<64>(p, fm.buf.as<int>(), taps, N, xs.as<bf16>(), C2, dys.as<bf16>(), Co2, part.as<float>(), s); break;
+        case 128: launch_dw<128>(p, fm.buf.as<int>(), taps, N, xs.as<bf16>(), C2, dys.as<bf16>(), Co2, part.as<float>(), s); break;
+        default: launch_dw<256>(p, fm.buf.as<int>(), taps, N, xs.as<bf16>(), C2, dys.as<bf16>(), Co2, part.as<float>(), s); break;
+    }
+    const long long total = (long long)cout_p * cin_p * taps;
+    k_reduce_dw<<<grid_for(total, 32), 256, 0, s>>>(part.as<float>(), p.g, taps, cin_p, cout_p, dw, cin, cout);
+    launched("dW split reduction (split precision)");
+    pack_x2(w, cout, cin, taps, 1, cout_p, cin_p, wp.as<bf16>(), Kp2, s);
+    conv_fwd_x2(fm.buf.as<int>(), taps, N, dys.as<bf16>(), Co2, wp.as<bf16>(), Kp2, 2 * cin_p, dxp.as<float>(), s);
+    to_cm(dxp.as<float>(), N, cin, cin_p, dx, s);
+}
+
 }  // namespace hcb
 
 using namespace hcb;
@@ -1290,8 +1581,9 @@ hc_status hc_native_gather_gemm(const int32_t* fmap, int32_t fmap_layout, int64_
 }
 
 size_t hc_native_dw_workspace(int64_t n_out, int32_t taps, int32_t c_in, int32_t c_out) {
-    const DwPlan p = dw_plan(n_out, taps, c_in, c_out);
-    return (size_t)p.partial_floats * sizeof(float);
+    size_t r = 0;  // 0 = unsupported shape (hc_native_conv_dw reports why)
+    const hc_status st = guard([&] { r = (size_t)dw_plan(n_out, taps, c_in, c_out).partial_floats * sizeof(float); });
+    return st == HC_OK ? r : 0;
 }
 
 hc_status hc_native_conv_dw(const int32_t* fmap, int32_t fmap_layout, int64_t n_out, int32_t taps, const void* x,
@@ -1318,8 +1610,98 @@ hc_status hc_native_conv_dw(const int32_t* fmap, int32_t fmap_layout, int64_t n_
             default: launch_dw<256>(p, fm.p, taps, n_out, X, c_in, DY, c_out, part, s); break;
         }
         const long long total = (long long)c_out * c_in * taps;
-        k_reduce_dw<<<grid_for(total, 32), 256, 0, s>>>(part, p.g, p.nb, taps, c_in, c_out, dw_ref);
+        k_reduce_dw<<<grid_for(total, 32), 256, 0, s>>>(part, p.g, taps, c_in, c_out, dw_ref, c_in, c_out);
         launched("dW split reduction");
+    });
+}
+
+// ---------------------------------------------------------------- split precision (fp32-accurate)
+int64_t hc_native_packed_k_x2(int32_t c, int32_t taps) { return ((int64_t)2 * c * taps + 63) / 64 * 64; }
+
+hc_status hc_native_split(const float* src, int32_t channel_major, int64_t c, int64_t n, void* out,
+                          hc_stream stream) {
+    return guard([&] {
+        if (c <= 0 || c % 4 != 0) throw std::invalid_argument("native split: channels must be a positive multiple of 4");
+        if (n <= 0) return;
+        cudaStream_t s = as_stream(stream);
+        bf16* o = static_cast<bf16*>(out);
+        if (channel_major) {
+            dim3 g((unsigned)((n + 31) / 32), (unsigned)((c + 31) / 32)), b(32, 8);
+            k_split_cm<<<g, b, 0, s>>>(src, c, n, n, c, o);
+        } else {
+            const long long total = n * (c / 4);
+            k_split_vm<<<grid_for(total, 256), 256, 0, s>>>(reinterpret_cast<const float4*>(src), n, (int)c, o);
+        }
+        launched("split fp32 -> bf16 hi/lo planes");
+    });
+}
+
+hc_status hc_native_pack_weights_x2(const float* w_ref, int32_t c_out, int32_t c_in, int32_t taps, int32_t mode,
+                                    void* w_packed, hc_stream stream) {
+    return guard([&] {
+        check_native(c_in, c_out, taps);
+        if (mode < 0 || mode > 2) throw std::invalid_argument("native conv: pack mode must be 0, 1 or 2");
+        const int rows = mode ? c_in : c_out;
+        const long long Kp2 = hc_native_packed_k_x2(mode ? c_out : c_in, taps);
+        const long long n = 2LL * rows * Kp2;
+        k_pack_w_x2<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(w_ref, c_out, c_in, taps, mode, (int)Kp2,
+                                                                      static_cast<bf16*>(w_packed), c_out, c_in);
+        launched("pack weights (split precision)");
+    });
+}
+
+hc_status hc_native_gather_gemm_x2(const int32_t* fmap, int32_t fmap_layout, int64_t n_out, int32_t taps,
+                                   const void* x_split, int32_t c_in, const void* w_packed_x2, int32_t c_out,
+                                   float* y, hc_stream stream) {
+    return guard([&] {
+        check_native(c_in, c_out, taps);
+        if (c_out > 128) throw std::invalid_argument("native conv (split precision): at most 128 output channels");
+        if (n_out <= 0) return;
+        cudaStream_t s = as_stream(stream);
+        const int Kp2 = (int)hc_native_packed_k_x2(c_in, taps);
+        const TiledMap fm(fmap, fmap_layout, n_out, taps, s);
+        conv_fwd_x2(fm.p, taps, n_out, static_cast<const bf16*>(x_split), 2 * c_in,
+                    static_cast<const bf16*>(w_packed_x2), Kp2, 2 * c_out, y, s);
+    });
+}
+
+size_t hc_native_dw_workspace_x2(int64_t n_out, int32_t taps, int32_t c_in, int32_t c_out) {
+    size_t r = 0;
+    const hc_status st = guard([&] {
+        const DwPlan p = dw_plan(n_out, taps, c_in, c_out, x2_dw_tps(), true);
+        r = (size_t)p.partial_floats * sizeof(float);
+    });
+    return st == HC_OK ? r : 0;
+}
+
+hc_status hc_native_conv_dw_x2(const int32_t* fmap, int32_t fmap_layout, int64_t n_out, int32_t taps,
+                               const void* x_split, int32_t c_in, const void* dy_split, int32_t c_out, float* dw_ref,
+                               void* workspace, size_t ws_bytes, hc_stream stream) {
+    return guard([&] {
+        check_native(c_in, c_out, taps);
+        if (c_out > 128) throw std::invalid_argument("native conv (split precision): dW supports up to 128 output channels");
+        cudaStream_t s = as_stream(stream);
+        if (n_out <= 0) {
+            cuda_check(cudaMemsetAsync(dw_ref, 0, sizeof(float) * c_out * c_in * taps, s), "memset");
+            return;
+        }
+        const int C2 = 2 * c_in, Co2 = 2 * c_out;
+        if (c_out % 16 != 0) throw std::invalid_argument("native conv (split precision): dW output channels must be a multiple of 16");
+        const DwPlan p = dw_plan(n_out, taps, c_in, c_out, x2_dw_tps(), true);
+        if (ws_bytes < (size_t)p.partial_floats * sizeof(float))
+            throw std::invalid_argument("native conv: dW workspace too small");
+        float* part = static_cast<float*>(workspace);
+        const TiledMap fm(fmap, fmap_layout, n_out, taps, s);
+        const bf16* X = static_cast<const bf16*>(x_split);
+        const bf16* DY = static_cast<const bf16*>(dy_split);
+        switch (p.nb) {
+            case 64: launch_dw<64>(p, fm.p, taps, n_out, X, C2, DY, Co2, part, s); break;
+            case 128: launch_dw<128>(p, fm.p, taps, n_out, X, C2, DY, Co2, part, s); break;
+            default: launch_dw<256>(p, fm.p, taps, n_out, X, C2, DY, Co2, part, s); break;
+        }
+        const long long total = (long long)c_out * c_in * taps;
+        k_reduce_dw<<<grid_for(total, 32), 256, 0, s>>>(part, p.g, taps, c_in, c_out, dw_ref, c_in, c_out);
+        launched("dW split reduction (split precision)");
     });
 }
 
@@ -1338,9 +1720,9 @@ hc_status hc_native_to_channel_major(const void* native, hc_dtype dtype, int64_t
         if (c <= 0 || n <= 0) return;
         dim3 g((unsigned)((n + 31) / 32), (unsigned)((c + 31) / 32)), b(32, 8);
         if (dtype == HC_DTYPE_F32)
-            k_to_channel_major<float><<<g, b, 0, as_stream(stream)>>>(static_cast<const float*>(native), n, c, out);
+            k_to_channel_major<float><<<g, b, 0, as_stream(stream)>>>(static_cast<const float*>(native), n, c, out, c);
         else
-            k_to_channel_major<bf16><<<g, b, 0, as_stream(stream)>>>(static_cast<const bf16*>(native), n, c, out);
+            k_to_channel_major<bf16><<<g, b, 0, as_stream(stream)>>>(static_cast<const bf16*>(native), n, c, out, c);
         launched("to channel-major");
     });
 }

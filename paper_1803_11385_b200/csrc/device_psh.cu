@@ -7,6 +7,8 @@
 #include <algorithm>
 #include <atomic>
 #include <cstring>
+#include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -55,6 +57,18 @@ namespace {
 std::atomic<long long> g_launches{0};
 }
 void count_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+long long fused_route_count(long long add) {
+    static std::atomic<long long> n{0};
+    return n.fetch_add(add, std::memory_order_relaxed) + add;
+}
+
+bool smem_optin_needed(const void* kern, int dev) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    std::lock_guard<std::mutex> lock(mu);
+    return done.insert({kern, dev}).second;
+}
 
 namespace {
 
@@ -234,6 +248,7 @@ extern "C" {
 const char* hc_last_error(void) { return g_last_error.c_str(); }
 const char* hc_version(void) { return "hashconv_b200 0.1 (sm_100a)"; }
 int64_t hc_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+int64_t hc_fused_route_count(void) { return hcb::fused_route_count(0); }
 
 hc_status hc_malloc(void** ptr, size_t bytes) {
     return guard([&] { *ptr = dev_alloc(bytes); });

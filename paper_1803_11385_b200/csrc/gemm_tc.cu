@@ -403,11 +403,7 @@ void launch(const float* asrc, const float* bsrc, float* C, long long ra, long l
             const float* blo = nullptr) {
     using Cfg = GCfg<BN, SPLIT>;
     auto kern = k_gemm_tf32<AMN, BMN, BN, SPLIT>;
-    static bool attr = false;
-    if (!attr) {
-        cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM), "smem attr");
-        attr = true;
-    }
+    smem_optin(kern, Cfg::SMEM);
     const CUtensorMap am = AMN ? fmap2d(asrc, cb, K, 32, 32, true) : fmap2d(asrc, K, cb, 32, BM, false);
     const CUtensorMap bm = BMN ? fmap2d(bsrc, ra, K, 32, 32, true) : fmap2d(bsrc, K, ra, 32, BN, false);
     const CUtensorMap blm = SPLIT == 5 ? fmap2d(blo, K, ra, 32, BN, false) : bm;

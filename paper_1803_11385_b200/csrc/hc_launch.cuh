@@ -23,6 +23,17 @@ inline void launched(const char* what, long long n = 1) {
 
 inline cudaStream_t as_stream(hc_stream s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// The dynamic shared-memory opt-in is a per-device-context attribute: set it once per
+// (kernel, device), so a process driving several GPUs sets it on each.
+bool smem_optin_needed(const void* kern, int dev);  // records (kern, dev) on first query
+template <typename K>
+void smem_optin(K kern, int bytes) {
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    if (!smem_optin_needed(reinterpret_cast<const void*>(kern), dev)) return;
+    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "smem attr");
+}
+
 inline unsigned grid_for(long long n, int threads) {
     return static_cast<unsigned>((n + threads - 1) / threads);
 }
@@ -50,6 +61,15 @@ struct Scratch {
         return static_cast<T*>(p);
     }
 };
+
+// Reference-signature conv in HC_MATH_FAST on the fused split-precision tensor-core path
+// (conv_tc.cu): eligible for a stride-1 field over one structure with <= 128 channels.
+bool fused_x2_eligible(const hc_psh* in, const hc_psh* out, hc_conv_spec sp, int taps);
+long long fused_route_count(long long add);  // hc_fused_route_count
+void fused_conv_forward_f32(const hc_psh* in, const float* data, const float* w, hc_conv_spec sp, int taps,
+                            long long N, float* result, cudaStream_t s);
+void fused_conv_backward_f32(const float* dy, const float* w, const float* cols, const hc_psh* in, hc_conv_spec sp,
+                             int taps, long long N, float* dw, float* dx, cudaStream_t s);
 
 // Exact GEMMs (gemm_exact.cu) — reference accumulation order, fp32 and fp64.
 void gemm_nn_exact(const float* a, const float* b, float* c, long long ra, long long k, long long cb, cudaStream_t s);

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <type_traits>
 #include <string>
 
 #include "dev_psh.cuh"
@@ -909,6 +910,13 @@ hc_status conv_forward_impl(const hc_psh* in, const T* data, int64_t data_rows, 
             throw std::invalid_argument("hash2col: input data shape mismatch");
         cudaStream_t s = as_stream(stream);
         const long long K = spec.in_channels * fd, N = out->d.N;
+        if constexpr (std::is_same_v<T, float>) {
+            if (current_math() == HC_MATH_FAST && N > 0 && fused_x2_eligible(in, out, spec, (int)fd)) {
+                fused_conv_forward_f32(in, data, w, spec, (int)fd, N, result, s);  // no column matrix
+                fused_route_count(1);
+                return;
+            }
+        }
         Scratch cols(sizeof(T) * K * N, s);
         launch_hash2col(in, data, out, spec, cols.as<T>(), s);
         gemm_nn(w, cols.as<T>(), result, spec.out_channels, K, N, s);
@@ -932,6 +940,13 @@ hc_status conv_backward_impl(const T* output_grad, int64_t g_rows, int64_t g_col
         check_pair(in, out, spec);
         if (w_cols != spec.in_channels * fd) throw std::invalid_argument("col2hash: column gradient shape mismatch");
         cudaStream_t s = as_stream(stream);
+        if constexpr (std::is_same_v<T, float>) {
+            if (current_math() == HC_MATH_FAST && g_cols > 0 && fused_x2_eligible(in, out, spec, (int)fd)) {
+                fused_conv_backward_f32(output_grad, w, cached_cols, in, spec, (int)fd, g_cols, dw, dx, s);
+                fused_route_count(1);
+                return;
+            }
+        }
         gemm_nt(output_grad, cached_cols, dw, g_rows, g_cols, c_rows, s);  // dW = dDo * cols^T
         Scratch dcols(sizeof(T) * w_cols * g_cols, s);
         gemm_tn(w, output_grad, dcols.as<T>(), w_rows, w_cols, g_cols, s);  // W^T * dDo

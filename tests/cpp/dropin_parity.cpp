@@ -139,6 +139,59 @@ static void layer_ops_equal(std::uint64_t seed) {
     CHECK(hb::dropout_backward(dy, m2, T(0.4)) == dropout_backward(dy, m1, T(0.4)), "dropout_backward");
 }
 
+template <class T>
+static double norm_rel(const FeatureMatrixT<T>& a, const FeatureMatrixT<double>& b) {
+    double num = 0, den = 0;
+    for (size_t i = 0; i < a.values.size(); ++i) {
+        const double d = double(a.values[i]) - b.values[i];
+        num += d * d;
+        den += b.values[i] * b.values[i];
+    }
+    return den > 0 ? std::sqrt(num / den) : std::sqrt(num);
+}
+
+static FeatureMatrixT<double> to64(const FeatureMatrix& m) {
+    FeatureMatrixT<double> r(m.rows, m.cols);
+    for (size_t i = 0; i < m.values.size(); ++i) r.values[i] = m.values[i];
+    return r;
+}
+
+// HC_MATH_FAST: the unchanged reference-signature float calls conv_forward / conv_backward of a
+// stride-1 layer over one structure run the fused split-precision tensor-core conv (no column
+// matrix; hc_fused_route_count proves the route) and land within 1e-5 (normwise) of the
+// reference's own double instantiation on the same fp32 inputs.
+static void fast_conv_close(int cin, int cout, std::uint64_t seed) {
+    std::vector<PshLevel> fl;
+    for (int k = 0; k < 2; ++k) {
+        const SparseVoxelSet s = testing::random_sparse_set(32, 3000 + 500 * k, mix_seed(seed, k));
+        PshBuildOptions o;
+        o.seed = mix_seed(seed, 20 + k);
+        fl.push_back(build_psh(s, o));
+    }
+    const SuperPsh fine = build_super(fl);
+    const ConvSpec spec{3, 1, 0, cin, cout};
+    const auto data = testing::random_matrix<float>(cin, fine.total_columns(), seed);
+    const KernelWeightsT<float> w{testing::random_matrix<float>(cout, cin * 27, seed + 1)};
+    const auto dout = testing::random_matrix<float>(cout, fine.total_columns(), seed + 2);
+    const auto data64 = to64(data), dout64 = to64(dout);
+    const KernelWeightsT<double> w64{to64(w.w)};
+    const auto y64 = conv_forward(fine, data64, fine, w64, spec);
+    const auto g64 = conv_backward(dout64, w64, hash2col(fine, data64, fine, spec), fine, fine, spec);
+    const auto cols = hash2col(fine, data, fine, spec);
+    const auto routed0 = hc_fused_route_count();
+    hb::set_fast_math(true);
+    const auto y = hb::conv_forward(fine, data, fine, w, spec);
+    const auto g = hb::conv_backward(dout, w, cols, fine, fine, spec);
+    hb::set_fast_math(false);
+    const char* tag = "FAST conv (fused split precision) within 1e-5 of the reference's double";
+    CHECK(hc_fused_route_count() - routed0 == 2, "FAST conv_forward/backward took the fused route");
+    CHECK(norm_rel(y, y64) <= 1e-5, tag);
+    CHECK(norm_rel(g.weights, g64.weights) <= 1e-5, tag);
+    CHECK(norm_rel(g.input, g64.input) <= 1e-5, tag);
+    std::printf("fast conv %d->%d: y %.3g dW %.3g dX %.3g (vs reference double)\n", cin, cout, norm_rel(y, y64),
+                norm_rel(g.weights, g64.weights), norm_rel(g.input, g64.input));
+}
+
 static SuperPsh single(const Coord& p, int res, float value) {
     FeatureMatrix f(1, 1);
     f.at(0, 0) = value;
@@ -205,6 +258,9 @@ int main() {
         ops_equal<float>(fx, specs[t % 4], 100 + t);
         ops_equal<double>(fx, specs[t % 4], 200 + t);  // the reference's double instantiation
     }
+    fast_conv_close(3, 5, 31);
+    fast_conv_close(64, 64, 32);
+    fast_conv_close(16, 128, 33);
     layer_ops_equal<float>(77);
     layer_ops_equal<double>(78);
     std::printf("%s: %d checks, %d failures\n", g_fail ? "DROPIN FAIL" : "DROPIN OK", g_checks, g_fail);

@@ -474,7 +474,10 @@ def test_full_size_int64_index_paths(shell256):
     """C = 64 at BASELINE config 4 size: the column matrix has 27 * 64 * 1,826,368 = 3.2e9
     elements (> 2^31), so hash2col's and the contraction's 64-bit index math is exercised.
     The centre-tap identity kernel must reproduce the input exactly (EXACT math: the zero
-    weights are skipped like gemm.cpp:21) and to fp32 accuracy through 3xTF32 (FAST)."""
+    weights are skipped like gemm.cpp:21) and to fp32 accuracy through 3xTF32 over the
+    materialised column matrix (FAST matmul). FAST conv_forward itself routes to the fused
+    split-precision conv (hc_fused_route_count), whose identity error is the hi/lo split's
+    representation bound, |y - x| <= 2^-17 |x| elementwise."""
     fine, _ = shell256
     C = 64
     n = fine.total_columns()
@@ -485,9 +488,16 @@ def test_full_size_int64_index_paths(shell256):
     w = torch.zeros((C, C * 27), device="cuda")
     w.view(C, C, 27)[torch.arange(C), torch.arange(C), 13] = 1.0
     assert torch.equal(ops.conv_forward(fine, x, fine, w, sp), x)
+    from paper_1803_11385_b200._lib import lib
     with ops.math_mode("fast"):
-        y = ops.conv_forward(fine, x, fine, w, sp)
+        cols = ops.hash2col(fine, x, fine, sp)
+        y = ops.matmul(w, cols)  # 3xTF32 over the 3.2e9-element column matrix
+        del cols
+        routed = lib.hc_fused_route_count()
+        yf = ops.conv_forward(fine, x, fine, w, sp)
+        assert lib.hc_fused_route_count() == routed + 1
     assert float((y - x).abs().max()) <= 1e-6
+    assert bool(((yf - x).abs() <= 2.0 ** -17 * x.abs()).all())
 
 
 def test_split_super_round_trip(cuda):
