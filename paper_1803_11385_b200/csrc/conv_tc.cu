@@ -671,8 +671,11 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, PW, sizeof(OutT)>::THREADS, CP
 // so each dY stage is loaded once and feeds all of them (the previous one-m-tile-per-
 // CTA plan re-read dY mt = 14 times at C=64).
 // Split plan, passed by value: group g owns m-tiles [m_begin[g], m_begin[g+1]) and CTAs
-// [cta_begin[g], cta_begin[g+1]), each CTA a run of tps[g] voxel tiles; its partials start
-// at part_begin[g] (floats), laid out [split][m-tile][rpm][pcols].
+// [cta_begin[g], cta_begin[g+1]). Its voxel range is cut into nchunk[g] chunks of tps[g] voxel
+// tiles; CTA k of the group runs chunks [k*cpc[g], (k+1)*cpc[g]) back to back, draining its
+// TMEM accumulators into one partial slot per chunk (a chunk is one accumulation chain: the
+// split-precision path bounds it to keep the tensor core's fp32 accumulation within 1e-5).
+// Partials start at part_begin[g] (floats), laid out [chunk][m-tile][rpm][pcols]:
 //   plain: rpm = 128 (t,ci) rows of the row width C, pcols = NB.
 //   pair (split precision, hc_native_conv_dw_x2): X rows are [hi | lo] (C = 2 c), dY rows
 //     [hi | lo] (2 c_out); m-tile j's 64-row blocks are the hi and the lo plane of the same 64
@@ -685,6 +688,8 @@ struct DwGroups {
     int m_begin[kMaxGroups + 1];
     int cta_begin[kMaxGroups + 1];
     int tps[kMaxGroups];
+    int nchunk[kMaxGroups];
+    int cpc[kMaxGroups];
     long long part_begin[kMaxGroups];
 };
 
@@ -700,12 +705,14 @@ struct DwCfg {
 #endif
     static constexpr int BSTAGES = HCB_DW_BSTAGES;
     static constexpr int NBR = 2 * NT * BM * 4;
-    static constexpr int BUDGET = (CPS == 2 ? 113 : 226) * 1024 - 1024 - 512 - 1024 - NBR - BSTAGES * B_BYTES;
+    static constexpr int XCH = 64 * 20 * 4;  // pair-mode epilogue exchange: 64 rows x 16 (+4 pad) floats
+    static constexpr int BUDGET = (CPS == 2 ? 113 : 226) * 1024 - 1024 - 512 - 1024 - NBR - BSTAGES * B_BYTES - XCH;
     static constexpr int STAGES = BUDGET / A_BYTES > 10 ? 10 : BUDGET / A_BYTES;
     static constexpr int PRODUCERS = PW * 32;
-    static constexpr int THREADS = PRODUCERS + 64;  // + MMA / TMEM warp PW, dY TMA warp PW+1
-    static constexpr int TMEM_COLS = 512 / CPS;     // per CTA (CPS resident CTAs per SM)
-    static constexpr int SMEM = 1024 + STAGES * A_BYTES + BSTAGES * B_BYTES + NBR + 1024 + 512;
+    // + MMA / TMEM warp PW, dY TMA warp PW+1, epilogue warps PW+2 .. PW+5 (TMEM lane quadrants)
+    static constexpr int THREADS = PRODUCERS + 64 + 128;
+    static constexpr int TMEM_COLS = 512 / CPS;  // per CTA (CPS resident CTAs per SM)
+    static constexpr int SMEM = 1024 + STAGES * A_BYTES + BSTAGES * B_BYTES + NBR + XCH + 1024 + 512;
 };
 
 template <int NB, int PW, int CPS, int NT>
@@ -722,28 +729,30 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* bsm = smem + S * Cfg::A_BYTES;
     int* nbr_s = reinterpret_cast<int*>(bsm + BS * Cfg::B_BYTES);
-    int* tab = nbr_s + 2 * NT * BM;  // [m-tile][2 blocks][8 chunks]: ((t - t_lo) << 16 | ci) or -1
+    float* xch = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(nbr_s) + Cfg::NBR);
+    int* tab = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(xch) + Cfg::XCH);  // [m-tile][2 blocks][8 chunks]
     uint64_t* bars = reinterpret_cast<uint64_t*>(tab + 256);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 2 * BS + 3);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 2 * BS + 4);
     int* nbr_cnt = reinterpret_cast<int*>(tmem_slot + 2);
 
     const int tid = threadIdx.x, warp = tid >> 5;
-    int grp = 0;  // this CTA's m-tile group and its voxel split inside the group
+    int grp = 0;  // this CTA's m-tile group, and its run of chunks inside the group
     while (grp + 1 < grp_tab.groups && (int)blockIdx.x >= grp_tab.cta_begin[grp + 1]) ++grp;
-    const int split = (int)blockIdx.x - grp_tab.cta_begin[grp];
     const int m0 = grp_tab.m_begin[grp];
     const int nm = grp_tab.m_begin[grp + 1] - m0;
     const int tps = grp_tab.tps[grp];
-    const int tile0 = split * tps;
-    const int ntl = max(0, min(tps, tiles - tile0));
+    const int chunk0 = ((int)blockIdx.x - grp_tab.cta_begin[grp]) * grp_tab.cpc[grp];
+    const int nch = max(0, min(grp_tab.cpc[grp], grp_tab.nchunk[grp] - chunk0));
+    const int tile0 = chunk0 * tps;
+    const int ntl = max(0, min(nch * tps, tiles - tile0));
     const int pair = grp_tab.pair;
-    const int Co = pair ? C / 2 : C;    // channels of one plane
-    const int RPM = pair ? 64 : 128;    // (t, ci) rows per m-tile
+    const int Co = pair ? C / 2 : C;  // channels of one plane
+    const int RPM = pair ? 64 : 128;  // (t, ci) rows per m-tile
     const int K = taps * Co;
     const uint32_t sbase = smem_u32(smem), bbase = smem_u32(bsm);
     const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S);
     const uint32_t bfull0 = smem_u32(bars + 2 * S), bempty0 = smem_u32(bars + 2 * S + BS);
-    const uint32_t nfull0 = smem_u32(bars + 2 * S + 2 * BS), done = nfull0 + 16;
+    const uint32_t nfull0 = smem_u32(bars + 2 * S + 2 * BS), done = nfull0 + 16, drained = nfull0 + 24;
     // taps [t_lo, t_lo + ntb) cover this CTA's (t, ci) rows; only they are staged
     const int t_lo = (m0 * RPM) / Co;
     const int ntb = min(NT, (min(K, (m0 + nm) * RPM) - 1) / Co - t_lo + 1);
@@ -767,6 +776,7 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
         mbar_init(nfull0 + 8, 1);
         nbr_cnt[0] = nbr_cnt[1] = 0;
         mbar_init(done, 1);
+        mbar_init(drained, 128);
         mbar_init_fence();
     }
     if (warp == PW) tmem_alloc(smem_u32(tmem_slot), Cfg::TMEM_COLS);
@@ -837,81 +847,6 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
                 if (lt + 2 < ntl) request(lt + 2, buf);
             }
         }
-
-        // ---------------- epilogue (warps 0-3 = TMEM lane quadrants): row m, columns co
-        if (warp < 4 && pair) {
-            // lanes 64..127 (lo plane rows) hand their column sums to lanes 0..63 through shared
-            // memory (the A ring is idle once `done` fired); fixed order (hi.hi + hi.lo) + (lo.hi + lo.lo)
-            const int row = warp * 32 + (int)lane_id();
-            const int r = row & 63;
-            const int pc = grp_tab.pcols;  // c_out (a multiple of 16)
-            const int xs = pc + 4;         // padded exchange row (floats)
-            float* xch = reinterpret_cast<float*>(smem);
-            if (ntl > 0) {
-                mbar_wait_sleep(done, 0);
-                tc_fence_after();
-            }
-            for (int mi = 0; mi < nm; ++mi) {
-                float* dst = partial + grp_tab.part_begin[grp] + (((long long)split * nm + mi) * 64 + r) * pc;
-                for (int ph2 = 1; ph2 >= 0; --ph2) {
-                    if ((row >> 6) == ph2) {
-                        for (int c0 = 0; c0 < pc; c0 += 16) {
-                            float f[16];
-                            if (ntl > 0) {
-                                uint32_t a[16], b[16];
-                                const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + mi * NB + c0;
-                                tmem_ld16(ta, a);
-                                tmem_ld16(ta + pc, b);
-                                tmem_ld_wait();
-#pragma unroll
-                                for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(a[e]) + __uint_as_float(b[e]);
-                            } else {
-#pragma unroll
-                                for (int e = 0; e < 16; ++e) f[e] = 0.0f;
-                            }
-                            float* x = xch + r * xs + c0;
-                            if (ph2 == 1) {
-#pragma unroll
-                                for (int e = 0; e < 16; e += 4)
-                                    *reinterpret_cast<float4*>(x + e) = make_float4(f[e], f[e + 1], f[e + 2], f[e + 3]);
-                            } else {
-#pragma unroll
-                                for (int e = 0; e < 16; e += 4) {
-                                    const float4 v = *reinterpret_cast<const float4*>(x + e);
-                                    f[e] += v.x, f[e + 1] += v.y, f[e + 2] += v.z, f[e + 3] += v.w;
-                                }
-                                store_row(dst + c0, f);
-                            }
-                        }
-                    }
-                    named_sync(1, 128);
-                }
-            }
-        } else if (warp < 4) {
-            const int row = warp * 32 + (int)lane_id();
-            if (ntl > 0) {
-                mbar_wait_sleep(done, 0);
-                tc_fence_after();
-            }
-            for (int mi = 0; mi < nm; ++mi) {
-                float* dst = partial + grp_tab.part_begin[grp] + (((long long)split * nm + mi) * BM + row) * NB;
-#pragma unroll
-                for (int c0 = 0; c0 < NB; c0 += 16) {
-                    float f[16];
-                    if (ntl > 0) {
-                        uint32_t v[16];
-                        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + mi * NB + c0, v);
-                        tmem_ld_wait();
-#pragma unroll
-                        for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(v[e]);
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < 16; ++e) f[e] = 0.0f;
-                    }
-                    store_row(dst + c0, f);
-                }
-            }
-        }
     } else if (tid == (PW + 1) * 32) {
         // ---------------- dY loader (own warp: a producer thread blocking on the B ring
         // would stall its A rows and with them every stage)
@@ -932,13 +867,20 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
                 }
             }
     } else if (warp == PW && ntl > 0) {
-        // ---------------- MMA issuer: warp-uniform loop, one elected lane issues
+        // ---------------- MMA issuer: warp-uniform loop, one elected lane issues. Each chunk
+        // starts a fresh accumulation (after the epilogue drained the previous chunk) and
+        // ends with a commit to `done`.
         constexpr uint32_t idesc = idesc_bf16_f32(BM, NB, true, true);
         constexpr uint32_t LBO = Cfg::KB * 128;  // next 64-wide MN block
         const uint64_t a0 = sw128_desc(sbase, LBO, 1024), b0 = sw128_desc(bbase, LBO, 1024);
         int s = 0, bs = 0;
         uint32_t ph = 0, bph = 0;
+        int cl = 0, ci = 0;  // tile index inside the chunk, chunk index
         for (int lt = 0; lt < ntl; ++lt) {
+            if (cl == 0 && ci > 0) {
+                mbar_wait(drained, (uint32_t)((ci - 1) & 1));
+                tc_fence_after();
+            }
             for (int h = 0; h < 2; ++h) {
                 mbar_wait(bfull0 + 8 * bs, bph);
                 const uint64_t bo = (uint64_t)((bs * Cfg::B_BYTES) >> 4);
@@ -951,7 +893,7 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
 #pragma unroll
                         for (int kk = 0; kk < Cfg::KB / 16; ++kk)  // 16 voxels = two 8-row atoms per MMA
                             mma_bf16(tmem + mi * NB, a0 + ao + 128 * kk, b0 + bo + 128 * kk, idesc,
-                                     (lt | h | kk) != 0);
+                                     (cl | h | kk) != 0);
                         mma_commit(empty0 + 8 * s);
                     }
                     __syncwarp();
@@ -967,9 +909,73 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
                     bph ^= 1;
                 }
             }
+            if (++cl == tps || lt == ntl - 1) {
+                if (elect_one()) mma_commit(done);
+                __syncwarp();
+                cl = 0;
+                ++ci;
+            }
         }
-        if (elect_one()) mma_commit(done);
-        __syncwarp();
+    } else if (warp >= PW + 2) {
+        // ---------------- epilogue warps: TMEM lane quadrant q = warp & 3, row = q*32 + lane.
+        const int q = warp & 3;
+        const int row = q * 32 + (int)lane_id();
+        const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
+        for (int c = 0; c < nch; ++c) {
+            mbar_wait_sleep(done, (uint32_t)(c & 1));
+            tc_fence_after();
+            const long long slot = chunk0 + c;
+            if (pair) {
+                // lanes 64..127 (lo plane rows) hand their column sums to lanes 0..63 through a
+                // 64 x 16 shared exchange; fixed order (hi.hi + hi.lo) + (lo.hi + lo.lo)
+                const int r = row & 63;
+                const int pc = grp_tab.pcols;  // c_out (a multiple of 16)
+                float* x = xch + r * 20;
+                for (int mi = 0; mi < nm; ++mi) {
+                    float* dst = partial + grp_tab.part_begin[grp] + ((slot * nm + mi) * 64 + r) * pc;
+                    for (int c0 = 0; c0 < pc; c0 += 16) {
+                        uint32_t a[16], b[16];
+                        tmem_ld16(tq + mi * NB + c0, a);
+                        tmem_ld16(tq + mi * NB + pc + c0, b);
+                        tmem_ld_wait();
+                        float f[16];
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(a[e]) + __uint_as_float(b[e]);
+                        if (row >= 64) {
+#pragma unroll
+                            for (int e = 0; e < 16; e += 4)
+                                *reinterpret_cast<float4*>(x + e) = make_float4(f[e], f[e + 1], f[e + 2], f[e + 3]);
+                        }
+                        named_sync(1, 128);
+                        if (row < 64) {
+#pragma unroll
+                            for (int e = 0; e < 16; e += 4) {
+                                const float4 v = *reinterpret_cast<const float4*>(x + e);
+                                f[e] += v.x, f[e + 1] += v.y, f[e + 2] += v.z, f[e + 3] += v.w;
+                            }
+                            store_row(dst + c0, f);
+                        }
+                        named_sync(1, 128);
+                    }
+                }
+            } else {
+                for (int mi = 0; mi < nm; ++mi) {
+                    float* dst = partial + grp_tab.part_begin[grp] + ((slot * nm + mi) * BM + row) * NB;
+#pragma unroll
+                    for (int c0 = 0; c0 < NB; c0 += 16) {
+                        uint32_t v[16];
+                        tmem_ld16(tq + mi * NB + c0, v);
+                        tmem_ld_wait();
+                        float f[16];
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(v[e]);
+                        store_row(dst + c0, f);
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(drained);
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -988,7 +994,7 @@ __device__ __forceinline__ float split_lane_sum(const float* __restrict__ partia
     int g = 0;
     while (g + 1 < grp_tab.groups && mtile >= grp_tab.m_begin[g + 1]) ++g;
     const int nm = grp_tab.m_begin[g + 1] - grp_tab.m_begin[g];
-    const int splits = grp_tab.cta_begin[g + 1] - grp_tab.cta_begin[g];
+    const int splits = grp_tab.nchunk[g];
     const float* p = partial + grp_tab.part_begin[g] + ((long long)(mtile - grp_tab.m_begin[g]) * rpm + row) * pc + n;
     const long long stride = (long long)nm * rpm * pc;
     float acc = 0.0f;
@@ -1361,12 +1367,13 @@ DwPlan dw_plan(long long rows, int taps, int cin, int cout, int max_tps = 0, boo
             const int end = (int)((long long)slots * g.m_begin[i + 1] / p.mt);
             want = std::max(1, std::min(p.tiles, end - g.cta_begin[i]));
         }
-        g.tps[i] = std::max(1, (p.tiles + want - 1) / want);
-        if (max_tps > 0) g.tps[i] = std::min(g.tps[i], max_tps);
-        const int splits = std::max(1, (p.tiles + g.tps[i] - 1) / g.tps[i]);
-        g.cta_begin[i + 1] = g.cta_begin[i] + splits;
+        g.tps[i] = std::max(1, (p.tiles + want - 1) / want);  // tiles per CTA ...
+        if (max_tps > 0) g.tps[i] = std::min(g.tps[i], max_tps);  // ... cut into chunks of <= max_tps
+        g.nchunk[i] = std::max(1, (p.tiles + g.tps[i] - 1) / g.tps[i]);
+        g.cpc[i] = (g.nchunk[i] + want - 1) / want;
+        g.cta_begin[i + 1] = g.cta_begin[i] + (g.nchunk[i] + g.cpc[i] - 1) / g.cpc[i];
         g.part_begin[i] = part;
-        part += (long long)splits * mg * rpm * g.pcols;
+        part += (long long)g.nchunk[i] * mg * rpm * g.pcols;
     }
     p.ctas = g.cta_begin[G];
     p.partial_floats = part;
