@@ -414,252 +414,6 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, PW, sizeof(OutT)>::THREADS, CP
     }
 }
 
-// ====================================================================== forward, CTA pairs
-// The same gather-GEMM on a cluster of two CTAs on two SMs (cta_group::2): the pair works on
-// two 128-voxel tiles at once as one M = 256 MMA whose B operand (the weight tile) is split
-// across the pair — each CTA's TMA loads and each SM's tensor core reads only BN/2 weight
-// rows — which cuts the shared-memory bytes per MAC by ~1/6 (the forward is shared-memory
-// bandwidth bound). The leader (rank 0) issues the MMAs; rank 1's idle MMA
-// warp relays "my stage is full" to the leader (cp.async completion can only arrive on a
-// CTA-local mbarrier); the MMA commits arrive on both CTAs' barriers (multicast); rank 1's
-// epilogue threads release the shared accumulator buffer on the leader's barrier.
-template <int BN, int PW, typename OutT, int CPS = 2>
-__global__ void __launch_bounds__(FwdCfg<BN, CPS, PW, sizeof(OutT)>::THREADS, CPS)
-    k_conv_fwd_pair(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap ymap,
-                    const int* __restrict__ fmap, int taps, long long rows, const bf16* __restrict__ X, int C,
-                    int nkb, int tiles) {
-    using Cfg = FwdCfg<BN, CPS, PW, sizeof(OutT)>;
-    constexpr int NP = Cfg::PRODUCERS;
-    constexpr int S = Cfg::STAGES;
-    constexpr int RS = NP / 8;
-    constexpr int J = BM / RS;
-    constexpr int BH_BYTES = BN / 2 * 128;  // this CTA's half of the weight tile
-    static_assert(BM % RS == 0 && S >= 2 && BN >= 32, "producer / ring shape");
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    int* nbr_s = reinterpret_cast<int*>(smem + S * Cfg::STAGE_BYTES);
-    uint8_t* epi_s = smem + S * Cfg::STAGE_BYTES + Cfg::NBR;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * Cfg::STAGE_BYTES + Cfg::NBR + Cfg::EPI);
-    // bars: full[S] empty[S] tfull[2] tempty[2] nfull[2] pfull[S] | tmem slot | map counters
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 6);
-    int* nbr_cnt = reinterpret_cast<int*>(tmem_slot + 2);
-
-    const int tid = threadIdx.x, warp = tid >> 5;
-    const uint32_t rank = cluster_ctarank();
-    const int npairs = (int)(gridDim.x >> 1);
-    const int pair0 = (int)(blockIdx.x >> 1);
-    const int tstride = 2 * npairs;  // tiles between this CTA's consecutive tiles
-    const uint32_t sbase = smem_u32(smem);
-    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S);
-    const uint32_t tfull0 = smem_u32(bars + 2 * S), tempty0 = smem_u32(bars + 2 * S + 2);
-    const uint32_t nfull0 = smem_u32(bars + 2 * S + 4), pfull0 = smem_u32(bars + 2 * S + 6);
-    const uint32_t nbr_bytes = (uint32_t)(taps * BM * 4);
-
-    if (tid == 0) {
-        for (int s = 0; s < S; ++s) {
-            mbar_init(full0 + 8 * s, NP + 1);
-            mbar_init(empty0 + 8 * s, 1);
-            mbar_init(pfull0 + 8 * s, 1);
-        }
-        for (int a = 0; a < 2; ++a) {
-            mbar_init(tfull0 + 8 * a, 1);
-            mbar_init(tempty0 + 8 * a, 256);  // leader: both CTAs' epilogue warpgroups
-            mbar_init(nfull0 + 8 * a, 1);
-            nbr_cnt[a] = 0;
-        }
-        mbar_init_fence();
-    }
-    if (warp == PW + 4) tmem_alloc_pair(smem_u32(tmem_slot), tmem_cols(2 * BN));
-    tc_fence_before();
-    __syncthreads();
-    cluster_sync_all();  // both CTAs' barriers exist before any remote arrive
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-
-    if (warp < PW) {
-        // ---------------- producers (as k_conv_fwd; the tile sequence is 2p + rank)
-        const int c = tid & 7;
-        const int r0 = (tid >> 3) * J;
-        static_assert(J % 4 == 0, "map entries are loaded 4 at a time");
-        uint32_t doff[J];
-#pragma unroll
-        for (int j = 0; j < J; ++j) doff[j] = sw128_offset(r0 + j, c);
-        const int t0 = (c * 8) / C, ci0 = c * 8 - t0 * C;
-        const uint32_t row_bytes = (uint32_t)C * 2;
-        auto request = [&](int tile, int buf) {
-            mbar_arrive_expect_tx(nfull0 + 8 * buf, nbr_bytes);
-            bulk_g2s(smem_u32(nbr_s + buf * kMaxTaps * BM), fmap + (long long)tile * taps * BM, nbr_bytes,
-                     nfull0 + 8 * buf);
-        };
-        const int first = 2 * pair0 + (int)rank;
-        if (tid == 0) {
-            if (first < tiles) request(first, 0);
-            if (first + tstride < tiles) request(first + tstride, 1);
-        }
-        int s = 0;
-        uint32_t ph = 0;
-        int i = 0;
-        for (int p = pair0; 2 * p < tiles; p += npairs, ++i) {
-            const int tile = 2 * p + (int)rank;
-            const bool valid = tile < tiles;  // the last pair of an odd tile count has one
-            const int buf = i & 1;
-            if (valid) mbar_wait_sleep(nfull0 + 8 * buf, (uint32_t)((i >> 1) & 1));
-            const uint32_t nb = smem_u32(nbr_s + buf * kMaxTaps * BM + r0);
-            int t = t0, ci = ci0;
-            for (int kb = 0; kb < nkb; ++kb) {
-                int g[J];
-                if (valid && t < taps) {
-#pragma unroll
-                    for (int j = 0; j < J; j += 4) {
-                        const int4 v = ld_shared_v4(nb + (t * BM + j) * 4);
-                        g[j] = v.x, g[j + 1] = v.y, g[j + 2] = v.z, g[j + 3] = v.w;
-                    }
-                } else {
-#pragma unroll
-                    for (int j = 0; j < J; ++j) g[j] = -1;
-                }
-                mbar_wait_sleep(empty0 + 8 * s, ph ^ 1);
-                const uint32_t A = sbase + s * Cfg::STAGE_BYTES;
-                const char* xs = reinterpret_cast<const char*>(X + ci);
-#pragma unroll
-                for (int j = 0; j < J; ++j) cp_async16_row(A + doff[j], xs, g[j], row_bytes);
-                cp_async_arrive_noinc(full0 + 8 * s);
-                ci += BK;
-                while (ci >= C) {
-                    ci -= C;
-                    ++t;
-                }
-                if (++s == S) {
-                    s = 0;
-                    ph ^= 1;
-                }
-            }
-            __syncwarp();
-            if (valid && (tid & 31) == 0 && atomicAdd(&nbr_cnt[buf], 1) == PW - 1) {
-                nbr_cnt[buf] = 0;
-                if (tile + 2 * tstride < tiles) request(tile + 2 * tstride, buf);
-            }
-        }
-    } else if (warp < PW + 4) {
-        // ---------------- epilogue: this CTA's 128 rows of the pair's accumulator
-        const int q = warp & 3;
-        const int lane = (int)lane_id();
-        uint8_t* stage = epi_s + q * (Cfg::EPI_BUFS * Cfg::EPI_BUF);
-        const uint32_t tempty_leader = mapa_shared(tempty0, 0);
-        int nb_issued = 0;
-        int i = 0;
-        for (int p = pair0; 2 * p < tiles; p += npairs, ++i) {
-            const int tile = 2 * p + (int)rank;
-            const int acc = i & 1;
-            mbar_wait_sleep(tfull0 + 8 * acc, (uint32_t)((i >> 1) & 1));
-            tc_fence_after();
-            const int r0 = tile * BM + q * 32;  // rows past `rows` are clipped by the TMA store
-#pragma unroll
-            for (int c0 = 0; c0 < BN; c0 += 16) {
-                uint32_t v[16];
-                tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c0, v);
-                tmem_ld_wait();
-                float f[16];
-#pragma unroll
-                for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(v[e]);
-                uint8_t* buf = stage + (nb_issued % Cfg::EPI_BUFS) * Cfg::EPI_BUF;
-                if (nb_issued >= Cfg::EPI_BUFS) {
-                    if (lane == 0) bulk_wait_read<Cfg::EPI_BUFS - 1>();
-                    __syncwarp();
-                }
-                stage_row16(buf, lane, f, (OutT*)nullptr);
-                fence_proxy_async();
-                __syncwarp();
-                if (lane == 0) {
-                    tma_store2d(&ymap, smem_u32(buf), c0, r0);
-                    bulk_commit();
-                }
-                ++nb_issued;
-            }
-            tc_fence_before();
-            mbar_arrive_cluster(tempty_leader + 8 * acc);  // the leader's barrier counts both halves
-        }
-        if (lane == 0) bulk_wait<0>();
-        __syncwarp();
-    } else if (tid == (PW + 5) * 32) {
-        // ---------------- weight loader: this CTA's BN/2 rows of each stage's weight tile
-        int s = 0;
-        uint32_t ph = 0;
-        for (int p = pair0; 2 * p < tiles; p += npairs) {
-            for (int kb = 0; kb < nkb; ++kb) {
-                mbar_wait_sleep(empty0 + 8 * s, ph ^ 1);
-                mbar_arrive_expect_tx(full0 + 8 * s, BH_BYTES);
-                tma_load2d(sbase + s * Cfg::STAGE_BYTES + Cfg::A_BYTES, &wmap, kb * BK, (int)rank * (BN / 2),
-                           full0 + 8 * s);
-                if (++s == S) {
-                    s = 0;
-                    ph ^= 1;
-                }
-            }
-        }
-    } else if (warp == PW + 4) {
-        if (rank == 0) {
-            // ---------------- leader: MMA issue for the pair
-            constexpr uint32_t idesc = idesc_bf16_f32(2 * BM, BN, false, false);
-            const uint64_t a0 = sw128_desc(sbase, 16, 1024), b0 = sw128_desc(sbase + Cfg::A_BYTES, 16, 1024);
-            int s = 0;
-            uint32_t ph = 0;
-            int i = 0;
-            for (int p = pair0; 2 * p < tiles; p += npairs, ++i) {
-                const int acc = i & 1;
-                mbar_wait(tempty0 + 8 * acc, (uint32_t)(((i >> 1) & 1) ^ 1));
-                tc_fence_after();
-                const uint32_t d = tmem + acc * BN;
-                for (int kb = 0; kb < nkb; ++kb) {
-                    mbar_wait(full0 + 8 * s, ph);   // this CTA's rows and weight half
-                    mbar_wait(pfull0 + 8 * s, ph);  // the peer's (relayed)
-                    fence_proxy_async();
-                    tc_fence_after();
-                    if (elect_one()) {
-                        const uint64_t so = (uint64_t)((s * Cfg::STAGE_BYTES) >> 4);
-#pragma unroll
-                        for (int kk = 0; kk < BK / 16; ++kk)
-                            mma_bf16_pair(d, a0 + so + 2 * kk, b0 + so + 2 * kk, idesc, (kb | kk) != 0);
-                        mma_commit_pair(empty0 + 8 * s, 0x3);
-                    }
-                    __syncwarp();
-                    if (++s == S) {
-                        s = 0;
-                        ph ^= 1;
-                    }
-                }
-                if (elect_one()) mma_commit_pair(tfull0 + 8 * acc, 0x3);
-                __syncwarp();
-            }
-        } else {
-            // ---------------- peer: relay stage completions to the leader
-            const uint32_t pfull_leader = mapa_shared(pfull0, 0);
-            int s = 0;
-            uint32_t ph = 0;
-            for (int p = pair0; 2 * p < tiles; p += npairs) {
-                for (int kb = 0; kb < nkb; ++kb) {
-                    mbar_wait(full0 + 8 * s, ph);
-                    fence_proxy_async();  // this CTA's cp.async rows -> the pair's tensor-core reads
-                    if (lane_id() == 0) mbar_arrive_cluster(pfull_leader + 8 * s);
-                    __syncwarp();
-                    if (++s == S) {
-                        s = 0;
-                        ph ^= 1;
-                    }
-                }
-            }
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    cluster_sync_all();  // the leader's last MMAs read the peer's shared memory / TMEM
-    if (warp == PW + 4) {
-        __syncwarp();
-        tc_fence_after();
-        tmem_dealloc_pair(tmem, tmem_cols(2 * BN));
-    }
-}
-
 // ====================================================================== weight gradient
 // Partial[split][m][co] = sum over this split's voxels n of A[m][n] * B[co][n]
 //   A[m][n] = X[nbr(n, m / C)][m % C]   (m = t*C + ci; MN-major: one 128-byte gathered row
@@ -1220,33 +974,6 @@ void launch_fwd(const int* fmap, int taps, long long rows, const bf16* X, int C,
     launched(SUMH ? "conv gather-GEMM, split precision (tcgen05)" : "conv gather-GEMM (tcgen05)");
 }
 
-// CTA-pair forward (k_conv_fwd_pair): clusters of 2, two CTAs per SM.
-template <int BN, int PW, typename OutT, int CPS = 2>
-void launch_fwd_pair(const int* fmap, int taps, long long rows, const bf16* X, int C, const bf16* Wp, int Kp, OutT* Y,
-                     cudaStream_t s) {
-    using Cfg = FwdCfg<BN, CPS, PW, sizeof(OutT)>;
-    auto kern = k_conv_fwd_pair<BN, PW, OutT, CPS>;
-    smem_optin(kern, Cfg::SMEM);
-    const CUtensorMap wm = map2d(Wp, (uint64_t)Kp, (uint64_t)BN, (uint64_t)Kp * 2, BN / 2);
-    const CUtensorMap ym = map_out(Y, sizeof(OutT) == 4, (uint64_t)BN, (uint64_t)rows, 16, 32);
-    const int tiles = (int)((rows + BM - 1) / BM);
-    const int pairs = std::min((tiles + 1) / 2, num_sms() * CPS / 2);  // CPS CTAs per SM, 2 per cluster
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(2 * pairs));
-    cfg.blockDim = dim3(Cfg::THREADS);
-    cfg.dynamicSmemBytes = Cfg::SMEM;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    cuda_check(cudaLaunchKernelEx(&cfg, kern, wm, ym, fmap, taps, rows, X, C, Kp / BK, tiles), "launch (pair)");
-    launched("conv gather-GEMM (tcgen05 CTA pair)");
-}
-
 template <int BN, typename OutT>
 void launch_fwd_bn(const int* fmap, int taps, long long rows, const bf16* X, int C, const bf16* Wp, int Kp, OutT* Y,
                    cudaStream_t s) {
@@ -1255,11 +982,6 @@ void launch_fwd_bn(const int* fmap, int taps, long long rows, const bf16* X, int
     // CTA with 4 producer warps.
     static const int cps = env_int("HCB_FWD_CPS", 2);
     static const int pw = env_int("HCB_FWD_PW", 4);
-    static const int pair = env_int("HCB_FWD_PAIR", 0);
-    if constexpr (BN == 32 || BN == 64) {
-        if (pair == 1 && cps == 2 && pw == 4) return launch_fwd_pair<BN, 4, OutT, 2>(fmap, taps, rows, X, C, Wp, Kp, Y, s);
-        if (pair == 2 && pw == 4) return launch_fwd_pair<BN, 4, OutT, 1>(fmap, taps, rows, X, C, Wp, Kp, Y, s);
-    }
     if constexpr (BN <= 64) {
         if (cps == 2) {
             if (pw == 2) return launch_fwd<BN, 2, 2>(fmap, taps, rows, X, C, Wp, Kp, Y, s);

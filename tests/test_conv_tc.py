@@ -268,38 +268,3 @@ def test_full_size_native_layer_properties(bench_shell):
     dw = nconv.conv_dw(fm, x, dy)
     dw_form = (dw.double() * w.double()).sum()
     assert abs(float(dw_form - fwd_form)) <= 1e-5 * scale, (float(dw_form), float(fwd_form), scale)
-
-
-def test_cta_pair_forward_variant(cuda):
-    """The experimental cta_group::2 forward (HCB_FWD_PAIR=1, k_conv_fwd_pair: CTA pairs, M = 256,
-    weight tile split across the pair) stays correct; run in a subprocess because the knob is
-    read once per process. Ragged tile counts exercise the pair's dummy second tile."""
-    import os
-    import subprocess
-    import sys
-    code = r"""
-import sys, torch
-sys.path.insert(0, "tests")
-from test_conv_tc import ref_gather_gemm, rel, bf16_round
-from helpers import random_pair
-from paper_1803_11385_b200 import conv as nconv, ops
-from paper_1803_11385_b200.ops import ConvSpec
-from paper_1803_11385_b200.psh import SuperPsh
-for c_out, models in ((64, 3), (32, 5)):
-    f, _ = random_pair(32, models, seed=c_out + models, n_lo=300, n_hi=900)
-    s = SuperPsh.from_levels(f)
-    n, c_in = s.total_columns(), 64
-    fm = ops.field_map(s, s, ConvSpec(3, 1, 0, c_in, c_out))
-    g = torch.Generator(device="cuda").manual_seed(c_out)
-    x = (torch.rand((n, c_in), device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
-    w = bf16_round(torch.rand((c_out, c_in * 27), device="cuda", generator=g) * 2 - 1)
-    y = nconv.gather_gemm(nconv.field_map_native(s, s, ConvSpec(3, 1, 0, c_in, c_out)), x,
-                          nconv.pack_weights(w, c_out, c_in, 27), c_out, torch.float32)
-    err = rel(y, ref_gather_gemm(fm, x, w, c_out))
-    assert err <= 1e-5, (c_out, n, err)
-print("pair ok")
-"""
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=240,
-                         env=dict(os.environ, HCB_FWD_PAIR="1"))
-    assert out.returncode == 0 and "pair ok" in out.stdout, out.stderr[-3000:]
