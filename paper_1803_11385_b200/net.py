@@ -131,7 +131,7 @@ class NativeHashNet:
         self.level_max, self.num_classes, self.input_channels = level_max, num_classes, input_channels
         self.dropout, self.lr, self.momentum, self.wd = dropout, lr, momentum, weight_decay
         self.bn_momentum, self.bn_eps = bn_momentum, bn_eps
-        self.sync_bn, self._ntot = sync_bn, {}
+        self.sync_bn = sync_bn
         g = torch.Generator(device="cuda").manual_seed(seed)
         self.blocks = []
         for lvl in range(level_max, 1, -1):
@@ -180,17 +180,14 @@ class NativeHashNet:
             self._ws["bn"] = t
         return t
 
-    def _n_total(self, i: int, n: int) -> int:
-        """Global row count of block i's batch norm (cached per local size, so CUDA-graph
-        capture after the warm-up steps does not synchronise)."""
-        if self.sync_bn is None:
-            return n
-        key = (i, n)
-        if key not in self._ntot:
-            t = torch.tensor([float(n)], dtype=torch.float64, device="cuda")
-            self.sync_bn(t)
-            self._ntot[key] = int(round(float(t.item())))
-        return self._ntot[key]
+    def _sync_sums(self, buf: torch.Tensor, n: int, c: int) -> torch.Tensor:
+        """All-reduce per-channel double sums buf[0:2c] TOGETHER with this rank's row count
+        (buf[2c] = n), so every step's global count rides in the same collective (ranks whose
+        shard sizes differ from step to step stay in lock step; no host synchronisation, so the
+        step still captures into a CUDA graph). Returns the global count as a device scalar."""
+        buf[2 * c:].fill_(float(n))
+        self.sync_bn(buf)
+        return buf[2 * c:]
 
     def _bn_relu_forward(self, i: int, y: torch.Tensor, xhat: torch.Tensor, r: torch.Tensor) -> None:
         blk = self.blocks[i]
@@ -201,16 +198,19 @@ class NativeHashNet:
                                                 _p(blk["run_var"]), _p(blk["inv_std"]), _p(xhat), _p(r), _p(ws),
                                                 ws.numel(), _s()))
             return
-        nt = self._n_total(i, n)
-        sx = torch.empty((2, c), dtype=torch.float64, device="cuda")
+        # the sums are divided by the global count on the device (the same IEEE double ops
+        # hc_native_bn_finalize applies), then finalised with n_total = 1
+        sxb = torch.empty(2 * c + 1, dtype=torch.float64, device="cuda")
         sq = torch.empty((2, c), dtype=torch.float64, device="cuda")
         mean = torch.empty(c, dtype=torch.float64, device="cuda")
-        check(lib.hc_native_bn_stat(0, _p(y), None, 0, n, c, None, _p(sx), _p(ws), ws.numel(), _s()))
-        self.sync_bn(sx)
-        check(lib.hc_native_bn_finalize(_p(sx), None, nt, c, 0.0, 0.0, None, None, _p(mean), None, _s()))
+        check(lib.hc_native_bn_stat(0, _p(y), None, 0, n, c, None, _p(sxb), _p(ws), ws.numel(), _s()))
+        nt = self._sync_sums(sxb, n, c)
+        sx = (sxb[:c] / nt).contiguous()
+        check(lib.hc_native_bn_finalize(_p(sx), None, 1, c, 0.0, 0.0, None, None, _p(mean), None, _s()))
         check(lib.hc_native_bn_stat(1, _p(y), None, 0, n, c, _p(mean), _p(sq), _p(ws), ws.numel(), _s()))
         self.sync_bn(sq)
-        check(lib.hc_native_bn_finalize(_p(sx), _p(sq), nt, c, self.bn_momentum, self.bn_eps, _p(blk["run_mean"]),
+        sq0 = (sq[0] / nt).contiguous()
+        check(lib.hc_native_bn_finalize(_p(sx), _p(sq0), 1, c, self.bn_momentum, self.bn_eps, _p(blk["run_mean"]),
                                         _p(blk["run_var"]), _p(mean), _p(blk["inv_std"]), _s()))
         check(lib.hc_native_bn_relu_apply(_p(y), n, c, _p(mean), _p(blk["inv_std"]), _p(xhat), _p(r), _s()))
 
@@ -223,11 +223,12 @@ class NativeHashNet:
             check(lib.hc_native_bn_relu_backward(_p(d_relu), d_dtype, _p(xhat), _p(blk["inv_std"]), n, c,
                                                  _p(d_conv), _p(ws), ws.numel(), _s()))
             return
-        st = torch.empty((2, c), dtype=torch.float64, device="cuda")
-        check(lib.hc_native_bn_stat(2, _p(xhat), _p(d_relu), d_dtype, n, c, None, _p(st), _p(ws), ws.numel(), _s()))
-        self.sync_bn(st)
+        stb = torch.empty(2 * c + 1, dtype=torch.float64, device="cuda")
+        check(lib.hc_native_bn_stat(2, _p(xhat), _p(d_relu), d_dtype, n, c, None, _p(stb), _p(ws), ws.numel(), _s()))
+        nt = self._sync_sums(stb, n, c)
+        st = (stb[:2 * c].view(2, c) * (1.0 / nt)).contiguous()  # s * inv_n, as the kernel forms it
         check(lib.hc_native_bn_relu_backward_apply(_p(d_relu), d_dtype, _p(xhat), _p(blk["inv_std"]), n, c,
-                                                   _p(st[0]), _p(st[1]), self._n_total(i, n), _p(d_conv), _s()))
+                                                   _p(st[0]), _p(st[1]), 1, _p(d_conv), _s()))
 
     def input_features(self, ref: torch.Tensor) -> torch.Tensor:
         """Finest-level data (C x N fp32, psh data array) -> padded voxel-major bf16."""
@@ -309,7 +310,10 @@ class NativeHashNet:
         st = scores.t().contiguous().double()
         logp = torch.log_softmax(st, dim=1)
         rows = torch.arange(b, device="cuda")
-        loss = -logp[rows, labels].mean()
+        # the reference's loss is the mean over the whole batch (net.cpp:283): with data
+        # parallelism each rank returns its share, sum / global_batch, so the ranks' losses
+        # add up to the global mean
+        loss = -logp[rows, labels].sum() / (global_batch or b)
         dscores_t = logp.exp()
         dscores_t[rows, labels] -= 1.0
         dscores = (dscores_t.t() / (global_batch or b)).float()
@@ -359,13 +363,13 @@ class NativeHashNet:
         """net.cpp:349-375 train_step: loss + SGD with momentum and weight decay. `allreduce`
         (e.g. dist.allreduce_gradients) sums the gradients over data-parallel ranks first."""
         loss, conv_grads, head_grads = self.loss_and_gradients(nb, x, labels, global_batch)
+        head_grads = [g.contiguous() for g in head_grads]  # the tensors reduced ARE the ones applied
         if allreduce is not None:
-            allreduce(list(conv_grads) + [g.contiguous() for g in head_grads])
+            allreduce(list(conv_grads) + head_grads)
         for blk, g in zip(self.blocks, conv_grads):
             check(lib.hc_native_sgd_update(_p(blk["w"]), _p(blk["v"]), _p(g), g.numel(), self.lr, self.momentum,
                                            self.wd, _s()))
         for w, v, g in zip((self.fc1_w, self.fc1_b, self.fc2_w, self.fc2_b), self.head_v, head_grads):
-            g = g.contiguous()
             check(lib.hc_native_sgd_update(_p(w), _p(v), _p(g), g.numel(), self.lr, self.momentum, self.wd, _s()))
         return loss
 

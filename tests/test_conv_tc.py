@@ -83,8 +83,11 @@ def test_gather_gemm_random_maps(cuda, c_in, c_out, n):
         assert torch.equal(nconv.gather_gemm(fm, x.to(torch.bfloat16), wp, c_out, torch.float32), y), fm.layout
 
 
-@pytest.mark.parametrize("c_in,c_out", [(8, 16), (16, 16), (16, 64), (64, 64), (64, 128), (32, 256), (128, 32)])
+@pytest.mark.parametrize("c_in,c_out", [(8, 16), (16, 16), (16, 64), (64, 64), (64, 128), (32, 256), (128, 32),
+                                        (320, 256)])
 def test_dw_random_maps(cuda, c_in, c_out):
+    """(320, 256): 68 m-tiles at 2 per CTA's TMEM -> 34 groups (a plan clamped to 32 groups would
+    give groups 3 m-tiles and overrun the 512-column allocation)."""
     g = torch.Generator(device="cuda").manual_seed(7 * c_in + c_out)
     n, n_in = 20011, 19000
     x = bf16_round(torch.rand((n_in, c_in), device="cuda", generator=g) * 2 - 1)
@@ -268,3 +271,16 @@ def test_full_size_native_layer_properties(bench_shell):
     dw = nconv.conv_dw(fm, x, dy)
     dw_form = (dw.double() * w.double()).sum()
     assert abs(float(dw_form - fwd_form)) <= 1e-5 * scale, (float(dw_form), float(fwd_form), scale)
+
+
+def test_dw_plan_rejects_shapes_beyond_tmem(cuda):
+    """A (taps x C_in) extent whose m-tile groups cannot keep their accumulators in TMEM is an
+    invalid argument (the workspace query returns 0), never a silent TMEM overrun."""
+    from paper_1803_11385_b200._lib import lib
+    assert lib.hc_native_dw_workspace(1000, 27, 2048, 256) == 0
+    assert lib.hc_native_dw_workspace(1000, 27, 320, 256) > 0
+    x = torch.zeros((64, 2048), dtype=torch.bfloat16, device="cuda")
+    dy = torch.zeros((64, 256), dtype=torch.bfloat16, device="cuda")
+    fmap = torch.zeros((64, 27), dtype=torch.int32, device="cuda")
+    with pytest.raises(ValueError, match="dW supports at most"):
+        nconv.conv_dw(fmap, x, dy)

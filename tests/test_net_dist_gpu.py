@@ -65,31 +65,37 @@ def test_phased_bn_equals_fused_bn_single_rank(cuda):
         assert torch.equal(ba["run_mean"], bb["run_mean"]) and torch.equal(ba["run_var"], bb["run_var"])
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, shardings):
+    """shardings: per step, each rank's list of shape indices of a b_total batch (ranks may own
+    different numbers of shapes, and the split may change from step to step)."""
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import sys
         sys.path.insert(0, ROOT)
-        from paper_1803_11385_b200.dist import allreduce_gradients, shard_range, sum_over_ranks
-        b_total = 4
-        mine = list(shard_range(b_total, world, rank))
-        nnet, levels, cols, labels = _setup(b_total, mine)
-        net, loss, conv_g, head_g = _run(nnet, levels, cols, labels, b_total, sum_over_ranks)
-        allreduce_gradients(conv_g + head_g)
-        lt = torch.tensor([loss * len(mine) / b_total], dtype=torch.float64)
-        dist.all_reduce(lt)
+        from paper_1803_11385_b200.dist import allreduce_gradients, sum_over_ranks
+        all_errs = []
+        for step in shardings:
+            b_total = sum(len(m) for m in step)
+            mine = step[rank]
+            nnet, levels, cols, labels = _setup(b_total, mine)
+            net, loss, conv_g, head_g = _run(nnet, levels, cols, labels, b_total, sum_over_ranks)
+            allreduce_gradients(conv_g + head_g)
+            lt = torch.tensor([loss], dtype=torch.float64)  # each rank's share of the global mean
+            dist.all_reduce(lt)
+            if rank == 0:
+                nnet1, levels1, cols1, labels1 = _setup(b_total, list(range(b_total)))
+                net1, loss1, conv1, head1 = _run(nnet1, levels1, cols1, labels1, b_total, None)
+                errs = {"loss": abs(float(lt) - loss1) / abs(loss1)}
+                for i, (a, b) in enumerate(zip(conv_g + head_g, conv1 + head1)):
+                    errs[f"grad{i}"] = _rel(a.cpu().numpy(), b.cpu().numpy())
+                for i, (ba, bb) in enumerate(zip(net.blocks, net1.blocks)):
+                    errs[f"run_mean{i}"] = _rel(ba["run_mean"].cpu().numpy(), bb["run_mean"].cpu().numpy())
+                    errs[f"run_var{i}"] = _rel(ba["run_var"].cpu().numpy(), bb["run_var"].cpu().numpy())
+                all_errs.append(errs)
         if rank == 0:
-            nnet1, levels1, cols1, labels1 = _setup(b_total, list(range(b_total)))
-            net1, loss1, conv1, head1 = _run(nnet1, levels1, cols1, labels1, b_total, None)
-            errs = {"loss": abs(float(lt) - loss1) / abs(loss1)}
-            for i, (a, b) in enumerate(zip(conv_g + head_g, conv1 + head1)):
-                errs[f"grad{i}"] = _rel(a.cpu().numpy(), b.cpu().numpy())
-            for i, (ba, bb) in enumerate(zip(net.blocks, net1.blocks)):
-                errs[f"run_mean{i}"] = _rel(ba["run_mean"].cpu().numpy(), bb["run_mean"].cpu().numpy())
-                errs[f"run_var{i}"] = _rel(ba["run_var"].cpu().numpy(), bb["run_var"].cpu().numpy())
-            q.put(errs)
+            q.put(all_errs)
         dist.barrier()
     except Exception as e:  # surface the failure instead of hanging the parent
         q.put({"error": repr(e)})
@@ -98,21 +104,38 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_two_rank_sync_bn_equals_whole_batch(cuda):
+def _spawn(shardings):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, shardings)) for r in range(2)]
     for p in procs:
         p.start()
-    errs = q.get(timeout=240)
+    res = q.get(timeout=300)
     for p in procs:
         p.join(timeout=60)
-    assert "error" not in errs, errs
+    assert not isinstance(res, dict), res  # {"error": ...}
+    return res
+
+
+def _check(errs):
     # BN statistics: double sums, order-only differences; gradients: bf16 conv operands with
     # identical values, fp32 split-K dW partials summed in a different grouping
     assert errs["loss"] < 1e-5, errs
     for k, v in errs.items():
         bar = 1e-6 if k.startswith("run_") else 1e-3
         assert v < bar, (k, v, errs)
+
+
+def test_two_rank_sync_bn_equals_whole_batch(cuda):
+    for errs in _spawn([[[0, 1], [2, 3]]]):
+        _check(errs)
+
+
+def test_two_rank_sync_bn_uneven_changing_shards(cuda):
+    """Shard sizes differ between the ranks AND change from step to step (2+1 shapes, then
+    1+2, then 1+3): the global row count rides in the statistics' all-reduce every step, so
+    the collectives stay matched and the statistics use that step's global batch."""
+    for errs in _spawn([[[0, 1], [2]], [[0], [1, 2]], [[0], [1, 2, 3]]]):
+        _check(errs)
