@@ -257,6 +257,8 @@ class NativeHashNet:
                 check(lib.hc_native_bn_relu_inference(_p(y), n, blk["cout_p"], _p(blk["run_mean"]), _p(blk["run_var"]),
                                                       self.bn_eps, _p(r), _s()))
             acts.append(dict(x=x, xhat=xhat))
+            if cache is not None and cache.get("trace") is not None:
+                cache["trace"].setdefault("blocks", []).append(dict(x=x, y=y.clone(), r=r))
             if i + 1 < len(self.blocks):
                 pm = nb.pool_maps[i]
                 nc = pm.shape[0]
@@ -265,6 +267,8 @@ class NativeHashNet:
                 check(lib.hc_native_max_pool(_p(pm), nc, 8, _p(r), _lib.HC_DTYPE_BF16, blk["cout_p"], _p(pooled),
                                              _p(sw), _s()))
                 acts[-1]["sw"] = sw
+                if cache is not None and cache.get("trace") is not None:
+                    cache["trace"]["blocks"][-1].update(pooled=pooled, sw=sw)
                 x = pooled
             else:
                 b = nb.batch
@@ -297,12 +301,12 @@ class NativeHashNet:
         return self.forward(nb, x, training=False).argmax(0)
 
     def loss_and_gradients(self, nb: NetBatch, x: torch.Tensor, labels: torch.Tensor,
-                           global_batch: Optional[int] = None):
+                           global_batch: Optional[int] = None, trace: Optional[dict] = None):
         """net.cpp:260-323: softmax cross-entropy (mean over the batch), gradients of every
         conv and FC weight; returns (loss tensor, conv weight gradients (padded ref layout),
         FC gradients). With data parallelism the scores' gradient is divided by the GLOBAL
         batch (net.cpp:281 divides by b; shards must not divide by their local b)."""
-        cache = {}
+        cache = {"trace": trace}
         scores = self.forward(nb, x, True, cache)
         b = scores.shape[1]
         # softmax over classes, computed on the contiguous [b][classes] transpose (torch's
@@ -337,6 +341,8 @@ class NativeHashNet:
             d_conv = torch.empty((n, c), dtype=BF16, device="cuda")
             self._bn_relu_backward(i, d_relu, d_dtype, a["xhat"], d_conv)
             conv_grads[i] = nconv.conv_dw(nb.conv_maps[i], a["x"], d_conv, self._dw_ws)
+            if trace is not None:
+                trace["blocks"][i].update(d_relu=d_relu, d_conv=d_conv, dw=conv_grads[i].clone())
             # input gradient (net.cpp:316-317; the finest one is the net's input gradient, g.input).
             # The tensor-core tile set starts at 16 output channels: an 8-channel input level
             # takes its gradient through a zero-padded 16-channel kernel.
@@ -347,6 +353,8 @@ class NativeHashNet:
                 w.view(blk["cout_p"], cin_g, 27)[:, :blk["cin_p"]] = blk["w"].view(blk["cout_p"], blk["cin_p"], 27)
             wb = nconv.pack_weights(w, blk["cout_p"], cin_g, 27, True)
             dx = nconv.gather_gemm(nb.conv_maps[i], d_conv, wb, cin_g, BF16)[:, :blk["cin_p"]]
+            if trace is not None:
+                trace["blocks"][i]["dx"] = dx
             if i > 0:  # net.cpp:296-300: unpool through the finer level's switches
                 prev = self.blocks[i - 1]
                 par, prow = nb.parents[i - 1]

@@ -102,26 +102,38 @@ class NativeSegNet:
         return out
 
     # ------------------------------------------------------------------ step
-    def step(self, x: torch.Tensor, labels: torch.Tensor, allreduce=None, world: int = 1):
+    def step(self, x: torch.Tensor, labels: torch.Tensor, allreduce=None, world: int = 1, trace: dict = None):
         """One training step; x [N_fine][c_in] bf16, labels [N_fine] int64. Returns the loss.
         Data parallel: `allreduce` sums the weight gradients over `world` equal shards, which
-        are then averaged (the loss is the mean over all voxels of the global batch)."""
+        are then averaged (the loss is the mean over all voxels of the global batch).
+        `trace` (a dict) receives every layer's inputs and outputs and the weight gradients
+        (before the update) for the layer-by-layer oracle comparison (tests/test_seg_parity.py)."""
         c, nc, nf = self.c, self.nc, self.nf
+        rec = trace.__setitem__ if trace is not None else (lambda k, v: None)
+        if trace is not None:
+            trace["w"] = {k: v.clone() for k, v in self.w.items()}
         # ---- encoder
-        r1, h1 = self._bn_relu(self._conv(self.fmap_f, x, "conv1", c), "bn1")
+        y1 = self._conv(self.fmap_f, x, "conv1", c)
+        r1, h1 = self._bn_relu(y1, "bn1")
         p1 = torch.empty((nc, c), dtype=BF16, device="cuda")
         sw = torch.empty((nc, c), dtype=torch.int8, device="cuda")
         check(lib.hc_native_max_pool(_p(self.pmap), nc, 8, _p(r1), _lib.HC_DTYPE_BF16, c, _p(p1), _p(sw), _s()))
-        e2, h2 = self._bn_relu(self._conv(self.fmap_c, p1, "conv2", 2 * c), "bn2")
+        y2 = self._conv(self.fmap_c, p1, "conv2", 2 * c)
+        e2, h2 = self._bn_relu(y2, "bn2")
         # ---- decoder: unpool(conv3(e2)) + deconv(e2)
         d3 = self._conv(self.fmap_c, e2, "conv3", c, BF16)
         up = torch.empty((nf, c), dtype=BF16, device="cuda")
         check(lib.hc_native_max_unpool(_p(self.parent), _p(self.prow), nf, _p(d3), _lib.HC_DTYPE_BF16, c, _p(sw),
                                        _p(up), _s()))
         s3 = self.deconv.forward(e2)  # fp32 (the deconvolution's output dtype)
+        if trace is not None:
+            for k, v in dict(x=x, y1=y1, r1=r1, p1=p1, sw=sw, y2=y2, e2=e2, d3=d3, up=up, dc=s3.clone()).items():
+                rec(k, v)
         s3.add_(up)                   # + unpooled branch, one mixed-precision add
         r3, h3 = self._bn_relu(s3, "bn3")
         scores = self._conv(self.fmap_f, r3, "conv4", self.k)  # [N_fine][K] fp32
+        rec("r3", r3)
+        rec("scores", scores)
         # ---- per-voxel softmax cross-entropy (mean over voxels)
         logp = torch.log_softmax(scores, dim=1)
         loss = -logp.gather(1, labels[:, None]).mean()
@@ -139,6 +151,10 @@ class NativeSegNet:
         check(lib.hc_native_switch_gather(_p(self.pmap), nc, 8, _p(d_s3), _lib.HC_DTYPE_BF16, c, _p(sw), _p(d_d3),
                                           _s()))
         g["conv3"], d_e2b = self._conv_bwd(self.fmap_c, e2, d_d3, "conv3")
+        if trace is not None:
+            for k, v in dict(dscores=dscores, d_r3=d_r3, d_s3=d_s3, d_e2a=d_e2a.clone(), d_d3=d_d3,
+                             d_e2b=d_e2b).items():
+                rec(k, v)
         d_e2 = d_e2a.float()  # fp32 already (no copy)
         d_e2.add_(d_e2b)
         d_y2 = self._bn_relu_bwd(d_e2, _lib.HC_DTYPE_F32, h2, "bn2")
@@ -148,6 +164,10 @@ class NativeSegNet:
                                        _p(d_r1), _s()))
         d_y1 = self._bn_relu_bwd(d_r1, _lib.HC_DTYPE_BF16, h1, "bn1")
         g["conv1"], _ = self._conv_bwd(self.fmap_f, x, d_y1, "conv1", need_dx=False)
+        if trace is not None:
+            for k, v in dict(d_y2=d_y2, d_p1=d_p1, d_r1=d_r1, d_y1=d_y1).items():
+                rec(k, v)
+            trace["grads"] = {k: v.clone() for k, v in g.items()}
         if allreduce is not None:
             allreduce(list(g.values()))
         for k, gr in g.items():  # plain SGD
