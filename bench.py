@@ -54,6 +54,8 @@ def parse():
                         "within 1e-5, the headline); bf16 = bf16 operands (faster, bf16 tolerance)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-ref-kernels", action="store_true",
+                   help="skip the reference-layout operator timings (hash2col/col2hash/pool/unpool vs HBM)")
     p.add_argument("--workload", default="conv", choices=["conv", "net", "seg"],
                    help="conv: one hash-conv layer fwd+bwd (the BASELINE metric); net: a full H-CNN "
                         "classification train step (BASELINE configs 2/3)")
@@ -97,9 +99,15 @@ def _init_dist(dev):
     import torch.distributed as dist
     backend = os.environ.get("HCB_TEST_DIST_BACKEND", "nccl")
     if backend == "nccl":
+        # NCCL's init lines (communicator size, NVLS / NVLink transport) land on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
     else:
         dist.init_process_group(backend)
+    if dist.get_rank() == 0:
+        print(f"[bench] process group: backend={dist.get_backend()} world_size={dist.get_world_size()}",
+              file=sys.stderr)
 
 
 def peaks():
@@ -286,11 +294,11 @@ class MaterializedStep:
         self.x_ref, self.dy_ref = self.x, self.dy
         self.op_names = ["hash2col", "fwd_gemm", "dW_gemm", "dcols_gemm", "col2hash"]
 
-    def run_ref(self, x, w, dy):
+    def run_ref(self, x, w, dy, on_dw=None):
         """Reference-layout device inputs -> reference-layout outputs (y, dw, dx)."""
-        return self.run(x, w, dy)
+        return self.run(x, w, dy, None, on_dw)
 
-    def run(self, x, w, dy, marks=None):
+    def run(self, x, w, dy, marks=None, on_dw=None):
         ops, f, sp = self.ops, self.fine, self.spec
         mark = (lambda i: marks[i].record()) if marks else (lambda i: None)
         with ops.math_mode("fast"):
@@ -300,6 +308,8 @@ class MaterializedStep:
             y = ops.matmul(w, cols)
             mark(2)
             dw = ops.matmul_trans_b(dy, cols)
+            if on_dw:
+                on_dw(dw)
             mark(3)
             dcols = ops.matmul_trans_a(w, dy)
             mark(4)
@@ -352,7 +362,7 @@ class FusedStepF32:
         self.N, self.cin, self.cout = N, cin, cout
         self.op_names = ["field_map", "split_pack", "fwd_conv", "dW_conv", "dX_conv"]
 
-    def _layer(self, fmap, xs, dys, w, marks):
+    def _layer(self, fmap, xs, dys, w, marks, on_dw=None):
         conv, sp = self.conv, self.spec
         mark = (lambda i: marks[i].record()) if marks else (lambda i: None)
         wf = conv.pack_weights_x2(w, sp.out_channels, sp.in_channels, 27, conv.PACK_FORWARD)
@@ -361,25 +371,28 @@ class FusedStepF32:
         y = conv.gather_gemm_x2(fmap, xs, wf, sp.out_channels)
         mark(3)
         dw = conv.conv_dw_x2(fmap, xs, dys, self.ws)
+        if on_dw:
+            on_dw(dw)  # the dW all-reduce overlaps the input gradient below
         mark(4)
         dx = conv.gather_gemm_x2(fmap, dys, wb, sp.in_channels)
         mark(5)
         return y, dw, dx
 
-    def run(self, x, w, dy, marks=None):
+    def run(self, x, w, dy, marks=None, on_dw=None):
         conv, f, sp = self.conv, self.fine, self.spec
         mark = (lambda i: marks[i].record()) if marks else (lambda i: None)
         mark(0)
         fmap = conv.field_map_native(f, f, sp, conv.TILED)
         mark(1)
-        return self._layer(fmap, conv.split(x), conv.split(dy), w, marks)
+        return self._layer(fmap, conv.split(x), conv.split(dy), w, marks, on_dw)
 
-    def run_ref(self, x, w, dy):
+    def run_ref(self, x, w, dy, on_dw=None):
         """The drop-in contract: reference-layout (C x N fp32) device inputs; the boundary
         transpose is fused into the hi/lo split; outputs back in the reference layout."""
         conv, f, sp = self.conv, self.fine, self.spec
         fmap = conv.field_map_native(f, f, sp, conv.TILED)
-        y, dw, dx = self._layer(fmap, conv.split(x, channel_major=True), conv.split(dy, channel_major=True), w, None)
+        y, dw, dx = self._layer(fmap, conv.split(x, channel_major=True), conv.split(dy, channel_major=True), w, None,
+                                on_dw)
         return conv.to_channel_major(y), dw, conv.to_channel_major(dx)
 
     def op_model(self, M, R):
@@ -422,7 +435,7 @@ class FusedStep:
         self.N, self.cin, self.cout = N, cin, cout
         self.op_names = ["field_map", "pack_w", "fwd_conv", "dW_conv", "dX_conv"]
 
-    def run(self, x, w, dy, marks=None):
+    def run(self, x, w, dy, marks=None, on_dw=None):
         ops, conv, f, sp = self.ops, self.conv, self.fine, self.spec
         mark = (lambda i: marks[i].record()) if marks else (lambda i: None)
         bf = self.torch.bfloat16
@@ -435,16 +448,18 @@ class FusedStep:
         y = conv.gather_gemm(fmap, x, wf, sp.out_channels, bf)
         mark(3)
         dw = conv.conv_dw(fmap, x, dy, self.ws)
+        if on_dw:
+            on_dw(dw)
         mark(4)
         dx = conv.gather_gemm(fmap, dy, wb, sp.in_channels, bf)
         mark(5)
         return y, dw, dx
 
-    def run_ref(self, x, w, dy):
+    def run_ref(self, x, w, dy, on_dw=None):
         """The drop-in contract: reference-layout (C x N fp32) device inputs, layout change
         at the boundary, the fused layer, results back in the reference layout."""
         conv = self.conv
-        y, dw, dx = self.run(conv.to_voxel_major(x), w, conv.to_voxel_major(dy))
+        y, dw, dx = self.run(conv.to_voxel_major(x), w, conv.to_voxel_major(dy), None, on_dw)
         return conv.to_channel_major(y), dw, conv.to_channel_major(dx)
 
     def op_model(self, M, R):
@@ -493,7 +508,7 @@ def main():
     from paper_1803_11385_b200 import _lib
     from paper_1803_11385_b200.psh import SuperPsh
 
-    from paper_1803_11385_b200.dist import allreduce_gradients, local_levels
+    from paper_1803_11385_b200.dist import local_levels
     lv = shell_levels(args.res)
     # global batch of shapes_per_gpu * world shells; this rank owns a contiguous block
     fine = SuperPsh.from_levels(local_levels([lv[0]] * (args.shapes_per_gpu * world), world, rank))
@@ -508,9 +523,25 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    # The one data-path exchange: dW summed over ranks. It is launched on a side
+    # stream as soon as the dW kernel is enqueued, so the collective overlaps the input gradient;
+    # the step ends when both are done.
+    side = torch.cuda.Stream() if world > 1 else None
+    pending = []
+
+    def on_dw(dw):
+        if world > 1:
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                pending.append(dist.all_reduce(dw, op=dist.ReduceOp.SUM, async_op=True))
+
+    def finish():
+        while pending:
+            pending.pop().wait()  # the current stream waits for the collective
+
     def one(marks=None):
-        y, dw, dx = step.run(step.x, step.w, step.dy, marks)
-        allreduce_gradients([dw])
+        y, dw, dx = step.run(step.x, step.w, step.dy, marks, on_dw)
+        finish()
         return dx
 
     args.warmup = max(args.warmup, 3)
@@ -573,9 +604,9 @@ def main():
                 sl["dy"].copy_(hdy, non_blocking=True)
                 sl["ready"].record(h2d_s)
             comp.wait_event(sl["ready"])
-            y, dw, dx = step.run_ref(sl["x"], sl["w"], sl["dy"])
+            y, dw, dx = step.run_ref(sl["x"], sl["w"], sl["dy"], on_dw)
             sl["free"].record(comp)
-            allreduce_gradients([dw])
+            finish()
             sl["done"].record(comp)
             d2h_s.wait_event(sl["done"])
             with torch.cuda.stream(d2h_s):
@@ -666,6 +697,13 @@ def main():
                 "peak_basis": tc_basis + (f" / {dk['bf16_products']} bf16 products per fp32 MAC"
                                           if dk["bf16_products"] > 1 else "")}
 
+    ref_layout = None
+    if not args.no_ref_kernels and args.path == "fused":
+        try:
+            ref_layout = ref_layout_kernels(args.res, args.shapes_per_gpu, args.cin, pk["hbm_gbs"])
+        except Exception as e:  # noqa: BLE001 — reported, never fatal for the headline
+            ref_layout = {"error": repr(e)}
+
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         secs, n1, kind, cores, sample = cpu_conv_sample(args.res, args.cin, args.cout)
@@ -679,12 +717,59 @@ def main():
         "config": dict(conv_config(args, world), voxels_per_gpu=N, path=step.name,
                        l2="working set >> L2 (no flush needed)"),
         "shapes_per_s": args.shapes_per_gpu * world / (ms_step / 1e3),
-        "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+        "roofline": roof, "kernels": kernels, "ref_layout_kernels": ref_layout, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": int(launches), "clocks": cs,
+        "comm": {"backend": dist.get_backend() if world > 1 else None, "world_size": world,
+                 "collective": "one all_reduce(sum) of dW per step on a side stream, overlapping dX"
+                 if world > 1 else None},
     }
     print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def ref_layout_kernels(res, shapes, C, hbm_gbs, reps=5):
+    """The reference-layout operators (include/hashconv_b200.h: hash2col, col2hash, max_pool,
+    max_unpool, the K0 field map) at the bench workload, fp32 C x N operands, vs the HBM
+    roofline. Algorithmic bytes per SURVEY.md §8d: hash2col / col2hash (27+1)*C*N*4 + 10*M +
+    3*R + 16*N; max_pool C*Nf*4 + C*Nc*8; max_unpool C*Nc*8 + C*Nf*4; field map 27*N*4 + 10*M +
+    3*R + 16*N. CUDA events around `reps` back-to-back calls (operands >> L2)."""
+    import torch
+    from paper_1803_11385_b200 import ops
+    from paper_1803_11385_b200.psh import SuperPsh
+    lv = shell_levels(res)
+    fine, coarse = SuperPsh.from_levels([lv[0]] * shapes), SuperPsh.from_levels([lv[1]] * shapes)
+    N, Nc, M, R = fine.total_columns(), coarse.total_columns(), fine.M, fine.R
+    sp, pool = ops.ConvSpec(3, 1, 0, C, C), ops.ConvSpec(2, 2, 0, C, C)
+    g = torch.Generator(device="cuda").manual_seed(9)
+    x = torch.rand((C, N), device="cuda", generator=g) * 2 - 1
+    cols = ops.hash2col(fine, x, fine, sp)
+    mp = ops.max_pool(fine, x, coarse, pool)
+    gather = 28 * C * N * 4 + 10 * M + 3 * R + 16 * N
+    rows = [("field_map", lambda: ops.field_map(fine, fine, sp), 27 * N * 4 + 10 * M + 3 * R + 16 * N),
+            ("hash2col", lambda: ops.hash2col(fine, x, fine, sp), gather),
+            ("col2hash", lambda: ops.col2hash(cols, fine, fine, sp), gather),
+            ("max_pool", lambda: ops.max_pool(fine, x, coarse, pool), C * N * 4 + C * Nc * 8),
+            ("max_unpool", lambda: ops.max_unpool(mp.output, mp.switches, fine, coarse, pool, check_now=False),
+             C * Nc * 8 + C * N * 4)]
+    out = {}
+    for name, fn, nbytes in rows:
+        fn()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / reps
+        gbs = nbytes / (ms / 1e3) / 1e9
+        out[name] = {"ms": ms, "algorithmic_bytes": nbytes, "achieved_GBps": gbs, "frac": gbs / hbm_gbs}
+    ops.check_deferred()
+    del cols
+    torch.cuda.empty_cache()
+    return {"workload": f"{res}^3 shell x {shapes}, C={C} fp32 (reference layout C x N)", "N_fine": N,
+            "N_coarse": Nc, "peak_GBps": hbm_gbs, "kernels": out}
 
 
 def conv_config(args, world):
@@ -721,6 +806,8 @@ def reference_arm(args, rank, world):
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (sphere shells, bench.cpp:33-77; uniform[-1,1] features/weights)",
         "config": dict(conv_config(args, world), sample_voxels_per_step=n1,
+                       sample_note=f"each step times 1 of the workload's {args.shapes_per_gpu} identical shapes "
+                               "(the reference's cost is linear in voxels, so voxels/s is the workload's rate)",
                        path="reference CPU (oracle/_ref: the unmodified reference library)"),
         "cpu_baseline": {"value": value, "unit": "voxels/s", "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "voxels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))

@@ -60,6 +60,10 @@ int64_t hc_launch_count(void);
  * fused split-precision tensor-core conv instead of hash2col + GEMMs (stride-1 layer over one
  * structure handle, <= 128 channels; HCB_FAST_FUSED=0 disables the route). */
 int64_t hc_fused_route_count(void);
+/* Deferred argument checks (max_unpool's switch range): HC_ERR_INVALID_ARGUMENT with the
+ * reference's message if a check run since the last call failed, else HC_OK; clears the flag.
+ * Call after synchronising the stream(s) that ran the checked operators. */
+hc_status hc_deferred_status(void);
 /* Math mode for the reference-layout contraction (thread-local; default EXACT). */
 hc_status hc_set_math(hc_math mode);
 hc_math hc_get_math(void);
@@ -204,7 +208,10 @@ hc_status hc_max_pool_f32(const hc_psh* in, const float* data, int64_t data_rows
 hc_status hc_avg_pool_f32(const hc_psh* in, const float* data, int64_t data_rows,
                           int64_t data_cols, const hc_psh* out, hc_conv_spec spec, float* result,
                           hc_stream stream);
-/* cnn_ops.cpp:336-372 max_unpool (switches validated as cnn_ops.cpp:326-332; syncs) */
+/* cnn_ops.cpp:336-372 max_unpool. The switch range check (cnn_ops.cpp:326-332) is stream-ordered
+ * and never synchronises: an out-of-range switch is reported by hc_deferred_status() after the
+ * caller synchronises the stream (the C++ shim and ops.py do, so they throw the reference's
+ * std::invalid_argument / ValueError at the call as the reference does). */
 hc_status hc_max_unpool_f32(const float* coarse_data, int64_t c_rows, int64_t c_cols,
                             const int32_t* switches, int64_t s_rows, int64_t s_cols,
                             const hc_psh* fine, const hc_psh* coarse, hc_conv_spec spec,

@@ -339,7 +339,9 @@ Mat max_unpool(const Mat& coarse_data, const Switches& switches, const Super& fi
     detail::check(detail::abi<T>::max_unpool(d.template as<T>(), coarse_data.rows, coarse_data.cols,
                                     s.template as<std::int32_t>(), switches.rows, switches.cols, f.get(), c.get(), sp,
                                     r.as<T>(), nullptr));
-    return detail::download<Mat>(r, sp.in_channels, f.columns());
+    Mat out = detail::download<Mat>(r, sp.in_channels, f.columns());  // synchronises
+    detail::check(hc_deferred_status());  // an out-of-range switch throws invalid_argument here
+    return out;
 }
 
 // cnn_ops.cpp:374-406

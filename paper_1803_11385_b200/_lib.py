@@ -163,6 +163,7 @@ lib.hc_native_dw_workspace_x2.restype = C.c_size_t
 lib.hc_native_dw_workspace_x2.argtypes = [_I64, _I32, _I32, _I32]
 lib.hc_launch_count.restype = C.c_int64
 lib.hc_fused_route_count.restype = C.c_int64
+lib.hc_deferred_status.restype = C.c_int
 for _name, _args in _SIGS.items():
     fn = getattr(lib, _name)
     fn.argtypes = _args

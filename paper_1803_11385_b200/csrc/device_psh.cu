@@ -63,6 +63,25 @@ long long fused_route_count(long long add) {
     return n.fetch_add(add, std::memory_order_relaxed) + add;
 }
 
+// One sticky status word in mapped pinned host memory (kernels write it through the device
+// alias; the host reads it after a synchronisation): deferred argument checks.
+static volatile int* g_deferred = nullptr;
+static int* g_deferred_dev = nullptr;
+static std::mutex g_deferred_mu;
+int* deferred_flag_device() {
+    std::lock_guard<std::mutex> lock(g_deferred_mu);
+    if (!g_deferred) {
+        void* h = nullptr;
+        cuda_check(cudaHostAlloc(&h, sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable), "cudaHostAlloc");
+        *static_cast<volatile int*>(h) = 0;
+        void* d = nullptr;
+        cuda_check(cudaHostGetDevicePointer(&d, h, 0), "cudaHostGetDevicePointer");
+        g_deferred = static_cast<volatile int*>(h);
+        g_deferred_dev = static_cast<int*>(d);
+    }
+    return g_deferred_dev;
+}
+
 bool smem_optin_needed(const void* kern, int dev) {
     static std::mutex mu;
     static std::set<std::pair<const void*, int>> done;
@@ -249,6 +268,15 @@ const char* hc_last_error(void) { return g_last_error.c_str(); }
 const char* hc_version(void) { return "hashconv_b200 0.1 (sm_100a)"; }
 int64_t hc_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 int64_t hc_fused_route_count(void) { return hcb::fused_route_count(0); }
+
+hc_status hc_deferred_status(void) {
+    if (g_deferred && *g_deferred) {
+        *g_deferred = 0;
+        set_last_error("unpool: switch index out of range");  // cnn_ops.cpp:331
+        return HC_ERR_INVALID_ARGUMENT;
+    }
+    return HC_OK;
+}
 
 hc_status hc_malloc(void** ptr, size_t bytes) {
     return guard([&] { *ptr = dev_alloc(bytes); });

@@ -66,6 +66,7 @@ struct Scratch {
 // (conv_tc.cu): eligible for a stride-1 field over one structure with <= 128 channels.
 bool fused_x2_eligible(const hc_psh* in, const hc_psh* out, hc_conv_spec sp, int taps);
 long long fused_route_count(long long add);  // hc_fused_route_count
+int* deferred_flag_device();                  // hc_deferred_status's word (device alias)
 void fused_conv_forward_f32(const hc_psh* in, const float* data, const float* w, hc_conv_spec sp, int taps,
                             long long N, float* result, cudaStream_t s);
 void fused_conv_backward_f32(const float* dy, const float* w, const float* cols, const hc_psh* in, hc_conv_spec sp,

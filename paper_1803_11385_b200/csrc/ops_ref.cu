@@ -633,7 +633,7 @@ __global__ void k_check_switches(const int* sw, long long n, int fd, int* bad) {
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int s = sw[i];
-    if (s >= fd || s < -1) atomicOr(bad, 1);
+    if (s >= fd || s < -1) *reinterpret_cast<volatile int*>(bad) = 1;  // mapped host word
 }
 
 // ============================================================== dispatch helpers
@@ -987,20 +987,17 @@ hc_status max_unpool_impl(const T* coarse_data, int64_t c_rows, int64_t c_cols, 
         const long long fd = field_volume(spec, fine->d.dim);
         if (c_rows != spec.in_channels || c_cols != coarse->d.N)
             throw std::invalid_argument("max_unpool: coarse data shape mismatch");
-        // cnn_ops.cpp:326-332 check_switches (device scan; synchronises)
+        // cnn_ops.cpp:326-332 check_switches, stream-ordered and without a host round trip: the
+        // scan raises a sticky flag in mapped host memory that hc_deferred_status() reports
+        // (with the reference's message) once the caller has synchronised; an out-of-range
+        // switch matches no field row, so the unpool itself stays in bounds.
         if (s_rows != spec.in_channels || s_cols != coarse->d.N)
             throw std::invalid_argument("unpool: switch shape mismatch");
         cudaStream_t s = as_stream(stream);
         const long long n = s_rows * s_cols;
         if (n > 0) {
-            Scratch flag(sizeof(int), s);
-            cuda_check(cudaMemsetAsync(flag.p, 0, sizeof(int), s), "memset");
-            k_check_switches<<<grid_for(n, kThreads), kThreads, 0, s>>>(switches, n, (int)fd, flag.as<int>());
+            k_check_switches<<<grid_for(n, kThreads), kThreads, 0, s>>>(switches, n, (int)fd, deferred_flag_device());
             launched("switch check");
-            int bad = 0;
-            cuda_check(cudaMemcpyAsync(&bad, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s), "switch check");
-            cuda_check(cudaStreamSynchronize(s), "switch check");
-            if (bad) throw std::invalid_argument("unpool: switch index out of range");
         }
         launch_unpool(false, coarse_data, switches, fine, coarse, spec, result, s);
     });

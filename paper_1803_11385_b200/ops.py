@@ -228,15 +228,28 @@ def avg_pool(input: SuperPsh, input_data, output: SuperPsh, spec: ConvSpec):
     return a.out(res)
 
 
-def max_unpool(coarse_data, switches, fine: SuperPsh, coarse: SuperPsh, spec: ConvSpec):
-    """cnn_ops.cpp:336-372 (switch range validated; synchronises)"""
+def max_unpool(coarse_data, switches, fine: SuperPsh, coarse: SuperPsh, spec: ConvSpec, check_now: bool = True):
+    """cnn_ops.cpp:336-372. The switch range check (cnn_ops.cpp:326-332) runs on the stream
+    without a host round trip; with check_now (the reference's semantics: raise at the call)
+    the stream is synchronised and hc_deferred_status() raises ValueError for an out-of-range
+    switch. check_now=False keeps the call asynchronous (graph capture, pipelines): call
+    check_deferred() after a later synchronisation."""
     spec = ConvSpec(*spec)
     a = _Args()
     cd, sw = a.fp(coarse_data), a.i32(switches)
     res = _empty(spec.in_channels, fine.total_columns(), a.dtype)
     check(a.fn("hc_max_unpool")(_p(cd), *_shape(cd), _p(sw), *_shape(sw), fine._h, coarse._h, spec.c(), _p(res),
                                 _stream()))
+    if check_now:
+        torch.cuda.current_stream().synchronize()
+        check_deferred()
     return a.out(res)
+
+
+def check_deferred() -> None:
+    """Raise the first deferred argument error (ValueError, the reference's message) recorded
+    by a stream-ordered check since the last call (hc_deferred_status)."""
+    check(lib.hc_deferred_status())
 
 
 def avg_unpool(coarse_data, fine: SuperPsh, coarse: SuperPsh, spec: ConvSpec):

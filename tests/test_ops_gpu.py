@@ -521,3 +521,36 @@ def test_split_super_round_trip(cuda):
     for name in ("hash", "offsets", "tags", "model_of_slot", "hash_acc", "offset_acc", "data_acc", "hash_dims",
                  "offset_dims"):
         assert np.array_equal(getattr(a, name), getattr(b, name)), name
+
+
+def test_unpool_switch_check_is_stream_ordered(cuda):
+    """The switch range check never synchronises (ops_ref.cu max_unpool): asynchronous calls
+    record the failure for hc_deferred_status (cnn_ops.cpp:326-332's message), a valid call
+    records nothing, and max_unpool captures into a CUDA graph."""
+    f, c = random_pair(16, 1, seed=97)
+    fine, coarse = SuperPsh.from_levels(f), SuperPsh.from_levels(c)
+    d = _dev(levels_to_arrays(f).data)
+    sp = ConvSpec(2, 2, 0, 3, 3)
+    mp = ops.max_pool(fine, d, coarse, sp)
+    good = ops.max_unpool(mp.output, mp.switches, fine, coarse, sp, check_now=False)
+    torch.cuda.synchronize()
+    ops.check_deferred()  # nothing recorded
+    bad = mp.switches.clone()
+    bad[1, 2] = -7
+    ops.max_unpool(mp.output, bad, fine, coarse, sp, check_now=False)  # returns without raising
+    torch.cuda.synchronize()
+    with pytest.raises(ValueError, match="unpool: switch index out of range"):
+        ops.check_deferred()
+    ops.check_deferred()  # the flag is cleared by the report
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        ops.max_unpool(mp.output, mp.switches, fine, coarse, sp, check_now=False)  # warm-up
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        out = ops.max_unpool(mp.output, mp.switches, fine, coarse, sp, check_now=False)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, good)
+    ops.check_deferred()
