@@ -48,7 +48,7 @@ def main():
         ("hash2col", lambda: ops.hash2col(fine, x, fine, sp), 28 * C * N * 4 + 10 * M + 3 * R + 16 * N),
         ("col2hash", lambda: ops.col2hash(cols, fine, fine, sp), 28 * C * N * 4 + 10 * M + 3 * R + 16 * N),
         ("max_pool", lambda: ops.max_pool(fine, x, coarse, pool), C * N * 4 + C * Nc * 8),
-        ("max_unpool(+check)", lambda: ops.max_unpool(mp.output, mp.switches, fine, coarse, pool),
+        ("max_unpool", lambda: ops.max_unpool(mp.output, mp.switches, fine, coarse, pool, check_now=False),
          C * Nc * 8 + C * N * 4),
         ("avg_pool", lambda: ops.avg_pool(fine, x, coarse, pool), C * N * 4 + C * Nc * 4),
     ]
