@@ -65,6 +65,13 @@ constexpr int BK = 64;   // K elements (bf16) per stage = one 128-byte row
 constexpr int kMaxTaps = 27;
 constexpr int kNbrBytes = kMaxTaps * BM * 4;  // 13.5 KB field-map block per tile
 
+// Split-row layout: the planes interleave in blocks of g channels, g = 64 when the plane's
+// channel count is a multiple of 64 (else g = C, i.e. [hi | lo]): channel c of plane p sits at
+// (c / g) * 2g + p * g + c % g, so a 64-wide K stage holds one plane of 64 channels and its hi
+// and lo stages are adjacent (k_conv_fwd_x2 shares their weight tile).
+__host__ __device__ __forceinline__ int x2_block(int C) { return C % 64 == 0 ? 64 : C; }
+__host__ __device__ __forceinline__ int x2_pos(int c, int p, int g) { return (c / g) * 2 * g + p * g + c % g; }
+
 __host__ __device__ constexpr int tmem_cols(int n) {
     return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512;
 }
@@ -180,7 +187,7 @@ template <int BN, int CPS, int PW, typename OutT, bool SUMH = false>
 __global__ void __launch_bounds__(FwdCfg<BN, CPS, PW, sizeof(OutT)>::THREADS, CPS)
     k_conv_fwd(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap ymap,
                const int* __restrict__ fmap, int taps, long long rows, const bf16* __restrict__ X, int C, int nkb,
-               int tiles, int skip_lolo) {
+               int tiles, int skip_lolo /* SUMH: plane block g, 0 = keep lo x lo */) {
     using Cfg = FwdCfg<BN, CPS, PW, sizeof(OutT)>;
     constexpr int NP = Cfg::PRODUCERS;
     constexpr int S = Cfg::STAGES;
@@ -267,8 +274,12 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, PW, sizeof(OutT)>::THREADS, CP
                 mbar_wait_sleep(empty0 + 8 * s, ph ^ 1);
                 const uint32_t A = sbase + s * Cfg::STAGE_BYTES;
                 const char* xs = reinterpret_cast<const char*>(X + ci);
+#ifndef HCB_NO_GATHER  // A/B only: the pipeline without the gathers (MMA / issue bound)
 #pragma unroll
                 for (int j = 0; j < J; ++j) cp_async16_row(A + doff[j], xs, g[j], row_bytes);
+#else
+                if (g[0] == -12345) cp_async16_row(A + doff[0], xs, g[0], row_bytes);
+#endif
                 cp_async_arrive_noinc(full0 + 8 * s);
                 ci += BK;
                 while (ci >= C) {
@@ -359,7 +370,7 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, PW, sizeof(OutT)>::THREADS, CP
         constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, false, false);
         constexpr uint32_t idesc_h = idesc_bf16_f32(BM, SUMH ? BN / 2 : BN, false, false);
         const uint64_t a0 = sw128_desc(sbase, 16, 1024), b0 = sw128_desc(sbase + Cfg::A_BYTES, 16, 1024);
-        const int half = C / 2;  // SUMH: K offsets >= half of a row are the lo feature plane
+        const int g2 = skip_lolo;  // SUMH: plane block g (0: keep lo x lo); row offset kp is lo iff kp % 2g >= g
         int s = 0;
         uint32_t ph = 0;
         int i = 0;
@@ -376,13 +387,13 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, PW, sizeof(OutT)>::THREADS, CP
                 if (elect_one()) {
                     const uint64_t so = (uint64_t)((s * Cfg::STAGE_BYTES) >> 4);  // descriptor start-address units
                     if constexpr (SUMH) {
-                        int kp = kpos;
+                        int kp = kpos;  // offset inside the current 2g-wide [hi | lo] block
 #pragma unroll
                         for (int kk = 0; kk < BK / 16; ++kk) {
-                            const bool lo = skip_lolo && kp >= half;
+                            const bool lo = g2 && kp >= g2;
                             mma_bf16(d, a0 + so + 2 * kk, b0 + so + 2 * kk, lo ? idesc_h : idesc, (kb | kk) != 0);
                             kp += 16;
-                            if (kp >= C) kp -= C;
+                            if (kp >= 2 * g2) kp -= 2 * g2;
                         }
                     } else {
 #pragma unroll
@@ -392,13 +403,253 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, PW, sizeof(OutT)>::THREADS, CP
                     mma_commit(empty0 + 8 * s);
                 }
                 if constexpr (SUMH) {
-                    kpos += BK;
-                    while (kpos >= C) kpos -= C;
+                    if (g2) {
+                        kpos += BK;
+                        while (kpos >= 2 * g2) kpos -= 2 * g2;
+                    }
                 }
                 __syncwarp();
                 if (++s == S) {
                     s = 0;
                     ph ^= 1;
+                }
+            }
+            if (elect_one()) mma_commit(tfull0 + 8 * acc);
+            __syncwarp();
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == PW + 4) {
+        __syncwarp();
+        tc_fence_after();
+        tmem_dealloc(tmem, tmem_cols(2 * BN));
+    }
+}
+
+// ====================================================================== split-precision forward, shared weight ring
+// k_conv_fwd_x2: the SUMH forward for rows interleaved at 64 channels (C_in a multiple of 64:
+// row = [hi c0..63 | lo c0..63 | hi c64..127 | lo c64..127 ...]), so every hi stage is followed
+// by the lo stage of the same 64 channels, whose weight slice is identical (the packed operand
+// repeats it). The weight tiles therefore live in their own ring, one per (hi, lo) pair: half the
+// TMA loads and L2 weight traffic of k_conv_fwd<SUMH>, and a weight tile is requested two A
+// stages further ahead. NBUF field-map buffers (1 frees 13.5 KB for a deeper A ring).
+//   hi stage: D[:, 0:BN] += A_hi . [W_hi; W_lo]^T  (N = BN)      lo stage: D[:, 0:BN/2] += A_lo . W_hi^T
+template <int BN, int CPS, int PW, int SA, int SB, int NBUF>
+struct FwdX2Cfg {
+    static constexpr int A_BYTES = BM * 128;
+    static constexpr int B_BYTES = BN * 128;
+    static constexpr int NBR = NBUF * kNbrBytes;
+    static constexpr int EPI = 4 * 32 * 16 * 4;  // fp32 staging, one 32 x 16 box per epilogue warp
+    static constexpr int THREADS = PW * 32 + 192;
+    static constexpr int SMEM = 1024 + SA * A_BYTES + SB * B_BYTES + NBR + EPI + 512;
+    static_assert(SMEM <= (CPS == 2 ? 113 : 226) * 1024, "shared memory budget");
+};
+
+template <int BN, int CPS, int PW, int SA, int SB, int NBUF>
+__global__ void __launch_bounds__(FwdX2Cfg<BN, CPS, PW, SA, SB, NBUF>::THREADS, CPS)
+    k_conv_fwd_x2(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap ymap,
+                  const int* __restrict__ fmap, int taps, const bf16* __restrict__ X, int C, int nkb, int tiles) {
+    using Cfg = FwdX2Cfg<BN, CPS, PW, SA, SB, NBUF>;
+    constexpr int NP = PW * 32;
+    constexpr int RS = NP / 8;
+    constexpr int J = BM / RS;
+    constexpr int BO = BN / 2;  // output channels
+    static_assert(BM % RS == 0 && J % 4 == 0 && SA >= 2 && SB >= 1, "producer / ring shape");
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* bsm = smem + SA * Cfg::A_BYTES;
+    int* nbr_s = reinterpret_cast<int*>(bsm + SB * Cfg::B_BYTES);
+    uint8_t* epi_s = reinterpret_cast<uint8_t*>(nbr_s) + Cfg::NBR;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(epi_s + Cfg::EPI);
+    // bars: afull[SA] aempty[SA] bfull[SB] bempty[SB] tfull[2] tempty[2] nfull[NBUF]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * SA + 2 * SB + 4 + NBUF);
+    int* nbr_cnt = reinterpret_cast<int*>(tmem_slot + 2);
+
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const uint32_t sbase = smem_u32(smem), bbase = smem_u32(bsm);
+    const uint32_t afull0 = smem_u32(bars), aempty0 = smem_u32(bars + SA);
+    const uint32_t bfull0 = smem_u32(bars + 2 * SA), bempty0 = smem_u32(bars + 2 * SA + SB);
+    const uint32_t tfull0 = smem_u32(bars + 2 * SA + 2 * SB), tempty0 = tfull0 + 16;
+    const uint32_t nfull0 = tfull0 + 32;
+    const uint32_t nbr_bytes = (uint32_t)(taps * BM * 4);
+
+    if (tid == 0) {
+        for (int s = 0; s < SA; ++s) {
+            mbar_init(afull0 + 8 * s, NP);
+            mbar_init(aempty0 + 8 * s, 1);
+        }
+        for (int s = 0; s < SB; ++s) {
+            mbar_init(bfull0 + 8 * s, 1);
+            mbar_init(bempty0 + 8 * s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(tfull0 + 8 * a, 1);
+            mbar_init(tempty0 + 8 * a, 128);
+        }
+        for (int a = 0; a < NBUF; ++a) {
+            mbar_init(nfull0 + 8 * a, 1);
+            nbr_cnt[a] = 0;
+        }
+        mbar_init_fence();
+    }
+    if (warp == PW + 4) tmem_alloc(smem_u32(tmem_slot), tmem_cols(2 * BN));
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp < PW) {
+        // ---------------- producers (as k_conv_fwd: J consecutive rows x one 16-byte chunk)
+        const int c = tid & 7;
+        const int r0 = (tid >> 3) * J;
+        uint32_t doff[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) doff[j] = sw128_offset(r0 + j, c);
+        const uint32_t row_bytes = (uint32_t)C * 2;
+        auto request = [&](int tile, int buf) {
+            mbar_arrive_expect_tx(nfull0 + 8 * buf, nbr_bytes);
+            bulk_g2s(smem_u32(nbr_s + buf * kMaxTaps * BM), fmap + (long long)tile * taps * BM, nbr_bytes,
+                     nfull0 + 8 * buf);
+        };
+        if (tid == 0)
+            for (int b = 0; b < NBUF; ++b)
+                if (blockIdx.x + b * gridDim.x < tiles) request(blockIdx.x + b * gridDim.x, b);
+        int s = 0;
+        uint32_t ph = 0;
+        int i = 0;
+        for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++i) {
+            const int buf = NBUF == 1 ? 0 : i % NBUF;
+            mbar_wait_sleep(nfull0 + 8 * buf, (uint32_t)((i / NBUF) & 1));
+            const uint32_t nb = smem_u32(nbr_s + buf * kMaxTaps * BM + r0);
+            int t = 0, ci = c * 8;  // C >= 128: a 64-wide stage never crosses a tap
+            for (int kb = 0; kb < nkb; ++kb) {
+                int g[J];
+                if (t < taps) {
+#pragma unroll
+                    for (int j = 0; j < J; j += 4) {
+                        const int4 v = ld_shared_v4(nb + (t * BM + j) * 4);
+                        g[j] = v.x, g[j + 1] = v.y, g[j + 2] = v.z, g[j + 3] = v.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < J; ++j) g[j] = -1;
+                }
+                mbar_wait_sleep(aempty0 + 8 * s, ph ^ 1);
+                const uint32_t A = sbase + s * Cfg::A_BYTES;
+                const char* xs = reinterpret_cast<const char*>(X + ci);
+#pragma unroll
+                for (int j = 0; j < J; ++j) cp_async16_row(A + doff[j], xs, g[j], row_bytes);
+                cp_async_arrive_noinc(afull0 + 8 * s);
+                ci += BK;
+                if (ci >= C) {
+                    ci -= C;
+                    ++t;
+                }
+                if (++s == SA) {
+                    s = 0;
+                    ph ^= 1;
+                }
+            }
+            __syncwarp();
+            if ((tid & 31) == 0 && atomicAdd(&nbr_cnt[buf], 1) == PW - 1) {
+                nbr_cnt[buf] = 0;
+                if (tile + NBUF * (int)gridDim.x < tiles) request(tile + NBUF * gridDim.x, buf);
+            }
+        }
+    } else if (warp < PW + 4) {
+        // ---------------- epilogue: D[:, co] + D[:, BO + co] -> fp32 -> staging -> TMA store
+        const int q = warp & 3;
+        const int lane = (int)lane_id();
+        uint8_t* stage = epi_s + q * (32 * 16 * 4);
+        int i = 0, issued = 0;
+        for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++i) {
+            const int acc = i & 1;
+            mbar_wait_sleep(tfull0 + 8 * acc, (uint32_t)((i >> 1) & 1));
+            tc_fence_after();
+            const int r0 = tile * BM + q * 32;
+#pragma unroll
+            for (int c0 = 0; c0 < BO; c0 += 16) {
+                uint32_t v[16], u[16];
+                const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + acc * BN + c0;
+                tmem_ld16(ta, v);
+                tmem_ld16(ta + BO, u);
+                tmem_ld_wait();
+                float f[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(v[e]) + __uint_as_float(u[e]);
+                if (issued) {  // the staging box's previous store has been read
+                    if (lane == 0) bulk_wait_read<0>();
+                    __syncwarp();
+                }
+                stage_row16(stage, lane, f, (float*)nullptr);
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store2d(&ymap, smem_u32(stage), c0, r0);
+                    bulk_commit();
+                }
+                issued = 1;
+            }
+            tc_fence_before();
+            mbar_arrive(tempty0 + 8 * acc);
+        }
+        if (lane == 0) bulk_wait<0>();
+        __syncwarp();
+    } else if (tid == (PW + 5) * 32) {
+        // ---------------- weight loader: one [W_hi; W_lo] tile per (hi, lo) stage pair
+        int s = 0;
+        uint32_t ph = 0;
+        for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+            for (int kb = 0; kb < nkb; kb += 2) {
+                mbar_wait_sleep(bempty0 + 8 * s, ph ^ 1);
+                mbar_arrive_expect_tx(bfull0 + 8 * s, Cfg::B_BYTES);
+                tma_load2d(bbase + s * Cfg::B_BYTES, &wmap, kb * BK, 0, bfull0 + 8 * s);
+                if (++s == SB) {
+                    s = 0;
+                    ph ^= 1;
+                }
+            }
+        }
+    } else if (warp == PW + 4) {
+        // ---------------- MMA issuer
+        constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, false, false);
+        constexpr uint32_t idesc_h = idesc_bf16_f32(BM, BO, false, false);
+        const uint64_t a0 = sw128_desc(sbase, 16, 1024), b0 = sw128_desc(bbase, 16, 1024);
+        int sa = 0, sb = 0;
+        uint32_t pha = 0, phb = 0;
+        int i = 0;
+        for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++i) {
+            const int acc = i & 1;
+            mbar_wait(tempty0 + 8 * acc, (uint32_t)(((i >> 1) & 1) ^ 1));
+            tc_fence_after();
+            const uint32_t d = tmem + acc * BN;
+            for (int kb = 0; kb < nkb; kb += 2) {
+                mbar_wait(bfull0 + 8 * sb, phb);
+                const uint64_t bo = (uint64_t)((sb * Cfg::B_BYTES) >> 4);
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {  // hi stage (N = BN), then lo stage (N = BN/2)
+                    mbar_wait(afull0 + 8 * sa, pha);
+                    fence_proxy_async();
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint64_t ao = (uint64_t)((sa * Cfg::A_BYTES) >> 4);
+#pragma unroll
+                        for (int kk = 0; kk < BK / 16; ++kk)
+                            mma_bf16(d, a0 + ao + 2 * kk, b0 + bo + 2 * kk, half ? idesc_h : idesc,
+                                     (kb | half | kk) != 0);
+                        mma_commit(aempty0 + 8 * sa);
+                        if (half) mma_commit(bempty0 + 8 * sb);
+                    }
+                    __syncwarp();
+                    if (++sa == SA) {
+                        sa = 0;
+                        pha ^= 1;
+                    }
+                }
+                if (++sb == SB) {
+                    sb = 0;
+                    phb ^= 1;
                 }
             }
             if (elect_one()) mma_commit(tfull0 + 8 * acc);
@@ -515,7 +766,7 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
     for (int e = tid; e < nm * 16; e += blockDim.x) {
         const int blk = (e / 8) & 1;
         const int m = pair ? (m0 + e / 16) * 64 + (e & 7) * 8 : (m0 + e / 16) * 128 + blk * 64 + (e & 7) * 8;
-        tab[e] = m < K ? ((m / Co - t_lo) << 16) | ((pair ? blk * Co : 0) + m % Co) : -1;
+        tab[e] = m < K ? ((m / Co - t_lo) << 16) | (pair ? x2_pos(m % Co, blk, x2_block(Co)) : m % Co) : -1;
     }
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
@@ -688,9 +939,9 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
                 for (int mi = 0; mi < nm; ++mi) {
                     float* dst = partial + grp_tab.part_begin[grp] + ((slot * nm + mi) * 64 + r) * pc;
                     for (int c0 = 0; c0 < pc; c0 += 16) {
-                        uint32_t a[16], b[16];
-                        tmem_ld16(tq + mi * NB + c0, a);
-                        tmem_ld16(tq + mi * NB + pc + c0, b);
+                        uint32_t a[16], b[16];  // dY planes interleave like X's (x2_pos)
+                        tmem_ld16(tq + mi * NB + x2_pos(c0, 0, x2_block(pc)), a);
+                        tmem_ld16(tq + mi * NB + x2_pos(c0, 1, x2_block(pc)), b);
                         tmem_ld_wait();
                         float f[16];
 #pragma unroll
@@ -848,11 +1099,12 @@ __global__ void k_pack_w_x2(const float* __restrict__ w, int cout, int cin, int 
     const int rr = (int)(i / Kp2), k = (int)(i % Kp2);
     const int q = rr >= rows, r = rr - q * rows;
     const int ck = mode ? cout_p : cin_p;
+    const int g = x2_block(ck);
     float v = 0.0f;
     if (k < taps * 2 * ck) {
         const int t = k / (2 * ck);
-        int c = k - t * 2 * ck;
-        if (c >= ck) c -= ck;
+        const int kr = k - t * 2 * ck;                     // position inside the tap's row
+        const int c = (kr / (2 * g)) * g + kr % g;         // channel (either plane)
         const int co = mode ? c : r, ci = mode ? r : c;
         if (co < cout && ci < cin)
             v = w[(long long)co * cin * taps + ci * taps + (mode == 1 ? taps - 1 - t : t)];
@@ -878,8 +1130,9 @@ __global__ void k_split_cm(const float* __restrict__ in, long long C, long long 
         if (c < Cp && n < N) {
             bf16 hi, lo;
             split2(tile[threadIdx.x][i], hi, lo);
-            out[n * 2 * Cp + c] = hi;
-            out[n * 2 * Cp + Cp + c] = lo;
+            const int g = x2_block((int)Cp);
+            out[n * 2 * Cp + x2_pos((int)c, 0, g)] = hi;
+            out[n * 2 * Cp + x2_pos((int)c, 1, g)] = lo;
         }
     }
 }
@@ -898,8 +1151,9 @@ __global__ void k_split_vm(const float4* __restrict__ in, long long N, int C, bf
     split2(v.z, h[2], l[2]);
     split2(v.w, h[3], l[3]);
     bf16* row = out + n * 2 * C;
-    *reinterpret_cast<uint2*>(row + c) = *reinterpret_cast<uint2*>(h);
-    *reinterpret_cast<uint2*>(row + C + c) = *reinterpret_cast<uint2*>(l);
+    const int g = x2_block(C);
+    *reinterpret_cast<uint2*>(row + x2_pos(c, 0, g)) = *reinterpret_cast<uint2*>(h);
+    *reinterpret_cast<uint2*>(row + x2_pos(c, 1, g)) = *reinterpret_cast<uint2*>(l);
 }
 
 // Transposed field map for the deconvolution (cnn_ops.cpp:408-419, col2hash of W^T D):
@@ -1000,16 +1254,54 @@ template <int BN>
 void launch_fwd_x2(const int* fmap, int taps, long long rows, const bf16* X, int C, const bf16* Wp, int Kp, float* Y,
                    cudaStream_t s, int skip_lolo) {
     static const int cps = env_int("HCB_X2_CPS", BN <= 128 ? 2 : 1);
+    static const int pw = env_int("HCB_X2_PW", 4);
     if constexpr (BN <= 128) {
+        if (cps == 2 && pw == 8) return launch_fwd<BN, 2, 8, float, true>(fmap, taps, rows, X, C, Wp, Kp, Y, s, skip_lolo);
+        if (cps == 2 && pw == 2) return launch_fwd<BN, 2, 2, float, true>(fmap, taps, rows, X, C, Wp, Kp, Y, s, skip_lolo);
         if (cps == 2) return launch_fwd<BN, 2, 4, float, true>(fmap, taps, rows, X, C, Wp, Kp, Y, s, skip_lolo);
     }
     launch_fwd<BN, 1, 4, float, true>(fmap, taps, rows, X, C, Wp, Kp, Y, s, skip_lolo);
 }
 
+template <int BN, int CPS, int PW, int SA, int SB, int NBUF>
+void launch_fwd_x2s(const int* fmap, int taps, long long rows, const bf16* X, int C, const bf16* Wp, int Kp, float* Y,
+                    cudaStream_t s) {
+    using Cfg = FwdX2Cfg<BN, CPS, PW, SA, SB, NBUF>;
+    auto kern = k_conv_fwd_x2<BN, CPS, PW, SA, SB, NBUF>;
+    smem_optin(kern, Cfg::SMEM);
+    const CUtensorMap wm = map2d(Wp, (uint64_t)Kp, (uint64_t)BN, (uint64_t)Kp * 2, BN);
+    const int tiles = (int)((rows + BM - 1) / BM);
+    const int grid = std::min(tiles, CPS * num_sms());
+    const CUtensorMap ym = map_out(Y, true, (uint64_t)(BN / 2), (uint64_t)rows, 16, 32);
+    kern<<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(wm, ym, fmap, taps, X, C, Kp / BK, tiles);
+    launched("conv gather-GEMM, split precision, shared weight ring (tcgen05)");
+}
+
+// C_in a multiple of 64 (rows interleaved per 64 channels): the shared-weight-ring kernel.
+// HCB_X2_RING: 0 = the generic SUMH kernel, 1 = (A 2, B 2, 2 map buffers), 2 = (A 3, B 2, 1 map buffer).
+bool conv_fwd_x2_shared(const int* fmap, int taps, long long rows, const bf16* X, int C2, const bf16* Wp, int Kp,
+                        int N2, float* Y, cudaStream_t s) {
+    static const int ring = env_int("HCB_X2_RING", 2);
+    if (ring == 0 || (C2 / 2) % 64 != 0) return false;
+    if (N2 == 128) {
+        if (ring == 2) launch_fwd_x2s<128, 2, 4, 3, 2, 1>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
+        else launch_fwd_x2s<128, 2, 4, 2, 2, 2>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
+        return true;
+    }
+    if (N2 == 64) {
+        if (ring == 2) launch_fwd_x2s<64, 2, 4, 3, 2, 1>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
+        else launch_fwd_x2s<64, 2, 4, 2, 2, 2>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
+        return true;
+    }
+    return false;
+}
+
 void conv_fwd_x2(const int* fmap, int taps, long long rows, const bf16* X, int C2, const bf16* Wp, int Kp, int N2,
                  float* Y, cudaStream_t s) {
+    if (conv_fwd_x2_shared(fmap, taps, rows, X, C2, Wp, Kp, N2, Y, s)) return;
     static const int keep_lolo = env_int("HCB_X2_LOLO", 0);
-    const int skip = (!keep_lolo && (C2 / 2) % 16 == 0) ? 1 : 0;
+    const int g = x2_block(C2 / 2);
+    const int skip = (!keep_lolo && g % 16 == 0) ? g : 0;  // the lo plane's K16 chunks issue N = BN/2
     switch (N2) {
         case 32: launch_fwd_x2<32>(fmap, taps, rows, X, C2, Wp, Kp, Y, s, skip); break;
         case 64: launch_fwd_x2<64>(fmap, taps, rows, X, C2, Wp, Kp, Y, s, skip); break;

@@ -1,2 +1,2 @@
-timeout 600 python -m pytest -q tests/test_dp_host.py 2>&1 | tail -3
-RANK=0 WORLD_SIZE=1 LOCAL_RANK=0 timeout 300 ./hosts/_build/dp_conv --psh paper_1803_11385_b200/_cache/shell256_l01.psh --steps 20 --warmup 5
+timeout 900 python -m pytest -q -x tests/test_conv_f32.py tests/test_dropin_cpp.py 2>&1 | grep -E "Error|error|assert|FAILED|passed|failed" | head -20
+./tests/cpp/_build/dropin_parity | grep -E "fast conv|DROPIN"
