@@ -538,8 +538,12 @@ __global__ void __launch_bounds__(FwdX2Cfg<BN, CPS, PW, SA, SB, NBUF>::THREADS, 
                 mbar_wait_sleep(aempty0 + 8 * s, ph ^ 1);
                 const uint32_t A = sbase + s * Cfg::A_BYTES;
                 const char* xs = reinterpret_cast<const char*>(X + ci);
+#ifndef HCB_NO_GATHER
 #pragma unroll
                 for (int j = 0; j < J; ++j) cp_async16_row(A + doff[j], xs, g[j], row_bytes);
+#else
+                if (g[0] == -12345) cp_async16_row(A + doff[0], xs, g[0], row_bytes);
+#endif
                 cp_async_arrive_noinc(afull0 + 8 * s);
                 ci += BK;
                 if (ci >= C) {
@@ -690,6 +694,7 @@ constexpr int kMaxGroups = 64;
 struct DwGroups {
     int groups;
     int pair, rpm, pcols;
+    int nacc;  // accumulator buffers per CTA (2: chunk drains overlap the next chunk's MMAs)
     int m_begin[kMaxGroups + 1];
     int cta_begin[kMaxGroups + 1];
     int tps[kMaxGroups];
@@ -737,7 +742,7 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
     float* xch = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(nbr_s) + Cfg::NBR);
     int* tab = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(xch) + Cfg::XCH);  // [m-tile][2 blocks][8 chunks]
     uint64_t* bars = reinterpret_cast<uint64_t*>(tab + 256);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 2 * BS + 4);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 2 * BS + 6);
     int* nbr_cnt = reinterpret_cast<int*>(tmem_slot + 2);
 
     const int tid = threadIdx.x, warp = tid >> 5;
@@ -757,7 +762,10 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
     const uint32_t sbase = smem_u32(smem), bbase = smem_u32(bsm);
     const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S);
     const uint32_t bfull0 = smem_u32(bars + 2 * S), bempty0 = smem_u32(bars + 2 * S + BS);
-    const uint32_t nfull0 = smem_u32(bars + 2 * S + 2 * BS), done = nfull0 + 16, drained = nfull0 + 24;
+    // done[b] / drained[b]: accumulator buffer b (nacc = 2: chunk c uses buffer c & 1, so the epilogue
+    // drains one chunk while the MMA accumulates the next)
+    const uint32_t nfull0 = smem_u32(bars + 2 * S + 2 * BS), done0 = nfull0 + 16, drained0 = nfull0 + 32;
+    const int nacc = grp_tab.nacc;
     // taps [t_lo, t_lo + ntb) cover this CTA's (t, ci) rows; only they are staged
     const int t_lo = (m0 * RPM) / Co;
     const int ntb = min(NT, (min(K, (m0 + nm) * RPM) - 1) / Co - t_lo + 1);
@@ -780,8 +788,10 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
         mbar_init(nfull0, 1);
         mbar_init(nfull0 + 8, 1);
         nbr_cnt[0] = nbr_cnt[1] = 0;
-        mbar_init(done, 1);
-        mbar_init(drained, 128);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(done0 + 8 * b, 1);
+            mbar_init(drained0 + 8 * b, 128);
+        }
         mbar_init_fence();
     }
     if (warp == PW) tmem_alloc(smem_u32(tmem_slot), Cfg::TMEM_COLS);
@@ -837,8 +847,12 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
                     mbar_wait_sleep(empty0 + 8 * s, ph ^ 1);
                     const uint32_t A = sbase + s * Cfg::A_BYTES;
                     const char* xs = reinterpret_cast<const char*>(X + (e & 0xffff));
+#ifndef HCB_NO_GATHER
 #pragma unroll
                     for (int j = 0; j < J; ++j) cp_async16_row(A + doff[j], xs, g[j], row_bytes);
+#else
+                    if (g[0] == -12345) cp_async16_row(A + doff[0], xs, g[0], row_bytes);
+#endif
                     cp_async_arrive_noinc(full0 + 8 * s);
                     if (++s == S) {
                         s = 0;
@@ -882,10 +896,13 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
         uint32_t ph = 0, bph = 0;
         int cl = 0, ci = 0;  // tile index inside the chunk, chunk index
         for (int lt = 0; lt < ntl; ++lt) {
-            if (cl == 0 && ci > 0) {
-                mbar_wait(drained, (uint32_t)((ci - 1) & 1));
+            const int ab = nacc == 2 ? (ci & 1) : 0;  // accumulator buffer of this chunk
+            if (cl == 0 && ci >= nacc) {                 // its previous chunk has been drained
+                const int prev = ci - nacc;
+                mbar_wait(drained0 + 8 * ab, (uint32_t)((nacc == 2 ? prev >> 1 : prev) & 1));
                 tc_fence_after();
             }
+            const uint32_t acc0 = tmem + ab * nm * NB;
             for (int h = 0; h < 2; ++h) {
                 mbar_wait(bfull0 + 8 * bs, bph);
                 const uint64_t bo = (uint64_t)((bs * Cfg::B_BYTES) >> 4);
@@ -897,7 +914,7 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
                         const uint64_t ao = (uint64_t)((s * Cfg::A_BYTES) >> 4);
 #pragma unroll
                         for (int kk = 0; kk < Cfg::KB / 16; ++kk)  // 16 voxels = two 8-row atoms per MMA
-                            mma_bf16(tmem + mi * NB, a0 + ao + 128 * kk, b0 + bo + 128 * kk, idesc,
+                            mma_bf16(acc0 + mi * NB, a0 + ao + 128 * kk, b0 + bo + 128 * kk, idesc,
                                      (cl | h | kk) != 0);
                         mma_commit(empty0 + 8 * s);
                     }
@@ -915,7 +932,7 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
                 }
             }
             if (++cl == tps || lt == ntl - 1) {
-                if (elect_one()) mma_commit(done);
+                if (elect_one()) mma_commit(done0 + 8 * ab);
                 __syncwarp();
                 cl = 0;
                 ++ci;
@@ -927,7 +944,9 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
         const int row = q * 32 + (int)lane_id();
         const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
         for (int c = 0; c < nch; ++c) {
-            mbar_wait_sleep(done, (uint32_t)(c & 1));
+            const int ab = nacc == 2 ? (c & 1) : 0;
+            mbar_wait_sleep(done0 + 8 * ab, (uint32_t)((nacc == 2 ? c >> 1 : c) & 1));
+            const uint32_t tqa = tq + ab * nm * NB;
             tc_fence_after();
             const long long slot = chunk0 + c;
             if (pair) {
@@ -940,8 +959,8 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
                     float* dst = partial + grp_tab.part_begin[grp] + ((slot * nm + mi) * 64 + r) * pc;
                     for (int c0 = 0; c0 < pc; c0 += 16) {
                         uint32_t a[16], b[16];  // dY planes interleave like X's (x2_pos)
-                        tmem_ld16(tq + mi * NB + x2_pos(c0, 0, x2_block(pc)), a);
-                        tmem_ld16(tq + mi * NB + x2_pos(c0, 1, x2_block(pc)), b);
+                        tmem_ld16(tqa + mi * NB + x2_pos(c0, 0, x2_block(pc)), a);
+                        tmem_ld16(tqa + mi * NB + x2_pos(c0, 1, x2_block(pc)), b);
                         tmem_ld_wait();
                         float f[16];
 #pragma unroll
@@ -969,7 +988,7 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
 #pragma unroll
                     for (int c0 = 0; c0 < NB; c0 += 16) {
                         uint32_t v[16];
-                        tmem_ld16(tq + mi * NB + c0, v);
+                        tmem_ld16(tqa + mi * NB + c0, v);
                         tmem_ld_wait();
                         float f[16];
 #pragma unroll
@@ -979,7 +998,7 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
                 }
             }
             tc_fence_before();
-            mbar_arrive(drained);
+            mbar_arrive(drained0 + 8 * ab);
         }
     }
     tc_fence_before();
@@ -1284,7 +1303,8 @@ bool conv_fwd_x2_shared(const int* fmap, int taps, long long rows, const bf16* X
     static const int ring = env_int("HCB_X2_RING", 2);
     if (ring == 0 || (C2 / 2) % 64 != 0) return false;
     if (N2 == 128) {
-        if (ring == 2) launch_fwd_x2s<128, 2, 4, 3, 2, 1>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
+        if (ring == 3) launch_fwd_x2s<128, 2, 4, 2, 3, 1>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
+        else if (ring == 2) launch_fwd_x2s<128, 2, 4, 3, 2, 1>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
         else launch_fwd_x2s<128, 2, 4, 2, 2, 2>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
         return true;
     }
@@ -1352,7 +1372,11 @@ DwPlan dw_plan(long long rows, int taps, int cin, int cout, int max_tps = 0, boo
     p.mt = (taps * cin + rpm - 1) / rpm;
     p.cps = dw_cps(p.nb);
     p.tiles = (int)((rows + BM - 1) / BM);
-    const int cap = 512 / (p.nb * p.cps);  // m-tiles whose accumulators fit one CTA's TMEM
+    // pair mode with chunked accumulation: HCB_DW_DBUF=1 keeps two accumulator sets per CTA (the
+    // epilogue drains one chunk while the next accumulates) at half the m-tiles per CTA
+    static const int dbuf_env = env_int("HCB_DW_DBUF", 0);
+    const int nacc = (pair && max_tps > 0 && dbuf_env) ? 2 : 1;
+    const int cap = 512 / (p.nb * p.cps * nacc);  // m-tiles whose accumulators fit one CTA's TMEM
     const int G = (p.mt + cap - 1) / cap;  // -> every group has <= cap m-tiles
     if (G > kMaxGroups)
         throw std::invalid_argument("native conv: dW supports at most " + std::to_string(kMaxGroups * cap * BM) +
@@ -1361,6 +1385,7 @@ DwPlan dw_plan(long long rows, int taps, int cin, int cout, int max_tps = 0, boo
     DwGroups& g = p.g;
     g.groups = G;
     g.pair = pair ? 1 : 0;
+    g.nacc = nacc;
     g.rpm = rpm;
     g.pcols = pair ? cout : p.nb;
     // Few groups (C_out <= 64): CTAs proportional to each group's m-tiles, so groups of
