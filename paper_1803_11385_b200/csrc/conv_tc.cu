@@ -607,8 +607,14 @@ __global__ void __launch_bounds__(FwdX2Cfg<BN, CPS, PW, SA, SB, NBUF>::THREADS, 
         for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
             for (int kb = 0; kb < nkb; kb += 2) {
                 mbar_wait_sleep(bempty0 + 8 * s, ph ^ 1);
+#ifdef HCB_NO_BLOAD  // A/B only (wrong results): weight tiles loaded once, then reused
+                if (tile != (int)blockIdx.x || kb >= 2 * SB) { mbar_arrive(bfull0 + 8 * s); goto next_w; }
+#endif
                 mbar_arrive_expect_tx(bfull0 + 8 * s, Cfg::B_BYTES);
                 tma_load2d(bbase + s * Cfg::B_BYTES, &wmap, kb * BK, 0, bfull0 + 8 * s);
+#ifdef HCB_NO_BLOAD
+            next_w:
+#endif
                 if (++s == SB) {
                     s = 0;
                     ph ^= 1;
@@ -874,12 +880,20 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
         for (int lt = 0; lt < ntl; ++lt)
             for (int h = 0; h < 2; ++h) {
                 mbar_wait_sleep(bempty0 + 8 * bs, bph ^ 1);
+#ifdef HCB_NO_BLOAD  // A/B only (wrong results): dY tiles loaded once, then reused
+                if (lt >= 1) { mbar_arrive(bfull0 + 8 * bs); goto next_b; }
+#endif
+                {
                 mbar_arrive_expect_tx(bfull0 + 8 * bs, Cfg::B_BYTES);
                 const int n0 = (tile0 + lt) * BM + h * 64;
 #pragma unroll
                 for (int cb = 0; cb < NB / 64; ++cb)
                     tma_load2d(bbase + bs * Cfg::B_BYTES + cb * (Cfg::KB * 128), &dymap, cb * 64, n0,
                                bfull0 + 8 * bs);
+                }
+#ifdef HCB_NO_BLOAD
+            next_b:
+#endif
                 if (++bs == BS) {
                     bs = 0;
                     bph ^= 1;
@@ -1304,6 +1318,10 @@ bool conv_fwd_x2_shared(const int* fmap, int taps, long long rows, const bf16* X
     if (ring == 0 || (C2 / 2) % 64 != 0) return false;
     if (N2 == 128) {
         if (ring == 3) launch_fwd_x2s<128, 2, 4, 2, 3, 1>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
+        else if (ring == 4) launch_fwd_x2s<128, 1, 4, 8, 2, 2>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
+        else if (ring == 5) launch_fwd_x2s<128, 1, 8, 8, 2, 2>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
+        else if (ring == 6) launch_fwd_x2s<128, 1, 8, 9, 3, 1>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
+        else if (ring == 7) launch_fwd_x2s<128, 2, 8, 3, 2, 1>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
         else if (ring == 2) launch_fwd_x2s<128, 2, 4, 3, 2, 1>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
         else launch_fwd_x2s<128, 2, 4, 2, 2, 2>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
         return true;
