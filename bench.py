@@ -333,7 +333,7 @@ class MaterializedStep:
 class FusedStepF32:
     """Native path at the reference's precision (include/hashconv_b200_native.h, split
     precision): field map K0 -> fp32 X and dY split into bf16 hi/lo planes -> tcgen05
-    gather-GEMM forward (hi.hi + hi.lo + lo.hi) -> split-K tcgen05 dW (four plane products,
+    gather-GEMM forward (hi.hi + hi.lo + lo.hi) -> split-K tcgen05 dW (three plane products,
     8192-voxel accumulation chains, fixed-order reduction) -> tcgen05 dX (flipped kernel).
     fp32 in, fp32 out, within 1e-5 (normwise) of the float64 instantiation on unquantised
     inputs (tests/test_conv_f32.py). The column matrix never exists in HBM; weights are
@@ -341,7 +341,7 @@ class FusedStepF32:
 
     name = "fused implicit-GEMM, fp32 via bf16 hi/lo split (tcgen05, fp32 accumulate)"
     dtype = "f32"
-    products = {"fwd_conv": 3, "dW_conv": 4, "dX_conv": 3}
+    products = {"fwd_conv": 3, "dW_conv": 3, "dX_conv": 3}  # dW: tri mode (c_out >= 32)
 
     def __init__(self, fine, cin, cout, dev):
         import torch
@@ -360,6 +360,7 @@ class FusedStepF32:
         self.dy = self.dy_ref.t().contiguous()
         self.ws = conv.DwWorkspace()
         self.N, self.cin, self.cout = N, cin, cout
+        self.products = dict(self.products, dW_conv=3 if cout >= 32 else 4)  # conv_tc.cu dw_plan: tri mode
         self.op_names = ["field_map", "split_pack", "fwd_conv", "dW_conv", "dX_conv"]
 
     def _layer(self, fmap, xs, dys, w, marks, on_dw=None):

@@ -690,6 +690,10 @@ __global__ void __launch_bounds__(FwdX2Cfg<BN, CPS, PW, SA, SB, NBUF>::THREADS, 
 // tiles; CTA k of the group runs chunks [k*cpc[g], (k+1)*cpc[g]) back to back, draining its
 // TMEM accumulators into one partial slot per chunk (a chunk is one accumulation chain: the
 // split-precision path bounds it to keep the tensor core's fp32 accumulation within 1e-5).
+//   tri (split precision, c_out >= 32, default): units of 128 (t, ci) rows; the hi-plane m-tile
+//     multiplies [dY_hi | dY_lo] (N = 2 c_out), the lo-plane m-tile dY_hi only (N = c_out), so the
+//     negligible lo.lo product is never computed (3 products instead of 4); each epilogue lane sums
+//     its own row (hi.hi + hi.lo) + lo.hi, rpm = 128 rows x c_out.
 // Partials start at part_begin[g] (floats), laid out [chunk][m-tile][rpm][pcols]:
 //   plain: rpm = 128 (t,ci) rows of the row width C, pcols = NB.
 //   pair (split precision, hc_native_conv_dw_x2): X rows are [hi | lo] (C = 2 c), dY rows
@@ -761,9 +765,11 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
     const int nch = max(0, min(grp_tab.cpc[grp], grp_tab.nchunk[grp] - chunk0));
     const int tile0 = chunk0 * tps;
     const int ntl = max(0, min(nch * tps, tiles - tile0));
-    const int pair = grp_tab.pair;
+    const int pair = grp_tab.pair;    // 0 plain, 1 pair (split precision, 4 products), 2 tri (3 products)
     const int Co = pair ? C / 2 : C;  // channels of one plane
-    const int RPM = pair ? 64 : 128;  // (t, ci) rows per m-tile
+    const int RPM = pair == 1 ? 64 : 128;  // (t, ci) rows per m-tile (tri: per unit)
+    const int nmt = pair == 2 ? 2 * nm : nm;  // m-tiles the producers fill / the MMA consumes per stage
+    const int pco = grp_tab.pcols;             // tri: c_out (one plane)
     const int K = taps * Co;
     const uint32_t sbase = smem_u32(smem), bbase = smem_u32(bsm);
     const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S);
@@ -777,10 +783,20 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
     const int ntb = min(NT, (min(K, (m0 + nm) * RPM) - 1) / Co - t_lo + 1);
     const uint32_t nbr_bytes = (uint32_t)(ntb * BM * 4);
 
-    for (int e = tid; e < nm * 16; e += blockDim.x) {
+    for (int e = tid; e < nmt * 16; e += blockDim.x) {
         const int blk = (e / 8) & 1;
-        const int m = pair ? (m0 + e / 16) * 64 + (e & 7) * 8 : (m0 + e / 16) * 128 + blk * 64 + (e & 7) * 8;
-        tab[e] = m < K ? ((m / Co - t_lo) << 16) | (pair ? x2_pos(m % Co, blk, x2_block(Co)) : m % Co) : -1;
+        int m, plane;
+        if (pair == 2) {  // m-tile 2u = hi plane, 2u + 1 = lo plane of unit u's 128 rows
+            m = (m0 + e / 32) * 128 + blk * 64 + (e & 7) * 8;
+            plane = (e / 16) & 1;
+        } else if (pair == 1) {
+            m = (m0 + e / 16) * 64 + (e & 7) * 8;
+            plane = blk;
+        } else {
+            m = (m0 + e / 16) * 128 + blk * 64 + (e & 7) * 8;
+            plane = 0;
+        }
+        tab[e] = m < K ? ((m / Co - t_lo) << 16) | (pair ? x2_pos(m % Co, plane, x2_block(Co)) : m % Co) : -1;
     }
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
@@ -837,7 +853,7 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
             const uint32_t nb = smem_u32(nbr_s + buf * NT * BM);
             for (int h = 0; h < 2; ++h) {
                 const uint32_t nbh = nb + h * 64 * 4;
-                for (int mi = 0; mi < nm; ++mi) {
+                for (int mi = 0; mi < nmt; ++mi) {
                     const int e = ld_shared_s32(tab_s + mi * 64);
                     int g[J];
                     if (e >= 0) {
@@ -906,6 +922,12 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
         constexpr uint32_t idesc = idesc_bf16_f32(BM, NB, true, true);
         constexpr uint32_t LBO = Cfg::KB * 128;  // next 64-wide MN block
         const uint64_t a0 = sw128_desc(sbase, LBO, 1024), b0 = sw128_desc(bbase, LBO, 1024);
+        // tri: the lo m-tile multiplies dY_hi only (N = c_out); with c_out >= 128 the dY tile's
+        // 64-wide blocks alternate hi / lo, so its hi blocks are two blocks apart
+        const uint32_t idesc_lo = pair == 2 ? idesc_bf16_f32(BM, pco, true, true) : idesc;
+        const uint32_t idesc_hi = pair == 2 ? idesc_bf16_f32(BM, 2 * pco, true, true) : idesc;  // [dY_hi | dY_lo]
+        const uint64_t b0_lo = sw128_desc(bbase, pco >= 128 ? 2 * LBO : LBO, 1024);
+        const int ucols = pair == 2 ? 3 * pco : NB;  // accumulator columns per m-tile (tri: per unit)
         int s = 0, bs = 0;
         uint32_t ph = 0, bph = 0;
         int cl = 0, ci = 0;  // tile index inside the chunk, chunk index
@@ -916,20 +938,23 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
                 mbar_wait(drained0 + 8 * ab, (uint32_t)((nacc == 2 ? prev >> 1 : prev) & 1));
                 tc_fence_after();
             }
-            const uint32_t acc0 = tmem + ab * nm * NB;
+            const uint32_t acc0 = tmem + ab * nm * ucols;
             for (int h = 0; h < 2; ++h) {
                 mbar_wait(bfull0 + 8 * bs, bph);
                 const uint64_t bo = (uint64_t)((bs * Cfg::B_BYTES) >> 4);
-                for (int mi = 0; mi < nm; ++mi) {
+                for (int mi = 0; mi < nmt; ++mi) {
                     mbar_wait(full0 + 8 * s, ph);
                     fence_proxy_async();
                     tc_fence_after();
                     if (elect_one()) {
                         const uint64_t ao = (uint64_t)((s * Cfg::A_BYTES) >> 4);
+                        const bool lo = pair == 2 && (mi & 1);
+                        const uint32_t d = pair == 2 ? acc0 + (mi >> 1) * ucols + (lo ? 2 * pco : 0) : acc0 + mi * NB;
+                        const uint64_t bd = (lo ? b0_lo : b0) + bo;
+                        const uint32_t id = lo ? idesc_lo : idesc_hi;
 #pragma unroll
                         for (int kk = 0; kk < Cfg::KB / 16; ++kk)  // 16 voxels = two 8-row atoms per MMA
-                            mma_bf16(acc0 + mi * NB, a0 + ao + 128 * kk, b0 + bo + 128 * kk, idesc,
-                                     (cl | h | kk) != 0);
+                            mma_bf16(d, a0 + ao + 128 * kk, bd + 128 * kk, id, (cl | h | kk) != 0);
                         mma_commit(empty0 + 8 * s);
                     }
                     __syncwarp();
@@ -960,10 +985,29 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
         for (int c = 0; c < nch; ++c) {
             const int ab = nacc == 2 ? (c & 1) : 0;
             mbar_wait_sleep(done0 + 8 * ab, (uint32_t)((nacc == 2 ? c >> 1 : c) & 1));
-            const uint32_t tqa = tq + ab * nm * NB;
+            const uint32_t tqa = tq + ab * nm * (pair == 2 ? 3 * pco : NB);
             tc_fence_after();
             const long long slot = chunk0 + c;
-            if (pair) {
+            if (pair == 2) {
+                // tri: lane = (t, ci) row of the unit; fixed order (hi.dY_hi + hi.dY_lo) + lo.dY_hi
+                const int g = x2_block(pco);
+                for (int u = 0; u < nm; ++u) {
+                    float* dst = partial + grp_tab.part_begin[grp] + ((slot * nm + u) * BM + row) * pco;
+                    const uint32_t tu = tqa + u * 3 * pco;
+                    for (int c0 = 0; c0 < pco; c0 += 16) {
+                        uint32_t a[16], b[16], l[16];
+                        tmem_ld16(tu + x2_pos(c0, 0, g), a);
+                        tmem_ld16(tu + x2_pos(c0, 1, g), b);
+                        tmem_ld16(tu + 2 * pco + c0, l);
+                        tmem_ld_wait();
+                        float f[16];
+#pragma unroll
+                        for (int e = 0; e < 16; ++e)
+                            f[e] = (__uint_as_float(a[e]) + __uint_as_float(b[e])) + __uint_as_float(l[e]);
+                        store_row(dst + c0, f);
+                    }
+                }
+            } else if (pair) {
                 // lanes 64..127 (lo plane rows) hand their column sums to lanes 0..63 through a
                 // 64 x 16 shared exchange; fixed order (hi.hi + hi.lo) + (lo.hi + lo.lo)
                 const int r = row & 63;
@@ -1383,26 +1427,36 @@ struct DwPlan {
 // max_tps > 0 caps a split's voxel tiles (the length of one TMEM accumulation chain).
 // pair: split precision — cin / cout are the channels of one plane, the GEMM runs on rows of
 // 2 cin (X) and 2 cout (dY) with 64 (t, ci) rows x both planes per m-tile (DwGroups).
+// mode (split precision): 1 = pair (four plane products per m-tile), 2 = tri (three products:
+// units of 128 (t, ci) rows, a hi m-tile against [dY_hi | dY_lo] and a lo m-tile against dY_hi).
+int x2_dw_mode() {
+    static const int v = env_int("HCB_X2_DW_TRI", 1) ? 2 : 1;
+    return v;
+}
+
 DwPlan dw_plan(long long rows, int taps, int cin, int cout, int max_tps = 0, bool pair = false) {
     DwPlan p{};
-    const int rpm = pair ? 64 : BM;
+    // tri needs c_out >= 32 to pay (C 16: 0.50 ms tri vs 0.43 pair; C 32: 0.62 vs 0.68; C 64: 1.46 vs 1.62)
+    const int mode = pair ? (cout >= 32 ? x2_dw_mode() : 1) : 0;
+    const int rpm = mode == 1 ? 64 : BM;
     p.nb = dw_nb(pair ? 2 * cout : cout);
-    p.mt = (taps * cin + rpm - 1) / rpm;
+    p.mt = (taps * cin + rpm - 1) / rpm;  // m-tiles (tri: units of a hi and a lo m-tile)
     p.cps = dw_cps(p.nb);
     p.tiles = (int)((rows + BM - 1) / BM);
     // pair mode with chunked accumulation: HCB_DW_DBUF=1 keeps two accumulator sets per CTA (the
     // epilogue drains one chunk while the next accumulates) at half the m-tiles per CTA
     static const int dbuf_env = env_int("HCB_DW_DBUF", 0);
     const int nacc = (pair && max_tps > 0 && dbuf_env) ? 2 : 1;
-    const int cap = 512 / (p.nb * p.cps * nacc);  // m-tiles whose accumulators fit one CTA's TMEM
+    const int unit_cols = mode == 2 ? 3 * cout : p.nb;  // tri: [hi.dY_hi | hi.dY_lo] + lo.dY_hi
+    const int cap = std::min(mode == 2 ? 8 : 16, 512 / (unit_cols * p.cps * nacc));  // m-tiles (units) per CTA
     const int G = (p.mt + cap - 1) / cap;  // -> every group has <= cap m-tiles
-    if (G > kMaxGroups)
-        throw std::invalid_argument("native conv: dW supports at most " + std::to_string(kMaxGroups * cap * BM) +
+    if (cap < 1 || G > kMaxGroups)
+        throw std::invalid_argument("native conv: dW supports at most " + std::to_string(kMaxGroups * std::max(cap, 0) * BM) +
                                     " (taps x input channels) rows at " + std::to_string(cout) + " output channels");
     const int slots = num_sms() * p.cps;
     DwGroups& g = p.g;
     g.groups = G;
-    g.pair = pair ? 1 : 0;
+    g.pair = mode;
     g.nacc = nacc;
     g.rpm = rpm;
     g.pcols = pair ? cout : p.nb;

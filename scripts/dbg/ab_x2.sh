@@ -1,3 +1,2 @@
-P="python scripts/dbg/x2_probe.py time 256 8 64 64"
-for v in nobload nobload_nogather nogather; do echo $v; HCB_LIB_PATH=paper_1803_11385_b200/_var/$v/libhcb200.so timeout 300 $P | cut -c1-200; done
-cd scripts/probes; ncu --metrics lts__throughput.avg.pct_of_peak_sustained_elapsed,lts__t_bytes.sum,gpu__time_duration.sum,lts__t_sectors_srcunit_tex.sum --clock-control none ./l1path 2>&1 | grep -E "k_ldg|lts|duration" | head -12
+timeout 900 python -m pytest -q -x tests/test_conv_f32.py tests/test_conv_tc.py tests/test_dropin_cpp.py -p no:cacheprovider 2>&1 | tail -3
+for c in "64 64" "16 16" "32 32" "128 128"; do HCB_X2_DW_TRI=1 timeout 300 python scripts/dbg/x2_probe.py time 256 8 $c | cut -c1-160; done
