@@ -554,3 +554,42 @@ def test_unpool_switch_check_is_stream_ordered(cuda):
     torch.cuda.synchronize()
     assert torch.equal(out, good)
     ops.check_deferred()
+
+
+def _tiled_to_rows(tiled, n, taps):
+    t = tiled.data.view(-1, taps, 128).permute(0, 2, 1).reshape(-1, taps)
+    return t[:n]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["random_dense", "random_sparse", "shell32x3", "edges"])
+def test_tiled_field_map_matches_rows(cuda, restated, case):
+    """The tile-major 3x3x3 map the fused conv consumes (k_field_map_tiled) equals the row-major
+    map (k_field_map) and the oracle's field_map (cnn_ops.cpp:100-119) entry for entry, on
+    dense random sets (x-runs across warp boundaries), sparse sets, a batched shell and a set
+    whose voxels all lie on the domain faces; the last tile's padding is -1."""
+    from paper_1803_11385_b200 import conv as nconv
+    if case == "random_dense":
+        f, _ = random_pair(16, 3, seed=31, n_lo=1500, n_hi=3000)  # long x-runs, warp-boundary runs
+    elif case == "random_sparse":
+        f, _ = random_pair(64, 4, seed=32, n_lo=200, n_hi=900)
+    elif case == "shell32x3":
+        f, _ = shell_pair(32, 3)
+    else:  # every voxel on the domain faces: the x-1 / x+1 columns leave the grid
+        from paper_1803_11385_b200.psh import PshLevel, VoxelSet, mix_seed
+        res = 8
+        g = np.stack(np.meshgrid(np.arange(res), np.arange(res), np.arange(res), indexing="ij"), -1).reshape(-1, 3)
+        g = g[(g == 0).any(1) | (g == res - 1).any(1)].astype(np.int32)
+        s0 = VoxelSet.make(3, res, g, np.zeros((1, len(g)), np.float32))
+        f = [PshLevel.build(s0, mix_seed(5, 1)), PshLevel.build(s0, mix_seed(5, 2))]
+    s = SuperPsh.from_levels(f)
+    n = s.total_columns()
+    spec = ConvSpec(3, 1, 0, 1, 1)
+    tm = nconv.field_map_native(s, s, spec, nconv.TILED)
+    rows = _tiled_to_rows(tm, n, 27)
+    rm = ops.field_map(s, s, spec)
+    assert torch.equal(rows, rm)
+    pad = tm.data.view(-1, 27, 128)[-1, :, (n % 128 or 128):]
+    assert bool((pad == -1).all())
+    fa = levels_to_arrays(f)
+    assert np.array_equal(_np(rows).astype(np.int64), restated.field_map(fa, fa, spec))
