@@ -403,8 +403,11 @@ __global__ void k_col2hash_any(DevPsh in, DevPsh out, int F, int S, int pad, int
 // compare, so each thread keeps CB*F^3 independent gathers in flight (a per-channel loop
 // is one dependent latency chain per channel). Per channel the taps are still visited in
 // row order with the same seed/tie rule -> bit-identical results.
+#ifndef HCB_POOL_MINB
+#define HCB_POOL_MINB 1
+#endif
 template <int F, int CB>
-__global__ void __launch_bounds__(256) k_max_pool(DevPsh in, DevPsh out, int S, int pad,
+__global__ void __launch_bounds__(256, HCB_POOL_MINB) k_max_pool(DevPsh in, DevPsh out, int S, int pad,
                                                   const float* __restrict__ data, int C, float* __restrict__ res,
                                                   int* __restrict__ sw) {
     constexpr int T = F * F * F;
@@ -484,7 +487,7 @@ __global__ void k_max_pool_any(DevPsh in, DevPsh out, int F, int S, int pad, int
 // cnn_ops.cpp:286-322 avg_pool: (sum over present taps, row order) * inv_fd; CB channels
 // per pass with independent loads (see k_max_pool).
 template <int F, int CB>
-__global__ void __launch_bounds__(256) k_avg_pool(DevPsh in, DevPsh out, int S, int pad,
+__global__ void __launch_bounds__(256, HCB_POOL_MINB) k_avg_pool(DevPsh in, DevPsh out, int S, int pad,
                                                   const float* __restrict__ data, int C, float inv,
                                                   float* __restrict__ res) {
     constexpr int T = F * F * F;
@@ -552,7 +555,7 @@ __global__ void k_avg_pool_any(DevPsh in, DevPsh out, int F, int S, int pad, int
 // CB channels per pass: the switch and value loads of all CB channels are issued before
 // any compare (the per-channel form serialised a switch load -> value load chain per channel).
 template <int KMAX, bool AVG, int CB>
-__global__ void __launch_bounds__(256) k_unpool(DevPsh fine, DevPsh coarse, int F, int S, int pad,
+__global__ void __launch_bounds__(256, HCB_POOL_MINB) k_unpool(DevPsh fine, DevPsh coarse, int F, int S, int pad,
                                                 const float* __restrict__ cd, const int* __restrict__ sw, int C,
                                                 float inv, float* __restrict__ res) {
     const long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x;
