@@ -886,7 +886,7 @@ def net_main(args, rank, world, local):
     feats = np.concatenate([pyr[0].arrays()[3]] * b, axis=1)
     # every rank starts from the same weights (data parallelism)
     net = nnet.NativeHashNet(lmax, args.classes, seed=0,
-                             sync_bn=sum_over_ranks if (args.sync_bn and world > 1) else None)
+                             sync_bn=sum_over_ranks if (args.sync_bn and world > 1) else None, precision=args.dtype)
     x = net.input_features(torch.from_numpy(np.ascontiguousarray(feats)).to(dev))
     labels = torch.randint(0, args.classes, (b,), device=dev)
     voxels = sum(s.total_columns() for s in levels)
@@ -947,7 +947,10 @@ def net_main(args, rank, world, local):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": vs,
             "vs_baseline_source": "paper GPU net iteration, batch 32 (BASELINE.md §1, PAPER.md:485)" if vs else None,
-            "dtype": "bf16",
+            "dtype": args.dtype,
+            "precision_note": "f32: fp32 activations, conv fwd/dW/dX via bf16 hi/lo split on tcgen05 (within 1e-5 "
+                              "of the fp32 reference net step, tests/test_net_gpu.py)" if args.dtype == "f32" else
+                              "bf16 conv operands and activations, fp32 accumulation",
             "data": "synthetic (sphere shell pyramid, bench.cpp:33-77; random labels)",
             "config": {"workload": f"hcnn classification net {args.res}^3, {lmax - 1} conv/pool levels, "
                                    f"{b} shells/GPU", "res": args.res, "global_batch": b * world,

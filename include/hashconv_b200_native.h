@@ -118,6 +118,19 @@ hc_status hc_native_bn_relu_backward(const void* d_relu, hc_dtype dtype, const f
 hc_status hc_native_bn_relu_inference(const float* x, int64_t n, int32_t c, const float* running_mean,
                                       const float* running_var, float eps, void* out_bf16,
                                       hc_stream stream);
+/* The same three with the output dtype explicit (HC_DTYPE_BF16 or HC_DTYPE_F32): the
+ * split-precision (fp32) native net keeps fp32 activations and conv-output gradients. */
+hc_status hc_native_bn_relu_forward_dt(const float* x, int64_t n, int32_t c, int32_t training,
+                                       float momentum, float eps, float* running_mean, float* running_var,
+                                       float* inv_std, float* xhat, void* out, hc_dtype out_dtype,
+                                       void* workspace, size_t ws_bytes, hc_stream stream);
+hc_status hc_native_bn_relu_backward_dt(const void* d_relu, hc_dtype dtype, const float* xhat,
+                                        const float* inv_std, int64_t n, int32_t c, void* d_conv,
+                                        hc_dtype out_dtype, void* workspace, size_t ws_bytes,
+                                        hc_stream stream);
+hc_status hc_native_bn_relu_inference_dt(const float* x, int64_t n, int32_t c, const float* running_mean,
+                                         const float* running_var, float eps, void* out, hc_dtype out_dtype,
+                                         hc_stream stream);
 /* Synchronised batch norm for data parallelism (the reference normalises over
  * the whole batch, cnn_ops.cpp:456-470), in phases so the caller can sum the per-channel
  * statistics over ranks (e.g. ncclAllReduce, double) between them:
@@ -139,10 +152,19 @@ hc_status hc_native_bn_relu_backward_apply(const void* d_relu, hc_dtype dtype, c
                                            const float* inv_std, int64_t n, int32_t c, const double* s1,
                                            const double* s2, int64_t n_total, void* d_conv_bf16,
                                            hc_stream stream);
+hc_status hc_native_bn_relu_apply_dt(const float* x, int64_t n, int32_t c, const double* mean,
+                                     const float* inv_std, float* xhat, void* out, hc_dtype out_dtype,
+                                     hc_stream stream);
+hc_status hc_native_bn_relu_backward_apply_dt(const void* d_relu, hc_dtype dtype, const float* xhat,
+                                              const float* inv_std, int64_t n, int32_t c, const double* s1,
+                                              const double* s2, int64_t n_total, void* d_conv,
+                                              hc_dtype out_dtype, hc_stream stream);
 /* Final dense pool: cmap [b][8 cells][8 children] resolution-4 columns (or -1); head
  * [(c*8 + cell)][b] fp32 = max over present children, src = winning column or -1. */
 hc_status hc_native_dense_pool(const int32_t* cmap, int32_t b, const void* x_bf16, int32_t c,
                                float* head, int32_t* src, hc_stream stream);
+hc_status hc_native_dense_pool_dt(const int32_t* cmap, int32_t b, const void* x, hc_dtype dtype, int32_t c,
+                                  float* head, int32_t* src, hc_stream stream);
 hc_status hc_native_dense_pool_backward(const float* d_head, const int32_t* src, int32_t b, int32_t c,
                                         int64_t n_fine, float* dx, hc_stream stream);
 /* SGD with momentum and weight decay (net.cpp:339-346): v = momentum*v + lr*(g + wd*w); w -= v. */

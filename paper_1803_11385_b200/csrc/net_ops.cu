@@ -303,10 +303,11 @@ __global__ void k_bn_finalize(const double* __restrict__ sum_x, const double* __
 
 // xhat = (x - mean) * inv_std (float, cnn_ops.cpp:472); out = relu(xhat) (bf16 for the
 // next layer); xhat kept (fp32) for the backward pass.
+template <typename OT>
 __global__ void __launch_bounds__(kT) k_bn_relu_apply(const float* __restrict__ x, long long n, int C,
                                                      const double* __restrict__ mean,
                                                      const float* __restrict__ inv_std, float* __restrict__ xhat,
-                                                     bf16* __restrict__ out) {
+                                                     OT* __restrict__ out) {
     const int chunks = C >> 3;
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= n * chunks) return;
@@ -326,9 +327,10 @@ __global__ void __launch_bounds__(kT) k_bn_relu_apply(const float* __restrict__ 
 // Inference batch norm + ReLU (cnn_ops.cpp:470-475 with training = false): the running
 // statistics stand in for the batch's, inv_std = T(1 / sqrt(double(var) + eps)),
 // y = (x - T(mean)) * inv_std, out = max(0, y) (bf16 for the next layer).
+template <typename OT>
 __global__ void __launch_bounds__(kT) k_bn_relu_infer(const float* __restrict__ x, long long n, int C,
                                                      const float* __restrict__ rmean, const float* __restrict__ rvar,
-                                                     float eps, bf16* __restrict__ out) {
+                                                     float eps, OT* __restrict__ out) {
     const int chunks = C >> 3;
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= n * chunks) return;
@@ -346,11 +348,11 @@ __global__ void __launch_bounds__(kT) k_bn_relu_infer(const float* __restrict__ 
 
 // dx = inv_std * (dyb - s1/n - xhat * s2/n), dyb = dy * (xhat > 0)  (cnn_ops.cpp:476-489
 // after relu_backward cnn_ops.cpp:553-561); bf16 out = the conv layer's output gradient.
-template <typename DT>
+template <typename DT, typename OT>
 __global__ void __launch_bounds__(kT) k_bn_relu_bwd_apply(const DT* __restrict__ dy, const float* __restrict__ xhat,
                                                          long long n, int C, const double* __restrict__ s1,
                                                          const double* __restrict__ s2,
-                                                         const float* __restrict__ inv_std, bf16* __restrict__ dx,
+                                                         const float* __restrict__ inv_std, OT* __restrict__ dx,
                                                          long long n_total) {
     const int chunks = C >> 3;
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -373,7 +375,11 @@ __global__ void __launch_bounds__(kT) k_bn_relu_bwd_apply(const DT* __restrict__
 // net.cpp:69-106: per model v and dense parent cell q of the 2^3 grid, max over the present
 // resolution-4 children (first hit seeds, strict '>'); head_in[(c*8 + cell)][v], src = the
 // winning fine column (-1 when the cell's field is empty). cmap: [b][8][8] child columns.
-__global__ void k_dense_pool(const int* __restrict__ cmap, int b, const bf16* __restrict__ x, int C,
+__device__ __forceinline__ float to_f(bf16 v) { return __bfloat162float(v); }
+__device__ __forceinline__ float to_f(float v) { return v; }
+
+template <typename T>
+__global__ void k_dense_pool(const int* __restrict__ cmap, int b, const T* __restrict__ x, int C,
                              float* __restrict__ head, int* __restrict__ src) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;  // over b * 8 * C
     if (i >= b * 8 * C) return;
@@ -384,7 +390,7 @@ __global__ void k_dense_pool(const int* __restrict__ cmap, int b, const bf16* __
     for (int k = 0; k < 8; ++k) {
         const int g = kids[k];
         if (g < 0) continue;
-        const float val = __bfloat162float(x[(long long)g * C + c]);
+        const float val = to_f(x[(long long)g * C + c]);
         if (col < 0 || val > best) {
             best = val;
             col = g;
@@ -419,6 +425,33 @@ __global__ void k_sgd(float* __restrict__ w, float* __restrict__ v, const float*
 
 void check_c8(int c) {
     if (c <= 0 || c % 8 != 0) throw std::invalid_argument("native net ops: channels must be a multiple of 8");
+}
+
+void check_out_dtype(hc_dtype t) {
+    if (t != HC_DTYPE_BF16 && t != HC_DTYPE_F32) throw std::invalid_argument("native net op: output dtype must be bf16 or f32");
+}
+
+// out = relu(xhat) as bf16 or fp32 (the split-precision net keeps fp32 activations)
+void bn_relu_apply_out(const float* x, long long n, int c, const double* mean, const float* inv_std, float* xhat,
+                              void* out, hc_dtype out_dtype, cudaStream_t s) {
+    const long long m = n * (c / 8);
+    if (out_dtype == HC_DTYPE_F32)
+        k_bn_relu_apply<float><<<grid_for(m, kT), kT, 0, s>>>(x, n, c, mean, inv_std, xhat, static_cast<float*>(out));
+    else
+        k_bn_relu_apply<bf16><<<grid_for(m, kT), kT, 0, s>>>(x, n, c, mean, inv_std, xhat, static_cast<bf16*>(out));
+    launched("batch-norm + relu");
+}
+
+template <typename DT>
+void bn_bwd_apply_out(const DT* d, const float* xhat, long long n, int c, const double* s1, const double* s2,
+                             const float* inv_std, void* out, hc_dtype out_dtype, long long n_total, cudaStream_t s) {
+    const long long m = n * (c / 8);
+    if (out_dtype == HC_DTYPE_F32)
+        k_bn_relu_bwd_apply<DT, float><<<grid_for(m, kT), kT, 0, s>>>(d, xhat, n, c, s1, s2, inv_std,
+                                                                      static_cast<float*>(out), n_total);
+    else
+        k_bn_relu_bwd_apply<DT, bf16><<<grid_for(m, kT), kT, 0, s>>>(d, xhat, n, c, s1, s2, inv_std,
+                                                                     static_cast<bf16*>(out), n_total);
 }
 
 }  // namespace
@@ -504,7 +537,16 @@ size_t hc_native_bn_workspace(int64_t n, int32_t c) {
 hc_status hc_native_bn_relu_forward(const float* x, int64_t n, int32_t c, int32_t training, float momentum, float eps,
                                     float* running_mean, float* running_var, float* inv_std, float* xhat,
                                     void* out_bf16, void* workspace, size_t ws_bytes, hc_stream stream) {
+    return hc_native_bn_relu_forward_dt(x, n, c, training, momentum, eps, running_mean, running_var, inv_std, xhat,
+                                        out_bf16, HC_DTYPE_BF16, workspace, ws_bytes, stream);
+}
+
+hc_status hc_native_bn_relu_forward_dt(const float* x, int64_t n, int32_t c, int32_t training, float momentum,
+                                       float eps, float* running_mean, float* running_var, float* inv_std, float* xhat,
+                                       void* out, hc_dtype out_dtype, void* workspace, size_t ws_bytes,
+                                       hc_stream stream) {
     return guard([&] {
+        check_out_dtype(out_dtype);
         check_c8(c);
         if (c > kT) throw std::invalid_argument("native batch norm: at most 256 channels");
         if (n <= 0) throw std::invalid_argument("batch_norm: empty input");
@@ -525,16 +567,22 @@ hc_status hc_native_bn_relu_forward(const float* x, int64_t n, int32_t c, int32_
         } else {
             throw std::invalid_argument("native batch norm: inference mode uses the reference-layout path");
         }
-        const long long m = n * (c / 8);
-        k_bn_relu_apply<<<grid_for(m, kT), kT, 0, s>>>(x, n, c, mean, inv_std, xhat, static_cast<bf16*>(out_bf16));
-        launched("batch-norm + relu");
+        bn_relu_apply_out(x, n, c, mean, inv_std, xhat, out, out_dtype, s);
     });
 }
 
 hc_status hc_native_bn_relu_backward(const void* d_relu, hc_dtype dtype, const float* xhat, const float* inv_std,
                                      int64_t n, int32_t c, void* d_conv_bf16, void* workspace, size_t ws_bytes,
                                      hc_stream stream) {
+    return hc_native_bn_relu_backward_dt(d_relu, dtype, xhat, inv_std, n, c, d_conv_bf16, HC_DTYPE_BF16, workspace,
+                                         ws_bytes, stream);
+}
+
+hc_status hc_native_bn_relu_backward_dt(const void* d_relu, hc_dtype dtype, const float* xhat, const float* inv_std,
+                                        int64_t n, int32_t c, void* d_conv, hc_dtype out_dtype, void* workspace,
+                                        size_t ws_bytes, hc_stream stream) {
     return guard([&] {
+        check_out_dtype(out_dtype);
         check_c8(c);
         if (c > kT) throw std::invalid_argument("native batch norm: at most 256 channels");
         if (n <= 0) return;
@@ -545,19 +593,16 @@ hc_status hc_native_bn_relu_backward(const void* d_relu, hc_dtype dtype, const f
         double* part = static_cast<double*>(workspace);
         double* s1 = part + (long long)blocks * 2 * c;
         double* s2 = s1 + c;
-        const long long m = n * (c / 8);
         if (dtype == HC_DTYPE_BF16) {
             const bf16* d = static_cast<const bf16*>(d_relu);
             k_col_partials<2, bf16><<<blocks, kT, 0, s>>>(xhat, d, n, c, nullptr, part, rpb);
             k_col_fold<2><<<c, kT, 0, s>>>(part, blocks, n, c, s1, s2, nullptr, nullptr, 0, 0, nullptr, nullptr);
-            k_bn_relu_bwd_apply<bf16><<<grid_for(m, kT), kT, 0, s>>>(d, xhat, n, c, s1, s2, inv_std,
-                                                                     static_cast<bf16*>(d_conv_bf16), n);
+            bn_bwd_apply_out(d, xhat, n, c, s1, s2, inv_std, d_conv, out_dtype, n, s);
         } else {
             const float* d = static_cast<const float*>(d_relu);
             k_col_partials<2, float><<<blocks, kT, 0, s>>>(xhat, d, n, c, nullptr, part, rpb);
             k_col_fold<2><<<c, kT, 0, s>>>(part, blocks, n, c, s1, s2, nullptr, nullptr, 0, 0, nullptr, nullptr);
-            k_bn_relu_bwd_apply<float><<<grid_for(m, kT), kT, 0, s>>>(d, xhat, n, c, s1, s2, inv_std,
-                                                                      static_cast<bf16*>(d_conv_bf16), n);
+            bn_bwd_apply_out(d, xhat, n, c, s1, s2, inv_std, d_conv, out_dtype, n, s);
         }
         launched("batch-norm + relu backward", 3);
     });
@@ -565,12 +610,24 @@ hc_status hc_native_bn_relu_backward(const void* d_relu, hc_dtype dtype, const f
 
 hc_status hc_native_bn_relu_inference(const float* x, int64_t n, int32_t c, const float* running_mean,
                                       const float* running_var, float eps, void* out_bf16, hc_stream stream) {
+    return hc_native_bn_relu_inference_dt(x, n, c, running_mean, running_var, eps, out_bf16, HC_DTYPE_BF16, stream);
+}
+
+hc_status hc_native_bn_relu_inference_dt(const float* x, int64_t n, int32_t c, const float* running_mean,
+                                         const float* running_var, float eps, void* out, hc_dtype out_dtype,
+                                         hc_stream stream) {
     return guard([&] {
         check_c8(c);
+        check_out_dtype(out_dtype);
         if (n <= 0) return;
         const long long m = n * (c / 8);
-        k_bn_relu_infer<<<grid_for(m, kT), kT, 0, as_stream(stream)>>>(x, n, c, running_mean, running_var, eps,
-                                                                       static_cast<bf16*>(out_bf16));
+        cudaStream_t s = as_stream(stream);
+        if (out_dtype == HC_DTYPE_F32)
+            k_bn_relu_infer<float><<<grid_for(m, kT), kT, 0, s>>>(x, n, c, running_mean, running_var, eps,
+                                                                  static_cast<float*>(out));
+        else
+            k_bn_relu_infer<bf16><<<grid_for(m, kT), kT, 0, s>>>(x, n, c, running_mean, running_var, eps,
+                                                                 static_cast<bf16*>(out));
         launched("batch-norm (inference) + relu");
     });
 }
@@ -616,44 +673,61 @@ hc_status hc_native_bn_finalize(const double* sum_x, const double* sum_sq, int64
 
 hc_status hc_native_bn_relu_apply(const float* x, int64_t n, int32_t c, const double* mean, const float* inv_std,
                                   float* xhat, void* out_bf16, hc_stream stream) {
+    return hc_native_bn_relu_apply_dt(x, n, c, mean, inv_std, xhat, out_bf16, HC_DTYPE_BF16, stream);
+}
+
+hc_status hc_native_bn_relu_apply_dt(const float* x, int64_t n, int32_t c, const double* mean, const float* inv_std,
+                                     float* xhat, void* out, hc_dtype out_dtype, hc_stream stream) {
     return guard([&] {
         check_c8(c);
+        check_out_dtype(out_dtype);
         if (n <= 0) return;
-        const long long m = n * (c / 8);
-        k_bn_relu_apply<<<grid_for(m, kT), kT, 0, as_stream(stream)>>>(x, n, c, mean, inv_std, xhat,
-                                                                       static_cast<bf16*>(out_bf16));
-        launched("batch-norm + relu");
+        bn_relu_apply_out(x, n, c, mean, inv_std, xhat, out, out_dtype, as_stream(stream));
     });
 }
 
 hc_status hc_native_bn_relu_backward_apply(const void* d_relu, hc_dtype dtype, const float* xhat, const float* inv_std,
                                            int64_t n, int32_t c, const double* s1, const double* s2, int64_t n_total,
                                            void* d_conv_bf16, hc_stream stream) {
+    return hc_native_bn_relu_backward_apply_dt(d_relu, dtype, xhat, inv_std, n, c, s1, s2, n_total, d_conv_bf16,
+                                               HC_DTYPE_BF16, stream);
+}
+
+hc_status hc_native_bn_relu_backward_apply_dt(const void* d_relu, hc_dtype dtype, const float* xhat,
+                                              const float* inv_std, int64_t n, int32_t c, const double* s1,
+                                              const double* s2, int64_t n_total, void* d_conv, hc_dtype out_dtype,
+                                              hc_stream stream) {
     return guard([&] {
         check_c8(c);
+        check_out_dtype(out_dtype);
         if (n <= 0) return;
         if (n_total <= 0) throw std::invalid_argument("batch_norm: empty input");
         cudaStream_t s = as_stream(stream);
-        const long long m = n * (c / 8);
         if (dtype == HC_DTYPE_BF16)
-            k_bn_relu_bwd_apply<bf16><<<grid_for(m, kT), kT, 0, s>>>(static_cast<const bf16*>(d_relu), xhat, n, c, s1,
-                                                                     s2, inv_std, static_cast<bf16*>(d_conv_bf16),
-                                                                     n_total);
+            bn_bwd_apply_out(static_cast<const bf16*>(d_relu), xhat, n, c, s1, s2, inv_std, d_conv, out_dtype, n_total, s);
         else
-            k_bn_relu_bwd_apply<float><<<grid_for(m, kT), kT, 0, s>>>(static_cast<const float*>(d_relu), xhat, n, c,
-                                                                      s1, s2, inv_std, static_cast<bf16*>(d_conv_bf16),
-                                                                      n_total);
+            bn_bwd_apply_out(static_cast<const float*>(d_relu), xhat, n, c, s1, s2, inv_std, d_conv, out_dtype, n_total,
+                             s);
         launched("batch-norm + relu backward");
     });
 }
 
 hc_status hc_native_dense_pool(const int32_t* cmap, int32_t b, const void* x_bf16, int32_t c, float* head,
                                int32_t* src, hc_stream stream) {
+    return hc_native_dense_pool_dt(cmap, b, x_bf16, HC_DTYPE_BF16, c, head, src, stream);
+}
+
+hc_status hc_native_dense_pool_dt(const int32_t* cmap, int32_t b, const void* x, hc_dtype dtype, int32_t c,
+                                  float* head, int32_t* src, hc_stream stream) {
     return guard([&] {
+        check_out_dtype(dtype);
         if (b <= 0 || c <= 0) return;
         const int n = b * 8 * c;
-        k_dense_pool<<<grid_for(n, kT), kT, 0, as_stream(stream)>>>(cmap, b, static_cast<const bf16*>(x_bf16), c, head,
-                                                                    src);
+        cudaStream_t s = as_stream(stream);
+        if (dtype == HC_DTYPE_F32)
+            k_dense_pool<float><<<grid_for(n, kT), kT, 0, s>>>(cmap, b, static_cast<const float*>(x), c, head, src);
+        else
+            k_dense_pool<bf16><<<grid_for(n, kT), kT, 0, s>>>(cmap, b, static_cast<const bf16*>(x), c, head, src);
         launched("dense pool");
     });
 }

@@ -119,11 +119,19 @@ class NativeHashNet:
 
     def __init__(self, level_max: int, num_classes: int, seed: int = 0, input_channels: int = 3,
                  dropout: float = 0.5, lr: float = 0.1, momentum: float = 0.9, weight_decay: float = 5e-4,
-                 bn_momentum: float = 0.1, bn_eps: float = 1e-5, sync_bn=None):
+                 bn_momentum: float = 0.1, bn_eps: float = 1e-5, sync_bn=None, precision: str = "bf16"):
         """sync_bn: data parallelism with whole-batch statistics — a callable
         that sums a float64 CUDA tensor in place over the ranks (e.g. dist.sum_over_ranks);
         batch norm then normalises over the global batch, as the reference does for one
-        process (cnn_ops.cpp:456-470). None: statistics over this process's batch."""
+        process (cnn_ops.cpp:456-470). None: statistics over this process's batch.
+        precision: "bf16" — bf16 conv operands and activations (fp32 accumulation); "f32" — the
+        reference's precision: fp32 activations and gradients, every conv (forward, dW, dX)
+        through the split-precision tcgen05 kernels (bf16 hi/lo planes, within 1e-5 of fp64)."""
+        if precision not in ("bf16", "f32"):
+            raise ValueError("precision must be 'bf16' or 'f32'")
+        self.f32 = precision == "f32"
+        self.adt = torch.float32 if self.f32 else BF16  # activation / conv-gradient dtype
+        self.adt_code = _lib.HC_DTYPE_F32 if self.f32 else _lib.HC_DTYPE_BF16
         if level_max < 2 or level_max > 16:
             raise ValueError("level_max out of range")
         if num_classes < 2:
@@ -194,9 +202,9 @@ class NativeHashNet:
         n, c = y.shape
         ws = self._bn_ws(n, c)
         if self.sync_bn is None:
-            check(lib.hc_native_bn_relu_forward(_p(y), n, c, 1, self.bn_momentum, self.bn_eps, _p(blk["run_mean"]),
-                                                _p(blk["run_var"]), _p(blk["inv_std"]), _p(xhat), _p(r), _p(ws),
-                                                ws.numel(), _s()))
+            check(lib.hc_native_bn_relu_forward_dt(_p(y), n, c, 1, self.bn_momentum, self.bn_eps,
+                                                   _p(blk["run_mean"]), _p(blk["run_var"]), _p(blk["inv_std"]),
+                                                   _p(xhat), _p(r), self.adt_code, _p(ws), ws.numel(), _s()))
             return
         # the sums are divided by the global count on the device (the same IEEE double ops
         # hc_native_bn_finalize applies), then finalised with n_total = 1
@@ -212,7 +220,8 @@ class NativeHashNet:
         sq0 = (sq[0] / nt).contiguous()
         check(lib.hc_native_bn_finalize(_p(sx), _p(sq0), 1, c, self.bn_momentum, self.bn_eps, _p(blk["run_mean"]),
                                         _p(blk["run_var"]), _p(mean), _p(blk["inv_std"]), _s()))
-        check(lib.hc_native_bn_relu_apply(_p(y), n, c, _p(mean), _p(blk["inv_std"]), _p(xhat), _p(r), _s()))
+        check(lib.hc_native_bn_relu_apply_dt(_p(y), n, c, _p(mean), _p(blk["inv_std"]), _p(xhat), _p(r), self.adt_code,
+                                             _s()))
 
     def _bn_relu_backward(self, i: int, d_relu: torch.Tensor, d_dtype: int, xhat: torch.Tensor,
                           d_conv: torch.Tensor) -> None:
@@ -220,22 +229,33 @@ class NativeHashNet:
         n, c = xhat.shape
         ws = self._bn_ws(n, c)
         if self.sync_bn is None:
-            check(lib.hc_native_bn_relu_backward(_p(d_relu), d_dtype, _p(xhat), _p(blk["inv_std"]), n, c,
-                                                 _p(d_conv), _p(ws), ws.numel(), _s()))
+            check(lib.hc_native_bn_relu_backward_dt(_p(d_relu), d_dtype, _p(xhat), _p(blk["inv_std"]), n, c,
+                                                    _p(d_conv), self.adt_code, _p(ws), ws.numel(), _s()))
             return
         stb = torch.empty(2 * c + 1, dtype=torch.float64, device="cuda")
         check(lib.hc_native_bn_stat(2, _p(xhat), _p(d_relu), d_dtype, n, c, None, _p(stb), _p(ws), ws.numel(), _s()))
         nt = self._sync_sums(stb, n, c)
         st = (stb[:2 * c].view(2, c) * (1.0 / nt)).contiguous()  # s * inv_n, as the kernel forms it
-        check(lib.hc_native_bn_relu_backward_apply(_p(d_relu), d_dtype, _p(xhat), _p(blk["inv_std"]), n, c,
-                                                   _p(st[0]), _p(st[1]), 1, _p(d_conv), _s()))
+        check(lib.hc_native_bn_relu_backward_apply_dt(_p(d_relu), d_dtype, _p(xhat), _p(blk["inv_std"]), n, c,
+                                                      _p(st[0]), _p(st[1]), 1, _p(d_conv), self.adt_code, _s()))
 
     def input_features(self, ref: torch.Tensor) -> torch.Tensor:
-        """Finest-level data (C x N fp32, psh data array) -> padded voxel-major bf16."""
+        """Finest-level data (C x N fp32, psh data array) -> padded voxel-major (bf16, or fp32 at
+        precision f32)."""
         c, n = ref.shape
-        x = torch.zeros((n, self.blocks[0]["cin_p"]), dtype=BF16, device="cuda")
-        x[:, :c] = nconv.to_voxel_major(ref)
+        x = torch.zeros((n, self.blocks[0]["cin_p"]), dtype=self.adt, device="cuda")
+        x[:, :c] = nconv.to_voxel_major(ref) if not self.f32 else ref.t()
         return x
+
+    def _conv_forward(self, i: int, x: torch.Tensor):
+        """Block i's conv: returns (fp32 output, what the backward needs of the input)."""
+        blk = self.blocks[i]
+        if self.f32:
+            xs = nconv.split(x)
+            wf = nconv.pack_weights_x2(blk["w"], blk["cout_p"], blk["cin_p"], 27, nconv.PACK_FORWARD)
+            return nconv.gather_gemm_x2(self._maps[i], xs, wf, blk["cout_p"]), xs
+        wf = nconv.pack_weights(blk["w"], blk["cout_p"], blk["cin_p"], 27, False)
+        return nconv.gather_gemm(self._maps[i], x, wf, blk["cout_p"], torch.float32), x
 
     # ------------------------------------------------------------------ forward / backward
     def forward(self, nb: NetBatch, x: torch.Tensor, training: bool = True, cache: Optional[dict] = None):
@@ -243,28 +263,28 @@ class NativeHashNet:
         statistics (running stats updated) and dropout; training=False: the running statistics
         normalise and dropout is the identity (net.cpp:203-208, 232-241)."""
         acts = []
+        self._maps = nb.conv_maps
         for i, blk in enumerate(self.blocks):
             s = nb.levels[i]
             n = s.total_columns()
-            wf = nconv.pack_weights(blk["w"], blk["cout_p"], blk["cin_p"], 27, False)
-            y = nconv.gather_gemm(nb.conv_maps[i], x, wf, blk["cout_p"], torch.float32)
-            r = torch.empty((n, blk["cout_p"]), dtype=BF16, device="cuda")
+            y, x_saved = self._conv_forward(i, x)
+            r = torch.empty((n, blk["cout_p"]), dtype=self.adt, device="cuda")
             if training:
                 xhat = torch.empty_like(y)
                 self._bn_relu_forward(i, y, xhat, r)
             else:
                 xhat = None
-                check(lib.hc_native_bn_relu_inference(_p(y), n, blk["cout_p"], _p(blk["run_mean"]), _p(blk["run_var"]),
-                                                      self.bn_eps, _p(r), _s()))
-            acts.append(dict(x=x, xhat=xhat))
+                check(lib.hc_native_bn_relu_inference_dt(_p(y), n, blk["cout_p"], _p(blk["run_mean"]),
+                                                         _p(blk["run_var"]), self.bn_eps, _p(r), self.adt_code, _s()))
+            acts.append(dict(x=x_saved, xhat=xhat))
             if cache is not None and cache.get("trace") is not None:
                 cache["trace"].setdefault("blocks", []).append(dict(x=x, y=y.clone(), r=r))
             if i + 1 < len(self.blocks):
                 pm = nb.pool_maps[i]
                 nc = pm.shape[0]
-                pooled = torch.empty((nc, blk["cout_p"]), dtype=BF16, device="cuda")
+                pooled = torch.empty((nc, blk["cout_p"]), dtype=self.adt, device="cuda")
                 sw = torch.empty((nc, blk["cout_p"]), dtype=torch.int8, device="cuda")
-                check(lib.hc_native_max_pool(_p(pm), nc, 8, _p(r), _lib.HC_DTYPE_BF16, blk["cout_p"], _p(pooled),
+                check(lib.hc_native_max_pool(_p(pm), nc, 8, _p(r), self.adt_code, blk["cout_p"], _p(pooled),
                                              _p(sw), _s()))
                 acts[-1]["sw"] = sw
                 if cache is not None and cache.get("trace") is not None:
@@ -275,7 +295,8 @@ class NativeHashNet:
                 c = blk["cout_p"]
                 head = torch.empty((c * 8, b), device="cuda")
                 src = torch.empty((c * 8, b), dtype=torch.int32, device="cuda")
-                check(lib.hc_native_dense_pool(_p(nb.dense_children), b, _p(r), c, _p(head), _p(src), _s()))
+                check(lib.hc_native_dense_pool_dt(_p(nb.dense_children), b, _p(r), self.adt_code, c, _p(head), _p(src),
+                                                  _s()))
                 acts[-1]["src"] = src
                 x = head
         # head: dropout -> FC(128) -> dropout -> FC(classes)   (net.cpp:236-251)
@@ -338,9 +359,13 @@ class NativeHashNet:
                 d_relu = torch.empty((n, c), device="cuda")
                 check(lib.hc_native_dense_pool_backward(_p(d_head), _p(a["src"]), nb.batch, c, n, _p(d_relu), _s()))
                 d_dtype = _lib.HC_DTYPE_F32
-            d_conv = torch.empty((n, c), dtype=BF16, device="cuda")
+            d_conv = torch.empty((n, c), dtype=self.adt, device="cuda")
             self._bn_relu_backward(i, d_relu, d_dtype, a["xhat"], d_conv)
-            conv_grads[i] = nconv.conv_dw(nb.conv_maps[i], a["x"], d_conv, self._dw_ws)
+            if self.f32:  # a["x"] holds the split input rows
+                d_conv_s = nconv.split(d_conv)
+                conv_grads[i] = nconv.conv_dw_x2(nb.conv_maps[i], a["x"], d_conv_s, self._dw_ws)
+            else:
+                conv_grads[i] = nconv.conv_dw(nb.conv_maps[i], a["x"], d_conv, self._dw_ws)
             if trace is not None:
                 trace["blocks"][i].update(d_relu=d_relu, d_conv=d_conv, dw=conv_grads[i].clone())
             # input gradient (net.cpp:316-317; the finest one is the net's input gradient, g.input).
@@ -351,18 +376,22 @@ class NativeHashNet:
             if cin_g != blk["cin_p"]:
                 w = torch.zeros((blk["cout_p"], cin_g * 27), device="cuda")
                 w.view(blk["cout_p"], cin_g, 27)[:, :blk["cin_p"]] = blk["w"].view(blk["cout_p"], blk["cin_p"], 27)
-            wb = nconv.pack_weights(w, blk["cout_p"], cin_g, 27, True)
-            dx = nconv.gather_gemm(nb.conv_maps[i], d_conv, wb, cin_g, BF16)[:, :blk["cin_p"]]
+            if self.f32:
+                wb = nconv.pack_weights_x2(w, blk["cout_p"], cin_g, 27, nconv.PACK_BACKWARD)
+                dx = nconv.gather_gemm_x2(nb.conv_maps[i], d_conv_s, wb, cin_g)[:, :blk["cin_p"]]
+            else:
+                wb = nconv.pack_weights(w, blk["cout_p"], cin_g, 27, True)
+                dx = nconv.gather_gemm(nb.conv_maps[i], d_conv, wb, cin_g, BF16)[:, :blk["cin_p"]]
             if trace is not None:
                 trace["blocks"][i]["dx"] = dx
             if i > 0:  # net.cpp:296-300: unpool through the finer level's switches
                 prev = self.blocks[i - 1]
                 par, prow = nb.parents[i - 1]
                 nf = nb.levels[i - 1].total_columns()
-                d_relu = torch.empty((nf, prev["cout_p"]), dtype=BF16, device="cuda")
-                check(lib.hc_native_max_unpool(_p(par), _p(prow), nf, _p(dx), _lib.HC_DTYPE_BF16, prev["cout_p"],
-                                               _p(acts[i - 1]["sw"]), _p(d_relu), _s()))
-                d_dtype = _lib.HC_DTYPE_BF16
+                d_relu = torch.empty((nf, prev["cout_p"]), dtype=self.adt, device="cuda")
+                check(lib.hc_native_max_unpool(_p(par), _p(prow), nf, _p(dx.contiguous()), self.adt_code,
+                                               prev["cout_p"], _p(acts[i - 1]["sw"]), _p(d_relu), _s()))
+                d_dtype = self.adt_code
         head_grads = (g_fc1_w, g_fc1_b, g_fc2_w, g_fc2_b)
         return loss, conv_grads, head_grads
 

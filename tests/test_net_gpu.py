@@ -215,3 +215,43 @@ def test_native_seg_step_descends(cuda):
     labels = (x[:, 0].float() > 0).long() + 2 * (x[:, 1].float() > 0).long()  # learnable from the input
     losses = [float(seg.step(x, labels)) for _ in range(15)]
     assert all(np.isfinite(losses)) and losses[-1] < 0.8 * losses[0], losses
+
+
+def test_native_net_step_f32_matches_reference_net(cuda, ref):
+    """precision="f32": fp32 activations, every conv through the split-precision tcgen05 kernels.
+    The same step as above against the unmodified fp32 reference net, now at the reference's
+    precision: loss 1e-6 relative, conv / FC weight gradients 5e-5 normwise, running statistics
+    1e-5 (the remaining differences are the reference's own fp32 summation order)."""
+    level_max, classes, b = 4, 5, 3
+    supers = _ref_pyramid_batch(ref, b, 1 << level_max, seed=11)
+    labels = np.array([0, 3, 1], np.int32)
+    rn = ref.net_make(level_max, classes, 7)
+    rn.set_dropout(0.0)
+    head_in = nnet.channels_at_level(2) * 8
+    net = nnet.NativeHashNet(level_max, classes, seed=1, dropout=0.0, precision="f32")
+    for i in range(rn.nblocks):
+        net.set_reference_weights(i, torch.from_numpy(rn.conv(i)).cuda())
+    for dst, src in zip((net.fc1_w, net.fc1_b, net.fc2_w, net.fc2_b), rn.fc(classes, head_in)):
+        dst.copy_(torch.from_numpy(src))
+    loss_r, grads_r, fc_r = rn.loss_and_gradients(supers, labels, classes, head_in)
+
+    nb = nnet.NetBatch.build([SuperPsh.from_host(s) for s in supers])
+    x = net.input_features(torch.from_numpy(supers[0].data).cuda())
+    assert x.dtype == torch.float32
+    loss_n, grads_n, fc_n = net.loss_and_gradients(nb, x, torch.from_numpy(labels).long().cuda())
+    errs = {"loss": abs(float(loss_n) - loss_r) / abs(loss_r)}
+    for i, gr in enumerate(grads_r):
+        blk = net.blocks[i]
+        gn = grads_n[i].view(blk["cout_p"], blk["cin_p"], 27)[:blk["cout"], :blk["cin"]].reshape(gr.shape)
+        errs[f"dw{i}"] = _rel(gn.cpu().numpy(), gr)
+        full = grads_n[i].view(blk["cout_p"], blk["cin_p"], 27)
+        assert float(full[blk["cout"]:].abs().sum()) == 0.0 and float(full[:, blk["cin"]:].abs().sum()) == 0.0
+        m_r, v_r = rn.bn(i)
+        errs[f"mean{i}"] = _rel(blk["run_mean"][:blk["cout"]].cpu().numpy(), m_r)
+        errs[f"var{i}"] = _rel(blk["run_var"][:blk["cout"]].cpu().numpy(), v_r)
+    for k, (a, r) in enumerate(zip(fc_n, fc_r)):
+        errs[f"fc{k}"] = _rel(a.cpu().numpy(), r)
+    print(errs)
+    assert errs["loss"] < 1e-6, errs  # measured 1.0e-7
+    assert all(v < 5e-5 for k, v in errs.items() if k.startswith(("dw", "fc"))), errs  # measured <= 1.0e-5
+    assert all(v < 1e-5 for k, v in errs.items() if k.startswith(("mean", "var"))), errs  # measured <= 3.1e-6
