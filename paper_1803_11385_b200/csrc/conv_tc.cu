@@ -705,6 +705,9 @@ struct DwGroups {
     int groups;
     int pair, rpm, pcols;
     int nacc;  // accumulator buffers per CTA (2: chunk drains overlap the next chunk's MMAs)
+    int strided;  // 1: CTA k of a group runs chunks k, k + n, k + 2n ... (n = the group's CTAs), so
+                  // the whole grid sweeps the voxels together and the groups' gathers of X and
+                  // loads of dY hit L2; 0: contiguous runs of cpc chunks
     int m_begin[kMaxGroups + 1];
     int cta_begin[kMaxGroups + 1];
     int tps[kMaxGroups];
@@ -761,10 +764,16 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
     const int m0 = grp_tab.m_begin[grp];
     const int nm = grp_tab.m_begin[grp + 1] - m0;
     const int tps = grp_tab.tps[grp];
-    const int chunk0 = ((int)blockIdx.x - grp_tab.cta_begin[grp]) * grp_tab.cpc[grp];
-    const int nch = max(0, min(grp_tab.cpc[grp], grp_tab.nchunk[grp] - chunk0));
-    const int tile0 = chunk0 * tps;
-    const int ntl = max(0, min(nch * tps, tiles - tile0));
+    const int kcta = (int)blockIdx.x - grp_tab.cta_begin[grp];
+    const int nct = grp_tab.cta_begin[grp + 1] - grp_tab.cta_begin[grp];
+    const int nchunk = grp_tab.nchunk[grp];
+    const int chunk0 = grp_tab.strided ? kcta : kcta * grp_tab.cpc[grp];
+    const int cstride = grp_tab.strided ? nct : 1;
+    const int nch = grp_tab.strided ? (kcta < nchunk ? (nchunk - kcta + nct - 1) / nct : 0)
+                                    : max(0, min(grp_tab.cpc[grp], nchunk - chunk0));
+    // this CTA's chunks are chunk0 + j * cstride; all hold tps tiles but the grid's last one
+    const int ntl = nch > 0 ? (nch - 1) * tps + min(tps, tiles - (chunk0 + (nch - 1) * cstride) * tps) : 0;
+    auto tile_of = [&](int lt) { return (chunk0 + (lt / tps) * cstride) * tps + lt % tps; };
     const int pair = grp_tab.pair;    // 0 plain, 1 pair (split precision, 4 products), 2 tri (3 products)
     const int Co = pair ? C / 2 : C;  // channels of one plane
     const int RPM = pair == 1 ? 64 : 128;  // (t, ci) rows per m-tile (tri: per unit)
@@ -838,7 +847,7 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
         for (int j = 0; j < J; ++j) doff[j] = blk * (Cfg::KB * 128) + sw128_offset(v0 + j, c);
         auto request = [&](int lt, int buf) {
             mbar_arrive_expect_tx(nfull0 + 8 * buf, nbr_bytes);
-            bulk_g2s(smem_u32(nbr_s + buf * NT * BM), fmap + ((long long)(tile0 + lt) * taps + t_lo) * BM, nbr_bytes,
+            bulk_g2s(smem_u32(nbr_s + buf * NT * BM), fmap + ((long long)tile_of(lt) * taps + t_lo) * BM, nbr_bytes,
                      nfull0 + 8 * buf);
         };
         if (tid == 0) {
@@ -901,7 +910,7 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
 #endif
                 {
                 mbar_arrive_expect_tx(bfull0 + 8 * bs, Cfg::B_BYTES);
-                const int n0 = (tile0 + lt) * BM + h * 64;
+                const int n0 = tile_of(lt) * BM + h * 64;
 #pragma unroll
                 for (int cb = 0; cb < NB / 64; ++cb)
                     tma_load2d(bbase + bs * Cfg::B_BYTES + cb * (Cfg::KB * 128), &dymap, cb * 64, n0,
@@ -987,7 +996,7 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
             mbar_wait_sleep(done0 + 8 * ab, (uint32_t)((nacc == 2 ? c >> 1 : c) & 1));
             const uint32_t tqa = tq + ab * nm * (pair == 2 ? 3 * pco : NB);
             tc_fence_after();
-            const long long slot = chunk0 + c;
+            const long long slot = chunk0 + (long long)c * cstride;
             if (pair == 2) {
                 // tri: lane = (t, ci) row of the unit; fixed order (hi.dY_hi + hi.dY_lo) + lo.dY_hi
                 const int g = x2_block(pco);
@@ -1446,8 +1455,8 @@ DwPlan dw_plan(long long rows, int taps, int cin, int cout, int max_tps = 0, boo
     // pair mode with chunked accumulation: HCB_DW_DBUF=1 keeps two accumulator sets per CTA (the
     // epilogue drains one chunk while the next accumulates) at half the m-tiles per CTA
     static const int dbuf_env = env_int("HCB_DW_DBUF", 0);
-    const int nacc = (pair && max_tps > 0 && dbuf_env) ? 2 : 1;
     const int unit_cols = mode == 2 ? 3 * cout : p.nb;  // tri: [hi.dY_hi | hi.dY_lo] + lo.dY_hi
+    const int nacc = (pair && max_tps > 0 && dbuf_env && 512 / (unit_cols * p.cps * 2) >= 1) ? 2 : 1;
     const int cap = std::min(mode == 2 ? 8 : 16, 512 / (unit_cols * p.cps * nacc));  // m-tiles (units) per CTA
     const int G = (p.mt + cap - 1) / cap;  // -> every group has <= cap m-tiles
     if (cap < 1 || G > kMaxGroups)
@@ -1458,6 +1467,8 @@ DwPlan dw_plan(long long rows, int taps, int cin, int cout, int max_tps = 0, boo
     g.groups = G;
     g.pair = mode;
     g.nacc = nacc;
+    static const int strided = env_int("HCB_DW_STRIDED", 1);
+    g.strided = strided;
     g.rpm = rpm;
     g.pcols = pair ? cout : p.nb;
     // Few groups (C_out <= 64): CTAs proportional to each group's m-tiles, so groups of
