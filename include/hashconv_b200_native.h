@@ -68,6 +68,18 @@ hc_status hc_native_split(const float* src, int32_t channel_major, int64_t c, in
 /* Same modes as hc_native_pack_weights; w_packed: bf16 [2*rows][hc_native_packed_k_x2(...)]. */
 hc_status hc_native_pack_weights_x2(const float* w_ref, int32_t c_out, int32_t c_in, int32_t taps,
                                     int32_t mode, void* w_packed, hc_stream stream);
+/* The forward with batch-norm statistics from the epilogue: besides y, per
+ * 128-row tile of the output and output channel, tile_stats[(tile * c_out + co) * 2 + {0, 1}] =
+ * {sum, sum of squares about the tile mean} of the fp32 values (rows >= n_out excluded);
+ * hc_native_bn_relu_forward_tiles folds them (replaces cnn_ops.cpp:455-466's two passes). */
+hc_status hc_native_gather_gemm_stats(const int32_t* fmap, int32_t fmap_layout, int64_t n_out,
+                                      int32_t taps, const void* x, int32_t c_in, const void* w_packed,
+                                      int32_t c_out, void* y, hc_dtype y_dtype, float* tile_stats,
+                                      hc_stream stream);
+hc_status hc_native_gather_gemm_x2_stats(const int32_t* fmap, int32_t fmap_layout, int64_t n_out,
+                                         int32_t taps, const void* x_split, int32_t c_in,
+                                         const void* w_packed_x2, int32_t c_out, float* y,
+                                         float* tile_stats, hc_stream stream);
 /* y fp32 [n_out][c_out] = gather-GEMM of the split rows (hc_native_gather_gemm semantics). */
 hc_status hc_native_gather_gemm_x2(const int32_t* fmap, int32_t fmap_layout, int64_t n_out,
                                    int32_t taps, const void* x_split, int32_t c_in,
@@ -159,6 +171,14 @@ hc_status hc_native_bn_relu_backward_apply_dt(const void* d_relu, hc_dtype dtype
                                               const float* inv_std, int64_t n, int32_t c, const double* s1,
                                               const double* s2, int64_t n_total, void* d_conv,
                                               hc_dtype out_dtype, hc_stream stream);
+/* Training batch norm + ReLU from the conv epilogue's tile statistics (hc_native_gather_gemm*
+ * _stats on the same n x c output x): Chan's merge of the tiles in double (fixed order) ->
+ * mean, biased variance, running stats, inv_std; then xhat / out as hc_native_bn_relu_forward_dt.
+ * workspace: >= c doubles. Two launches instead of five. */
+hc_status hc_native_bn_relu_forward_tiles(const float* tile_stats, int64_t n, int32_t c, float momentum,
+                                          float eps, float* running_mean, float* running_var, float* inv_std,
+                                          const float* x, float* xhat, void* out, hc_dtype out_dtype,
+                                          void* workspace, size_t ws_bytes, hc_stream stream);
 /* Final dense pool: cmap [b][8 cells][8 children] resolution-4 columns (or -1); head
  * [(c*8 + cell)][b] fp32 = max over present children, src = winning column or -1. */
 hc_status hc_native_dense_pool(const int32_t* cmap, int32_t b, const void* x_bf16, int32_t c,

@@ -145,6 +145,10 @@ _SIGS.update({
     "hc_native_bn_relu_backward_apply": [_P, C.c_int, _P, _P, _I64, _I32, _P, _P, _I64, _P, _P],
     "hc_native_dense_pool": [_P, _I32, _P, _I32, _P, _P, _P],
     "hc_native_dense_pool_dt": [_P, _I32, _P, C.c_int, _I32, _P, _P, _P],
+    "hc_native_bn_relu_forward_tiles": [_P, _I64, _I32, C.c_float, C.c_float, _P, _P, _P, _P, _P, _P, C.c_int, _P,
+                                        C.c_size_t, _P],
+    "hc_native_gather_gemm_stats": [_P, _I32, _I64, _I32, _P, _I32, _P, _I32, _P, C.c_int, _P, _P],
+    "hc_native_gather_gemm_x2_stats": [_P, _I32, _I64, _I32, _P, _I32, _P, _I32, _P, _P, _P],
     "hc_native_bn_relu_forward_dt": [_P, _I64, _I32, _I32, C.c_float, C.c_float, _P, _P, _P, _P, _P, C.c_int, _P,
                                      C.c_size_t, _P],
     "hc_native_bn_relu_backward_dt": [_P, C.c_int, _P, _P, _I64, _I32, _P, C.c_int, _P, C.c_size_t, _P],

@@ -155,6 +155,69 @@ __device__ __forceinline__ void store_row(float* dst, const float (&v)[16]) {
     for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
 }
 
+
+// ---------------------------------------------------------------------- batch-norm statistics
+// The forward epilogue can emit, per 128-row tile and output channel, the tile's sum and its
+// centred sum of squares (BN statistics from the conv epilogue instead of two
+// extra passes over Y; cnn_ops.cpp:455-466 takes the mean and the centred variance in double).
+// hc_native_bn_relu_forward_tiles merges the tiles with Chan's parallel formula in double in a
+// fixed order, so the result is the two-pass statistic up to fp32 rounding inside a tile.
+//
+// Sum over a warp's 32 lanes of 16 values per lane in 16 shuffles (recursive halving): after
+// the call, lane l holds the total of channel (l >> 1) & 15.
+__device__ __forceinline__ float warp_sum16(float (&v)[16], int lane) {
+#pragma unroll
+    for (int w = 8, off = 16; w >= 1; w >>= 1, off >>= 1) {
+        const bool up = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < w; ++i) {
+            const float send = up ? v[i] : v[w + i];
+            const float keep = up ? v[w + i] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+    }
+    return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+
+// Tile statistics of one 16-channel chunk: f = this lane's row (rows >= `count` are padding and
+// excluded), q = the warp's lane quadrant (rows q*32 ...). red: 2 x [4][16] floats of shared
+// memory (buffer `buf` alternates per chunk). Named barrier 1 over the 4 epilogue warps.
+__device__ __forceinline__ void tile_stats16(const float (&f)[16], bool valid, int count, int q, int lane, float* red,
+                                             float2* out) {
+    float v[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = valid ? f[e] : 0.0f;
+    const int ch = (lane >> 1) & 15;
+    float* r1 = red;       // [4][16] warp sums
+    float* r2 = red + 64;  // [4][16] warp centred squares
+    const float s1 = warp_sum16(v, lane);
+    if ((lane & 1) == 0) r1[q * 16 + ch] = s1;
+    named_sync(1, 128);
+    const float inv = 1.0f / (float)count;
+    float tot = 0.0f;  // lane < 16: the tile sum of channel `lane` (read before r1 can be reused)
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        const float t = ((r1[e] + r1[16 + e]) + r1[32 + e]) + r1[48 + e];
+        if (e == lane) tot = t;
+        const float d = f[e] - t * inv;
+        v[e] = valid ? d * d : 0.0f;
+    }
+    const float s2 = warp_sum16(v, lane);
+    if ((lane & 1) == 0) r2[q * 16 + ch] = s2;
+    named_sync(1, 128);
+    // r1 may be overwritten by the next chunk from here on (a warp passes this barrier only after
+    // its own reads); r2 is rewritten only after the next chunk's first barrier
+    if (q == 0 && lane < 16) out[lane] = make_float2(tot, ((r2[lane] + r2[16 + lane]) + r2[32 + lane]) + r2[48 + lane]);
+}
+
+// Per-launch target of the epilogue statistics (hc_native_gather_gemm*_stats set it around
+// the launch; the launchers pass it to the kernels): [tiles][c_out] float2 {sum, M2}.
+thread_local float2* g_tile_stats = nullptr;
+struct TileStatsScope {
+    explicit TileStatsScope(float2* p) { g_tile_stats = p; }
+    ~TileStatsScope() { g_tile_stats = nullptr; }
+};
+
 // ====================================================================== forward gather-GEMM
 // Y[m][0:BN] = sum_k A[m][k] * Wp[0:BN][k],  A[m][k] = X[nbr(m, k / C)][k % C] (0 if -1)
 // CPS resident CTAs per SM (1: one deep ring; 2: two shallower rings), PW producer warps.
@@ -168,7 +231,7 @@ struct FwdCfg {
     static constexpr int EPI_BUFS = (OUT_BYTES == 2 && BN < 256) ? 2 : 1;  // BN=256 keeps a 4-stage ring
     static constexpr int EPI_BUF = 32 * 16 * OUT_BYTES;
     static constexpr int EPI = 4 * EPI_BUFS * EPI_BUF;
-    static constexpr int BUDGET = (CPS == 2 ? 113 : 226) * 1024 - 1024 - 320 - NBR - EPI;
+    static constexpr int BUDGET = (CPS == 2 ? 113 : 226) * 1024 - 1024 - 320 - NBR - EPI - 1024;  // - stats scratch
 #ifndef HCB_FWD_MAXSTAGES
 #define HCB_FWD_MAXSTAGES 10
 #endif
@@ -187,7 +250,8 @@ template <int BN, int CPS, int PW, typename OutT, bool SUMH = false>
 __global__ void __launch_bounds__(FwdCfg<BN, CPS, PW, sizeof(OutT)>::THREADS, CPS)
     k_conv_fwd(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap ymap,
                const int* __restrict__ fmap, int taps, long long rows, const bf16* __restrict__ X, int C, int nkb,
-               int tiles, int skip_lolo /* SUMH: plane block g, 0 = keep lo x lo */) {
+               int tiles, int skip_lolo /* SUMH: plane block g, 0 = keep lo x lo */, float2* __restrict__ stats) {
+    __shared__ float red_s[128];  // epilogue BN statistics scratch (tile_stats16)
     using Cfg = FwdCfg<BN, CPS, PW, sizeof(OutT)>;
     constexpr int NP = Cfg::PRODUCERS;
     constexpr int S = Cfg::STAGES;
@@ -331,6 +395,9 @@ __global__ void __launch_bounds__(FwdCfg<BN, CPS, PW, sizeof(OutT)>::THREADS, CP
 #pragma unroll
                     for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(v[e]);
                 }
+                if (stats)  // BN statistics of the fp32 values before the output rounding
+                    tile_stats16(f, r0 + lane < rows, (int)min(128LL, rows - (long long)tile * BM), q, lane, red_s,
+                                 stats + (long long)tile * BO + c0);
                 uint8_t* buf = stage + (nb_issued % Cfg::EPI_BUFS) * Cfg::EPI_BUF;
                 if (nb_issued >= Cfg::EPI_BUFS) {  // that buffer's previous store has been read
                     if (lane == 0) bulk_wait_read<Cfg::EPI_BUFS - 1>();
@@ -449,7 +516,9 @@ struct FwdX2Cfg {
 template <int BN, int CPS, int PW, int SA, int SB, int NBUF>
 __global__ void __launch_bounds__(FwdX2Cfg<BN, CPS, PW, SA, SB, NBUF>::THREADS, CPS)
     k_conv_fwd_x2(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap ymap,
-                  const int* __restrict__ fmap, int taps, const bf16* __restrict__ X, int C, int nkb, int tiles) {
+                  const int* __restrict__ fmap, int taps, const bf16* __restrict__ X, int C, int nkb, int tiles,
+                  long long rows, float2* __restrict__ stats) {
+    __shared__ float red_s[128];  // epilogue BN statistics scratch (tile_stats16)
     using Cfg = FwdX2Cfg<BN, CPS, PW, SA, SB, NBUF>;
     constexpr int NP = PW * 32;
     constexpr int RS = NP / 8;
@@ -582,6 +651,9 @@ __global__ void __launch_bounds__(FwdX2Cfg<BN, CPS, PW, SA, SB, NBUF>::THREADS, 
                 float f[16];
 #pragma unroll
                 for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(v[e]) + __uint_as_float(u[e]);
+                if (stats)
+                    tile_stats16(f, r0 + lane < rows, (int)min(128LL, rows - (long long)tile * BM), q, lane, red_s,
+                                 stats + (long long)tile * BO + c0);
                 if (issued) {  // the staging box's previous store has been read
                     if (lane == 0) bulk_wait_read<0>();
                     __syncwarp();
@@ -1310,7 +1382,7 @@ void launch_fwd(const int* fmap, int taps, long long rows, const bf16* X, int C,
     const int tiles = (int)((rows + BM - 1) / BM);
     const int grid = std::min(tiles, CPS * num_sms());
     const CUtensorMap ym = map_out(Y, sizeof(OutT) == 4, (uint64_t)(SUMH ? BN / 2 : BN), (uint64_t)rows, 16, 32);
-    kern<<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(wm, ym, fmap, taps, rows, X, C, Kp / BK, tiles, skip_lolo);
+    kern<<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(wm, ym, fmap, taps, rows, X, C, Kp / BK, tiles, skip_lolo, g_tile_stats);
     launched(SUMH ? "conv gather-GEMM, split precision (tcgen05)" : "conv gather-GEMM (tcgen05)");
 }
 
@@ -1359,7 +1431,7 @@ void launch_fwd_x2s(const int* fmap, int taps, long long rows, const bf16* X, in
     const int tiles = (int)((rows + BM - 1) / BM);
     const int grid = std::min(tiles, CPS * num_sms());
     const CUtensorMap ym = map_out(Y, true, (uint64_t)(BN / 2), (uint64_t)rows, 16, 32);
-    kern<<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(wm, ym, fmap, taps, X, C, Kp / BK, tiles);
+    kern<<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(wm, ym, fmap, taps, X, C, Kp / BK, tiles, rows, g_tile_stats);
     launched("conv gather-GEMM, split precision, shared weight ring (tcgen05)");
 }
 
@@ -1777,6 +1849,20 @@ hc_status hc_native_pack_weights_x2(const float* w_ref, int32_t c_out, int32_t c
                                                                       static_cast<bf16*>(w_packed), c_out, c_in);
         launched("pack weights (split precision)");
     });
+}
+
+hc_status hc_native_gather_gemm_stats(const int32_t* fmap, int32_t fmap_layout, int64_t n_out, int32_t taps,
+                                      const void* x, int32_t c_in, const void* w_packed, int32_t c_out, void* y,
+                                      hc_dtype y_dtype, float* tile_stats, hc_stream stream) {
+    const TileStatsScope scope(reinterpret_cast<float2*>(tile_stats));
+    return hc_native_gather_gemm(fmap, fmap_layout, n_out, taps, x, c_in, w_packed, c_out, y, y_dtype, stream);
+}
+
+hc_status hc_native_gather_gemm_x2_stats(const int32_t* fmap, int32_t fmap_layout, int64_t n_out, int32_t taps,
+                                         const void* x_split, int32_t c_in, const void* w_packed_x2, int32_t c_out,
+                                         float* y, float* tile_stats, hc_stream stream) {
+    const TileStatsScope scope(reinterpret_cast<float2*>(tile_stats));
+    return hc_native_gather_gemm_x2(fmap, fmap_layout, n_out, taps, x_split, c_in, w_packed_x2, c_out, y, stream);
 }
 
 hc_status hc_native_gather_gemm_x2(const int32_t* fmap, int32_t fmap_layout, int64_t n_out, int32_t taps,

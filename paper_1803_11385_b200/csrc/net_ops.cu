@@ -280,6 +280,54 @@ __global__ void k_col_fold(const double* __restrict__ part, int blocks, long lon
     }
 }
 
+// Batch-norm statistics from the conv epilogue's per-tile {sum, centred sum of squares}
+// (hc_native_gather_gemm*_stats): one block per channel; thread j merges tiles j*T/kT ..
+// (j+1)*T/kT - 1 in order with Chan's formula in double, then a fixed-shape tree over the
+// lanes -> mean, biased variance (cnn_ops.cpp:455-466), running stats and inv_std exactly as
+// k_col_fold MODE 1 forms them.
+__global__ void __launch_bounds__(kT) k_bn_fold_tiles(const float2* __restrict__ st, long long tiles, long long n,
+                                                     int C, float* __restrict__ run_mean, float* __restrict__ run_var,
+                                                     float momentum, float eps, double* __restrict__ mean_out,
+                                                     float* __restrict__ inv_std) {
+    const int c = blockIdx.x;
+    __shared__ double sn[kT], sm[kT], s2[kT];
+    const long long t0 = tiles * threadIdx.x / kT, t1 = tiles * (threadIdx.x + 1) / kT;
+    double cnt = 0.0, mean = 0.0, m2 = 0.0;
+    for (long long t = t0; t < t1; ++t) {
+        const float2 v = st[t * C + c];
+        const double nb = (double)min(128LL, n - t * 128);
+        const double mb = (double)v.x / nb;
+        const double tot = cnt + nb;
+        const double delta = mb - mean;
+        mean += delta * nb / tot;
+        m2 += (double)v.y + delta * delta * cnt * nb / tot;
+        cnt = tot;
+    }
+    sn[threadIdx.x] = cnt;
+    sm[threadIdx.x] = mean;
+    s2[threadIdx.x] = m2;
+    __syncthreads();
+    for (int w = 1; w < kT; w <<= 1) {  // lane j absorbs lane j + w (adjacent ranges, fixed order)
+        if ((threadIdx.x & (2 * w - 1)) == 0) {
+            const double na = sn[threadIdx.x], nb = sn[threadIdx.x + w];
+            const double tot = na + nb;
+            if (nb > 0.0) {
+                const double delta = sm[threadIdx.x + w] - sm[threadIdx.x];
+                sm[threadIdx.x] += delta * nb / tot;
+                s2[threadIdx.x] += s2[threadIdx.x + w] + delta * delta * na * nb / tot;
+                sn[threadIdx.x] = tot;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
+    const double mu = sm[0], var = s2[0] / (double)n;
+    mean_out[c] = mu;
+    run_mean[c] = (1.0f - momentum) * run_mean[c] + momentum * (float)mu;
+    run_var[c] = (1.0f - momentum) * run_var[c] + momentum * (float)var;
+    inv_std[c] = (float)(1.0 / sqrt(var + (double)eps));
+}
+
 // Synchronised (data-parallel) batch norm: statistics from sums taken over the GLOBAL batch
 // (all-reduced by the caller). sum_sq == nullptr: mean = sum_x / n_total; otherwise
 // var = sum_sq / n_total (biased, cnn_ops.cpp:463-466), running stats, inv_std — the same
@@ -629,6 +677,26 @@ hc_status hc_native_bn_relu_inference_dt(const float* x, int64_t n, int32_t c, c
             k_bn_relu_infer<bf16><<<grid_for(m, kT), kT, 0, s>>>(x, n, c, running_mean, running_var, eps,
                                                                  static_cast<bf16*>(out));
         launched("batch-norm (inference) + relu");
+    });
+}
+
+hc_status hc_native_bn_relu_forward_tiles(const float* tile_stats, int64_t n, int32_t c, float momentum, float eps,
+                                          float* running_mean, float* running_var, float* inv_std, const float* x,
+                                          float* xhat, void* out, hc_dtype out_dtype, void* workspace,
+                                          size_t ws_bytes, hc_stream stream) {
+    return guard([&] {
+        check_c8(c);
+        check_out_dtype(out_dtype);
+        if (c > kT) throw std::invalid_argument("native batch norm: at most 256 channels");
+        if (n <= 0) throw std::invalid_argument("batch_norm: empty input");
+        if (ws_bytes < (size_t)c * sizeof(double)) throw std::invalid_argument("native batch norm: workspace too small");
+        cudaStream_t s = as_stream(stream);
+        double* mean = static_cast<double*>(workspace);
+        const long long tiles = (n + 127) / 128;
+        k_bn_fold_tiles<<<c, kT, 0, s>>>(reinterpret_cast<const float2*>(tile_stats), tiles, n, c, running_mean,
+                                        running_var, momentum, eps, mean, inv_std);
+        launched("batch-norm statistics from conv tiles");
+        bn_relu_apply_out(x, n, c, mean, inv_std, xhat, out, out_dtype, s);
     });
 }
 

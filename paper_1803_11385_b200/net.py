@@ -132,6 +132,9 @@ class NativeHashNet:
         self.f32 = precision == "f32"
         self.adt = torch.float32 if self.f32 else BF16  # activation / conv-gradient dtype
         self.adt_code = _lib.HC_DTYPE_F32 if self.f32 else _lib.HC_DTYPE_BF16
+        # batch-norm statistics from the conv epilogue (per-tile sums merged in double) instead of
+        # two passes over the conv output; sync BN keeps the phased path (its sums are all-reduced)
+        self.epilogue_stats = True
         if level_max < 2 or level_max > 16:
             raise ValueError("level_max out of range")
         if num_classes < 2:
@@ -247,15 +250,24 @@ class NativeHashNet:
         x[:, :c] = nconv.to_voxel_major(ref) if not self.f32 else ref.t()
         return x
 
-    def _conv_forward(self, i: int, x: torch.Tensor):
-        """Block i's conv: returns (fp32 output, what the backward needs of the input)."""
+    def _conv_forward(self, i: int, x: torch.Tensor, stats: Optional[torch.Tensor] = None):
+        """Block i's conv: returns (fp32 output, what the backward needs of the input). stats:
+        [tiles][c_out][2] fp32 receives the epilogue's per-tile batch-norm statistics."""
         blk = self.blocks[i]
+        fm = self._maps[i]
+        n, co = fm.n, blk["cout_p"]
+        y = torch.empty((n, co), dtype=torch.float32, device="cuda")
         if self.f32:
             xs = nconv.split(x)
-            wf = nconv.pack_weights_x2(blk["w"], blk["cout_p"], blk["cin_p"], 27, nconv.PACK_FORWARD)
-            return nconv.gather_gemm_x2(self._maps[i], xs, wf, blk["cout_p"]), xs
-        wf = nconv.pack_weights(blk["w"], blk["cout_p"], blk["cin_p"], 27, False)
-        return nconv.gather_gemm(self._maps[i], x, wf, blk["cout_p"], torch.float32), x
+            wf = nconv.pack_weights_x2(blk["w"], co, blk["cin_p"], 27, nconv.PACK_FORWARD)
+            check(lib.hc_native_gather_gemm_x2_stats(_p(fm.data), fm.layout, n, fm.taps, _p(xs), blk["cin_p"], _p(wf),
+                                                     co, _p(y), _p(stats) if stats is not None else None, _s()))
+            return y, xs
+        wf = nconv.pack_weights(blk["w"], co, blk["cin_p"], 27, False)
+        check(lib.hc_native_gather_gemm_stats(_p(fm.data), fm.layout, n, fm.taps, _p(x), blk["cin_p"], _p(wf), co,
+                                              _p(y), _lib.HC_DTYPE_F32, _p(stats) if stats is not None else None,
+                                              _s()))
+        return y, x
 
     # ------------------------------------------------------------------ forward / backward
     def forward(self, nb: NetBatch, x: torch.Tensor, training: bool = True, cache: Optional[dict] = None):
@@ -267,9 +279,18 @@ class NativeHashNet:
         for i, blk in enumerate(self.blocks):
             s = nb.levels[i]
             n = s.total_columns()
-            y, x_saved = self._conv_forward(i, x)
+            fused = training and self.sync_bn is None and self.epilogue_stats
+            stats = torch.empty(((n + 127) // 128, blk["cout_p"], 2), device="cuda") if fused else None
+            y, x_saved = self._conv_forward(i, x, stats)
             r = torch.empty((n, blk["cout_p"]), dtype=self.adt, device="cuda")
-            if training:
+            if fused:  # batch-norm statistics from the conv epilogue: fold + apply (2 launches)
+                xhat = torch.empty_like(y)
+                ws = self._bn_ws(n, blk["cout_p"])
+                check(lib.hc_native_bn_relu_forward_tiles(_p(stats), n, blk["cout_p"], self.bn_momentum, self.bn_eps,
+                                                          _p(blk["run_mean"]), _p(blk["run_var"]), _p(blk["inv_std"]),
+                                                          _p(y), _p(xhat), _p(r), self.adt_code, _p(ws), ws.numel(),
+                                                          _s()))
+            elif training:
                 xhat = torch.empty_like(y)
                 self._bn_relu_forward(i, y, xhat, r)
             else:

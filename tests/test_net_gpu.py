@@ -255,3 +255,92 @@ def test_native_net_step_f32_matches_reference_net(cuda, ref):
     assert errs["loss"] < 1e-6, errs  # measured 1.0e-7
     assert all(v < 5e-5 for k, v in errs.items() if k.startswith(("dw", "fc"))), errs  # measured <= 1.0e-5
     assert all(v < 1e-5 for k, v in errs.items() if k.startswith(("mean", "var"))), errs  # measured <= 3.1e-6
+
+
+@pytest.mark.parametrize("x2", [False, True])
+@pytest.mark.parametrize("c_in,c_out", [(8, 16), (32, 64), (64, 128)])
+def test_conv_epilogue_tile_stats(cuda, x2, c_in, c_out):
+    """hc_native_gather_gemm[_x2]_stats: the epilogue's per-tile {sum, centred sum of squares}
+    equal float64 statistics of the same fp32 output tiles (ragged last tile excluded rows),
+    and hc_native_bn_relu_forward_tiles reproduces the two-pass batch norm (cnn_ops.cpp:455-466)."""
+    f, _ = random_pair(32, 3, seed=c_out + x2, n_lo=900, n_hi=2500)
+    s = SuperPsh.from_levels(f)
+    n = s.total_columns()
+    assert n % 128 != 0
+    fm = nconv.field_map_native(s, s, ConvSpec(3, 1, 0, c_in, c_out), nconv.TILED)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.rand((n, c_in), device="cuda", generator=g) * 2 - 1 + 0.3
+    w = (torch.rand((c_out, c_in * 27), device="cuda", generator=g) * 2 - 1) * 0.2
+    tiles = (n + 127) // 128
+    st = torch.full((tiles, c_out, 2), float("nan"), device="cuda")
+    y = torch.empty((n, c_out), device="cuda")
+    if x2:
+        xs = nconv.split(x)
+        wp = nconv.pack_weights_x2(w, c_out, c_in, 27, nconv.PACK_FORWARD)
+        _lib.check(_lib.lib.hc_native_gather_gemm_x2_stats(_p(fm.data), fm.layout, n, 27, _p(xs), c_in, _p(wp), c_out,
+                                                           _p(y), _p(st), None))
+        assert torch.equal(y, nconv.gather_gemm_x2(fm, xs, wp, c_out))
+    else:
+        xb = x.to(torch.bfloat16)
+        wp = nconv.pack_weights(w, c_out, c_in, 27, False)
+        _lib.check(_lib.lib.hc_native_gather_gemm_stats(_p(fm.data), fm.layout, n, 27, _p(xb), c_in, _p(wp), c_out,
+                                                        _p(y), _lib.HC_DTYPE_F32, _p(st), None))
+        assert torch.equal(y, nconv.gather_gemm(fm, xb, wp, c_out, torch.float32))
+    yd = torch.cat([y.double(), torch.zeros((tiles * 128 - n, c_out), dtype=torch.float64, device="cuda")])
+    yd = yd.view(tiles, 128, c_out)
+    cnt = torch.clamp(n - torch.arange(tiles, device="cuda") * 128, max=128).double()
+    mask = (torch.arange(128, device="cuda")[None, :] < cnt[:, None]).double()[:, :, None]
+    s1 = (yd * mask).sum(1)
+    m2 = (((yd - (s1 / cnt[:, None])[:, None, :]) ** 2) * mask).sum(1)
+    assert _rel(st[..., 0].cpu().numpy(), s1.cpu().numpy()) < 1e-6
+    assert _rel(st[..., 1].cpu().numpy(), m2.cpu().numpy()) < 1e-6
+    # fold + apply vs the two-pass kernels
+    rm1, rv1 = torch.zeros(c_out, device="cuda"), torch.ones(c_out, device="cuda")
+    rm2, rv2 = rm1.clone(), rv1.clone()
+    inv1, inv2 = torch.empty(c_out, device="cuda"), torch.empty(c_out, device="cuda")
+    xh1, xh2 = torch.empty_like(y), torch.empty_like(y)
+    o1, o2 = torch.empty_like(y), torch.empty_like(y)
+    ws = torch.empty(int(_lib.lib.hc_native_bn_workspace(n, c_out)), dtype=torch.uint8, device="cuda")
+    _lib.check(_lib.lib.hc_native_bn_relu_forward_tiles(_p(st), n, c_out, 0.1, 1e-5, _p(rm1), _p(rv1), _p(inv1), _p(y),
+                                                        _p(xh1), _p(o1), _lib.HC_DTYPE_F32, _p(ws), ws.numel(), None))
+    _lib.check(_lib.lib.hc_native_bn_relu_forward_dt(_p(y), n, c_out, 1, 0.1, 1e-5, _p(rm2), _p(rv2), _p(inv2), _p(xh2),
+                                                     _p(o2), _lib.HC_DTYPE_F32, _p(ws), ws.numel(), None))
+    assert _rel(rm1.cpu().numpy(), rm2.cpu().numpy()) < 1e-6
+    assert _rel(rv1.cpu().numpy(), rv2.cpu().numpy()) < 1e-6
+    assert _rel(inv1.cpu().numpy(), inv2.cpu().numpy()) < 1e-6
+    assert _rel(xh1.cpu().numpy(), xh2.cpu().numpy()) < 1e-6
+
+
+@pytest.mark.parametrize("precision", ["bf16", "f32"])
+def test_net_epilogue_stats_equals_two_pass(cuda, precision):
+    """The net step with batch-norm statistics from the conv epilogue gives the same loss,
+    gradients and running statistics as with the separate two-pass statistics kernels."""
+    from paper_1803_11385_b200.psh import PshLevel, VoxelSet, mix_seed
+    levels = []
+    s = VoxelSet.sphere(32, True)
+    cur, li = s, 0
+    while True:
+        levels.append(SuperPsh.from_levels([PshLevel.build(cur, mix_seed(3, li))] * 4))
+        if cur.resolution == 4:
+            break
+        cur = cur.coarsen()
+        li += 1
+    labels = torch.tensor([1, 0, 3, 2], device="cuda")
+    out = []
+    for epi in (True, False):
+        net = nnet.NativeHashNet(5, 4, seed=3, dropout=0.0, precision=precision)
+        net.epilogue_stats = epi
+        nb = nnet.NetBatch.build(levels)
+        gen = torch.Generator(device="cuda").manual_seed(1)
+        feats = torch.rand((3, levels[0].total_columns()), device="cuda", generator=gen)
+        x = net.input_features(feats)
+        loss, grads, fc = net.loss_and_gradients(nb, x, labels)
+        out.append((float(loss), [g.clone() for g in grads], [b["run_mean"].clone() for b in net.blocks],
+                    [b["run_var"].clone() for b in net.blocks]))
+    (l1, g1, m1, v1), (l2, g2, m2, v2) = out
+    tol = 1e-5 if precision == "f32" else 1e-3
+    assert abs(l1 - l2) <= tol * abs(l2)
+    for a, b in zip(g1, g2):
+        assert _rel(a.cpu().numpy(), b.cpu().numpy()) < tol
+    for a, b in zip(m1 + v1, m2 + v2):
+        assert _rel(a.cpu().numpy(), b.cpu().numpy()) < 1e-5
