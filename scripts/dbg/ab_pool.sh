@@ -1,4 +1,3 @@
-for v in "" poolminb6 poolminb8; do
-  if [ -n "$v" ]; then export HCB_LIB_PATH=paper_1803_11385_b200/_var/$v/libhcb200.so; fi
-  echo "== $v"; timeout 300 python scripts/kbench_ref.py 64 2>&1 | grep -E "C=" | head -12
-done
+timeout 900 python -m pytest -q -x tests/test_ops_gpu.py tests/test_net_gpu.py -p no:cacheprovider -k "pool or golden or random or kat or idempot" 2>&1 | tail -2
+for v in 1 0 1; do echo "== HCB_POOL_SEG=$v"; HCB_POOL_SEG=$v timeout 300 python scripts/kbench_ref.py 64 2>&1 | grep -E "pool"; done
+HCB_RES=512 HCB_BATCH=8 timeout 300 python scripts/kbench_ref.py 16 2>&1 | grep -E "pool"
