@@ -568,7 +568,54 @@ __global__ void __launch_bounds__(FwdX2Cfg<BN, CPS, PW, SA, SB, NBUF>::THREADS, 
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp < PW) {
+    if (warp < PW && NBUF == 0) {
+        // ---------------- producers, map entries straight from global memory (NBUF = 0): each
+        // thread loads its J entries of the next tap (2 x 16 bytes, L1-shared by the 8 threads of
+        // a row group) one tap ahead, so no shared map block is needed and its 13.5 KB become a
+        // fourth A stage
+        const int c = tid & 7;
+        const int r0 = (tid >> 3) * J;
+        uint32_t doff[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) doff[j] = sw128_offset(r0 + j, c);
+        const uint32_t row_bytes = (uint32_t)C * 2;
+        const int spt = C / BK;  // stages per tap (C >= 128: a 64-wide stage never crosses a tap)
+        int s = 0;
+        uint32_t ph = 0;
+        for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+            const int* mt = fmap + (long long)tile * taps * BM + r0;
+            int gn[J];
+#pragma unroll
+            for (int j = 0; j < J; j += 4) {
+                const int4 v = __ldg(reinterpret_cast<const int4*>(mt + j));
+                gn[j] = v.x, gn[j + 1] = v.y, gn[j + 2] = v.z, gn[j + 3] = v.w;
+            }
+            for (int t = 0; t < taps; ++t) {
+                int g[J];
+#pragma unroll
+                for (int j = 0; j < J; ++j) g[j] = gn[j];
+                if (t + 1 < taps) {
+#pragma unroll
+                    for (int j = 0; j < J; j += 4) {
+                        const int4 v = __ldg(reinterpret_cast<const int4*>(mt + (t + 1) * BM + j));
+                        gn[j] = v.x, gn[j + 1] = v.y, gn[j + 2] = v.z, gn[j + 3] = v.w;
+                    }
+                }
+                for (int k = 0; k < spt; ++k) {
+                    mbar_wait_sleep(aempty0 + 8 * s, ph ^ 1);
+                    const uint32_t A = sbase + s * Cfg::A_BYTES;
+                    const char* xs = reinterpret_cast<const char*>(X + k * BK + c * 8);
+#pragma unroll
+                    for (int j = 0; j < J; ++j) cp_async16_row(A + doff[j], xs, g[j], row_bytes);
+                    cp_async_arrive_noinc(afull0 + 8 * s);
+                    if (++s == SA) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp < PW) {
         // ---------------- producers (as k_conv_fwd: J consecutive rows x one 16-byte chunk)
         const int c = tid & 7;
         const int r0 = (tid >> 3) * J;
@@ -1436,10 +1483,12 @@ void launch_fwd_x2s(const int* fmap, int taps, long long rows, const bf16* X, in
 }
 
 // C_in a multiple of 64 (rows interleaved per 64 channels): the shared-weight-ring kernel.
-// HCB_X2_RING: 0 = the generic SUMH kernel, 1 = (A 2, B 2, 2 map buffers), 2 = (A 3, B 2, 1 map buffer).
+// HCB_X2_RING: 0 = the generic SUMH kernel, 1 = (A 2, B 2, 2 map buffers), 2 = (A 3, B 2, 1 map buffer),
+// 8 (default) = (A 4, B 2, map entries from global one tap ahead; 1-2% faster than 2 at C 64->64).
+// 3-7: deeper rings / one CTA per SM / 8 producer warps, all measured slower.
 bool conv_fwd_x2_shared(const int* fmap, int taps, long long rows, const bf16* X, int C2, const bf16* Wp, int Kp,
                         int N2, float* Y, cudaStream_t s) {
-    static const int ring = env_int("HCB_X2_RING", 2);
+    static const int ring = env_int("HCB_X2_RING", 8);
     if (ring == 0 || (C2 / 2) % 64 != 0) return false;
     if (N2 == 128) {
         if (ring == 3) launch_fwd_x2s<128, 2, 4, 2, 3, 1>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
@@ -1447,12 +1496,15 @@ bool conv_fwd_x2_shared(const int* fmap, int taps, long long rows, const bf16* X
         else if (ring == 5) launch_fwd_x2s<128, 1, 8, 8, 2, 2>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
         else if (ring == 6) launch_fwd_x2s<128, 1, 8, 9, 3, 1>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
         else if (ring == 7) launch_fwd_x2s<128, 2, 8, 3, 2, 1>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
-        else if (ring == 2) launch_fwd_x2s<128, 2, 4, 3, 2, 1>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
+        else if (ring == 8 && Kp / BK == taps * (C2 / BK))  // map from global, 4-deep A ring
+            launch_fwd_x2s<128, 2, 4, 4, 2, 0>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
+        else if (ring == 2 || ring == 8) launch_fwd_x2s<128, 2, 4, 3, 2, 1>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
         else launch_fwd_x2s<128, 2, 4, 2, 2, 2>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
         return true;
     }
     if (N2 == 64) {
-        if (ring == 2) launch_fwd_x2s<64, 2, 4, 3, 2, 1>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
+        if (ring == 8 && Kp / BK == taps * (C2 / BK)) launch_fwd_x2s<64, 2, 4, 4, 2, 0>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
+        else if (ring == 2 || ring == 8) launch_fwd_x2s<64, 2, 4, 3, 2, 1>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
         else launch_fwd_x2s<64, 2, 4, 2, 2, 2>(fmap, taps, rows, X, C2, Wp, Kp, Y, s);
         return true;
     }
