@@ -330,6 +330,31 @@ class MaterializedStep:
                 "col2hash": ("hbm", gather)}
 
 
+
+def _tile(c: int) -> int:
+    return next(t for t in (16, 32, 64, 128, 256) if c <= t)
+
+
+def _padded_operands(torch, conv, cin, cout, N, dev, g):
+    """Random reference-layout X (cin x N), W (cout x cin*27), dY (cout x N) — zero-padded to
+    the tensor-core channel tile set {16, 32, 64, 128, 256} when cin / cout are not in it (the
+    native layer's own padding, conv.HashConv): padded rows and weights are zero, so the real
+    channels' results are unchanged; the kernels then run (and are timed) at the padded sizes."""
+    cin_p, cout_p = conv._tile_channels(cin), conv._tile_channels(cout)
+    x = torch.rand((cin, N), device=dev, generator=g) * 2 - 1
+    w = torch.rand((cout, cin * 27), device=dev, generator=g) * 2 - 1
+    dy = torch.rand((cout, N), device=dev, generator=g) * 2 - 1
+    if (cin_p, cout_p) == (cin, cout):
+        return x, w, dy, cin, cout
+    xp = torch.zeros((cin_p, N), device=dev)
+    xp[:cin] = x
+    wp = torch.zeros((cout_p, cin_p * 27), device=dev)
+    wp.view(cout_p, cin_p, 27)[:cout, :cin] = w.view(cout, cin, 27)
+    dyp = torch.zeros((cout_p, N), device=dev)
+    dyp[:cout] = dy
+    return xp, wp, dyp, cin_p, cout_p
+
+
 class FusedStepF32:
     """Native path at the reference's precision (include/hashconv_b200_native.h, split
     precision): field map K0 -> fp32 X and dY split into bf16 hi/lo planes -> tcgen05
@@ -348,19 +373,17 @@ class FusedStepF32:
         from paper_1803_11385_b200 import conv, ops
         self.ops, self.conv, self.torch = ops, conv, torch
         self.fine = fine
-        self.spec = ops.ConvSpec(3, 1, 0, cin, cout)
         N = fine.total_columns()
         g = torch.Generator(device=dev).manual_seed(0)
-        # reference-layout (channel-major fp32) host-facing tensors ...
-        self.x_ref = torch.rand((cin, N), device=dev, generator=g) * 2 - 1
-        self.w = torch.rand((cout, cin * 27), device=dev, generator=g) * 2 - 1
-        self.dy_ref = torch.rand((cout, N), device=dev, generator=g) * 2 - 1
+        # reference-layout (channel-major fp32) host-facing tensors (tile-set padded) ...
+        self.x_ref, self.w, self.dy_ref, cin_p, cout_p = _padded_operands(torch, conv, cin, cout, N, dev, g)
+        self.spec = ops.ConvSpec(3, 1, 0, cin_p, cout_p)
         # ... and the native voxel-major fp32 tensors the layer consumes
         self.x = self.x_ref.t().contiguous()
         self.dy = self.dy_ref.t().contiguous()
         self.ws = conv.DwWorkspace()
         self.N, self.cin, self.cout = N, cin, cout
-        self.products = dict(self.products, dW_conv=3 if cout >= 32 else 4)  # conv_tc.cu dw_plan: tri mode
+        self.products = dict(self.products, dW_conv=3 if cout_p >= 32 else 4)  # conv_tc.cu dw_plan: tri mode
         self.op_names = ["field_map", "split_pack", "fwd_conv", "dW_conv", "dX_conv"]
 
     def _layer(self, fmap, xs, dys, w, marks, on_dw=None):
@@ -422,13 +445,11 @@ class FusedStep:
         from paper_1803_11385_b200 import conv, ops
         self.ops, self.conv, self.torch = ops, conv, torch
         self.fine = fine
-        self.spec = ops.ConvSpec(3, 1, 0, cin, cout)
         N = fine.total_columns()
         g = torch.Generator(device=dev).manual_seed(0)
-        # reference-layout (channel-major fp32) host-facing tensors ...
-        self.x_ref = torch.rand((cin, N), device=dev, generator=g) * 2 - 1
-        self.w = torch.rand((cout, cin * 27), device=dev, generator=g) * 2 - 1
-        self.dy_ref = torch.rand((cout, N), device=dev, generator=g) * 2 - 1
+        # reference-layout (channel-major fp32) host-facing tensors (tile-set padded) ...
+        self.x_ref, self.w, self.dy_ref, cin_p, cout_p = _padded_operands(torch, conv, cin, cout, N, dev, g)
+        self.spec = ops.ConvSpec(3, 1, 0, cin_p, cout_p)
         # ... and the native voxel-major bf16 operands the layer consumes
         self.x = conv.to_voxel_major(self.x_ref)
         self.dy = conv.to_voxel_major(self.dy_ref)
@@ -581,8 +602,9 @@ def main():
         hx = step.x_ref.cpu().pin_memory()
         hw = step.w.cpu().pin_memory()
         hdy = step.dy_ref.cpu().pin_memory()
-        outs = [torch.empty((args.cout, N), pin_memory=True), torch.empty((args.cout, args.cin * 27),
-                pin_memory=True), torch.empty((args.cin, N), pin_memory=True)]
+        cin_p, cout_p = step.spec.in_channels, step.spec.out_channels  # = cin / cout unless tile-padded
+        outs = [torch.empty((cout_p, N), pin_memory=True), torch.empty((cout_p, cin_p * 27), pin_memory=True),
+                torch.empty((cin_p, N), pin_memory=True)]
 
         # Pipelined across steps: H2D of step k+1 and D2H of step k-1 run on their own
         # copy streams (independent copy engines) while step k computes; NSLOT slots of
@@ -779,7 +801,9 @@ def conv_config(args, world):
     return {"workload": f"{args.res}^3 shell x {args.shapes_per_gpu}/GPU, 3x3x3 hash-conv "
                         f"{args.cin}->{args.cout} fwd+bwd (BASELINE config 4 per-GPU shard)",
             "res": args.res, "shapes_per_gpu": args.shapes_per_gpu, "global_batch": args.shapes_per_gpu * world,
-            "c_in": args.cin, "c_out": args.cout, "parallelism": f"dp{world} (shapes sharded, dW all-reduce)"}
+            "c_in": args.cin, "c_out": args.cout, "parallelism": f"dp{world} (shapes sharded, dW all-reduce)",
+            "channels_padded_to": None if (args.cin, args.cout) == (_tile(args.cin), _tile(args.cout))
+            else [_tile(args.cin), _tile(args.cout)]}
 
 
 def reference_arm(args, rank, world):
