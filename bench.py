@@ -233,6 +233,17 @@ def _level_arrays(level):
     return a
 
 
+def _all_host_threads(ref):
+    """The reference's OpenMP loops run with every host thread this process may use: torchrun
+    exports OMP_NUM_THREADS=1 to each rank, which would leave the reference single-threaded at N>1
+    (threading.cpp:24-33 set_thread_override wins over the OpenMP default)."""
+    try:
+        n = len(os.sched_getaffinity(0))
+    except AttributeError:
+        n = os.cpu_count() or 1
+    ref.lib.hcref_set_threads(int(n))
+
+
 def cpu_conv_sample(res, cin, cout, reps=1):
     """Time the reference CPU conv layer fwd+bwd (hash2col, matmul, conv_backward —
     cnn_ops.cpp:123-232) on ONE shape of the workload."""
@@ -247,6 +258,7 @@ def cpu_conv_sample(res, cin, cout, reps=1):
     spec = (3, 1, 0, cin, cout)
     if have_ref():
         ref = Ref()
+        _all_host_threads(ref)
         s = ref.super_from(arr)
         kind, cores = "reference", ref.max_threads()
 
@@ -859,6 +871,7 @@ def cpu_net_sample(res: int, b: int, classes: int):
     """The reference net's net_loss_and_gradients (net.cpp:260-323) on b shell copies."""
     from oracle.oracle import Ref
     ref = Ref()
+    _all_host_threads(ref)
     s = ref.sphere_set(res, True)
     levels, cur, i = [], s, 0
     while True:
