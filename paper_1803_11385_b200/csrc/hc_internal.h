@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "hashconv_b200.h"
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: a no-op unless a profiler injects a handler
 
 namespace hcb {
 
@@ -21,8 +22,16 @@ void set_last_error(const std::string& msg);
 // Run `f`, converting exceptions to hc_status + thread-local message. Mirrors
 // the reference's exception types: std::invalid_argument -> INVALID_ARGUMENT,
 // std::runtime_error -> RUNTIME.
+// Every ABI entry runs inside guard(), so each call is also one NVTX range named after the entry
+// point (nsys / ncu --nvtx show the operator boundaries; SURVEY.md §5 tracing).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 template <class F>
-hc_status guard(F&& f) {
+hc_status guard(F&& f, const char* fn = __builtin_FUNCTION()) {
+    const NvtxRange range(fn);
     try {
         f();
         return HC_OK;
