@@ -6,6 +6,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
 timeout 600 python bench.py --dtype bf16 --no-cpu-baseline --no-ref-kernels > gpurun_out/bench_bf16.json 2> gpurun_out/bench_bf16.err; echo "bench bf16 rc=$?"
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2>&1; echo "ref rc=$?"
+timeout 600 python bench.py --workload net --res 64 --shapes-per-gpu 32 --steps 20 > gpurun_out/bench_net64.json 2>gpurun_out/bench_net64.err; echo "net64 rc=$?"
 timeout 600 python bench.py --workload seg --cin 32 --steps 10 --no-cpu-baseline > gpurun_out/bench_seg.json 2>gpurun_out/bench_seg.err; echo "seg rc=$?"
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_f32.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-ref-kernels > /dev/null 2>&1; echo "ncu list rc=$?"
