@@ -1023,10 +1023,12 @@ def seg_main(args, rank, world, local):
     lv = shell_levels(args.res)
     b = args.shapes_per_gpu
     fine, coarse = SuperPsh.from_levels([lv[0]] * b), SuperPsh.from_levels([lv[1]] * b)
-    seg = NativeSegNet(fine, coarse, c_in=8, c=args.cin, classes=16, seed=rank)
+    seg = NativeSegNet(fine, coarse, c_in=8, c=args.cin, classes=16, seed=rank, precision=args.dtype)
     g = torch.Generator(device=dev).manual_seed(rank)
     nf = fine.total_columns()
-    x = (torch.rand((nf, 8), device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
+    x = torch.rand((nf, 8), device=dev, generator=g) * 2 - 1
+    if args.dtype == "bf16":
+        x = x.to(torch.bfloat16)
     labels = torch.randint(0, 16, (nf,), device=dev, generator=g)
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -1050,7 +1052,7 @@ def seg_main(args, rank, world, local):
         print(json.dumps({
             "metric": "segmentation train step occupied voxels/sec", "value": nf * world / (ms / 1e3),
             "unit": "voxels/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
             "data": "synthetic (sphere shells; random features and per-voxel labels)",
             "config": {"workload": f"seg encoder-decoder {args.res}^3 -> {args.res // 2}^3 -> {args.res}^3, "
                                    f"{b} shells/GPU, C={args.cin}", "res": args.res, "global_batch": b * world,

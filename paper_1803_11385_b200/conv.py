@@ -289,9 +289,15 @@ class HashDeconv:
     with the forward operand. Nothing is materialised (no column matrix, no col2hash)."""
 
     def __init__(self, coarse: SuperPsh, fine: SuperPsh, weights: torch.Tensor, spec: ConvSpec,
-                 out_dtype=torch.bfloat16):
+                 out_dtype=torch.bfloat16, precision: str = "bf16"):
+        """precision "f32": fp32 data carried as bf16 hi/lo planes through the split-precision
+        kernels (fp32 outputs within 1e-5 of float64); "bf16": bf16 operands."""
         spec = ConvSpec(*spec)
-        self.coarse, self.fine, self.spec, self.out_dtype = coarse, fine, spec, out_dtype
+        if precision not in ("bf16", "f32"):
+            raise ValueError("HashDeconv: precision must be 'bf16' or 'f32'")
+        self.f32 = precision == "f32"
+        self.coarse, self.fine, self.spec = coarse, fine, spec
+        self.out_dtype = torch.float32 if self.f32 else out_dtype
         self.taps = field_size(spec, fine.dim)
         if tuple(weights.shape) != (spec.out_channels, spec.in_channels * self.taps):
             raise ValueError("deconv_forward: weight shape mismatch")
@@ -306,12 +312,20 @@ class HashDeconv:
     def forward(self, coarse_data: torch.Tensor) -> torch.Tensor:
         """[N_coarse][C_out] bf16 -> [N_fine][C_in]   (cnn_ops.cpp:408-419)"""
         sp = self.spec
+        if self.f32:
+            wt = pack_weights_x2(self.w, sp.out_channels, sp.in_channels, self.taps, PACK_TRANSPOSE)
+            return gather_gemm_x2(self.tmap, split(coarse_data), wt, sp.in_channels)
         wt = pack_weights(self.w, sp.out_channels, sp.in_channels, self.taps, mode=PACK_TRANSPOSE)
         return gather_gemm(self.tmap, coarse_data, wt, sp.in_channels, self.out_dtype)
 
     def backward(self, fine_grad: torch.Tensor, coarse_data: torch.Tensor, d_dtype=None):
         """-> (dW [C_out][C_in*taps] fp32, dD_coarse [N_coarse][C_out])   (cnn_ops.cpp:421-435)"""
         sp = self.spec
+        if self.f32:
+            fs = split(fine_grad)
+            dw = conv_dw_x2(self.pmap, fs, split(coarse_data))
+            wf = pack_weights_x2(self.w, sp.out_channels, sp.in_channels, self.taps, PACK_FORWARD)
+            return dw, gather_gemm_x2(self.pmap, fs, wf, sp.out_channels)
         dw = conv_dw(self.pmap, fine_grad, coarse_data)
         wf = pack_weights(self.w, sp.out_channels, sp.in_channels, self.taps, mode=PACK_FORWARD)
         dd = gather_gemm(self.pmap, fine_grad, wf, sp.out_channels, d_dtype or self.out_dtype)

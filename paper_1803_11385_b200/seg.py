@@ -32,9 +32,18 @@ from .psh import SuperPsh
 
 class NativeSegNet:
     def __init__(self, fine: SuperPsh, coarse: SuperPsh, c_in: int = 8, c: int = 32, classes: int = 16,
-                 seed: int = 0, lr: float = 0.01):
+                 seed: int = 0, lr: float = 0.01, precision: str = "bf16"):
+        """precision "bf16": bf16 activations and conv operands; "f32": fp32 activations and
+        gradients, every conv / deconv through the split-precision tcgen05 kernels (the
+        reference's precision, within 1e-5 of float64 per operator)."""
         if c_in % 8 or c % 16 or classes % 16:
             raise ValueError("native seg net: c_in % 8, c % 16, classes % 16 (tensor-core tile set)")
+        if precision not in ("bf16", "f32"):
+            raise ValueError("precision must be 'bf16' or 'f32'")
+        self.f32 = precision == "f32"
+        self.adt = torch.float32 if self.f32 else BF16
+        self.adt_code = _lib.HC_DTYPE_F32 if self.f32 else _lib.HC_DTYPE_BF16
+        self._splits = {}
         self.fine, self.coarse, self.c_in, self.c, self.k, self.lr = fine, coarse, c_in, c, classes, lr
         g = torch.Generator(device="cuda").manual_seed(seed)
 
@@ -53,7 +62,8 @@ class NativeSegNet:
         self.parent = torch.empty(nf, dtype=torch.int32, device="cuda")
         self.prow = torch.empty(nf, dtype=torch.int8, device="cuda")
         check(lib.hc_native_pool_parents(_p(self.pmap), nc, 8, nf, _p(self.parent), _p(self.prow), _s()))
-        self.deconv = nconv.HashDeconv(coarse, fine, self.w["deconv"], ConvSpec(2, 2, 0, c, 2 * c), torch.float32)
+        self.deconv = nconv.HashDeconv(coarse, fine, self.w["deconv"], ConvSpec(2, 2, 0, c, 2 * c), torch.float32,
+                                       precision="f32" if self.f32 else "bf16")
         self.bn = {k: dict(mean=torch.zeros(n, device="cuda"), var=torch.ones(n, device="cuda"),
                            inv=torch.empty(n, device="cuda"))
                    for k, n in (("bn1", c), ("bn2", 2 * c), ("bn3", c))}
@@ -70,14 +80,26 @@ class NativeSegNet:
 
     def _conv(self, fmap, x, name, c_out, dtype=torch.float32):
         w = self.w[name]
+        if self.f32:  # split rows kept for the layer's dW
+            xs = self._splits[name] = nconv.split(x)
+            wf = nconv.pack_weights_x2(w, c_out, x.shape[1], 27, nconv.PACK_FORWARD)
+            return nconv.gather_gemm_x2(fmap, xs, wf, c_out)
         wf = nconv.pack_weights(w, c_out, x.shape[1], 27, False)
         return nconv.gather_gemm(fmap, x, wf, c_out, dtype)
 
     def _conv_bwd(self, fmap, x, dy, name, need_dx=True):
         w = self.w[name]
         c_out, c_in = w.shape[0], x.shape[1]
-        dw = nconv.conv_dw(fmap, x, dy, self._dw)
         dx = None
+        if self.f32:
+            xs = self._splits.pop(name, None)
+            dys = nconv.split(dy)
+            dw = nconv.conv_dw_x2(fmap, xs if xs is not None else nconv.split(x), dys, self._dw)
+            if need_dx:
+                wb = nconv.pack_weights_x2(w, c_out, c_in, 27, nconv.PACK_BACKWARD)
+                dx = nconv.gather_gemm_x2(fmap, dys, wb, c_in)
+            return dw, dx
+        dw = nconv.conv_dw(fmap, x, dy, self._dw)
         if need_dx:
             wb = nconv.pack_weights(w, c_out, c_in, 27, True)
             dx = nconv.gather_gemm(fmap, dy, wb, c_in, BF16)
@@ -87,44 +109,45 @@ class NativeSegNet:
         n, c = y.shape
         b = self.bn[name]
         xhat = torch.empty_like(y)
-        out = torch.empty((n, c), dtype=BF16, device="cuda")
+        out = torch.empty((n, c), dtype=self.adt, device="cuda")
         ws = self._bnws_for(n, c)
-        check(lib.hc_native_bn_relu_forward(_p(y), n, c, 1, 0.1, 1e-5, _p(b["mean"]), _p(b["var"]), _p(b["inv"]),
-                                            _p(xhat), _p(out), _p(ws), ws.numel(), _s()))
+        check(lib.hc_native_bn_relu_forward_dt(_p(y), n, c, 1, 0.1, 1e-5, _p(b["mean"]), _p(b["var"]), _p(b["inv"]),
+                                               _p(xhat), _p(out), self.adt_code, _p(ws), ws.numel(), _s()))
         return out, xhat
 
     def _bn_relu_bwd(self, d, dtype, xhat, name):
         n, c = xhat.shape
-        out = torch.empty((n, c), dtype=BF16, device="cuda")
+        out = torch.empty((n, c), dtype=self.adt, device="cuda")
         ws = self._bnws_for(n, c)
-        check(lib.hc_native_bn_relu_backward(_p(d), dtype, _p(xhat), _p(self.bn[name]["inv"]), n, c, _p(out), _p(ws),
-                                             ws.numel(), _s()))
+        check(lib.hc_native_bn_relu_backward_dt(_p(d), dtype, _p(xhat), _p(self.bn[name]["inv"]), n, c, _p(out),
+                                                self.adt_code, _p(ws), ws.numel(), _s()))
         return out
 
     # ------------------------------------------------------------------ step
     def step(self, x: torch.Tensor, labels: torch.Tensor, allreduce=None, world: int = 1, trace: dict = None):
-        """One training step; x [N_fine][c_in] bf16, labels [N_fine] int64. Returns the loss.
+        """One training step; x [N_fine][c_in] (bf16, or fp32 at precision f32), labels [N_fine]
+        int64. Returns the loss.
         Data parallel: `allreduce` sums the weight gradients over `world` equal shards, which
         are then averaged (the loss is the mean over all voxels of the global batch).
         `trace` (a dict) receives every layer's inputs and outputs and the weight gradients
         (before the update) for the layer-by-layer oracle comparison (tests/test_seg_parity.py)."""
         c, nc, nf = self.c, self.nc, self.nf
+        A, AC = self.adt, self.adt_code
         rec = trace.__setitem__ if trace is not None else (lambda k, v: None)
         if trace is not None:
             trace["w"] = {k: v.clone() for k, v in self.w.items()}
         # ---- encoder
         y1 = self._conv(self.fmap_f, x, "conv1", c)
         r1, h1 = self._bn_relu(y1, "bn1")
-        p1 = torch.empty((nc, c), dtype=BF16, device="cuda")
+        p1 = torch.empty((nc, c), dtype=A, device="cuda")
         sw = torch.empty((nc, c), dtype=torch.int8, device="cuda")
-        check(lib.hc_native_max_pool(_p(self.pmap), nc, 8, _p(r1), _lib.HC_DTYPE_BF16, c, _p(p1), _p(sw), _s()))
+        check(lib.hc_native_max_pool(_p(self.pmap), nc, 8, _p(r1), AC, c, _p(p1), _p(sw), _s()))
         y2 = self._conv(self.fmap_c, p1, "conv2", 2 * c)
         e2, h2 = self._bn_relu(y2, "bn2")
         # ---- decoder: unpool(conv3(e2)) + deconv(e2)
-        d3 = self._conv(self.fmap_c, e2, "conv3", c, BF16)
-        up = torch.empty((nf, c), dtype=BF16, device="cuda")
-        check(lib.hc_native_max_unpool(_p(self.parent), _p(self.prow), nf, _p(d3), _lib.HC_DTYPE_BF16, c, _p(sw),
-                                       _p(up), _s()))
+        d3 = self._conv(self.fmap_c, e2, "conv3", c, A)
+        up = torch.empty((nf, c), dtype=A, device="cuda")
+        check(lib.hc_native_max_unpool(_p(self.parent), _p(self.prow), nf, _p(d3), AC, c, _p(sw), _p(up), _s()))
         s3 = self.deconv.forward(e2)  # fp32 (the deconvolution's output dtype)
         if trace is not None:
             for k, v in dict(x=x, y1=y1, r1=r1, p1=p1, sw=sw, y2=y2, e2=e2, d3=d3, up=up, dc=s3.clone()).items():
@@ -141,15 +164,14 @@ class NativeSegNet:
         if self._neg is None or self._neg.shape[0] != nf:
             self._neg = torch.full((nf, 1), -1.0, device="cuda")
         dscores.scatter_add_(1, labels[:, None], self._neg)
-        dscores = dscores.mul_(1.0 / nf).to(BF16)
+        dscores = dscores.mul_(1.0 / nf).to(A)
         # ---- backward
         g = {}
         g["conv4"], d_r3 = self._conv_bwd(self.fmap_f, r3, dscores, "conv4")
-        d_s3 = self._bn_relu_bwd(d_r3, _lib.HC_DTYPE_BF16, h3, "bn3")          # [N_fine][C] bf16
+        d_s3 = self._bn_relu_bwd(d_r3, AC, h3, "bn3")                          # [N_fine][C]
         g["deconv"], d_e2a = self.deconv.backward(d_s3, e2)                    # deconv branch
-        d_d3 = torch.empty((nc, c), dtype=BF16, device="cuda")                  # unpool branch: adjoint =
-        check(lib.hc_native_switch_gather(_p(self.pmap), nc, 8, _p(d_s3), _lib.HC_DTYPE_BF16, c, _p(sw), _p(d_d3),
-                                          _s()))
+        d_d3 = torch.empty((nc, c), dtype=A, device="cuda")                     # unpool branch: adjoint =
+        check(lib.hc_native_switch_gather(_p(self.pmap), nc, 8, _p(d_s3), AC, c, _p(sw), _p(d_d3), _s()))
         g["conv3"], d_e2b = self._conv_bwd(self.fmap_c, e2, d_d3, "conv3")
         if trace is not None:
             for k, v in dict(dscores=dscores, d_r3=d_r3, d_s3=d_s3, d_e2a=d_e2a.clone(), d_d3=d_d3,
@@ -157,12 +179,12 @@ class NativeSegNet:
                 rec(k, v)
         d_e2 = d_e2a.float()  # fp32 already (no copy)
         d_e2.add_(d_e2b)
+        d_e2 = d_e2.contiguous()
         d_y2 = self._bn_relu_bwd(d_e2, _lib.HC_DTYPE_F32, h2, "bn2")
         g["conv2"], d_p1 = self._conv_bwd(self.fmap_c, p1, d_y2, "conv2")
-        d_r1 = torch.empty((nf, c), dtype=BF16, device="cuda")                 # pool backward = unpool
-        check(lib.hc_native_max_unpool(_p(self.parent), _p(self.prow), nf, _p(d_p1), _lib.HC_DTYPE_BF16, c, _p(sw),
-                                       _p(d_r1), _s()))
-        d_y1 = self._bn_relu_bwd(d_r1, _lib.HC_DTYPE_BF16, h1, "bn1")
+        d_r1 = torch.empty((nf, c), dtype=A, device="cuda")                    # pool backward = unpool
+        check(lib.hc_native_max_unpool(_p(self.parent), _p(self.prow), nf, _p(d_p1), AC, c, _p(sw), _p(d_r1), _s()))
+        d_y1 = self._bn_relu_bwd(d_r1, AC, h1, "bn1")
         g["conv1"], _ = self._conv_bwd(self.fmap_f, x, d_y1, "conv1", need_dx=False)
         if trace is not None:
             for k, v in dict(d_y2=d_y2, d_p1=d_p1, d_r1=d_r1, d_y1=d_y1).items():
