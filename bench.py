@@ -712,6 +712,16 @@ def main():
                 per_clk = nbytes / (kernels[name]["ms"] / 1e3) / (pk.get("sms", 148) * clk_mhz * 1e6)
                 kernels[name]["smem_bytes"] = nbytes
                 kernels[name]["smem_B_per_clk_per_sm"] = per_clk  # fills + MMA operand reads (traffic figure)
+    kpath = os.path.join(ROOT, "profiles", "ncu_kernels.json")
+    if os.path.exists(kpath):  # ncu counters of the same kernels (one --set full capture, profiles/)
+        try:
+            ncu_k = json.load(open(kpath))
+            for name in kernels:
+                src = "fwd_conv" if name == "dX_conv" else name  # dX runs the forward kernel
+                if src in ncu_k:
+                    kernels[name]["ncu"] = ncu_k[src]
+        except Exception:  # noqa: BLE001 — evidence only
+            pass
     dom = max(step.op_names, key=lambda n: per_op[step.op_names.index(n)])
     dk = kernels[dom]
     traffic = None

@@ -2,7 +2,9 @@
 
     python scripts/ncu_summary.py REPORT.ncu-rep [launches.csv] > profiles/xxx.md
 Also writes profiles/ncu_traffic.json: per bench op, DRAM bytes (read+write) per launch
-from the full capture (bench.py reads it into roofline.traffic).
+from the full capture (bench.py reads it into roofline.traffic), and profiles/ncu_kernels.json:
+per bench op, the counters that bound it (DRAM bytes, tensor pipe, the tensor core's and the
+LSU's shared-memory pipes, L2 hit rate) — bench.py attaches them to its per-kernel entries.
 """
 import csv
 import io
@@ -12,7 +14,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-OP_OF = {"k_field_map": "field_map", "k_conv_dw": "dW_conv", "k_conv_fwd": "fwd_conv",
+OP_OF = {"k_field_map": "field_map", "k_conv_dw": "dW_conv", "k_conv_fwd": "fwd_conv", "k_split_vm": "split_pack",
          "k_hash2col": "hash2col", "k_col2hash": "col2hash",
          # reference-layout contraction (gemm_tc.cu: <MMA-A MN-major, MMA-B MN-major, ...>)
          "k_gemm_tf32<1, 0": "fwd_gemm", "k_gemm_tf32<0, 0": "dW_gemm", "k_gemm_tf32<1, 1": "dcols_gemm"}
@@ -29,6 +31,12 @@ METRICS = [
     ("launch__registers_per_thread", "regs"),
     ("launch__grid_size", "grid"),
 ]
+# extra counters kept per op in ncu_kernels.json (not printed in the table)
+EXTRA = [("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "tensor_pipe_pct"),
+         ("l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "tc_smem_pipe_pct"),
+         ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "lsu_smem_pipe_pct"),
+         ("lts__t_sector_hit_rate.pct", "l2_hit_pct"),
+         ("sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.sum", "bf16_mma_flop")]
 
 
 def scale(v, unit):
@@ -47,6 +55,7 @@ def main():
     print("| kernel | " + " | ".join(name for _, name in METRICS) + " |")
     print("|---" * (len(METRICS) + 1) + "|")
     traffic = {}
+    counters = {}
     for d in data:
         name = d[hdr.index("Kernel Name")].split("(")[0].replace("void ", "").replace("(anonymous namespace)::", "")
         name = name.replace("unnamed>::", "").strip()
@@ -75,6 +84,16 @@ def main():
         for k, op in OP_OF.items():
             if k in name and "DRAM read" in vals:
                 traffic.setdefault(op, vals["DRAM read"] * 1e6 + vals.get("DRAM write", 0) * 1e6)
+                if op not in counters:
+                    c = {"kernel": name[:80], "time_ms": vals.get("time"),
+                         "dram_bytes": vals["DRAM read"] * 1e6 + vals.get("DRAM write", 0) * 1e6}
+                    for m, key in EXTRA:
+                        if m in hdr:
+                            try:
+                                c[key] = float(d[hdr.index(m)])
+                            except ValueError:
+                                pass
+                    counters[op] = c
     if len(sys.argv) > 2:
         print("\n### launch list (cold, serialised — compare shares, not absolutes)\n")
         txt = open(sys.argv[2]).read()
@@ -100,6 +119,10 @@ def main():
     merged = json.load(open(path)) if os.path.exists(path) else {}
     merged.update(traffic)  # captures of other workloads keep their entries
     json.dump(merged, open(path, "w"), indent=1)
+    kpath = os.path.join(ROOT, "profiles", "ncu_kernels.json")
+    kmerged = json.load(open(kpath)) if os.path.exists(kpath) else {}
+    kmerged.update(counters)
+    json.dump(kmerged, open(kpath, "w"), indent=1)
 
 
 if __name__ == "__main__":
