@@ -9,7 +9,7 @@ reference layout W[co][ci*F^3 + t] (cnn_ops.hpp:21-27).
 from __future__ import annotations
 
 import ctypes as C
-from typing import NamedTuple
+from typing import NamedTuple, Optional
 
 import numpy as np
 import torch
@@ -175,27 +175,38 @@ def conv_dw(fmap, x: torch.Tensor, dy: torch.Tensor, ws: DwWorkspace = None) -> 
 
 
 class HashConv:
-    """One hash-conv layer (stride 1, odd F) in the native layout.
+    """One hash-conv layer in the native layout.
 
     forward(x) -> y          : conv_forward (cnn_ops.cpp:206-215)
-    backward(dy, x) -> dw, dx: conv_backward (cnn_ops.cpp:217-232); dx via the flipped
-                               transposed kernel on the same field map (stride 1)
+    backward(dy, x) -> dw, dx: conv_backward (cnn_ops.cpp:217-232). Stride 1 (same structure):
+                               dx via the flipped transposed kernel on the same field map.
+                               Strided (output = a coarser structure): dx is the gather-GEMM
+                               over the TRANSPOSED field map (fine voxel, tap -> the coarse voxel
+                               whose field holds it), the col2hash of cnn_ops.cpp:229-231 without
+                               a column matrix.
     """
 
     def __init__(self, structure: SuperPsh, weights: torch.Tensor, spec: ConvSpec, out_dtype=torch.bfloat16,
-                 precision: str = "bf16"):
+                 precision: str = "bf16", output: Optional[SuperPsh] = None):
         """precision "bf16": bf16 operands (features voxel-major bf16), fp32 accumulation;
         "f32": fp32 features and weights carried as bf16 hi/lo planes (hc_native_*_x2),
-        fp32 outputs within 1e-5 of the float64 reference — the reference's own precision."""
+        fp32 outputs within 1e-5 of the float64 reference — the reference's own precision.
+        output: the output structure of a strided conv (e.g. the next-coarser level for
+        stride 2; cnn_ops.cpp:20-33 check_pair); None = `structure` (stride 1)."""
         spec = ConvSpec(*spec)
-        if spec.stride != 1:
-            raise ValueError("HashConv native layer: stride-1 convolution (use ops.* for strided)")
         if precision not in ("bf16", "f32"):
             raise ValueError("HashConv: precision must be 'bf16' or 'f32'")
+        if spec.stride != 1 and output is None:
+            raise ValueError("HashConv: a strided conv needs its output structure (output=...)")
         self.precision = precision
         self.s, self.spec = structure, spec
+        self.out = output if output is not None else structure
+        self.strided = output is not None and (spec.stride != 1 or output is not structure)
         self.out_dtype = torch.float32 if precision == "f32" else out_dtype
         self.taps = field_size(spec, structure.dim)
+        if self.taps > 27:
+            raise ValueError("native conv: at most 27 field taps (3x3x3)")
+        self.tmap = None
         # any channel counts (the reference takes e.g. 3 -> 2): the tensor-core tile set is
         # {16, 32, 64, 128, 256} channels, so both sides are zero-padded to it; padded weight
         # rows/columns are zero, so the padded outputs and gradients are exactly zero
@@ -216,16 +227,26 @@ class HashConv:
             wp = torch.zeros((self.cout_p, self.cin_p * self.taps), dtype=w.dtype, device=w.device)
             wp.view(self.cout_p, self.cin_p, self.taps)[:sp.out_channels, :sp.in_channels] = \
                 w.view(sp.out_channels, sp.in_channels, self.taps)
+        # dX operand: the flipped kernel on the same map (stride 1), or the unflipped transpose on
+        # the transposed map (strided)
+        back = PACK_TRANSPOSE if self.strided else PACK_BACKWARD
         if self.precision == "f32":
             self.wf = pack_weights_x2(wp, self.cout_p, self.cin_p, self.taps, PACK_FORWARD)
-            self.wb = pack_weights_x2(wp, self.cout_p, self.cin_p, self.taps, PACK_BACKWARD)
+            self.wb = pack_weights_x2(wp, self.cout_p, self.cin_p, self.taps, back)
         else:
             self.wf = pack_weights(wp, self.cout_p, self.cin_p, self.taps, False)
-            self.wb = pack_weights(wp, self.cout_p, self.cin_p, self.taps, True)
+            self.wb = pack_weights(wp, self.cout_p, self.cin_p, self.taps, mode=back)
 
     def build_map(self) -> FieldMap:
-        """K0 in the tile-major layout (coalesced build; one bulk copy per tile in the GEMM)."""
-        self.fmap = field_map_native(self.s, self.s, self.spec, TILED)
+        """K0 in the tile-major layout (coalesced build; one bulk copy per tile in the GEMM);
+        strided: also its transpose (input voxel, tap -> output voxel) for the input gradient."""
+        self.fmap = field_map_native(self.s, self.out, self.spec, TILED)
+        if self.strided:
+            rows = field_map(self.s, self.out, self.spec)  # same map, row-major [n_out][taps]
+            n_in = self.s.total_columns()
+            tm = torch.empty(((n_in + 127) // 128, self.taps, 128), dtype=torch.int32, device=rows.device)
+            check(lib.hc_native_transpose_map(_p(rows), rows.shape[0], self.taps, n_in, _p(tm), _s()))
+            self.tmap = FieldMap(tm, n_in, self.taps, TILED)
         return self.fmap
 
     @staticmethod
@@ -258,7 +279,7 @@ class HashConv:
             if (self.cin_p, self.cout_p) != (sp.in_channels, sp.out_channels):
                 dw = dw.view(self.cout_p, self.cin_p, self.taps)[:sp.out_channels, :sp.in_channels].reshape(
                     sp.out_channels, sp.in_channels * self.taps)
-            dx = gather_gemm_x2(self.fmap, dys, self.wb, self.cin_p)
+            dx = gather_gemm_x2(self.tmap if self.strided else self.fmap, dys, self.wb, self.cin_p)
             if self.cin_p != sp.in_channels:
                 dx = dx[:, :sp.in_channels].contiguous()
             return dw, dx
@@ -267,7 +288,7 @@ class HashConv:
         if (self.cin_p, self.cout_p) != (sp.in_channels, sp.out_channels):
             dw = dw.view(self.cout_p, self.cin_p, self.taps)[:sp.out_channels, :sp.in_channels].reshape(
                 sp.out_channels, sp.in_channels * self.taps)
-        dx = gather_gemm(self.fmap, dyp, self.wb, self.cin_p, dx_dtype or self.out_dtype)
+        dx = gather_gemm(self.tmap if self.strided else self.fmap, dyp, self.wb, self.cin_p, dx_dtype or self.out_dtype)
         if self.cin_p != sp.in_channels:
             dx = dx[:, :sp.in_channels].contiguous()
         return dw, dx

@@ -284,3 +284,42 @@ def test_dw_plan_rejects_shapes_beyond_tmem(cuda):
     fmap = torch.zeros((64, 27), dtype=torch.int32, device="cuda")
     with pytest.raises(ValueError, match="dW supports at most"):
         nconv.conv_dw(fmap, x, dy)
+
+
+@pytest.mark.parametrize("precision", ["bf16", "f32"])
+@pytest.mark.parametrize("kernel,stride,pad", [(2, 2, 0), (3, 2, 0), (3, 2, 1)])
+def test_strided_layer_vs_oracle(cuda, restated, precision, kernel, stride, pad):
+    """Strided native layer (fine -> next-coarser structure): forward over the strided field map,
+    dW by the split-K kernel on it, dX by the gather-GEMM over the TRANSPOSED map (cnn_ops.cpp:
+    217-232 col2hash without a column matrix) vs the double oracle; bf16 on quantised operands,
+    f32 on unquantised fp32 inputs (split precision), both within 1e-5 (dW 5e-5 at bf16)."""
+    from helpers import random_pair
+    f, c = random_pair(32, 3, seed=kernel * 10 + pad, n_lo=900, n_hi=2500)
+    fa, ca = levels_to_arrays(f), levels_to_arrays(c)
+    fine, coarse = SuperPsh.from_levels(f), SuperPsh.from_levels(c)
+    nf, nc = fine.total_columns(), coarse.total_columns()
+    c_in, c_out = 32, 64
+    rng = np.random.default_rng(kernel + pad)
+    q = (lambda a: torch.from_numpy(a).to(torch.bfloat16).float().numpy()) if precision == "bf16" else (lambda a: a)
+    x = q(rng.uniform(-1, 1, (c_in, nf)).astype(np.float32))
+    taps = kernel ** 3
+    w = q(rng.uniform(-1, 1, (c_out, c_in * taps)).astype(np.float32))
+    dy = q(rng.uniform(-1, 1, (c_out, nc)).astype(np.float32))
+    spec = ConvSpec(kernel, stride, pad, c_in, c_out)
+    f64 = np.float64
+    cols64 = restated.hash2col(fa, x.astype(f64), ca, spec, f64)
+    y64 = restated.matmul(w.astype(f64), cols64, f64)
+    dw64, dx64 = restated.conv_backward(dy.astype(f64), w.astype(f64), cols64, fa, ca, spec, f64)
+    layer = nconv.HashConv(fine, torch.from_numpy(w).cuda(), spec, out_dtype=torch.float32, precision=precision,
+                           output=coarse)
+    if precision == "f32":
+        xv, dyv = torch.from_numpy(x).cuda().t().contiguous(), torch.from_numpy(dy).cuda().t().contiguous()
+    else:
+        xv, dyv = nconv.to_voxel_major(torch.from_numpy(x).cuda()), nconv.to_voxel_major(torch.from_numpy(dy).cuda())
+    y = layer.forward(xv).float().t().cpu().numpy()
+    dw, dxv = layer.backward(dyv, xv, torch.float32)
+    dx = dxv.float().t().cpu().numpy()
+    assert y.shape == (c_out, nc) and dx.shape == (c_in, nf)
+    assert rel(torch.from_numpy(y), torch.from_numpy(y64)) <= TOL_F32_OUT
+    assert rel(dw.cpu(), torch.from_numpy(dw64)) <= (TOL_DW if precision == "bf16" else 1e-5)
+    assert rel(torch.from_numpy(dx), torch.from_numpy(dx64)) <= TOL_F32_OUT
