@@ -653,7 +653,7 @@ def main():
         comp.wait_stream(d2h_s)
         barrier()
         es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ke = max(20, args.steps)  # long enough that pipeline fill / drain amortise
+        ke = max(50, args.steps)  # long enough that pipeline fill / drain amortise (~1 step of 50)
         es.record(comp)
         for k in range(ke):
             e2e_step(k)
