@@ -1208,8 +1208,19 @@ __device__ __forceinline__ float split_lane_sum(const float* __restrict__ partia
     const float* p = partial + grp_tab.part_begin[g] + ((long long)(mtile - grp_tab.m_begin[g]) * rpm + row) * pc + n;
     const long long stride = (long long)nm * rpm * pc;
     float acc = 0.0f;
-#pragma unroll 4
-    for (int s = j; s < splits; s += 8) acc += p[s * stride];
+#ifndef HCB_REDUCE_UNROLL
+#define HCB_REDUCE_UNROLL 8
+#endif
+    constexpr int U = HCB_REDUCE_UNROLL;  // loads in flight per lane (the sum order is unchanged)
+    int s = j;
+    for (; s + 8 * (U - 1) < splits; s += 8 * U) {
+        float v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = p[(long long)(s + 8 * u) * stride];
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc += v[u];
+    }
+    for (; s < splits; s += 8) acc += p[(long long)s * stride];
     return acc;
 }
 
