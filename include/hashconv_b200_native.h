@@ -68,6 +68,10 @@ hc_status hc_native_split(const float* src, int32_t channel_major, int64_t c, in
 /* Same modes as hc_native_pack_weights; w_packed: bf16 [2*rows][hc_native_packed_k_x2(...)]. */
 hc_status hc_native_pack_weights_x2(const float* w_ref, int32_t c_out, int32_t c_in, int32_t taps,
                                     int32_t mode, void* w_packed, hc_stream stream);
+/* Both split operands of one layer in one launch: forward (mode 0) into w_fwd and flipped dX
+ * (mode 1) into w_bwd, the latter zero-padded to c_in_bwd >= c_in rows (a multiple of 8). */
+hc_status hc_native_pack_weights_x2_fb(const float* w_ref, int32_t c_out, int32_t c_in, int32_t taps,
+                                       int32_t c_in_bwd, void* w_fwd, void* w_bwd, hc_stream stream);
 /* The forward with batch-norm statistics from the epilogue: besides y, per
  * 128-row tile of the output and output channel, tile_stats[(tile * c_out + co) * 2 + {0, 1}] =
  * {sum, sum of squares about the tile mean} of the fp32 values (rows >= n_out excluded);
@@ -188,6 +192,10 @@ hc_status hc_native_dense_pool_dt(const int32_t* cmap, int32_t b, const void* x,
 hc_status hc_native_dense_pool_backward(const float* d_head, const int32_t* src, int32_t b, int32_t c,
                                         int64_t n_fine, float* dx, hc_stream stream);
 /* SGD with momentum and weight decay (net.cpp:339-346): v = momentum*v + lr*(g + wd*w); w -= v. */
+/* The same update for `count` (<= 32) tensors in one launch (host arrays of device pointers / sizes). */
+hc_status hc_native_sgd_update_multi(float* const* w, float* const* v, const float* const* g, const int64_t* n,
+                                     int32_t count, float lr, float momentum, float weight_decay,
+                                     hc_stream stream);
 hc_status hc_native_sgd_update(float* w, float* v, const float* g, int64_t n, float lr, float momentum,
                                float weight_decay, hc_stream stream);
 

@@ -157,8 +157,10 @@ _SIGS.update({
     "hc_native_bn_relu_backward_apply_dt": [_P, C.c_int, _P, _P, _I64, _I32, _P, _P, _I64, _P, C.c_int, _P],
     "hc_native_dense_pool_backward": [_P, _P, _I32, _I32, _I64, _P, _P],
     "hc_native_sgd_update": [_P, _P, _P, _I64, C.c_float, C.c_float, C.c_float, _P],
+    "hc_native_sgd_update_multi": [_P, _P, _P, _P, _I32, C.c_float, C.c_float, C.c_float, _P],
     "hc_native_split": [_P, _I32, _I64, _I64, _P, _P],
     "hc_native_pack_weights_x2": [_P, _I32, _I32, _I32, _I32, _P, _P],
+    "hc_native_pack_weights_x2_fb": [_P, _I32, _I32, _I32, _I32, _P, _P, _P],
     "hc_native_gather_gemm_x2": [_P, _I32, _I64, _I32, _P, _I32, _P, _I32, _P, _P],
     "hc_native_conv_dw_x2": [_P, _I32, _I64, _I32, _P, _I32, _P, _I32, _P, _P, C.c_size_t, _P],
 })

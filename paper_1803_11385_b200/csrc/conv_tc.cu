@@ -1900,6 +1900,46 @@ hc_status hc_native_split(const float* src, int32_t channel_major, int64_t c, in
     });
 }
 
+// Forward and flipped (dX) operands of one layer in one launch (blockIdx.y selects the mode);
+// the dX operand may be zero-padded to c_in_bwd >= c_in input channels (the tile set starts at 16).
+__global__ void k_pack_w_x2_fb(const float* __restrict__ w, int cout, int cin, int taps, int Kf, int Kb, int cin_bwd,
+                               bf16* __restrict__ wf, bf16* __restrict__ wb) {
+    const bool b = blockIdx.y == 1;
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const int rows = b ? cin_bwd : cout;
+    const int Kp2 = b ? Kb : Kf;
+    if (i >= 2LL * rows * Kp2) return;
+    const int rr = (int)(i / Kp2), k = (int)(i % Kp2);
+    const int q = rr >= rows, r = rr - q * rows;
+    const int ck = b ? cout : cin;  // K-side channels of this operand
+    const int g = x2_block(ck);
+    float v = 0.0f;
+    if (k < taps * 2 * ck) {
+        const int t = k / (2 * ck);
+        const int kr = k - t * 2 * ck;
+        const int c = (kr / (2 * g)) * g + kr % g;
+        const int co = b ? c : r, ci = b ? r : c;
+        if (co < cout && ci < cin) v = w[(long long)co * cin * taps + ci * taps + (b ? taps - 1 - t : t)];
+    }
+    bf16 hi, lo;
+    split2(v, hi, lo);
+    (b ? wb : wf)[i] = q ? lo : hi;
+}
+
+hc_status hc_native_pack_weights_x2_fb(const float* w_ref, int32_t c_out, int32_t c_in, int32_t taps,
+                                       int32_t c_in_bwd, void* w_fwd, void* w_bwd, hc_stream stream) {
+    return guard([&] {
+        check_native(c_in, c_out, taps);
+        if (c_in_bwd < c_in || c_in_bwd % 8) throw std::invalid_argument("native conv: c_in_bwd must be >= c_in, % 8");
+        const long long Kf = hc_native_packed_k_x2(c_in, taps), Kb = hc_native_packed_k_x2(c_out, taps);
+        const long long n = std::max(2LL * c_out * Kf, 2LL * c_in_bwd * Kb);
+        const dim3 grid((unsigned)grid_for(n, 256), 2);
+        k_pack_w_x2_fb<<<grid, 256, 0, as_stream(stream)>>>(w_ref, c_out, c_in, taps, (int)Kf, (int)Kb, c_in_bwd,
+                                                            static_cast<bf16*>(w_fwd), static_cast<bf16*>(w_bwd));
+        launched("pack weights fwd + dX (split precision)");
+    });
+}
+
 hc_status hc_native_pack_weights_x2(const float* w_ref, int32_t c_out, int32_t c_in, int32_t taps, int32_t mode,
                                     void* w_packed, hc_stream stream) {
     return guard([&] {

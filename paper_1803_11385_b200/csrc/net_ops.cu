@@ -462,6 +462,31 @@ __global__ void k_dense_pool_bwd(const float* __restrict__ dhead, const int* __r
 
 // net.cpp:339-346 sgd_update: v = momentum*v + lr*(g + wd*w); w -= v (separate fp32
 // roundings, as the reference's non-FMA build).
+// Multi-tensor SGD: up to kSgdMax (w, v, g, n) tensors in one launch (a training step updates every
+// conv and FC tensor; one launch instead of one per tensor). Tensor k owns blocks
+// [first[k], first[k+1]); the per-element arithmetic is k_sgd's.
+constexpr int kSgdMax = 32;
+struct SgdList {
+    float* w[kSgdMax];
+    float* v[kSgdMax];
+    const float* g[kSgdMax];
+    long long n[kSgdMax];
+    int first[kSgdMax + 1];
+    int count;
+};
+
+__global__ void __launch_bounds__(kT) k_sgd_multi(const SgdList L, float lr, float momentum, float wd) {
+    int k = 0;
+    while (k + 1 < L.count && (int)blockIdx.x >= L.first[k + 1]) ++k;
+    const long long i = (long long)(blockIdx.x - L.first[k]) * blockDim.x + threadIdx.x;
+    if (i >= L.n[k]) return;
+    float* w = L.w[k];
+    float* v = L.v[k];
+    const float vi = __fadd_rn(__fmul_rn(momentum, v[i]), __fmul_rn(lr, __fadd_rn(L.g[k][i], __fmul_rn(wd, w[i]))));
+    v[i] = vi;
+    w[i] = __fsub_rn(w[i], vi);
+}
+
 __global__ void k_sgd(float* __restrict__ w, float* __restrict__ v, const float* __restrict__ g, long long n, float lr,
                       float momentum, float wd) {
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -809,6 +834,29 @@ hc_status hc_native_dense_pool_backward(const float* d_head, const int32_t* src,
         const int n = c * 8 * b;
         k_dense_pool_bwd<<<grid_for(n, kT), kT, 0, s>>>(d_head, src, b, c, dx);
         launched("dense pool backward");
+    });
+}
+
+hc_status hc_native_sgd_update_multi(float* const* w, float* const* v, const float* const* g, const int64_t* n,
+                                     int32_t count, float lr, float momentum, float weight_decay, hc_stream stream) {
+    return guard([&] {
+        if (count < 0 || count > kSgdMax) throw std::invalid_argument("native sgd: 0..32 tensors per call");
+        SgdList L{};
+        L.count = count;
+        int blocks = 0;
+        for (int k = 0; k < count; ++k) {
+            if (n[k] < 0) throw std::invalid_argument("native sgd: negative tensor size");
+            L.w[k] = w[k];
+            L.v[k] = v[k];
+            L.g[k] = g[k];
+            L.n[k] = n[k];
+            L.first[k] = blocks;
+            blocks += (int)((n[k] + kT - 1) / kT);
+        }
+        L.first[count] = blocks;
+        if (blocks == 0) return;
+        k_sgd_multi<<<blocks, kT, 0, as_stream(stream)>>>(L, lr, momentum, weight_decay);
+        launched("sgd update (multi-tensor)");
     });
 }
 

@@ -169,6 +169,7 @@ class NativeHashNet:
         self.head_v = [torch.zeros_like(t) for t in (self.fc1_w, self.fc1_b, self.fc2_w, self.fc2_b)]
         self._ws = {}
         self._dw_ws = nconv.DwWorkspace()
+        self._wb = {}  # f32: dX weight operands packed in the forward pass
         self._seed = seed + 1
         self._gen = None  # dropout masks: a private generator in eager mode, the default one in graphs
 
@@ -259,7 +260,14 @@ class NativeHashNet:
         y = torch.empty((n, co), dtype=torch.float32, device="cuda")
         if self.f32:
             xs = nconv.split(x)
-            wf = nconv.pack_weights_x2(blk["w"], co, blk["cin_p"], 27, nconv.PACK_FORWARD)
+            # forward and dX operands in one launch; the dX one is kept for the backward pass (the
+            # tensor-core tile set starts at 16 output channels: an 8-channel input level takes its
+            # gradient through a zero-padded 16-channel kernel)
+            cin_g = max(16, blk["cin_p"])
+            wf = torch.empty((2 * co, int(lib.hc_native_packed_k_x2(blk["cin_p"], 27))), dtype=BF16, device="cuda")
+            wb = torch.empty((2 * cin_g, int(lib.hc_native_packed_k_x2(co, 27))), dtype=BF16, device="cuda")
+            check(lib.hc_native_pack_weights_x2_fb(_p(blk["w"]), co, blk["cin_p"], 27, cin_g, _p(wf), _p(wb), _s()))
+            self._wb[i] = wb
             check(lib.hc_native_gather_gemm_x2_stats(_p(fm.data), fm.layout, n, fm.taps, _p(xs), blk["cin_p"], _p(wf),
                                                      co, _p(y), _p(stats) if stats is not None else None, _s()))
             return y, xs
@@ -393,14 +401,13 @@ class NativeHashNet:
             # The tensor-core tile set starts at 16 output channels: an 8-channel input level
             # takes its gradient through a zero-padded 16-channel kernel.
             cin_g = max(16, blk["cin_p"])
-            w = blk["w"]
-            if cin_g != blk["cin_p"]:
-                w = torch.zeros((blk["cout_p"], cin_g * 27), device="cuda")
-                w.view(blk["cout_p"], cin_g, 27)[:, :blk["cin_p"]] = blk["w"].view(blk["cout_p"], blk["cin_p"], 27)
-            if self.f32:
-                wb = nconv.pack_weights_x2(w, blk["cout_p"], cin_g, 27, nconv.PACK_BACKWARD)
-                dx = nconv.gather_gemm_x2(nb.conv_maps[i], d_conv_s, wb, cin_g)[:, :blk["cin_p"]]
+            if self.f32:  # the operand packed with the forward one (_conv_forward)
+                dx = nconv.gather_gemm_x2(nb.conv_maps[i], d_conv_s, self._wb.pop(i), cin_g)[:, :blk["cin_p"]]
             else:
+                w = blk["w"]
+                if cin_g != blk["cin_p"]:
+                    w = torch.zeros((blk["cout_p"], cin_g * 27), device="cuda")
+                    w.view(blk["cout_p"], cin_g, 27)[:, :blk["cin_p"]] = blk["w"].view(blk["cout_p"], blk["cin_p"], 27)
                 wb = nconv.pack_weights(w, blk["cout_p"], cin_g, 27, True)
                 dx = nconv.gather_gemm(nb.conv_maps[i], d_conv, wb, cin_g, BF16)[:, :blk["cin_p"]]
             if trace is not None:
@@ -424,11 +431,15 @@ class NativeHashNet:
         head_grads = [g.contiguous() for g in head_grads]  # the tensors reduced ARE the ones applied
         if allreduce is not None:
             allreduce(list(conv_grads) + head_grads)
-        for blk, g in zip(self.blocks, conv_grads):
-            check(lib.hc_native_sgd_update(_p(blk["w"]), _p(blk["v"]), _p(g), g.numel(), self.lr, self.momentum,
-                                           self.wd, _s()))
-        for w, v, g in zip((self.fc1_w, self.fc1_b, self.fc2_w, self.fc2_b), self.head_v, head_grads):
-            check(lib.hc_native_sgd_update(_p(w), _p(v), _p(g), g.numel(), self.lr, self.momentum, self.wd, _s()))
+        # every conv and FC tensor in one multi-tensor launch (net.cpp:339-346 per tensor)
+        ws = [blk["w"] for blk in self.blocks] + [self.fc1_w, self.fc1_b, self.fc2_w, self.fc2_b]
+        vs = [blk["v"] for blk in self.blocks] + list(self.head_v)
+        gs = list(conv_grads) + list(head_grads)
+        k = len(ws)
+        arr = lambda ts: (C.c_void_p * k)(*[t.data_ptr() for t in ts])  # noqa: E731
+        ns = (C.c_int64 * k)(*[t.numel() for t in ws])
+        check(lib.hc_native_sgd_update_multi(arr(ws), arr(vs), arr(gs), ns, k, self.lr, self.momentum, self.wd,
+                                             _s()))
         return loss
 
 
