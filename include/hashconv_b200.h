@@ -49,7 +49,10 @@ typedef enum {
 } hc_status;
 
 typedef enum { HC_MATH_EXACT = 0, HC_MATH_FAST = 1, HC_MATH_TF32 = 2 } hc_math;
-typedef enum { HC_DTYPE_F32 = 0, HC_DTYPE_BF16 = 1 } hc_dtype;
+/* HC_DTYPE_SPLIT (outputs of some native layers only): fp32 values written as the split-precision
+ * rows the x2 conv kernels consume — bf16 [N][2C], hi = rn(v), lo = rn(v - hi), hi and lo planes
+ * interleaved per 64 channels (hc_native_split's layout). */
+typedef enum { HC_DTYPE_F32 = 0, HC_DTYPE_BF16 = 1, HC_DTYPE_SPLIT = 2 } hc_dtype;
 
 /* Thread-local text of the last error (exact reference message for 1/2). */
 const char* hc_last_error(void);

@@ -23,7 +23,7 @@ lib = C.CDLL(LIB_PATH)
 
 HC_OK, HC_ERR_INVALID_ARGUMENT, HC_ERR_RUNTIME, HC_ERR_CUDA = 0, 1, 2, 3
 HC_MATH_EXACT, HC_MATH_FAST, HC_MATH_TF32 = 0, 1, 2
-HC_DTYPE_F32, HC_DTYPE_BF16 = 0, 1
+HC_DTYPE_F32, HC_DTYPE_BF16, HC_DTYPE_SPLIT = 0, 1, 2
 
 
 class HashConvCudaError(RuntimeError):

@@ -44,6 +44,7 @@
 #include "hashconv_b200_native.h"
 #include "hc_internal.h"
 #include "hc_launch.cuh"
+#include "x2_layout.cuh"
 #include "tc_common.cuh"
 #include "tma_host.h"
 
@@ -65,12 +66,8 @@ constexpr int BK = 64;   // K elements (bf16) per stage = one 128-byte row
 constexpr int kMaxTaps = 27;
 constexpr int kNbrBytes = kMaxTaps * BM * 4;  // 13.5 KB field-map block per tile
 
-// Split-row layout: the planes interleave in blocks of g channels, g = 64 when the plane's
-// channel count is a multiple of 64 (else g = C, i.e. [hi | lo]): channel c of plane p sits at
-// (c / g) * 2g + p * g + c % g, so a 64-wide K stage holds one plane of 64 channels and its hi
-// and lo stages are adjacent (k_conv_fwd_x2 shares their weight tile).
-__host__ __device__ __forceinline__ int x2_block(int C) { return C % 64 == 0 ? 64 : C; }
-__host__ __device__ __forceinline__ int x2_pos(int c, int p, int g) { return (c / g) * 2 * g + p * g + c % g; }
+// Split-row layout (x2_layout.cuh: x2_block, x2_pos, split2): a 64-wide K stage holds one plane of
+// 64 channels and its hi and lo stages are adjacent (k_conv_fwd_x2 shares their weight tile).
 
 __host__ __device__ constexpr int tmem_cols(int n) {
     return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512;
@@ -1298,10 +1295,6 @@ __global__ void k_pack_w(const float* __restrict__ w, int cout, int cin, int tap
 
 // Split precision: an fp32 value v is carried as two bf16 planes hi = rn(v), lo = rn(v - hi)
 // (|v - hi - lo| <= 2^-17 |v|); the products hi.hi + hi.lo + lo.hi (+ lo.lo) accumulate in fp32.
-__device__ __forceinline__ void split2(float v, bf16& hi, bf16& lo) {
-    hi = __float2bfloat16_rn(v);
-    lo = __float2bfloat16_rn(v - __bfloat162float(hi));
-}
 
 // Weights in the split layout: rows [0, R) the hi plane, [R, 2R) the lo plane of the mode's
 // matrix (as k_pack_w); each tap's K segment is [hi features | lo features] (2 Ck wide) with

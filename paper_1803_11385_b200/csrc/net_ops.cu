@@ -23,6 +23,7 @@
 #include "hashconv_b200_native.h"
 #include "hc_internal.h"
 #include "hc_launch.cuh"
+#include "x2_layout.cuh"
 
 namespace hcb {
 namespace {
@@ -71,9 +72,11 @@ __global__ void k_pool_parents(const int* __restrict__ pmap, long long nc, int f
 
 // cnn_ops.cpp:234-284: per channel, the first present field row seeds the max and a
 // later row replaces it only if strictly greater; an empty field gives 0 and switch -1.
-template <typename T, int FD>
+// OT: the output element type (T, or bf16 with SPLIT: the split-precision rows [nc][2C] the next
+// conv consumes, so no separate split pass).
+template <typename T, int FD, typename OT = T, bool SPLIT = false>
 __global__ void __launch_bounds__(kT) k_nmax_pool(const int* __restrict__ pmap, long long nc, const T* __restrict__ x,
-                                                 int C, T* __restrict__ y, signed char* __restrict__ sw) {
+                                                 int C, OT* __restrict__ y, signed char* __restrict__ sw) {
     const int chunks = C >> 3;
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // over nc * chunks
     if (i >= nc * chunks) return;
@@ -99,7 +102,8 @@ __global__ void __launch_bounds__(kT) k_nmax_pool(const int* __restrict__ pmap, 
                 arg[e] = t;
             }
     }
-    store8(y + p * C + c0, best);
+    if constexpr (SPLIT) store8_split(y + p * 2 * C, c0, C, best);
+    else store8(y + p * C + c0, best);
     char4 s0 = make_char4(arg[0], arg[1], arg[2], arg[3]), s1 = make_char4(arg[4], arg[5], arg[6], arg[7]);
     *reinterpret_cast<int2*>(sw + p * C + c0) = make_int2(*reinterpret_cast<int*>(&s0), *reinterpret_cast<int*>(&s1));
 }
@@ -396,7 +400,7 @@ __global__ void __launch_bounds__(kT) k_bn_relu_infer(const float* __restrict__ 
 
 // dx = inv_std * (dyb - s1/n - xhat * s2/n), dyb = dy * (xhat > 0)  (cnn_ops.cpp:476-489
 // after relu_backward cnn_ops.cpp:553-561); bf16 out = the conv layer's output gradient.
-template <typename DT, typename OT>
+template <typename DT, typename OT, bool SPLIT = false>
 __global__ void __launch_bounds__(kT) k_bn_relu_bwd_apply(const DT* __restrict__ dy, const float* __restrict__ xhat,
                                                          long long n, int C, const double* __restrict__ s1,
                                                          const double* __restrict__ s2,
@@ -416,7 +420,8 @@ __global__ void __launch_bounds__(kT) k_bn_relu_bwd_apply(const DT* __restrict__
         const double g = h[e] > 0.0f ? (double)d[e] : 0.0;
         o[e] = (float)((double)inv_std[c0 + e] * (g - s1[c0 + e] * inv_n - (double)h[e] * s2[c0 + e] * inv_n));
     }
-    store8(dx + row * C + c0, o);
+    if constexpr (SPLIT) store8_split(dx + row * 2 * C, c0, C, o);
+    else store8(dx + row * C + c0, o);
 }
 
 // ---------------------------------------------------------------------- final dense pool
@@ -503,6 +508,11 @@ void check_c8(int c) {
 void check_out_dtype(hc_dtype t) {
     if (t != HC_DTYPE_BF16 && t != HC_DTYPE_F32) throw std::invalid_argument("native net op: output dtype must be bf16 or f32");
 }
+// the batch-norm backward may also write the split-precision rows its conv's dW / dX consume
+void check_grad_out_dtype(hc_dtype t) {
+    if (t != HC_DTYPE_BF16 && t != HC_DTYPE_F32 && t != HC_DTYPE_SPLIT)
+        throw std::invalid_argument("native batch norm backward: output dtype must be bf16, f32 or split");
+}
 
 // out = relu(xhat) as bf16 or fp32 (the split-precision net keeps fp32 activations)
 void bn_relu_apply_out(const float* x, long long n, int c, const double* mean, const float* inv_std, float* xhat,
@@ -519,7 +529,10 @@ template <typename DT>
 void bn_bwd_apply_out(const DT* d, const float* xhat, long long n, int c, const double* s1, const double* s2,
                              const float* inv_std, void* out, hc_dtype out_dtype, long long n_total, cudaStream_t s) {
     const long long m = n * (c / 8);
-    if (out_dtype == HC_DTYPE_F32)
+    if (out_dtype == HC_DTYPE_SPLIT)
+        k_bn_relu_bwd_apply<DT, bf16, true><<<grid_for(m, kT), kT, 0, s>>>(d, xhat, n, c, s1, s2, inv_std,
+                                                                           static_cast<bf16*>(out), n_total);
+    else if (out_dtype == HC_DTYPE_F32)
         k_bn_relu_bwd_apply<DT, float><<<grid_for(m, kT), kT, 0, s>>>(d, xhat, n, c, s1, s2, inv_std,
                                                                       static_cast<float*>(out), n_total);
     else
@@ -558,6 +571,9 @@ hc_status hc_native_max_pool(const int32_t* pmap, int64_t n_coarse, int32_t fd, 
         if (dtype == HC_DTYPE_BF16)
             k_nmax_pool<bf16, 8><<<grid_for(n, kT), kT, 0, s>>>(pmap, n_coarse, static_cast<const bf16*>(x), c,
                                                                 static_cast<bf16*>(y), sw);
+        else if (dtype == HC_DTYPE_SPLIT)  // fp32 input, split-precision output rows
+            k_nmax_pool<float, 8, bf16, true><<<grid_for(n, kT), kT, 0, s>>>(
+                pmap, n_coarse, static_cast<const float*>(x), c, static_cast<bf16*>(y), sw);
         else
             k_nmax_pool<float, 8><<<grid_for(n, kT), kT, 0, s>>>(pmap, n_coarse, static_cast<const float*>(x), c,
                                                                  static_cast<float*>(y), sw);
@@ -655,7 +671,7 @@ hc_status hc_native_bn_relu_backward_dt(const void* d_relu, hc_dtype dtype, cons
                                         int64_t n, int32_t c, void* d_conv, hc_dtype out_dtype, void* workspace,
                                         size_t ws_bytes, hc_stream stream) {
     return guard([&] {
-        check_out_dtype(out_dtype);
+        check_grad_out_dtype(out_dtype);
         check_c8(c);
         if (c > kT) throw std::invalid_argument("native batch norm: at most 256 channels");
         if (n <= 0) return;
@@ -792,7 +808,7 @@ hc_status hc_native_bn_relu_backward_apply_dt(const void* d_relu, hc_dtype dtype
                                               hc_stream stream) {
     return guard([&] {
         check_c8(c);
-        check_out_dtype(out_dtype);
+        check_grad_out_dtype(out_dtype);
         if (n <= 0) return;
         if (n_total <= 0) throw std::invalid_argument("batch_norm: empty input");
         cudaStream_t s = as_stream(stream);

@@ -228,20 +228,21 @@ class NativeHashNet:
                                              _s()))
 
     def _bn_relu_backward(self, i: int, d_relu: torch.Tensor, d_dtype: int, xhat: torch.Tensor,
-                          d_conv: torch.Tensor) -> None:
+                          d_conv: torch.Tensor, out_code: Optional[int] = None) -> None:
         blk = self.blocks[i]
+        out_code = self.adt_code if out_code is None else out_code
         n, c = xhat.shape
         ws = self._bn_ws(n, c)
         if self.sync_bn is None:
             check(lib.hc_native_bn_relu_backward_dt(_p(d_relu), d_dtype, _p(xhat), _p(blk["inv_std"]), n, c,
-                                                    _p(d_conv), self.adt_code, _p(ws), ws.numel(), _s()))
+                                                    _p(d_conv), out_code, _p(ws), ws.numel(), _s()))
             return
         stb = torch.empty(2 * c + 1, dtype=torch.float64, device="cuda")
         check(lib.hc_native_bn_stat(2, _p(xhat), _p(d_relu), d_dtype, n, c, None, _p(stb), _p(ws), ws.numel(), _s()))
         nt = self._sync_sums(stb, n, c)
         st = (stb[:2 * c].view(2, c) * (1.0 / nt)).contiguous()  # s * inv_n, as the kernel forms it
         check(lib.hc_native_bn_relu_backward_apply_dt(_p(d_relu), d_dtype, _p(xhat), _p(blk["inv_std"]), n, c,
-                                                      _p(st[0]), _p(st[1]), 1, _p(d_conv), self.adt_code, _s()))
+                                                      _p(st[0]), _p(st[1]), 1, _p(d_conv), out_code, _s()))
 
     def input_features(self, ref: torch.Tensor) -> torch.Tensor:
         """Finest-level data (C x N fp32, psh data array) -> padded voxel-major (bf16, or fp32 at
@@ -259,7 +260,8 @@ class NativeHashNet:
         n, co = fm.n, blk["cout_p"]
         y = torch.empty((n, co), dtype=torch.float32, device="cuda")
         if self.f32:
-            xs = nconv.split(x)
+            # split rows arrive straight from the previous level's pool (HC_DTYPE_SPLIT output)
+            xs = x if x.dtype == BF16 else nconv.split(x)
             # forward and dX operands in one launch; the dX one is kept for the backward pass (the
             # tensor-core tile set starts at 16 output channels: an 8-channel input level takes its
             # gradient through a zero-padded 16-channel kernel)
@@ -311,10 +313,14 @@ class NativeHashNet:
             if i + 1 < len(self.blocks):
                 pm = nb.pool_maps[i]
                 nc = pm.shape[0]
-                pooled = torch.empty((nc, blk["cout_p"]), dtype=self.adt, device="cuda")
                 sw = torch.empty((nc, blk["cout_p"]), dtype=torch.int8, device="cuda")
-                check(lib.hc_native_max_pool(_p(pm), nc, 8, _p(r), self.adt_code, blk["cout_p"], _p(pooled),
-                                             _p(sw), _s()))
+                if self.f32:  # fp32 max, written as the split rows the next conv consumes
+                    pooled = torch.empty((nc, 2 * blk["cout_p"]), dtype=BF16, device="cuda")
+                    code = _lib.HC_DTYPE_SPLIT
+                else:
+                    pooled = torch.empty((nc, blk["cout_p"]), dtype=self.adt, device="cuda")
+                    code = self.adt_code
+                check(lib.hc_native_max_pool(_p(pm), nc, 8, _p(r), code, blk["cout_p"], _p(pooled), _p(sw), _s()))
                 acts[-1]["sw"] = sw
                 if cache is not None and cache.get("trace") is not None:
                     cache["trace"]["blocks"][-1].update(pooled=pooled, sw=sw)
@@ -388,10 +394,13 @@ class NativeHashNet:
                 d_relu = torch.empty((n, c), device="cuda")
                 check(lib.hc_native_dense_pool_backward(_p(d_head), _p(a["src"]), nb.batch, c, n, _p(d_relu), _s()))
                 d_dtype = _lib.HC_DTYPE_F32
-            d_conv = torch.empty((n, c), dtype=self.adt, device="cuda")
-            self._bn_relu_backward(i, d_relu, d_dtype, a["xhat"], d_conv)
+            if self.f32:  # the BN backward writes the split rows dW / dX consume (no split pass)
+                d_conv = d_conv_s = torch.empty((n, 2 * c), dtype=BF16, device="cuda")
+                self._bn_relu_backward(i, d_relu, d_dtype, a["xhat"], d_conv, _lib.HC_DTYPE_SPLIT)
+            else:
+                d_conv = torch.empty((n, c), dtype=self.adt, device="cuda")
+                self._bn_relu_backward(i, d_relu, d_dtype, a["xhat"], d_conv)
             if self.f32:  # a["x"] holds the split input rows
-                d_conv_s = nconv.split(d_conv)
                 conv_grads[i] = nconv.conv_dw_x2(nb.conv_maps[i], a["x"], d_conv_s, self._dw_ws)
             else:
                 conv_grads[i] = nconv.conv_dw(nb.conv_maps[i], a["x"], d_conv, self._dw_ws)
