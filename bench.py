@@ -401,8 +401,7 @@ class FusedStepF32:
     def _layer(self, fmap, xs, dys, w, marks, on_dw=None):
         conv, sp = self.conv, self.spec
         mark = (lambda i: marks[i].record()) if marks else (lambda i: None)
-        wf = conv.pack_weights_x2(w, sp.out_channels, sp.in_channels, 27, conv.PACK_FORWARD)
-        wb = conv.pack_weights_x2(w, sp.out_channels, sp.in_channels, 27, conv.PACK_BACKWARD)
+        wf, wb = conv.pack_weights_x2_fb(w, sp.out_channels, sp.in_channels, 27)  # one launch
         mark(2)
         y = conv.gather_gemm_x2(fmap, xs, wf, sp.out_channels)
         mark(3)

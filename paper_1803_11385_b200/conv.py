@@ -128,6 +128,19 @@ def pack_weights_x2(w_ref: torch.Tensor, c_out: int, c_in: int, taps: int, mode:
     return wp
 
 
+def pack_weights_x2_fb(w_ref: torch.Tensor, c_out: int, c_in: int, taps: int, c_in_bwd: int = None):
+    """Forward and flipped (dX) split operands in one launch (hc_native_pack_weights_x2_fb); the dX
+    operand zero-padded to c_in_bwd >= c_in rows."""
+    w_ref = w_ref.contiguous().float()
+    c_in_bwd = c_in if c_in_bwd is None else c_in_bwd
+    wf = torch.empty((2 * c_out, int(lib.hc_native_packed_k_x2(c_in, taps))), dtype=torch.bfloat16,
+                     device=w_ref.device)
+    wb = torch.empty((2 * c_in_bwd, int(lib.hc_native_packed_k_x2(c_out, taps))), dtype=torch.bfloat16,
+                     device=w_ref.device)
+    check(lib.hc_native_pack_weights_x2_fb(_p(w_ref), c_out, c_in, taps, c_in_bwd, _p(wf), _p(wb), _s()))
+    return wf, wb
+
+
 def gather_gemm_x2(fmap, xs: torch.Tensor, wp2: torch.Tensor, c_out: int) -> torch.Tensor:
     """fp32 Y[n] = sum_t X[fmap(n,t)] . W_t from split operands (hc_native_gather_gemm_x2)."""
     fm = as_field_map(fmap)
@@ -231,8 +244,11 @@ class HashConv:
         # the transposed map (strided)
         back = PACK_TRANSPOSE if self.strided else PACK_BACKWARD
         if self.precision == "f32":
-            self.wf = pack_weights_x2(wp, self.cout_p, self.cin_p, self.taps, PACK_FORWARD)
-            self.wb = pack_weights_x2(wp, self.cout_p, self.cin_p, self.taps, back)
+            if back == PACK_BACKWARD:  # both operands in one launch
+                self.wf, self.wb = pack_weights_x2_fb(wp, self.cout_p, self.cin_p, self.taps)
+            else:
+                self.wf = pack_weights_x2(wp, self.cout_p, self.cin_p, self.taps, PACK_FORWARD)
+                self.wb = pack_weights_x2(wp, self.cout_p, self.cin_p, self.taps, back)
         else:
             self.wf = pack_weights(wp, self.cout_p, self.cin_p, self.taps, False)
             self.wb = pack_weights(wp, self.cout_p, self.cin_p, self.taps, mode=back)
