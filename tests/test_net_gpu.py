@@ -388,3 +388,26 @@ def test_native_net_step_f32_matches_reference_net_cfg2(cuda, ref):
     assert errs["loss"] < 1e-5, errs
     assert all(v < 1e-4 for k, v in errs.items() if k.startswith(("dw", "fc"))), errs
     assert all(v < 1e-5 for k, v in errs.items() if k.startswith(("mean", "var"))), errs
+
+
+def test_multi_tensor_sgd_bit_exact(cuda):
+    """hc_native_sgd_update_multi (one launch for many tensors) applies net.cpp:339-346's update
+    v = momentum*v + lr*(g + wd*w); w -= v with separate fp32 roundings to every tensor, bit for
+    bit the per-element numpy float32 restatement (sizes straddle the 256-thread blocks)."""
+    rng = np.random.default_rng(0)
+    sizes = [1, 255, 256, 257, 5000, 70001]
+    ws = [rng.standard_normal(n).astype(np.float32) for n in sizes]
+    vs = [rng.standard_normal(n).astype(np.float32) for n in sizes]
+    gs = [rng.standard_normal(n).astype(np.float32) for n in sizes]
+    lr, mom, wd = np.float32(0.1), np.float32(0.9), np.float32(5e-4)
+    tw = [torch.from_numpy(a.copy()).cuda() for a in ws]
+    tv = [torch.from_numpy(a.copy()).cuda() for a in vs]
+    tg = [torch.from_numpy(a.copy()).cuda() for a in gs]
+    k = len(sizes)
+    arr = lambda ts: (C.c_void_p * k)(*[t.data_ptr() for t in ts])  # noqa: E731
+    _lib.check(_lib.lib.hc_native_sgd_update_multi(arr(tw), arr(tv), arr(tg), (C.c_int64 * k)(*sizes), k,
+                                                   float(lr), float(mom), float(wd), None))
+    for w, v, g, dw, dv in zip(ws, vs, gs, tw, tv):
+        v_new = (mom * v) + (lr * (g + (wd * w)))
+        w_new = w - v_new
+        assert np.array_equal(dv.cpu().numpy(), v_new) and np.array_equal(dw.cpu().numpy(), w_new)
