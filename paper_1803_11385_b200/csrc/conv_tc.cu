@@ -821,6 +821,9 @@ struct DwGroups {
     int groups;
     int pair, rpm, pcols;
     int nacc;  // accumulator buffers per CTA (2: chunk drains overlap the next chunk's MMAs)
+    int shift[kMaxGroups];  // chunk c of group g covers tiles [c*tps - shift, (c+1)*tps - shift) (clipped):
+                            // groups alternate between 0 and tps/2, so the two CTAs an SM holds (of
+                            // different groups) drain their accumulators at different times
     int strided;  // 1: CTA k of a group runs chunks k, k + n, k + 2n ... (n = the group's CTAs), so
                   // the whole grid sweeps the voxels together and the groups' gathers of X and
                   // loads of dY hit L2; 0: contiguous runs of cpc chunks
@@ -887,9 +890,19 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
     const int cstride = grp_tab.strided ? nct : 1;
     const int nch = grp_tab.strided ? (kcta < nchunk ? (nchunk - kcta + nct - 1) / nct : 0)
                                     : max(0, min(grp_tab.cpc[grp], nchunk - chunk0));
-    // this CTA's chunks are chunk0 + j * cstride; all hold tps tiles but the grid's last one
-    const int ntl = nch > 0 ? (nch - 1) * tps + min(tps, tiles - (chunk0 + (nch - 1) * cstride) * tps) : 0;
-    auto tile_of = [&](int lt) { return (chunk0 + (lt / tps) * cstride) * tps + lt % tps; };
+    // this CTA's chunks are chunk0 + j * cstride; chunk c covers [c*tps - sh, (c+1)*tps - sh) within
+    // [0, tiles): all hold tps tiles but the group's first (tps - sh) and last ones
+    const int sh = grp_tab.shift[grp];
+    auto cstart = [&](int c) { return max(0, c * tps - sh); };
+    auto cend = [&](int c) { return min(tiles, (c + 1) * tps - sh); };
+    const int len0 = nch > 0 ? cend(chunk0) - cstart(chunk0) : 0;  // this CTA's first chunk
+    const int ntl = nch == 0 ? 0 : nch == 1 ? len0
+                  : len0 + (nch - 2) * tps + (cend(chunk0 + (nch - 1) * cstride) - cstart(chunk0 + (nch - 1) * cstride));
+    auto tile_of = [&](int lt) {
+        if (lt < len0) return cstart(chunk0) + lt;
+        const int r = lt - len0;
+        return cstart(chunk0 + (1 + r / tps) * cstride) + r % tps;
+    };
     const int pair = grp_tab.pair;    // 0 plain, 1 pair (split precision, 4 products), 2 tri (3 products)
     const int Co = pair ? C / 2 : C;  // channels of one plane
     const int RPM = pair == 1 ? 64 : 128;  // (t, ci) rows per m-tile (tri: per unit)
@@ -1056,6 +1069,7 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
         int s = 0, bs = 0;
         uint32_t ph = 0, bph = 0;
         int cl = 0, ci = 0;  // tile index inside the chunk, chunk index
+        int clen = len0;     // tiles of the current chunk
         for (int lt = 0; lt < ntl; ++lt) {
             const int ab = nacc == 2 ? (ci & 1) : 0;  // accumulator buffer of this chunk
             if (cl == 0 && ci >= nacc) {                 // its previous chunk has been drained
@@ -1095,11 +1109,13 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
                     bph ^= 1;
                 }
             }
-            if (++cl == tps || lt == ntl - 1) {
+            if (++cl == clen || lt == ntl - 1) {
                 if (elect_one()) mma_commit(done0 + 8 * ab);
                 __syncwarp();
                 cl = 0;
                 ++ci;
+                const int c = chunk0 + ci * cstride;
+                clen = cend(c) - cstart(c);
             }
         }
     } else if (warp >= PW + 2) {
@@ -1619,7 +1635,9 @@ DwPlan dw_plan(long long rows, int taps, int cin, int cout, int max_tps = 0, boo
         }
         g.tps[i] = std::max(1, (p.tiles + want - 1) / want);  // tiles per CTA ...
         if (max_tps > 0) g.tps[i] = std::min(g.tps[i], max_tps);  // ... cut into chunks of <= max_tps
-        g.nchunk[i] = std::max(1, (p.tiles + g.tps[i] - 1) / g.tps[i]);
+        static const int phase = env_int("HCB_DW_PHASE", 1);
+        g.shift[i] = (phase && strided && max_tps > 0 && (i & 1) && g.tps[i] >= 2 && p.tiles > g.tps[i]) ? g.tps[i] / 2 : 0;
+        g.nchunk[i] = std::max(1, (p.tiles + g.shift[i] + g.tps[i] - 1) / g.tps[i]);
         g.cpc[i] = (g.nchunk[i] + want - 1) / want;
         g.cta_begin[i + 1] = g.cta_begin[i] + (g.nchunk[i] + g.cpc[i] - 1) / g.cpc[i];
         g.part_begin[i] = part;
