@@ -809,7 +809,10 @@ __global__ void __launch_bounds__(FwdX2Cfg<BN, CPS, PW, SA, SB, NBUF>::THREADS, 
 //   tri (split precision, c_out >= 32, default): units of 128 (t, ci) rows; the hi-plane m-tile
 //     multiplies [dY_hi | dY_lo] (N = 2 c_out), the lo-plane m-tile dY_hi only (N = c_out), so the
 //     negligible lo.lo product is never computed (3 products instead of 4); each epilogue lane sums
-//     its own row (hi.hi + hi.lo) + lo.hi, rpm = 128 rows x c_out.
+//     its own row, rpm = 128 rows x c_out. For 32 < c_out <= 64 (tshared) the lo-plane m-tile
+//     accumulates into the hi.dY_hi columns — 2 c_out TMEM columns per unit, two units per CTA,
+//     half the dY loads — and the lane sums (hi.dY_hi + lo.dY_hi) + hi.dY_lo; otherwise lo.dY_hi
+//     keeps its own c_out columns and the sum is (hi.dY_hi + hi.dY_lo) + lo.dY_hi.
 // Partials start at part_begin[g] (floats), laid out [chunk][m-tile][rpm][pcols]:
 //   plain: rpm = 128 (t,ci) rows of the row width C, pcols = NB.
 //   pair (split precision, hc_native_conv_dw_x2): X rows are [hi | lo] (C = 2 c), dY rows
@@ -824,6 +827,7 @@ struct DwGroups {
     int shift[kMaxGroups];  // chunk c of group g covers tiles [c*tps - shift, (c+1)*tps - shift) (clipped):
                             // groups alternate between 0 and tps/2, so the two CTAs an SM holds (of
                             // different groups) drain their accumulators at different times
+    int tshared;  // tri: the lo-plane m-tile accumulates into the hi.dY_hi columns (c_out <= 64)
     int strided;  // 1: CTA k of a group runs chunks k, k + n, k + 2n ... (n = the group's CTAs), so
                   // the whole grid sweeps the voxels together and the groups' gathers of X and
                   // loads of dY hit L2; 0: contiguous runs of cpc chunks
@@ -1065,7 +1069,11 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
         const uint32_t idesc_lo = pair == 2 ? idesc_bf16_f32(BM, pco, true, true) : idesc;
         const uint32_t idesc_hi = pair == 2 ? idesc_bf16_f32(BM, 2 * pco, true, true) : idesc;  // [dY_hi | dY_lo]
         const uint64_t b0_lo = sw128_desc(bbase, pco >= 128 ? 2 * LBO : LBO, 1024);
-        const int ucols = pair == 2 ? 3 * pco : NB;  // accumulator columns per m-tile (tri: per unit)
+        // tri: c_out <= 64 -> the lo-plane m-tile accumulates into the hi.dY_hi columns (its D columns are the
+        // hi channels 0 .. c_out - 1, the first half of the [dY_hi | dY_lo] row), 2 c_out columns per unit;
+        // wider: dY_hi's 64-blocks are not contiguous there, so lo.dY_hi keeps its own c_out columns
+        const bool tshared = pair == 2 && grp_tab.tshared;
+        const int ucols = pair == 2 ? (tshared ? 2 * pco : 3 * pco) : NB;  // accumulator columns per m-tile / unit
         int s = 0, bs = 0;
         uint32_t ph = 0, bph = 0;
         int cl = 0, ci = 0;  // tile index inside the chunk, chunk index
@@ -1088,12 +1096,17 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
                     if (elect_one()) {
                         const uint64_t ao = (uint64_t)((s * Cfg::A_BYTES) >> 4);
                         const bool lo = pair == 2 && (mi & 1);
-                        const uint32_t d = pair == 2 ? acc0 + (mi >> 1) * ucols + (lo ? 2 * pco : 0) : acc0 + mi * NB;
+                        const uint32_t d = pair == 2 ? acc0 + (mi >> 1) * ucols + (lo && !tshared ? 2 * pco : 0)
+                                                     : acc0 + mi * NB;
                         const uint64_t bd = (lo ? b0_lo : b0) + bo;
                         const uint32_t id = lo ? idesc_lo : idesc_hi;
 #pragma unroll
+                        // a shared lo accumulator (tshared) always adds: the unit's hi m-tile stage, issued
+                        // first, zero-initialises those columns at the chunk's first K step
+                        const bool first = (cl | h) == 0 && !(lo && tshared);
+#pragma unroll
                         for (int kk = 0; kk < Cfg::KB / 16; ++kk)  // 16 voxels = two 8-row atoms per MMA
-                            mma_bf16(d, a0 + ao + 128 * kk, bd + 128 * kk, id, (cl | h | kk) != 0);
+                            mma_bf16(d, a0 + ao + 128 * kk, bd + 128 * kk, id, !(first && kk == 0));
                         mma_commit(empty0 + 8 * s);
                     }
                     __syncwarp();
@@ -1126,7 +1139,9 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
         for (int c = 0; c < nch; ++c) {
             const int ab = nacc == 2 ? (c & 1) : 0;
             mbar_wait_sleep(done0 + 8 * ab, (uint32_t)((nacc == 2 ? c >> 1 : c) & 1));
-            const uint32_t tqa = tq + ab * nm * (pair == 2 ? 3 * pco : NB);
+            const bool tsh = pair == 2 && grp_tab.tshared;  // as the MMA issuer's tshared
+            const int uc = pair == 2 ? (tsh ? 2 * pco : 3 * pco) : NB;
+            const uint32_t tqa = tq + ab * nm * uc;
             tc_fence_after();
             const long long slot = chunk0 + (long long)c * cstride;
             if (pair == 2) {
@@ -1134,17 +1149,22 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
                 const int g = x2_block(pco);
                 for (int u = 0; u < nm; ++u) {
                     float* dst = partial + grp_tab.part_begin[grp] + ((slot * nm + u) * BM + row) * pco;
-                    const uint32_t tu = tqa + u * 3 * pco;
+                    const uint32_t tu = tqa + u * uc;
                     for (int c0 = 0; c0 < pco; c0 += 16) {
                         uint32_t a[16], b[16], l[16];
                         tmem_ld16(tu + x2_pos(c0, 0, g), a);
                         tmem_ld16(tu + x2_pos(c0, 1, g), b);
-                        tmem_ld16(tu + 2 * pco + c0, l);
+                        if (!tsh) tmem_ld16(tu + 2 * pco + c0, l);
                         tmem_ld_wait();
                         float f[16];
+                        if (tsh) {  // (hi.dY_hi + lo.dY_hi) + hi.dY_lo
 #pragma unroll
-                        for (int e = 0; e < 16; ++e)
-                            f[e] = (__uint_as_float(a[e]) + __uint_as_float(b[e])) + __uint_as_float(l[e]);
+                            for (int e = 0; e < 16; ++e) f[e] = __uint_as_float(a[e]) + __uint_as_float(b[e]);
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 16; ++e)
+                                f[e] = (__uint_as_float(a[e]) + __uint_as_float(b[e])) + __uint_as_float(l[e]);
+                        }
                         store_row(dst + c0, f);
                     }
                 }
@@ -1599,7 +1619,10 @@ DwPlan dw_plan(long long rows, int taps, int cin, int cout, int max_tps = 0, boo
     // pair mode with chunked accumulation: HCB_DW_DBUF=1 keeps two accumulator sets per CTA (the
     // epilogue drains one chunk while the next accumulates) at half the m-tiles per CTA
     static const int dbuf_env = env_int("HCB_DW_DBUF", 0);
-    const int unit_cols = mode == 2 ? 3 * cout : p.nb;  // tri: [hi.dY_hi | hi.dY_lo] + lo.dY_hi
+    // tri: [hi.dY_hi + lo.dY_hi | hi.dY_lo] (c_out <= 64, shared) or + a separate lo.dY_hi (wider)
+    static const int tshared_env = env_int("HCB_DW_TRI_SHARED", 1);
+    const bool tshared = mode == 2 && cout > 32 && cout <= 64 && tshared_env;  // C 64: 1.47 -> 1.42 ms; C 32 slower (0.68 vs 0.67)
+    const int unit_cols = mode == 2 ? (tshared ? 2 * cout : 3 * cout) : p.nb;
     const int nacc = (pair && max_tps > 0 && dbuf_env && 512 / (unit_cols * p.cps * 2) >= 1) ? 2 : 1;
     const int cap = std::min(mode == 2 ? 8 : 16, 512 / (unit_cols * p.cps * nacc));  // m-tiles (units) per CTA
     const int G = (p.mt + cap - 1) / cap;  // -> every group has <= cap m-tiles
@@ -1610,6 +1633,7 @@ DwPlan dw_plan(long long rows, int taps, int cin, int cout, int max_tps = 0, boo
     DwGroups& g = p.g;
     g.groups = G;
     g.pair = mode;
+    g.tshared = tshared ? 1 : 0;
     g.nacc = nacc;
     static const int strided = env_int("HCB_DW_STRIDED", 1);
     g.strided = strided;

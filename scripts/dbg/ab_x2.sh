@@ -1,8 +1,2 @@
-timeout 900 python -m pytest -q -x tests/test_conv_f32.py tests/test_conv_tc.py -p no:cacheprovider 2>&1 | tail -1
-P="python scripts/dbg/x2_probe.py time 256 8 64 64"
-run() { echo "$* : "; env "$@" timeout 300 $P 2>&1 | tail -1 | cut -c1-150; }
-run HCB_DW_PHASE=1
-run HCB_DW_PHASE=0
-run HCB_DW_PHASE=1
-run HCB_DW_PHASE=0
-for c in "128 128" "32 32"; do for ph in 1 0; do echo "C=$c phase=$ph"; HCB_DW_PHASE=$ph timeout 300 python scripts/dbg/x2_probe.py time 256 8 $c 2>&1 | tail -1 | cut -c1-150; done; done
+P="python scripts/dbg/x2_probe.py time 256 8"
+for c in "64 64" "32 32" "64 64" "32 32"; do for t in 1 0; do echo -n "C=$c shared=$t "; HCB_DW_TRI_SHARED=$t timeout 300 $P $c 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['dw'],3), round(d['fwd'],3))"; done; done
