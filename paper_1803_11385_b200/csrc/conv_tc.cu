@@ -1660,7 +1660,10 @@ DwPlan dw_plan(long long rows, int taps, int cin, int cout, int max_tps = 0, boo
         g.tps[i] = std::max(1, (p.tiles + want - 1) / want);  // tiles per CTA ...
         if (max_tps > 0) g.tps[i] = std::min(g.tps[i], max_tps);  // ... cut into chunks of <= max_tps
         static const int phase = env_int("HCB_DW_PHASE", 1);
-        g.shift[i] = (phase && strided && max_tps > 0 && (i & 1) && g.tps[i] >= 2 && p.tiles > g.tps[i]) ? g.tps[i] / 2 : 0;
+        // half-chunk phase shift of odd groups: C 128 5.45 -> 5.29 ms; with the shared tri accumulator
+        // (C 64, 7 groups) it costs 3% (1.31 -> 1.35), so not there
+        g.shift[i] = (phase && strided && max_tps > 0 && !tshared && (i & 1) && g.tps[i] >= 2 && p.tiles > g.tps[i])
+                         ? g.tps[i] / 2 : 0;
         g.nchunk[i] = std::max(1, (p.tiles + g.shift[i] + g.tps[i] - 1) / g.tps[i]);
         g.cpc[i] = (g.nchunk[i] + want - 1) / want;
         g.cta_begin[i + 1] = g.cta_begin[i] + (g.nchunk[i] + g.cpc[i] - 1) / g.cpc[i];
