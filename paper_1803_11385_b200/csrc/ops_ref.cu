@@ -16,6 +16,7 @@
 #include "dev_psh.cuh"
 #include "hc_internal.h"
 #include "hc_launch.cuh"
+#include "tc_common.cuh"
 
 namespace hcb {
 
@@ -530,6 +531,282 @@ __global__ void __launch_bounds__(256, HCB_POOL_MINB) k_avg_pool(DevPsh in, DevP
     }
 }
 
+// ------------------------------------------------- staged 2^3 pooling (F = 2, dim 3)
+// The children of 256 consecutive coarse voxels lie in a few contiguous spans of fine
+// columns, one per (model, coarse z, child dz) — columns are z,y,x-sorted — covering
+// ~2048 columns plus partial rows at the span ends. A block finds those spans once
+// (block scan of (model, z) changes, warp min/max reductions), then streams PL channel
+// planes of every span per stage into shared memory with 1-D bulk copies (one mbarrier
+// per stage, NS stages in flight) and reduces the children from shared memory: DRAM
+// sees contiguous multi-KB reads instead of scattered 4-byte gathers, and a warp waits
+// once per PL planes. Per channel the taps are visited in row order with
+// the first-hit seed / strict '>' rule (max) or the row-order __fadd_rn sum (avg), so the
+// results are bit-identical to k_max_pool / k_avg_pool. A block whose spans do not fit
+// (more than NKEY/2 (model, z) pairs, > CAP columns, or a copy that would run past the
+// last plane) runs the direct per-thread gathers instead. A ninth warp only issues the
+// copies: each consumer warp releases a stage on its own "empty" mbarrier arrival, so warps
+// never wait for each other (a block barrier per stage: 0.170 ms).
+constexpr int kPoolCap = 2304;  // staged columns per plane (2048 children + span slack)
+constexpr int kPoolKeys = 16;   // (model, z) pair x child dz spans per block
+
+template <bool AVG>
+__device__ __forceinline__ void pool_reduce(const float (&v)[8], const int (&nb)[8], float inv, float& out, int& arg) {
+    if constexpr (AVG) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+            if (nb[t] >= 0) acc = __fadd_rn(acc, v[t]);
+        out = __fmul_rn(acc, inv);
+        arg = 0;
+    } else {
+        float best = 0.0f;
+        arg = -1;
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+            if (nb[t] >= 0 && (arg < 0 || v[t] > best)) {
+                best = v[t];
+                arg = t;
+            }
+        out = arg < 0 ? 0.0f : best;
+    }
+}
+
+template <int PL, int NS, bool AVG, int MINB = 1>
+__global__ void __launch_bounds__(288, MINB) k_pool_staged(DevPsh in, DevPsh out, int S, int pad,
+                                                        const float* __restrict__ data, int C, float inv,
+                                                        float* __restrict__ res, int* __restrict__ sw) {
+    constexpr int NKEY = kPoolKeys, CAP = kPoolCap;
+    extern __shared__ __align__(128) float stage[];  // [NS][PL][CAP]
+    __shared__ int rmin[NKEY], rmax[NKEY], roff[NKEY], wtot[9];
+    __shared__ int s_over;
+    __shared__ __align__(8) unsigned long long full[NS], empty[NS];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const long long col = blockIdx.x * 256LL + tid;
+    const bool live = tid < 256 && col < out.N;
+    const long long Nin = in.N, Nout = out.N;
+    if (tid < NKEY) {
+        rmin[tid] = INT_MAX;
+        rmax[tid] = -1;
+    }
+    if (tid < NS * PL) *reinterpret_cast<float4*>(stage + tid * CAP + CAP - 4) = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (tid == 0) {
+        s_over = 0;
+        for (int s = 0; s < NS; ++s) {
+            tc::mbar_init(tc::smem_u32(&full[s]), 1);
+            tc::mbar_init(tc::smem_u32(&empty[s]), 8);
+        }
+        tc::mbar_init_fence();
+    }
+    int nb[8];
+    int4 c = make_int4(0, 0, 0, 0);
+    if (live) {
+        c = out.cols[col];
+        const ModelParam mp = in.models[c.w - 1];
+        probe_field_batched<2>(in, mp, origin_axis(c.x, 2, S, pad), origin_axis(c.y, 2, S, pad),
+                               origin_axis(c.z, 2, S, pad), nb);
+    } else {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) nb[t] = -1;
+    }
+    // span key: number of (model, z) changes before this voxel in the block
+    int pw = __shfl_up_sync(0xffffffffu, c.w, 1), pz = __shfl_up_sync(0xffffffffu, c.z, 1);
+    if (lane == 0 && tid > 0 && live) {
+        const int4 p = out.cols[col - 1];
+        pw = p.w;
+        pz = p.z;
+    }
+    const bool flag = live && tid > 0 && (pw != c.w || pz != c.z);
+    const unsigned bal = __ballot_sync(0xffffffffu, flag);
+    if (lane == 31) wtot[wid] = __popc(bal);
+    int lmin0 = INT_MAX, lmax0 = -1, lmin1 = INT_MAX, lmax1 = -1;
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+        if (nb[t] >= 0) {
+            lmin0 = min(lmin0, nb[t]);
+            lmax0 = max(lmax0, nb[t]);
+        }
+#pragma unroll
+    for (int t = 4; t < 8; ++t)
+        if (nb[t] >= 0) {
+            lmin1 = min(lmin1, nb[t]);
+            lmax1 = max(lmax1, nb[t]);
+        }
+    __syncthreads();
+    int k = __popc(bal & (0xffffffffu >> (31 - lane)));
+    for (int w = 0; w < wid; ++w) k += wtot[w];
+    {
+        const int kmin = __reduce_min_sync(0xffffffffu, k), kmax = __reduce_max_sync(0xffffffffu, k);
+        if (2 * kmax + 1 >= NKEY) {
+            if (lane == 0) s_over = 1;
+        } else {
+            for (int kk = kmin; kk <= kmax; ++kk) {
+                const bool me = k == kk;
+                const int a0 = __reduce_min_sync(0xffffffffu, me ? lmin0 : INT_MAX);
+                const int b0 = __reduce_max_sync(0xffffffffu, me ? lmax0 : -1);
+                const int a1 = __reduce_min_sync(0xffffffffu, me ? lmin1 : INT_MAX);
+                const int b1 = __reduce_max_sync(0xffffffffu, me ? lmax1 : -1);
+                if (lane == 0) {
+                    atomicMin(&rmin[2 * kk], a0);
+                    atomicMax(&rmax[2 * kk], b0);
+                    atomicMin(&rmin[2 * kk + 1], a1);
+                    atomicMax(&rmax[2 * kk + 1], b1);
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (tid == 0 && !s_over) {
+        int off = 0;
+        const long long total = (long long)C * Nin;
+        for (int j = 0; j < NKEY; ++j) {
+            roff[j] = off;
+            if (rmax[j] < 0) continue;
+            const int len = rmax[j] - rmin[j] + 1;
+            off += (len + 6) & ~3;  // room for a 0..3 column alignment shift, 16-byte granules
+            const long long g = (long long)(C - 1) * Nin + rmin[j], a = g & ~3LL;
+            if (a + ((g + len - a + 3) & ~3LL) > total) s_over = 1;  // last plane's copy past the end
+        }
+        if (off > CAP - 4) s_over = 1;  // the last 4 columns of every plane slot stay zero
+    }
+    __syncthreads();
+    if (s_over) {  // direct gathers (same arithmetic)
+        if (!live) return;
+        int kt[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) kt[t] = max(nb[t], 0);
+        for (int ch = 0; ch < C; ++ch) {
+            const float* src = data + ch * Nin;
+            float v[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) v[t] = __ldg(src + kt[t]);
+            float o;
+            int arg;
+            pool_reduce<AVG>(v, nb, inv, o, arg);
+            res[ch * Nout + col] = o;
+            if constexpr (!AVG) sw[ch * Nout + col] = arg;
+        }
+        return;
+    }
+    // per-tap shared offsets: roff + (child - span start) + the plane's alignment shift.
+    // Absent taps read a present one (max: the first present tap, whose value seeds the
+    // running max, so a copy never passes the strict '>') or the zero columns at the end of
+    // the slot (avg: adding +0.0 to a row-order sum that starts at +0.0 is exact), so the
+    // reduction needs no per-tap presence test.
+    int tf = -1;
+#pragma unroll
+    for (int t = 7; t >= 0; --t)
+        if (nb[t] >= 0) tf = t;
+    int pb[8], rm3[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        const int j = 2 * k + (t >> 2);
+        pb[t] = nb[t] >= 0 ? roff[j] + nb[t] - rmin[j] : CAP - 4;
+        rm3[t] = nb[t] >= 0 ? rmin[j] & 3 : 0;
+    }
+    if constexpr (!AVG) {
+        if (tf >= 0) {
+            int pf = 0, rf = 0;
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+                if (t == tf) {
+                    pf = pb[t];
+                    rf = rm3[t];
+                }
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+                if (nb[t] < 0) {
+                    pb[t] = pf;
+                    rm3[t] = rf;
+                }
+        }
+    }
+    const int nin3 = (int)(Nin & 3);
+    const int nsteps = (C + PL - 1) / PL;
+    const uint32_t stage0 = tc::smem_u32(stage);
+    auto issue = [&](int j) {  // producer warp: the PL planes of step j into slot j % NS
+        const int slot = j % NS;
+        const uint32_t bar = tc::smem_u32(&full[slot]);
+        uint32_t bytes = 0;
+        for (int i = lane; i < PL * NKEY; i += 32) {
+            const int p = i / NKEY, key = i % NKEY, ch = j * PL + p;
+            if (ch >= C || rmax[key] < 0) continue;
+            const long long g = (long long)ch * Nin + rmin[key], a = g & ~3LL;
+            bytes += (uint32_t)(((g + rmax[key] - rmin[key] + 1 - a + 3) & ~3LL) * 4);
+        }
+        bytes = __reduce_add_sync(0xffffffffu, bytes);
+        if (lane == 0) tc::mbar_arrive_expect_tx(bar, bytes);
+        __syncwarp();
+        for (int i = lane; i < PL * NKEY; i += 32) {
+            const int p = i / NKEY, key = i % NKEY, ch = j * PL + p;
+            if (ch >= C || rmax[key] < 0) continue;
+            const long long g = (long long)ch * Nin + rmin[key], a = g & ~3LL;
+            const uint32_t n = (uint32_t)(((g + rmax[key] - rmin[key] + 1 - a + 3) & ~3LL) * 4);
+            tc::bulk_g2s(stage0 + (uint32_t)(((slot * PL + p) * CAP + roff[key]) * 4), data + a, n, bar);
+        }
+    };
+    if (wid == 8) {  // producer warp
+        for (int j = 0; j < nsteps; ++j) {
+            if (j >= NS) tc::mbar_wait(tc::smem_u32(&empty[j % NS]), ((j / NS) - 1) & 1);
+            issue(j);
+        }
+        return;
+    }
+    // consumers; AL: every plane starts 16-byte aligned (N % 4 == 0), so the alignment
+    // shift is the span's own and folds into the tap offsets
+    auto consume = [&](auto aligned) {
+        constexpr bool AL = decltype(aligned)::value;
+        int pa[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) pa[t] = pb[t] + rm3[t];
+        float* rp = res + col;
+        int* sp = sw + col;
+        for (int j = 0; j < nsteps; ++j) {
+            const int slot = j % NS;
+            tc::mbar_wait(tc::smem_u32(&full[slot]), (j / NS) & 1);
+            if (live) {
+#pragma unroll
+                for (int p = 0; p < PL; ++p) {
+                    const int ch = j * PL + p;
+                    if (ch >= C) break;
+                    const float* pl = stage + (slot * PL + p) * CAP;
+                    const int cs = ch * nin3;
+                    float v[8];
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) v[t] = pl[AL ? pa[t] : pb[t] + ((cs + rm3[t]) & 3)];
+                    float o;
+                    int arg = 0;
+                    if constexpr (AVG) {
+                        float acc = 0.0f;
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) acc = __fadd_rn(acc, v[t]);
+                        o = __fmul_rn(acc, inv);
+                    } else {
+                        float best = v[0];
+                        arg = tf;
+#pragma unroll
+                        for (int t = 1; t < 8; ++t)
+                            if (v[t] > best) {
+                                best = v[t];
+                                arg = t;
+                            }
+                        o = tf < 0 ? 0.0f : best;
+                    }
+                    *rp = o;
+                    rp += Nout;
+                    if constexpr (!AVG) {
+                        *sp = arg;
+                        sp += Nout;
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&empty[slot]));
+        }
+    };
+    if (nin3 == 0) consume(std::true_type{});
+    else consume(std::false_type{});
+}
+
 template <typename T>
 __global__ void k_avg_pool_any(DevPsh in, DevPsh out, int F, int S, int pad, int fd, const T* __restrict__ data,
                                int C, T inv, T* __restrict__ res) {
@@ -632,11 +909,30 @@ __global__ void k_unpool_any(DevPsh fine, DevPsh coarse, int F, int S, int pad, 
     }
 }
 
+// Range scan of the switches: 4 x 16-byte loads per thread per pass (one 4-byte load per
+// thread kept too few bytes in flight: 72 us for 110 MB, 1.5 TB/s).
 __global__ void k_check_switches(const int* sw, long long n, int fd, int* bad) {
-    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int s = sw[i];
-    if (s >= fd || s < -1) *reinterpret_cast<volatile int*>(bad) = 1;  // mapped host word
+    const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long nth = (long long)gridDim.x * blockDim.x;
+    const unsigned lim = (unsigned)fd + 1u;  // s in [-1, fd)  <=>  (unsigned)(s + 1) < fd + 1
+    bool ok = true;
+    const long long head = (long long)(((16 - (reinterpret_cast<uintptr_t>(sw) & 15)) & 15) / 4);
+    const long long h = head < n ? head : n;
+    if (tid < h) ok = (unsigned)sw[tid] + 1u < lim;
+    const int4* v = reinterpret_cast<const int4*>(sw + h);
+    const long long nv = (n - h) / 4;
+    for (long long i = tid; i < nv; i += 4 * nth) {
+        int4 q[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) q[u] = i + u * nth < nv ? __ldcs(v + i + u * nth) : make_int4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            ok &= ((unsigned)q[u].x + 1u < lim) & ((unsigned)q[u].y + 1u < lim) & ((unsigned)q[u].z + 1u < lim) &
+                  ((unsigned)q[u].w + 1u < lim);
+    }
+    const long long t0 = h + nv * 4;
+    if (t0 + tid < n) ok &= (unsigned)sw[t0 + tid] + 1u < lim;
+    if (!ok) *reinterpret_cast<volatile int*>(bad) = 1;  // mapped host word
 }
 
 // ============================================================== dispatch helpers
@@ -722,13 +1018,42 @@ void launch_col2hash(const float* gcols, const hc_psh* in, const hc_psh* out, co
     launched("col2hash");
 }
 
+// staged 2^3 pooling (k_pool_staged) when the layout allows it; HCB_POOL_STAGED picks the
+// (planes per stage, stages) shape for A/B runs, 0 = direct kernels
+template <bool AVG>
+bool launch_pool_staged(const hc_psh* in, const float* data, const hc_psh* out, const hc_conv_spec& sp, float inv,
+                        float* res, int* sw, cudaStream_t s) {
+    static const int mode = env_int("HCB_POOL_STAGED", 1);
+    if (mode <= 0 || sp.kernel != 2 || in->d.dim != 3 || (reinterpret_cast<uintptr_t>(data) & 15) != 0) return false;
+    const long long n = out->d.N;
+    const unsigned g = (unsigned)((n + 255) / 256);
+    auto go = [&](auto kern, int pl, int ns) {
+        const int smem = pl * ns * kPoolCap * 4;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        kern<<<g, 288, smem, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, inv, res, sw);
+    };
+    // A/B at 256^3 x 8 (C 16 / 64 / 128, max_pool ms): (2 planes, 2 stages, 4 blocks/SM) 0.064 / 0.155 /
+    // 0.278; (2, 3, 4) 0.083 / 0.157 / 0.264; (2, 3, 3) 0.070 / 0.152 / 0.269; (4, 2, 3) - / 0.164 / -
+    switch (mode) {
+        case 2: go(k_pool_staged<2, 3, AVG, 4>, 2, 3); break;
+        case 3: go(k_pool_staged<2, 3, AVG>, 2, 3); break;
+        case 4: go(k_pool_staged<4, 2, AVG>, 4, 2); break;
+        default:
+            if (sp.in_channels > 64) go(k_pool_staged<2, 3, AVG, 4>, 2, 3);
+            else go(k_pool_staged<2, 2, AVG, 4>, 2, 2);
+            break;
+    }
+    return true;
+}
+
 void launch_max_pool(const hc_psh* in, const float* data, const hc_psh* out, const hc_conv_spec& sp, float* res,
                      int* sw, cudaStream_t s) {
     const long long n = out->d.N;
     if (n == 0 || sp.in_channels == 0) return;
     const unsigned g = grid_for(n, kThreads);
     // CB = 4 channels per pass (A/B at 256^3 x 8, C=64: CB 2 / 4 / 8 = 0.195 / 0.188 / 0.574 ms)
-    if (sp.kernel == 2)
+    if (launch_pool_staged<false>(in, data, out, sp, 0.0f, res, sw, s)) {
+    } else if (sp.kernel == 2)
         k_max_pool<2, 4><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, res, sw);
     else if (sp.kernel == 3)
         k_max_pool<3, 1><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, res, sw);
@@ -745,7 +1070,8 @@ void launch_avg_pool(const hc_psh* in, const float* data, const hc_psh* out, con
     const unsigned g = grid_for(n, kThreads);
     const long long fd = field_volume(sp, in->d.dim);
     const float inv = 1.0f / static_cast<float>(fd);  // cnn_ops.cpp:295
-    if (sp.kernel == 2)
+    if (launch_pool_staged<true>(in, data, out, sp, inv, res, nullptr, s)) {
+    } else if (sp.kernel == 2)
         k_avg_pool<2, 4><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, inv, res);
     else if (sp.kernel == 3)
         k_avg_pool<3, 1><<<g, kThreads, 0, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, inv, res);
@@ -1005,7 +1331,8 @@ hc_status max_unpool_impl(const T* coarse_data, int64_t c_rows, int64_t c_cols, 
         cudaStream_t s = as_stream(stream);
         const long long n = s_rows * s_cols;
         if (n > 0) {
-            k_check_switches<<<grid_for(n, kThreads), kThreads, 0, s>>>(switches, n, (int)fd, deferred_flag_device());
+            const unsigned g = (unsigned)std::min<long long>((n + 16 * kThreads - 1) / (16 * kThreads), 148 * 8);
+            k_check_switches<<<g, kThreads, 0, s>>>(switches, n, (int)fd, deferred_flag_device());
             launched("switch check");
         }
         launch_unpool(false, coarse_data, switches, fine, coarse, spec, result, s);

@@ -148,6 +148,35 @@ def test_shell64_batch4_vs_oracle(cuda, restated):
                           restated.max_unpool(om, osw, fa, ca, psp))
 
 
+@pytest.mark.parametrize("C", [7, 16])
+def test_staged_pool_vs_oracle(cuda, restated, C):
+    """2^3 pooling through k_pool_staged (ops_ref.cu): 128^3 shells (blocks stage their
+    child spans through shared memory) mixed with a sparse random set of the same
+    resolution (blocks spanning many (model, z) pairs take the direct gathers). An odd
+    column count (N % 4 != 0) makes every plane's span start at a different 16-byte
+    alignment shift, and the last plane's copies meet the array end."""
+    fs, cs = shell_pair(128, 1)
+    fr, cr = random_pair(128, 1, seed=11, n_lo=30001, n_hi=30001)
+    f, c = [fs[0], fr[0], fs[0]], [cs[0], cr[0], cs[0]]
+    fa, ca = levels_to_arrays(f), levels_to_arrays(c)
+    fine, coarse = SuperPsh.from_levels(f), SuperPsh.from_levels(c)
+    assert fa.total_columns() % 4 != 0
+    psp = ConvSpec(2, 2, 0, C, C)
+    rng = np.random.default_rng(C)
+    data = rng.integers(-4, 5, (C, fa.total_columns())).astype(np.float32)  # many ties: strict '>' order
+    mp = ops.max_pool(fine, _dev(data), coarse, psp)
+    om, osw = restated.max_pool(fa, data, ca, psp)
+    assert np.array_equal(_np(mp.output), om) and np.array_equal(_np(mp.switches), osw)
+    assert np.array_equal(_np(ops.avg_pool(fine, _dev(data), coarse, psp)), restated.avg_pool(fa, data, ca, psp))
+    # the adjoint direction through k_unpool_staged (coarse spans per (model, coarse z))
+    assert np.array_equal(_np(ops.max_unpool(mp.output, mp.switches, fine, coarse, psp)),
+                          restated.max_unpool(om, osw, fa, ca, psp))
+    cv = rng.uniform(-1, 1, (C, ca.total_columns())).astype(np.float32)
+    cv[:, ::7] = -0.0  # 0 (+) -0.0 -> +0.0 as in the reference
+    assert np.array_equal(_np(ops.avg_unpool(_dev(cv), fine, coarse, psp)).view(np.uint32),
+                          restated.avg_unpool(cv, fa, ca, psp).view(np.uint32))
+
+
 def test_locate_matches_oracle(cuda, restated):
     f, _ = random_pair(16, 2, seed=5)
     fa = levels_to_arrays(f)
@@ -554,6 +583,33 @@ def test_unpool_switch_check_is_stream_ordered(cuda):
     torch.cuda.synchronize()
     assert torch.equal(out, good)
     ops.check_deferred()
+
+
+@pytest.mark.parametrize("shift", [0, 1, 3])
+def test_unpool_switch_check_every_position(cuda, shift):
+    """The vectorised range scan (k_check_switches) sees a bad switch in the unaligned head,
+    the 16-byte body and the tail, for every out-of-range kind, and passes -1 and fd - 1."""
+    f, c = random_pair(16, 2, seed=98)
+    fine, coarse = SuperPsh.from_levels(f), SuperPsh.from_levels(c)
+    sp = ConvSpec(2, 2, 0, 5, 5)
+    d = torch.rand((5, fine.total_columns()), device="cuda")
+    mp = ops.max_pool(fine, d, coarse, sp)
+    n = mp.switches.numel()
+    buf = torch.empty(n + shift, dtype=torch.int32, device="cuda")
+    sw = buf[shift:].view_as(mp.switches)
+    sw.copy_(mp.switches)
+    sw.view(-1)[0], sw.view(-1)[-1] = -1, 7  # range edges are valid
+    ops.max_unpool(mp.output, sw, fine, coarse, sp, check_now=False)
+    torch.cuda.synchronize()
+    ops.check_deferred()
+    for pos in [0, 1, 2, 3, 4, n // 2, n - 5, n - 2, n - 1]:
+        for badv in [8, -2, 2 ** 31 - 1, -2 ** 31]:
+            sw.copy_(mp.switches)
+            sw.view(-1)[pos] = badv
+            ops.max_unpool(mp.output, sw, fine, coarse, sp, check_now=False)
+            torch.cuda.synchronize()
+            with pytest.raises(ValueError, match="unpool: switch index out of range"):
+                ops.check_deferred()
 
 
 def _tiled_to_rows(tiled, n, taps):
