@@ -618,14 +618,46 @@ def _tiled_to_rows(tiled, n, taps):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("case", ["random_dense", "random_sparse", "shell32x3", "edges"])
+def _zyx_sorted_levels(res, models, seed, n_lo, n_hi):
+    """Random sets whose columns are (z, y, x)-sorted like the shells'."""
+    from paper_1803_11385_b200.psh import PshLevel, VoxelSet, mix_seed
+    rng = np.random.default_rng(seed)
+    out = []
+    for k in range(models):
+        n = int(rng.integers(n_lo, n_hi + 1))
+        flat = np.sort(rng.choice(res ** 3, size=n, replace=False))
+        coords = np.stack([flat % res, (flat // res) % res, flat // (res * res)], axis=1).astype(np.int32)
+        out.append(PshLevel.build(VoxelSet.make(3, res, coords, np.zeros((1, n), np.float32)), mix_seed(seed, k)))
+    return out
+
+
+@pytest.mark.parametrize("case", ["random_dense", "random_sparse", "shell32x3", "edges", "sorted_dense",
+                                  "sorted_sparse", "sorted_edges", "shell_two_handles"])
 def test_tiled_field_map_matches_rows(cuda, restated, case):
     """The tile-major 3x3x3 map the fused conv consumes (k_field_map_tiled) equals the row-major
     map (k_field_map) and the oracle's field_map (cnn_ops.cpp:100-119) entry for entry, on
     dense random sets (x-runs across warp boundaries), sparse sets, a batched shell and a set
-    whose voxels all lie on the domain faces; the last tile's padding is -1."""
+    whose voxels all lie on the domain faces; the last tile's padding is -1. Also on
+    (z, y, x)-sorted random sets and faces (x-runs adjacent in column order, identical models
+    back to back) and with separate input / output handles of one level."""
     from paper_1803_11385_b200 import conv as nconv
-    if case == "random_dense":
+    s_out = None
+    if case == "sorted_dense":
+        f = _zyx_sorted_levels(16, 3, 41, 1500, 3000)
+    elif case == "sorted_sparse":
+        f = _zyx_sorted_levels(64, 4, 42, 200, 900)
+    elif case == "sorted_edges":
+        res = 8
+        g = np.stack(np.meshgrid(np.arange(res), np.arange(res), np.arange(res), indexing="ij"), -1).reshape(-1, 3)
+        g = g[(g == 0).any(1) | (g == res - 1).any(1)]
+        g = g[np.lexsort((g[:, 0], g[:, 1], g[:, 2]))].astype(np.int32)
+        from paper_1803_11385_b200.psh import PshLevel, VoxelSet, mix_seed
+        s0 = VoxelSet.make(3, res, g, np.zeros((1, len(g)), np.float32))
+        f = [PshLevel.build(s0, mix_seed(6, 1))] * 3
+    elif case == "shell_two_handles":
+        f, _ = shell_pair(32, 2)
+        s_out = SuperPsh.from_levels(f)
+    elif case == "random_dense":
         f, _ = random_pair(16, 3, seed=31, n_lo=1500, n_hi=3000)  # long x-runs, warp-boundary runs
     elif case == "random_sparse":
         f, _ = random_pair(64, 4, seed=32, n_lo=200, n_hi=900)
@@ -639,11 +671,12 @@ def test_tiled_field_map_matches_rows(cuda, restated, case):
         s0 = VoxelSet.make(3, res, g, np.zeros((1, len(g)), np.float32))
         f = [PshLevel.build(s0, mix_seed(5, 1)), PshLevel.build(s0, mix_seed(5, 2))]
     s = SuperPsh.from_levels(f)
+    so = s_out if s_out is not None else s
     n = s.total_columns()
     spec = ConvSpec(3, 1, 0, 1, 1)
-    tm = nconv.field_map_native(s, s, spec, nconv.TILED)
+    tm = nconv.field_map_native(s, so, spec, nconv.TILED)
     rows = _tiled_to_rows(tm, n, 27)
-    rm = ops.field_map(s, s, spec)
+    rm = ops.field_map(s, so, spec)
     assert torch.equal(rows, rm)
     pad = tm.data.view(-1, 27, 128)[-1, :, (n % 128 or 128):]
     assert bool((pad == -1).all())
