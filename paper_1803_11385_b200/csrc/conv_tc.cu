@@ -632,8 +632,9 @@ __global__ void __launch_bounds__(FwdX2Cfg<BN, CPS, PW, SA, SB, NBUF>::THREADS, 
         uint32_t ph = 0;
         int i = 0;
         for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++i) {
-            const int buf = NBUF == 1 ? 0 : i % NBUF;
-            mbar_wait_sleep(nfull0 + 8 * buf, (uint32_t)((i / NBUF) & 1));
+            constexpr int NB1 = NBUF > 0 ? NBUF : 1;  // (this branch runs only with NBUF > 0)
+            const int buf = NB1 == 1 ? 0 : i % NB1;
+            mbar_wait_sleep(nfull0 + 8 * buf, (uint32_t)((i / NB1) & 1));
             const uint32_t nb = smem_u32(nbr_s + buf * kMaxTaps * BM + r0);
             int t = 0, ci = c * 8;  // C >= 128: a 64-wide stage never crosses a tap
             for (int kb = 0; kb < nkb; ++kb) {
@@ -1100,7 +1101,6 @@ __global__ void __launch_bounds__(DwCfg<NB, PW, CPS, NT>::THREADS, CPS)
                                                      : acc0 + mi * NB;
                         const uint64_t bd = (lo ? b0_lo : b0) + bo;
                         const uint32_t id = lo ? idesc_lo : idesc_hi;
-#pragma unroll
                         // a shared lo accumulator (tshared) always adds: the unit's hi m-tile stage, issued
                         // first, zero-initialises those columns at the chunk's first K step
                         const bool first = (cl | h) == 0 && !(lo && tshared);
