@@ -285,47 +285,54 @@ __global__ void k_col_fold(const double* __restrict__ part, int blocks, long lon
 }
 
 // Batch-norm statistics from the conv epilogue's per-tile {sum, centred sum of squares}
-// (hc_native_gather_gemm*_stats): one block per channel; thread j merges tiles j*T/kT ..
-// (j+1)*T/kT - 1 in order with Chan's formula in double, then a fixed-shape tree over the
-// lanes -> mean, biased variance (cnn_ops.cpp:455-466), running stats and inv_std exactly as
-// k_col_fold MODE 1 forms them.
+// (hc_native_gather_gemm*_stats): one block per channel, two passes in double over the
+// tiles, each a per-thread sum over a contiguous tile range (4 loads in flight) and a
+// fixed-shape tree: the mean S / n, then the exact decomposition
+//   M2 = sum_t [ M2_t + n_t (s_t / n_t - mean)^2 ]
+// (no division per tile: n_t = 128 except the last tile), -> biased variance
+// (cnn_ops.cpp:455-466), running stats and inv_std as k_col_fold MODE 1 forms them.
+// Deterministic; replaces a serial Chan merge (a double division chain per tile).
+__device__ __forceinline__ double block_sum_fixed(double v, double* sh) {
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int w = kT / 2; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+        __syncthreads();
+    }
+    const double r = sh[0];
+    __syncthreads();
+    return r;
+}
+
 __global__ void __launch_bounds__(kT) k_bn_fold_tiles(const float2* __restrict__ st, long long tiles, long long n,
                                                      int C, float* __restrict__ run_mean, float* __restrict__ run_var,
                                                      float momentum, float eps, double* __restrict__ mean_out,
                                                      float* __restrict__ inv_std) {
     const int c = blockIdx.x;
-    __shared__ double sn[kT], sm[kT], s2[kT];
+    __shared__ double sh[kT];
     const long long t0 = tiles * threadIdx.x / kT, t1 = tiles * (threadIdx.x + 1) / kT;
-    double cnt = 0.0, mean = 0.0, m2 = 0.0;
-    for (long long t = t0; t < t1; ++t) {
+    double s = 0.0;
+    long long t = t0;
+    for (; t + 4 <= t1; t += 4) {
+        const float a = st[t * C + c].x, b = st[(t + 1) * C + c].x, d = st[(t + 2) * C + c].x,
+                    e = st[(t + 3) * C + c].x;
+        s += (double)a;
+        s += (double)b;
+        s += (double)d;
+        s += (double)e;
+    }
+    for (; t < t1; ++t) s += (double)st[t * C + c].x;
+    const double mu = block_sum_fixed(s, sh) / (double)n;
+    double m2 = 0.0;
+    const long long full = n / 128;  // tiles [0, full) hold 128 voxels
+    for (t = t0; t < t1; ++t) {
         const float2 v = st[t * C + c];
-        const double nb = (double)min(128LL, n - t * 128);
-        const double mb = (double)v.x / nb;
-        const double tot = cnt + nb;
-        const double delta = mb - mean;
-        mean += delta * nb / tot;
-        m2 += (double)v.y + delta * delta * cnt * nb / tot;
-        cnt = tot;
+        const double nt = t < full ? 128.0 : (double)(n - t * 128);
+        const double d = (double)v.x * (t < full ? 0.0078125 : 1.0 / nt) - mu;
+        m2 += (double)v.y + nt * d * d;
     }
-    sn[threadIdx.x] = cnt;
-    sm[threadIdx.x] = mean;
-    s2[threadIdx.x] = m2;
-    __syncthreads();
-    for (int w = 1; w < kT; w <<= 1) {  // lane j absorbs lane j + w (adjacent ranges, fixed order)
-        if ((threadIdx.x & (2 * w - 1)) == 0) {
-            const double na = sn[threadIdx.x], nb = sn[threadIdx.x + w];
-            const double tot = na + nb;
-            if (nb > 0.0) {
-                const double delta = sm[threadIdx.x + w] - sm[threadIdx.x];
-                sm[threadIdx.x] += delta * nb / tot;
-                s2[threadIdx.x] += s2[threadIdx.x + w] + delta * delta * na * nb / tot;
-                sn[threadIdx.x] = tot;
-            }
-        }
-        __syncthreads();
-    }
+    const double var = block_sum_fixed(m2, sh) / (double)n;
     if (threadIdx.x != 0) return;
-    const double mu = sm[0], var = s2[0] / (double)n;
     mean_out[c] = mu;
     run_mean[c] = (1.0f - momentum) * run_mean[c] + momentum * (float)mu;
     run_var[c] = (1.0f - momentum) * run_var[c] + momentum * (float)var;
