@@ -10,7 +10,7 @@ timeout 600 python bench.py --workload net --res 64 --shapes-per-gpu 32 --steps 
 timeout 600 python bench.py --workload seg --cin 32 --steps 10 --no-cpu-baseline > gpurun_out/bench_seg.json 2>gpurun_out/bench_seg.err; echo "seg rc=$?"
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_f32.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-ref-kernels > /dev/null 2>&1; echo "ncu list rc=$?"
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_conv|k_field_map_tiled|k_split|k_reduce" -s 12 -c 7 \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_conv|k_field_map|k_split|k_reduce" -s 12 -c 7 \
   -o gpurun_out/prof_f32 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-ref-kernels > gpurun_out/prof_f32.log 2>&1; echo "ncu full rc=$?"
 python -c "
 import json
