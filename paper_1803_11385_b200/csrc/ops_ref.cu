@@ -759,7 +759,7 @@ __global__ void __launch_bounds__(288, MINB) k_pool_staged(DevPsh in, DevPsh out
 #pragma unroll
         for (int t = 0; t < 8; ++t) pa[t] = pb[t] + rm3[t];
         float* rp = res + col;
-        int* sp = sw + col;
+        int* sp = AVG ? nullptr : sw + col;  // avg pooling has no switches (sw == nullptr)
         for (int j = 0; j < nsteps; ++j) {
             const int slot = j % NS;
             tc::mbar_wait(tc::smem_u32(&full[slot]), (j / NS) & 1);
@@ -1029,7 +1029,7 @@ bool launch_pool_staged(const hc_psh* in, const float* data, const hc_psh* out, 
     const unsigned g = (unsigned)((n + 255) / 256);
     auto go = [&](auto kern, int pl, int ns) {
         const int smem = pl * ns * kPoolCap * 4;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        smem_optin(kern, smem);  // once per (kernel, device)
         kern<<<g, 288, smem, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, inv, res, sw);
     };
     // A/B at 256^3 x 8 (C 16 / 64 / 128, max_pool ms): (2 planes, 2 stages, 4 blocks/SM) 0.064 / 0.155 /

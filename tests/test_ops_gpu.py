@@ -177,6 +177,29 @@ def test_staged_pool_vs_oracle(cuda, restated, C):
                           restated.avg_unpool(cv, fa, ca, psp).view(np.uint32))
 
 
+def test_staged_pool_captures_into_a_graph(cuda):
+    """k_pool_staged (2^3 max / avg pooling) replays from a CUDA graph with the same results."""
+    f, c = shell_pair(64, 2)
+    fine, coarse = SuperPsh.from_levels(f), SuperPsh.from_levels(c)
+    sp = ConvSpec(2, 2, 0, 16, 16)
+    x = torch.randn((16, fine.total_columns()), device="cuda")
+    want = ops.max_pool(fine, x, coarse, sp)
+    want_avg = ops.avg_pool(fine, x, coarse, sp)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        ops.max_pool(fine, x, coarse, sp)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        got = ops.max_pool(fine, x, coarse, sp)
+        got_avg = ops.avg_pool(fine, x, coarse, sp)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(got.output, want.output) and torch.equal(got.switches, want.switches)
+    assert torch.equal(got_avg, want_avg)
+
+
 def test_locate_matches_oracle(cuda, restated):
     f, _ = random_pair(16, 2, seed=5)
     fa = levels_to_arrays(f)
