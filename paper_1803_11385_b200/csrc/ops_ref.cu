@@ -831,10 +831,36 @@ __global__ void k_avg_pool_any(DevPsh in, DevPsh out, int F, int S, int pad, int
 // outputs whose switch equals g's field row, ascending output order.
 // CB channels per pass: the switch and value loads of all CB channels are issued before
 // any compare (the per-channel form serialised a switch load -> value load chain per channel).
+// Range scan of the switches (cnn_ops.cpp:326-332): 4 x 16-byte loads per thread per pass (one
+// 4-byte load per thread kept too few bytes in flight: 72 us for 110 MB, 1.5 TB/s); thread tid
+// of nth scanning threads; an out-of-range switch raises the mapped host flag.
+__device__ __forceinline__ void check_switches_body(const int* sw, long long n, int fd, int* bad, long long tid,
+                                                    long long nth) {
+    const unsigned lim = (unsigned)fd + 1u;  // s in [-1, fd)  <=>  (unsigned)(s + 1) < fd + 1
+    bool ok = true;
+    const long long head = (long long)(((16 - (reinterpret_cast<uintptr_t>(sw) & 15)) & 15) / 4);
+    const long long h = head < n ? head : n;
+    if (tid < h) ok = (unsigned)sw[tid] + 1u < lim;
+    const int4* v = reinterpret_cast<const int4*>(sw + h);
+    const long long nv = (n - h) / 4;
+    for (long long i = tid; i < nv; i += 4 * nth) {
+        int4 q[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) q[u] = i + u * nth < nv ? __ldcs(v + i + u * nth) : make_int4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            ok &= ((unsigned)q[u].x + 1u < lim) & ((unsigned)q[u].y + 1u < lim) & ((unsigned)q[u].z + 1u < lim) &
+                  ((unsigned)q[u].w + 1u < lim);
+    }
+    const long long t0 = h + nv * 4;
+    if (t0 + tid < n) ok &= (unsigned)sw[t0 + tid] + 1u < lim;
+    if (!ok) *reinterpret_cast<volatile int*>(bad) = 1;  // mapped host word
+}
+
 template <int KMAX, bool AVG, int CB>
-__global__ void __launch_bounds__(256, HCB_POOL_MINB) k_unpool(DevPsh fine, DevPsh coarse, int F, int S, int pad,
-                                                const float* __restrict__ cd, const int* __restrict__ sw, int C,
-                                                float inv, float* __restrict__ res) {
+__device__ __forceinline__ void unpool_body(const DevPsh& fine, const DevPsh& coarse, int F, int S, int pad,
+                                            const float* __restrict__ cd, const int* __restrict__ sw, int C,
+                                            float inv, float* __restrict__ res) {
     const long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (gi >= fine.N) return;
     const int4 c = fine.cols[gi];
@@ -876,6 +902,29 @@ __global__ void __launch_bounds__(256, HCB_POOL_MINB) k_unpool(DevPsh fine, DevP
     }
 }
 
+template <int KMAX, bool AVG, int CB>
+__global__ void __launch_bounds__(256, HCB_POOL_MINB) k_unpool(DevPsh fine, DevPsh coarse, int F, int S, int pad,
+                                                const float* __restrict__ cd, const int* __restrict__ sw, int C,
+                                                float inv, float* __restrict__ res) {
+    unpool_body<KMAX, AVG, CB>(fine, coarse, F, S, pad, cd, sw, C, inv, res);
+}
+
+// max_unpool (one covering output per fine voxel) and its switch-range check in one launch:
+// blocks [0, ub) unpool, the others scan the switches, so the scan's 4 bytes per coarse entry
+// stream beside the unpool's traffic instead of in a launch of their own.
+__global__ void __launch_bounds__(256, HCB_POOL_MINB) k_unpool1_checked(DevPsh fine, DevPsh coarse, int F, int S,
+                                                                        int pad, const float* __restrict__ cd,
+                                                                        const int* __restrict__ sw, int C,
+                                                                        float* __restrict__ res, long long nsw,
+                                                                        int fd, int* bad, unsigned ub) {
+    if (blockIdx.x >= ub) {
+        check_switches_body(sw, nsw, fd, bad, (blockIdx.x - ub) * (long long)blockDim.x + threadIdx.x,
+                            (long long)(gridDim.x - ub) * blockDim.x);
+        return;
+    }
+    unpool_body<1, false, 16>(fine, coarse, F, S, pad, cd, sw, C, 0.0f, res);
+}
+
 template <bool AVG, typename T>
 __global__ void k_unpool_any(DevPsh fine, DevPsh coarse, int F, int S, int pad, const T* __restrict__ cd,
                              const int* __restrict__ sw, int C, T inv, T* __restrict__ res) {
@@ -909,30 +958,11 @@ __global__ void k_unpool_any(DevPsh fine, DevPsh coarse, int F, int S, int pad, 
     }
 }
 
-// Range scan of the switches: 4 x 16-byte loads per thread per pass (one 4-byte load per
-// thread kept too few bytes in flight: 72 us for 110 MB, 1.5 TB/s).
+// Range scan of the switches (check_switches_body above): a standalone launch for the unpool
+// variants that do not fold it in.
 __global__ void k_check_switches(const int* sw, long long n, int fd, int* bad) {
-    const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    const long long nth = (long long)gridDim.x * blockDim.x;
-    const unsigned lim = (unsigned)fd + 1u;  // s in [-1, fd)  <=>  (unsigned)(s + 1) < fd + 1
-    bool ok = true;
-    const long long head = (long long)(((16 - (reinterpret_cast<uintptr_t>(sw) & 15)) & 15) / 4);
-    const long long h = head < n ? head : n;
-    if (tid < h) ok = (unsigned)sw[tid] + 1u < lim;
-    const int4* v = reinterpret_cast<const int4*>(sw + h);
-    const long long nv = (n - h) / 4;
-    for (long long i = tid; i < nv; i += 4 * nth) {
-        int4 q[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) q[u] = i + u * nth < nv ? __ldcs(v + i + u * nth) : make_int4(0, 0, 0, 0);
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            ok &= ((unsigned)q[u].x + 1u < lim) & ((unsigned)q[u].y + 1u < lim) & ((unsigned)q[u].z + 1u < lim) &
-                  ((unsigned)q[u].w + 1u < lim);
-    }
-    const long long t0 = h + nv * 4;
-    if (t0 + tid < n) ok &= (unsigned)sw[t0 + tid] + 1u < lim;
-    if (!ok) *reinterpret_cast<volatile int*>(bad) = 1;  // mapped host word
+    check_switches_body(sw, n, fd, bad, blockIdx.x * (long long)blockDim.x + threadIdx.x,
+                        (long long)gridDim.x * blockDim.x);
 }
 
 // ============================================================== dispatch helpers
@@ -1081,10 +1111,32 @@ void launch_avg_pool(const hc_psh* in, const float* data, const hc_psh* out, con
     launched("avg_pool");
 }
 
+unsigned check_grid(long long nsw) {
+    return (unsigned)std::min<long long>((nsw + 16 * kThreads - 1) / (16 * kThreads), 148 * 8);
+}
+
+// chk_flag: max_unpool's switch-range check (nsw switches, fd field rows) — folded into the
+// F == S unpool launch, else launched first on its own
 void launch_unpool(bool avg, const float* cd, const int* sw, const hc_psh* fine, const hc_psh* coarse,
-                   const hc_conv_spec& sp, float* res, cudaStream_t s) {
+                   const hc_conv_spec& sp, float* res, cudaStream_t s, int* chk_flag = nullptr, long long nsw = 0,
+                   int fd = 0) {
     const long long n = fine->d.N;
+    const int ka1 = cover_per_axis(sp);
+    const bool fold = chk_flag && nsw > 0 && !avg && (fine->d.dim == 3 ? ka1 * ka1 * ka1 : ka1 * ka1) <= 1 &&
+                      n > 0 && sp.in_channels > 0;
+    if (chk_flag && nsw > 0 && !fold) {
+        k_check_switches<<<check_grid(nsw), kThreads, 0, s>>>(sw, nsw, fd, chk_flag);
+        launched("switch check");
+    }
     if (n == 0 || sp.in_channels == 0) return;
+    if (fold) {
+        const unsigned ub = grid_for(n, kThreads);
+        k_unpool1_checked<<<ub + check_grid(nsw), kThreads, 0, s>>>(fine->d, coarse->d, sp.kernel, sp.stride, sp.pad,
+                                                                     cd, sw, sp.in_channels, res, nsw, fd, chk_flag,
+                                                                     ub);
+        launched("unpool + switch check");
+        return;
+    }
     const unsigned g = grid_for(n, kThreads);
     const float inv = 1.0f / static_cast<float>(field_volume(sp, fine->d.dim));  // cnn_ops.cpp:381
     const int ka = cover_per_axis(sp);
@@ -1330,12 +1382,16 @@ hc_status max_unpool_impl(const T* coarse_data, int64_t c_rows, int64_t c_cols, 
             throw std::invalid_argument("unpool: switch shape mismatch");
         cudaStream_t s = as_stream(stream);
         const long long n = s_rows * s_cols;
-        if (n > 0) {
-            const unsigned g = (unsigned)std::min<long long>((n + 16 * kThreads - 1) / (16 * kThreads), 148 * 8);
-            k_check_switches<<<g, kThreads, 0, s>>>(switches, n, (int)fd, deferred_flag_device());
-            launched("switch check");
+        if constexpr (std::is_same_v<T, float>) {
+            launch_unpool(false, coarse_data, switches, fine, coarse, spec, result, s, deferred_flag_device(), n,
+                          (int)fd);
+        } else {
+            if (n > 0) {
+                k_check_switches<<<check_grid(n), kThreads, 0, s>>>(switches, n, (int)fd, deferred_flag_device());
+                launched("switch check");
+            }
+            launch_unpool(false, coarse_data, switches, fine, coarse, spec, result, s);
         }
-        launch_unpool(false, coarse_data, switches, fine, coarse, spec, result, s);
     });
 }
 
