@@ -148,8 +148,8 @@ def test_shell64_batch4_vs_oracle(cuda, restated):
                           restated.max_unpool(om, osw, fa, ca, psp))
 
 
-@pytest.mark.parametrize("C", [7, 16])
-def test_staged_pool_vs_oracle(cuda, restated, C):
+@pytest.mark.parametrize("C,pad", [(7, 0), (16, 0), (5, 1)])
+def test_staged_pool_vs_oracle(cuda, restated, C, pad):
     """2^3 pooling through k_pool_staged (ops_ref.cu): 128^3 shells (blocks stage their
     child spans through shared memory) mixed with a sparse random set of the same
     resolution (blocks spanning many (model, z) pairs take the direct gathers). An odd
@@ -161,7 +161,7 @@ def test_staged_pool_vs_oracle(cuda, restated, C):
     fa, ca = levels_to_arrays(f), levels_to_arrays(c)
     fine, coarse = SuperPsh.from_levels(f), SuperPsh.from_levels(c)
     assert fa.total_columns() % 4 != 0
-    psp = ConvSpec(2, 2, 0, C, C)
+    psp = ConvSpec(2, 2, pad, C, C)  # pad 1: every field straddles two coarse-z child planes differently
     rng = np.random.default_rng(C)
     data = rng.integers(-4, 5, (C, fa.total_columns())).astype(np.float32)  # many ties: strict '>' order
     mp = ops.max_pool(fine, _dev(data), coarse, psp)
