@@ -571,18 +571,18 @@ __device__ __forceinline__ void pool_reduce(const float (&v)[8], const int (&nb)
     }
 }
 
-template <int PL, int NS, bool AVG, int MINB = 1>
-__global__ void __launch_bounds__(288, MINB) k_pool_staged(DevPsh in, DevPsh out, int S, int pad,
+template <int PL, int NS, bool AVG, int MINB = 1, int BO = 256>
+__global__ void __launch_bounds__(BO + 32, MINB) k_pool_staged(DevPsh in, DevPsh out, int S, int pad,
                                                         const float* __restrict__ data, int C, float inv,
                                                         float* __restrict__ res, int* __restrict__ sw) {
-    constexpr int NKEY = kPoolKeys, CAP = kPoolCap;
+    constexpr int NKEY = kPoolKeys, CAP = kPoolCap * BO / 256, NW = BO / 32;  // NW consumer warps
     extern __shared__ __align__(128) float stage[];  // [NS][PL][CAP]
-    __shared__ int rmin[NKEY], rmax[NKEY], roff[NKEY], wtot[9];
+    __shared__ int rmin[NKEY], rmax[NKEY], roff[NKEY], wtot[NW + 1];
     __shared__ int s_over;
     __shared__ __align__(8) unsigned long long full[NS], empty[NS];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const long long col = blockIdx.x * 256LL + tid;
-    const bool live = tid < 256 && col < out.N;
+    const long long col = blockIdx.x * (long long)BO + tid;
+    const bool live = tid < BO && col < out.N;
     const long long Nin = in.N, Nout = out.N;
     if (tid < NKEY) {
         rmin[tid] = INT_MAX;
@@ -593,7 +593,7 @@ __global__ void __launch_bounds__(288, MINB) k_pool_staged(DevPsh in, DevPsh out
         s_over = 0;
         for (int s = 0; s < NS; ++s) {
             tc::mbar_init(tc::smem_u32(&full[s]), 1);
-            tc::mbar_init(tc::smem_u32(&empty[s]), 8);
+            tc::mbar_init(tc::smem_u32(&empty[s]), NW);
         }
         tc::mbar_init_fence();
     }
@@ -744,7 +744,7 @@ __global__ void __launch_bounds__(288, MINB) k_pool_staged(DevPsh in, DevPsh out
             tc::bulk_g2s(stage0 + (uint32_t)(((slot * PL + p) * CAP + roff[key]) * 4), data + a, n, bar);
         }
     };
-    if (wid == 8) {  // producer warp
+    if (wid == NW) {  // producer warp
         for (int j = 0; j < nsteps; ++j) {
             if (j >= NS) tc::mbar_wait(tc::smem_u32(&empty[j % NS]), ((j / NS) - 1) & 1);
             issue(j);
@@ -1056,20 +1056,24 @@ bool launch_pool_staged(const hc_psh* in, const float* data, const hc_psh* out, 
     static const int mode = env_int("HCB_POOL_STAGED", 1);
     if (mode <= 0 || sp.kernel != 2 || in->d.dim != 3 || (reinterpret_cast<uintptr_t>(data) & 15) != 0) return false;
     const long long n = out->d.N;
-    const unsigned g = (unsigned)((n + 255) / 256);
-    auto go = [&](auto kern, int pl, int ns) {
-        const int smem = pl * ns * kPoolCap * 4;
+    auto go = [&](auto kern, int pl, int ns, int bo = 256) {
+        const int smem = pl * ns * (kPoolCap * bo / 256) * 4;
+        const unsigned g = (unsigned)((n + bo - 1) / bo);
         smem_optin(kern, smem);  // once per (kernel, device)
-        kern<<<g, 288, smem, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, inv, res, sw);
+        kern<<<g, bo + 32, smem, s>>>(in->d, out->d, sp.stride, sp.pad, data, sp.in_channels, inv, res, sw);
     };
     // A/B at 256^3 x 8 (C 16 / 64 / 128, max_pool ms): (2 planes, 2 stages, 4 blocks/SM) 0.064 / 0.155 /
     // 0.278; (2, 3, 4) 0.083 / 0.157 / 0.264; (2, 3, 3) 0.070 / 0.152 / 0.269; (4, 2, 3) - / 0.164 / -
+    // (before the presence-free reduction and batched probes); 128-voxel blocks: C 16 / 32 / 64 / 128
+    // 0.058 / 0.086 / 0.143 / 0.258 vs 256-voxel blocks 0.058 / 0.087 / 0.147 / 0.260
     switch (mode) {
         case 2: go(k_pool_staged<2, 3, AVG, 4>, 2, 3); break;
         case 3: go(k_pool_staged<2, 3, AVG>, 2, 3); break;
         case 4: go(k_pool_staged<4, 2, AVG>, 4, 2); break;
-        default:
-            if (sp.in_channels > 64) go(k_pool_staged<2, 3, AVG, 4>, 2, 3);
+        case 5: go(k_pool_staged<2, 2, AVG, 8, 128>, 2, 2, 128); break;
+        case 6: go(k_pool_staged<2, 3, AVG, 6, 128>, 2, 3, 128); break;
+        default:  // C >= 64: 128 coarse voxels per block, 6 blocks/SM (C 64 max 0.147 -> 0.143 ms)
+            if (sp.in_channels >= 64) go(k_pool_staged<2, 3, AVG, 6, 128>, 2, 3, 128);
             else go(k_pool_staged<2, 2, AVG, 4>, 2, 2);
             break;
     }
