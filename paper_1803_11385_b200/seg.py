@@ -78,22 +78,36 @@ class NativeSegNet:
             self._bnws = torch.empty(need, dtype=torch.uint8, device="cuda")
         return self._bnws
 
-    def _conv(self, fmap, x, name, c_out, dtype=torch.float32):
+    def _conv(self, fmap, x, name, c_out, dtype=torch.float32, pre_split=False, stats=None):
+        """stats: [tiles][c_out][2] fp32 receives the epilogue's per-tile batch-norm statistics
+        (hc_native_gather_gemm[_x2]_stats; fp32 output only)."""
         w = self.w[name]
-        if self.f32:  # split rows kept for the layer's dW
-            xs = self._splits[name] = nconv.split(x)
-            wf = nconv.pack_weights_x2(w, c_out, x.shape[1], 27, nconv.PACK_FORWARD)
-            return nconv.gather_gemm_x2(fmap, xs, wf, c_out)
+        fm = nconv.as_field_map(fmap)
+        if self.f32:  # split rows kept for the layer's dW (pre_split: x already holds them)
+            xs = self._splits[name] = x if pre_split else nconv.split(x)
+            c_in = w.shape[1] // 27
+            wf = nconv.pack_weights_x2(w, c_out, c_in, 27, nconv.PACK_FORWARD)
+            if stats is None:
+                return nconv.gather_gemm_x2(fmap, xs, wf, c_out)
+            y = torch.empty((fm.n, c_out), dtype=torch.float32, device="cuda")
+            check(lib.hc_native_gather_gemm_x2_stats(_p(fm.data), fm.layout, fm.n, fm.taps, _p(xs), c_in, _p(wf),
+                                                     c_out, _p(y), _p(stats), _s()))
+            return y
         wf = nconv.pack_weights(w, c_out, x.shape[1], 27, False)
-        return nconv.gather_gemm(fmap, x, wf, c_out, dtype)
+        if stats is None:
+            return nconv.gather_gemm(fmap, x, wf, c_out, dtype)
+        y = torch.empty((fm.n, c_out), dtype=torch.float32, device="cuda")
+        check(lib.hc_native_gather_gemm_stats(_p(fm.data), fm.layout, fm.n, fm.taps, _p(x), x.shape[1], _p(wf), c_out,
+                                              _p(y), _lib.HC_DTYPE_F32, _p(stats), _s()))
+        return y
 
-    def _conv_bwd(self, fmap, x, dy, name, need_dx=True):
+    def _conv_bwd(self, fmap, x, dy, name, need_dx=True, dy_split=False):
         w = self.w[name]
-        c_out, c_in = w.shape[0], x.shape[1]
+        c_out, c_in = w.shape[0], w.shape[1] // 27
         dx = None
         if self.f32:
             xs = self._splits.pop(name, None)
-            dys = nconv.split(dy)
+            dys = dy if dy_split else nconv.split(dy)
             dw = nconv.conv_dw_x2(fmap, xs if xs is not None else nconv.split(x), dys, self._dw)
             if need_dx:
                 wb = nconv.pack_weights_x2(w, c_out, c_in, 27, nconv.PACK_BACKWARD)
@@ -105,22 +119,34 @@ class NativeSegNet:
             dx = nconv.gather_gemm(fmap, dy, wb, c_in, BF16)
         return dw, dx
 
-    def _bn_relu(self, y, name):
+    def _bn_relu(self, y, name, stats=None):
+        """stats: the producing conv's epilogue tile statistics — merged in double in a fixed
+        order (hc_native_bn_relu_forward_tiles), no statistics pass over y."""
         n, c = y.shape
         b = self.bn[name]
         xhat = torch.empty_like(y)
         out = torch.empty((n, c), dtype=self.adt, device="cuda")
         ws = self._bnws_for(n, c)
+        if stats is not None:
+            check(lib.hc_native_bn_relu_forward_tiles(_p(stats), n, c, 0.1, 1e-5, _p(b["mean"]), _p(b["var"]),
+                                                      _p(b["inv"]), _p(y), _p(xhat), _p(out), self.adt_code, _p(ws),
+                                                      ws.numel(), _s()))
+            return out, xhat
         check(lib.hc_native_bn_relu_forward_dt(_p(y), n, c, 1, 0.1, 1e-5, _p(b["mean"]), _p(b["var"]), _p(b["inv"]),
                                                _p(xhat), _p(out), self.adt_code, _p(ws), ws.numel(), _s()))
         return out, xhat
 
-    def _bn_relu_bwd(self, d, dtype, xhat, name):
+    def _bn_relu_bwd(self, d, dtype, xhat, name, split=False):
+        """split (fp32 only): write the split-precision rows the conv backward consumes
+        (HC_DTYPE_SPLIT, no separate split pass)."""
         n, c = xhat.shape
-        out = torch.empty((n, c), dtype=self.adt, device="cuda")
+        if split:
+            out, code = torch.empty((n, 2 * c), dtype=BF16, device="cuda"), _lib.HC_DTYPE_SPLIT
+        else:
+            out, code = torch.empty((n, c), dtype=self.adt, device="cuda"), self.adt_code
         ws = self._bnws_for(n, c)
         check(lib.hc_native_bn_relu_backward_dt(_p(d), dtype, _p(xhat), _p(self.bn[name]["inv"]), n, c, _p(out),
-                                                self.adt_code, _p(ws), ws.numel(), _s()))
+                                                code, _p(ws), ws.numel(), _s()))
         return out
 
     # ------------------------------------------------------------------ step
@@ -137,20 +163,33 @@ class NativeSegNet:
         if trace is not None:
             trace["w"] = {k: v.clone() for k, v in self.w.items()}
         # ---- encoder
-        y1 = self._conv(self.fmap_f, x, "conv1", c)
-        r1, h1 = self._bn_relu(y1, "bn1")
-        p1 = torch.empty((nc, c), dtype=A, device="cuda")
+        st1 = torch.empty(((nf + 127) // 128, c, 2), device="cuda")  # conv epilogue BN statistics
+        y1 = self._conv(self.fmap_f, x, "conv1", c, stats=st1)
+        r1, h1 = self._bn_relu(y1, "bn1", st1)
         sw = torch.empty((nc, c), dtype=torch.int8, device="cuda")
-        check(lib.hc_native_max_pool(_p(self.pmap), nc, 8, _p(r1), AC, c, _p(p1), _p(sw), _s()))
-        y2 = self._conv(self.fmap_c, p1, "conv2", 2 * c)
-        e2, h2 = self._bn_relu(y2, "bn2")
+        if self.f32:  # the pool writes the split rows conv2 consumes (no split pass)
+            p1 = torch.empty((nc, 2 * c), dtype=BF16, device="cuda")
+            check(lib.hc_native_max_pool(_p(self.pmap), nc, 8, _p(r1), _lib.HC_DTYPE_SPLIT, c, _p(p1), _p(sw), _s()))
+            st2 = torch.empty(((nc + 127) // 128, 2 * c, 2), device="cuda")
+            y2 = self._conv(self.fmap_c, p1, "conv2", 2 * c, pre_split=True, stats=st2)
+        else:
+            p1 = torch.empty((nc, c), dtype=A, device="cuda")
+            check(lib.hc_native_max_pool(_p(self.pmap), nc, 8, _p(r1), AC, c, _p(p1), _p(sw), _s()))
+            st2 = torch.empty(((nc + 127) // 128, 2 * c, 2), device="cuda")
+            y2 = self._conv(self.fmap_c, p1, "conv2", 2 * c, stats=st2)
+        e2, h2 = self._bn_relu(y2, "bn2", st2)
         # ---- decoder: unpool(conv3(e2)) + deconv(e2)
         d3 = self._conv(self.fmap_c, e2, "conv3", c, A)
         up = torch.empty((nf, c), dtype=A, device="cuda")
         check(lib.hc_native_max_unpool(_p(self.parent), _p(self.prow), nf, _p(d3), AC, c, _p(sw), _p(up), _s()))
         s3 = self.deconv.forward(e2)  # fp32 (the deconvolution's output dtype)
         if trace is not None:
-            for k, v in dict(x=x, y1=y1, r1=r1, p1=p1, sw=sw, y2=y2, e2=e2, d3=d3, up=up, dc=s3.clone()).items():
+            p1t = p1
+            if self.f32:  # the fp32 pooled rows the split rows hold (trace only)
+                p1t = torch.empty((nc, c), dtype=torch.float32, device="cuda")
+                swt = torch.empty_like(sw)
+                check(lib.hc_native_max_pool(_p(self.pmap), nc, 8, _p(r1), AC, c, _p(p1t), _p(swt), _s()))
+            for k, v in dict(x=x, y1=y1, r1=r1, p1=p1t, sw=sw, y2=y2, e2=e2, d3=d3, up=up, dc=s3.clone()).items():
                 rec(k, v)
         s3.add_(up)                   # + unpooled branch, one mixed-precision add
         r3, h3 = self._bn_relu(s3, "bn3")
@@ -180,12 +219,16 @@ class NativeSegNet:
         d_e2 = d_e2a.float()  # fp32 already (no copy)
         d_e2.add_(d_e2b)
         d_e2 = d_e2.contiguous()
-        d_y2 = self._bn_relu_bwd(d_e2, _lib.HC_DTYPE_F32, h2, "bn2")
-        g["conv2"], d_p1 = self._conv_bwd(self.fmap_c, p1, d_y2, "conv2")
+        d_y2 = self._bn_relu_bwd(d_e2, _lib.HC_DTYPE_F32, h2, "bn2", split=self.f32)
+        g["conv2"], d_p1 = self._conv_bwd(self.fmap_c, p1, d_y2, "conv2", dy_split=self.f32)
+        if trace is not None and self.f32:  # fp32 rows for the oracle comparison (trace only)
+            d_y2 = self._bn_relu_bwd(d_e2, _lib.HC_DTYPE_F32, h2, "bn2")
         d_r1 = torch.empty((nf, c), dtype=A, device="cuda")                    # pool backward = unpool
         check(lib.hc_native_max_unpool(_p(self.parent), _p(self.prow), nf, _p(d_p1), AC, c, _p(sw), _p(d_r1), _s()))
-        d_y1 = self._bn_relu_bwd(d_r1, AC, h1, "bn1")
-        g["conv1"], _ = self._conv_bwd(self.fmap_f, x, d_y1, "conv1", need_dx=False)
+        d_y1 = self._bn_relu_bwd(d_r1, AC, h1, "bn1", split=self.f32)
+        g["conv1"], _ = self._conv_bwd(self.fmap_f, x, d_y1, "conv1", need_dx=False, dy_split=self.f32)
+        if trace is not None and self.f32:
+            d_y1 = self._bn_relu_bwd(d_r1, AC, h1, "bn1")
         if trace is not None:
             for k, v in dict(d_y2=d_y2, d_p1=d_p1, d_r1=d_r1, d_y1=d_y1).items():
                 rec(k, v)
