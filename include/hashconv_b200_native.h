@@ -113,6 +113,12 @@ hc_status hc_native_max_pool(const int32_t* pmap, int64_t n_coarse, int32_t fd, 
 hc_status hc_native_max_unpool(const int32_t* parent, const int8_t* prow, int64_t n_fine, const void* dy,
                                hc_dtype dtype, int32_t c, const int8_t* switches, void* dx,
                                hc_stream stream);
+/* hc_native_max_unpool accumulated into an fp32 [n_fine][c] buffer: acc += unpooled rows, in one
+ * pass (acc.add_(hc_native_max_unpool(...)) without materialising the unpooled rows). Used where an
+ * unpooled branch joins a skip branch (the segmentation decoder). */
+hc_status hc_native_max_unpool_add(const int32_t* parent, const int8_t* prow, int64_t n_fine, const void* dy,
+                                   hc_dtype dtype, int32_t c, const int8_t* switches, float* acc,
+                                   hc_stream stream);
 /* Adjoint of hc_native_max_unpool: out[p][c] = fine[pmap[p][switches[p][c]]][c] (0 for -1). */
 hc_status hc_native_switch_gather(const int32_t* pmap, int64_t n_coarse, int32_t fd, const void* fine,
                                   hc_dtype dtype, int32_t c, const int8_t* switches, void* out,

@@ -113,7 +113,8 @@ __global__ void __launch_bounds__(kT) k_nmax_pool(const int* __restrict__ pmap, 
 template <typename T>
 __global__ void __launch_bounds__(kT) k_nmax_unpool(const int* __restrict__ parent, const signed char* __restrict__ prow,
                                                    long long nf, const T* __restrict__ dy,
-                                                   const signed char* __restrict__ sw, int C, T* __restrict__ dx) {
+                                                   const signed char* __restrict__ sw, int C, T* __restrict__ dx,
+                                                   float* __restrict__ acc = nullptr) {
     const int chunks = C >> 3;
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // over nf * chunks
     if (i >= nf * chunks) return;
@@ -131,6 +132,14 @@ __global__ void __launch_bounds__(kT) k_nmax_unpool(const int* __restrict__ pare
         const signed char* sc = reinterpret_cast<const signed char*>(&s);
 #pragma unroll
         for (int e = 0; e < 8; ++e) o[e] = sc[e] == r ? 0.0f + v[e] : 0.0f;
+    }
+    if (acc) {  // acc += the unpooled row (o is exact in T: what acc.add_(unpooled row) computes)
+        float a[8];
+        load8(acc + g * C + c0, a);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) a[e] = __fadd_rn(a[e], o[e]);
+        store8(acc + g * C + c0, a);
+        return;
     }
     store8(dx + g * C + c0, o);
 }
@@ -604,6 +613,27 @@ hc_status hc_native_max_unpool(const int32_t* parent, const int8_t* prow, int64_
             k_nmax_unpool<float><<<grid_for(n, kT), kT, 0, s>>>(parent, pr, n_fine, static_cast<const float*>(dy), sw,
                                                                 c, static_cast<float*>(dx));
         launched("native max_unpool");
+    });
+}
+
+hc_status hc_native_max_unpool_add(const int32_t* parent, const int8_t* prow, int64_t n_fine, const void* dy,
+                                   hc_dtype dtype, int32_t c, const int8_t* switches, float* acc,
+                                   hc_stream stream) {
+    return guard([&] {
+        check_c8(c);
+        if (!acc) throw std::invalid_argument("native max_unpool_add: null accumulator");
+        if (n_fine <= 0) return;
+        cudaStream_t s = as_stream(stream);
+        const long long n = n_fine * (c / 8);
+        const signed char* pr = reinterpret_cast<const signed char*>(prow);
+        const signed char* sw = reinterpret_cast<const signed char*>(switches);
+        if (dtype == HC_DTYPE_BF16)
+            k_nmax_unpool<bf16><<<grid_for(n, kT), kT, 0, s>>>(parent, pr, n_fine, static_cast<const bf16*>(dy), sw,
+                                                               c, nullptr, acc);
+        else
+            k_nmax_unpool<float><<<grid_for(n, kT), kT, 0, s>>>(parent, pr, n_fine, static_cast<const float*>(dy), sw,
+                                                                c, nullptr, acc);
+        launched("native max_unpool (accumulating)");
     });
 }
 

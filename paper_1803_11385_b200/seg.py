@@ -180,9 +180,11 @@ class NativeSegNet:
         e2, h2 = self._bn_relu(y2, "bn2", st2)
         # ---- decoder: unpool(conv3(e2)) + deconv(e2)
         d3 = self._conv(self.fmap_c, e2, "conv3", c, A)
-        up = torch.empty((nf, c), dtype=A, device="cuda")
-        check(lib.hc_native_max_unpool(_p(self.parent), _p(self.prow), nf, _p(d3), AC, c, _p(sw), _p(up), _s()))
         s3 = self.deconv.forward(e2)  # fp32 (the deconvolution's output dtype)
+        up = None
+        if trace is not None:  # the unpooled branch on its own (trace only)
+            up = torch.empty((nf, c), dtype=A, device="cuda")
+            check(lib.hc_native_max_unpool(_p(self.parent), _p(self.prow), nf, _p(d3), AC, c, _p(sw), _p(up), _s()))
         if trace is not None:
             p1t = p1
             if self.f32:  # the fp32 pooled rows the split rows hold (trace only)
@@ -191,7 +193,8 @@ class NativeSegNet:
                 check(lib.hc_native_max_pool(_p(self.pmap), nc, 8, _p(r1), AC, c, _p(p1t), _p(swt), _s()))
             for k, v in dict(x=x, y1=y1, r1=r1, p1=p1t, sw=sw, y2=y2, e2=e2, d3=d3, up=up, dc=s3.clone()).items():
                 rec(k, v)
-        s3.add_(up)                   # + unpooled branch, one mixed-precision add
+        # + the unpooled branch, accumulated in place (no unpooled tensor, no separate add pass)
+        check(lib.hc_native_max_unpool_add(_p(self.parent), _p(self.prow), nf, _p(d3), AC, c, _p(sw), _p(s3), _s()))
         r3, h3 = self._bn_relu(s3, "bn3")
         scores = self._conv(self.fmap_f, r3, "conv4", self.k)  # [N_fine][K] fp32
         rec("r3", r3)

@@ -87,6 +87,11 @@ def test_seg_forward_layers_vs_oracle(seg_trace, restated):
     # stride-2 deconvolution coarse -> fine (cnn_ops.cpp:408-419): col2hash(W^T D)
     dc = restated.deconv_forward(ca, cm(tr["e2"]), fa, wq(w["deconv"]), dspec, F64)
     assert rel(cm(tr["dc"]), dc) <= TOL_F32
+    # skip join (the unpooled branch accumulated into the deconvolution's output in place,
+    # hc_native_max_unpool_add) -> batch norm (biased batch statistics, eps 1e-5) -> ReLU
+    s3v = tr["dc"].double() + tr["up"].double()
+    xh = (s3v - s3v.mean(0)) / torch.sqrt(s3v.var(0, unbiased=False) + 1e-5)
+    assert rel(cm(tr["r3"].float()), cm(torch.clamp(xh, min=0).float())) <= TOL_BF16_
     sc = restated.conv_forward(fa, cm(tr["r3"]), fa, wq(w["conv4"]), s4, F64)
     assert rel(cm(tr["scores"]), sc) <= TOL_F32
 
