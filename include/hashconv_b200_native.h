@@ -197,6 +197,11 @@ hc_status hc_native_dense_pool_dt(const int32_t* cmap, int32_t b, const void* x,
                                   float* head, int32_t* src, hc_stream stream);
 hc_status hc_native_dense_pool_backward(const float* d_head, const int32_t* src, int32_t b, int32_t c,
                                         int64_t n_fine, float* dx, hc_stream stream);
+/* Softmax cross-entropy (net.cpp:260-283): scores [classes][b] fp32, labels [b]; loss[0] (double)
+ * = sum_j -log softmax(scores[:, j])[labels[j]] / denom, dscores = (softmax - onehot) / denom
+ * (denom = the global batch under data parallelism). One launch, deterministic. */
+hc_status hc_native_softmax_xent(const float* scores, int32_t classes, int32_t b, const int64_t* labels,
+                                 int64_t denom, double* loss, float* dscores, hc_stream stream);
 /* SGD with momentum and weight decay (net.cpp:339-346): v = momentum*v + lr*(g + wd*w); w -= v. */
 /* The same update for `count` (<= 32) tensors in one launch (host arrays of device pointers / sizes). */
 hc_status hc_native_sgd_update_multi(float* const* w, float* const* v, const float* const* g, const int64_t* n,

@@ -556,6 +556,42 @@ void bn_bwd_apply_out(const DT* d, const float* xhat, long long n, int c, const 
                                                                      static_cast<bf16*>(out), n_total);
 }
 
+// Softmax cross-entropy of the net's scores [classes][b] (net.cpp:260-283) in one launch: warp
+// w takes columns w, w + 32, ...; per column the class max, sum of exp (double), log-sum-exp, the
+// label's negative log-probability and the scores' gradient (softmax - onehot) * inv_b. The loss
+// is summed per warp over its columns in order, then over the warps in order (deterministic).
+__global__ void __launch_bounds__(1024) k_softmax_xent(const float* __restrict__ scores, int classes, int b,
+                                                       const long long* __restrict__ labels, double inv_b,
+                                                       double* __restrict__ loss, float* __restrict__ dscores) {
+    __shared__ double part[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double lsum = 0.0;
+    for (int j = w; j < b; j += 32) {
+        double m = -INFINITY;
+        for (int k = lane; k < classes; k += 32) m = fmax(m, (double)scores[(long long)k * b + j]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        double se = 0.0;
+        for (int k = lane; k < classes; k += 32) se += exp((double)scores[(long long)k * b + j] - m);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+        const double lse = m + log(se);
+        const long long lab = labels[j];
+        for (int k = lane; k < classes; k += 32) {
+            const double p = exp((double)scores[(long long)k * b + j] - lse);
+            dscores[(long long)k * b + j] = (float)((p - (k == lab ? 1.0 : 0.0)) * inv_b);
+        }
+        if (lane == 0) lsum += lse - (double)scores[lab * b + j];
+    }
+    if (lane == 0) part[w] = lsum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int q = 0; q < 32; ++q) t += part[q];
+        loss[0] = t * inv_b;
+    }
+}
+
 }  // namespace
 }  // namespace hcb
 
@@ -887,6 +923,17 @@ hc_status hc_native_dense_pool_backward(const float* d_head, const int32_t* src,
         const int n = c * 8 * b;
         k_dense_pool_bwd<<<grid_for(n, kT), kT, 0, s>>>(d_head, src, b, c, dx);
         launched("dense pool backward");
+    });
+}
+
+hc_status hc_native_softmax_xent(const float* scores, int32_t classes, int32_t b, const int64_t* labels,
+                                 int64_t denom, double* loss, float* dscores, hc_stream stream) {
+    return guard([&] {
+        if (classes <= 0 || b <= 0 || denom <= 0 || !scores || !labels || !loss || !dscores)
+            throw std::invalid_argument("native softmax cross-entropy: bad arguments");
+        k_softmax_xent<<<1, 1024, 0, as_stream(stream)>>>(scores, classes, b, reinterpret_cast<const long long*>(labels),
+                                                          1.0 / (double)denom, loss, dscores);
+        launched("softmax cross-entropy");
     });
 }
 

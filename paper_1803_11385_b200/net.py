@@ -364,19 +364,18 @@ class NativeHashNet:
         batch (net.cpp:281 divides by b; shards must not divide by their local b)."""
         cache = {"trace": trace}
         scores = self.forward(nb, x, True, cache)
-        b = scores.shape[1]
-        # softmax over classes, computed on the contiguous [b][classes] transpose (torch's
-        # inner-dimension softmax kernel; over dim 0 it takes a slow strided path)
-        st = scores.t().contiguous().double()
-        logp = torch.log_softmax(st, dim=1)
-        rows = torch.arange(b, device="cuda")
-        # the reference's loss is the mean over the whole batch (net.cpp:283): with data
-        # parallelism each rank returns its share, sum / global_batch, so the ranks' losses
-        # add up to the global mean
-        loss = -logp[rows, labels].sum() / (global_batch or b)
-        dscores_t = logp.exp()
-        dscores_t[rows, labels] -= 1.0
-        dscores = (dscores_t.t() / (global_batch or b)).float()
+        classes, b = scores.shape
+        # softmax cross-entropy and its gradient in one launch (hc_native_softmax_xent, double
+        # log-sum-exp per shape). The reference's loss is the mean over the whole batch
+        # (net.cpp:283): with data parallelism each rank returns its share, sum / global_batch,
+        # so the ranks' losses add up to the global mean
+        scores = scores.contiguous()
+        lab = labels.to(device="cuda", dtype=torch.int64).contiguous()
+        loss_t = torch.empty(1, dtype=torch.float64, device="cuda")
+        dscores = torch.empty_like(scores)
+        check(lib.hc_native_softmax_xent(_p(scores), classes, b, _p(lab), int(global_batch or b), _p(loss_t),
+                                         _p(dscores), _s()))
+        loss = loss_t[0]
         g_fc2_w = dscores @ cache["fc2_in"].t()
         g_fc2_b = dscores.sum(1)
         d_fc1_out = (self.fc2_w.t() @ dscores) * cache["m2"]
