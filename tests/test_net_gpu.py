@@ -411,3 +411,28 @@ def test_multi_tensor_sgd_bit_exact(cuda):
         v_new = (mom * v) + (lr * (g + (wd * w)))
         w_new = w - v_new
         assert np.array_equal(dv.cpu().numpy(), v_new) and np.array_equal(dw.cpu().numpy(), w_new)
+
+
+@pytest.mark.parametrize("classes,b,denom", [(40, 32, 32), (7, 100, 400), (256, 3, 3)])
+def test_softmax_xent_matches_double_reference(cuda, classes, b, denom):
+    """hc_native_softmax_xent (net.cpp:260-283): loss and scores gradient equal a float64
+    log-softmax to 1e-12 / fp32 rounding, for column counts above and below a warp's 32."""
+    from paper_1803_11385_b200 import _lib
+    from paper_1803_11385_b200._lib import check, lib
+    g = torch.Generator(device="cuda").manual_seed(classes + b)
+    scores = (torch.randn((classes, b), device="cuda", generator=g) * 8).contiguous()
+    labels = torch.randint(0, classes, (b,), device="cuda", generator=g)
+    loss = torch.empty(1, dtype=torch.float64, device="cuda")
+    d = torch.empty_like(scores)
+    s = torch.cuda.current_stream().cuda_stream
+    import ctypes
+    check(lib.hc_native_softmax_xent(ctypes.c_void_p(scores.data_ptr()), classes, b,
+                                     ctypes.c_void_p(labels.data_ptr()), denom, ctypes.c_void_p(loss.data_ptr()),
+                                     ctypes.c_void_p(d.data_ptr()), ctypes.c_void_p(s)))
+    logp = torch.log_softmax(scores.double().t(), dim=1)
+    rows = torch.arange(b, device="cuda")
+    want = -logp[rows, labels].sum() / denom
+    assert abs(float(loss[0]) - float(want)) <= 1e-12 * max(1.0, abs(float(want)))
+    dw = logp.exp()
+    dw[rows, labels] -= 1.0
+    assert torch.allclose(d.double(), (dw.t() / denom), rtol=0, atol=1e-7 / denom + 1e-12)
