@@ -344,10 +344,10 @@ class NativeHashNet:
         gen = None if torch.cuda.is_current_stream_capturing() else self._gen
         m1 = (torch.rand(x.shape, device="cuda", generator=gen) < keep).float() / keep
         fc1_in = x * m1
-        fc1_out = self.fc1_w @ fc1_in + self.fc1_b[:, None]
+        fc1_out = torch.addmm(self.fc1_b[:, None], self.fc1_w, fc1_in)  # bias in the GEMM epilogue
         m2 = (torch.rand(fc1_out.shape, device="cuda", generator=gen) < keep).float() / keep
         fc2_in = fc1_out * m2
-        scores = self.fc2_w @ fc2_in + self.fc2_b[:, None]
+        scores = torch.addmm(self.fc2_b[:, None], self.fc2_w, fc2_in)
         if cache is not None:
             cache.update(acts=acts, m1=m1, m2=m2, fc1_in=fc1_in, fc2_in=fc2_in)
         return scores
