@@ -197,6 +197,9 @@ hc_status hc_native_dense_pool_dt(const int32_t* cmap, int32_t b, const void* x,
                                   float* head, int32_t* src, hc_stream stream);
 hc_status hc_native_dense_pool_backward(const float* d_head, const int32_t* src, int32_t b, int32_t c,
                                         int64_t n_fine, float* dx, hc_stream stream);
+/* Dropout (net.cpp:236-251) from uniform draws u[n]: mask = (u < keep) / keep, out = x * mask. */
+hc_status hc_native_dropout_apply(const float* u, const float* x, int64_t n, float keep, float* mask, float* out,
+                                  hc_stream stream);
 /* Softmax cross-entropy (net.cpp:260-283): scores [classes][b] fp32, labels [b]; loss[0] (double)
  * = sum_j -log softmax(scores[:, j])[labels[j]] / denom, dscores = (softmax - onehot) / denom
  * (denom = the global batch under data parallelism). One launch, deterministic. */

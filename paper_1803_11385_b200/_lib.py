@@ -120,6 +120,7 @@ _SIGS.update({
     "hc_native_max_unpool": [_P, _P, _I64, _P, C.c_int, _I32, _P, _P, _P],
     "hc_native_max_unpool_add": [_P, _P, _I64, _P, C.c_int, _I32, _P, _P, _P],
     "hc_native_softmax_xent": [_P, _I32, _I32, _P, _I64, _P, _P, _P],
+    "hc_native_dropout_apply": [_P, _P, _I64, C.c_float, _P, _P, _P],
     "hc_native_switch_gather": [_P, _I64, _I32, _P, C.c_int, _I32, _P, _P, _P],
     "hc_native_bn_relu_forward": [_P, _I64, _I32, _I32, C.c_float, C.c_float, _P, _P, _P, _P, _P, _P, C.c_size_t,
                                   _P],

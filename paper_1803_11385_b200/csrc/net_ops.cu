@@ -556,6 +556,17 @@ void bn_bwd_apply_out(const DT* d, const float* xhat, long long n, int c, const 
                                                                      static_cast<bf16*>(out), n_total);
 }
 
+// Dropout (net.cpp:236-251) from uniform draws u: mask = (u < keep) / keep, out = x * mask — the
+// same fp32 operations as the torch composition it replaces, in one pass.
+__global__ void k_dropout_apply(const float* __restrict__ u, const float* __restrict__ x, long long n, float keep,
+                                float* __restrict__ mask, float* __restrict__ out) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float m = u[i] < keep ? 1.0f / keep : 0.0f;
+    mask[i] = m;
+    out[i] = x[i] * m;
+}
+
 // Softmax cross-entropy of the net's scores [classes][b] (net.cpp:260-283) in one launch: warp
 // w takes columns w, w + 32, ...; per column the class max, sum of exp (double), log-sum-exp, the
 // label's negative log-probability and the scores' gradient (softmax - onehot) * inv_b. The loss
@@ -923,6 +934,16 @@ hc_status hc_native_dense_pool_backward(const float* d_head, const int32_t* src,
         const int n = c * 8 * b;
         k_dense_pool_bwd<<<grid_for(n, kT), kT, 0, s>>>(d_head, src, b, c, dx);
         launched("dense pool backward");
+    });
+}
+
+hc_status hc_native_dropout_apply(const float* u, const float* x, int64_t n, float keep, float* mask, float* out,
+                                  hc_stream stream) {
+    return guard([&] {
+        if (n < 0 || !(keep > 0.0f && keep <= 1.0f)) throw std::invalid_argument("native dropout: bad arguments");
+        if (n == 0) return;
+        k_dropout_apply<<<grid_for(n, kT), kT, 0, as_stream(stream)>>>(u, x, n, keep, mask, out);
+        launched("dropout");
     });
 }
 

@@ -342,11 +342,15 @@ class NativeHashNet:
         if self._gen is None and not torch.cuda.is_current_stream_capturing():
             self._gen = torch.Generator(device="cuda").manual_seed(self._seed)
         gen = None if torch.cuda.is_current_stream_capturing() else self._gen
-        m1 = (torch.rand(x.shape, device="cuda", generator=gen) < keep).float() / keep
-        fc1_in = x * m1
+        def dropout(t):  # uniform draws from torch's (graph-safe) generator; mask and product in one launch
+            t = t.contiguous()
+            u = torch.rand(t.shape, device="cuda", generator=gen)
+            m, o = torch.empty_like(t), torch.empty_like(t)
+            check(lib.hc_native_dropout_apply(_p(u), _p(t), t.numel(), keep, _p(m), _p(o), _s()))
+            return m, o
+        m1, fc1_in = dropout(x)
         fc1_out = torch.addmm(self.fc1_b[:, None], self.fc1_w, fc1_in)  # bias in the GEMM epilogue
-        m2 = (torch.rand(fc1_out.shape, device="cuda", generator=gen) < keep).float() / keep
-        fc2_in = fc1_out * m2
+        m2, fc2_in = dropout(fc1_out)
         scores = torch.addmm(self.fc2_b[:, None], self.fc2_w, fc2_in)
         if cache is not None:
             cache.update(acts=acts, m1=m1, m2=m2, fc1_in=fc1_in, fc2_in=fc2_in)

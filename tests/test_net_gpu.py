@@ -436,3 +436,19 @@ def test_softmax_xent_matches_double_reference(cuda, classes, b, denom):
     dw = logp.exp()
     dw[rows, labels] -= 1.0
     assert torch.allclose(d.double(), (dw.t() / denom), rtol=0, atol=1e-7 / denom + 1e-12)
+
+
+def test_dropout_apply_equals_torch_composition(cuda):
+    """hc_native_dropout_apply == ((u < keep).float() / keep, x * mask) bit for bit."""
+    import ctypes
+    from paper_1803_11385_b200._lib import check, lib
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn((1000, 32), device="cuda", generator=g)
+    u = torch.rand(x.shape, device="cuda", generator=g)
+    for keep in (0.5, 0.8, 1.0):
+        m, o = torch.empty_like(x), torch.empty_like(x)
+        p = lambda t: ctypes.c_void_p(t.data_ptr())
+        check(lib.hc_native_dropout_apply(p(u), p(x), x.numel(), keep, p(m), p(o),
+                                          ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        want_m = (u < keep).float() / keep
+        assert torch.equal(m, want_m) and torch.equal(o, x * want_m)
