@@ -61,6 +61,14 @@ def test_native_max_pool_unpool_bit_exact(cuda, restated, c):
     _lib.check(_lib.lib.hc_native_max_unpool(_p(par), _p(prow), nf, _p(dyv), _lib.HC_DTYPE_F32, c, _p(sw), _p(dx),
                                              None))
     assert np.array_equal(dx.cpu().numpy().T, ou)
+    # accumulating form (the segmentation decoder's skip join): acc += unpooled rows, bit for bit
+    # what acc.add_(unpooled) gives, with -0.0 entries in acc
+    acc = torch.randn((nf, c), device="cuda")
+    acc[::7] = -0.0
+    want = acc + dx
+    _lib.check(_lib.lib.hc_native_max_unpool_add(_p(par), _p(prow), nf, _p(dyv), _lib.HC_DTYPE_F32, c, _p(sw),
+                                                 _p(acc), None))
+    assert torch.equal(acc.view(torch.int32), want.view(torch.int32))
 
 
 def test_native_bn_relu_forward_backward(cuda):
